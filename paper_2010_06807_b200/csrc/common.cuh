@@ -1,0 +1,140 @@
+// Shared definitions of the sm_100a spaQR kernels.
+//
+// Storage convention for every dense operand: fp64, COLUMN-major, explicit
+// leading dimension.  Index arrays are int64 on the host, int32 on the
+// device where sizes allow.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+#define SPQ_HD __host__ __device__ __forceinline__
+
+namespace spq {
+
+// ----------------------------------------------------------- copy tasks
+// dst[dr(i) + j*ldd] = src[sr(i) + j*lds]   (i < nr, j < nc)
+//   sr(i) = src_rows ? src_rows[i] : i ;  dr(i) = dst_rows ? dst_rows[i] : i
+// trans: dst[j + i*ldd] = src[sr(i) + j*lds]   (src rows -> dst columns)
+// src == nullptr: zero fill of the destination rectangle.
+// ident: write the identity into the (square) destination.
+struct CopyTask {
+  const double* src;
+  double* dst;
+  const int* src_rows;
+  const int* dst_rows;
+  int nr, nc;
+  int lds, ldd;
+  int trans;
+  int ident;
+};
+
+// ------------------------------------------------------------- gemm
+// C = alpha * op(A) * B + beta * C ; op(A) = A (m x k, lda) or A^T (A is k x m)
+struct GemmProb {
+  const double* A;
+  const double* B;
+  double* C;
+  int m, n, k;
+  int lda, ldb, ldc;
+  double alpha, beta;
+  int tile0;  // first CTA index of this problem in the launch
+};
+
+// -------------------------------------------------- panel QR (one nb-block)
+// Factor columns [j0, j0+kb) of the m x k panel P (ld = m), rows j0..m-1.
+// On exit P holds V (unit lower trapezoidal, explicit, zeros above), R the
+// upper triangle, tau the coefficients; Tb (kb x kb, ld = ldT) the block's
+// compact-WY T when want_T.
+struct PanelJob {
+  double* P;
+  double* R;     // k x k, ld = k
+  double* tau;   // k
+  double* T;     // k x k, ld = k (diagonal block written when want_T)
+  int m, k, j0, kb;
+  int want_T;
+};
+
+// ------------------------------------------------------ pivot check
+struct PivotJob {
+  const double* R;
+  int k, ld;
+  int slot;
+};
+
+// ------------------------------------------------------ right TRSM
+// X R = B in place on B (n x k, ldb), R k x k upper (ldr)
+struct TrsmJob {
+  const double* R;
+  double* B;
+  int n, k, ldr, ldb;
+  int tile0;
+};
+
+struct LarftJob {
+  const double* G;   // k x k Gram V^T V (ld = ldg)
+  const double* tau;
+  double* T;         // k x k (ld = ldt)
+  int k, ldg, ldt;
+  int tile0;
+};
+
+struct CpqrArgs {
+  double* W;            // m x ncols (ld m), compacted candidate columns, in/out
+  int m, ncols_cap;     // ncols_cap: allocated columns; live count in *nk
+  const int* nk;        // device: number of live columns
+  const double* eps;    // device: threshold ratio
+  int min_rank;
+  double* V;            // m x kmax (ld m), pre-zeroed; explicit unit-lower out
+  double* tau;          // kmax
+  double* beta;         // kmax (R diagonal of accepted steps)
+  int* rank;            // out
+  int* perm;            // out: phys_at (logical -> physical), ncols_cap
+  double* slot_val;     // [2][G]
+  int* slot_pos;        // [2][G]
+  int finalize;         // write beta/zeros into W's pivot columns (Tred)
+};
+
+}  // namespace spq
+
+// ---------------------------------------------------------------- launchers
+namespace spq {
+void launch_copy(const CopyTask* d_tasks, int ntasks, int64_t max_elems, cudaStream_t st);
+void launch_rowflags(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
+                     const int64_t* d_off, unsigned char* d_out, int nblk, cudaStream_t st);
+void launch_count_nnz(const double* const* d_ptrs, const int64_t* d_sizes, int nblk,
+                      unsigned long long* d_count, cudaStream_t st);
+void launch_colnorms_scale(const int64_t* indptr, const int64_t* indices, double* data,
+                           int64_t N, double* scale, int* zero_col, int equilibrate, cudaStream_t st);
+void launch_csc_scatter(const int64_t* indptr, const int64_t* indices, const double* data,
+                        int64_t N, const int64_t* dest_off, double* const* blk_base,
+                        const int* entry_blk, cudaStream_t st);
+void launch_gemm(const GemmProb* d_probs, int nprob, int total_tiles, bool transA, cudaStream_t st);
+int gemm_tiles(int m, int n);
+void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t slab_elems,
+                     bool smem, int kbmax, cudaStream_t st);
+void launch_larft(const LarftJob* d_jobs, int njobs, int total_tiles, cudaStream_t st);
+int larft_tiles(int k);
+void launch_pivot_check(const PivotJob* d_jobs, int njobs, int64_t* d_err_idx,
+                        double* d_err_val, cudaStream_t st);
+void launch_trsm_right(const TrsmJob* d_jobs, int njobs, int total_tiles, cudaStream_t st);
+int trsm_tiles(int n);
+}  // namespace spq
+
+#define CUDA_TRY(x)                                                        \
+  do {                                                                     \
+    cudaError_t e_ = (x);                                                  \
+    if (e_ != cudaSuccess) {                                               \
+      throw spq::CudaFailure(e_, #x, __FILE__, __LINE__);                  \
+    }                                                                      \
+  } while (0)
+
+#include <stdexcept>
+#include <string>
+namespace spq {
+struct CudaFailure : std::runtime_error {
+  CudaFailure(cudaError_t e, const char* what, const char* f, int l)
+      : std::runtime_error(std::string(cudaGetErrorString(e)) + " at " + f + ":" +
+                           std::to_string(l) + " (" + what + ")") {}
+};
+}  // namespace spq

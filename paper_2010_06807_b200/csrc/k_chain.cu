@@ -1,0 +1,174 @@
+// Solve-phase transform-chain kernels: the per-record
+// applications behind Factorization.apply_qt / solve_w / apply_w
+// (factor.py:97-241, 281-300) on an N x nrhs column-major block z.
+//
+//   WY on an index subset:  z[rows] <- z[rows] - V T^T V^T z[rows]   (or T)
+//     wy_dot    : w = V^T z[rows]        warp per reflector column
+//     tri_mv    : w2 = T^T w (or T w)    one CTA, k x k upper triangle
+//     wy_update : z[rows] -= V w2        thread per row (coalesced V rows)
+//   BlockHouseholder.solve_w: rhs = y[cols_s] - R_sn y[cols_n] (column-chunk
+//     partial sums + one reduction CTA), then R_ss back substitution.
+//   apply_w: y_s = R_ss x_s + R_sn x_n ; DiagonalScaling ; Permutation.
+// All HBM-bound (~0.4 flop/byte).
+#include "common.cuh"
+
+namespace spq {
+
+// w[c + r*k] = sum_i V[i + c*m] * z[rows[i] + r*N]
+__global__ void wy_dot_kernel(const double* __restrict__ V, int m, int k,
+                              const double* __restrict__ z, const int* __restrict__ rows,
+                              int64_t N, int nrhs, double* __restrict__ w) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (c >= k) return;
+  const double* v = V + (int64_t)c * m;
+  for (int r = 0; r < nrhs; ++r) {
+    const double* zr = z + (int64_t)r * N;
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s += v[i] * zr[rows[i]];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) w[c + (int64_t)r * k] = s;
+  }
+}
+
+// w2 = T^T w (trans) or T w ; one CTA; T upper (k x k, ld k)
+__global__ void tri_mv_kernel(const double* __restrict__ T, int k, const double* __restrict__ w,
+                              int nrhs, int trans, double* __restrict__ w2) {
+  for (int r = 0; r < nrhs; ++r)
+    for (int a = threadIdx.x; a < k; a += blockDim.x) {
+      double s = 0.0;
+      if (trans) {   // (T^T w)_a = sum_{b <= a} T[b,a] w_b
+        for (int b = 0; b <= a; ++b) s += T[b + (int64_t)a * k] * w[b + (int64_t)r * k];
+      } else {       // (T w)_a = sum_{b >= a} T[a,b] w_b
+        for (int b = a; b < k; ++b) s += T[a + (int64_t)b * k] * w[b + (int64_t)r * k];
+      }
+      w2[a + (int64_t)r * k] = s;
+    }
+}
+
+// z[rows[i]] -= sum_c V[i + c*m] w2[c]
+__global__ void wy_update_kernel(const double* __restrict__ V, int m, int k,
+                                 double* __restrict__ z, const int* __restrict__ rows, int64_t N,
+                                 int nrhs, const double* __restrict__ w2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  for (int r = 0; r < nrhs; ++r) {
+    double s = 0.0;
+    for (int c = 0; c < k; ++c) s += V[i + (int64_t)c * m] * w2[c + (int64_t)r * k];
+    z[rows[i] + (int64_t)r * N] -= s;
+  }
+}
+
+// part[chunk*k + a + r*k*nchunk] = sum_{j in chunk} Rsn[a + j*k] y[cols_n[j]]
+__global__ void rsn_partial_kernel(const double* __restrict__ Rsn, int k, int n,
+                                   const double* __restrict__ y, const int* __restrict__ cols_n,
+                                   int64_t N, int nrhs, int chunk, double* __restrict__ part) {
+  const int ch = blockIdx.y;
+  const int j0 = ch * chunk, j1 = min(n, j0 + chunk);
+  const int nch = gridDim.y;
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < k; a += gridDim.x * blockDim.x)
+    for (int r = 0; r < nrhs; ++r) {
+      double s = 0.0;
+      for (int j = j0; j < j1; ++j) s += Rsn[a + (int64_t)j * k] * y[cols_n[j] + (int64_t)r * N];
+      part[(int64_t)ch * k + a + (int64_t)r * k * nch] = s;
+    }
+}
+
+// mode 0 (solve_w of BlockHouseholder / InterfaceScaling):
+//   b = y[cols] - sum_chunks part ; y[cols] = R^{-1} b      (back substitution)
+// mode 1 (apply_w): y[cols] = R y[cols] + sum_chunks part
+__global__ void __launch_bounds__(1024) tri_solve_vec_kernel(const double* __restrict__ R, int k,
+                                                             double* __restrict__ y,
+                                                             const int* __restrict__ cols,
+                                                             int64_t N, int nrhs,
+                                                             const double* __restrict__ part,
+                                                             int nch, int mode) {
+  extern __shared__ double b[];   // k
+  for (int r = 0; r < nrhs; ++r) {
+    double* yr = y + (int64_t)r * N;
+    for (int a = threadIdx.x; a < k; a += blockDim.x) {
+      double s = 0.0;
+      if (part)
+        for (int ch = 0; ch < nch; ++ch) s += part[(int64_t)ch * k + a + (int64_t)r * k * nch];
+      if (mode == 0) {
+        b[a] = yr[cols[a]] - s;
+      } else {
+        double t = 0.0;
+        for (int c = a; c < k; ++c) t += R[a + (int64_t)c * k] * yr[cols[c]];
+        b[a] = t + s;
+      }
+    }
+    __syncthreads();
+    if (mode == 0) {
+      for (int i = k - 1; i >= 0; --i) {
+        if (threadIdx.x == 0) b[i] = b[i] / R[i + (int64_t)i * k];
+        __syncthreads();
+        const double xi = b[i];
+        for (int a = threadIdx.x; a < i; a += blockDim.x) b[a] -= R[a + (int64_t)i * k] * xi;
+        __syncthreads();
+      }
+    }
+    for (int a = threadIdx.x; a < k; a += blockDim.x) yr[cols[a]] = b[a];
+    __syncthreads();
+  }
+}
+
+__global__ void diag_scale_kernel(double* __restrict__ y, const double* __restrict__ s, int64_t N,
+                                  int nrhs, int divide) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= N * nrhs) return;
+  const double d = s[t % N];
+  y[t] = divide ? y[t] / d : y[t] * d;
+}
+
+__global__ void permute_kernel(const double* __restrict__ z, const int* __restrict__ roc,
+                               int64_t N, int nrhs, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= N * nrhs) return;
+  const int64_t j = t % N, r = t / N;
+  out[t] = z[roc[j] + r * N];
+}
+
+// ------------------------------------------------------------- launchers
+void chain_wy(const double* V, const double* T, int m, int k, double* z, const int* rows,
+              int64_t N, int nrhs, bool transpose, double* w, double* w2, cudaStream_t st) {
+  if (k <= 0 || m <= 0) return;
+  wy_dot_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(V, m, k, z, rows, N, nrhs, w);
+  tri_mv_kernel<<<1, 256, 0, st>>>(T, k, w, nrhs, transpose ? 1 : 0, w2);
+  wy_update_kernel<<<(m + 127) / 128, 128, 0, st>>>(V, m, k, z, rows, N, nrhs, w2);
+}
+
+int chain_rsn_chunks(int n) { return n <= 0 ? 0 : (n + 127) / 128; }
+
+void chain_tri(const double* R, int k, const double* Rsn, int n, double* y, const int* cols_s,
+               const int* cols_n, int64_t N, int nrhs, int mode, double* part, cudaStream_t st) {
+  if (k <= 0) return;
+  const int nch = chain_rsn_chunks(n);
+  if (nch > 0)
+    rsn_partial_kernel<<<dim3((k + 127) / 128, nch), 128, 0, st>>>(Rsn, k, n, y, cols_n, N, nrhs,
+                                                                   128, part);
+  const size_t smem = (size_t)k * sizeof(double);
+  static size_t conf = 0;
+  if (smem > 48 * 1024 && smem > conf) {
+    CUDA_TRY(cudaFuncSetAttribute(tri_solve_vec_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    conf = smem;
+  }
+  tri_solve_vec_kernel<<<1, 1024, smem, st>>>(R, k, y, cols_s, N, nrhs, nch ? part : nullptr, nch,
+                                              mode);
+}
+
+void chain_diag(double* y, const double* s, int64_t N, int nrhs, bool divide, cudaStream_t st) {
+  const int64_t t = N * nrhs;
+  if (t <= 0) return;
+  diag_scale_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(y, s, N, nrhs, divide ? 1 : 0);
+}
+
+void chain_perm(const double* z, const int* roc, int64_t N, int nrhs, double* out,
+                cudaStream_t st) {
+  const int64_t t = N * nrhs;
+  if (t <= 0) return;
+  permute_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(z, roc, N, nrhs, out);
+}
+
+}  // namespace spq

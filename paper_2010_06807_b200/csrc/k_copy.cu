@@ -1,0 +1,138 @@
+// Data-movement kernels of the block-sparse store (SURVEY §8a rows a2, a3,
+// a13, a14): batched gather/scatter/transposed copies between blocks and
+// front buffers, zero fills, identity writes, row-nonzero flags for the host
+// planner (the device twin of `np.any(blk, axis=1)` at factor.py:422 and
+// `np.any(sub)` at factor.py:454), the CSC equilibration + block scatter of
+// TrailingState.__init__ (factor.py:335-374, sparse.py:142-166), and the
+// exact nonzero count behind the `trailing_nnz` statistic (factor.py:887).
+//
+// All of these are HBM-bound byte movers: coalesced along the contiguous
+// (row) dimension of the column-major blocks, grid-strided.
+#include "common.cuh"
+
+namespace spq {
+
+__global__ void __launch_bounds__(256) copy_tasks_kernel(const CopyTask* __restrict__ tasks) {
+  const CopyTask t = tasks[blockIdx.x];
+  const int64_t total = (int64_t)t.nr * t.nc;
+  const int64_t stride = (int64_t)gridDim.y * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int i = (int)(e % t.nr);
+    const int j = (int)(e / t.nr);
+    double v;
+    if (t.ident) {
+      v = (i == j) ? 1.0 : 0.0;
+    } else if (t.src == nullptr) {
+      v = 0.0;
+    } else {
+      const int si = t.src_rows ? t.src_rows[i] : i;
+      v = t.src[si + (int64_t)j * t.lds];
+    }
+    if (t.trans) {
+      t.dst[j + (int64_t)i * t.ldd] = v;
+    } else {
+      const int di = t.dst_rows ? t.dst_rows[i] : i;
+      t.dst[di + (int64_t)j * t.ldd] = v;
+    }
+  }
+}
+
+void launch_copy(const CopyTask* d_tasks, int ntasks, int64_t max_elems, cudaStream_t st) {
+  if (ntasks <= 0) return;
+  int64_t y = (max_elems + 256 * 8 - 1) / (256 * 8);
+  if (y < 1) y = 1;
+  if (y > 512) y = 512;
+  // grid.x limit is 2^31-1; y <= 512 stays far below the 65535 limit
+  dim3 grid((unsigned)ntasks, (unsigned)y);
+  copy_tasks_kernel<<<grid, 256, 0, st>>>(d_tasks);
+}
+
+// one CTA per block; thread per row; flag = any nonzero in the row
+__global__ void __launch_bounds__(256) rowflags_kernel(const double* const* __restrict__ ptrs,
+                                                       const int* __restrict__ nr,
+                                                       const int* __restrict__ nc,
+                                                       const int64_t* __restrict__ off,
+                                                       unsigned char* __restrict__ out) {
+  const int b = blockIdx.x;
+  const double* p = ptrs[b];
+  const int R = nr[b], C = nc[b];
+  unsigned char* o = out + off[b];
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    unsigned char f = 0;
+    for (int j = 0; j < C; ++j) {
+      if (p[i + (int64_t)j * R] != 0.0) { f = 1; break; }
+    }
+    o[i] = f;
+  }
+}
+
+void launch_rowflags(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
+                     const int64_t* d_off, unsigned char* d_out, int nblk, cudaStream_t st) {
+  if (nblk <= 0) return;
+  rowflags_kernel<<<nblk, 128, 0, st>>>(d_ptrs, d_nr, d_nc, d_off, d_out);
+}
+
+__global__ void __launch_bounds__(256) count_nnz_kernel(const double* const* __restrict__ ptrs,
+                                                        const int64_t* __restrict__ sizes,
+                                                        unsigned long long* count) {
+  const double* p = ptrs[blockIdx.x];
+  const int64_t n = sizes[blockIdx.x];
+  unsigned long long c = 0;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) c += (p[e] != 0.0);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+void launch_count_nnz(const double* const* d_ptrs, const int64_t* d_sizes, int nblk,
+                      unsigned long long* d_count, cudaStream_t st) {
+  if (nblk <= 0) return;
+  count_nnz_kernel<<<nblk, 256, 0, st>>>(d_ptrs, d_sizes, d_count);
+}
+
+// Column 2-norms accumulated sequentially in CSC entry order, no FMA
+// contraction: bit-identical to `np.add.at(sq, col_of, data**2)` followed by
+// sqrt and division (sparse.py:96-106, 158-166).
+__global__ void colnorms_scale_kernel(const int64_t* __restrict__ indptr, double* data, int64_t N,
+                                      double* scale, int* zero_col, int equilibrate) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const int64_t a = indptr[j], b = indptr[j + 1];
+  double s = 0.0;
+  for (int64_t e = a; e < b; ++e) s = __dadd_rn(s, __dmul_rn(data[e], data[e]));
+  const double nrm = sqrt(s);
+  if (nrm == 0.0) atomicMin(zero_col, (int)j);
+  if (equilibrate) {
+    scale[j] = nrm;
+    if (nrm != 0.0)
+      for (int64_t e = a; e < b; ++e) data[e] = data[e] / nrm;
+  }
+}
+
+void launch_colnorms_scale(const int64_t* indptr, const int64_t* /*indices*/, double* data,
+                           int64_t N, double* scale, int* zero_col, int equilibrate,
+                           cudaStream_t st) {
+  if (N <= 0) return;
+  colnorms_scale_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(indptr, data, N, scale,
+                                                                      zero_col, equilibrate);
+}
+
+// entry e of the CSC goes to blk_base[entry_blk[e]][dest_off[e]]
+__global__ void csc_scatter_kernel(const double* __restrict__ data, int64_t nnz,
+                                   const int64_t* __restrict__ dest_off,
+                                   double* const* __restrict__ blk_base,
+                                   const int* __restrict__ entry_blk) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  blk_base[entry_blk[e]][dest_off[e]] = data[e];
+}
+
+void launch_csc_scatter(const int64_t* indptr, const int64_t* /*indices*/, const double* data,
+                        int64_t nnz, const int64_t* dest_off, double* const* blk_base,
+                        const int* entry_blk, cudaStream_t st) {
+  (void)indptr;
+  if (nnz <= 0) return;
+  csc_scatter_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(data, nnz, dest_off,
+                                                                     blk_base, entry_blk);
+}
+
+}  // namespace spq

@@ -1,0 +1,300 @@
+// Threshold column-pivoted Householder QR, the
+// sparsification kernel: `cpqr_threshold` (kernels/_numba.py:120-167) with
+// the reference's exact rules — trailing column norms RECOMPUTED every step
+// (here fused into the update pass), argmax with the LOWEST current
+// position winning ties, stop at step i >= 1 once max norm < eps * norm0
+// (and i >= min_rank), swap, reflect, rank-1 update.
+//
+// One cooperative launch per interface: CTAs own contiguous ranges of
+// physical columns; swaps are logical (every CTA keeps identical copies of
+// the position <-> column maps in shared memory), so each step costs one
+// grid-wide barrier: publish local argmax -> sync -> every CTA reduces the
+// G candidates identically, recomputes the pivot reflector from the pivot
+// column (deterministic block reduction) and updates its own columns.
+//
+// Also here: the sparsify preamble (`factor.py:583-604`: column norms of
+// M = [A_np^T, A_pn], maxcol, ratio = min(eps/maxcol, 0.999999), the
+// `ncols > 4|p|` column filter and its compaction) kept on the device so
+// the host syncs once per interface, for the accepted rank.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace spq {
+
+constexpr int CP_NT = 256;
+
+
+
+__device__ __forceinline__ bool better(double v, int pos, double bv, int bpos) {
+  // strict '>' scan in position order == max value, lowest position on ties
+  return v > bv || (v == bv && pos < bpos);
+}
+
+__global__ void __launch_bounds__(CP_NT) cpqr_kernel(CpqrArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = CP_NT / 32;
+  const int m = a.m;
+  const int nk = *a.nk;
+  const double eps = *a.eps;
+  const int kmax = min(m, nk);
+  const int cpc = (nk + G - 1) / G;
+  const int c0 = min(nk, g * cpc), c1 = min(nk, c0 + cpc);
+
+  extern __shared__ __align__(16) unsigned char smraw[];
+  int* pos_of = reinterpret_cast<int*>(smraw);          // [ncols_cap]
+  int* phys_at = pos_of + a.ncols_cap;                   // [ncols_cap]
+  double* v = reinterpret_cast<double*>(phys_at + a.ncols_cap);  // [m]; 2*ncols ints keep 8B alignment
+  __shared__ double red_v[NW];
+  __shared__ int red_p[NW];
+  __shared__ double sc[4];
+  __shared__ int colpos_s[1];
+
+  for (int j = tid; j < nk; j += CP_NT) { pos_of[j] = j; phys_at[j] = j; }
+
+  // initial norms (rows 0..m-1), warp per column, then local best
+  double bv = -1.0;
+  int bp = 0x7fffffff;
+  for (int j = c0 + warp; j < c1; j += NW) {
+    const double* col = a.W + (int64_t)j * m;
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) s += col[r] * col[r];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double nv = sqrt(s);
+    if (better(nv, j, bv, bp)) { bv = nv; bp = j; }
+  }
+  if (lane == 0) { red_v[warp] = bv; red_p[warp] = bp; }
+  __syncthreads();
+  if (tid == 0) {
+    double v0 = -1.0; int p0 = 0x7fffffff;
+    for (int w = 0; w < NW; ++w) if (better(red_v[w], red_p[w], v0, p0)) { v0 = red_v[w]; p0 = red_p[w]; }
+    a.slot_val[g] = v0;
+    a.slot_pos[g] = p0;
+  }
+
+  double norm0 = 0.0;
+  int r = kmax;
+  for (int i = 0; i < kmax; ++i) {
+    const int par = i & 1;
+    grid.sync();
+    // ---- global argmax (identical in every CTA)
+    if (tid == 0) {
+      double v0 = -1.0; int p0 = 0x7fffffff;
+      for (int h = 0; h < G; ++h) {
+        const double hv = a.slot_val[par * G + h];
+        const int hp = a.slot_pos[par * G + h];
+        if (better(hv, hp, v0, p0)) { v0 = hv; p0 = hp; }
+      }
+      sc[0] = v0;
+      colpos_s[0] = p0;
+    }
+    __syncthreads();
+    const double nrm = sc[0];
+    const int lp = colpos_s[0];     // logical position of the pivot
+    if (i == 0) {
+      norm0 = nrm;
+      if (norm0 == 0.0) { r = 0; break; }
+    } else if (nrm < eps * norm0 && i >= a.min_rank) {
+      r = i;
+      break;
+    }
+    // ---- logical swap of positions i and lp
+    const int phys_p = phys_at[lp];
+    const int phys_i = phys_at[i];
+    __syncthreads();
+    if (tid == 0) {
+      phys_at[i] = phys_p; phys_at[lp] = phys_i;
+      pos_of[phys_p] = i; pos_of[phys_i] = lp;
+    }
+    // ---- reflector from the pivot column (rows i..m-1)
+    const double* x = a.W + (int64_t)phys_p * m;
+    double s = 0.0;
+    for (int rr = i + 1 + tid; rr < m; rr += CP_NT) s += x[rr] * x[rr];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red_v[warp] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double sigma = 0.0;
+      for (int w = 0; w < NW; ++w) sigma += red_v[w];
+      const double alpha = x[i];
+      double tau, beta, v0 = 1.0, zero = 0.0;
+      if (sigma == 0.0) {
+        zero = 1.0;
+        if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+      } else {
+        beta = sqrt(alpha * alpha + sigma);
+        v0 = (alpha <= 0.0) ? alpha - beta : -sigma / (alpha + beta);
+        tau = -v0 / beta;
+      }
+      sc[1] = tau; sc[2] = v0; sc[3] = zero;
+      if (g == 0) { a.tau[i] = tau; a.beta[i] = beta; }
+    }
+    __syncthreads();
+    const double tau = sc[1], v0 = sc[2];
+    const bool zero = sc[3] != 0.0;
+    for (int rr = i + tid; rr < m; rr += CP_NT)
+      v[rr] = (rr == i) ? 1.0 : (zero ? 0.0 : x[rr] / v0);
+    __syncthreads();
+    if (g == 0)
+      for (int rr = i + tid; rr < m; rr += CP_NT) a.V[rr + (int64_t)i * m] = v[rr];
+    // ---- update own trailing columns, fused norm over rows i+1..m-1
+    bv = -1.0;
+    bp = 0x7fffffff;
+    for (int j = c0 + warp; j < c1; j += NW) {
+      const int pj = pos_of[j];
+      if (pj <= i) continue;       // retired pivot columns (incl. this step's)
+      double* col = a.W + (int64_t)j * m;
+      double ns = 0.0;
+      if (tau != 0.0) {
+        double d = 0.0;
+        for (int rr = i + lane; rr < m; rr += 32) d += v[rr] * col[rr];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        const double w = tau * d;
+        for (int rr = i + lane; rr < m; rr += 32) {
+          const double nv = col[rr] - w * v[rr];
+          col[rr] = nv;
+          if (rr > i) ns += nv * nv;
+        }
+      } else {
+        for (int rr = i + 1 + lane; rr < m; rr += 32) ns += col[rr] * col[rr];
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+      const double nv = sqrt(ns);
+      if (better(nv, pj, bv, bp)) { bv = nv; bp = pj; }
+    }
+    if (lane == 0) { red_v[warp] = bv; red_p[warp] = bp; }
+    __syncthreads();
+    if (tid == 0) {
+      double v1 = -1.0; int p1 = 0x7fffffff;
+      for (int w = 0; w < NW; ++w) if (better(red_v[w], red_p[w], v1, p1)) { v1 = red_v[w]; p1 = red_p[w]; }
+      a.slot_val[(par ^ 1) * G + g] = v1;
+      a.slot_pos[(par ^ 1) * G + g] = p1;
+    }
+    // the pivot column's rows stay intact until every CTA has read x: the
+    // owner writes beta/zeros in the finalize pass below
+  }
+  if (g == 0 && tid == 0) *a.rank = r;
+  if (g == 0)
+    for (int j = tid; j < nk; j += CP_NT) a.perm[j] = phys_at[j];
+  if (a.finalize) {
+    grid.sync();
+    for (int j = c0 + warp; j < c1; j += NW) {
+      const int pj = pos_of[j];
+      if (pj >= r) continue;
+      double* col = a.W + (int64_t)j * m;
+      for (int rr = pj + lane; rr < m; rr += 32) col[rr] = (rr == pj) ? a.beta[pj] : 0.0;
+    }
+  }
+}
+
+size_t cpqr_smem_bytes(int ncols_cap, int m) {
+  return (size_t)(2 * ncols_cap + 2) * sizeof(int) + (size_t)m * sizeof(double) + 16;
+}
+
+int cpqr_grid(int ncols, int nsm) {
+  int g = (ncols + 7) / 8;
+  if (g > nsm) g = nsm;
+  if (g < 1) g = 1;
+  return g;
+}
+
+void launch_cpqr(const CpqrArgs& a, int G, cudaStream_t st) {
+  const size_t bytes = cpqr_smem_bytes(a.ncols_cap, a.m);
+  static size_t configured = 0;
+  if (bytes > 48 * 1024 && bytes > configured) {
+    CUDA_TRY(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)bytes));
+    configured = bytes;
+  }
+  CpqrArgs args = a;
+  void* params[] = {&args};
+  CUDA_TRY(cudaLaunchCooperativeKernel((void*)cpqr_kernel, dim3(G), dim3(CP_NT), params, bytes,
+                                       st));
+}
+
+// ------------------------------------------------------ sparsify preamble
+// warp per column: squared norm of column j of M (m x n, ld m)
+__global__ void colsq_kernel(const double* __restrict__ M, int m, int n, double* __restrict__ sq) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const double* col = M + (int64_t)w * m;
+  double s = 0.0;
+  for (int r = lane; r < m; r += 32) s += col[r] * col[r];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) sq[w] = s;
+}
+
+// single CTA: maxcol, ratio, keep filter, compaction list
+__global__ void __launch_bounds__(1024) sparsify_select_kernel(const double* __restrict__ sq,
+                                                               int m, int n, double eps_user,
+                                                               int* __restrict__ keep_idx,
+                                                               int* nk, double* ratio_out,
+                                                               double* maxcol_out) {
+  __shared__ double red[32];
+  __shared__ int cnt[33];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double mx = 0.0;
+  for (int j = tid; j < n; j += blockDim.x) mx = fmax(mx, sqrt(sq[j]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    red[0] = v;
+  }
+  __syncthreads();
+  const double maxcol = red[0];
+  const double ratio = (maxcol == 0.0) ? 0.0 : fmin(eps_user / maxcol, 0.999999);
+  const bool filter = maxcol > 0.0 && n > 4 * m;
+  const double thr = ratio * maxcol;
+  // ordered compaction in chunks of blockDim
+  int base = 0;
+  for (int j0 = 0; j0 < n; j0 += blockDim.x) {
+    const int j = j0 + tid;
+    const bool keep = j < n && (!filter || sqrt(sq[j]) >= thr);
+    const unsigned ball = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) cnt[warp] = __popc(ball);
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { const int c = cnt[w]; cnt[w] = acc; acc += c; }
+      cnt[32] = acc;
+    }
+    __syncthreads();
+    if (keep) keep_idx[base + cnt[warp] + __popc(ball & ((1u << lane) - 1u))] = j;
+    base += cnt[32];
+    __syncthreads();
+  }
+  if (tid == 0) { *nk = base; *ratio_out = ratio; *maxcol_out = maxcol; }
+}
+
+// W[:, t] = M[:, keep_idx[t]] for t < *nk
+__global__ void gather_cols_kernel(const double* __restrict__ M, int m, const int* __restrict__ idx,
+                                   const int* nk, double* __restrict__ W) {
+  const int t = blockIdx.y;
+  if (t >= *nk) return;
+  const double* src = M + (int64_t)idx[t] * m;
+  double* dst = W + (int64_t)t * m;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x)
+    dst[r] = src[r];
+}
+
+void launch_sparsify_prep(const double* M, int m, int n, double eps, double* sq, int* keep_idx,
+                          int* nk, double* ratio, double* maxcol, double* W, cudaStream_t st) {
+  if (n > 0) colsq_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(M, m, n, sq);
+  sparsify_select_kernel<<<1, 1024, 0, st>>>(sq, m, n, eps, keep_idx, nk, ratio, maxcol);
+  if (n > 0) gather_cols_kernel<<<dim3((m + 255) / 256, n), 256, 0, st>>>(M, m, keep_idx, nk, W);
+}
+
+}  // namespace spq

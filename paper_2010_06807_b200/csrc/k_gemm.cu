@@ -1,0 +1,142 @@
+// Batched fp64 tensor-core GEMM for the compact-WY updates
+//   W = V^T C,  W = T^T W,  C -= V W        (kernels/__init__.py:100-118)
+// and the Gram products V^T V behind the T factor (kernels/_numba.py:101-117).
+//
+// sm_100a has no fp64 tcgen05 kind (ptxas rejects .kind::f64),
+// so the fp64 tensor path is the warp-level DMMA `mma.sync.m8n8k4.f64`.
+// Tile 64x64x16, 4 warps each owning 32x32 (4x4 DMMA tiles, 32 fp64
+// accumulators per thread), register-prefetched double-buffered shared
+// memory with a 68-double row pitch (conflict-free fragment loads: the 4
+// k-rows of a fragment land on disjoint 8-bank groups).  One launch covers
+// every problem of a wave; each CTA finds its problem by binary search over
+// the per-problem first-tile prefix.
+#include "common.cuh"
+
+namespace spq {
+
+namespace {
+constexpr int BM = 64, BN = 64, BK = 16, PITCH = 68, NT = 128;
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+}  // namespace
+
+template <bool TA>
+__global__ void __launch_bounds__(NT) gemm_dmma_kernel(const GemmProb* __restrict__ probs,
+                                                       int nprob) {
+  int lo = 0, hi = nprob - 1;
+  const int bid = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (probs[mid].tile0 <= bid) lo = mid; else hi = mid - 1;
+  }
+  const GemmProb p = probs[lo];
+  const int tm = (p.m + BM - 1) / BM;
+  const int t = bid - p.tile0;
+  const int m0 = (t % tm) * BM, n0 = (t / tm) * BN;
+
+  __shared__ double As[2][BK][PITCH];
+  __shared__ double Bs[2][BK][PITCH];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int g = lane >> 2, q = lane & 3;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double ra[8], rb[8];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int l = tid + e * NT;
+      int mi, ki;
+      if (TA) { ki = l & 15; mi = l >> 4; } else { mi = l & 63; ki = l >> 6; }
+      const int gm = m0 + mi, gk = k0 + ki;
+      double v = 0.0;
+      if (gm < p.m && gk < p.k)
+        v = TA ? p.A[gk + (int64_t)gm * p.lda] : p.A[gm + (int64_t)gk * p.lda];
+      ra[e] = v;
+      const int kb = l & 15, nb = l >> 4;
+      const int gk2 = k0 + kb, gn = n0 + nb;
+      rb[e] = (gk2 < p.k && gn < p.n) ? p.B[gk2 + (int64_t)gn * p.ldb] : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int l = tid + e * NT;
+      int mi, ki;
+      if (TA) { ki = l & 15; mi = l >> 4; } else { mi = l & 63; ki = l >> 6; }
+      As[buf][ki][mi] = ra[e];
+      Bs[buf][l & 15][l >> 4] = rb[e];
+    }
+  };
+
+  const int nk = (p.k + BK - 1) / BK;
+  if (nk > 0) {
+    load(0);
+    store(0);
+    __syncthreads();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) load((kt + 1) * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk + q][wm + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk + q][wn + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], a[i], b[j]);
+    }
+    if (kt + 1 < nk) {
+      store(buf ^ 1);
+      __syncthreads();
+    }
+  }
+
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm + i * 8 + g;
+    if (row >= p.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + wn + j * 8 + 2 * q + h;
+        if (col >= p.n) continue;
+        double* c = p.C + row + (int64_t)col * p.ldc;
+        const double v = p.alpha * acc[i][j][h];
+        *c = (p.beta == 0.0) ? v : v + p.beta * (*c);
+      }
+    }
+  }
+}
+
+int gemm_tiles(int m, int n) {
+  if (m <= 0 || n <= 0) return 0;
+  return ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
+}
+
+void launch_gemm(const GemmProb* d_probs, int nprob, int total_tiles, bool transA,
+                 cudaStream_t st) {
+  if (nprob <= 0 || total_tiles <= 0) return;
+  if (transA)
+    gemm_dmma_kernel<true><<<total_tiles, NT, 0, st>>>(d_probs, nprob);
+  else
+    gemm_dmma_kernel<false><<<total_tiles, NT, 0, st>>>(d_probs, nprob);
+}
+
+}  // namespace spq

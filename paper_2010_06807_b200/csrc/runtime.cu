@@ -1,0 +1,1937 @@
+// Native runtime of the B200 spaQR path: the HBM-resident block store, the
+// wave planner that batches independent eliminations, the level operations
+// (a) factor, (b) scale, (c) sparsify, (d) merge, the transform records and
+// the solve-phase chains (e), exported through the C-ABI in
+// include/spaqr_b200.h.
+//
+// Semantics follow the reference TrailingState (pkg/src/nestqr/factor.py):
+// the host keeps the block STRUCTURE (which (row cluster, col cluster)
+// blocks exist, their row/col index sets, row_of_col) exactly as the
+// reference's dicts do; every VALUE lives in device memory.  Data-dependent
+// structure decisions (`np.any` row subsets and present-column filters,
+// factor.py:422,454) read per-row nonzero flags computed on the device.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/spaqr_b200.h"
+#include "common.cuh"
+
+namespace spq {
+// launchers defined in other translation units
+
+void launch_cpqr(const CpqrArgs& a, int G, cudaStream_t st);
+int cpqr_grid(int ncols, int nsm);
+void launch_sparsify_prep(const double* M, int m, int n, double eps, double* sq, int* keep_idx,
+                          int* nk, double* ratio, double* maxcol, double* W, cudaStream_t st);
+void chain_wy(const double* V, const double* T, int m, int k, double* z, const int* rows,
+              int64_t N, int nrhs, bool transpose, double* w, double* w2, cudaStream_t st);
+void chain_tri(const double* R, int k, const double* Rsn, int n, double* y, const int* cols_s,
+               const int* cols_n, int64_t N, int nrhs, int mode, double* part, cudaStream_t st);
+int chain_rsn_chunks(int n);
+void chain_diag(double* y, const double* s, int64_t N, int nrhs, bool divide, cudaStream_t st);
+void chain_perm(const double* z, const int* roc, int64_t N, int nrhs, double* out,
+                cudaStream_t st);
+}  // namespace spq
+
+using namespace spq;
+
+namespace {
+
+struct SpqError : std::runtime_error {
+  int code;
+  int64_t index;
+  double value;
+  SpqError(int c, const std::string& m, int64_t i = -1, double v = 0.0)
+      : std::runtime_error(m), code(c), index(i), value(v) {}
+};
+
+inline uint64_t bkey(int i, int j) { return ((uint64_t)(uint32_t)i << 32) | (uint32_t)j; }
+
+struct Block {
+  double* p = nullptr;
+  int nr = 0, nc = 0;
+  std::vector<uint8_t> flags;  // per row: 0 zero, 1 nonzero, 2 unknown (written)
+  bool clean = false;
+};
+
+enum RecKind { REC_ELIM = 1, REC_SCALE = 2, REC_SPARSIFY = 3 };
+
+struct Record {
+  int kind = 0;
+  int m = 0, k = 0, n = 0, rank = 0;
+  std::vector<int64_t> rows, cols_s, cols_n;
+  double* payload = nullptr;
+  double *V = nullptr, *tau = nullptr, *T = nullptr, *R = nullptr, *Rsn = nullptr;
+  int *d_rows = nullptr, *d_cols_s = nullptr, *d_cols_n = nullptr;
+  int64_t payload_scalars = 0;
+};
+
+// families for device timing / flop accounting
+enum Fam { F_COPY = 0, F_QR, F_WY, F_TRSM, F_CPQR, F_FLAGS, F_CHAIN, F_NFAM };
+
+struct FamTimer {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[F_NFAM];
+  double ms[F_NFAM] = {0};
+  double flops[F_NFAM] = {0};
+  double bytes[F_NFAM] = {0};
+  int64_t launches[F_NFAM] = {0};
+};
+
+constexpr double kPivotFloor = 1e-14;  // kernels/__init__.py:70
+
+}  // namespace
+
+struct spq_ctx {
+  int dev = 0;
+  int nsm = 148;
+  cudaStream_t st = nullptr;
+  // pinned upload ring
+  char* pin = nullptr;
+  char* dring = nullptr;
+  size_t ring_cap = 0, ring_off = 0;
+  // error
+  int err_code = 0;
+  int64_t err_index = -1;
+  double err_value = 0.0;
+  std::string err_msg;
+  // structure
+  int64_t N = 0;
+  int ncl = 0;
+  std::vector<std::vector<int64_t>> rows_of, cols_of;
+  std::vector<char> active;
+  std::vector<std::set<int>> rix, cix;
+  std::unordered_map<uint64_t, Block> blk;
+  std::vector<int64_t> row_of_col;
+  std::vector<double*> deferred;
+  // transform chain
+  std::vector<Record> recs;
+  double* d_scale = nullptr;
+  bool equil = false;
+  int* d_roc = nullptr;
+  int* d_index_pack = nullptr;
+  bool finished = false;
+  // device error slots for pivot checks
+  int64_t* d_err_idx = nullptr;
+  double* d_err_val = nullptr;
+  int err_slots = 0;
+  // timing
+  bool timing = true;
+  FamTimer tm;
+  // scratch for chains
+  double* d_vec = nullptr;
+  double* d_vec2 = nullptr;
+  double* d_w = nullptr;
+  double* d_w2 = nullptr;
+  double* d_part = nullptr;
+  size_t vec_cap = 0, w_cap = 0, part_cap = 0;
+  // plugin-API scratch
+  std::vector<int> row_stamp;
+  int stamp = 0;
+};
+
+namespace {
+
+// ------------------------------------------------------------ utilities
+double* dalloc(spq_ctx* c, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  void* p = nullptr;
+  CUDA_TRY(cudaMallocAsync(&p, bytes, c->st));
+  return (double*)p;
+}
+void dfree(spq_ctx* c, void* p) {
+  if (p) CUDA_TRY(cudaFreeAsync(p, c->st));
+}
+
+void sync(spq_ctx* c) {
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  c->ring_off = 0;
+}
+
+template <class T>
+T* upload(spq_ctx* c, const T* src, size_t n) {
+  const size_t bytes = n * sizeof(T);
+  if (bytes == 0) return nullptr;
+  size_t aligned = (bytes + 255) & ~(size_t)255;
+  if (aligned > c->ring_cap) {
+    // oversize: dedicated allocation, freed stream-ordered after use by caller
+    T* d = (T*)dalloc(c, bytes);
+    CUDA_TRY(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, c->st));
+    c->deferred.push_back((double*)d);
+    return d;
+  }
+  if (c->ring_off + aligned > c->ring_cap) sync(c);
+  std::memcpy(c->pin + c->ring_off, src, bytes);
+  T* d = (T*)(c->dring + c->ring_off);
+  CUDA_TRY(cudaMemcpyAsync(d, c->pin + c->ring_off, bytes, cudaMemcpyHostToDevice, c->st));
+  c->ring_off += aligned;
+  return d;
+}
+template <class T>
+T* upload(spq_ctx* c, const std::vector<T>& v) {
+  return upload(c, v.data(), v.size());
+}
+
+void flush_deferred(spq_ctx* c) {
+  for (double* p : c->deferred) dfree(c, p);
+  c->deferred.clear();
+}
+
+struct Scope {
+  spq_ctx* c;
+  int fam;
+  cudaEvent_t a, b;
+  Scope(spq_ctx* c_, int f) : c(c_), fam(f) {
+    if (c->timing) {
+      CUDA_TRY(cudaEventCreate(&a));
+      CUDA_TRY(cudaEventRecord(a, c->st));
+    }
+  }
+  ~Scope() {
+    if (c->timing) {
+      cudaEventCreate(&b);
+      cudaEventRecord(b, c->st);
+      c->tm.ev[fam].push_back({a, b});
+    }
+  }
+};
+
+void collect_timings(spq_ctx* c) {
+  for (int f = 0; f < F_NFAM; ++f) {
+    for (auto& e : c->tm.ev[f]) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventSynchronize(e.second));
+      CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+      c->tm.ms[f] += ms;
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    c->tm.ev[f].clear();
+  }
+}
+
+void ensure_err_slots(spq_ctx* c, int n) {
+  if (n <= c->err_slots) return;
+  dfree(c, c->d_err_idx);
+  dfree(c, c->d_err_val);
+  int cap = std::max(n, 2 * c->err_slots + 64);
+  c->d_err_idx = (int64_t*)dalloc(c, cap * sizeof(int64_t));
+  c->d_err_val = dalloc(c, cap * sizeof(double));
+  c->err_slots = cap;
+}
+
+// --------------------------------------------------------- copy batches
+struct CopyBatch {
+  std::vector<CopyTask> t;
+  int64_t maxe = 0;
+  void add(const CopyTask& x) {
+    if (x.nr <= 0 || x.nc <= 0) return;
+    t.push_back(x);
+    maxe = std::max<int64_t>(maxe, (int64_t)x.nr * x.nc);
+  }
+  void zero(double* dst, int64_t n) {
+    if (n <= 0) return;
+    // split very long fills into columns of 1<<20 for the 2D grid
+    const int64_t col = 1 << 20;
+    CopyTask x{};
+    x.dst = dst;
+    if (n <= col) {
+      x.nr = (int)n; x.nc = 1; x.ldd = (int)n;
+      add(x);
+    } else {
+      const int64_t full = n / col;
+      x.nr = (int)col; x.nc = (int)full; x.ldd = (int)col;
+      add(x);
+      if (n - full * col > 0) zero(dst + full * col, n - full * col);
+    }
+  }
+  void run(spq_ctx* c) {
+    if (t.empty()) return;
+    Scope s(c, F_COPY);
+    const CopyTask* d = upload(c, t);
+    launch_copy(d, (int)t.size(), maxe, c->st);
+    c->tm.launches[F_COPY]++;
+    t.clear();
+    maxe = 0;
+  }
+};
+
+// --------------------------------------------------------- gemm batches
+struct GemmBatch {
+  std::vector<GemmProb> p;
+  int tiles = 0;
+  void add(const double* A, int lda, const double* B, int ldb, double* C, int ldc, int m, int n,
+           int k, double alpha, double beta) {
+    const int t = gemm_tiles(m, n);
+    if (t == 0) return;
+    GemmProb g{A, B, C, m, n, k, lda, ldb, ldc, alpha, beta, tiles};
+    p.push_back(g);
+    tiles += t;
+  }
+  void run(spq_ctx* c, bool transA, double flops) {
+    if (p.empty()) return;
+    Scope s(c, F_WY);
+    const GemmProb* d = upload(c, p);
+    launch_gemm(d, (int)p.size(), tiles, transA, c->st);
+    c->tm.launches[F_WY]++;
+    c->tm.flops[F_WY] += flops;
+    p.clear();
+    tiles = 0;
+  }
+};
+
+// ----------------------------------------------------------- QR engine
+struct QrProb {
+  double* P;  // m x k, ld m -> V on exit
+  int m, k;
+  double* R;  // k x k
+  double* tau;
+  double* T;  // k x k
+};
+
+constexpr int NB = 32;
+constexpr size_t SLAB_BYTES = 190 * 1024;
+
+void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs, int fam_flops = F_QR) {
+  if (probs.empty()) return;
+  double qr_flops = 0;
+  for (auto& q : probs) qr_flops += 2.0 * q.m * (double)q.k * q.k - 2.0 * q.k * (double)q.k * q.k / 3.0;
+  c->tm.flops[fam_flops] += qr_flops;
+  // classify
+  std::vector<int> single, blocked;
+  for (int i = 0; i < (int)probs.size(); ++i) {
+    const auto& q = probs[i];
+    if (q.k <= 0) continue;
+    if (q.k <= 128 && (size_t)q.m * q.k * 8 <= SLAB_BYTES - 8 * 1024)
+      single.push_back(i);
+    else
+      blocked.push_back(i);
+  }
+  // scratch: per blocked prob trailing W/W2 (NB x k each), G (k x k) for all
+  size_t g_off = 0;
+  std::vector<size_t> goff(probs.size()), woff(probs.size());
+  for (size_t i = 0; i < probs.size(); ++i) {
+    goff[i] = g_off;
+    g_off += (size_t)probs[i].k * probs[i].k;
+  }
+  size_t w_tot = 0;
+  for (int i : blocked) {
+    woff[i] = w_tot;
+    w_tot += 2 * (size_t)NB * probs[i].k;
+  }
+  double* scratch = dalloc(c, (g_off + w_tot) * sizeof(double));
+  double* Gs = scratch;
+  double* Ws = scratch + g_off;
+
+  {
+    Scope s(c, F_QR);
+    if (!single.empty()) {
+      std::vector<PanelJob> jobs;
+      int kbmax = 0;
+      int64_t slab = 0;
+      for (int i : single) {
+        const auto& q = probs[i];
+        jobs.push_back(PanelJob{q.P, q.R, q.tau, q.T, q.m, q.k, 0, q.k, 0});
+        kbmax = std::max(kbmax, q.k);
+        slab = std::max<int64_t>(slab, (int64_t)q.m * q.k);
+      }
+      launch_panel_qr(upload(c, jobs), (int)jobs.size(), 1, slab, true, kbmax, c->st);
+      c->tm.launches[F_QR]++;
+    }
+  }
+  if (!blocked.empty()) {
+    int maxk = 0;
+    for (int i : blocked) maxk = std::max(maxk, probs[i].k);
+    for (int j0 = 0; j0 < maxk; j0 += NB) {
+      // group jobs by (cluster size, smem)
+      std::map<std::pair<int, int>, std::pair<std::vector<PanelJob>, int64_t>> groups;
+      GemmBatch g1, g2, g3;
+      for (int i : blocked) {
+        const auto& q = probs[i];
+        if (j0 >= q.k) continue;
+        const int kb = std::min(NB, q.k - j0);
+        const int mh = q.m - j0;
+        int cl = (int)(((size_t)mh * kb * 8 + SLAB_BYTES - 1) / SLAB_BYTES);
+        cl = std::max(1, cl);
+        int smem = 1;
+        if (cl > 8) { cl = 8; smem = 0; }
+        // keep at least ~64 rows per CTA
+        while (cl > 1 && (mh + cl - 1) / cl < 64) --cl;
+        const int rpc = (mh + cl - 1) / cl;
+        const int j1 = j0 + kb;
+        auto& grp = groups[{cl, smem}];
+        grp.first.push_back(PanelJob{q.P, q.R, q.tau, q.T, q.m, q.k, j0, kb, j1 < q.k ? 1 : 0});
+        grp.second = std::max<int64_t>(grp.second, (int64_t)rpc * kb);
+        if (j1 < q.k) {
+          double* W = Ws + woff[i];
+          double* W2 = W + (size_t)NB * q.k;
+          const int nt = q.k - j1;
+          double* Vb = q.P + j0 + (int64_t)j0 * q.m;
+          double* Pt = q.P + j0 + (int64_t)j1 * q.m;
+          g1.add(Vb, q.m, Pt, q.m, W, kb, kb, nt, mh, 1.0, 0.0);
+          g2.add(q.T + j0 + (int64_t)j0 * q.k, q.k, W, kb, W2, kb, kb, nt, kb, 1.0, 0.0);
+          g3.add(Vb, q.m, W2, kb, Pt, q.m, mh, nt, kb, -1.0, 1.0);
+        }
+      }
+      {
+        Scope s(c, F_QR);
+        for (auto& kv : groups) {
+          launch_panel_qr(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first.first,
+                          kv.second.second, kv.first.second != 0, NB, c->st);
+          c->tm.launches[F_QR]++;
+        }
+      }
+      g1.run(c, true, 0);
+      g2.run(c, true, 0);
+      g3.run(c, false, 0);
+    }
+  }
+  // full T: G = V^T V, then the row recurrence
+  GemmBatch gg;
+  std::vector<LarftJob> lj;
+  int ltiles = 0;
+  for (size_t i = 0; i < probs.size(); ++i) {
+    const auto& q = probs[i];
+    if (q.k <= 0) continue;
+    gg.add(q.P, q.m, q.P, q.m, Gs + goff[i], q.k, q.k, q.k, q.m, 1.0, 0.0);
+    lj.push_back(LarftJob{Gs + goff[i], q.tau, q.T, q.k, q.k, q.k, ltiles});
+    ltiles += larft_tiles(q.k);
+  }
+  gg.run(c, true, 0);
+  {
+    Scope s(c, F_QR);
+    launch_larft(upload(c, lj), (int)lj.size(), ltiles, c->st);
+    c->tm.launches[F_QR]++;
+  }
+  dfree(c, scratch);
+}
+
+// C <- C - V T^T V^T C (transpose) or C - V T V^T C
+struct WyProb {
+  const double* V;
+  const double* T;
+  int m, k;
+  double* C;
+  int ldc, n;
+};
+
+void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs, bool transpose, int fam = F_WY) {
+  size_t tot = 0;
+  double flops = 0;
+  for (auto& p : probs) {
+    if (p.k > 0 && p.n > 0 && p.m > 0) tot += 2 * (size_t)p.k * p.n;
+    flops += 4.0 * p.m * (double)p.n * p.k - (double)p.n * p.k * p.k;
+  }
+  (void)fam;
+  if (tot == 0) return;
+  double* scr = dalloc(c, tot * sizeof(double));
+  GemmBatch g1, g2, g3;
+  size_t off = 0;
+  for (auto& p : probs) {
+    if (p.k <= 0 || p.n <= 0 || p.m <= 0) continue;
+    double* W = scr + off;
+    double* W2 = W + (size_t)p.k * p.n;
+    off += 2 * (size_t)p.k * p.n;
+    g1.add(p.V, p.m, p.C, p.ldc, W, p.k, p.k, p.n, p.m, 1.0, 0.0);
+    g2.add(p.T, p.k, W, p.k, W2, p.k, p.k, p.n, p.k, 1.0, 0.0);
+    g3.add(p.V, p.m, W2, p.k, p.C, p.ldc, p.m, p.n, p.k, -1.0, 1.0);
+  }
+  g1.run(c, true, flops);
+  g2.run(c, transpose, 0);
+  g3.run(c, false, 0);
+  dfree(c, scr);
+}
+
+// pivot checks for a batch; returns the first failing job (in order) or -1
+struct PivotSet {
+  std::vector<PivotJob> jobs;
+  std::vector<std::string> ctx;
+};
+
+void pivot_launch(spq_ctx* c, PivotSet& ps) {
+  if (ps.jobs.empty()) return;
+  ensure_err_slots(c, (int)ps.jobs.size());
+  for (int i = 0; i < (int)ps.jobs.size(); ++i) ps.jobs[i].slot = i;
+  launch_pivot_check(upload(c, ps.jobs), (int)ps.jobs.size(), c->d_err_idx, c->d_err_val, c->st);
+}
+
+void pivot_raise(spq_ctx* c, PivotSet& ps) {
+  if (ps.jobs.empty()) return;
+  const int n = (int)ps.jobs.size();
+  std::vector<int64_t> idx(n);
+  std::vector<double> val(n);
+  CUDA_TRY(cudaMemcpyAsync(idx.data(), c->d_err_idx, n * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           c->st));
+  CUDA_TRY(cudaMemcpyAsync(val.data(), c->d_err_val, n * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->st));
+  sync(c);
+  for (int i = 0; i < n; ++i)
+    if (idx[i] >= 0) throw SpqError(SPQ_ERR_SINGULAR, ps.ctx[i], idx[i], val[i]);
+  ps.jobs.clear();
+  ps.ctx.clear();
+}
+
+// ----------------------------------------------------- block bookkeeping
+Block* find_block(spq_ctx* c, int i, int j) {
+  auto it = c->blk.find(bkey(i, j));
+  return it == c->blk.end() ? nullptr : &it->second;
+}
+
+Block& put_block(spq_ctx* c, int i, int j, double* p, int nr, int nc) {
+  Block& b = c->blk[bkey(i, j)];
+  b.p = p;
+  b.nr = nr;
+  b.nc = nc;
+  c->rix[i].insert(j);
+  c->cix[j].insert(i);
+  return b;
+}
+
+void drop_block(spq_ctx* c, int i, int j) {
+  auto it = c->blk.find(bkey(i, j));
+  if (it != c->blk.end()) {
+    if (it->second.p) c->deferred.push_back(it->second.p);
+    c->blk.erase(it);
+  }
+  c->rix[i].erase(j);
+  c->cix[j].erase(i);
+}
+
+void retire(spq_ctx* c, int s) {
+  c->active[s] = 0;
+  c->rows_of[s].clear();
+  c->cols_of[s].clear();
+  c->rix[s].clear();
+  c->cix[s].clear();
+}
+
+double* new_block_mem(spq_ctx* c, int nr, int nc) {
+  return dalloc(c, (size_t)std::max(1, nr) * std::max(1, nc) * sizeof(double));
+}
+
+// refresh row flags of every non-clean block in the given row clusters
+void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
+  std::vector<const double*> ptrs;
+  std::vector<int> nr, nc;
+  std::vector<int64_t> off;
+  std::vector<Block*> which;
+  int64_t tot = 0;
+  for (int r : row_clusters) {
+    for (int cc : c->rix[r]) {
+      Block* b = find_block(c, r, cc);
+      if (!b || b->clean) continue;
+      if (b->nr == 0) { b->flags.clear(); b->clean = true; continue; }
+      if (b->nc == 0) { b->flags.assign(b->nr, 0); b->clean = true; continue; }
+      ptrs.push_back(b->p);
+      nr.push_back(b->nr);
+      nc.push_back(b->nc);
+      off.push_back(tot);
+      which.push_back(b);
+      tot += b->nr;
+    }
+  }
+  if (which.empty()) return;
+  unsigned char* d_out = (unsigned char*)dalloc(c, tot);
+  {
+    Scope s(c, F_FLAGS);
+    launch_rowflags(upload(c, ptrs), upload(c, nr), upload(c, nc), upload(c, off), d_out,
+                    (int)which.size(), c->st);
+    c->tm.launches[F_FLAGS]++;
+  }
+  std::vector<unsigned char> h(tot);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), d_out, tot, cudaMemcpyDeviceToHost, c->st));
+  dfree(c, d_out);
+  sync(c);
+  for (size_t t = 0; t < which.size(); ++t) {
+    Block* b = which[t];
+    b->flags.assign(h.begin() + off[t], h.begin() + off[t] + b->nr);
+    b->clean = true;
+  }
+}
+
+int* upload_idx32(spq_ctx* c, const std::vector<int64_t>& v) {
+  std::vector<int> t(v.begin(), v.end());
+  return upload(c, t);
+}
+
+int* persist_idx32(spq_ctx* c, const std::vector<int64_t>& v) {
+  if (v.empty()) return nullptr;
+  std::vector<int> t(v.begin(), v.end());
+  int* d = (int*)dalloc(c, t.size() * sizeof(int));
+  CUDA_TRY(cudaMemcpyAsync(d, t.data(), t.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
+  sync(c);  // t is pageable/stack memory: keep it alive until the copy is done
+  return d;
+}
+
+// ================================================================ (a) factor
+struct Part {
+  int r;
+  std::vector<int> ix;  // local rows (empty => all rows when full)
+  bool full;
+  int o0, o1;
+};
+
+struct Front {
+  int s = -1;
+  int m = 0, k = 0, n = 0;
+  std::vector<Part> parts;
+  std::vector<int> cols_t;
+  std::vector<int> woff;
+  std::vector<int64_t> stack_rows;
+  // captured gather sources (pre-update pointers)
+  struct Src { const double* p; int nr; int part; int col_off; int ncols; bool full; };
+  std::vector<Src> gsrc;       // C gather
+  std::vector<Src> psrc;       // panel gather
+  // scatter destinations (post-update pointers)
+  struct Dst { double* p; int nr; int part; int col_off; int ncols; bool full; };
+  std::vector<Dst> dsts;
+  std::vector<const int*> d_ix;  // per part: device local-row list (nullptr = all rows)
+  int rec = -1;
+};
+
+// plan front s from the current structure; returns false if a queried row
+// is not known yet (written earlier in this wave)
+bool plan_front(spq_ctx* c, int s, Front& f) {
+  f = Front();
+  f.s = s;
+  const auto& rows_s = c->rows_of[s];
+  const auto& cols_s = c->cols_of[s];
+  f.k = (int)cols_s.size();
+  Part p0;
+  p0.r = s;
+  p0.full = true;
+  p0.o0 = 0;
+  p0.o1 = (int)rows_s.size();
+  f.parts.push_back(p0);
+  std::vector<int> rs(c->cix[s].begin(), c->cix[s].end());
+  int off = p0.o1;
+  for (int r : rs) {
+    if (r == s) continue;
+    Block* b = find_block(c, r, s);
+    if (!b) continue;
+    Part p;
+    p.r = r;
+    for (int i = 0; i < b->nr; ++i) {
+      const uint8_t fl = b->clean ? b->flags[i] : (b->flags.empty() ? 2 : b->flags[i]);
+      if (fl == 2) return false;
+      if (fl == 1) p.ix.push_back(i);
+    }
+    if (p.ix.empty()) continue;
+    p.full = (int)p.ix.size() == b->nr;
+    p.o0 = off;
+    off += (int)p.ix.size();
+    p.o1 = off;
+    f.parts.push_back(std::move(p));
+  }
+  f.m = off;
+  // candidate trailing columns
+  std::set<int> cand;
+  for (auto& p : f.parts)
+    for (int cc : c->rix[p.r])
+      if (cc != s) cand.insert(cc);
+  int w = 0;
+  for (int cc : cand) {
+    bool present = false;
+    for (auto& p : f.parts) {
+      Block* b = find_block(c, p.r, cc);
+      if (!b || b->nr == 0 || b->nc == 0) continue;
+      const auto& fl = b->flags;
+      const bool known = b->clean || !fl.empty();
+      if (p.full) {
+        for (int i = 0; i < b->nr; ++i) {
+          const uint8_t v = known ? fl[i] : 2;
+          if (v == 2) return false;
+          if (v == 1) { present = true; break; }
+        }
+      } else {
+        for (int i : p.ix) {
+          const uint8_t v = known ? fl[i] : 2;
+          if (v == 2) return false;
+          if (v == 1) { present = true; break; }
+        }
+      }
+      if (present) break;
+    }
+    if (present) {
+      f.cols_t.push_back(cc);
+      f.woff.push_back(w);
+      w += (int)c->cols_of[cc].size();
+    }
+  }
+  f.n = w;
+  for (auto& p : f.parts) {
+    const auto& rr = c->rows_of[p.r];
+    if (p.r == s || p.full)
+      f.stack_rows.insert(f.stack_rows.end(), rr.begin(), rr.end());
+    else
+      for (int i : p.ix) f.stack_rows.push_back(rr[i]);
+  }
+  return true;
+}
+
+void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
+  const int s = f.s;
+  // gather sources (current blocks, before any replacement)
+  for (int pi = 0; pi < (int)f.parts.size(); ++pi) {
+    auto& p = f.parts[pi];
+    Block* b = find_block(c, p.r, s);
+    if (b && b->nc > 0 && b->nr > 0) f.psrc.push_back({b->p, b->nr, pi, 0, b->nc, p.full});
+    for (int ci = 0; ci < (int)f.cols_t.size(); ++ci) {
+      Block* bc = find_block(c, p.r, f.cols_t[ci]);
+      if (bc && bc->nr > 0 && bc->nc > 0)
+        f.gsrc.push_back({bc->p, bc->nr, pi, f.woff[ci], bc->nc, p.full});
+    }
+  }
+  // trailing blocks of the neighbour rows (factor.py:467-480)
+  for (int ci = 0; ci < (int)f.cols_t.size(); ++ci) {
+    const int cc = f.cols_t[ci];
+    const int ncol = (int)c->cols_of[cc].size();
+    for (int pi = 1; pi < (int)f.parts.size(); ++pi) {
+      auto& p = f.parts[pi];
+      const int nr = (int)c->rows_of[p.r].size();
+      if (p.full) {
+        Block* old = find_block(c, p.r, cc);
+        if (old && old->p) c->deferred.push_back(old->p);
+        double* mem = new_block_mem(c, nr, ncol);
+        Block& b = put_block(c, p.r, cc, mem, nr, ncol);
+        b.flags.assign(nr, 2);
+        b.clean = false;
+        f.dsts.push_back({mem, nr, pi, f.woff[ci], ncol, true});
+      } else {
+        Block* b = find_block(c, p.r, cc);
+        if (!b) {
+          double* mem = new_block_mem(c, nr, ncol);
+          zeros.zero(mem, (int64_t)nr * ncol);
+          Block& nb = put_block(c, p.r, cc, mem, nr, ncol);
+          nb.flags.assign(nr, 0);
+          nb.clean = false;
+          b = &nb;
+        } else if (b->flags.size() != (size_t)nr) {
+          b->flags.assign(nr, 2);
+        }
+        for (int i : p.ix) b->flags[i] = 2;
+        b->clean = false;
+        f.dsts.push_back({b->p, nr, pi, f.woff[ci], ncol, false});
+      }
+    }
+  }
+  // delete row/col s (factor.py:481-484)
+  std::vector<int> rr(c->cix[s].begin(), c->cix[s].end());
+  for (int r : rr) drop_block(c, r, s);
+  std::vector<int> cc2(c->rix[s].begin(), c->rix[s].end());
+  for (int cc : cc2) drop_block(c, s, cc);
+  // record + bookkeeping (factor.py:486-492)
+  Record rec;
+  rec.kind = REC_ELIM;
+  rec.m = f.m;
+  rec.k = f.k;
+  rec.n = f.n;
+  rec.rows = f.stack_rows;
+  rec.cols_s = c->cols_of[s];
+  for (int cc : f.cols_t) rec.cols_n.insert(rec.cols_n.end(), c->cols_of[cc].begin(), c->cols_of[cc].end());
+  const size_t mk = (size_t)f.m * f.k, kk = (size_t)f.k * f.k, kn = (size_t)f.k * f.n;
+  rec.payload = dalloc(c, (mk + f.k + 2 * kk + kn) * sizeof(double));
+  rec.V = rec.payload;
+  rec.tau = rec.V + mk;
+  rec.T = rec.tau + f.k;
+  rec.R = rec.T + kk;
+  rec.Rsn = rec.R + kk;
+  rec.payload_scalars = (int64_t)(mk + f.k + kk) + (int64_t)kk + (int64_t)kn;
+  zeros.zero(rec.payload, (int64_t)(mk + f.k + 2 * kk));
+  for (size_t i = 0; i < c->cols_of[s].size(); ++i) c->row_of_col[c->cols_of[s][i]] = c->rows_of[s][i];
+  f.rec = (int)c->recs.size();
+  c->recs.push_back(std::move(rec));
+  retire(c, s);
+}
+
+void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotSet& ps) {
+  // scratch per front: C (m x n)
+  size_t tot = 0;
+  std::vector<size_t> coff(wave.size());
+  for (size_t i = 0; i < wave.size(); ++i) {
+    coff[i] = tot;
+    tot += (size_t)wave[i].m * wave[i].n;
+  }
+  double* scr = tot ? dalloc(c, tot * sizeof(double)) : nullptr;
+  for (size_t i = 0; i < wave.size(); ++i) zeros.zero(scr + coff[i], (int64_t)wave[i].m * wave[i].n);
+  zeros.run(c);
+  // gather
+  CopyBatch g;
+  for (size_t fi = 0; fi < wave.size(); ++fi) {
+    Front& f = wave[fi];
+    Record& rec = c->recs[f.rec];
+    double* C = scr + coff[fi];
+    f.d_ix.assign(f.parts.size(), nullptr);
+    for (size_t pi = 0; pi < f.parts.size(); ++pi) {
+      auto& p = f.parts[pi];
+      if (p.r != f.s && !p.full) f.d_ix[pi] = upload(c, p.ix);
+    }
+    for (auto& sp : f.psrc) {
+      auto& p = f.parts[sp.part];
+      CopyTask t{};
+      t.src = sp.p; t.dst = rec.V + p.o0; t.src_rows = f.d_ix[sp.part];
+      t.nr = p.o1 - p.o0; t.nc = sp.ncols; t.lds = sp.nr; t.ldd = f.m;
+      g.add(t);
+    }
+    for (auto& sg : f.gsrc) {
+      auto& p = f.parts[sg.part];
+      CopyTask t{};
+      t.src = sg.p; t.dst = C + p.o0 + (int64_t)sg.col_off * f.m; t.src_rows = f.d_ix[sg.part];
+      t.nr = p.o1 - p.o0; t.nc = sg.ncols; t.lds = sg.nr; t.ldd = f.m;
+      g.add(t);
+    }
+  }
+  g.run(c);
+  // QR of every panel
+  std::vector<QrProb> qp;
+  for (auto& f : wave) {
+    Record& rec = c->recs[f.rec];
+    qp.push_back(QrProb{rec.V, f.m, f.k, rec.R, rec.tau, rec.T});
+  }
+  qr_batch(c, qp);
+  for (auto& f : wave) {
+    Record& rec = c->recs[f.rec];
+    ps.jobs.push_back(PivotJob{rec.R, f.k, f.k, 0});
+    ps.ctx.push_back("pivot block of cluster " + std::to_string(f.s));
+  }
+  // trailing update C <- H^T C
+  std::vector<WyProb> wp;
+  for (size_t fi = 0; fi < wave.size(); ++fi) {
+    Front& f = wave[fi];
+    Record& rec = c->recs[f.rec];
+    wp.push_back(WyProb{rec.V, rec.T, f.m, f.k, scr + coff[fi], f.m, f.n});
+  }
+  wy_batch(c, wp, true);
+  // scatter: R_sn = C[:k], neighbour rows back into blocks
+  CopyBatch sc;
+  for (size_t fi = 0; fi < wave.size(); ++fi) {
+    Front& f = wave[fi];
+    Record& rec = c->recs[f.rec];
+    double* C = scr + coff[fi];
+    CopyTask t{};
+    t.src = C; t.dst = rec.Rsn; t.nr = f.k; t.nc = f.n; t.lds = f.m; t.ldd = f.k;
+    sc.add(t);
+    for (auto& d : f.dsts) {
+      auto& p = f.parts[d.part];
+      CopyTask u{};
+      u.src = C + p.o0 + (int64_t)d.col_off * f.m;
+      u.dst = d.p;
+      u.nr = p.o1 - p.o0;
+      u.nc = d.ncols;
+      u.lds = f.m;
+      u.ldd = d.nr;
+      u.dst_rows = d.full ? nullptr : f.d_ix[d.part];
+      sc.add(u);
+    }
+  }
+  sc.run(c);
+  pivot_launch(c, ps);
+  dfree(c, scr);
+  flush_deferred(c);
+}
+
+void do_factor(spq_ctx* c, const std::vector<int>& ids) {
+  size_t pos = 0;
+  std::vector<int> stamp(c->N, -1);
+  int wave_id = 0;
+  PivotSet ps;
+  while (pos < ids.size()) {
+    // refresh flags of every row cluster any pending op may query
+    std::set<int> rows;
+    for (size_t t = pos; t < ids.size(); ++t) {
+      const int s = ids[t];
+      rows.insert(s);
+      for (int r : c->cix[s]) rows.insert(r);
+    }
+    refresh_flags(c, std::vector<int>(rows.begin(), rows.end()));
+    pivot_raise(c, ps);   // previous wave (synced by refresh)
+    ++wave_id;
+    std::vector<Front> wave;
+    CopyBatch zeros;
+    while (pos < ids.size()) {
+      const int s = ids[pos];
+      if (!c->active[s]) throw SpqError(SPQ_ERR_BAD_INPUT, "factor of inactive cluster " + std::to_string(s));
+      if (c->cols_of[s].empty()) {  // factor.py:413-415
+        retire(c, s);
+        ++pos;
+        continue;
+      }
+      Front f;
+      if (!plan_front(c, s, f)) break;
+      bool clash = false;
+      for (int64_t r : f.stack_rows)
+        if (stamp[r] == wave_id) { clash = true; break; }
+      if (clash) break;
+      for (int64_t r : f.stack_rows) stamp[r] = wave_id;
+      apply_front_structure(c, f, zeros);
+      wave.push_back(std::move(f));
+      ++pos;
+    }
+    if (wave.empty()) {
+      if (pos < ids.size()) throw SpqError(SPQ_ERR_INTERNAL, "wave planner made no progress");
+      break;
+    }
+    execute_wave(c, wave, zeros, ps);
+  }
+  pivot_raise(c, ps);
+  flush_deferred(c);
+}
+
+// ================================================================ (b) scale
+void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
+  std::vector<int> todo;
+  for (size_t t = 0; t < ids.size(); ++t) {
+    done[t] = 0;
+    const int p = ids[t];
+    if (!c->active[p]) throw SpqError(SPQ_ERR_BAD_INPUT, "scale of inactive cluster");
+    if (!c->cols_of[p].empty()) { todo.push_back(p); done[t] = 1; }
+  }
+  if (todo.empty()) return;
+  CopyBatch zeros, g;
+  std::vector<QrProb> qp;
+  std::vector<int> recid;
+  for (int p : todo) {
+    const int np = (int)c->cols_of[p].size();
+    Record rec;
+    rec.kind = REC_SCALE;
+    rec.m = np; rec.k = np; rec.n = 0;
+    rec.rows = c->rows_of[p];
+    rec.cols_s = c->cols_of[p];
+    const size_t kk = (size_t)np * np;
+    rec.payload = dalloc(c, (kk + np + 2 * kk) * sizeof(double));
+    rec.V = rec.payload; rec.tau = rec.V + kk; rec.T = rec.tau + np; rec.R = rec.T + kk;
+    rec.payload_scalars = (int64_t)(kk + np + kk) + (int64_t)kk;
+    zeros.zero(rec.payload, (int64_t)(3 * kk + np));
+    Block* b = find_block(c, p, p);
+    if (b && b->nr == np && b->nc == np) {
+      CopyTask t{};
+      t.src = b->p; t.dst = rec.V; t.nr = np; t.nc = np; t.lds = np; t.ldd = np;
+      g.add(t);
+    }
+    qp.push_back(QrProb{rec.V, np, np, rec.R, rec.tau, rec.T});
+    recid.push_back((int)c->recs.size());
+    c->recs.push_back(std::move(rec));
+  }
+  zeros.run(c);
+  g.run(c);
+  qr_batch(c, qp);
+  PivotSet ps;
+  for (size_t t = 0; t < todo.size(); ++t) {
+    Record& rec = c->recs[recid[t]];
+    ps.jobs.push_back(PivotJob{rec.R, rec.k, rec.k, 0});
+    ps.ctx.push_back("diagonal block of interface " + std::to_string(todo[t]));
+  }
+  pivot_launch(c, ps);
+  // left: U^T on every (p, c) block; right: R^{-1} on every (r, p) block
+  std::vector<WyProb> wp;
+  std::vector<TrsmJob> tj;
+  int ttiles = 0;
+  double trsm_flops = 0;
+  for (size_t t = 0; t < todo.size(); ++t) {
+    const int p = todo[t];
+    Record& rec = c->recs[recid[t]];
+    for (int cc : c->rix[p]) {
+      if (cc == p) continue;
+      Block* b = find_block(c, p, cc);
+      if (b && b->nc > 0) {
+        wp.push_back(WyProb{rec.V, rec.T, rec.m, rec.k, b->p, b->nr, b->nc});
+        b->clean = false;
+      }
+    }
+    for (int r : c->cix[p]) {
+      if (r == p) continue;
+      Block* b = find_block(c, r, p);
+      if (b && b->nr > 0) {
+        tj.push_back(TrsmJob{rec.R, b->p, b->nr, rec.k, rec.k, b->nr, ttiles});
+        ttiles += trsm_tiles(b->nr);
+        trsm_flops += (double)b->nr * rec.k * rec.k;
+        b->clean = false;
+      }
+    }
+  }
+  wy_batch(c, wp, true);
+  {
+    Scope s(c, F_TRSM);
+    launch_trsm_right(upload(c, tj), (int)tj.size(), ttiles, c->st);
+    c->tm.launches[F_TRSM]++;
+    c->tm.flops[F_TRSM] += trsm_flops;
+  }
+  CopyBatch id;
+  for (int p : todo) {
+    const int np = (int)c->cols_of[p].size();
+    Block* b = find_block(c, p, p);
+    double* mem;
+    if (b && b->nr == np && b->nc == np) {
+      mem = b->p;
+    } else {
+      mem = new_block_mem(c, np, np);
+      Block& nb = put_block(c, p, p, mem, np, np);
+      (void)nb;
+      b = find_block(c, p, p);
+    }
+    b->clean = false;
+    CopyTask t{};
+    t.dst = mem; t.nr = np; t.nc = np; t.ldd = np; t.ident = 1;
+    id.add(t);
+  }
+  id.run(c);
+  pivot_raise(c, ps);
+  flush_deferred(c);
+}
+
+// ============================================================ (c) sparsify
+struct SparsifyOut {
+  int rank;
+  int before;
+  double dropped;
+  int done;
+};
+
+SparsifyOut do_sparsify_one(spq_ctx* c, int p, double eps) {
+  SparsifyOut o{-1, 0, 0.0, 0};
+  if (!c->active[p]) throw SpqError(SPQ_ERR_BAD_INPUT, "sparsify of inactive cluster");
+  const std::vector<int64_t> cols_p = c->cols_of[p], rows_p = c->rows_of[p];
+  const int np = (int)cols_p.size();
+  o.before = np;
+  if (np == 0) return o;
+  std::vector<int> us, cs;
+  for (int u : c->cix[p]) if (u != p) us.push_back(u);
+  for (int cc : c->rix[p]) if (cc != p) cs.push_back(cc);
+  std::vector<int> hu, wc;
+  int nu = 0, ncl = 0;
+  for (int u : us) { hu.push_back(find_block(c, u, p)->nr); nu += hu.back(); }
+  for (int cc : cs) { wc.push_back(find_block(c, p, cc)->nc); ncl += wc.back(); }
+  const int ncols = nu + ncl;
+  // device buffers: M (np x ncols), W (np x ncols), V (np x kmax), misc
+  const int kmax = std::min(np, ncols);
+  const size_t Msz = (size_t)np * std::max(ncols, 1);
+  double* M = dalloc(c, Msz * sizeof(double));
+  double* Wm = dalloc(c, Msz * sizeof(double));
+  double* sq = dalloc(c, std::max(ncols, 1) * sizeof(double));
+  int* keep = (int*)dalloc(c, std::max(ncols, 1) * sizeof(int));
+  const int G = cpqr_grid(std::max(ncols, 1), c->nsm);
+  // small device scalars block
+  struct Sc { int nk; int rank; double ratio; double maxcol; };
+  Sc* dsc = (Sc*)dalloc(c, sizeof(Sc));
+  double* slots = dalloc(c, 2 * G * sizeof(double));
+  int* slotp = (int*)dalloc(c, 2 * G * sizeof(int));
+  int* perm = (int*)dalloc(c, std::max(ncols, 1) * sizeof(int));
+  // the record payload: V (np x kmax) | tau | beta | T (kmax^2)
+  const size_t vsz = (size_t)np * std::max(kmax, 1);
+  double* pay = dalloc(c, (vsz + 2 * (size_t)std::max(kmax, 1) + (size_t)kmax * kmax) * sizeof(double));
+  double* V = pay;
+  double* tau = V + vsz;
+  double* beta = tau + std::max(kmax, 1);
+  double* T = beta + std::max(kmax, 1);
+  CopyBatch g;
+  g.zero(V, (int64_t)vsz);
+  int off = 0;
+  for (size_t t = 0; t < us.size(); ++t) {
+    Block* b = find_block(c, us[t], p);
+    CopyTask x{};
+    x.src = b->p; x.dst = M + (int64_t)off * np; x.nr = b->nr; x.nc = np; x.lds = b->nr;
+    x.ldd = np; x.trans = 1;
+    g.add(x);
+    off += b->nr;
+  }
+  for (size_t t = 0; t < cs.size(); ++t) {
+    Block* b = find_block(c, p, cs[t]);
+    CopyTask x{};
+    x.src = b->p; x.dst = M + (int64_t)off * np; x.nr = np; x.nc = b->nc; x.lds = np; x.ldd = np;
+    g.add(x);
+    off += b->nc;
+  }
+  g.run(c);
+  {
+    Scope s(c, F_CPQR);
+    launch_sparsify_prep(M, np, ncols, eps, sq, keep, &dsc->nk, &dsc->ratio, &dsc->maxcol, Wm,
+                         c->st);
+    CpqrArgs a{};
+    a.W = Wm; a.m = np; a.ncols_cap = std::max(ncols, 1); a.nk = &dsc->nk; a.eps = &dsc->ratio;
+    a.min_rank = 0; a.V = V; a.tau = tau; a.beta = beta; a.rank = &dsc->rank; a.perm = perm;
+    a.slot_val = slots; a.slot_pos = slotp; a.finalize = 0;
+    launch_cpqr(a, G, c->st);
+    c->tm.launches[F_CPQR] += 4;
+  }
+  Sc h{};
+  CUDA_TRY(cudaMemcpyAsync(&h, dsc, sizeof(Sc), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  const int r = h.rank;
+  o.rank = r;
+  {
+    const double mm = np, nn = h.nk, rr = r;
+    c->tm.flops[F_CPQR] += 4.0 * mm * nn * rr - 2.0 * rr * rr * (mm + nn) + 4.0 * rr * rr * rr / 3.0;
+  }
+  auto release = [&]() {
+    dfree(c, M); dfree(c, Wm); dfree(c, sq); dfree(c, keep); dfree(c, dsc);
+    dfree(c, slots); dfree(c, slotp); dfree(c, perm);
+  };
+  if (r >= np) {  // factor.py:630-631
+    release();
+    dfree(c, pay);
+    return o;
+  }
+  // T of the accepted reflectors, then Q^T M
+  if (r > 0) {
+    double* G2 = dalloc(c, (size_t)r * r * sizeof(double));
+    GemmBatch gg;
+    gg.add(V, np, V, np, G2, r, r, r, np, 1.0, 0.0);
+    gg.run(c, true, 0);
+    std::vector<LarftJob> lj{LarftJob{G2, tau, T, r, r, r, 0}};
+    launch_larft(upload(c, lj), 1, larft_tiles(r), c->st);
+    std::vector<WyProb> wp{WyProb{V, T, np, r, M, np, ncols}};
+    wy_batch(c, wp, true);
+    dfree(c, G2);
+  }
+  // split back (factor.py:617-658)
+  CopyBatch sc;
+  off = 0;
+  for (size_t t = 0; t < us.size(); ++t) {
+    const int u = us[t];
+    const int h_u = hu[t];
+    Block* old = find_block(c, u, p);
+    if (old && old->p) c->deferred.push_back(old->p);
+    if ((int64_t)h_u * r > 0) {
+      double* mem = new_block_mem(c, h_u, r);
+      CopyTask x{};
+      x.src = M + (int64_t)off * np; x.dst = mem; x.nr = r; x.nc = h_u; x.lds = np; x.ldd = h_u;
+      x.trans = 1;
+      sc.add(x);
+      Block& b = put_block(c, u, p, mem, h_u, r);
+      b.clean = false;
+      b.flags.clear();
+    } else {
+      if (old) old->p = nullptr;
+      drop_block(c, u, p);
+    }
+    off += h_u;
+  }
+  for (size_t t = 0; t < cs.size(); ++t) {
+    const int cc = cs[t];
+    const int w = wc[t];
+    Block* old = find_block(c, p, cc);
+    if (old && old->p) c->deferred.push_back(old->p);
+    if ((int64_t)w * r > 0) {
+      double* mem = new_block_mem(c, r, w);
+      CopyTask x{};
+      x.src = M + (int64_t)off * np; x.dst = mem; x.nr = r; x.nc = w; x.lds = np; x.ldd = r;
+      sc.add(x);
+      Block& b = put_block(c, p, cc, mem, r, w);
+      b.clean = false;
+      b.flags.clear();
+    } else {
+      if (old) old->p = nullptr;
+      drop_block(c, p, cc);
+    }
+    off += w;
+  }
+  // diagonal block: I_r or removal
+  Block* dp = find_block(c, p, p);
+  if (dp && dp->p) c->deferred.push_back(dp->p);
+  if (dp) dp->p = nullptr;
+  if (r > 0) {
+    double* mem = new_block_mem(c, r, r);
+    CopyTask x{};
+    x.dst = mem; x.nr = r; x.nc = r; x.ldd = r; x.ident = 1;
+    sc.add(x);
+    Block& b = put_block(c, p, p, mem, r, r);
+    b.clean = false;
+    b.flags.clear();
+  } else {
+    drop_block(c, p, p);
+    for (int u : us) drop_block(c, u, p);
+    for (int cc : cs) drop_block(c, p, cc);
+  }
+  sc.run(c);
+  // record (factor.py:645-649)
+  Record rec;
+  rec.kind = REC_SPARSIFY;
+  rec.m = np; rec.k = r; rec.n = 0; rec.rank = r;
+  rec.rows = rows_p;
+  rec.cols_s = cols_p;
+  rec.payload = pay;
+  rec.V = V; rec.tau = tau; rec.T = T;
+  // V stored np x kmax (ld np): the first r columns are the panel
+  rec.payload_scalars = (int64_t)np * r + r + (int64_t)r * r;
+  for (int i = r; i < np; ++i) c->row_of_col[cols_p[i]] = rows_p[i];
+  c->rows_of[p].assign(rows_p.begin(), rows_p.begin() + r);
+  c->cols_of[p].assign(cols_p.begin(), cols_p.begin() + r);
+  c->recs.push_back(std::move(rec));
+  o.done = 1;
+  o.dropped = std::nan("");
+  release();
+  flush_deferred(c);
+  return o;
+}
+
+// ================================================================ (d) merge
+void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, const int32_t* cid) {
+  std::vector<int> parent_of(c->ncl, -1), roff(c->ncl, 0), coff(c->ncl, 0);
+  std::vector<std::vector<int64_t>> nrows(np_), ncols(np_);
+  for (int t = 0; t < np_; ++t) {
+    int ro = 0, co = 0;
+    for (int q = cptr[t]; q < cptr[t + 1]; ++q) {
+      const int k = cid[q];
+      if (k < 0 || k >= c->ncl) throw SpqError(SPQ_ERR_BAD_INPUT, "merge: bad child id");
+      parent_of[k] = pid[t];
+      roff[k] = ro;
+      coff[k] = co;
+      ro += (int)c->rows_of[k].size();
+      co += (int)c->cols_of[k].size();
+      nrows[t].insert(nrows[t].end(), c->rows_of[k].begin(), c->rows_of[k].end());
+      ncols[t].insert(ncols[t].end(), c->cols_of[k].begin(), c->cols_of[k].end());
+    }
+  }
+  std::unordered_map<uint64_t, Block> old;
+  old.swap(c->blk);
+  for (int s = 0; s < c->ncl; ++s) {
+    if (c->active[s]) { c->rows_of[s].clear(); c->cols_of[s].clear(); }
+    c->active[s] = 0;
+    c->rix[s].clear();
+    c->cix[s].clear();
+  }
+  for (int t = 0; t < np_; ++t) {
+    const int P = pid[t];
+    c->rows_of[P] = std::move(nrows[t]);
+    c->cols_of[P] = std::move(ncols[t]);
+    c->active[P] = 1;
+  }
+  CopyBatch zeros, cp;
+  // deterministic order: sort old keys
+  std::vector<uint64_t> keys;
+  keys.reserve(old.size());
+  for (auto& kv : old) keys.push_back(kv.first);
+  std::sort(keys.begin(), keys.end());
+  for (uint64_t key : keys) {
+    Block& B = old[key];
+    const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
+    if ((int64_t)B.nr * B.nc == 0) {
+      if (B.p) c->deferred.push_back(B.p);
+      continue;
+    }
+    const int Pi = parent_of[i], Pj = parent_of[j];
+    if (Pi < 0 || Pj < 0) throw SpqError(SPQ_ERR_BAD_INPUT, "merge: block of unmerged cluster");
+    Block* tgt = find_block(c, Pi, Pj);
+    const int R = (int)c->rows_of[Pi].size(), C = (int)c->cols_of[Pj].size();
+    if (!tgt) {
+      double* mem = new_block_mem(c, R, C);
+      zeros.zero(mem, (int64_t)R * C);
+      tgt = &put_block(c, Pi, Pj, mem, R, C);
+      tgt->clean = false;
+    }
+    CopyTask x{};
+    x.src = B.p; x.dst = tgt->p + roff[i] + (int64_t)coff[j] * R; x.nr = B.nr; x.nc = B.nc;
+    x.lds = B.nr; x.ldd = R;
+    cp.add(x);
+    c->deferred.push_back(B.p);
+  }
+  zeros.run(c);
+  cp.run(c);
+  flush_deferred(c);
+}
+
+// ================================================================== load
+void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indices,
+             const double* data, int equilibrate, int ncl, int nleaf, const int32_t* leaf_ids,
+             const int64_t* rptr, const int64_t* rows, const int64_t* cptr, const int64_t* cols) {
+  c->N = N;
+  c->ncl = ncl;
+  c->rows_of.assign(ncl, {});
+  c->cols_of.assign(ncl, {});
+  c->active.assign(ncl, 0);
+  c->rix.assign(ncl, {});
+  c->cix.assign(ncl, {});
+  c->row_of_col.assign(N, -1);
+  const int64_t nnz = indptr[N];
+  for (int64_t j = 0; j < N; ++j) {
+    for (int64_t e = indptr[j]; e < indptr[j + 1]; ++e) {
+      if (indices[e] < 0 || indices[e] >= N) throw SpqError(SPQ_ERR_BAD_INPUT, "row index out of range");
+      if (e > indptr[j] && indices[e] <= indices[e - 1])
+        throw SpqError(SPQ_ERR_BAD_INPUT, "CSC row indices must be strictly increasing per column");
+    }
+  }
+  std::vector<int> rown(N, -1), coln(N, -1), rpos(N), cpos(N);
+  for (int t = 0; t < nleaf; ++t) {
+    const int id = leaf_ids[t];
+    if (id < 0 || id >= ncl) throw SpqError(SPQ_ERR_BAD_INPUT, "leaf id out of range");
+    c->rows_of[id].assign(rows + rptr[t], rows + rptr[t + 1]);
+    c->cols_of[id].assign(cols + cptr[t], cols + cptr[t + 1]);
+    c->active[id] = 1;
+    for (size_t i = 0; i < c->rows_of[id].size(); ++i) {
+      rown[c->rows_of[id][i]] = id;
+      rpos[c->rows_of[id][i]] = (int)i;
+    }
+    for (size_t i = 0; i < c->cols_of[id].size(); ++i) {
+      coln[c->cols_of[id][i]] = id;
+      cpos[c->cols_of[id][i]] = (int)i;
+    }
+  }
+  for (int64_t i = 0; i < N; ++i)
+    if (rown[i] < 0 || coln[i] < 0) throw SpqError(SPQ_ERR_BAD_INPUT, "leaf clusters do not cover all rows/columns");
+  // block structure of the entries
+  std::unordered_map<uint64_t, int> bidx;
+  std::vector<std::pair<int, int>> bkeys;
+  std::vector<int> eb(nnz);
+  std::vector<int64_t> eoff(nnz);
+  for (int64_t j = 0; j < N; ++j) {
+    const int cj = coln[j];
+    for (int64_t e = indptr[j]; e < indptr[j + 1]; ++e) {
+      const int64_t r = indices[e];
+      const int ri = rown[r];
+      const uint64_t key = bkey(ri, cj);
+      auto it = bidx.find(key);
+      int b;
+      if (it == bidx.end()) {
+        b = (int)bkeys.size();
+        bidx.emplace(key, b);
+        bkeys.push_back({ri, cj});
+      } else {
+        b = it->second;
+      }
+      eb[e] = b;
+      eoff[e] = rpos[r] + (int64_t)cpos[j] * (int64_t)c->rows_of[ri].size();
+    }
+  }
+  std::vector<double*> bases(bkeys.size());
+  CopyBatch zeros;
+  for (size_t b = 0; b < bkeys.size(); ++b) {
+    const int i = bkeys[b].first, j = bkeys[b].second;
+    const int nr = (int)c->rows_of[i].size(), nc = (int)c->cols_of[j].size();
+    double* mem = new_block_mem(c, nr, nc);
+    zeros.zero(mem, (int64_t)nr * nc);
+    Block& B = put_block(c, i, j, mem, nr, nc);
+    B.clean = false;
+    bases[b] = mem;
+  }
+  zeros.run(c);
+  int64_t* d_indptr = (int64_t*)dalloc(c, (N + 1) * sizeof(int64_t));
+  double* d_data = dalloc(c, std::max<int64_t>(nnz, 1) * sizeof(double));
+  CUDA_TRY(cudaMemcpyAsync(d_indptr, indptr, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaMemcpyAsync(d_data, data, nnz * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  c->equil = equilibrate != 0;
+  c->d_scale = dalloc(c, N * sizeof(double));
+  int* d_zero = (int*)dalloc(c, sizeof(int));
+  const int big = 0x7fffffff;
+  CUDA_TRY(cudaMemcpyAsync(d_zero, &big, sizeof(int), cudaMemcpyHostToDevice, c->st));
+  {
+    Scope s(c, F_COPY);
+    launch_colnorms_scale(d_indptr, nullptr, d_data, N, c->d_scale, d_zero, equilibrate, c->st);
+    int64_t* d_off = (int64_t*)dalloc(c, std::max<int64_t>(nnz, 1) * sizeof(int64_t));
+    int* d_eb = (int*)dalloc(c, std::max<int64_t>(nnz, 1) * sizeof(int));
+    CUDA_TRY(cudaMemcpyAsync(d_off, eoff.data(), nnz * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+    CUDA_TRY(cudaMemcpyAsync(d_eb, eb.data(), nnz * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    double** d_bases = (double**)dalloc(c, std::max<size_t>(bases.size(), 1) * sizeof(double*));
+    CUDA_TRY(cudaMemcpyAsync(d_bases, bases.data(), bases.size() * sizeof(double*), cudaMemcpyHostToDevice, c->st));
+    launch_csc_scatter(d_indptr, nullptr, d_data, nnz, d_off, d_bases, d_eb, c->st);
+    int hz = big;
+    CUDA_TRY(cudaMemcpyAsync(&hz, d_zero, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    dfree(c, d_off);
+    dfree(c, d_eb);
+    dfree(c, d_bases);
+    if (equilibrate && hz != big)
+      throw SpqError(SPQ_ERR_BAD_INPUT, "cannot equilibrate: column " + std::to_string(hz) + " has zero norm");
+  }
+  dfree(c, d_indptr);
+  dfree(c, d_data);
+  dfree(c, d_zero);
+}
+
+// ================================================================ chains
+void ensure_chain_scratch(spq_ctx* c, int nrhs) {
+  size_t maxk = 1, maxp = 1;
+  for (auto& r : c->recs) {
+    maxk = std::max<size_t>(maxk, (size_t)std::max(r.k, r.m));
+    maxp = std::max<size_t>(maxp, (size_t)chain_rsn_chunks(r.n) * std::max(r.k, 1));
+  }
+  const size_t vneed = (size_t)c->N * nrhs;
+  if (vneed > c->vec_cap) {
+    dfree(c, c->d_vec);
+    dfree(c, c->d_vec2);
+    c->d_vec = dalloc(c, vneed * sizeof(double));
+    c->d_vec2 = dalloc(c, vneed * sizeof(double));
+    c->vec_cap = vneed;
+  }
+  if (maxk * nrhs > c->w_cap) {
+    dfree(c, c->d_w);
+    dfree(c, c->d_w2);
+    c->d_w = dalloc(c, maxk * nrhs * sizeof(double));
+    c->d_w2 = dalloc(c, maxk * nrhs * sizeof(double));
+    c->w_cap = maxk * nrhs;
+  }
+  if (maxp * nrhs > c->part_cap) {
+    dfree(c, c->d_part);
+    c->d_part = dalloc(c, maxp * nrhs * sizeof(double));
+    c->part_cap = maxp * nrhs;
+  }
+}
+
+// z (device, N x nrhs) -> P^T Q^T z  ; result left in *out (d_vec or d_vec2)
+double* run_apply_qt(spq_ctx* c, double* z, int nrhs) {
+  Scope s(c, F_CHAIN);
+  for (auto& r : c->recs)
+    chain_wy(r.V, r.T, r.m, r.k, z, r.d_rows, c->N, nrhs, true, c->d_w, c->d_w2, c->st);
+  double* out = (z == c->d_vec) ? c->d_vec2 : c->d_vec;
+  chain_perm(z, c->d_roc, c->N, nrhs, out, c->st);
+  return out;
+}
+
+void run_solve_w(spq_ctx* c, double* y, int nrhs) {
+  Scope s(c, F_CHAIN);
+  for (auto it = c->recs.rbegin(); it != c->recs.rend(); ++it) {
+    Record& r = *it;
+    if (r.kind == REC_SPARSIFY) {
+      chain_wy(r.V, r.T, r.m, r.k, y, r.d_cols_s, c->N, nrhs, false, c->d_w, c->d_w2, c->st);
+    } else if (r.kind == REC_SCALE) {
+      chain_tri(r.R, r.k, nullptr, 0, y, r.d_cols_s, nullptr, c->N, nrhs, 0, c->d_part, c->st);
+    } else {
+      chain_tri(r.R, r.k, r.Rsn, r.n, y, r.d_cols_s, r.d_cols_n, c->N, nrhs, 0, c->d_part, c->st);
+    }
+  }
+  if (c->equil) chain_diag(y, c->d_scale, c->N, nrhs, true, c->st);
+}
+
+void run_apply_w(spq_ctx* c, double* x, int nrhs) {
+  Scope s(c, F_CHAIN);
+  if (c->equil) chain_diag(x, c->d_scale, c->N, nrhs, false, c->st);
+  for (auto& r : c->recs) {
+    if (r.kind == REC_SPARSIFY) {
+      chain_wy(r.V, r.T, r.m, r.k, x, r.d_cols_s, c->N, nrhs, true, c->d_w, c->d_w2, c->st);
+    } else if (r.kind == REC_SCALE) {
+      chain_tri(r.R, r.k, nullptr, 0, x, r.d_cols_s, nullptr, c->N, nrhs, 1, c->d_part, c->st);
+    } else {
+      chain_tri(r.R, r.k, r.Rsn, r.n, x, r.d_cols_s, r.d_cols_n, c->N, nrhs, 1, c->d_part, c->st);
+    }
+  }
+}
+
+template <class F>
+int guarded(spq_ctx* c, F&& fn) {
+  try {
+    fn();
+    return SPQ_OK;
+  } catch (const SpqError& e) {
+    if (c) {
+      c->err_code = e.code;
+      c->err_index = e.index;
+      c->err_value = e.value;
+      c->err_msg = e.what();
+    }
+    return e.code;
+  } catch (const CudaFailure& e) {
+    if (c) {
+      c->err_code = SPQ_ERR_CUDA;
+      c->err_msg = e.what();
+    }
+    return SPQ_ERR_CUDA;
+  } catch (const std::exception& e) {
+    if (c) {
+      c->err_code = SPQ_ERR_INTERNAL;
+      c->err_msg = e.what();
+    }
+    return SPQ_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+int spq_version(void) { return 1; }
+
+int spq_device_info(char* buf, int len) {
+  int dev = 0;
+  cudaDeviceProp p;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&p, dev) != cudaSuccess)
+    return SPQ_ERR_CUDA;
+  snprintf(buf, len, "%s sm_%d%d SMs=%d smem/block=%zu", p.name, p.major, p.minor,
+           p.multiProcessorCount, p.sharedMemPerBlockOptin);
+  return SPQ_OK;
+}
+
+int spq_create(spq_ctx** out, int device) {
+  *out = nullptr;
+  spq_ctx* c = new spq_ctx();
+  int rc = guarded(c, [&] {
+    c->dev = device;
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp p;
+    CUDA_TRY(cudaGetDeviceProperties(&p, device));
+    if (p.major < 10) throw SpqError(SPQ_ERR_CUDA, "sm_100a device required");
+    c->nsm = p.multiProcessorCount;
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    c->ring_cap = 64u << 20;
+    CUDA_TRY(cudaMallocHost(&c->pin, c->ring_cap));
+    CUDA_TRY(cudaMalloc(&c->dring, c->ring_cap));
+  });
+  if (rc != SPQ_OK) {
+    *out = c;  // caller may query the error, then destroy
+    return rc;
+  }
+  *out = c;
+  return SPQ_OK;
+}
+
+void spq_destroy(spq_ctx* c) {
+  if (!c) return;
+  try {
+    if (c->st) cudaStreamSynchronize(c->st);
+    for (auto& kv : c->blk) if (kv.second.p) cudaFreeAsync(kv.second.p, c->st);
+    for (auto& r : c->recs) {
+      if (r.payload) cudaFreeAsync(r.payload, c->st);
+    }
+    for (void* p : {(void*)c->d_scale, (void*)c->d_roc, (void*)c->d_err_idx, (void*)c->d_err_val,
+                    (void*)c->d_vec, (void*)c->d_vec2, (void*)c->d_w, (void*)c->d_w2,
+                    (void*)c->d_part})
+      if (p) cudaFreeAsync(p, c->st);
+    for (int f = 0; f < F_NFAM; ++f)
+      for (auto& e : c->tm.ev[f]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    if (c->st) cudaStreamSynchronize(c->st);
+    if (c->pin) cudaFreeHost(c->pin);
+    if (c->dring) cudaFree(c->dring);
+    if (c->st) cudaStreamDestroy(c->st);
+  } catch (...) {
+  }
+  delete c;
+}
+
+int spq_last_error(spq_ctx* c, int* code, int64_t* index, double* value, char* msg, int msglen) {
+  if (!c) return SPQ_ERR_BAD_INPUT;
+  if (code) *code = c->err_code;
+  if (index) *index = c->err_index;
+  if (value) *value = c->err_value;
+  if (msg && msglen > 0) snprintf(msg, msglen, "%s", c->err_msg.c_str());
+  return SPQ_OK;
+}
+
+int spq_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indices,
+             const double* data, int equilibrate, int n_clusters_total, int n_leaf,
+             const int32_t* leaf_ids, const int64_t* rows_ptr, const int64_t* rows,
+             const int64_t* cols_ptr, const int64_t* cols) {
+  return guarded(c, [&] {
+    do_load(c, N, indptr, indices, data, equilibrate, n_clusters_total, n_leaf, leaf_ids,
+            rows_ptr, rows, cols_ptr, cols);
+  });
+}
+
+int spq_factor(spq_ctx* c, int n, const int32_t* ids) {
+  return guarded(c, [&] { do_factor(c, std::vector<int>(ids, ids + n)); });
+}
+
+int spq_scale(spq_ctx* c, int n, const int32_t* ids, int32_t* out_done) {
+  return guarded(c, [&] { do_scale(c, std::vector<int>(ids, ids + n), out_done); });
+}
+
+int spq_sparsify(spq_ctx* c, int n, const int32_t* ids, double eps, int32_t* out_rank,
+                 int32_t* out_before, double* out_dropped, int32_t* out_done) {
+  return guarded(c, [&] {
+    for (int t = 0; t < n; ++t) {
+      out_rank[t] = -1; out_before[t] = 0; out_dropped[t] = 0.0; out_done[t] = 0;
+    }
+    for (int t = 0; t < n; ++t) {
+      SparsifyOut o = do_sparsify_one(c, ids[t], eps);
+      out_rank[t] = o.rank;
+      out_before[t] = o.before;
+      out_dropped[t] = o.dropped;
+      out_done[t] = o.done;
+    }
+  });
+}
+
+int spq_merge(spq_ctx* c, int n_parents, const int32_t* parent_ids, const int32_t* child_ptr,
+              const int32_t* child_ids) {
+  return guarded(c, [&] { do_merge(c, n_parents, parent_ids, child_ptr, child_ids); });
+}
+
+int spq_finish(spq_ctx* c) {
+  return guarded(c, [&] {
+    for (int64_t j = 0; j < c->N; ++j)
+      if (c->row_of_col[j] < 0) {
+        int64_t miss = 0;
+        for (int64_t t = 0; t < c->N; ++t) miss += c->row_of_col[t] < 0;
+        throw SpqError(SPQ_ERR_BAD_INPUT, std::to_string(miss) + " columns were never factored (inconsistent tree?)");
+      }
+    // one packed device array for row_of_col and every record's index sets
+    std::vector<int> pack(c->row_of_col.begin(), c->row_of_col.end());
+    std::vector<size_t> offs;
+    for (auto& r : c->recs)
+      for (auto* v : {&r.rows, &r.cols_s, &r.cols_n}) {
+        offs.push_back(pack.size());
+        pack.insert(pack.end(), v->begin(), v->end());
+      }
+    int* d = (int*)dalloc(c, std::max<size_t>(pack.size(), 1) * sizeof(int));
+    CUDA_TRY(cudaMemcpyAsync(d, pack.data(), pack.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    c->d_roc = d;
+    c->d_index_pack = d;
+    size_t q = 0;
+    for (auto& r : c->recs) {
+      r.d_rows = d + offs[q++];
+      r.d_cols_s = d + offs[q++];
+      r.d_cols_n = d + offs[q++];
+    }
+    c->finished = true;
+    sync(c);
+  });
+}
+
+int spq_cluster_size(spq_ctx* c, int id, int64_t* nr, int64_t* nc) {
+  return guarded(c, [&] {
+    if (id < 0 || id >= c->ncl) throw SpqError(SPQ_ERR_BAD_INPUT, "cluster id out of range");
+    *nr = (int64_t)c->rows_of[id].size();
+    *nc = (int64_t)c->cols_of[id].size();
+  });
+}
+
+int spq_total_cols(spq_ctx* c, int64_t* out) {
+  return guarded(c, [&] {
+    int64_t t = 0;
+    for (int s = 0; s < c->ncl; ++s) if (c->active[s]) t += (int64_t)c->cols_of[s].size();
+    *out = t;
+  });
+}
+
+int spq_trailing_stats(spq_ctx* c, int64_t* nblocks, int64_t* nnz) {
+  return guarded(c, [&] {
+    *nblocks = (int64_t)c->blk.size();
+    std::vector<const double*> ptrs;
+    std::vector<int64_t> sizes;
+    for (auto& kv : c->blk) {
+      const int64_t n = (int64_t)kv.second.nr * kv.second.nc;
+      if (n > 0) { ptrs.push_back(kv.second.p); sizes.push_back(n); }
+    }
+    unsigned long long* d = (unsigned long long*)dalloc(c, sizeof(unsigned long long));
+    CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->st));
+    if (!ptrs.empty())
+      launch_count_nnz(upload(c, ptrs), upload(c, sizes), (int)ptrs.size(), d, c->st);
+    unsigned long long h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    dfree(c, d);
+    *nnz = (int64_t)h;
+  });
+}
+
+int spq_row_of_col(spq_ctx* c, int64_t* out) {
+  return guarded(c, [&] { std::copy(c->row_of_col.begin(), c->row_of_col.end(), out); });
+}
+
+int spq_payload_scalars(spq_ctx* c, int64_t* out) {
+  return guarded(c, [&] {
+    int64_t t = c->equil ? c->N : 0;
+    for (auto& r : c->recs) t += r.payload_scalars;
+    *out = t;
+  });
+}
+
+int spq_timings(spq_ctx* c, double* out, int n) {
+  return guarded(c, [&] {
+    collect_timings(c);
+    // layout: [ms, flops, launches] per family
+    for (int f = 0; f < F_NFAM && 3 * f + 2 < n; ++f) {
+      out[3 * f] = c->tm.ms[f];
+      out[3 * f + 1] = c->tm.flops[f];
+      out[3 * f + 2] = (double)c->tm.launches[f];
+    }
+  });
+}
+
+int spq_reset_timings(spq_ctx* c) {
+  return guarded(c, [&] {
+    collect_timings(c);
+    for (int f = 0; f < F_NFAM; ++f) {
+      c->tm.ms[f] = 0; c->tm.flops[f] = 0; c->tm.launches[f] = 0; c->tm.bytes[f] = 0;
+    }
+  });
+}
+
+int spq_num_records(spq_ctx* c) { return c ? (int)c->recs.size() : 0; }
+
+int spq_record_info(spq_ctx* c, int idx, int64_t* info) {
+  return guarded(c, [&] {
+    if (idx < 0 || idx >= (int)c->recs.size()) throw SpqError(SPQ_ERR_BAD_INPUT, "record index");
+    Record& r = c->recs[idx];
+    info[0] = r.kind; info[1] = r.m; info[2] = r.k; info[3] = r.n; info[4] = r.rank;
+  });
+}
+
+int spq_record_get(spq_ctx* c, int idx, int which, void* out) {
+  return guarded(c, [&] {
+    if (idx < 0 || idx >= (int)c->recs.size()) throw SpqError(SPQ_ERR_BAD_INPUT, "record index");
+    Record& r = c->recs[idx];
+    auto cp = [&](const double* d, size_t n) {
+      if (n) CUDA_TRY(cudaMemcpyAsync(out, d, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+    };
+    switch (which) {
+      case 0: std::copy(r.rows.begin(), r.rows.end(), (int64_t*)out); break;
+      case 1: std::copy(r.cols_s.begin(), r.cols_s.end(), (int64_t*)out); break;
+      case 2: std::copy(r.cols_n.begin(), r.cols_n.end(), (int64_t*)out); break;
+      case 3: cp(r.V, (size_t)r.m * r.k); break;
+      case 4: cp(r.tau, r.k); break;
+      case 5: cp(r.T, (size_t)r.k * r.k); break;
+      case 6: if (r.R) cp(r.R, (size_t)r.k * r.k); break;
+      case 7: if (r.Rsn) cp(r.Rsn, (size_t)r.k * r.n); break;
+      default: throw SpqError(SPQ_ERR_BAD_INPUT, "record field");
+    }
+  });
+}
+
+static int chain_host(spq_ctx* c, const double* in, double* out, int nrhs, int which) {
+  return guarded(c, [&] {
+    if (!c->finished) throw SpqError(SPQ_ERR_BAD_INPUT, "factorization not finished");
+    ensure_chain_scratch(c, nrhs);
+    const size_t bytes = (size_t)c->N * nrhs * sizeof(double);
+    CUDA_TRY(cudaMemcpyAsync(c->d_vec, in, bytes, cudaMemcpyHostToDevice, c->st));
+    double* res = c->d_vec;
+    if (which == 0) res = run_apply_qt(c, c->d_vec, nrhs);
+    else if (which == 1) run_solve_w(c, c->d_vec, nrhs);
+    else run_apply_w(c, c->d_vec, nrhs);
+    CUDA_TRY(cudaMemcpyAsync(out, res, bytes, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+  });
+}
+
+int spq_apply_qt_host(spq_ctx* c, const double* in, double* out, int nrhs) { return chain_host(c, in, out, nrhs, 0); }
+int spq_solve_w_host(spq_ctx* c, const double* in, double* out, int nrhs) { return chain_host(c, in, out, nrhs, 1); }
+int spq_apply_w_host(spq_ctx* c, const double* in, double* out, int nrhs) { return chain_host(c, in, out, nrhs, 2); }
+
+int spq_apply_qt_dev(spq_ctx* c, double* d, int nrhs) {
+  return guarded(c, [&] {
+    ensure_chain_scratch(c, nrhs);
+    const size_t bytes = (size_t)c->N * nrhs * sizeof(double);
+    CUDA_TRY(cudaMemcpyAsync(c->d_vec, d, bytes, cudaMemcpyDeviceToDevice, c->st));
+    double* res = run_apply_qt(c, c->d_vec, nrhs);
+    CUDA_TRY(cudaMemcpyAsync(d, res, bytes, cudaMemcpyDeviceToDevice, c->st));
+  });
+}
+
+int spq_solve_w_dev(spq_ctx* c, double* d, int nrhs) {
+  return guarded(c, [&] {
+    ensure_chain_scratch(c, nrhs);
+    run_solve_w(c, d, nrhs);
+  });
+}
+
+int spq_synchronize(spq_ctx* c) {
+  return guarded(c, [&] { sync(c); });
+}
+
+// ------------------------------------------------------ kernel plugin API
+// host row-major (numpy) <-> device column-major via transposing copies
+static double* to_dev_colmajor(spq_ctx* c, const double* h, int64_t m, int64_t k, CopyBatch& cb) {
+  double* raw = dalloc(c, (size_t)std::max<int64_t>(m * k, 1) * sizeof(double));
+  double* cm = dalloc(c, (size_t)std::max<int64_t>(m * k, 1) * sizeof(double));
+  if (m * k) CUDA_TRY(cudaMemcpyAsync(raw, h, m * k * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CopyTask t{};
+  t.src = raw; t.dst = cm; t.nr = (int)k; t.nc = (int)m; t.lds = (int)std::max<int64_t>(k, 1);
+  t.ldd = (int)std::max<int64_t>(m, 1); t.trans = 1;
+  cb.add(t);
+  c->deferred.push_back(raw);
+  return cm;
+}
+
+static void to_host_rowmajor(spq_ctx* c, const double* d, int64_t m, int64_t k, int64_t ld,
+                             double* h) {
+  if (m * k == 0) return;
+  double* raw = dalloc(c, (size_t)(m * k) * sizeof(double));
+  CopyBatch cb;
+  CopyTask t{};
+  t.src = d; t.dst = raw; t.nr = (int)m; t.nc = (int)k; t.lds = (int)ld; t.ldd = (int)k; t.trans = 1;
+  cb.add(t);
+  cb.run(c);
+  CUDA_TRY(cudaMemcpyAsync(h, raw, m * k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  dfree(c, raw);
+}
+
+int spq_qr_house(spq_ctx* c, int64_t m, int64_t k, const double* B, double* V, double* tau,
+                 double* T, double* R) {
+  return guarded(c, [&] {
+    if (m < k) throw SpqError(SPQ_ERR_BAD_INPUT, "qr_house needs m >= k");
+    if (k == 0) return;
+    CopyBatch cb;
+    double* P = to_dev_colmajor(c, B, m, k, cb);
+    double* aux = dalloc(c, (size_t)(k + 2 * k * k) * sizeof(double));
+    cb.zero(aux, k + 2 * k * k);
+    cb.run(c);
+    double* dtau = aux;
+    double* dT = aux + k;
+    double* dR = dT + k * k;
+    qr_batch(c, {QrProb{P, (int)m, (int)k, dR, dtau, dT}});
+    to_host_rowmajor(c, P, m, k, m, V);
+    to_host_rowmajor(c, dT, k, k, k, T);
+    to_host_rowmajor(c, dR, k, k, k, R);
+    CUDA_TRY(cudaMemcpyAsync(tau, dtau, k * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    dfree(c, P);
+    dfree(c, aux);
+    flush_deferred(c);
+  });
+}
+
+int spq_apply_panel(spq_ctx* c, int64_t m, int64_t k, int64_t n, const double* V, const double* T,
+                    double* C, int transpose) {
+  return guarded(c, [&] {
+    if (k == 0 || n == 0 || m == 0) return;
+    CopyBatch cb;
+    double* dV = to_dev_colmajor(c, V, m, k, cb);
+    double* dT = to_dev_colmajor(c, T, k, k, cb);
+    double* dC = to_dev_colmajor(c, C, m, n, cb);
+    cb.run(c);
+    wy_batch(c, {WyProb{dV, dT, (int)m, (int)k, dC, (int)m, (int)n}}, transpose != 0);
+    to_host_rowmajor(c, dC, m, n, m, C);
+    dfree(c, dV); dfree(c, dT); dfree(c, dC);
+    flush_deferred(c);
+  });
+}
+
+int spq_rrqr(spq_ctx* c, int64_t m, int64_t k, const double* M, double eps, int64_t min_rank,
+             double* V, double* tau, double* Tred, int64_t* perm, int64_t* rank) {
+  return guarded(c, [&] {
+    const int kmax = (int)std::min(m, k);
+    CopyBatch cb;
+    double* W = to_dev_colmajor(c, M, m, k, cb);
+    const int G = cpqr_grid((int)std::max<int64_t>(k, 1), c->nsm);
+    const size_t vsz = (size_t)std::max<int64_t>(m, 1) * std::max(kmax, 1);
+    double* aux = dalloc(c, (vsz + 2 * (size_t)std::max(kmax, 1) + 2 * G + 2) * sizeof(double));
+    double* dV = aux;
+    double* dtau = dV + vsz;
+    double* dbeta = dtau + std::max(kmax, 1);
+    double* slots = dbeta + std::max(kmax, 1);
+    double* deps = slots + 2 * G;
+    cb.zero(dV, vsz);
+    cb.run(c);
+    int* ints = (int*)dalloc(c, (2 * G + 2 + std::max<int64_t>(k, 1)) * sizeof(int));
+    int* slotp = ints;
+    int* dnk = ints + 2 * G;
+    int* drank = dnk + 1;
+    int* dperm = drank + 1;
+    int hk[1] = {(int)k};
+    CUDA_TRY(cudaMemcpyAsync(dnk, hk, sizeof(int), cudaMemcpyHostToDevice, c->st));
+    CUDA_TRY(cudaMemcpyAsync(deps, &eps, sizeof(double), cudaMemcpyHostToDevice, c->st));
+    sync(c);
+    CpqrArgs a{};
+    a.W = W; a.m = (int)m; a.ncols_cap = (int)std::max<int64_t>(k, 1); a.nk = dnk; a.eps = deps;
+    a.min_rank = (int)min_rank; a.V = dV; a.tau = dtau; a.beta = dbeta; a.rank = drank;
+    a.perm = dperm; a.slot_val = slots; a.slot_pos = slotp; a.finalize = 1;
+    if (m > 0 && k > 0) {
+      launch_cpqr(a, G, c->st);
+    } else {
+      int z = 0;
+      CUDA_TRY(cudaMemcpyAsync(drank, &z, sizeof(int), cudaMemcpyHostToDevice, c->st));
+    }
+    int hr = 0;
+    CUDA_TRY(cudaMemcpyAsync(&hr, drank, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    *rank = hr;
+    std::vector<int> hp(std::max<int64_t>(k, 1));
+    if (k) CUDA_TRY(cudaMemcpyAsync(hp.data(), dperm, k * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    for (int64_t j = 0; j < k; ++j) perm[j] = hp[j];
+    // Tred in pivoted order: column l = W[:, perm[l]]
+    if (m * k) {
+      double* Tp = dalloc(c, (size_t)(m * k) * sizeof(double));
+      CopyBatch g;
+      for (int64_t l = 0; l < k; ++l) {
+        CopyTask t{};
+        t.src = W + (int64_t)hp[l] * m; t.dst = Tp + l * m; t.nr = (int)m; t.nc = 1;
+        t.lds = (int)m; t.ldd = (int)m;
+        g.add(t);
+      }
+      g.run(c);
+      to_host_rowmajor(c, Tp, m, k, m, Tred);
+      dfree(c, Tp);
+    }
+    if (hr > 0) {
+      to_host_rowmajor(c, dV, m, hr, m, V);
+      CUDA_TRY(cudaMemcpyAsync(tau, dtau, hr * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }
+    sync(c);
+    dfree(c, W); dfree(c, aux); dfree(c, ints);
+    flush_deferred(c);
+  });
+}
+
+int spq_tri_solve(spq_ctx* c, int64_t k, int64_t n, const double* R, const double* Cm, int side,
+                  double* X) {
+  return guarded(c, [&] {
+    if (k == 0) return;
+    // pivot rule (kernels/__init__.py:211-223) evaluated on the device
+    CopyBatch cb;
+    double* dR = to_dev_colmajor(c, R, k, k, cb);
+    cb.run(c);
+    PivotSet ps;
+    ps.jobs.push_back(PivotJob{dR, (int)k, (int)k, 0});
+    ps.ctx.push_back("");
+    pivot_launch(c, ps);
+    pivot_raise(c, ps);
+    if (n == 0) { dfree(c, dR); flush_deferred(c); return; }
+    if (side == 1) {
+      // X R = C with C (n x k) row-major
+      CopyBatch cb2;
+      double* dC = to_dev_colmajor(c, Cm, n, k, cb2);
+      cb2.run(c);
+      std::vector<TrsmJob> tj{TrsmJob{dR, dC, (int)n, (int)k, (int)k, (int)n, 0}};
+      launch_trsm_right(upload(c, tj), 1, trsm_tiles((int)n), c->st);
+      to_host_rowmajor(c, dC, n, k, n, X);
+      dfree(c, dC);
+    } else {
+      // R X = C  <=>  X^T R^T = C^T : solve column by column with the chain kernel
+      CopyBatch cb2;
+      double* dC = to_dev_colmajor(c, Cm, k, n, cb2);
+      cb2.run(c);
+      std::vector<int64_t> ids(k);
+      std::iota(ids.begin(), ids.end(), 0);
+      int* dids = upload_idx32(c, ids);
+      chain_tri(dR, (int)k, nullptr, 0, dC, dids, nullptr, k, (int)n, 0, nullptr, c->st);
+      to_host_rowmajor(c, dC, k, n, k, X);
+      dfree(c, dC);
+    }
+    dfree(c, dR);
+    flush_deferred(c);
+  });
+}
+
+int spq_build_t(spq_ctx* c, int64_t m, int64_t k, const double* V, const double* tau,
+                double* T) {
+  return guarded(c, [&] {
+    if (k == 0) return;
+    CopyBatch cb;
+    double* dV = to_dev_colmajor(c, V, m, k, cb);
+    double* aux = dalloc(c, (size_t)(k + 2 * k * k) * sizeof(double));
+    cb.run(c);
+    double* dtau = aux;
+    double* G = aux + k;
+    double* dT = G + k * k;
+    CUDA_TRY(cudaMemcpyAsync(dtau, tau, k * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    GemmBatch gg;
+    gg.add(dV, (int)m, dV, (int)m, G, (int)k, (int)k, (int)k, (int)m, 1.0, 0.0);
+    gg.run(c, true, 0);
+    std::vector<LarftJob> lj{LarftJob{G, dtau, dT, (int)k, (int)k, (int)k, 0}};
+    launch_larft(upload(c, lj), 1, larft_tiles((int)k), c->st);
+    to_host_rowmajor(c, dT, k, k, k, T);
+    dfree(c, dV);
+    dfree(c, aux);
+    flush_deferred(c);
+  });
+}
+
+int spq_bench_batched_qr(spq_ctx*, int, const int64_t*, const int64_t*, const int64_t*, double*,
+                         const int64_t*, double*, double*, const int64_t*, double*,
+                         const int64_t*, float*, float*) {
+  return SPQ_ERR_INTERNAL;  // implemented in a later revision
+}
+
+}  // extern "C"

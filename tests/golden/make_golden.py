@@ -1,0 +1,198 @@
+"""Generate the golden vectors from the REAL reference package.
+
+Run in the build container only (it imports /root/reference, which does not
+exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src:/root/repo NUMBA_CACHE_DIR=/tmp/nbc \
+        python tests/golden/make_golden.py [--big]
+
+Outputs (committed, small):
+  kernels.npz   known-answer cases for qr_house / rrqr_threshold / tri_solve
+                (reference `kernels/__init__.py:147-233`, numba backend)
+  factor_<case>.npz  per-case factorization results: per-level stats, the
+                per-interface rank sequence, row_of_col, diag(R_ss) of every
+                elimination record, full R_ss of a few records, GMRES history;
+                plus the numpy-backend R_ss divergence envelope per level (F3)
+  trees.json    tree digests of the reference's partition_geometric per config
+--big adds the full C3 (256^2) and C4 (32^3) runs (minutes of CPU).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import nestqr.kernels as K                                    # noqa: E402
+from nestqr.factor import (BlockHouseholder, InterfaceScaling,  # noqa: E402
+                           Sparsifier, factorize)
+from nestqr.ordering import partition_geometric as ref_partition  # noqa: E402
+from nestqr.solve import gmres                                 # noqa: E402
+from nestqr.sparse import SparseMat                            # noqa: E402
+
+from paper_2010_06807_b200.ordering import tree_digest         # noqa: E402
+from paper_2010_06807_b200.problems import make_config         # noqa: E402
+
+CASES = {
+    # name: (config, n override)
+    "C1_n24": ("C1", 24),
+    "C1": ("C1", None),
+    "C3_n48": ("C3", 48),
+    "C4_n12": ("C4", 12),
+}
+BIG = {"C3": ("C3", None), "C4": ("C4", None)}
+
+
+def kernel_cases():
+    rng = np.random.default_rng(2024)
+    out = {}
+    shapes = [(1, 1), (2, 1), (7, 7), (20, 5), (64, 40), (130, 33), (200, 96), (37, 36)]
+    for t, (m, k) in enumerate(shapes):
+        B = rng.standard_normal((m, k))
+        if t == 3:
+            B[:, 2] = 0.0                       # zero column -> tau = 0
+        if t == 4:
+            B[5:, 7] = 0.0
+            B[:5, 7] = -1.0                     # sigma != 0, alpha < 0
+        if t == 5:
+            B[1:, 0] = 0.0
+            B[0, 0] = -3.0                      # sigma == 0, alpha < 0 -> tau = 2
+        panel, R = K.qr_house(B)
+        C = rng.standard_normal((m, 3))
+        out[f"qr{t}_B"] = B
+        out[f"qr{t}_V"] = panel.V
+        out[f"qr{t}_tau"] = panel.tau
+        out[f"qr{t}_T"] = panel.T
+        out[f"qr{t}_R"] = R
+        out[f"qr{t}_C"] = C
+        out[f"qr{t}_HtC"] = K.apply_panel_left(panel, C, transpose=True)
+    rr = []
+    for t in range(8):
+        m, k = [(12, 9), (30, 80), (64, 192), (10, 14), (50, 50), (8, 8), (40, 300), (5, 3)][t]
+        if t in (2, 6):
+            U, _ = np.linalg.qr(rng.standard_normal((m, m)))
+            W, _ = np.linalg.qr(rng.standard_normal((k, m)))
+            M = U @ np.diag(10.0 ** (-np.arange(m) / 8.0)) @ W.T
+        elif t == 5:
+            M = np.outer(rng.standard_normal(m), rng.standard_normal(k))
+        else:
+            M = rng.standard_normal((m, k)) @ np.diag(10.0 ** -np.linspace(0, 9, k))
+        for e, eps in enumerate([0.0, 1e-8, 1e-4, 1e-2, 0.5]):
+            res = K.rrqr_threshold(M, eps)
+            key = f"rr{t}_{e}"
+            out[f"rr{t}_M"] = M
+            out[key + "_eps"] = np.float64(eps)
+            out[key + "_rank"] = np.int64(res.rank)
+            out[key + "_perm"] = res.perm
+            out[key + "_R"] = res.R
+            out[key + "_V"] = res.panel.V
+            out[key + "_tau"] = res.panel.tau
+            rr.append(key)
+    for t, k in enumerate([1, 5, 33, 70]):
+        Rm = np.triu(rng.standard_normal((k, k))) + 4 * np.eye(k)
+        C = rng.standard_normal((k, 4))
+        Cr = rng.standard_normal((9, k))
+        out[f"ts{t}_R"] = Rm
+        out[f"ts{t}_C"] = C
+        out[f"ts{t}_Cr"] = Cr
+        out[f"ts{t}_left"] = K.tri_solve(Rm, C, side="left")
+        out[f"ts{t}_right"] = K.tri_solve(Rm, Cr, side="right")
+    out["n_qr"] = np.int64(len(shapes))
+    out["rr_keys"] = np.array(rr)
+    out["n_ts"] = np.int64(4)
+    np.savez_compressed(os.path.join(HERE, "kernels.npz"), **out)
+
+
+class RankLog:
+    """observer: record (level, interface id, cols before, cols after)."""
+
+    def __init__(self):
+        self.rows = []
+        self.lev = None
+
+    def on_sparsify(self, state, p, when):
+        if when == "before":
+            self._b = len(state.cols_of[p])
+        else:
+            self.rows.append((p, self._b, len(state.cols_of[p])))
+
+
+def factor_case(name, cfg, n):
+    A0, dims, L, eps, b, tol = make_config(cfg, n=n)
+    A = SparseMat(A0.nrows, A0.ncols, A0.indptr, A0.indices, A0.data)
+    tree = ref_partition(dims, L)
+    K.set_backend("numba")
+    log = RankLog()
+    t0 = time.perf_counter()
+    F = factorize(A, tree, eps=eps, observer=log)
+    t_fac = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    x, rep = gmres(A, b, F, tol=tol)
+    t_sol = time.perf_counter() - t0
+    out = {"dims": np.array(dims), "L": np.int64(L), "eps": np.float64(eps),
+           "tol": np.float64(tol), "t_factor": np.float64(t_fac),
+           "t_gmres": np.float64(t_sol)}
+    keys = [k for k in F.stats[0] if not k.startswith("t_")]
+    out["stat_keys"] = np.array(keys)
+    out["stats"] = np.array([[float(s[k]) for k in keys] for s in F.stats])
+    out["sparsify_log"] = np.array(log.rows, dtype=np.int64).reshape(-1, 3)
+    out["row_of_col"] = F.row_of_col
+    out["payload"] = np.int64(F.payload_scalars)
+    bh = [r for r in F.q_chain if isinstance(r, BlockHouseholder)]
+    out["rss_diag"] = np.concatenate([np.diag(r.R_ss) for r in bh])
+    out["rss_k"] = np.array([r.R_ss.shape[0] for r in bh])
+    pick = sorted(i for i in set([0, 1, len(bh) // 2, len(bh) - 2, len(bh) - 1])
+                  if bh[i].R_ss.shape[0] <= 256)
+    out["rss_pick"] = np.array(pick)
+    for i in pick:
+        out[f"rss_{i}"] = bh[i].R_ss
+        out[f"rsn_{i}_shape"] = np.array(bh[i].R_sn.shape)
+        out[f"rsn_{i}_fro"] = np.float64(np.linalg.norm(bh[i].R_sn))
+    out["chain_kinds"] = np.array([type(r).__name__ for r in F.q_chain[:-1]])
+    out["gmres_iters"] = np.int64(rep.iterations)
+    out["gmres_hist"] = rep.residuals
+    out["gmres_converged"] = np.bool_(rep.converged)
+    out["x_norm"] = np.float64(np.linalg.norm(x))
+    # rounding envelope (F3): numpy backend on the same inputs
+    if A.ncols <= 8192:
+        K.set_backend("numpy")
+        F2 = factorize(A, tree, eps=eps)
+        K.set_backend("numba")
+        bh2 = [r for r in F2.q_chain if isinstance(r, BlockHouseholder)]
+        env = [float(np.abs(a.R_ss - c.R_ss).max() / max(np.abs(a.R_ss).max(), 1e-300))
+               if a.R_ss.shape == c.R_ss.shape else np.inf for a, c in zip(bh, bh2)]
+        out["rss_envelope"] = np.array(env)
+    np.savez_compressed(os.path.join(HERE, f"factor_{name}.npz"), **out)
+    print(f"{name}: N={A.ncols} L={L} factor {t_fac:.2f}s gmres {t_sol:.2f}s "
+          f"its={rep.iterations} res={rep.final_residual:.3e}", flush=True)
+
+
+def trees():
+    dig = {}
+    for cfg, dims, L in [("C1", (64, 64), 6), ("C3", (256, 256), 10),
+                         ("C4", (32, 32, 32), 9), ("C5", (64, 64, 64), 11),
+                         ("C1_n24", (24, 24), 4), ("C3_n48", (48, 48), 6),
+                         ("C4_n12", (12, 12, 12), 5), ("odd", (20, 37), 4),
+                         ("odd3", (12, 9, 17), 4)]:
+        dig[cfg] = {"dims": list(dims), "L": L, "sha256": tree_digest(ref_partition(dims, L))}
+    with open(os.path.join(HERE, "trees.json"), "w") as fh:
+        json.dump(dig, fh, indent=1)
+
+
+if __name__ == "__main__":
+    trees()
+    kernel_cases()
+    cases = dict(CASES)
+    if "--big" in sys.argv:
+        cases.update(BIG)
+    only = [a for a in sys.argv[1:] if not a.startswith("--")]
+    for name, (cfg, n) in cases.items():
+        if only and name not in only:
+            continue
+        factor_case(name, cfg, n)

@@ -1,0 +1,116 @@
+"""GPU parity of the full factorization path against the reference's golden
+vectors (tests/golden, generated from the live reference) and against the
+CPU oracle on the same seeded inputs."""
+
+import numpy as np
+import pytest
+
+from parity import compare_structure, load, rss_bar, rss_diag_errors
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(name, cfg, n):
+    from paper_2010_06807_b200.factor import BlockHouseholder, factorize
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    from paper_2010_06807_b200.solve import gmres
+    A, dims, L, eps, b, tol = make_config(cfg, n=n)
+    tree = partition_geometric(dims, L)
+    F = factorize(A, tree, eps=eps)
+    x, rep = gmres(A, b, F, tol=tol)
+    return A, b, F, x, rep
+
+
+@pytest.mark.parametrize("name,cfg,n", [("C1_n24", "C1", 24), ("C3_n48", "C3", 48),
+                                        ("C4_n12", "C4", 12), ("C1", "C1", None)])
+def test_factor_matches_reference(name, cfg, n):
+    from paper_2010_06807_b200.factor import BlockHouseholder
+    g = load(name)
+    A, b, F, x, rep = _run(name, cfg, n)
+    problems = compare_structure(F.stats, F.sparsify_log, F.row_of_col, g)
+    assert not problems, "\n".join(problems)
+    bh = [r for r in F.q_chain if isinstance(r, BlockHouseholder)]
+    assert len(bh) == len(g["rss_k"])
+    errs = rss_diag_errors([r.R_ss for r in bh], g)
+    bar = rss_bar(g, len(errs))
+    assert (errs <= bar).all(), f"R_ss diag beyond envelope at {np.nonzero(errs > bar)[0][:10]}: {errs[errs > bar][:10]}"
+    for i in g["rss_pick"]:
+        Rref = g[f"rss_{i}"]
+        R = bh[i].R_ss
+        assert np.abs(R - Rref).max() <= max(bar[i], 1e-10) * np.abs(Rref).max()
+        assert tuple(bh[i].R_sn.shape) == tuple(g[f"rsn_{i}_shape"])
+    assert F.payload_scalars == int(g["payload"])
+    gi, gres = int(g["gmres_iters"]), float(g["gmres_hist"][-1])
+    assert abs(rep.iterations - gi) <= 1
+    assert rep.final_residual <= 10 * max(gres, 1e-16) and rep.converged
+
+
+def test_chains_match_oracle():
+    """apply_qt / solve_w / apply_w on the device equal the CPU oracle's
+    chains on the same factorization input (C3 shape at 40^2)."""
+    from oracle import spaqr_oracle as O
+    from paper_2010_06807_b200.factor import factorize
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    A, dims, L, eps, b, tol = make_config("C3", n=40)
+    tree = partition_geometric(dims, L)
+    F = factorize(A, tree, eps=eps)
+    Fo = O.factorize(A, tree, eps=eps)
+    rng = np.random.default_rng(5)
+    for nrhs in (1, 3):
+        v = rng.standard_normal((A.ncols, nrhs)) if nrhs > 1 else rng.standard_normal(A.ncols)
+        for fn in ("apply_qt", "solve_w", "apply_w"):
+            a = getattr(F, fn)(v)
+            o = getattr(Fo, fn)(v)
+            assert np.abs(a - o).max() <= 1e-8 * max(np.abs(o).max(), 1.0), fn
+
+
+def test_exact_mode_identity():
+    """eps = 0 / no sparsification: P^T Q^T A W^{-1} = I (reference
+    test_factor.py:395-402) and W^T W = A^T A for the equilibrated A."""
+    from paper_2010_06807_b200.factor import factorize
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    for sparsify in (False, True):
+        A, dims, L, eps, b, tol = make_config("C1", n=16)
+        tree = partition_geometric(dims, 3)
+        F = factorize(A, tree, eps=0.0, sparsify=sparsify)
+        M = F.materialize_preconditioned()
+        assert np.linalg.norm(M - np.eye(A.ncols)) <= 1e-11
+        W = F.materialize_w()
+        D = A.to_dense()
+        assert np.linalg.norm(W.T @ W - D.T @ D) <= 1e-10 * np.linalg.norm(D.T @ D)
+        Y = np.random.default_rng(0).standard_normal(A.ncols)
+        assert np.allclose(F.apply_w(F.solve_w(Y)), Y, atol=1e-11)
+
+
+def test_singular_pivot_raises():
+    from paper_2010_06807_b200.errors import SingularPivotError
+    from paper_2010_06807_b200.factor import factorize
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.sparse import SparseMat
+    n = 8
+    D = np.eye(n * n)
+    D[3, 3] = 0.0          # empty column -> zero pivot in its leaf block
+    A = SparseMat.from_dense(D)
+    tree = partition_geometric((n, n), 2)
+    with pytest.raises(SingularPivotError):
+        factorize(A, tree, eps=0.0, sparsify=False, equilibrate=False)
+
+
+@pytest.mark.slow
+def test_c3_full_matches_reference():
+    """BASELINE metric config (256^2, L=10, eps=1e-3) against the reference's
+    golden run: identical per-level ranks/statistics, GMRES its +-1."""
+    from paper_2010_06807_b200.factor import BlockHouseholder
+    g = load("C3")
+    A, b, F, x, rep = _run("C3", "C3", None)
+    problems = compare_structure(F.stats, F.sparsify_log, F.row_of_col, g)
+    assert not problems, "\n".join(problems[:20])
+    bh = [r for r in F.q_chain if isinstance(r, BlockHouseholder)]
+    errs = rss_diag_errors([r.R_ss for r in bh], g)
+    bar = rss_bar(g, len(errs))
+    assert (errs <= bar).all(), f"{np.nonzero(errs > bar)[0][:10]} {errs[errs > bar][:10]}"
+    assert abs(rep.iterations - int(g["gmres_iters"])) <= 1
+    assert rep.final_residual <= 10 * float(g["gmres_hist"][-1])

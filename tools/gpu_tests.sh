@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q -k "not slow" --timeout 240 -p no:cacheprovider > gpurun_out/t1.log 2>&1
+echo "exit=$?" >> gpurun_out/t1.log
