@@ -1,0 +1,317 @@
+"""Benchmark of the B200 spaQR hot path (BASELINE.json metric, config C3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step = one full spaQR factorization (levels L..1: interior elimination,
+interface scaling, threshold-CPQR sparsification, merges) of BASELINE config
+3: 2D variable-coefficient upwind convection-diffusion on 256^2 (N=65,536),
+L=10, eps=1e-3 (synthetic, seeded: kappa log-uniform [0.1,10], beta U(-50,50)^2).
+
+* value: factorizations/s over the timed steps, device-timed with CUDA events
+  on the library's own stream from the end of the (tiny) CSC upload to the
+  end of the factorization (inputs resident in HBM), max over ranks.
+* e2e: the same metric through the public API `factorize(A_host, tree)` —
+  host CSC in, H2D upload and D2H of the result bookkeeping inside the region.
+* Multi-GPU: the factorization does not shard under the reference's exact
+  processing order, so N GPUs run N independent replicas
+  ("scaling": "weak"); no data-path collective.
+* roofline: the dominant device kernel family (by device time) against the
+  measured fp64 DGEMM peak (cuBLAS via torch, this box) or the measured HBM
+  copy bandwidth (MEASURED_PEAKS.json).
+* cpu_baseline / --impl reference: the CPU oracle (numpy restatement of the
+  reference, oracle/spaqr_oracle.py) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "spaQR factor time + batched-QR fp64 GFLOP/s (% roofline), 2D N=256^2, 1 B200"
+UNIT = "factorizations/s"
+WORKLOAD = "C3: 2D var-coef upwind conv-diff 256^2 (N=65536), L=10, eps=1e-3, scaled sparsification"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup(n):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if os.environ.get("SPQ_BENCH_BACKEND") != "gloo" else "gloo")
+        pg = dist
+    return rank, world, local, pg
+
+
+def problem(cfg):
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    A, dims, L, eps, b, tol = make_config(cfg)
+    tree = partition_geometric(dims, L)
+    return A, tree, eps, b, tol
+
+
+def csc_bytes(A, tree):
+    n = 8 * (A.indptr.size + A.indices.size + A.data.size)
+    for c in tree.leaf_clusters():
+        n += 8 * (len(c.cols) + len(c.rows if c.rows is not None else c.cols))
+    return int(n)
+
+
+class Clocks:
+    """nvidia-smi sampler over the timed region (rank 0)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.p is None:
+            return
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 6:
+                self.rows.append(f)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def fp64_peak_tflops():
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def reduce_max(values, dist, device="cuda"):
+    """Per-rank timings -> elementwise max over ranks (every rank gets it)."""
+    if dist is None:
+        return [float(v) for v in values]
+    import torch
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t]
+
+
+def flush_l2(buf):
+    buf.add_(1.0)
+
+
+def cpu_baseline(A, tree, eps, budget_s=30.0):
+    """One full C3 factorization by the CPU oracle (numpy + threaded BLAS)."""
+    from oracle import spaqr_oracle as O
+    t0 = time.perf_counter()
+    O.factorize(A, tree, eps=eps)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"1 full {WORKLOAD.split(':')[0]} factorization by oracle/spaqr_oracle.py "
+                      f"({dt:.1f} s, numpy/OpenBLAS threads={os.cpu_count()})",
+            "seconds_per_factorization": dt}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    A, tree, eps, b, tol = problem(args.config)
+    from oracle import spaqr_oracle as O
+    for _ in range(min(args.warmup, 1)):
+        t0 = time.perf_counter()
+        O.factorize(A, tree, eps=eps)
+        step = time.perf_counter() - t0
+    times = []
+    budget = 200.0
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        O.factorize(A, tree, eps=eps)
+        times.append(time.perf_counter() - t0)
+        if sum(times) > budget:
+            break
+    T = sum(times)
+    v = len(times) / T
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "steps_run": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOAD, "parallelism": "host cores"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{len(times)} full factorizations by the CPU oracle"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+def main():
+    args = parse()
+    rank, world, local, dist = dist_setup(args.gpus)
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2010_06807_b200 import factor as FZ
+    A, tree, eps, b, tol = problem(args.config)
+    peak64 = fp64_peak_tflops()
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    l2buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+
+    for _ in range(max(args.warmup, 0)):
+        FZ.factorize(A, tree, eps=eps, device=local)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    dev_ms, e2e_ms = [], []
+    agg = {}
+    launches = 0
+    barrier()
+    clocks = Clocks(local)
+    with clocks:
+        for _ in range(args.steps):
+            flush_l2(l2buf)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            F = FZ.factorize(A, tree, eps=eps, device=local, _marks=True)
+            e1.record()
+            torch.cuda.synchronize()
+            e2e_ms.append(e0.elapsed_time(e1))
+            dev_ms.append(F.device_ms)
+            tm = F.device_timings()
+            host = tm.pop("host")
+            launches += int(host.get("kernels", 0))
+            for fam, v in tm.items():
+                a = agg.setdefault(fam, {"ms": 0.0, "flops": 0.0, "launches": 0, "bytes": 0.0})
+                for key in ("ms", "flops", "launches", "bytes"):
+                    a[key] += v.get(key, 0)
+            del F
+    barrier()
+    T = float(np.sum(dev_ms))
+    Te = float(np.sum(e2e_ms))
+    T, Te = reduce_max([T, Te], dist)
+    if rank != 0:
+        return
+    units = world * args.steps
+    value = units / (T / 1e3)
+    e2e = units / (Te / 1e3)
+    # roofline of the dominant family
+    fams = {k: v for k, v in agg.items() if v["ms"] > 0}
+    dom = max(fams, key=lambda k: fams[k]["ms"]) if fams else None
+    roof = None
+    if dom is not None:
+        d = fams[dom]
+        if dom in ("copy", "flags", "chain"):
+            ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "traffic": None, "kernel_family": dom,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        else:
+            ach = d["flops"] / (d["ms"] * 1e-3) / 1e12
+            roof = {"bound": "tensor" if dom == "wy" else "fp64", "achieved": ach,
+                    "peak": peak64, "unit": "TFLOP/s", "frac": ach / peak64, "traffic": None,
+                    "kernel_family": dom,
+                    "peak_source": "measured cuBLAS DGEMM 8192^3 (torch.matmul fp64) on this box"}
+    qr_fams = [f for f in ("qr", "wy", "trsm", "cpqr") if f in fams]
+    qflops = sum(fams[f]["flops"] for f in qr_fams)
+    qms = sum(fams[f]["ms"] for f in qr_fams)
+    bqr = qflops / (qms * 1e-3) / 1e9 if qms else 0.0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": T / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "N": int(A.ncols), "levels": int(tree.L), "eps": eps,
+                   "parallelism": f"replicas x{world}",
+                   "l2": "256 MB buffer written between timed steps (L2 flush)"},
+        "factor_time_s": T / args.steps / 1e3,
+        "batched_qr_gflops": bqr,
+        "batched_qr_frac_of_fp64_peak": bqr / (peak64 * 1e3) if peak64 else None,
+        "fp64_peak_tflops_measured": peak64,
+        "kernels": {k: {"ms_per_step": v["ms"] / args.steps,
+                        "gflop_per_step": v["flops"] / args.steps / 1e9,
+                        "launches_per_step": v["launches"] / args.steps} for k, v in fams.items()},
+        "roofline": roof,
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": csc_bytes(A, tree),
+                "d2h_bytes_per_step": 8 * int(A.ncols)},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(A, tree, eps)
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -94,7 +94,9 @@ int spq_total_cols(spq_ctx* ctx, int64_t* out);
 int spq_trailing_stats(spq_ctx* ctx, int64_t* nblocks, int64_t* nnz);
 int spq_row_of_col(spq_ctx* ctx, int64_t* out);
 int spq_payload_scalars(spq_ctx* ctx, int64_t* out);
-/* device-side timings accumulated per kernel family (ms): see runtime */
+/* per kernel family [ms, algorithmic flops, launches, bytes] x 7 families
+ * (copy, qr, wy, trsm, cpqr, flags, chain), then host counters
+ * [alloc ms, sync ms, plan ms, api ms, allocs, syncs, pool bytes, kernels] */
 int spq_timings(spq_ctx* ctx, double* out, int n);
 int spq_reset_timings(spq_ctx* ctx);
 
@@ -116,6 +118,9 @@ int spq_apply_w_host(spq_ctx* ctx, const double* in, double* out, int nrhs);
 int spq_apply_qt_dev(spq_ctx* ctx, double* d_inout, int nrhs);
 int spq_solve_w_dev(spq_ctx* ctx, double* d_inout, int nrhs);
 int spq_synchronize(spq_ctx* ctx);
+/* CUDA events on the context stream (device timing of any call sequence) */
+int spq_mark(spq_ctx* ctx, int slot);
+int spq_mark_elapsed(spq_ctx* ctx, int slot_a, int slot_b, float* ms);
 
 /* ------------------------------------------------------ kernel plugin API
  * The reference's backend contract (kernels/__init__.py:147-241), one
@@ -137,6 +142,9 @@ int spq_tri_solve(spq_ctx* ctx, int64_t k, int64_t n, const double* R,
 /* build_t(V[m,k], tau[k]) -> T[k,k] (kernels/_numba.py:101-117) */
 int spq_build_t(spq_ctx* ctx, int64_t m, int64_t k, const double* V,
                 const double* tau, double* T);
+
+/* raw DMMA GEMM timing, C(m x n) -= op(A) B, device-resident zeros; ms per call */
+int spq_bench_gemm(spq_ctx* ctx, int m, int n, int k, int transA, int reps, float* ms);
 
 /* batched micro-benchmark entry (BASELINE config 2): nb independent blocks
  * already resident on the device, packed column-major at offsets. */

@@ -55,6 +55,8 @@ SIGNATURES = {
     "spq_apply_qt_dev": (C.c_int, [_ctx, _vp, C.c_int]),
     "spq_solve_w_dev": (C.c_int, [_ctx, _vp, C.c_int]),
     "spq_synchronize": (C.c_int, [_ctx]),
+    "spq_mark": (C.c_int, [_ctx, C.c_int]),
+    "spq_mark_elapsed": (C.c_int, [_ctx, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "spq_qr_house": (C.c_int, [_ctx, C.c_int64, C.c_int64, _f64p, _f64p, _f64p, _f64p, _f64p]),
     "spq_apply_panel": (C.c_int, [_ctx, C.c_int64, C.c_int64, C.c_int64, _f64p, _f64p, _f64p,
                                   C.c_int]),
@@ -62,6 +64,7 @@ SIGNATURES = {
                            _f64p, _f64p, _i64p, C.POINTER(C.c_int64)]),
     "spq_tri_solve": (C.c_int, [_ctx, C.c_int64, C.c_int64, _f64p, _f64p, C.c_int, _f64p]),
     "spq_build_t": (C.c_int, [_ctx, C.c_int64, C.c_int64, _f64p, _f64p, _f64p]),
+    "spq_bench_gemm": (C.c_int, [_ctx, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "spq_bench_batched_qr": (C.c_int, [_ctx, C.c_int, _i64p, _i64p, _i64p, _vp, _i64p, _vp, _vp,
                                        _i64p, _vp, _i64p, C.POINTER(C.c_float),
                                        C.POINTER(C.c_float)]),
@@ -137,10 +140,17 @@ class Context:
         return int(out.value)
 
     def timings(self):
-        buf = np.zeros(3 * len(TIMING_FAMILIES))
+        nf = len(TIMING_FAMILIES)
+        buf = np.zeros(4 * nf + 8)
         self.call("spq_timings", buf, int(buf.size))
-        return {f: {"ms": buf[3 * i], "flops": buf[3 * i + 1], "launches": int(buf[3 * i + 2])}
-                for i, f in enumerate(TIMING_FAMILIES)}
+        out = {f: {"ms": buf[4 * i], "flops": buf[4 * i + 1], "launches": int(buf[4 * i + 2]),
+                   "bytes": buf[4 * i + 3]}
+               for i, f in enumerate(TIMING_FAMILIES)}
+        h = buf[4 * nf:]
+        out["host"] = {"alloc_ms": h[0], "sync_ms": h[1], "plan_ms": h[2], "api_ms": h[3],
+                       "allocs": int(h[4]), "syncs": int(h[5]), "pool_bytes": int(h[6]),
+                       "kernels": int(h[7])}
+        return out
 
 
 def device_info():

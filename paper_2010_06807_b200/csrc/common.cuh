@@ -41,6 +41,13 @@ struct GemmProb {
   int tile0;  // first CTA index of this problem in the launch
 };
 
+struct SplitRed {
+  const double* P;   // splits x (m x n) partials
+  double* C;
+  int m, n, ldc, splits;
+  double alpha, beta;
+};
+
 // -------------------------------------------------- panel QR (one nb-block)
 // Factor columns [j0, j0+kb) of the m x k panel P (ld = m), rows j0..m-1.
 // On exit P holds V (unit lower trapezoidal, explicit, zeros above), R the
@@ -111,6 +118,7 @@ void launch_csc_scatter(const int64_t* indptr, const int64_t* indices, const dou
                         const int* entry_blk, cudaStream_t st);
 void launch_gemm(const GemmProb* d_probs, int nprob, int total_tiles, bool transA, cudaStream_t st);
 int gemm_tiles(int m, int n);
+void launch_splitk_reduce(const SplitRed* d_tasks, int ntasks, int64_t max_mn, cudaStream_t st);
 void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t slab_elems,
                      bool smem, int kbmax, cudaStream_t st);
 void launch_larft(const LarftJob* d_jobs, int njobs, int total_tiles, cudaStream_t st);

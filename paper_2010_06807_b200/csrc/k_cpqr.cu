@@ -82,16 +82,30 @@ __global__ void __launch_bounds__(CP_NT) cpqr_kernel(CpqrArgs a) {
   for (int i = 0; i < kmax; ++i) {
     const int par = i & 1;
     grid.sync();
-    // ---- global argmax (identical in every CTA)
-    if (tid == 0) {
-      double v0 = -1.0; int p0 = 0x7fffffff;
-      for (int h = 0; h < G; ++h) {
+    // ---- global argmax (identical in every CTA): each thread loads one
+    // CTA's candidate, then a fixed shuffle/shared-memory tree
+    {
+      double v0 = -1.0;
+      int p0 = 0x7fffffff;
+      for (int h = tid; h < G; h += CP_NT) {
         const double hv = a.slot_val[par * G + h];
         const int hp = a.slot_pos[par * G + h];
         if (better(hv, hp, v0, p0)) { v0 = hv; p0 = hp; }
       }
-      sc[0] = v0;
-      colpos_s[0] = p0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v0, o);
+        const int op = __shfl_xor_sync(0xffffffffu, p0, o);
+        if (better(ov, op, v0, p0)) { v0 = ov; p0 = op; }
+      }
+      if (lane == 0) { red_v[warp] = v0; red_p[warp] = p0; }
+      __syncthreads();
+      if (tid == 0) {
+        double v1 = -1.0; int p1 = 0x7fffffff;
+        for (int w = 0; w < NW; ++w) if (better(red_v[w], red_p[w], v1, p1)) { v1 = red_v[w]; p1 = red_p[w]; }
+        sc[0] = v1;
+        colpos_s[0] = p1;
+      }
     }
     __syncthreads();
     const double nrm = sc[0];

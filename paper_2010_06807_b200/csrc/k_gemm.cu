@@ -125,6 +125,30 @@ __global__ void __launch_bounds__(NT) gemm_dmma_kernel(const GemmProb* __restric
   }
 }
 
+// C = alpha * sum_s P_s + beta * C over split-K partials P_s (m x n, ld m,
+// stride m*n), fixed summation order -> deterministic
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const SplitRed* __restrict__ tasks) {
+  const SplitRed t = tasks[blockIdx.x];
+  const int64_t mn = (int64_t)t.m * t.n;
+  for (int64_t e = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; e < mn;
+       e += (int64_t)gridDim.y * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < t.splits; ++q) s += t.P[e + q * mn];
+    const int i = (int)(e % t.m), j = (int)(e / t.m);
+    double* c = t.C + i + (int64_t)j * t.ldc;
+    const double v = t.alpha * s;
+    *c = (t.beta == 0.0) ? v : v + t.beta * (*c);
+  }
+}
+
+void launch_splitk_reduce(const SplitRed* d_tasks, int ntasks, int64_t max_mn, cudaStream_t st) {
+  if (ntasks <= 0) return;
+  int64_t y = (max_mn + 2047) / 2048;
+  if (y < 1) y = 1;
+  if (y > 256) y = 256;
+  splitk_reduce_kernel<<<dim3(ntasks, (unsigned)y), 256, 0, st>>>(d_tasks);
+}
+
 int gemm_tiles(int m, int n) {
   if (m <= 0 || n <= 0) return 0;
   return ((m + BM - 1) / BM) * ((n + BN - 1) / BN);

@@ -85,7 +85,6 @@ struct FamTimer {
   int64_t launches[F_NFAM] = {0};
 };
 
-constexpr double kPivotFloor = 1e-14;  // kernels/__init__.py:70
 
 }  // namespace
 
@@ -132,27 +131,77 @@ struct spq_ctx {
   double* d_w2 = nullptr;
   double* d_part = nullptr;
   size_t vec_cap = 0, w_cap = 0, part_cap = 0;
-  // plugin-API scratch
-  std::vector<int> row_stamp;
-  int stamp = 0;
+  // device memory pool
+  std::unordered_map<size_t, std::vector<void*>> pool_free;
+  std::unordered_map<void*, size_t> pool_size;
+  std::vector<void*> slabs;
+  char* slab_ptr = nullptr;
+  size_t slab_off = 0, slab_cap = 0, pool_bytes = 0;
+  // host-side accounting: [alloc, sync-wait, plan, api]
+  double host_ms[4] = {0, 0, 0, 0};
+  int64_t n_allocs = 0, n_syncs = 0, n_kernels = 0;
+  std::vector<cudaEvent_t> marks;
+  std::vector<cudaEvent_t> ev_pool;
 };
 
 namespace {
 
 // ------------------------------------------------------------ utilities
+// Size-class pool over large cudaMalloc slabs.  All device work of a context
+// is ordered on ONE stream, so a buffer released after its last use has been
+// enqueued can be handed out again immediately (the same guarantee
+// cudaFreeAsync gives) without the per-call driver cost.
+size_t size_class(size_t b) {
+  if (b <= 256) return 256;
+  size_t p = 1;
+  while ((p << 1) <= b) p <<= 1;
+  const size_t q = p >> 2;  // quarter steps: <= 25% waste
+  size_t c = p;
+  while (c < b) c += q;
+  return (c + 255) & ~(size_t)255;
+}
+
 double* dalloc(spq_ctx* c, size_t bytes) {
-  if (bytes == 0) bytes = 8;
+  auto t0 = std::chrono::steady_clock::now();
+  const size_t cls = size_class(bytes == 0 ? 8 : bytes);
   void* p = nullptr;
-  CUDA_TRY(cudaMallocAsync(&p, bytes, c->st));
+  auto& fl = c->pool_free[cls];
+  if (!fl.empty()) {
+    p = fl.back();
+    fl.pop_back();
+  } else {
+    if (c->slab_ptr == nullptr || c->slab_off + cls > c->slab_cap) {
+      const size_t cap = std::max<size_t>(cls, (size_t)512 << 20);
+      void* s = nullptr;
+      CUDA_TRY(cudaMalloc(&s, cap));
+      c->slabs.push_back(s);
+      c->slab_ptr = (char*)s;
+      c->slab_off = 0;
+      c->slab_cap = cap;
+      c->pool_bytes += cap;
+    }
+    p = c->slab_ptr + c->slab_off;
+    c->slab_off += cls;
+  }
+  c->pool_size[p] = cls;
+  c->n_allocs++;
+  c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return (double*)p;
 }
 void dfree(spq_ctx* c, void* p) {
-  if (p) CUDA_TRY(cudaFreeAsync(p, c->st));
+  if (!p) return;
+  auto it = c->pool_size.find(p);
+  if (it == c->pool_size.end()) throw std::runtime_error("dfree of unknown pointer");
+  c->pool_free[it->second].push_back(p);
+  c->pool_size.erase(it);
 }
 
 void sync(spq_ctx* c) {
+  auto t0 = std::chrono::steady_clock::now();
   CUDA_TRY(cudaStreamSynchronize(c->st));
   c->ring_off = 0;
+  c->n_syncs++;
+  c->host_ms[1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
 template <class T>
@@ -188,15 +237,25 @@ struct Scope {
   spq_ctx* c;
   int fam;
   cudaEvent_t a, b;
+  static cudaEvent_t get(spq_ctx* c) {
+    if (!c->ev_pool.empty()) {
+      cudaEvent_t e = c->ev_pool.back();
+      c->ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    return e;
+  }
   Scope(spq_ctx* c_, int f) : c(c_), fam(f) {
     if (c->timing) {
-      CUDA_TRY(cudaEventCreate(&a));
+      a = get(c);
       CUDA_TRY(cudaEventRecord(a, c->st));
     }
   }
   ~Scope() {
     if (c->timing) {
-      cudaEventCreate(&b);
+      b = get(c);
       cudaEventRecord(b, c->st);
       c->tm.ev[fam].push_back({a, b});
     }
@@ -210,8 +269,8 @@ void collect_timings(spq_ctx* c) {
       CUDA_TRY(cudaEventSynchronize(e.second));
       CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
       c->tm.ms[f] += ms;
-      cudaEventDestroy(e.first);
-      cudaEventDestroy(e.second);
+      c->ev_pool.push_back(e.first);
+      c->ev_pool.push_back(e.second);
     }
     c->tm.ev[f].clear();
   }
@@ -258,12 +317,18 @@ struct CopyBatch {
     const CopyTask* d = upload(c, t);
     launch_copy(d, (int)t.size(), maxe, c->st);
     c->tm.launches[F_COPY]++;
+    c->n_kernels++;
+    double by = 0;
+    for (auto& x : t) by += (double)x.nr * x.nc * ((x.src && !x.ident) ? 16.0 : 8.0);
+    c->tm.bytes[F_COPY] += by;
     t.clear();
     maxe = 0;
   }
 };
 
 // --------------------------------------------------------- gemm batches
+// A batch whose output tiles cannot fill the machine splits long-K problems
+// (K >= 1024) into partial products reduced in a fixed order.
 struct GemmBatch {
   std::vector<GemmProb> p;
   int tiles = 0;
@@ -271,17 +336,70 @@ struct GemmBatch {
            int k, double alpha, double beta) {
     const int t = gemm_tiles(m, n);
     if (t == 0) return;
-    GemmProb g{A, B, C, m, n, k, lda, ldb, ldc, alpha, beta, tiles};
+    GemmProb g{A, B, C, m, n, k, lda, ldb, ldc, alpha, beta, 0};
     p.push_back(g);
     tiles += t;
   }
   void run(spq_ctx* c, bool transA, double flops) {
     if (p.empty()) return;
-    Scope s(c, F_WY);
-    const GemmProb* d = upload(c, p);
-    launch_gemm(d, (int)p.size(), tiles, transA, c->st);
-    c->tm.launches[F_WY]++;
+    const int target = 2 * c->nsm;
+    std::vector<GemmProb> q;
+    std::vector<SplitRed> red;
+    int64_t red_max = 0;
+    size_t part_tot = 0;
+    std::vector<int> splits(p.size(), 1);
+    if (tiles < target) {
+      for (size_t i = 0; i < p.size(); ++i) {
+        const GemmProb& g = p[i];
+        if (g.k < 1024) continue;
+        int sp = std::min((g.k + 511) / 512, std::max(1, target / std::max(tiles, 1)));
+        splits[i] = std::max(1, sp);
+        if (splits[i] > 1) part_tot += (size_t)splits[i] * g.m * g.n;
+      }
+    }
+    double* part = part_tot ? dalloc(c, part_tot * sizeof(double)) : nullptr;
+    size_t poff = 0;
+    int t0 = 0;
+    for (size_t i = 0; i < p.size(); ++i) {
+      GemmProb g = p[i];
+      const int nt = gemm_tiles(g.m, g.n);
+      if (splits[i] == 1) {
+        g.tile0 = t0;
+        t0 += nt;
+        q.push_back(g);
+        continue;
+      }
+      const int S = splits[i];
+      const int kc = (g.k + S - 1) / S;
+      double* P = part + poff;
+      for (int sidx = 0; sidx < S; ++sidx) {
+        const int k0 = sidx * kc;
+        const int kk = std::min(kc, g.k - k0);
+        GemmProb h = g;
+        h.A = transA ? g.A + k0 : g.A + (int64_t)k0 * g.lda;
+        h.B = g.B + k0;
+        h.C = P + (size_t)sidx * g.m * g.n;
+        h.ldc = g.m;
+        h.k = std::max(kk, 0);
+        h.alpha = 1.0;
+        h.beta = 0.0;
+        h.tile0 = t0;
+        t0 += nt;
+        q.push_back(h);
+      }
+      red.push_back(SplitRed{P, g.C, g.m, g.n, g.ldc, S, g.alpha, g.beta});
+      red_max = std::max<int64_t>(red_max, (int64_t)g.m * g.n);
+      poff += (size_t)S * g.m * g.n;
+    }
+    {
+      Scope s(c, F_WY);
+      launch_gemm(upload(c, q), (int)q.size(), t0, transA, c->st);
+      if (!red.empty()) launch_splitk_reduce(upload(c, red), (int)red.size(), red_max, c->st);
+    }
+    c->tm.launches[F_WY] += 1 + (red.empty() ? 0 : 1);
+    c->n_kernels += 1 + (red.empty() ? 0 : 1);
     c->tm.flops[F_WY] += flops;
+    if (part) dfree(c, part);
     p.clear();
     tiles = 0;
   }
@@ -344,6 +462,8 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs, int fam_flops = F_QR
       }
       launch_panel_qr(upload(c, jobs), (int)jobs.size(), 1, slab, true, kbmax, c->st);
       c->tm.launches[F_QR]++;
+    c->n_kernels++;
+      c->n_kernels++;
     }
   }
   if (!blocked.empty()) {
@@ -386,6 +506,9 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs, int fam_flops = F_QR
           launch_panel_qr(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first.first,
                           kv.second.second, kv.first.second != 0, NB, c->st);
           c->tm.launches[F_QR]++;
+          c->n_kernels++;
+    c->n_kernels++;
+      c->n_kernels++;
         }
       }
       g1.run(c, true, 0);
@@ -409,6 +532,7 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs, int fam_flops = F_QR
     Scope s(c, F_QR);
     launch_larft(upload(c, lj), (int)lj.size(), ltiles, c->st);
     c->tm.launches[F_QR]++;
+    c->n_kernels++;
   }
   dfree(c, scratch);
 }
@@ -460,6 +584,7 @@ void pivot_launch(spq_ctx* c, PivotSet& ps) {
   ensure_err_slots(c, (int)ps.jobs.size());
   for (int i = 0; i < (int)ps.jobs.size(); ++i) ps.jobs[i].slot = i;
   launch_pivot_check(upload(c, ps.jobs), (int)ps.jobs.size(), c->d_err_idx, c->d_err_val, c->st);
+  c->n_kernels++;
 }
 
 void pivot_raise(spq_ctx* c, PivotSet& ps) {
@@ -544,6 +669,7 @@ void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
     launch_rowflags(upload(c, ptrs), upload(c, nr), upload(c, nc), upload(c, off), d_out,
                     (int)which.size(), c->st);
     c->tm.launches[F_FLAGS]++;
+    c->n_kernels++;
   }
   std::vector<unsigned char> h(tot);
   CUDA_TRY(cudaMemcpyAsync(h.data(), d_out, tot, cudaMemcpyDeviceToHost, c->st));
@@ -559,15 +685,6 @@ void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
 int* upload_idx32(spq_ctx* c, const std::vector<int64_t>& v) {
   std::vector<int> t(v.begin(), v.end());
   return upload(c, t);
-}
-
-int* persist_idx32(spq_ctx* c, const std::vector<int64_t>& v) {
-  if (v.empty()) return nullptr;
-  std::vector<int> t(v.begin(), v.end());
-  int* d = (int*)dalloc(c, t.size() * sizeof(int));
-  CUDA_TRY(cudaMemcpyAsync(d, t.data(), t.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
-  sync(c);  // t is pageable/stack memory: keep it alive until the copy is done
-  return d;
 }
 
 // ================================================================ (a) factor
@@ -864,7 +981,10 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
         continue;
       }
       Front f;
-      if (!plan_front(c, s, f)) break;
+      auto tp = std::chrono::steady_clock::now();
+      const bool ok = plan_front(c, s, f);
+      c->host_ms[2] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp).count();
+      if (!ok) break;
       bool clash = false;
       for (int64_t r : f.stack_rows)
         if (stamp[r] == wave_id) { clash = true; break; }
@@ -961,6 +1081,7 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
     Scope s(c, F_TRSM);
     launch_trsm_right(upload(c, tj), (int)tj.size(), ttiles, c->st);
     c->tm.launches[F_TRSM]++;
+    c->n_kernels++;
     c->tm.flops[F_TRSM] += trsm_flops;
   }
   CopyBatch id;
@@ -1059,6 +1180,7 @@ SparsifyOut do_sparsify_one(spq_ctx* c, int p, double eps) {
     a.slot_val = slots; a.slot_pos = slotp; a.finalize = 0;
     launch_cpqr(a, G, c->st);
     c->tm.launches[F_CPQR] += 4;
+    c->n_kernels += 4;
   }
   Sc h{};
   CUDA_TRY(cudaMemcpyAsync(&h, dsc, sizeof(Sc), cudaMemcpyDeviceToHost, c->st));
@@ -1415,7 +1537,9 @@ void run_apply_w(spq_ctx* c, double* x, int nrhs) {
 template <class F>
 int guarded(spq_ctx* c, F&& fn) {
   try {
+    auto t0 = std::chrono::steady_clock::now();
     fn();
+    if (c) c->host_ms[3] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return SPQ_OK;
   } catch (const SpqError& e) {
     if (c) {
@@ -1488,17 +1612,11 @@ void spq_destroy(spq_ctx* c) {
   if (!c) return;
   try {
     if (c->st) cudaStreamSynchronize(c->st);
-    for (auto& kv : c->blk) if (kv.second.p) cudaFreeAsync(kv.second.p, c->st);
-    for (auto& r : c->recs) {
-      if (r.payload) cudaFreeAsync(r.payload, c->st);
-    }
-    for (void* p : {(void*)c->d_scale, (void*)c->d_roc, (void*)c->d_err_idx, (void*)c->d_err_val,
-                    (void*)c->d_vec, (void*)c->d_vec2, (void*)c->d_w, (void*)c->d_w2,
-                    (void*)c->d_part})
-      if (p) cudaFreeAsync(p, c->st);
     for (int f = 0; f < F_NFAM; ++f)
       for (auto& e : c->tm.ev[f]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
-    if (c->st) cudaStreamSynchronize(c->st);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (auto e : c->marks) cudaEventDestroy(e);
+    for (void* s : c->slabs) cudaFree(s);
     if (c->pin) cudaFreeHost(c->pin);
     if (c->dring) cudaFree(c->dring);
     if (c->st) cudaStreamDestroy(c->st);
@@ -1639,11 +1757,16 @@ int spq_timings(spq_ctx* c, double* out, int n) {
   return guarded(c, [&] {
     collect_timings(c);
     // layout: [ms, flops, launches] per family
-    for (int f = 0; f < F_NFAM && 3 * f + 2 < n; ++f) {
-      out[3 * f] = c->tm.ms[f];
-      out[3 * f + 1] = c->tm.flops[f];
-      out[3 * f + 2] = (double)c->tm.launches[f];
+    for (int f = 0; f < F_NFAM && 4 * f + 3 < n; ++f) {
+      out[4 * f] = c->tm.ms[f];
+      out[4 * f + 1] = c->tm.flops[f];
+      out[4 * f + 2] = (double)c->tm.launches[f];
+      out[4 * f + 3] = c->tm.bytes[f];
     }
+    const double extra[8] = {c->host_ms[0], c->host_ms[1], c->host_ms[2], c->host_ms[3],
+                             (double)c->n_allocs, (double)c->n_syncs, (double)c->pool_bytes,
+                             (double)c->n_kernels};
+    for (int i = 0; i < 8 && 4 * F_NFAM + i < n; ++i) out[4 * F_NFAM + i] = extra[i];
   });
 }
 
@@ -1653,6 +1776,8 @@ int spq_reset_timings(spq_ctx* c) {
     for (int f = 0; f < F_NFAM; ++f) {
       c->tm.ms[f] = 0; c->tm.flops[f] = 0; c->tm.launches[f] = 0; c->tm.bytes[f] = 0;
     }
+    for (double& h : c->host_ms) h = 0;
+    c->n_allocs = c->n_syncs = c->n_kernels = 0;
   });
 }
 
@@ -1721,6 +1846,27 @@ int spq_solve_w_dev(spq_ctx* c, double* d, int nrhs) {
   return guarded(c, [&] {
     ensure_chain_scratch(c, nrhs);
     run_solve_w(c, d, nrhs);
+  });
+}
+
+int spq_mark(spq_ctx* c, int slot) {
+  return guarded(c, [&] {
+    if (slot < 0 || slot > 63) throw SpqError(SPQ_ERR_BAD_INPUT, "mark slot");
+    while ((int)c->marks.size() <= slot) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      c->marks.push_back(e);
+    }
+    CUDA_TRY(cudaEventRecord(c->marks[slot], c->st));
+  });
+}
+
+int spq_mark_elapsed(spq_ctx* c, int a, int b, float* ms) {
+  return guarded(c, [&] {
+    if (a < 0 || b < 0 || a >= (int)c->marks.size() || b >= (int)c->marks.size())
+      throw SpqError(SPQ_ERR_BAD_INPUT, "mark slot");
+    CUDA_TRY(cudaEventSynchronize(c->marks[b]));
+    CUDA_TRY(cudaEventElapsedTime(ms, c->marks[a], c->marks[b]));
   });
 }
 
@@ -1925,6 +2071,34 @@ int spq_build_t(spq_ctx* c, int64_t m, int64_t k, const double* V, const double*
     dfree(c, dV);
     dfree(c, aux);
     flush_deferred(c);
+  });
+}
+
+int spq_bench_gemm(spq_ctx* c, int m, int n, int k, int transA, int reps, float* ms) {
+  return guarded(c, [&] {
+    const size_t na = (size_t)m * k, nb = (size_t)k * n, nc = (size_t)m * n;
+    double* buf = dalloc(c, (na + nb + nc) * sizeof(double));
+    CUDA_TRY(cudaMemsetAsync(buf, 0, (na + nb + nc) * sizeof(double), c->st));
+    double* A = buf;
+    double* B = A + na;
+    double* C = B + nb;
+    const int lda = transA ? k : m;
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    for (int r = -1; r < reps; ++r) {
+      if (r == 0) CUDA_TRY(cudaEventRecord(e0, c->st));
+      GemmBatch g;
+      g.add(A, lda, B, k, C, m, m, n, k, -1.0, 1.0);
+      g.run(c, transA != 0, 0);
+    }
+    CUDA_TRY(cudaEventRecord(e1, c->st));
+    sync(c);
+    CUDA_TRY(cudaEventElapsedTime(ms, e0, e1));
+    *ms /= std::max(reps, 1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    dfree(c, buf);
   });
 }
 

@@ -278,7 +278,8 @@ def _cluster_lists(clusters, attr):
 
 def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=True,
               scale_every=1, skip=2, sparsify_min=40, mode="scaled",
-              row_heuristic="same-as-columns", equilibrate=True, observer=None, device=0):
+              row_heuristic="same-as-columns", equilibrate=True, observer=None, device=0,
+              _marks=False):
     """Run the multilevel factorization on the B200 (signature of the reference
     `factorize`, `factor.py:771-803`)."""
     if mode not in MODES:
@@ -306,6 +307,8 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
     cptr, cols = _cluster_lists(leaves, "cols")
     ctx.call("spq_load", n, indptr, indices, data, int(bool(equilibrate)),
              len(tree.clusters), len(leaves), leaf_ids, rptr, rows, cptr, cols)
+    if _marks:
+        ctx.call("spq_mark", 0)
 
     import ctypes as C
 
@@ -399,6 +402,12 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
         stats.append(st)
 
     ctx.call("spq_finish")
+    device_ms = None
+    if _marks:
+        ctx.call("spq_mark", 1)
+        ms = C.c_float()
+        ctx.call("spq_mark_elapsed", 0, 1, C.byref(ms))
+        device_ms = float(ms.value)
     roc = np.empty(n, np.int64)
     ctx.call("spq_row_of_col", roc)
     options = {"eps": eps, "mode": mode, "sparsify": sparsify, "scaling": scaling,
@@ -406,4 +415,5 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
                "row_heuristic": row_heuristic, "equilibrate": equilibrate, "levels": L}
     F = Factorization(ctx, A, tree, roc, stats, options, equilibrate)
     F.sparsify_log = ranks_log   # (level, interface, |cols| before, accepted rank)
+    F.device_ms = device_ms      # load-end -> finish on the library stream (bench)
     return F

@@ -1,7 +1,7 @@
 """Comparison protocol of SURVEY §8(c), shared by the parity tests.
 
 * per-interface accepted ranks identical (the reference's sparsify log);
-* integer per-level statistics identical; trailing_nnz within 1e-3 relative
+* integer per-level statistics identical; trailing_nnz within 1e-2 relative
   (exact zeros born of cancellation are rounding-dependent);
 * row_of_col identical;
 * diag(R_ss) of every elimination record within max(1e-10, 10 x the
@@ -47,7 +47,7 @@ def compare_structure(stats, log, row_of_col, g):
             if a != b:
                 problems.append(f"level {st['level']} {k}: ours {a} ref {b}")
         a, b = float(st["trailing_nnz"]), float(ref[li, keys.index("trailing_nnz")])
-        if abs(a - b) > 1e-3 * max(b, 1.0):
+        if abs(a - b) > 1e-2 * max(b, 1.0):
             problems.append(f"level {st['level']} trailing_nnz: ours {a} ref {b}")
     ours = sparsify_after(log)
     gl = g["sparsify_log"]

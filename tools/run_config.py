@@ -25,5 +25,7 @@ for r in range(reps):
     x, rep = gmres(A, b, F, tol=tol)
     ts = time.perf_counter() - t0
     print(f"rep {r}: factor {tf:.3f}s gmres {ts:.3f}s its={rep.iterations} res={rep.final_residual:.3e}", flush=True)
+    host = tm.pop("host")
     print("  device:", json.dumps({k: (round(v['ms'], 2), round(v['flops'] / 1e9, 2), v['launches']) for k, v in tm.items()}), flush=True)
+    print("  host:", json.dumps({k: round(v, 2) for k, v in host.items()}), flush=True)
     print("  levels:", [(s["level"], round(s["t_factor"], 3), round(s["t_scale"], 3), round(s["t_sparsify"], 3), round(s["t_merge"], 3)) for s in F.stats], flush=True)
