@@ -141,7 +141,7 @@ class Context:
 
     def timings(self):
         nf = len(TIMING_FAMILIES)
-        buf = np.zeros(4 * nf + 8)
+        buf = np.zeros(4 * nf + 20)
         self.call("spq_timings", buf, int(buf.size))
         out = {f: {"ms": buf[4 * i], "flops": buf[4 * i + 1], "launches": int(buf[4 * i + 2]),
                    "bytes": buf[4 * i + 3]}
@@ -149,7 +149,11 @@ class Context:
         h = buf[4 * nf:]
         out["host"] = {"alloc_ms": h[0], "sync_ms": h[1], "plan_ms": h[2], "api_ms": h[3],
                        "allocs": int(h[4]), "syncs": int(h[5]), "pool_bytes": int(h[6]),
-                       "kernels": int(h[7])}
+                       "kernels": int(h[7]),
+                       "flags_ms": h[8], "flags_wait_ms": h[9], "front_struct_ms": h[10],
+                       "wave_exec_ms": h[11], "sparsify_ms": h[12], "sparsify_wait_ms": h[13],
+                       "merge_ms": h[14], "scale_ms": h[15], "pivot_wait_ms": h[16],
+                       "stats_ms": h[17]}
         return out
 
 

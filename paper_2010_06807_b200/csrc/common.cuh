@@ -49,10 +49,10 @@ struct SplitRed {
 };
 
 // -------------------------------------------------- panel QR (one nb-block)
-// Factor columns [j0, j0+kb) of the m x k panel P (ld = m), rows j0..m-1.
-// On exit P holds V (unit lower trapezoidal, explicit, zeros above), R the
-// upper triangle, tau the coefficients; Tb (kb x kb, ld = ldT) the block's
-// compact-WY T when want_T.
+// Factor columns [j0, j0+kb) (kb <= 32) of the m x k panel P (ld = m), rows
+// j0..m-1.  On exit P holds V (unit lower trapezoidal, explicit, zeros
+// above), R the upper triangle, tau the coefficients, and the block's
+// compact-WY T_b in T[j0:j0+kb, j0:j0+kb].
 struct PanelJob {
   double* P;
   double* R;     // k x k, ld = k
@@ -82,6 +82,7 @@ struct LarftJob {
   const double* G;   // k x k Gram V^T V (ld = ldg)
   const double* tau;
   double* T;         // k x k (ld = ldt)
+  double* Y;         // scratch k x 32
   int k, ldg, ldt;
   int tile0;
 };

@@ -10,6 +10,8 @@
 // k-rows of a fragment land on disjoint 8-bank groups).  One launch covers
 // every problem of a wave; each CTA finds its problem by binary search over
 // the per-problem first-tile prefix.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace spq {
@@ -149,14 +151,154 @@ void launch_splitk_reduce(const SplitRed* d_tasks, int ntasks, int64_t max_mn, c
   splitk_reduce_kernel<<<dim3(ntasks, (unsigned)y), 256, 0, st>>>(d_tasks);
 }
 
+
+// ---------------------------------------------------------------- v2
+// 128x64x16 CTA tile, 8 warps (4 along M x 2 along N, 32x32 each), 3-stage
+// cp.async pipeline (8-byte copies with zero-fill for the ragged edges, any
+// leading dimension), same conflict-free k-major shared layout.
+namespace {
+constexpr int BM2 = 128, BN2 = 64, BK2 = 16, PA2 = 132, PB2 = 68, NT2 = 256, ST2 = 3;
+
+__device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = ok ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(ok ? src : nullptr), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+}  // namespace
+
+template <bool TA>
+__global__ void __launch_bounds__(NT2) gemm_dmma2_kernel(const GemmProb* __restrict__ probs,
+                                                         int nprob) {
+  int lo = 0, hi = nprob - 1;
+  const int bid = blockIdx.x;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (probs[mid].tile0 <= bid) lo = mid; else hi = mid - 1;
+  }
+  const GemmProb p = probs[lo];
+  const int tm = (p.m + BM2 - 1) / BM2;
+  const int t = bid - p.tile0;
+  const int m0 = (t % tm) * BM2, n0 = (t / tm) * BN2;
+
+  extern __shared__ __align__(16) double smem2[];
+  double* As = smem2;                       // [ST2][BK2][PA2]
+  double* Bs = smem2 + ST2 * BK2 * PA2;     // [ST2][BK2][PB2]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  const int g = lane >> 2, q = lane & 3;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto issue = [&](int stage, int k0) {
+    double* a = As + stage * BK2 * PA2;
+    double* b = Bs + stage * BK2 * PB2;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {      // A: 128 x 16 = 2048 elements
+      const int l = tid + e * NT2;
+      int mi, ki;
+      if (TA) { ki = l & 15; mi = l >> 4; } else { mi = l & 127; ki = l >> 7; }
+      const int gm = m0 + mi, gk = k0 + ki;
+      const bool ok = gm < p.m && gk < p.k;
+      const double* src = TA ? p.A + gk + (int64_t)gm * p.lda : p.A + gm + (int64_t)gk * p.lda;
+      cp8(a + ki * PA2 + mi, src, ok);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {      // B: 16 x 64 = 1024 elements
+      const int l = tid + e * NT2;
+      const int kb = l & 15, nb = l >> 4;
+      const int gk = k0 + kb, gn = n0 + nb;
+      const bool ok = gk < p.k && gn < p.n;
+      cp8(b + kb * PB2 + nb, p.B + gk + (int64_t)gn * p.ldb, ok);
+    }
+  };
+
+  const int nk = (p.k + BK2 - 1) / BK2;
+#pragma unroll
+  for (int s = 0; s < ST2 - 1; ++s) {
+    if (s < nk) issue(s, s * BK2);
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<ST2 - 2>();
+    __syncthreads();
+    const int nxt = kt + ST2 - 1;
+    if (nxt < nk) issue(nxt % ST2, nxt * BK2);
+    cp_commit();
+    const double* a = As + (kt % ST2) * BK2 * PA2;
+    const double* b = Bs + (kt % ST2) * BK2 * PB2;
+#pragma unroll
+    for (int kk = 0; kk < BK2; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = a[(kk + q) * PA2 + wm + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = b[(kk + q) * PB2 + wn + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], fa[i], fb[j]);
+    }
+  }
+  cp_wait<0>();
+
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm + i * 8 + g;
+    if (row >= p.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + wn + j * 8 + 2 * q + h;
+        if (col >= p.n) continue;
+        double* c = p.C + row + (int64_t)col * p.ldc;
+        const double v = p.alpha * acc[i][j][h];
+        *c = (p.beta == 0.0) ? v : v + p.beta * (*c);
+      }
+    }
+  }
+}
+
+static int gemm_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPQ_GEMM");
+    v = (e && e[0] == '1') ? 1 : 2;
+  }
+  return v;
+}
+
 int gemm_tiles(int m, int n) {
   if (m <= 0 || n <= 0) return 0;
+  if (gemm_variant() == 2) return ((m + BM2 - 1) / BM2) * ((n + BN2 - 1) / BN2);
   return ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
 }
 
 void launch_gemm(const GemmProb* d_probs, int nprob, int total_tiles, bool transA,
                  cudaStream_t st) {
   if (nprob <= 0 || total_tiles <= 0) return;
+  if (gemm_variant() == 2) {
+    const size_t smem = (size_t)ST2 * BK2 * (PA2 + PB2) * sizeof(double);
+    static bool init = false;
+    if (!init) {
+      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      init = true;
+    }
+    if (transA)
+      gemm_dmma2_kernel<true><<<total_tiles, NT2, smem, st>>>(d_probs, nprob);
+    else
+      gemm_dmma2_kernel<false><<<total_tiles, NT2, smem, st>>>(d_probs, nprob);
+    return;
+  }
   if (transA)
     gemm_dmma_kernel<true><<<total_tiles, NT, 0, st>>>(d_probs, nprob);
   else

@@ -24,10 +24,15 @@ namespace cg = cooperative_groups;
 namespace spq {
 
 constexpr int QR_NT = 256;
+constexpr int QR_NB = 32;   // columns per panel block (T_b is QR_NB x QR_NB)
+
+// Shared-memory layout (doubles): exchange [2][XCH] | red [8][32] | dtot[32] |
+// apiv[32] | wv[32] | scal[4] | Gs[32][33] | slab (nloc x kb, odd ld)
+constexpr int XCH = 1 + 2 * QR_NB;
+constexpr int SM_FIXED = 2 * XCH + 8 * QR_NB + 3 * QR_NB + 4 + QR_NB * (QR_NB + 1);
 
 template <bool SMEM>
-__global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restrict__ jobs,
-                                                         int kbmax) {
+__global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restrict__ jobs) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int q = (int)cluster.block_rank();
@@ -38,25 +43,24 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
   const int r0 = min(mh, q * rpc);
   const int r1 = min(mh, r0 + rpc);
   const int nloc = r1 - r0;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = QR_NT / 32;
+  const int tid = threadIdx.x;
 
-  extern __shared__ double sm[];
-  const int XCH = 1 + 2 * kbmax;
-  double* xch = sm;                       // [2][XCH]
-  double* dtot = xch + 2 * XCH;           // [kbmax]
-  double* apiv = dtot + kbmax;            // [kbmax]
-  double* wv = apiv + kbmax;              // [kbmax]
-  double* scal = wv + kbmax;              // [4]
-  double* gram = scal + 4;                // [kbmax*kbmax] only when want_T (kb <= 32)
-  double* slab_s = gram + (kbmax <= 32 ? kbmax * kbmax : 0);
+  extern __shared__ __align__(16) double sm[];
+  double* xch = sm;                        // [2][XCH]
+  double* red = xch + 2 * XCH;             // [8][QR_NB]
+  double* dtot = red + 8 * QR_NB;          // [QR_NB]
+  double* apiv = dtot + QR_NB;             // [QR_NB]
+  double* wv = apiv + QR_NB;               // [QR_NB]
+  double* scal = wv + QR_NB;               // [4]
+  double* Gs = scal + 4;                   // [QR_NB][QR_NB+1]  Gs[b + i*33] = V_b^T v_i
+  double* slab_s = Gs + QR_NB * (QR_NB + 1);
 
-  double* P0 = J.P + (int64_t)j0 * m + j0 + r0;  // (row r0 of the block, col j0)
+  double* P0 = J.P + (int64_t)j0 * m + j0 + r0;  // (block row r0, col j0)
   double* S;
   int lds;
   if (SMEM) {
     S = slab_s;
-    lds = nloc > 0 ? nloc : 1;
+    lds = nloc | 1;                         // odd: thread-per-column reads conflict-free
     for (int e = tid; e < nloc * kb; e += QR_NT) {
       const int i = e % nloc, c = e / nloc;
       S[i + c * lds] = P0[i + (int64_t)c * m];
@@ -65,8 +69,7 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
     S = P0;
     lds = m;
   }
-  // rows above the block in its columns are finished R entries: move them
-  if (q == 0 && j0 > 0) {
+  if (q == 0 && j0 > 0) {   // finished R entries above the block
     for (int e = tid; e < j0 * kb; e += QR_NT) {
       const int i = e % j0, c = e / j0;
       double* src = J.P + i + (int64_t)(j0 + c) * m;
@@ -76,31 +79,39 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
   }
   __syncthreads();
 
+  // thread -> (column c, row partition pr): kb <= 32 columns x NP partitions
+  const int NP = QR_NT / QR_NB;            // 8
+  const int c_of = tid % QR_NB, p_of = tid / QR_NB;
+
   for (int jj = 0; jj < kb; ++jj) {
-    const int par = jj & 1;
-    double* X = xch + par * XCH;
+    double* X = xch + (jj & 1) * XCH;
     const int ist = max(0, jj - r0 + 1);   // first local row strictly below the pivot
-    const int ploc = jj - r0;              // local pivot row (owner iff 0 <= ploc < nloc)
-    // ---- partial dots: column c = jj gives sigma, c > jj gives d_c
-    for (int c = jj + warp; c < kb; c += NW) {
+    const int ploc = jj - r0;
+    const bool owner = ploc >= 0 && ploc < nloc;
+    // dots of the pivot column (rows below the pivot) with EVERY block column:
+    //   c == jj -> sigma, c > jj -> trailing d_c, c < jj -> Gram column for T
+    if (c_of < kb) {
       double s = 0.0;
-      for (int i = ist + lane; i < nloc; i += 32) s += S[i + jj * lds] * S[i + c * lds];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) X[1 + c] = s;
+      const double* xc = S + jj * lds;
+      const double* ac = S + c_of * lds;
+      for (int i = ist + p_of; i < nloc; i += NP) s += xc[i] * ac[i];
+      red[p_of * QR_NB + c_of] = s;
     }
-    if (ploc >= 0 && ploc < nloc)
-      for (int c = jj + tid; c < kb; c += QR_NT) X[1 + kbmax + c] = S[ploc + c * lds];
-    cluster.sync();
-    const int owner = min(CL - 1, jj / rpc);
-    for (int c = jj + tid; c < kb; c += QR_NT) {
+    __syncthreads();
+    if (tid < kb) {
       double s = 0.0;
-      for (int r = 0; r < CL; ++r) {
-        const double* Xr = cluster.map_shared_rank(X, r);
-        s += Xr[1 + c];
-      }
-      dtot[c] = s;
-      apiv[c] = cluster.map_shared_rank(X, owner)[1 + kbmax + c];
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) s += red[pp * QR_NB + tid];
+      X[1 + tid] = s;
+      if (owner) X[1 + QR_NB + tid] = S[ploc + tid * lds];
+    }
+    cluster.sync();
+    const int own = min(CL - 1, jj / rpc);
+    if (tid < kb) {
+      double s = 0.0;
+      for (int r = 0; r < CL; ++r) s += cluster.map_shared_rank(X, r)[1 + tid];
+      dtot[tid] = s;
+      apiv[tid] = cluster.map_shared_rank(X, own)[1 + QR_NB + tid];
     }
     __syncthreads();
     if (tid == 0) {
@@ -120,15 +131,17 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
     __syncthreads();
     const double tau = scal[0], v0 = scal[1], beta = scal[2];
     const bool zero = scal[3] != 0.0;
-    for (int c = jj + 1 + tid; c < kb; c += QR_NT)
-      wv[c] = zero ? tau * apiv[c] : tau * (apiv[c] + dtot[c] / v0);
-    // reflector entries below the pivot: v_i = x_i / v0
+    if (tid < kb) {
+      const double gv = zero ? apiv[tid] : apiv[tid] + dtot[tid] / v0;   // V_c^T v_jj
+      if (tid < jj) Gs[tid + jj * (QR_NB + 1)] = gv;
+      if (tid > jj) wv[tid] = tau * gv;                                   // w_c = tau v^T a_c
+    }
     for (int i = ist + tid; i < nloc; i += QR_NT)
       S[i + jj * lds] = zero ? 0.0 : S[i + jj * lds] / v0;
     __syncthreads();
     if (tau != 0.0) {
       const int ncol = kb - jj - 1;
-      const int ibeg = (ploc >= 0 && ploc < nloc) ? ploc : ist;
+      const int ibeg = owner ? ploc : ist;
       const int nr = nloc - ibeg;
       for (int e = tid; e < nr * ncol; e += QR_NT) {
         const int i = ibeg + e % nr, c = jj + 1 + e / nr;
@@ -136,56 +149,37 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
         S[i + c * lds] -= wv[c] * vi;
       }
     }
-    if (ploc >= 0 && ploc < nloc && tid == 0) S[ploc + jj * lds] = beta;
+    if (owner && tid == 0) S[ploc + jj * lds] = beta;
     __syncthreads();
   }
 
   // R entries of the diagonal block out, explicit unit-lower V in
   for (int e = tid; e < nloc * kb; e += QR_NT) {
     const int i = e % nloc, c = e / nloc;
-    const int a = r0 + i;   // block-relative row
+    const int a = r0 + i;
     if (a < kb && c >= a) {
       J.R[(j0 + a) + (int64_t)(j0 + c) * k] = S[i + c * lds];
       S[i + c * lds] = (c == a) ? 1.0 : 0.0;
     }
   }
-  __syncthreads();
-
-  if (J.want_T) {
-    // partial Gram of this CTA's rows, cluster reduction into CTA 0, then
-    // the row-parallel T recurrence (kb <= 32): T[a,i] = -tau_i sum T[a,b] G[b,i]
-    for (int e = tid; e < kb * kb; e += QR_NT) {
-      const int a = e % kb, b = e / kb;
+  // T_b from the Gram columns gathered above: row-parallel recurrence
+  //   T[a,a] = tau_a,  T[a,i] = -tau_i sum_{b=a}^{i-1} T[a,b] G[b,i]
+  if (q == 0 && tid < kb) {
+    const int a = tid;
+    double trow[QR_NB];
+#pragma unroll
+    for (int b = 0; b < QR_NB; ++b) trow[b] = 0.0;
+    trow[a] = J.tau[j0 + a];
+    for (int i = a + 1; i < kb; ++i) {
+      const double ti = J.tau[j0 + i];
       double s = 0.0;
-      if (a <= b)
-        for (int i = 0; i < nloc; ++i) s += S[i + a * lds] * S[i + b * lds];
-      gram[e] = s;
+      for (int b = a; b < i; ++b) s += trow[b] * Gs[b + i * (QR_NB + 1)];
+      trow[i] = (ti != 0.0) ? -ti * s : 0.0;
     }
-    cluster.sync();
-    if (q == 0) {
-      for (int e = tid; e < kb * kb; e += QR_NT) {
-        double s = 0.0;
-        for (int r = 0; r < CL; ++r) s += cluster.map_shared_rank(gram, r)[e];
-        gram[e] = s;   // only CTA 0 reads CTA 0's partials: in-place is safe
-      }
-      __syncthreads();
-      if (tid < kb) {
-        const int a = tid;
-        double trow[32];
-        for (int b = 0; b < kb; ++b) trow[b] = 0.0;
-        trow[a] = J.tau[j0 + a];
-        for (int i = a + 1; i < kb; ++i) {
-          const double ti = J.tau[j0 + i];
-          double s = 0.0;
-          for (int b = a; b < i; ++b) s += trow[b] * gram[b + i * kb];
-          trow[i] = (ti != 0.0) ? -ti * s : 0.0;
-        }
-        double* Tg = J.T + j0 + (int64_t)j0 * k;
-        for (int i = 0; i < kb; ++i) Tg[a + (int64_t)i * k] = trow[i];
-      }
-    }
+    double* Tg = J.T + j0 + (int64_t)j0 * k;
+    for (int i = 0; i < kb; ++i) Tg[a + (int64_t)i * k] = trow[i];
   }
-
+  __syncthreads();
   if (SMEM) {
     for (int e = tid; e < nloc * kb; e += QR_NT) {
       const int i = e % nloc, c = e / nloc;
@@ -195,18 +189,14 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
   cluster.sync();   // no CTA leaves while others may still read its shared memory
 }
 
-static size_t panel_smem_bytes(int kbmax, bool want_T, int64_t slab_elems, bool smem) {
-  size_t n = 2 * (1 + 2 * (size_t)kbmax) + 3 * (size_t)kbmax + 4;
-  if (want_T) n += (size_t)kbmax * kbmax;
-  if (smem) n += (size_t)slab_elems;
-  return n * sizeof(double);
+size_t panel_smem_bytes(int64_t slab_elems, bool smem) {
+  return (size_t)(SM_FIXED + (smem ? slab_elems : 0)) * sizeof(double);
 }
 
 void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t slab_elems,
-                     bool smem, int kbmax, cudaStream_t st) {
+                     bool smem, int /*kbmax*/, cudaStream_t st) {
   if (njobs <= 0) return;
-  const bool want_T = kbmax <= 32;
-  const size_t bytes = panel_smem_bytes(kbmax, want_T, slab_elems, smem);
+  const size_t bytes = panel_smem_bytes(slab_elems, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(njobs * cluster));
   cfg.blockDim = dim3(QR_NT);
@@ -219,60 +209,87 @@ void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t sla
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (smem) {
-    static bool init = false;
-    if (!init) {
-      CUDA_TRY(cudaFuncSetAttribute(panel_qr_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      CUDA_TRY(cudaFuncSetAttribute(panel_qr_kernel<true>,
-                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      init = true;
+  static bool init = false;
+  if (!init) {
+    for (auto fn : {panel_qr_kernel<true>, panel_qr_kernel<false>}) {
+      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     }
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_qr_kernel<true>, d_jobs, kbmax));
-  } else {
-    static bool init = false;
-    if (!init) {
-      CUDA_TRY(cudaFuncSetAttribute(panel_qr_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      CUDA_TRY(cudaFuncSetAttribute(panel_qr_kernel<false>,
-                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      init = true;
-    }
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_qr_kernel<false>, d_jobs, kbmax));
+    init = true;
   }
+  if (smem)
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_qr_kernel<true>, d_jobs));
+  else
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_qr_kernel<false>, d_jobs));
 }
 
 // ------------------------------------------------------------------ larft
-constexpr int LARFT_NT = 128;
+// Full compact-WY T (k x k) from G = V^T V and tau, one CTA per job, in
+// 32-column block columns J:  T_JJ by the row recurrence (one warp),
+// Y = G[0:j0,J] T_JJ (scratch), T[0:j0,J] = -T[0:j0,0:j0] Y.
+constexpr int LARFT_NT = 256;
 
-__global__ void __launch_bounds__(LARFT_NT) larft_kernel(const LarftJob* __restrict__ jobs,
-                                                         int njobs) {
-  int lo = 0, hi = njobs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (jobs[mid].tile0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
-  }
-  const LarftJob J = jobs[lo];
-  const int a = (blockIdx.x - J.tile0) * LARFT_NT + threadIdx.x;
-  if (a >= J.k) return;
-  const int k = J.k;
-  double* T = J.T;
-  for (int b = 0; b < a; ++b) T[a + (int64_t)b * J.ldt] = 0.0;
-  T[a + (int64_t)a * J.ldt] = J.tau[a];
-  for (int i = a + 1; i < k; ++i) {
-    const double ti = J.tau[i];
-    double s = 0.0;
-    if (ti != 0.0)
-      for (int b = a; b < i; ++b) s += T[a + (int64_t)b * J.ldt] * J.G[b + (int64_t)i * J.ldg];
-    T[a + (int64_t)i * J.ldt] = (ti != 0.0) ? -ti * s : 0.0;
+__global__ void __launch_bounds__(LARFT_NT) larft_kernel(const LarftJob* __restrict__ jobs) {
+  const LarftJob J = jobs[blockIdx.x];
+  const int k = J.k, tid = threadIdx.x;
+  __shared__ double Tjj[32 * 33];
+  __shared__ double Gjj[32 * 33];
+  for (int j0 = 0; j0 < k; j0 += 32) {
+    const int w = min(32, k - j0);
+    for (int e = tid; e < w * w; e += LARFT_NT) {
+      const int a = e % w, b = e / w;
+      Gjj[a + b * 33] = J.G[(j0 + a) + (int64_t)(j0 + b) * J.ldg];
+    }
+    __syncthreads();
+    if (tid < w) {
+      const int a = tid;
+      double trow[32];
+#pragma unroll
+      for (int b = 0; b < 32; ++b) trow[b] = 0.0;
+      trow[a] = J.tau[j0 + a];
+      for (int i = a + 1; i < w; ++i) {
+        const double ti = J.tau[j0 + i];
+        double s = 0.0;
+        for (int b = a; b < i; ++b) s += trow[b] * Gjj[b + i * 33];
+        trow[i] = (ti != 0.0) ? -ti * s : 0.0;
+      }
+      for (int i = 0; i < w; ++i) Tjj[a + i * 33] = trow[i];
+    }
+    __syncthreads();
+    for (int e = tid; e < w * w; e += LARFT_NT) {
+      const int a = e % w, i = e / w;
+      J.T[(j0 + a) + (int64_t)(j0 + i) * J.ldt] = (a <= i) ? Tjj[a + i * 33] : 0.0;
+    }
+    for (int e = tid; e < (k - j0 - w) * w; e += LARFT_NT) {   // strictly below: zeros
+      const int a = j0 + w + e % (k - j0 - w), i = e / (k - j0 - w);
+      J.T[a + (int64_t)(j0 + i) * J.ldt] = 0.0;
+    }
+    if (j0 > 0) {
+      // Y[a,e] = sum_{f<=e} G[a, j0+f] T_JJ[f,e]   (a < j0)
+      for (int t = tid; t < j0 * w; t += LARFT_NT) {
+        const int a = t % j0, e = t / j0;
+        double s = 0.0;
+        for (int f = 0; f <= e; ++f) s += J.G[a + (int64_t)(j0 + f) * J.ldg] * Tjj[f + e * 33];
+        J.Y[a + (int64_t)e * k] = s;
+      }
+      __syncthreads();
+      // T[a, j0+e] = -sum_{b=a}^{j0-1} T[a,b] Y[b,e]
+      for (int t = tid; t < j0 * w; t += LARFT_NT) {
+        const int a = t % j0, e = t / j0;
+        double s = 0.0;
+        for (int b = a; b < j0; ++b) s += J.T[a + (int64_t)b * J.ldt] * J.Y[b + (int64_t)e * k];
+        J.T[a + (int64_t)(j0 + e) * J.ldt] = -s;
+      }
+    }
+    __syncthreads();
   }
 }
 
-int larft_tiles(int k) { return (k + LARFT_NT - 1) / LARFT_NT; }
+int larft_tiles(int) { return 1; }
 
-void launch_larft(const LarftJob* d_jobs, int njobs, int total_tiles, cudaStream_t st) {
-  if (njobs <= 0 || total_tiles <= 0) return;
-  larft_kernel<<<total_tiles, LARFT_NT, 0, st>>>(d_jobs, njobs);
+void launch_larft(const LarftJob* d_jobs, int njobs, int /*total_tiles*/, cudaStream_t st) {
+  if (njobs <= 0) return;
+  larft_kernel<<<njobs, LARFT_NT, 0, st>>>(d_jobs);
 }
 
 // ------------------------------------------------------------ pivot check

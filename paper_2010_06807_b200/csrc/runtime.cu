@@ -138,7 +138,7 @@ struct spq_ctx {
   char* slab_ptr = nullptr;
   size_t slab_off = 0, slab_cap = 0, pool_bytes = 0;
   // host-side accounting: [alloc, sync-wait, plan, api]
-  double host_ms[4] = {0, 0, 0, 0};
+  double host_ms[16] = {0};
   int64_t n_allocs = 0, n_syncs = 0, n_kernels = 0;
   std::vector<cudaEvent_t> marks;
   std::vector<cudaEvent_t> ev_pool;
@@ -147,6 +147,14 @@ struct spq_ctx {
 namespace {
 
 // ------------------------------------------------------------ utilities
+struct HostTimer {
+  double* acc;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostTimer(double* a) : acc(a), t0(std::chrono::steady_clock::now()) {}
+  ~HostTimer() {
+    *acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
 // Size-class pool over large cudaMalloc slabs.  All device work of a context
 // is ordered on ONE stream, so a buffer released after its last use has been
 // enqueued can be handed out again immediately (the same guarantee
@@ -406,135 +414,131 @@ struct GemmBatch {
 };
 
 // ----------------------------------------------------------- QR engine
+// Blocked Householder QR of a batch of panels (nb = 32 columns per block).
+// After each block's panel kernel, its compact WY (V_b, T_b) is applied to
+// the rest of the panel AND to every extra target C (rows j0..m-1):
+//   W = V_b^T X,  W = T_b^T W,  X -= V_b W      (batched DMMA GEMMs)
+// so the factorization never needs the full k x k T; records get it in one
+// batched build at spq_finish (build_full_T).
+struct CTarget {
+  double* C;
+  int ldc, n;
+};
+
 struct QrProb {
   double* P;  // m x k, ld m -> V on exit
   int m, k;
   double* R;  // k x k
   double* tau;
-  double* T;  // k x k
+  double* T;  // k x k (diagonal 32-blocks written)
+  std::vector<CTarget> targets;
 };
 
 constexpr int NB = 32;
-constexpr size_t SLAB_BYTES = 190 * 1024;
+constexpr size_t SLAB_BYTES = 200 * 1024;
 
-void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs, int fam_flops = F_QR) {
+void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
   if (probs.empty()) return;
-  double qr_flops = 0;
-  for (auto& q : probs) qr_flops += 2.0 * q.m * (double)q.k * q.k - 2.0 * q.k * (double)q.k * q.k / 3.0;
-  c->tm.flops[fam_flops] += qr_flops;
-  // classify
-  std::vector<int> single, blocked;
-  for (int i = 0; i < (int)probs.size(); ++i) {
-    const auto& q = probs[i];
-    if (q.k <= 0) continue;
-    if (q.k <= 128 && (size_t)q.m * q.k * 8 <= SLAB_BYTES - 8 * 1024)
-      single.push_back(i);
-    else
-      blocked.push_back(i);
+  double qr_flops = 0, wy_flops = 0;
+  int maxk = 0;
+  for (auto& q : probs) {
+    qr_flops += 2.0 * q.m * (double)q.k * q.k - 2.0 * q.k * (double)q.k * q.k / 3.0;
+    for (auto& t : q.targets) wy_flops += 4.0 * q.m * (double)t.n * q.k - (double)t.n * q.k * q.k;
+    maxk = std::max(maxk, q.k);
   }
-  // scratch: per blocked prob trailing W/W2 (NB x k each), G (k x k) for all
-  size_t g_off = 0;
-  std::vector<size_t> goff(probs.size()), woff(probs.size());
-  for (size_t i = 0; i < probs.size(); ++i) {
-    goff[i] = g_off;
-    g_off += (size_t)probs[i].k * probs[i].k;
+  c->tm.flops[F_QR] += qr_flops;
+  c->tm.flops[F_WY] += wy_flops;
+  for (int j0 = 0; j0 < maxk; j0 += NB) {
+    std::map<std::pair<int, int>, std::pair<std::vector<PanelJob>, int64_t>> groups;
+    size_t wtot = 0;
+    for (auto& q : probs) {
+      if (j0 >= q.k) continue;
+      const int kb = std::min(NB, q.k - j0);
+      const int mh = q.m - j0;
+      int cl = (int)(((size_t)mh * kb * 8 + SLAB_BYTES - 1) / SLAB_BYTES);
+      cl = std::max(1, cl);
+      int smem = 1;
+      if (cl > 8) { cl = 8; smem = 0; }
+      while (cl > 1 && (mh + cl - 1) / cl < 64) --cl;
+      const int rpc = (mh + cl - 1) / cl;
+      auto& grp = groups[{cl, smem}];
+      grp.first.push_back(PanelJob{q.P, q.R, q.tau, q.T, q.m, q.k, j0, kb, 1});
+      grp.second = std::max<int64_t>(grp.second, (int64_t)(rpc | 1) * kb);
+      const int j1 = j0 + kb;
+      if (j1 < q.k) wtot += 2 * (size_t)kb * (q.k - j1);
+      for (auto& t : q.targets) wtot += 2 * (size_t)kb * t.n;
+    }
+    {
+      Scope s(c, F_QR);
+      for (auto& kv : groups) {
+        launch_panel_qr(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first.first,
+                        kv.second.second, kv.first.second != 0, NB, c->st);
+        c->tm.launches[F_QR]++;
+        c->n_kernels++;
+      }
+    }
+    if (wtot == 0) continue;
+    double* Ws = dalloc(c, wtot * sizeof(double));
+    size_t off = 0;
+    GemmBatch g1, g2, g3;
+    for (auto& q : probs) {
+      if (j0 >= q.k) continue;
+      const int kb = std::min(NB, q.k - j0);
+      const int mh = q.m - j0;
+      const int j1 = j0 + kb;
+      double* Vb = q.P + j0 + (int64_t)j0 * q.m;
+      const double* Tb = q.T + j0 + (int64_t)j0 * q.k;
+      auto add = [&](double* X, int ldx, int nx) {
+        if (nx <= 0 || mh <= 0) return;
+        double* W = Ws + off;
+        double* W2 = W + (size_t)kb * nx;
+        off += 2 * (size_t)kb * nx;
+        g1.add(Vb, q.m, X, ldx, W, kb, kb, nx, mh, 1.0, 0.0);
+        g2.add(Tb, q.k, W, kb, W2, kb, kb, nx, kb, 1.0, 0.0);
+        g3.add(Vb, q.m, W2, kb, X, ldx, mh, nx, kb, -1.0, 1.0);
+      };
+      if (j1 < q.k) add(q.P + j0 + (int64_t)j1 * q.m, q.m, q.k - j1);
+      for (auto& t : q.targets) add(t.C + j0, t.ldc, t.n);
+    }
+    g1.run(c, true, 0);
+    g2.run(c, true, 0);
+    g3.run(c, false, 0);
+    dfree(c, Ws);
   }
-  size_t w_tot = 0;
-  for (int i : blocked) {
-    woff[i] = w_tot;
-    w_tot += 2 * (size_t)NB * probs[i].k;
-  }
-  double* scratch = dalloc(c, (g_off + w_tot) * sizeof(double));
-  double* Gs = scratch;
-  double* Ws = scratch + g_off;
+}
 
-  {
-    Scope s(c, F_QR);
-    if (!single.empty()) {
-      std::vector<PanelJob> jobs;
-      int kbmax = 0;
-      int64_t slab = 0;
-      for (int i : single) {
-        const auto& q = probs[i];
-        jobs.push_back(PanelJob{q.P, q.R, q.tau, q.T, q.m, q.k, 0, q.k, 0});
-        kbmax = std::max(kbmax, q.k);
-        slab = std::max<int64_t>(slab, (int64_t)q.m * q.k);
-      }
-      launch_panel_qr(upload(c, jobs), (int)jobs.size(), 1, slab, true, kbmax, c->st);
-      c->tm.launches[F_QR]++;
-    c->n_kernels++;
-      c->n_kernels++;
-    }
-  }
-  if (!blocked.empty()) {
-    int maxk = 0;
-    for (int i : blocked) maxk = std::max(maxk, probs[i].k);
-    for (int j0 = 0; j0 < maxk; j0 += NB) {
-      // group jobs by (cluster size, smem)
-      std::map<std::pair<int, int>, std::pair<std::vector<PanelJob>, int64_t>> groups;
-      GemmBatch g1, g2, g3;
-      for (int i : blocked) {
-        const auto& q = probs[i];
-        if (j0 >= q.k) continue;
-        const int kb = std::min(NB, q.k - j0);
-        const int mh = q.m - j0;
-        int cl = (int)(((size_t)mh * kb * 8 + SLAB_BYTES - 1) / SLAB_BYTES);
-        cl = std::max(1, cl);
-        int smem = 1;
-        if (cl > 8) { cl = 8; smem = 0; }
-        // keep at least ~64 rows per CTA
-        while (cl > 1 && (mh + cl - 1) / cl < 64) --cl;
-        const int rpc = (mh + cl - 1) / cl;
-        const int j1 = j0 + kb;
-        auto& grp = groups[{cl, smem}];
-        grp.first.push_back(PanelJob{q.P, q.R, q.tau, q.T, q.m, q.k, j0, kb, j1 < q.k ? 1 : 0});
-        grp.second = std::max<int64_t>(grp.second, (int64_t)rpc * kb);
-        if (j1 < q.k) {
-          double* W = Ws + woff[i];
-          double* W2 = W + (size_t)NB * q.k;
-          const int nt = q.k - j1;
-          double* Vb = q.P + j0 + (int64_t)j0 * q.m;
-          double* Pt = q.P + j0 + (int64_t)j1 * q.m;
-          g1.add(Vb, q.m, Pt, q.m, W, kb, kb, nt, mh, 1.0, 0.0);
-          g2.add(q.T + j0 + (int64_t)j0 * q.k, q.k, W, kb, W2, kb, kb, nt, kb, 1.0, 0.0);
-          g3.add(Vb, q.m, W2, kb, Pt, q.m, mh, nt, kb, -1.0, 1.0);
-        }
-      }
-      {
-        Scope s(c, F_QR);
-        for (auto& kv : groups) {
-          launch_panel_qr(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first.first,
-                          kv.second.second, kv.first.second != 0, NB, c->st);
-          c->tm.launches[F_QR]++;
-          c->n_kernels++;
-    c->n_kernels++;
-      c->n_kernels++;
-        }
-      }
-      g1.run(c, true, 0);
-      g2.run(c, true, 0);
-      g3.run(c, false, 0);
-    }
-  }
-  // full T: G = V^T V, then the row recurrence
+// full k x k T for a batch of (V, tau, T) triples: G = V^T V, blocked larft
+struct TProb {
+  const double* V;
+  int m, k;
+  const double* tau;
+  double* T;
+};
+
+void build_full_T(spq_ctx* c, const std::vector<TProb>& tp) {
+  size_t gsz = 0;
+  for (auto& t : tp) gsz += (size_t)t.k * t.k + (size_t)t.k * 32;
+  if (gsz == 0) return;
+  double* scr = dalloc(c, gsz * sizeof(double));
   GemmBatch gg;
   std::vector<LarftJob> lj;
-  int ltiles = 0;
-  for (size_t i = 0; i < probs.size(); ++i) {
-    const auto& q = probs[i];
-    if (q.k <= 0) continue;
-    gg.add(q.P, q.m, q.P, q.m, Gs + goff[i], q.k, q.k, q.k, q.m, 1.0, 0.0);
-    lj.push_back(LarftJob{Gs + goff[i], q.tau, q.T, q.k, q.k, q.k, ltiles});
-    ltiles += larft_tiles(q.k);
+  size_t off = 0;
+  for (auto& t : tp) {
+    if (t.k <= 0) continue;
+    double* G = scr + off;
+    double* Y = G + (size_t)t.k * t.k;
+    off += (size_t)t.k * t.k + (size_t)t.k * 32;
+    gg.add(t.V, t.m, t.V, t.m, G, t.k, t.k, t.k, t.m, 1.0, 0.0);
+    lj.push_back(LarftJob{G, t.tau, t.T, Y, t.k, t.k, t.k, 0});
   }
   gg.run(c, true, 0);
   {
     Scope s(c, F_QR);
-    launch_larft(upload(c, lj), (int)lj.size(), ltiles, c->st);
+    launch_larft(upload(c, lj), (int)lj.size(), 0, c->st);
     c->tm.launches[F_QR]++;
     c->n_kernels++;
   }
-  dfree(c, scratch);
+  dfree(c, scr);
 }
 
 // C <- C - V T^T V^T C (transpose) or C - V T V^T C
@@ -589,6 +593,7 @@ void pivot_launch(spq_ctx* c, PivotSet& ps) {
 
 void pivot_raise(spq_ctx* c, PivotSet& ps) {
   if (ps.jobs.empty()) return;
+  HostTimer ht(&c->host_ms[12]);
   const int n = (int)ps.jobs.size();
   std::vector<int64_t> idx(n);
   std::vector<double> val(n);
@@ -643,6 +648,7 @@ double* new_block_mem(spq_ctx* c, int nr, int nc) {
 
 // refresh row flags of every non-clean block in the given row clusters
 void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
+  HostTimer ht(&c->host_ms[4]);
   std::vector<const double*> ptrs;
   std::vector<int> nr, nc;
   std::vector<int64_t> off;
@@ -672,9 +678,12 @@ void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
     c->n_kernels++;
   }
   std::vector<unsigned char> h(tot);
-  CUDA_TRY(cudaMemcpyAsync(h.data(), d_out, tot, cudaMemcpyDeviceToHost, c->st));
-  dfree(c, d_out);
-  sync(c);
+  {
+    HostTimer hw(&c->host_ms[5]);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), d_out, tot, cudaMemcpyDeviceToHost, c->st));
+    dfree(c, d_out);
+    sync(c);
+  }
   for (size_t t = 0; t < which.size(); ++t) {
     Block* b = which[t];
     b->flags.assign(h.begin() + off[t], h.begin() + off[t] + b->nr);
@@ -794,6 +803,7 @@ bool plan_front(spq_ctx* c, int s, Front& f) {
 }
 
 void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
+  HostTimer ht(&c->host_ms[6]);
   const int s = f.s;
   // gather sources (current blocks, before any replacement)
   for (int pi = 0; pi < (int)f.parts.size(); ++pi) {
@@ -869,6 +879,7 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
 }
 
 void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotSet& ps) {
+  HostTimer ht(&c->host_ms[7]);
   // scratch per front: C (m x n)
   size_t tot = 0;
   std::vector<size_t> coff(wave.size());
@@ -906,11 +917,14 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
     }
   }
   g.run(c);
-  // QR of every panel
+  // QR of every panel, its reflectors applied block by block to C_all
   std::vector<QrProb> qp;
-  for (auto& f : wave) {
+  for (size_t fi = 0; fi < wave.size(); ++fi) {
+    Front& f = wave[fi];
     Record& rec = c->recs[f.rec];
-    qp.push_back(QrProb{rec.V, f.m, f.k, rec.R, rec.tau, rec.T});
+    QrProb q{rec.V, f.m, f.k, rec.R, rec.tau, rec.T, {}};
+    if (f.n > 0) q.targets.push_back(CTarget{scr + coff[fi], f.m, f.n});
+    qp.push_back(std::move(q));
   }
   qr_batch(c, qp);
   for (auto& f : wave) {
@@ -918,14 +932,6 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
     ps.jobs.push_back(PivotJob{rec.R, f.k, f.k, 0});
     ps.ctx.push_back("pivot block of cluster " + std::to_string(f.s));
   }
-  // trailing update C <- H^T C
-  std::vector<WyProb> wp;
-  for (size_t fi = 0; fi < wave.size(); ++fi) {
-    Front& f = wave[fi];
-    Record& rec = c->recs[f.rec];
-    wp.push_back(WyProb{rec.V, rec.T, f.m, f.k, scr + coff[fi], f.m, f.n});
-  }
-  wy_batch(c, wp, true);
   // scatter: R_sn = C[:k], neighbour rows back into blocks
   CopyBatch sc;
   for (size_t fi = 0; fi < wave.size(); ++fi) {
@@ -1006,6 +1012,7 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
 
 // ================================================================ (b) scale
 void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
+  HostTimer ht(&c->host_ms[11]);
   std::vector<int> todo;
   for (size_t t = 0; t < ids.size(); ++t) {
     done[t] = 0;
@@ -1035,7 +1042,17 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
       t.src = b->p; t.dst = rec.V; t.nr = np; t.nc = np; t.lds = np; t.ldd = np;
       g.add(t);
     }
-    qp.push_back(QrProb{rec.V, np, np, rec.R, rec.tau, rec.T});
+    // left application U_pp^T to every (p, c) block rides on the QR (factor.py:512-520)
+    QrProb q{rec.V, np, np, rec.R, rec.tau, rec.T, {}};
+    for (int cc : c->rix[p]) {
+      if (cc == p) continue;
+      Block* bc = find_block(c, p, cc);
+      if (bc && bc->nc > 0 && bc->nr == np) {
+        q.targets.push_back(CTarget{bc->p, bc->nr, bc->nc});
+        bc->clean = false;
+      }
+    }
+    qp.push_back(std::move(q));
     recid.push_back((int)c->recs.size());
     c->recs.push_back(std::move(rec));
   }
@@ -1049,22 +1066,13 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
     ps.ctx.push_back("diagonal block of interface " + std::to_string(todo[t]));
   }
   pivot_launch(c, ps);
-  // left: U^T on every (p, c) block; right: R^{-1} on every (r, p) block
-  std::vector<WyProb> wp;
+  // right: R_pp^{-1} on every (r, p) block (factor.py:521-529)
   std::vector<TrsmJob> tj;
   int ttiles = 0;
   double trsm_flops = 0;
   for (size_t t = 0; t < todo.size(); ++t) {
     const int p = todo[t];
     Record& rec = c->recs[recid[t]];
-    for (int cc : c->rix[p]) {
-      if (cc == p) continue;
-      Block* b = find_block(c, p, cc);
-      if (b && b->nc > 0) {
-        wp.push_back(WyProb{rec.V, rec.T, rec.m, rec.k, b->p, b->nr, b->nc});
-        b->clean = false;
-      }
-    }
     for (int r : c->cix[p]) {
       if (r == p) continue;
       Block* b = find_block(c, r, p);
@@ -1076,7 +1084,6 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
       }
     }
   }
-  wy_batch(c, wp, true);
   {
     Scope s(c, F_TRSM);
     launch_trsm_right(upload(c, tj), (int)tj.size(), ttiles, c->st);
@@ -1116,6 +1123,7 @@ struct SparsifyOut {
 };
 
 SparsifyOut do_sparsify_one(spq_ctx* c, int p, double eps) {
+  HostTimer ht(&c->host_ms[8]);
   SparsifyOut o{-1, 0, 0.0, 0};
   if (!c->active[p]) throw SpqError(SPQ_ERR_BAD_INPUT, "sparsify of inactive cluster");
   const std::vector<int64_t> cols_p = c->cols_of[p], rows_p = c->rows_of[p];
@@ -1183,8 +1191,11 @@ SparsifyOut do_sparsify_one(spq_ctx* c, int p, double eps) {
     c->n_kernels += 4;
   }
   Sc h{};
-  CUDA_TRY(cudaMemcpyAsync(&h, dsc, sizeof(Sc), cudaMemcpyDeviceToHost, c->st));
-  sync(c);
+  {
+    HostTimer hw(&c->host_ms[9]);
+    CUDA_TRY(cudaMemcpyAsync(&h, dsc, sizeof(Sc), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+  }
   const int r = h.rank;
   o.rank = r;
   {
@@ -1202,15 +1213,9 @@ SparsifyOut do_sparsify_one(spq_ctx* c, int p, double eps) {
   }
   // T of the accepted reflectors, then Q^T M
   if (r > 0) {
-    double* G2 = dalloc(c, (size_t)r * r * sizeof(double));
-    GemmBatch gg;
-    gg.add(V, np, V, np, G2, r, r, r, np, 1.0, 0.0);
-    gg.run(c, true, 0);
-    std::vector<LarftJob> lj{LarftJob{G2, tau, T, r, r, r, 0}};
-    launch_larft(upload(c, lj), 1, larft_tiles(r), c->st);
+    build_full_T(c, {TProb{V, np, r, tau, T}});
     std::vector<WyProb> wp{WyProb{V, T, np, r, M, np, ncols}};
     wy_batch(c, wp, true);
-    dfree(c, G2);
   }
   // split back (factor.py:617-658)
   CopyBatch sc;
@@ -1295,6 +1300,7 @@ SparsifyOut do_sparsify_one(spq_ctx* c, int p, double eps) {
 
 // ================================================================ (d) merge
 void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, const int32_t* cid) {
+  HostTimer ht(&c->host_ms[10]);
   std::vector<int> parent_of(c->ncl, -1), roff(c->ncl, 0), coff(c->ncl, 0);
   std::vector<std::vector<int64_t>> nrows(np_), ncols(np_);
   for (int t = 0; t < np_; ++t) {
@@ -1699,6 +1705,10 @@ int spq_finish(spq_ctx* c) {
       r.d_cols_s = d + offs[q++];
       r.d_cols_n = d + offs[q++];
     }
+    std::vector<TProb> tp;
+    for (auto& r : c->recs)
+      if (r.kind != REC_SPARSIFY && r.k > 0) tp.push_back(TProb{r.V, r.m, r.k, r.tau, r.T});
+    build_full_T(c, tp);
     c->finished = true;
     sync(c);
   });
@@ -1722,6 +1732,7 @@ int spq_total_cols(spq_ctx* c, int64_t* out) {
 
 int spq_trailing_stats(spq_ctx* c, int64_t* nblocks, int64_t* nnz) {
   return guarded(c, [&] {
+    HostTimer ht(&c->host_ms[13]);
     *nblocks = (int64_t)c->blk.size();
     std::vector<const double*> ptrs;
     std::vector<int64_t> sizes;
@@ -1767,6 +1778,7 @@ int spq_timings(spq_ctx* c, double* out, int n) {
                              (double)c->n_allocs, (double)c->n_syncs, (double)c->pool_bytes,
                              (double)c->n_kernels};
     for (int i = 0; i < 8 && 4 * F_NFAM + i < n; ++i) out[4 * F_NFAM + i] = extra[i];
+    for (int i = 4; i < 16 && 4 * F_NFAM + 8 + (i - 4) < n; ++i) out[4 * F_NFAM + 8 + (i - 4)] = c->host_ms[i];
   });
 }
 
@@ -1915,7 +1927,8 @@ int spq_qr_house(spq_ctx* c, int64_t m, int64_t k, const double* B, double* V, d
     double* dtau = aux;
     double* dT = aux + k;
     double* dR = dT + k * k;
-    qr_batch(c, {QrProb{P, (int)m, (int)k, dR, dtau, dT}});
+    qr_batch(c, {QrProb{P, (int)m, (int)k, dR, dtau, dT, {}}});
+    build_full_T(c, {TProb{P, (int)m, (int)k, dtau, dT}});
     to_host_rowmajor(c, P, m, k, m, V);
     to_host_rowmajor(c, dT, k, k, k, T);
     to_host_rowmajor(c, dR, k, k, k, R);
@@ -2062,11 +2075,8 @@ int spq_build_t(spq_ctx* c, int64_t m, int64_t k, const double* V, const double*
     double* G = aux + k;
     double* dT = G + k * k;
     CUDA_TRY(cudaMemcpyAsync(dtau, tau, k * sizeof(double), cudaMemcpyHostToDevice, c->st));
-    GemmBatch gg;
-    gg.add(dV, (int)m, dV, (int)m, G, (int)k, (int)k, (int)k, (int)m, 1.0, 0.0);
-    gg.run(c, true, 0);
-    std::vector<LarftJob> lj{LarftJob{G, dtau, dT, (int)k, (int)k, (int)k, 0}};
-    launch_larft(upload(c, lj), 1, larft_tiles((int)k), c->st);
+    (void)G;
+    build_full_T(c, {TProb{dV, (int)m, (int)k, dtau, dT}});
     to_host_rowmajor(c, dT, k, k, k, T);
     dfree(c, dV);
     dfree(c, aux);

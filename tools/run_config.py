@@ -20,6 +20,7 @@ for r in range(reps):
     t0 = time.perf_counter()
     F = factorize(A, tree, eps=eps)
     tf = time.perf_counter() - t0
+    tfac_py = tf
     tm = F.device_timings()
     t0 = time.perf_counter()
     x, rep = gmres(A, b, F, tol=tol)
