@@ -103,6 +103,22 @@ struct CpqrArgs {
   int finalize;         // write beta/zeros into W's pivot columns (Tred)
 };
 
+// one problem of the batched CTA-resident CPQR
+struct CpqrJob {
+  double* W;           // m x n (ldw), candidate columns (compacted), read (and written back)
+  int m, n, ncap, ldw; // n used when nk == nullptr; ncap sizes shared memory
+  const int* nk;       // device live column count (sparsify) or nullptr
+  const double* eps;   // device threshold
+  int min_rank;
+  double* V;           // m x kmax (ldv), pre-zeroed
+  int ldv;
+  double* tau;
+  double* beta;
+  int* rank;
+  int* perm;
+  int write_back;      // store the reduced matrix (Tred) back into W
+};
+
 }  // namespace spq
 
 // ---------------------------------------------------------------- launchers
@@ -128,6 +144,8 @@ void launch_pivot_check(const PivotJob* d_jobs, int njobs, int64_t* d_err_idx,
                         double* d_err_val, cudaStream_t st);
 void launch_trsm_right(const TrsmJob* d_jobs, int njobs, int total_tiles, cudaStream_t st);
 int trsm_tiles(int n);
+size_t cpqr_cta_smem(int m, int ncap);
+void launch_cpqr_cta(const CpqrJob* d_jobs, int njobs, size_t smem, cudaStream_t st);
 }  // namespace spq
 
 #define CUDA_TRY(x)                                                        \

@@ -18,6 +18,8 @@
 // the host syncs once per interface, for the accepted rank.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -309,6 +311,213 @@ void launch_sparsify_prep(const double* M, int m, int n, double eps, double* sq,
   if (n > 0) colsq_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(M, m, n, sq);
   sparsify_select_kernel<<<1, 1024, 0, st>>>(sq, m, n, eps, keep_idx, nk, ratio, maxcol);
   if (n > 0) gather_cols_kernel<<<dim3((m + 255) / 256, n), 256, 0, st>>>(M, m, keep_idx, nk, W);
+}
+
+}  // namespace spq
+
+// ===================================================================== batched
+// CTA-resident threshold CPQR: one CTA per problem, the m x n candidate
+// matrix held in shared memory (physical column swaps, exactly the
+// reference's sequence), __syncthreads-only steps.  Used for every
+// interface whose M fits (and for BASELINE config 2's 4096 x (64x192)
+// batch).  Same semantics as cpqr_kernel / kernels/_numba.py:120-167.
+namespace spq {
+
+constexpr int CB_NT = 512;
+constexpr int CB_NW = CB_NT / 32;
+
+__device__ __forceinline__ void argmax_merge(double& v, int& p, double ov, int op) {
+  if (ov > v || (ov == v && op < p)) { v = ov; p = op; }
+}
+
+struct CbLayout {
+  int lds, n1, m1;
+  __host__ __device__ CbLayout(int m, int n) : lds(m | 1), n1(n > 0 ? n : 1), m1(m > 0 ? m : 1) {}
+  // doubles: S (lds*n1) | nrm (n1) | v (m1) | dpart (8*n1) | npart (8*n1) | redv (CB_NW)
+  // ints after: perm (n1) | redp (CB_NW)
+  __host__ __device__ size_t doubles() const {
+    return (size_t)lds * n1 + n1 + m1 + 16 * (size_t)n1 + CB_NW;
+  }
+  __host__ __device__ size_t bytes() const { return doubles() * 8 + ((size_t)n1 + CB_NW) * 4; }
+};
+
+__global__ void __launch_bounds__(CB_NT) cpqr_cta_kernel(const CpqrJob* __restrict__ jobs) {
+  const CpqrJob J = jobs[blockIdx.x];
+  const int m = J.m;
+  const int n = J.nk ? *J.nk : J.n;
+  const double eps = *J.eps;
+  const int kmax = min(m, n);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(16) double cs[];
+  const CbLayout L(m, J.ncap);
+  const int lds = L.lds;
+  double* S = cs;
+  double* nrm = S + (size_t)lds * L.n1;
+  double* v = nrm + L.n1;
+  double* dpart = v + L.m1;
+  double* npart = dpart + 8 * L.n1;
+  double* redv = npart + 8 * L.n1;
+  int* perm = reinterpret_cast<int*>(redv + CB_NW);
+  int* redp = perm + L.n1;
+  __shared__ double sc[4];
+  __shared__ int sp[1];
+
+  for (int e = tid; e < m * n; e += CB_NT) {
+    const int a = e % m, j = e / m;
+    S[a + j * lds] = J.W[a + (int64_t)j * J.ldw];
+  }
+  for (int j = tid; j < n; j += CB_NT) perm[j] = j;
+  int P = CB_NT / (n > 0 ? n : 1);
+  P = P >= 8 ? 8 : (P >= 4 ? 4 : (P >= 2 ? 2 : 1));
+  __syncthreads();
+  for (int t = tid; t < n * P; t += CB_NT) {
+    const int j = t % n, pr = t / n;
+    double s = 0.0;
+    for (int a = pr; a < m; a += P) s += S[a + j * lds] * S[a + j * lds];
+    npart[pr * L.n1 + j] = s;
+  }
+  __syncthreads();
+  for (int j = tid; j < n; j += CB_NT) {
+    double s = 0.0;
+    for (int pr = 0; pr < P; ++pr) s += npart[pr * L.n1 + j];
+    nrm[j] = sqrt(s);
+  }
+  __syncthreads();
+
+  double norm0 = 0.0;
+  int r = kmax;
+  for (int i = 0; i < kmax; ++i) {
+    double bv = -1.0;
+    int bp = 0x7fffffff;
+    for (int j = i + tid; j < n; j += CB_NT) argmax_merge(bv, bp, nrm[j], j);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      argmax_merge(bv, bp, ov, op);
+    }
+    if (lane == 0) { redv[warp] = bv; redp[warp] = bp; }
+    __syncthreads();
+    if (tid == 0) {
+      double v1 = -1.0; int p1 = 0x7fffffff;
+      for (int w = 0; w < CB_NW; ++w) argmax_merge(v1, p1, redv[w], redp[w]);
+      sc[0] = v1;
+      sp[0] = p1;
+    }
+    __syncthreads();
+    const double best = sc[0];
+    const int p = sp[0];
+    if (i == 0) {
+      norm0 = best;
+      if (norm0 == 0.0) { r = 0; break; }
+    } else if (best < eps * norm0 && i >= J.min_rank) {
+      r = i;
+      break;
+    }
+    if (p != i) {   // physical swap, like the reference
+      for (int a = tid; a < m; a += CB_NT) {
+        const double t0 = S[a + i * lds];
+        S[a + i * lds] = S[a + p * lds];
+        S[a + p * lds] = t0;
+      }
+      if (tid == 0) {
+        const double tn = nrm[i]; nrm[i] = nrm[p]; nrm[p] = tn;
+        const int tp = perm[i]; perm[i] = perm[p]; perm[p] = tp;
+      }
+    }
+    __syncthreads();
+    double s = 0.0;
+    for (int a = i + 1 + tid; a < m; a += CB_NT) s += S[a + i * lds] * S[a + i * lds];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) redv[warp] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double sigma = 0.0;
+      for (int w = 0; w < CB_NW; ++w) sigma += redv[w];
+      const double alpha = S[i + i * lds];
+      double tau, beta, v0 = 1.0, zero = 0.0;
+      if (sigma == 0.0) {
+        zero = 1.0;
+        if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+      } else {
+        beta = sqrt(alpha * alpha + sigma);
+        v0 = (alpha <= 0.0) ? alpha - beta : -sigma / (alpha + beta);
+        tau = -v0 / beta;
+      }
+      sc[1] = tau; sc[2] = v0; sc[3] = zero;
+      J.tau[i] = tau;
+      J.beta[i] = beta;
+    }
+    __syncthreads();
+    const double tau = sc[1], v0 = sc[2];
+    const bool zero = sc[3] != 0.0;
+    for (int a = i + tid; a < m; a += CB_NT) {
+      const double va = (a == i) ? 1.0 : (zero ? 0.0 : S[a + i * lds] / v0);
+      v[a] = va;
+      J.V[a + (int64_t)i * J.ldv] = va;
+    }
+    __syncthreads();
+    const int nt = n - i - 1;
+    if (tau != 0.0 && nt > 0) {
+      for (int t = tid; t < nt * P; t += CB_NT) {
+        const int j = i + 1 + t % nt, pr = t / nt;
+        double d = 0.0;
+        for (int a = i + pr; a < m; a += P) d += v[a] * S[a + j * lds];
+        dpart[pr * L.n1 + j] = d;
+      }
+      __syncthreads();
+      for (int t = tid; t < nt * P; t += CB_NT) {
+        const int j = i + 1 + t % nt, pr = t / nt;
+        double d = 0.0;
+        for (int q = 0; q < P; ++q) d += dpart[q * L.n1 + j];
+        const double w = tau * d;
+        double ns = 0.0;
+        for (int a = i + pr; a < m; a += P) {
+          const double nv = S[a + j * lds] - w * v[a];
+          S[a + j * lds] = nv;
+          if (a > i) ns += nv * nv;
+        }
+        npart[pr * L.n1 + j] = ns;
+      }
+    } else {
+      for (int t = tid; t < nt * P; t += CB_NT) {
+        const int j = i + 1 + t % nt, pr = t / nt;
+        double ns = 0.0;
+        for (int a = i + 1 + pr; a < m; a += P) ns += S[a + j * lds] * S[a + j * lds];
+        npart[pr * L.n1 + j] = ns;
+      }
+    }
+    __syncthreads();
+    for (int j = i + 1 + tid; j < n; j += CB_NT) {
+      double ns = 0.0;
+      for (int q = 0; q < P; ++q) ns += npart[q * L.n1 + j];
+      nrm[j] = sqrt(ns);
+    }
+    if (tid == 0) S[i + i * lds] = J.beta[i];
+    for (int a = i + 1 + tid; a < m; a += CB_NT) S[a + i * lds] = 0.0;
+    __syncthreads();
+  }
+  if (tid == 0) *J.rank = r;
+  for (int j = tid; j < n; j += CB_NT) J.perm[j] = perm[j];
+  if (J.write_back)
+    for (int e = tid; e < m * n; e += CB_NT) {
+      const int a = e % m, j = e / m;
+      J.W[a + (int64_t)j * J.ldw] = S[a + j * lds];
+    }
+}
+
+size_t cpqr_cta_smem(int m, int ncap) { return CbLayout(m, ncap).bytes() + 64; }
+
+void launch_cpqr_cta(const CpqrJob* d_jobs, int njobs, size_t smem, cudaStream_t st) {
+  if (njobs <= 0) return;
+  static size_t conf = 0;
+  if (smem > conf) {
+    CUDA_TRY(cudaFuncSetAttribute(cpqr_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(smem, 48 * 1024)));
+    conf = smem;
+  }
+  cpqr_cta_kernel<<<njobs, CB_NT, smem, st>>>(d_jobs);
 }
 
 }  // namespace spq

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <set>
 #include <string>
@@ -57,6 +58,7 @@ inline uint64_t bkey(int i, int j) { return ((uint64_t)(uint32_t)i << 32) | (uin
 
 struct Block {
   double* p = nullptr;
+  void* base = nullptr;        // shared (refcounted) allocation this block lives in
   int nr = 0, nc = 0;
   std::vector<uint8_t> flags;  // per row: 0 zero, 1 nonzero, 2 unknown (written)
   bool clean = false;
@@ -135,6 +137,8 @@ struct spq_ctx {
   std::unordered_map<size_t, std::vector<void*>> pool_free;
   std::unordered_map<void*, size_t> pool_size;
   std::vector<void*> slabs;
+  std::vector<size_t> slab_caps;
+  std::unordered_map<void*, int> refcnt;   // shared block allocations
   char* slab_ptr = nullptr;
   size_t slab_off = 0, slab_cap = 0, pool_bytes = 0;
   // host-side accounting: [alloc, sync-wait, plan, api]
@@ -147,6 +151,18 @@ struct spq_ctx {
 namespace {
 
 // ------------------------------------------------------------ utilities
+// Process-wide caches: device slabs and the pinned upload ring outlive a
+// context, so repeated factorizations do not pay cudaMalloc/cudaMallocHost.
+struct GlobalCache {
+  std::mutex mu;
+  std::vector<std::pair<void*, size_t>> slabs;   // (ptr, bytes)
+  std::vector<std::pair<char*, char*>> rings;    // (pinned, device) of RING_BYTES
+};
+GlobalCache& gcache() {
+  static GlobalCache* g = new GlobalCache();   // leaked on purpose (process lifetime)
+  return *g;
+}
+
 struct HostTimer {
   double* acc;
   std::chrono::steady_clock::time_point t0;
@@ -179,10 +195,22 @@ double* dalloc(spq_ctx* c, size_t bytes) {
     fl.pop_back();
   } else {
     if (c->slab_ptr == nullptr || c->slab_off + cls > c->slab_cap) {
-      const size_t cap = std::max<size_t>(cls, (size_t)512 << 20);
+      size_t cap = std::max<size_t>(cls, (size_t)512 << 20);
       void* s = nullptr;
-      CUDA_TRY(cudaMalloc(&s, cap));
+      {
+        auto& g = gcache();
+        std::lock_guard<std::mutex> lk(g.mu);
+        for (size_t i = 0; i < g.slabs.size(); ++i)
+          if (g.slabs[i].second >= cap) {
+            s = g.slabs[i].first;
+            cap = g.slabs[i].second;
+            g.slabs.erase(g.slabs.begin() + i);
+            break;
+          }
+      }
+      if (!s) CUDA_TRY(cudaMalloc(&s, cap));
       c->slabs.push_back(s);
+      c->slab_caps.push_back(cap);
       c->slab_ptr = (char*)s;
       c->slab_off = 0;
       c->slab_cap = cap;
@@ -202,6 +230,27 @@ void dfree(spq_ctx* c, void* p) {
   if (it == c->pool_size.end()) throw std::runtime_error("dfree of unknown pointer");
   c->pool_free[it->second].push_back(p);
   c->pool_size.erase(it);
+}
+
+// stream-ordered release of a block's memory (shared allocations refcounted)
+void release_mem(spq_ctx* c, Block& b) {
+  if (b.base) {
+    auto it = c->refcnt.find(b.base);
+    if (it != c->refcnt.end() && --it->second == 0) {
+      c->deferred.push_back((double*)b.base);
+      c->refcnt.erase(it);
+    }
+  } else if (b.p) {
+    c->deferred.push_back(b.p);
+  }
+  b.p = nullptr;
+  b.base = nullptr;
+}
+
+double* shared_alloc(spq_ctx* c, size_t elems, int nref) {
+  double* base = dalloc(c, std::max<size_t>(elems, 1) * sizeof(double));
+  c->refcnt[base] = nref;
+  return base;
 }
 
 void sync(spq_ctx* c) {
@@ -614,9 +663,10 @@ Block* find_block(spq_ctx* c, int i, int j) {
   return it == c->blk.end() ? nullptr : &it->second;
 }
 
-Block& put_block(spq_ctx* c, int i, int j, double* p, int nr, int nc) {
+Block& put_block(spq_ctx* c, int i, int j, double* p, int nr, int nc, void* base = nullptr) {
   Block& b = c->blk[bkey(i, j)];
   b.p = p;
+  b.base = base;
   b.nr = nr;
   b.nc = nc;
   c->rix[i].insert(j);
@@ -627,7 +677,7 @@ Block& put_block(spq_ctx* c, int i, int j, double* p, int nr, int nc) {
 void drop_block(spq_ctx* c, int i, int j) {
   auto it = c->blk.find(bkey(i, j));
   if (it != c->blk.end()) {
-    if (it->second.p) c->deferred.push_back(it->second.p);
+    release_mem(c, it->second);
     c->blk.erase(it);
   }
   c->rix[i].erase(j);
@@ -816,7 +866,17 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
         f.gsrc.push_back({bc->p, bc->nr, pi, f.woff[ci], bc->nc, p.full});
     }
   }
-  // trailing blocks of the neighbour rows (factor.py:467-480)
+  // trailing blocks of the neighbour rows (factor.py:467-480).  A fully
+  // covered row cluster gets ONE allocation holding all its new blocks
+  // side by side (block (r,c) = slab + woff_c * nr, ld nr) and one scatter.
+  std::vector<double*> full_slab(f.parts.size(), nullptr);
+  for (int pi = 1; pi < (int)f.parts.size(); ++pi) {
+    auto& p = f.parts[pi];
+    if (!p.full || f.cols_t.empty()) continue;
+    const int nr = (int)c->rows_of[p.r].size();
+    full_slab[pi] = shared_alloc(c, (size_t)nr * f.n, (int)f.cols_t.size());
+    f.dsts.push_back({full_slab[pi], nr, pi, 0, f.n, true});
+  }
   for (int ci = 0; ci < (int)f.cols_t.size(); ++ci) {
     const int cc = f.cols_t[ci];
     const int ncol = (int)c->cols_of[cc].size();
@@ -825,12 +885,11 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
       const int nr = (int)c->rows_of[p.r].size();
       if (p.full) {
         Block* old = find_block(c, p.r, cc);
-        if (old && old->p) c->deferred.push_back(old->p);
-        double* mem = new_block_mem(c, nr, ncol);
-        Block& b = put_block(c, p.r, cc, mem, nr, ncol);
+        if (old) release_mem(c, *old);
+        Block& b = put_block(c, p.r, cc, full_slab[pi] + (int64_t)f.woff[ci] * nr, nr, ncol,
+                             full_slab[pi]);
         b.flags.assign(nr, 2);
         b.clean = false;
-        f.dsts.push_back({mem, nr, pi, f.woff[ci], ncol, true});
       } else {
         Block* b = find_block(c, p.r, cc);
         if (!b) {
@@ -1122,180 +1181,258 @@ struct SparsifyOut {
   int done;
 };
 
-SparsifyOut do_sparsify_one(spq_ctx* c, int p, double eps) {
+// One sparsification job (an interface of a wave).
+struct SpJob {
+  int p = -1;
+  std::vector<int64_t> cols_p, rows_p;
+  int np = 0;
+  std::vector<int> us, cs, hu, wc;
+  int nu = 0, ncols = 0, kmax = 0;
+  double *M = nullptr, *Wm = nullptr, *sq = nullptr, *pay = nullptr;
+  double *V = nullptr, *tau = nullptr, *beta = nullptr, *T = nullptr;
+  int *keep = nullptr, *perm = nullptr;
+  bool cta = false;
+  int rank = -1;
+};
+
+struct SpScal { int nk; int rank; double ratio; double maxcol; };
+
+constexpr size_t CPQR_CTA_MAX_SMEM = 220 * 1024;
+
+// sparsify_interface for a WAVE of mutually independent interfaces (no
+// shared block): identical to running them one after another in order.
+void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
+                      std::vector<SparsifyOut>& outs) {
   HostTimer ht(&c->host_ms[8]);
-  SparsifyOut o{-1, 0, 0.0, 0};
-  if (!c->active[p]) throw SpqError(SPQ_ERR_BAD_INPUT, "sparsify of inactive cluster");
-  const std::vector<int64_t> cols_p = c->cols_of[p], rows_p = c->rows_of[p];
-  const int np = (int)cols_p.size();
-  o.before = np;
-  if (np == 0) return o;
-  std::vector<int> us, cs;
-  for (int u : c->cix[p]) if (u != p) us.push_back(u);
-  for (int cc : c->rix[p]) if (cc != p) cs.push_back(cc);
-  std::vector<int> hu, wc;
-  int nu = 0, ncl = 0;
-  for (int u : us) { hu.push_back(find_block(c, u, p)->nr); nu += hu.back(); }
-  for (int cc : cs) { wc.push_back(find_block(c, p, cc)->nc); ncl += wc.back(); }
-  const int ncols = nu + ncl;
-  // device buffers: M (np x ncols), W (np x ncols), V (np x kmax), misc
-  const int kmax = std::min(np, ncols);
-  const size_t Msz = (size_t)np * std::max(ncols, 1);
-  double* M = dalloc(c, Msz * sizeof(double));
-  double* Wm = dalloc(c, Msz * sizeof(double));
-  double* sq = dalloc(c, std::max(ncols, 1) * sizeof(double));
-  int* keep = (int*)dalloc(c, std::max(ncols, 1) * sizeof(int));
-  const int G = cpqr_grid(std::max(ncols, 1), c->nsm);
-  // small device scalars block
-  struct Sc { int nk; int rank; double ratio; double maxcol; };
-  Sc* dsc = (Sc*)dalloc(c, sizeof(Sc));
-  double* slots = dalloc(c, 2 * G * sizeof(double));
-  int* slotp = (int*)dalloc(c, 2 * G * sizeof(int));
-  int* perm = (int*)dalloc(c, std::max(ncols, 1) * sizeof(int));
-  // the record payload: V (np x kmax) | tau | beta | T (kmax^2)
-  const size_t vsz = (size_t)np * std::max(kmax, 1);
-  double* pay = dalloc(c, (vsz + 2 * (size_t)std::max(kmax, 1) + (size_t)kmax * kmax) * sizeof(double));
-  double* V = pay;
-  double* tau = V + vsz;
-  double* beta = tau + std::max(kmax, 1);
-  double* T = beta + std::max(kmax, 1);
+  const int nw = (int)wave.size();
+  std::vector<SpJob> J(nw);
   CopyBatch g;
-  g.zero(V, (int64_t)vsz);
-  int off = 0;
-  for (size_t t = 0; t < us.size(); ++t) {
-    Block* b = find_block(c, us[t], p);
-    CopyTask x{};
-    x.src = b->p; x.dst = M + (int64_t)off * np; x.nr = b->nr; x.nc = np; x.lds = b->nr;
-    x.ldd = np; x.trans = 1;
-    g.add(x);
-    off += b->nr;
-  }
-  for (size_t t = 0; t < cs.size(); ++t) {
-    Block* b = find_block(c, p, cs[t]);
-    CopyTask x{};
-    x.src = b->p; x.dst = M + (int64_t)off * np; x.nr = np; x.nc = b->nc; x.lds = np; x.ldd = np;
-    g.add(x);
-    off += b->nc;
+  for (int t = 0; t < nw; ++t) {
+    SpJob& j = J[t];
+    j.p = wave[t];
+    j.cols_p = c->cols_of[j.p];
+    j.rows_p = c->rows_of[j.p];
+    j.np = (int)j.cols_p.size();
+    outs[t] = SparsifyOut{-1, j.np, 0.0, 0};
+    if (j.np == 0) continue;
+    for (int u : c->cix[j.p]) if (u != j.p) j.us.push_back(u);
+    for (int cc : c->rix[j.p]) if (cc != j.p) j.cs.push_back(cc);
+    for (int u : j.us) { j.hu.push_back(find_block(c, u, j.p)->nr); j.nu += j.hu.back(); }
+    int ncl = 0;
+    for (int cc : j.cs) { j.wc.push_back(find_block(c, j.p, cc)->nc); ncl += j.wc.back(); }
+    j.ncols = j.nu + ncl;
+    j.kmax = std::min(j.np, j.ncols);
+    const size_t Msz = (size_t)j.np * std::max(j.ncols, 1);
+    j.M = dalloc(c, Msz * sizeof(double));
+    j.Wm = dalloc(c, Msz * sizeof(double));
+    j.sq = dalloc(c, std::max(j.ncols, 1) * sizeof(double));
+    j.keep = (int*)dalloc(c, std::max(j.ncols, 1) * sizeof(int));
+    j.perm = (int*)dalloc(c, std::max(j.ncols, 1) * sizeof(int));
+    const size_t vsz = (size_t)j.np * std::max(j.kmax, 1);
+    const int k1 = std::max(j.kmax, 1);
+    j.pay = dalloc(c, (vsz + 2 * (size_t)k1 + (size_t)k1 * k1) * sizeof(double));
+    j.V = j.pay;
+    j.tau = j.V + vsz;
+    j.beta = j.tau + k1;
+    j.T = j.beta + k1;
+    g.zero(j.V, (int64_t)vsz);
+    int off = 0;
+    for (size_t q = 0; q < j.us.size(); ++q) {
+      Block* b = find_block(c, j.us[q], j.p);
+      CopyTask x{};
+      x.src = b->p; x.dst = j.M + (int64_t)off * j.np; x.nr = b->nr; x.nc = j.np; x.lds = b->nr;
+      x.ldd = j.np; x.trans = 1;
+      g.add(x);
+      off += b->nr;
+    }
+    for (size_t q = 0; q < j.cs.size(); ++q) {
+      Block* b = find_block(c, j.p, j.cs[q]);
+      CopyTask x{};
+      x.src = b->p; x.dst = j.M + (int64_t)off * j.np; x.nr = j.np; x.nc = b->nc; x.lds = j.np;
+      x.ldd = j.np;
+      g.add(x);
+      off += b->nc;
+    }
+    j.cta = cpqr_cta_smem(j.np, std::max(j.ncols, 1)) <= CPQR_CTA_MAX_SMEM;
   }
   g.run(c);
+  SpScal* dsc = (SpScal*)dalloc(c, std::max(nw, 1) * sizeof(SpScal));
+  std::vector<CpqrJob> cj;
+  size_t cta_smem = 0;
   {
     Scope s(c, F_CPQR);
-    launch_sparsify_prep(M, np, ncols, eps, sq, keep, &dsc->nk, &dsc->ratio, &dsc->maxcol, Wm,
-                         c->st);
-    CpqrArgs a{};
-    a.W = Wm; a.m = np; a.ncols_cap = std::max(ncols, 1); a.nk = &dsc->nk; a.eps = &dsc->ratio;
-    a.min_rank = 0; a.V = V; a.tau = tau; a.beta = beta; a.rank = &dsc->rank; a.perm = perm;
-    a.slot_val = slots; a.slot_pos = slotp; a.finalize = 0;
-    launch_cpqr(a, G, c->st);
-    c->tm.launches[F_CPQR] += 4;
-    c->n_kernels += 4;
+    for (int t = 0; t < nw; ++t) {
+      SpJob& j = J[t];
+      if (j.np == 0) continue;
+      launch_sparsify_prep(j.M, j.np, j.ncols, eps, j.sq, j.keep, &dsc[t].nk, &dsc[t].ratio,
+                           &dsc[t].maxcol, j.Wm, c->st);
+      c->tm.launches[F_CPQR] += 3;
+      c->n_kernels += 3;
+      if (j.cta) {
+        CpqrJob q{};
+        q.W = j.Wm; q.m = j.np; q.n = j.ncols; q.ncap = std::max(j.ncols, 1); q.ldw = j.np;
+        q.nk = &dsc[t].nk; q.eps = &dsc[t].ratio; q.min_rank = 0; q.V = j.V; q.ldv = j.np;
+        q.tau = j.tau; q.beta = j.beta; q.rank = &dsc[t].rank; q.perm = j.perm; q.write_back = 0;
+        cj.push_back(q);
+        cta_smem = std::max(cta_smem, cpqr_cta_smem(j.np, std::max(j.ncols, 1)));
+      }
+    }
+    if (!cj.empty()) {
+      launch_cpqr_cta(upload(c, cj), (int)cj.size(), cta_smem, c->st);
+      c->tm.launches[F_CPQR]++;
+      c->n_kernels++;
+    }
+    for (int t = 0; t < nw; ++t) {
+      SpJob& j = J[t];
+      if (j.np == 0 || j.cta) continue;
+      const int G = cpqr_grid(std::max(j.ncols, 1), c->nsm);
+      double* slots = dalloc(c, 2 * G * sizeof(double));
+      int* slotp = (int*)dalloc(c, 2 * G * sizeof(int));
+      CpqrArgs a{};
+      a.W = j.Wm; a.m = j.np; a.ncols_cap = std::max(j.ncols, 1); a.nk = &dsc[t].nk;
+      a.eps = &dsc[t].ratio; a.min_rank = 0; a.V = j.V; a.tau = j.tau; a.beta = j.beta;
+      a.rank = &dsc[t].rank; a.perm = j.perm; a.slot_val = slots; a.slot_pos = slotp;
+      a.finalize = 0;
+      launch_cpqr(a, G, c->st);
+      c->tm.launches[F_CPQR]++;
+      c->n_kernels++;
+      dfree(c, slots);
+      dfree(c, slotp);
+    }
   }
-  Sc h{};
+  std::vector<SpScal> h(std::max(nw, 1));
   {
     HostTimer hw(&c->host_ms[9]);
-    CUDA_TRY(cudaMemcpyAsync(&h, dsc, sizeof(Sc), cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaMemcpyAsync(h.data(), dsc, nw * sizeof(SpScal), cudaMemcpyDeviceToHost, c->st));
     sync(c);
   }
-  const int r = h.rank;
-  o.rank = r;
-  {
-    const double mm = np, nn = h.nk, rr = r;
+  dfree(c, dsc);
+  // T of the accepted reflectors + Q^T M for every compressed interface
+  std::vector<TProb> tp;
+  std::vector<WyProb> wp;
+  for (int t = 0; t < nw; ++t) {
+    SpJob& j = J[t];
+    if (j.np == 0) continue;
+    j.rank = h[t].rank;
+    outs[t].rank = j.rank;
+    const double mm = j.np, nn = h[t].nk, rr = j.rank;
     c->tm.flops[F_CPQR] += 4.0 * mm * nn * rr - 2.0 * rr * rr * (mm + nn) + 4.0 * rr * rr * rr / 3.0;
+    if (j.rank >= j.np || j.rank <= 0) continue;
+    tp.push_back(TProb{j.V, j.np, j.rank, j.tau, j.T});
+    wp.push_back(WyProb{j.V, j.T, j.np, j.rank, j.M, j.np, j.ncols});
   }
-  auto release = [&]() {
-    dfree(c, M); dfree(c, Wm); dfree(c, sq); dfree(c, keep); dfree(c, dsc);
-    dfree(c, slots); dfree(c, slotp); dfree(c, perm);
-  };
-  if (r >= np) {  // factor.py:630-631
-    release();
-    dfree(c, pay);
-    return o;
-  }
-  // T of the accepted reflectors, then Q^T M
-  if (r > 0) {
-    build_full_T(c, {TProb{V, np, r, tau, T}});
-    std::vector<WyProb> wp{WyProb{V, T, np, r, M, np, ncols}};
-    wy_batch(c, wp, true);
-  }
-  // split back (factor.py:617-658)
+  build_full_T(c, tp);
+  wy_batch(c, wp, true);
+  // split back + structure, in order (factor.py:617-658)
   CopyBatch sc;
-  off = 0;
-  for (size_t t = 0; t < us.size(); ++t) {
-    const int u = us[t];
-    const int h_u = hu[t];
-    Block* old = find_block(c, u, p);
-    if (old && old->p) c->deferred.push_back(old->p);
-    if ((int64_t)h_u * r > 0) {
-      double* mem = new_block_mem(c, h_u, r);
+  for (int t = 0; t < nw; ++t) {
+    SpJob& j = J[t];
+    if (j.np == 0) continue;
+    const int p = j.p, r = j.rank, np = j.np;
+    // M is still read by the queued split-back copies: free after sc.run
+    auto release = [&]() {
+      for (void* q : {(void*)j.M, (void*)j.Wm, (void*)j.sq, (void*)j.keep, (void*)j.perm})
+        c->deferred.push_back((double*)q);
+    };
+    if (r >= np) {   // factor.py:630-631
+      release();
+      dfree(c, j.pay);
+      continue;
+    }
+    int off = 0;
+    for (size_t q = 0; q < j.us.size(); ++q) {
+      const int u = j.us[q], h_u = j.hu[q];
+      Block* old = find_block(c, u, p);
+      if (old) release_mem(c, *old);
+      if ((int64_t)h_u * r > 0) {
+        double* mem = new_block_mem(c, h_u, r);
+        CopyTask x{};
+        x.src = j.M + (int64_t)off * np; x.dst = mem; x.nr = r; x.nc = h_u; x.lds = np;
+        x.ldd = h_u; x.trans = 1;
+        sc.add(x);
+        Block& b = put_block(c, u, p, mem, h_u, r);
+        b.clean = false;
+        b.flags.clear();
+      } else {
+        drop_block(c, u, p);
+      }
+      off += h_u;
+    }
+    for (size_t q = 0; q < j.cs.size(); ++q) {
+      const int cc = j.cs[q], w = j.wc[q];
+      Block* old = find_block(c, p, cc);
+      if (old) release_mem(c, *old);
+      if ((int64_t)w * r > 0) {
+        double* mem = new_block_mem(c, r, w);
+        CopyTask x{};
+        x.src = j.M + (int64_t)off * np; x.dst = mem; x.nr = r; x.nc = w; x.lds = np; x.ldd = r;
+        sc.add(x);
+        Block& b = put_block(c, p, cc, mem, r, w);
+        b.clean = false;
+        b.flags.clear();
+      } else {
+        drop_block(c, p, cc);
+      }
+      off += w;
+    }
+    Block* dp = find_block(c, p, p);
+    if (dp) release_mem(c, *dp);
+    if (r > 0) {
+      double* mem = new_block_mem(c, r, r);
       CopyTask x{};
-      x.src = M + (int64_t)off * np; x.dst = mem; x.nr = r; x.nc = h_u; x.lds = np; x.ldd = h_u;
-      x.trans = 1;
+      x.dst = mem; x.nr = r; x.nc = r; x.ldd = r; x.ident = 1;
       sc.add(x);
-      Block& b = put_block(c, u, p, mem, h_u, r);
+      Block& b = put_block(c, p, p, mem, r, r);
       b.clean = false;
       b.flags.clear();
     } else {
-      if (old) old->p = nullptr;
-      drop_block(c, u, p);
+      drop_block(c, p, p);
+      for (int u : j.us) drop_block(c, u, p);
+      for (int cc : j.cs) drop_block(c, p, cc);
     }
-    off += h_u;
-  }
-  for (size_t t = 0; t < cs.size(); ++t) {
-    const int cc = cs[t];
-    const int w = wc[t];
-    Block* old = find_block(c, p, cc);
-    if (old && old->p) c->deferred.push_back(old->p);
-    if ((int64_t)w * r > 0) {
-      double* mem = new_block_mem(c, r, w);
-      CopyTask x{};
-      x.src = M + (int64_t)off * np; x.dst = mem; x.nr = r; x.nc = w; x.lds = np; x.ldd = r;
-      sc.add(x);
-      Block& b = put_block(c, p, cc, mem, r, w);
-      b.clean = false;
-      b.flags.clear();
-    } else {
-      if (old) old->p = nullptr;
-      drop_block(c, p, cc);
-    }
-    off += w;
-  }
-  // diagonal block: I_r or removal
-  Block* dp = find_block(c, p, p);
-  if (dp && dp->p) c->deferred.push_back(dp->p);
-  if (dp) dp->p = nullptr;
-  if (r > 0) {
-    double* mem = new_block_mem(c, r, r);
-    CopyTask x{};
-    x.dst = mem; x.nr = r; x.nc = r; x.ldd = r; x.ident = 1;
-    sc.add(x);
-    Block& b = put_block(c, p, p, mem, r, r);
-    b.clean = false;
-    b.flags.clear();
-  } else {
-    drop_block(c, p, p);
-    for (int u : us) drop_block(c, u, p);
-    for (int cc : cs) drop_block(c, p, cc);
+    Record rec;
+    rec.kind = REC_SPARSIFY;
+    rec.m = np; rec.k = r; rec.n = 0; rec.rank = r;
+    rec.rows = j.rows_p;
+    rec.cols_s = j.cols_p;
+    rec.payload = j.pay;
+    rec.V = j.V; rec.tau = j.tau; rec.T = j.T;
+    rec.payload_scalars = (int64_t)np * r + r + (int64_t)r * r;
+    for (int i = r; i < np; ++i) c->row_of_col[j.cols_p[i]] = j.rows_p[i];
+    c->rows_of[p].assign(j.rows_p.begin(), j.rows_p.begin() + r);
+    c->cols_of[p].assign(j.cols_p.begin(), j.cols_p.begin() + r);
+    c->recs.push_back(std::move(rec));
+    outs[t].done = 1;
+    outs[t].dropped = std::nan("");
+    release();   // M etc. are read by the queued copies: stream order keeps them valid
   }
   sc.run(c);
-  // record (factor.py:645-649)
-  Record rec;
-  rec.kind = REC_SPARSIFY;
-  rec.m = np; rec.k = r; rec.n = 0; rec.rank = r;
-  rec.rows = rows_p;
-  rec.cols_s = cols_p;
-  rec.payload = pay;
-  rec.V = V; rec.tau = tau; rec.T = T;
-  // V stored np x kmax (ld np): the first r columns are the panel
-  rec.payload_scalars = (int64_t)np * r + r + (int64_t)r * r;
-  for (int i = r; i < np; ++i) c->row_of_col[cols_p[i]] = rows_p[i];
-  c->rows_of[p].assign(rows_p.begin(), rows_p.begin() + r);
-  c->cols_of[p].assign(cols_p.begin(), cols_p.begin() + r);
-  c->recs.push_back(std::move(rec));
-  o.done = 1;
-  o.dropped = std::nan("");
-  release();
   flush_deferred(c);
-  return o;
+}
+
+void do_sparsify(spq_ctx* c, const std::vector<int>& ids, double eps,
+                 std::vector<SparsifyOut>& outs) {
+  outs.assign(ids.size(), SparsifyOut{-1, 0, 0.0, 0});
+  size_t pos = 0;
+  while (pos < ids.size()) {
+    std::vector<int> wave;
+    std::set<int> members;
+    while (pos < ids.size()) {
+      const int p = ids[pos];
+      if (!c->active[p]) throw SpqError(SPQ_ERR_BAD_INPUT, "sparsify of inactive cluster");
+      bool clash = false;
+      for (int q : c->cix[p]) if (q != p && members.count(q)) { clash = true; break; }
+      if (!clash)
+        for (int q : c->rix[p]) if (q != p && members.count(q)) { clash = true; break; }
+      if (clash) break;
+      wave.push_back(p);
+      members.insert(p);
+      ++pos;
+    }
+    std::vector<SparsifyOut> wo(wave.size());
+    do_sparsify_wave(c, wave, eps, wo);
+    std::copy(wo.begin(), wo.end(), outs.begin() + (pos - wave.size()));
+  }
 }
 
 // ================================================================ (d) merge
@@ -1337,28 +1474,49 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
   keys.reserve(old.size());
   for (auto& kv : old) keys.push_back(kv.first);
   std::sort(keys.begin(), keys.end());
+  // parent blocks needed, grouped by parent row: one zeroed allocation per row
+  std::map<int, std::vector<int>> prow;   // Pi -> sorted Pj
+  for (uint64_t key : keys) {
+    Block& B = old[key];
+    if ((int64_t)B.nr * B.nc == 0) continue;
+    const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
+    const int Pi = parent_of[i], Pj = parent_of[j];
+    if (Pi < 0 || Pj < 0) throw SpqError(SPQ_ERR_BAD_INPUT, "merge: block of unmerged cluster");
+    prow[Pi].push_back(Pj);
+  }
+  for (auto& kv : prow) {
+    auto& v = kv.second;
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    const int Pi = kv.first;
+    const int R = (int)c->rows_of[Pi].size();
+    size_t tot = 0;
+    for (int Pj : v) tot += (size_t)R * c->cols_of[Pj].size();
+    double* slab = shared_alloc(c, tot, (int)v.size());
+    zeros.zero(slab, (int64_t)tot);
+    size_t off = 0;
+    for (int Pj : v) {
+      const int C = (int)c->cols_of[Pj].size();
+      Block& nb = put_block(c, Pi, Pj, slab + off, R, C, slab);
+      nb.clean = false;
+      off += (size_t)R * C;
+    }
+  }
   for (uint64_t key : keys) {
     Block& B = old[key];
     const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
     if ((int64_t)B.nr * B.nc == 0) {
-      if (B.p) c->deferred.push_back(B.p);
+      release_mem(c, B);
       continue;
     }
     const int Pi = parent_of[i], Pj = parent_of[j];
-    if (Pi < 0 || Pj < 0) throw SpqError(SPQ_ERR_BAD_INPUT, "merge: block of unmerged cluster");
     Block* tgt = find_block(c, Pi, Pj);
-    const int R = (int)c->rows_of[Pi].size(), C = (int)c->cols_of[Pj].size();
-    if (!tgt) {
-      double* mem = new_block_mem(c, R, C);
-      zeros.zero(mem, (int64_t)R * C);
-      tgt = &put_block(c, Pi, Pj, mem, R, C);
-      tgt->clean = false;
-    }
+    const int R = (int)c->rows_of[Pi].size();
     CopyTask x{};
     x.src = B.p; x.dst = tgt->p + roff[i] + (int64_t)coff[j] * R; x.nr = B.nr; x.nc = B.nc;
     x.lds = B.nr; x.ldd = R;
     cp.add(x);
-    c->deferred.push_back(B.p);
+    release_mem(c, B);
   }
   zeros.run(c);
   cp.run(c);
@@ -1603,8 +1761,19 @@ int spq_create(spq_ctx** out, int device) {
     uint64_t thr = UINT64_MAX;
     CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     c->ring_cap = 64u << 20;
-    CUDA_TRY(cudaMallocHost(&c->pin, c->ring_cap));
-    CUDA_TRY(cudaMalloc(&c->dring, c->ring_cap));
+    {
+      auto& g = gcache();
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (!g.rings.empty()) {
+        c->pin = g.rings.back().first;
+        c->dring = g.rings.back().second;
+        g.rings.pop_back();
+      }
+    }
+    if (!c->pin) {
+      CUDA_TRY(cudaMallocHost(&c->pin, c->ring_cap));
+      CUDA_TRY(cudaMalloc(&c->dring, c->ring_cap));
+    }
   });
   if (rc != SPQ_OK) {
     *out = c;  // caller may query the error, then destroy
@@ -1622,9 +1791,12 @@ void spq_destroy(spq_ctx* c) {
       for (auto& e : c->tm.ev[f]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (auto e : c->marks) cudaEventDestroy(e);
-    for (void* s : c->slabs) cudaFree(s);
-    if (c->pin) cudaFreeHost(c->pin);
-    if (c->dring) cudaFree(c->dring);
+    {
+      auto& g = gcache();
+      std::lock_guard<std::mutex> lk(g.mu);
+      for (size_t i = 0; i < c->slabs.size(); ++i) g.slabs.push_back({c->slabs[i], c->slab_caps[i]});
+      if (c->pin && c->dring) g.rings.push_back({c->pin, c->dring});
+    }
     if (c->st) cudaStreamDestroy(c->st);
   } catch (...) {
   }
@@ -1664,12 +1836,13 @@ int spq_sparsify(spq_ctx* c, int n, const int32_t* ids, double eps, int32_t* out
     for (int t = 0; t < n; ++t) {
       out_rank[t] = -1; out_before[t] = 0; out_dropped[t] = 0.0; out_done[t] = 0;
     }
+    std::vector<SparsifyOut> outs;
+    do_sparsify(c, std::vector<int>(ids, ids + n), eps, outs);
     for (int t = 0; t < n; ++t) {
-      SparsifyOut o = do_sparsify_one(c, ids[t], eps);
-      out_rank[t] = o.rank;
-      out_before[t] = o.before;
-      out_dropped[t] = o.dropped;
-      out_done[t] = o.done;
+      out_rank[t] = outs[t].rank;
+      out_before[t] = outs[t].before;
+      out_dropped[t] = outs[t].dropped;
+      out_done[t] = outs[t].done;
     }
   });
 }
