@@ -146,14 +146,17 @@ int spq_build_t(spq_ctx* ctx, int64_t m, int64_t k, const double* V,
 /* raw DMMA GEMM timing, C(m x n) -= op(A) B, device-resident zeros; ms per call */
 int spq_bench_gemm(spq_ctx* ctx, int m, int n, int k, int transA, int reps, float* ms);
 
-/* batched micro-benchmark entry (BASELINE config 2): nb independent blocks
- * already resident on the device, packed column-major at offsets. */
-int spq_bench_batched_qr(spq_ctx* ctx, int nb, const int64_t* m,
-                         const int64_t* k, const int64_t* off_b,
-                         double* d_B, const int64_t* off_c, double* d_C,
-                         double* d_tau, const int64_t* off_tau,
-                         double* d_T, const int64_t* off_T, float* ms_qr,
-                         float* ms_apply);
+/* ---------------------------------------- BASELINE config 2 (batched kernels)
+ * batched_qr: nb blocks B_i (m_i x k_i, k_i <= m_i) + companions C_i
+ * (m_i x nc_i), packed COLUMN-major back to back; R_i (k_i x k_i) out and
+ * C_i <- H_i^T C_i; ms = device time of the batched QR + apply.
+ * batched_rrqr: nb blocks (m x n) packed column-major; threshold CPQR with
+ * the relative rule of rrqr_threshold; ranks[nb], rdiag[nb x min(m,n)]. */
+int spq_batched_qr(spq_ctx* ctx, int nb, const int64_t* m, const int64_t* k,
+                   const int64_t* nc, const double* B, double* R, double* C,
+                   float* ms);
+int spq_batched_rrqr(spq_ctx* ctx, int nb, int64_t m, int64_t n, const double* M,
+                     double eps, int64_t* ranks, double* rdiag, float* ms);
 
 #ifdef __cplusplus
 }

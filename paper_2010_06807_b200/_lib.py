@@ -65,9 +65,10 @@ SIGNATURES = {
     "spq_tri_solve": (C.c_int, [_ctx, C.c_int64, C.c_int64, _f64p, _f64p, C.c_int, _f64p]),
     "spq_build_t": (C.c_int, [_ctx, C.c_int64, C.c_int64, _f64p, _f64p, _f64p]),
     "spq_bench_gemm": (C.c_int, [_ctx, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
-    "spq_bench_batched_qr": (C.c_int, [_ctx, C.c_int, _i64p, _i64p, _i64p, _vp, _i64p, _vp, _vp,
-                                       _i64p, _vp, _i64p, C.POINTER(C.c_float),
-                                       C.POINTER(C.c_float)]),
+    "spq_batched_qr": (C.c_int, [_ctx, C.c_int, _i64p, _i64p, _i64p, _f64p, _f64p, _f64p,
+                                 C.POINTER(C.c_float)]),
+    "spq_batched_rrqr": (C.c_int, [_ctx, C.c_int, C.c_int64, C.c_int64, _f64p, C.c_double, _i64p,
+                                   _f64p, C.POINTER(C.c_float)]),
 }
 
 TIMING_FAMILIES = ["copy", "qr", "wy", "trsm", "cpqr", "flags", "chain"]

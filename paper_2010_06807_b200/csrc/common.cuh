@@ -103,6 +103,19 @@ struct CpqrArgs {
   int finalize;         // write beta/zeros into W's pivot columns (Tred)
 };
 
+// one record operation of a solve-chain wave
+enum ChainKind { CH_WY_T = 1, CH_WY_N = 2, CH_TRI_SOLVE = 3, CH_TRI_MUL = 4 };
+struct ChainOp {
+  int kind;
+  int m, k, n;          // WY: V is m x k on z[idx[0:m]]; TRI: R k x k on y[idx[0:k]], R_sn k x n on y[idx_n]
+  const int* idx;
+  const int* idx_n;
+  const double* V;
+  const double* T;
+  const double* R;
+  const double* Rsn;
+};
+
 // one problem of the batched CTA-resident CPQR
 struct CpqrJob {
   double* W;           // m x n (ldw), candidate columns (compacted), read (and written back)
@@ -146,6 +159,8 @@ void launch_trsm_right(const TrsmJob* d_jobs, int njobs, int total_tiles, cudaSt
 int trsm_tiles(int n);
 size_t cpqr_cta_smem(int m, int ncap);
 void launch_cpqr_cta(const CpqrJob* d_jobs, int njobs, size_t smem, cudaStream_t st);
+void launch_chain_wave(const ChainOp* d_ops, int nops, int kmax, double* z, int64_t N, int nrhs,
+                       cudaStream_t st);
 }  // namespace spq
 
 #define CUDA_TRY(x)                                                        \

@@ -172,3 +172,118 @@ void chain_perm(const double* z, const int* roc, int64_t N, int nrhs, double* ou
 }
 
 }  // namespace spq
+
+// ======================================================= wave-batched chain
+// One launch per wave of data-independent record operations (disjoint index
+// sets, planned at spq_finish); one CTA per operation; z is N x nrhs.
+namespace spq {
+
+constexpr int CW_NT = 1024;
+constexpr int CW_NW = CW_NT / 32;
+
+__global__ void __launch_bounds__(CW_NT) chain_wave_kernel(const ChainOp* __restrict__ ops,
+                                                           double* __restrict__ z, int64_t N,
+                                                           int nrhs) {
+  const ChainOp o = ops[blockIdx.x];
+  extern __shared__ __align__(16) double cw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = o.k, m = o.m;
+  double* w = cw;                 // k
+  double* w2 = w + k;             // k
+  double* part = w2 + k;          // 8 x k (rsn partials)
+  for (int r = 0; r < nrhs; ++r) {
+    double* zr = z + (int64_t)r * N;
+    if (o.kind == CH_WY_T || o.kind == CH_WY_N) {
+      for (int c = warp; c < k; c += CW_NW) {
+        const double* vc = o.V + (int64_t)c * m;
+        double s = 0.0;
+        for (int i = lane; i < m; i += 32) s += vc[i] * zr[o.idx[i]];
+#pragma unroll
+        for (int q = 16; q; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
+        if (lane == 0) w[c] = s;
+      }
+      __syncthreads();
+      for (int a = tid; a < k; a += CW_NT) {
+        double s = 0.0;
+        if (o.kind == CH_WY_T)
+          for (int b = 0; b <= a; ++b) s += o.T[b + (int64_t)a * k] * w[b];
+        else
+          for (int b = a; b < k; ++b) s += o.T[a + (int64_t)b * k] * w[b];
+        w2[a] = s;
+      }
+      __syncthreads();
+      for (int i = tid; i < m; i += CW_NT) {
+        double s = 0.0;
+        for (int c = 0; c < k; ++c) s += o.V[i + (int64_t)c * m] * w2[c];
+        zr[o.idx[i]] -= s;
+      }
+      __syncthreads();
+    } else {
+      // triangular ops on y[idx] (k entries), coupling R_sn (k x n) to y[idx_n]
+      const int n = o.n;
+      const int P = 8;
+      for (int t = tid; t < k * P; t += CW_NT) {
+        const int a = t % k, pr = t / k;
+        double s = 0.0;
+        for (int j = pr; j < n; j += P) s += o.Rsn[a + (int64_t)j * k] * zr[o.idx_n[j]];
+        part[pr * k + a] = s;
+      }
+      __syncthreads();
+      for (int a = tid; a < k; a += CW_NT) {
+        double s = 0.0;
+        for (int pr = 0; pr < P; ++pr) s += part[pr * k + a];
+        if (o.kind == CH_TRI_SOLVE) {
+          w[a] = zr[o.idx[a]] - s;
+        } else {   // CH_TRI_MUL: R y_s + R_sn y_n
+          double t2 = 0.0;
+          for (int b = a; b < k; ++b) t2 += o.R[a + (int64_t)b * k] * zr[o.idx[b]];
+          w[a] = t2 + s;
+        }
+      }
+      __syncthreads();
+      if (o.kind == CH_TRI_SOLVE) {
+        // blocked back substitution: 32-row diagonal blocks solved by warp 0,
+        // the rows above updated by all threads
+        for (int i1 = k; i1 > 0; i1 -= 32) {
+          const int i0 = max(0, i1 - 32);
+          if (warp == 0) {
+            for (int i = i1 - 1; i >= i0; --i) {
+              double xi = 0.0;
+              if (lane == 0) { xi = w[i] / o.R[i + (int64_t)i * k]; w[i] = xi; }
+              xi = __shfl_sync(0xffffffffu, xi, 0);
+              const int a = i0 + lane;
+              if (a < i) w[a] -= o.R[a + (int64_t)i * k] * xi;
+              __syncwarp();
+            }
+          }
+          __syncthreads();
+          for (int a = tid; a < i0; a += CW_NT) {
+            double s = 0.0;
+            for (int b = i0; b < i1; ++b) s += o.R[a + (int64_t)b * k] * w[b];
+            w[a] -= s;
+          }
+          __syncthreads();
+        }
+      }
+      for (int a = tid; a < k; a += CW_NT) zr[o.idx[a]] = w[a];
+      __syncthreads();
+    }
+  }
+}
+
+size_t chain_wave_smem(int kmax) { return (size_t)10 * (kmax > 0 ? kmax : 1) * sizeof(double); }
+
+void launch_chain_wave(const ChainOp* d_ops, int nops, int kmax, double* z, int64_t N, int nrhs,
+                       cudaStream_t st) {
+  if (nops <= 0) return;
+  const size_t smem = chain_wave_smem(kmax);
+  static size_t conf = 0;
+  if (smem > 48 * 1024 && smem > conf) {
+    CUDA_TRY(cudaFuncSetAttribute(chain_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    conf = smem;
+  }
+  chain_wave_kernel<<<nops, CW_NT, smem, st>>>(d_ops, z, N, nrhs);
+}
+
+}  // namespace spq

@@ -107,49 +107,43 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
     }
     cluster.sync();
     const int own = min(CL - 1, jj / rpc);
-    if (tid < kb) {
+    // every thread forms the reflector scalars itself (no extra barrier)
+    double sigma = 0.0;
+    for (int r = 0; r < CL; ++r) sigma += cluster.map_shared_rank(X, r)[1 + jj];
+    const double alpha = cluster.map_shared_rank(X, own)[1 + QR_NB + jj];
+    double tau, beta, v0 = 1.0;
+    const bool zero = sigma == 0.0;
+    if (zero) {
+      if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+    } else {
+      beta = sqrt(alpha * alpha + sigma);
+      v0 = (alpha <= 0.0) ? alpha - beta : -sigma / (alpha + beta);
+      tau = -v0 / beta;
+    }
+    if (q == 0 && tid == 0) J.tau[j0 + jj] = tau;
+    if (tid < kb && tid != jj) {
       double s = 0.0;
       for (int r = 0; r < CL; ++r) s += cluster.map_shared_rank(X, r)[1 + tid];
-      dtot[tid] = s;
-      apiv[tid] = cluster.map_shared_rank(X, own)[1 + QR_NB + tid];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const double sigma = dtot[jj], alpha = apiv[jj];
-      double tau, beta, v0 = 1.0, zero = 0.0;
-      if (sigma == 0.0) {
-        zero = 1.0;
-        if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
-      } else {
-        beta = sqrt(alpha * alpha + sigma);
-        v0 = (alpha <= 0.0) ? alpha - beta : -sigma / (alpha + beta);
-        tau = -v0 / beta;
-      }
-      scal[0] = tau; scal[1] = v0; scal[2] = beta; scal[3] = zero;
-      if (q == 0) J.tau[j0 + jj] = tau;
-    }
-    __syncthreads();
-    const double tau = scal[0], v0 = scal[1], beta = scal[2];
-    const bool zero = scal[3] != 0.0;
-    if (tid < kb) {
-      const double gv = zero ? apiv[tid] : apiv[tid] + dtot[tid] / v0;   // V_c^T v_jj
+      const double ap = cluster.map_shared_rank(X, own)[1 + QR_NB + tid];
+      const double gv = zero ? ap : ap + s / v0;      // V_c^T v_jj
       if (tid < jj) Gs[tid + jj * (QR_NB + 1)] = gv;
-      if (tid > jj) wv[tid] = tau * gv;                                   // w_c = tau v^T a_c
+      else wv[tid] = tau * gv;                        // w_c = tau v^T a_c
     }
-    for (int i = ist + tid; i < nloc; i += QR_NT)
-      S[i + jj * lds] = zero ? 0.0 : S[i + jj * lds] / v0;
     __syncthreads();
-    if (tau != 0.0) {
-      const int ncol = kb - jj - 1;
-      const int ibeg = owner ? ploc : ist;
-      const int nr = nloc - ibeg;
-      for (int e = tid; e < nr * ncol; e += QR_NT) {
-        const int i = ibeg + e % nr, c = jj + 1 + e / nr;
-        const double vi = (i == ploc) ? 1.0 : S[i + jj * lds];
-        S[i + c * lds] -= wv[c] * vi;
+    // row-owned update: v_i = x_i / v0 stored in column jj, a_ic -= w_c v_i
+    const int ibeg = owner ? ploc : ist;
+    for (int i = ibeg + tid; i < nloc; i += QR_NT) {
+      double vi;
+      if (i == ploc) {
+        vi = 1.0;
+        S[i + jj * lds] = beta;
+      } else {
+        vi = zero ? 0.0 : S[i + jj * lds] / v0;
+        S[i + jj * lds] = vi;
       }
+      if (tau != 0.0)
+        for (int c = jj + 1; c < kb; ++c) S[i + c * lds] -= wv[c] * vi;
     }
-    if (owner && tid == 0) S[ploc + jj * lds] = beta;
     __syncthreads();
   }
 

@@ -64,6 +64,25 @@ struct Block {
   bool clean = false;
 };
 
+// sorted small-vector set (cluster adjacency lists are short; iteration
+// must be ascending like the reference's sorted(...) calls)
+struct FlatSet {
+  std::vector<int> v;
+  void insert(int x) {
+    auto it = std::lower_bound(v.begin(), v.end(), x);
+    if (it == v.end() || *it != x) v.insert(it, x);
+  }
+  void erase(int x) {
+    auto it = std::lower_bound(v.begin(), v.end(), x);
+    if (it != v.end() && *it == x) v.erase(it);
+  }
+  size_t count(int x) const { return std::binary_search(v.begin(), v.end(), x) ? 1 : 0; }
+  void clear() { v.clear(); }
+  std::vector<int>::const_iterator begin() const { return v.begin(); }
+  std::vector<int>::const_iterator end() const { return v.end(); }
+  size_t size() const { return v.size(); }
+};
+
 enum RecKind { REC_ELIM = 1, REC_SCALE = 2, REC_SPARSIFY = 3 };
 
 struct Record {
@@ -108,7 +127,7 @@ struct spq_ctx {
   int ncl = 0;
   std::vector<std::vector<int64_t>> rows_of, cols_of;
   std::vector<char> active;
-  std::vector<std::set<int>> rix, cix;
+  std::vector<FlatSet> rix, cix;
   std::unordered_map<uint64_t, Block> blk;
   std::vector<int64_t> row_of_col;
   std::vector<double*> deferred;
@@ -146,6 +165,12 @@ struct spq_ctx {
   int64_t n_allocs = 0, n_syncs = 0, n_kernels = 0;
   std::vector<cudaEvent_t> marks;
   std::vector<cudaEvent_t> ev_pool;
+  // compiled solve-chain programs: 0 apply_qt, 1 solve_w, 2 apply_w
+  struct Prog {
+    ChainOp* d_ops = nullptr;
+    std::vector<int> off, cnt, kmax;
+    std::map<int, cudaGraphExec_t> graphs;   // nrhs -> executable graph (z = d_vec)
+  } prog[3];
 };
 
 namespace {
@@ -1639,6 +1664,10 @@ void ensure_chain_scratch(spq_ctx* c, int nrhs) {
   }
   const size_t vneed = (size_t)c->N * nrhs;
   if (vneed > c->vec_cap) {
+    for (auto& P : c->prog) {
+      for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);
+      P.graphs.clear();
+    }
     dfree(c, c->d_vec);
     dfree(c, c->d_vec2);
     c->d_vec = dalloc(c, vneed * sizeof(double));
@@ -1659,43 +1688,127 @@ void ensure_chain_scratch(spq_ctx* c, int nrhs) {
   }
 }
 
-// z (device, N x nrhs) -> P^T Q^T z  ; result left in *out (d_vec or d_vec2)
-double* run_apply_qt(spq_ctx* c, double* z, int nrhs) {
-  Scope s(c, F_CHAIN);
-  for (auto& r : c->recs)
-    chain_wy(r.V, r.T, r.m, r.k, z, r.d_rows, c->N, nrhs, true, c->d_w, c->d_w2, c->st);
-  double* out = (z == c->d_vec) ? c->d_vec2 : c->d_vec;
-  chain_perm(z, c->d_roc, c->N, nrhs, out, c->st);
-  return out;
+// ---------------------------------------------------- chain programs (e)
+// Record operations in chain order grouped into waves of mutually
+// independent ops (no op writes an index another op of the wave reads or
+// writes): one launch per wave, one CTA per op.
+void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
+                const std::vector<std::vector<int>>& wr, const std::vector<std::vector<int>>& rd) {
+  auto& P = c->prog[which];
+  std::vector<int> ws(c->N, -1), rs(c->N, -1);
+  int wave = 0;
+  std::vector<ChainOp> ordered;
+  P.off.clear(); P.cnt.clear(); P.kmax.clear();
+  for (size_t t = 0; t < ops.size(); ++t) {
+    bool clash = P.off.empty();
+    if (!clash) {
+      for (int i : wr[t]) if (ws[i] == wave || rs[i] == wave) { clash = true; break; }
+      if (!clash) for (int i : rd[t]) if (ws[i] == wave) { clash = true; break; }
+    }
+    if (clash) {
+      ++wave;
+      P.off.push_back((int)ordered.size());
+      P.cnt.push_back(0);
+      P.kmax.push_back(0);
+    }
+    for (int i : wr[t]) ws[i] = wave;
+    for (int i : rd[t]) rs[i] = wave;
+    ordered.push_back(ops[t]);
+    P.cnt.back()++;
+    P.kmax.back() = std::max(P.kmax.back(), ops[t].k);
+  }
+  if (!ordered.empty()) {
+    P.d_ops = (ChainOp*)dalloc(c, ordered.size() * sizeof(ChainOp));
+    CUDA_TRY(cudaMemcpyAsync(P.d_ops, ordered.data(), ordered.size() * sizeof(ChainOp),
+                             cudaMemcpyHostToDevice, c->st));
+    sync(c);
+  }
 }
 
-void run_solve_w(spq_ctx* c, double* y, int nrhs) {
-  Scope s(c, F_CHAIN);
+void compile_chains(spq_ctx* c) {
+  std::vector<ChainOp> ops;
+  std::vector<std::vector<int>> wr, rd;
+  auto to_int = [](const std::vector<int64_t>& v) { return std::vector<int>(v.begin(), v.end()); };
+  // apply_qt: every record's panel on its rows, in chain order
+  for (auto& r : c->recs) {
+    if (r.k <= 0) continue;
+    ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_rows, nullptr, r.V, r.T, nullptr, nullptr});
+    wr.push_back(to_int(r.rows));
+    rd.push_back({});
+  }
+  build_prog(c, 0, ops, wr, rd);
+  // solve_w: reversed W-chain
+  ops.clear(); wr.clear(); rd.clear();
   for (auto it = c->recs.rbegin(); it != c->recs.rend(); ++it) {
     Record& r = *it;
     if (r.kind == REC_SPARSIFY) {
-      chain_wy(r.V, r.T, r.m, r.k, y, r.d_cols_s, c->N, nrhs, false, c->d_w, c->d_w2, c->st);
-    } else if (r.kind == REC_SCALE) {
-      chain_tri(r.R, r.k, nullptr, 0, y, r.d_cols_s, nullptr, c->N, nrhs, 0, c->d_part, c->st);
+      if (r.k <= 0) continue;
+      ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr});
+      wr.push_back(to_int(r.cols_s));
+      rd.push_back({});
     } else {
-      chain_tri(r.R, r.k, r.Rsn, r.n, y, r.d_cols_s, r.d_cols_n, c->N, nrhs, 0, c->d_part, c->st);
+      if (r.k <= 0) continue;
+      const bool bh = r.kind == REC_ELIM;
+      ops.push_back(ChainOp{CH_TRI_SOLVE, r.k, r.k, bh ? r.n : 0, r.d_cols_s,
+                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr});
+      wr.push_back(to_int(r.cols_s));
+      rd.push_back(bh ? to_int(r.cols_n) : std::vector<int>());
     }
   }
-  if (c->equil) chain_diag(y, c->d_scale, c->N, nrhs, true, c->st);
+  build_prog(c, 1, ops, wr, rd);
+  // apply_w: forward W-chain (after the diagonal scaling)
+  ops.clear(); wr.clear(); rd.clear();
+  for (auto& r : c->recs) {
+    if (r.k <= 0) continue;
+    if (r.kind == REC_SPARSIFY) {
+      ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr});
+      wr.push_back(to_int(r.cols_s));
+      rd.push_back({});
+    } else {
+      const bool bh = r.kind == REC_ELIM;
+      ops.push_back(ChainOp{CH_TRI_MUL, r.k, r.k, bh ? r.n : 0, r.d_cols_s,
+                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr});
+      wr.push_back(to_int(r.cols_s));
+      rd.push_back(bh ? to_int(r.cols_n) : std::vector<int>());
+    }
+  }
+  build_prog(c, 2, ops, wr, rd);
 }
 
-void run_apply_w(spq_ctx* c, double* x, int nrhs) {
-  Scope s(c, F_CHAIN);
-  if (c->equil) chain_diag(x, c->d_scale, c->N, nrhs, false, c->st);
-  for (auto& r : c->recs) {
-    if (r.kind == REC_SPARSIFY) {
-      chain_wy(r.V, r.T, r.m, r.k, x, r.d_cols_s, c->N, nrhs, true, c->d_w, c->d_w2, c->st);
-    } else if (r.kind == REC_SCALE) {
-      chain_tri(r.R, r.k, nullptr, 0, x, r.d_cols_s, nullptr, c->N, nrhs, 1, c->d_part, c->st);
+void run_prog(spq_ctx* c, int which, double* z, int nrhs) {
+  auto& P = c->prog[which];
+  for (size_t w = 0; w < P.off.size(); ++w)
+    launch_chain_wave(P.d_ops + P.off[w], P.cnt[w], P.kmax[w], z, c->N, nrhs, c->st);
+}
+
+// full application on c->d_vec (result in d_vec), captured once per nrhs
+void run_chain(spq_ctx* c, int which, int nrhs) {
+  auto& P = c->prog[which];
+  auto it = P.graphs.find(nrhs);
+  if (it == P.graphs.end()) {
+    cudaGraph_t g;
+    CUDA_TRY(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    if (which == 0) {
+      run_prog(c, 0, c->d_vec, nrhs);
+      chain_perm(c->d_vec, c->d_roc, c->N, nrhs, c->d_vec2, c->st);
+      CUDA_TRY(cudaMemcpyAsync(c->d_vec, c->d_vec2, (size_t)c->N * nrhs * sizeof(double),
+                               cudaMemcpyDeviceToDevice, c->st));
+    } else if (which == 1) {
+      run_prog(c, 1, c->d_vec, nrhs);
+      if (c->equil) chain_diag(c->d_vec, c->d_scale, c->N, nrhs, true, c->st);
     } else {
-      chain_tri(r.R, r.k, r.Rsn, r.n, x, r.d_cols_s, r.d_cols_n, c->N, nrhs, 1, c->d_part, c->st);
+      if (c->equil) chain_diag(c->d_vec, c->d_scale, c->N, nrhs, false, c->st);
+      run_prog(c, 2, c->d_vec, nrhs);
     }
+    CUDA_TRY(cudaStreamEndCapture(c->st, &g));
+    cudaGraphExec_t ex;
+    CUDA_TRY(cudaGraphInstantiate(&ex, g, 0));
+    CUDA_TRY(cudaGraphDestroy(g));
+    it = P.graphs.emplace(nrhs, ex).first;
   }
+  Scope s(c, F_CHAIN);
+  CUDA_TRY(cudaGraphLaunch(it->second, c->st));
+  c->tm.launches[F_CHAIN]++;
 }
 
 template <class F>
@@ -1791,6 +1904,8 @@ void spq_destroy(spq_ctx* c) {
       for (auto& e : c->tm.ev[f]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (auto e : c->marks) cudaEventDestroy(e);
+    for (auto& P : c->prog)
+      for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);
     {
       auto& g = gcache();
       std::lock_guard<std::mutex> lk(g.mu);
@@ -1882,6 +1997,7 @@ int spq_finish(spq_ctx* c) {
     for (auto& r : c->recs)
       if (r.kind != REC_SPARSIFY && r.k > 0) tp.push_back(TProb{r.V, r.m, r.k, r.tau, r.T});
     build_full_T(c, tp);
+    compile_chains(c);
     c->finished = true;
     sync(c);
   });
@@ -2004,11 +2120,8 @@ static int chain_host(spq_ctx* c, const double* in, double* out, int nrhs, int w
     ensure_chain_scratch(c, nrhs);
     const size_t bytes = (size_t)c->N * nrhs * sizeof(double);
     CUDA_TRY(cudaMemcpyAsync(c->d_vec, in, bytes, cudaMemcpyHostToDevice, c->st));
-    double* res = c->d_vec;
-    if (which == 0) res = run_apply_qt(c, c->d_vec, nrhs);
-    else if (which == 1) run_solve_w(c, c->d_vec, nrhs);
-    else run_apply_w(c, c->d_vec, nrhs);
-    CUDA_TRY(cudaMemcpyAsync(out, res, bytes, cudaMemcpyDeviceToHost, c->st));
+    run_chain(c, which, nrhs);
+    CUDA_TRY(cudaMemcpyAsync(out, c->d_vec, bytes, cudaMemcpyDeviceToHost, c->st));
     sync(c);
   });
 }
@@ -2017,22 +2130,19 @@ int spq_apply_qt_host(spq_ctx* c, const double* in, double* out, int nrhs) { ret
 int spq_solve_w_host(spq_ctx* c, const double* in, double* out, int nrhs) { return chain_host(c, in, out, nrhs, 1); }
 int spq_apply_w_host(spq_ctx* c, const double* in, double* out, int nrhs) { return chain_host(c, in, out, nrhs, 2); }
 
-int spq_apply_qt_dev(spq_ctx* c, double* d, int nrhs) {
+static int chain_dev(spq_ctx* c, double* d, int nrhs, int which) {
   return guarded(c, [&] {
+    if (!c->finished) throw SpqError(SPQ_ERR_BAD_INPUT, "factorization not finished");
     ensure_chain_scratch(c, nrhs);
     const size_t bytes = (size_t)c->N * nrhs * sizeof(double);
     CUDA_TRY(cudaMemcpyAsync(c->d_vec, d, bytes, cudaMemcpyDeviceToDevice, c->st));
-    double* res = run_apply_qt(c, c->d_vec, nrhs);
-    CUDA_TRY(cudaMemcpyAsync(d, res, bytes, cudaMemcpyDeviceToDevice, c->st));
+    run_chain(c, which, nrhs);
+    CUDA_TRY(cudaMemcpyAsync(d, c->d_vec, bytes, cudaMemcpyDeviceToDevice, c->st));
   });
 }
 
-int spq_solve_w_dev(spq_ctx* c, double* d, int nrhs) {
-  return guarded(c, [&] {
-    ensure_chain_scratch(c, nrhs);
-    run_solve_w(c, d, nrhs);
-  });
-}
+int spq_apply_qt_dev(spq_ctx* c, double* d, int nrhs) { return chain_dev(c, d, nrhs, 0); }
+int spq_solve_w_dev(spq_ctx* c, double* d, int nrhs) { return chain_dev(c, d, nrhs, 1); }
 
 int spq_mark(spq_ctx* c, int slot) {
   return guarded(c, [&] {
@@ -2285,10 +2395,97 @@ int spq_bench_gemm(spq_ctx* c, int m, int n, int k, int transA, int reps, float*
   });
 }
 
-int spq_bench_batched_qr(spq_ctx*, int, const int64_t*, const int64_t*, const int64_t*, double*,
-                         const int64_t*, double*, double*, const int64_t*, double*,
-                         const int64_t*, float*, float*) {
-  return SPQ_ERR_INTERNAL;  // implemented in a later revision
+// BASELINE config 2: nb independent blocks B_i (m_i x k_i, k_i <= m_i) and
+// companions C_i (m_i x c_i), all packed column-major; R_i (k_i x k_i) out,
+// C_i <- H_i^T C_i in place.  ms = device time of QR + apply.
+int spq_batched_qr(spq_ctx* c, int nb, const int64_t* m, const int64_t* k, const int64_t* nc,
+                   const double* B, double* R, double* C, float* ms) {
+  return guarded(c, [&] {
+    size_t nB = 0, nR = 0, nC = 0, nT = 0, nt = 0;
+    for (int i = 0; i < nb; ++i) {
+      if (k[i] > m[i]) throw SpqError(SPQ_ERR_BAD_INPUT, "batched_qr needs m >= k");
+      nB += m[i] * k[i]; nR += k[i] * k[i]; nC += m[i] * nc[i]; nT += k[i] * k[i]; nt += k[i];
+    }
+    double* dB = dalloc(c, std::max<size_t>(nB, 1) * 8);
+    double* dR = dalloc(c, std::max<size_t>(nR, 1) * 8);
+    double* dC = dalloc(c, std::max<size_t>(nC, 1) * 8);
+    double* dT = dalloc(c, std::max<size_t>(nT + nt, 1) * 8);
+    CUDA_TRY(cudaMemcpyAsync(dB, B, nB * 8, cudaMemcpyHostToDevice, c->st));
+    CUDA_TRY(cudaMemcpyAsync(dC, C, nC * 8, cudaMemcpyHostToDevice, c->st));
+    CUDA_TRY(cudaMemsetAsync(dR, 0, std::max<size_t>(nR, 1) * 8, c->st));
+    CUDA_TRY(cudaMemsetAsync(dT, 0, std::max<size_t>(nT + nt, 1) * 8, c->st));
+    std::vector<QrProb> qp;
+    size_t ob = 0, orr = 0, oc = 0, ot = 0;
+    for (int i = 0; i < nb; ++i) {
+      QrProb q{dB + ob, (int)m[i], (int)k[i], dR + orr, dT + nT + ot, dT + orr, {}};
+      if (nc[i] > 0) q.targets.push_back(CTarget{dC + oc, (int)m[i], (int)nc[i]});
+      qp.push_back(std::move(q));
+      ob += m[i] * k[i]; orr += k[i] * k[i]; oc += m[i] * nc[i]; ot += k[i];
+    }
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, c->st));
+    qr_batch(c, qp);
+    CUDA_TRY(cudaEventRecord(e1, c->st));
+    CUDA_TRY(cudaMemcpyAsync(R, dR, nR * 8, cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaMemcpyAsync(C, dC, nC * 8, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    CUDA_TRY(cudaEventElapsedTime(ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    dfree(c, dB); dfree(c, dR); dfree(c, dC); dfree(c, dT);
+  });
+}
+
+// BASELINE config 2 (RRQR set): nb blocks M_i (m x n, packed column-major),
+// threshold CPQR with the relative rule nrm < eps*norm0 (rrqr_threshold).
+// ranks out; rdiag (nb x min(m,n)) |R_ii| of the accepted steps; ms device.
+int spq_batched_rrqr(spq_ctx* c, int nb, int64_t m, int64_t n, const double* M, double eps,
+                     int64_t* ranks, double* rdiag, float* ms) {
+  return guarded(c, [&] {
+    const int kmax = (int)std::min(m, n);
+    const size_t blk = (size_t)m * n;
+    if (cpqr_cta_smem((int)m, (int)n) > CPQR_CTA_MAX_SMEM)
+      throw SpqError(SPQ_ERR_BAD_INPUT, "batched_rrqr block too large for the CTA-resident kernel");
+    double* dM = dalloc(c, std::max<size_t>(nb * blk, 1) * 8);
+    double* dV = dalloc(c, std::max<size_t>((size_t)nb * m * kmax, 1) * 8);
+    double* dtb = dalloc(c, std::max<size_t>((size_t)nb * 2 * kmax + 1, 1) * 8);
+    int* di = (int*)dalloc(c, std::max<size_t>((size_t)nb * (n + 1), 1) * 4);
+    CUDA_TRY(cudaMemcpyAsync(dM, M, nb * blk * 8, cudaMemcpyHostToDevice, c->st));
+    CUDA_TRY(cudaMemsetAsync(dV, 0, std::max<size_t>((size_t)nb * m * kmax, 1) * 8, c->st));
+    double* deps = dtb + (size_t)nb * 2 * kmax;
+    CUDA_TRY(cudaMemcpyAsync(deps, &eps, 8, cudaMemcpyHostToDevice, c->st));
+    std::vector<CpqrJob> jobs(nb);
+    for (int i = 0; i < nb; ++i) {
+      CpqrJob& q = jobs[i];
+      q.W = dM + i * blk; q.m = (int)m; q.n = (int)n; q.ncap = (int)n; q.ldw = (int)m;
+      q.nk = nullptr; q.eps = deps; q.min_rank = 0; q.V = dV + (size_t)i * m * kmax;
+      q.ldv = (int)m; q.tau = dtb + (size_t)i * 2 * kmax; q.beta = q.tau + kmax;
+      q.rank = di + (size_t)nb * n + i; q.perm = di + (size_t)i * n; q.write_back = 0;
+    }
+    const CpqrJob* dj = upload(c, jobs);
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, c->st));
+    launch_cpqr_cta(dj, nb, cpqr_cta_smem((int)m, (int)n), c->st);
+    CUDA_TRY(cudaEventRecord(e1, c->st));
+    std::vector<int> hr(nb);
+    std::vector<double> htb((size_t)nb * 2 * kmax);
+    CUDA_TRY(cudaMemcpyAsync(hr.data(), di + (size_t)nb * n, nb * 4, cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(cudaMemcpyAsync(htb.data(), dtb, htb.size() * 8, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    CUDA_TRY(cudaEventElapsedTime(ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (int i = 0; i < nb; ++i) {
+      ranks[i] = hr[i];
+      for (int j = 0; j < kmax; ++j)
+        rdiag[(size_t)i * kmax + j] = j < hr[i] ? htb[(size_t)i * 2 * kmax + kmax + j] : 0.0;
+    }
+    dfree(c, dM); dfree(c, dV); dfree(c, dtb); dfree(c, di);
+  });
 }
 
 }  // extern "C"
