@@ -589,8 +589,10 @@ class BlockState:
 
 
 def factorize(A, tree, eps=1e-3, *, sparsify=True, scaling=True, skip=2,
-              sparsify_min=40, equilibrate=True):
-    """Level driver (`factor.py:771-911`), scaled mode, scale_every=1."""
+              sparsify_min=40, equilibrate=True, stop_level=None):
+    """Level driver (`factor.py:771-911`), scaled mode, scale_every=1.
+    ``stop_level`` (diagnostics): return the ranks/stats logged down to that
+    level without finishing the factorization."""
     st = BlockState(A, tree, equilibrate)
     L = tree.L
     q_chain = []
@@ -641,6 +643,8 @@ def factorize(A, tree, eps=1e-3, *, sparsify=True, scaling=True, skip=2,
         if lev >= 2:
             st.merge(lev)
         stats.append(row)
+        if stop_level is not None and lev <= stop_level:
+            return OracleFactorization(st.N, q_chain, w_chain, st.row_of_col, stats, ranks)
     if (st.row_of_col < 0).any():
         raise OracleError("columns never factored")
     q_chain.append(RecPerm(st.row_of_col))

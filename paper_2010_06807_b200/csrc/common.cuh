@@ -101,6 +101,8 @@ struct CpqrArgs {
   double* slot_val;     // [2][G]
   int* slot_pos;        // [2][G]
   int finalize;         // write beta/zeros into W's pivot columns (Tred)
+  int* gmaps;           // per-CTA position maps [G][2][ncols] when shared memory is too small
+  int force_gmaps;      // test switch: use gmaps even when shared memory would fit
 };
 
 // one record operation of a solve-chain wave
@@ -114,7 +116,9 @@ struct ChainOp {
   const double* T;
   const double* R;
   const double* Rsn;
+  double* scratch;      // 10*k doubles of global scratch when k is too big for shared memory
 };
+constexpr size_t CHAIN_SMEM_MAX = 200 * 1024;
 
 // one problem of the batched CTA-resident CPQR
 struct CpqrJob {

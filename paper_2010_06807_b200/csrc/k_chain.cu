@@ -188,9 +188,10 @@ __global__ void __launch_bounds__(CW_NT) chain_wave_kernel(const ChainOp* __rest
   extern __shared__ __align__(16) double cw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = o.k, m = o.m;
-  double* w = cw;                 // k
-  double* w2 = w + k;             // k
-  double* part = w2 + k;          // 8 x k (rsn partials)
+  // w | w2 | 8 partial rows: shared memory, or this op's global scratch
+  double* w = o.scratch ? o.scratch : cw;   // k
+  double* w2 = w + k;                       // k
+  double* part = w2 + k;                    // 8 x k (rsn partials)
   for (int r = 0; r < nrhs; ++r) {
     double* zr = z + (int64_t)r * N;
     if (o.kind == CH_WY_T || o.kind == CH_WY_N) {
@@ -271,7 +272,10 @@ __global__ void __launch_bounds__(CW_NT) chain_wave_kernel(const ChainOp* __rest
   }
 }
 
-size_t chain_wave_smem(int kmax) { return (size_t)10 * (kmax > 0 ? kmax : 1) * sizeof(double); }
+size_t chain_wave_smem(int kmax) {
+  const size_t b = (size_t)10 * (kmax > 0 ? kmax : 1) * sizeof(double);
+  return b <= CHAIN_SMEM_MAX ? b : 0;   // bigger ops carry global scratch
+}
 
 void launch_chain_wave(const ChainOp* d_ops, int nops, int kmax, double* z, int64_t N, int nrhs,
                        cudaStream_t st) {

@@ -30,6 +30,10 @@ constexpr int CP_NT = 256;
 
 
 
+__host__ __device__ __forceinline__ bool cpqr_maps_in_smem(int ncols_cap, int m) {
+  return ncols_cap >= 0 && (size_t)(2 * ncols_cap + 2) * 4 + (size_t)m * 8 + 16 <= 200 * 1024;
+}
+
 __device__ __forceinline__ bool better(double v, int pos, double bv, int bpos) {
   // strict '>' scan in position order == max value, lowest position on ties
   return v > bv || (v == bv && pos < bpos);
@@ -48,9 +52,11 @@ __global__ void __launch_bounds__(CP_NT) cpqr_kernel(CpqrArgs a) {
   const int c0 = min(nk, g * cpc), c1 = min(nk, c0 + cpc);
 
   extern __shared__ __align__(16) unsigned char smraw[];
-  int* pos_of = reinterpret_cast<int*>(smraw);          // [ncols_cap]
-  int* phys_at = pos_of + a.ncols_cap;                   // [ncols_cap]
-  double* v = reinterpret_cast<double*>(phys_at + a.ncols_cap);  // [m]; 2*ncols ints keep 8B alignment
+  const bool smaps = !a.force_gmaps && cpqr_maps_in_smem(a.ncols_cap, m);
+  int* pos_of = smaps ? reinterpret_cast<int*>(smraw)
+                      : a.gmaps + (size_t)blockIdx.x * 2 * a.ncols_cap;   // [ncols_cap]
+  int* phys_at = pos_of + a.ncols_cap;                                  // [ncols_cap]
+  double* v = reinterpret_cast<double*>(smaps ? (void*)(phys_at + a.ncols_cap) : (void*)smraw);  // [m]
   __shared__ double red_v[NW];
   __shared__ int red_p[NW];
   __shared__ double sc[4];
@@ -211,8 +217,10 @@ __global__ void __launch_bounds__(CP_NT) cpqr_kernel(CpqrArgs a) {
   }
 }
 
-size_t cpqr_smem_bytes(int ncols_cap, int m) {
-  return (size_t)(2 * ncols_cap + 2) * sizeof(int) + (size_t)m * sizeof(double) + 16;
+size_t cpqr_smem_bytes(int ncols_cap, int m, bool force_gmaps) {
+  if (!force_gmaps && cpqr_maps_in_smem(ncols_cap, m))
+    return (size_t)(2 * ncols_cap + 2) * sizeof(int) + (size_t)m * sizeof(double) + 16;
+  return (size_t)m * sizeof(double) + 16;
 }
 
 int cpqr_grid(int ncols, int nsm) {
@@ -223,7 +231,7 @@ int cpqr_grid(int ncols, int nsm) {
 }
 
 void launch_cpqr(const CpqrArgs& a, int G, cudaStream_t st) {
-  const size_t bytes = cpqr_smem_bytes(a.ncols_cap, a.m);
+  const size_t bytes = cpqr_smem_bytes(a.ncols_cap, a.m, a.force_gmaps != 0);
   static size_t configured = 0;
   if (bytes > 48 * 1024 && bytes > configured) {
     CUDA_TRY(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -258,7 +258,12 @@ __global__ void __launch_bounds__(LARFT_NT) larft_kernel(const LarftJob* __restr
       const int a = j0 + w + e % (k - j0 - w), i = e / (k - j0 - w);
       J.T[a + (int64_t)(j0 + i) * J.ldt] = 0.0;
     }
-    if (j0 > 0) {
+    if (J.Y == nullptr)   // off-diagonal blocks are filled by the GEMM doubling
+      for (int e = tid; e < j0 * w; e += LARFT_NT) {
+        const int a = e % j0, i = e / j0;
+        J.T[a + (int64_t)(j0 + i) * J.ldt] = 0.0;
+      }
+    if (j0 > 0 && J.Y != nullptr) {
       // Y[a,e] = sum_{f<=e} G[a, j0+f] T_JJ[f,e]   (a < j0)
       for (int t = tid; t < j0 * w; t += LARFT_NT) {
         const int a = t % j0, e = t / j0;

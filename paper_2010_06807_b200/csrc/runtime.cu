@@ -12,6 +12,7 @@
 // factor.py:422,454) read per-row nonzero flags computed on the device.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -93,6 +94,7 @@ struct Record {
   double *V = nullptr, *tau = nullptr, *T = nullptr, *R = nullptr, *Rsn = nullptr;
   int *d_rows = nullptr, *d_cols_s = nullptr, *d_cols_n = nullptr;
   int64_t payload_scalars = 0;
+  bool full_T = false;   // T already complete (built for a target update)
 };
 
 // families for device timing / flop accounting
@@ -158,11 +160,12 @@ struct spq_ctx {
   std::vector<void*> slabs;
   std::vector<size_t> slab_caps;
   std::unordered_map<void*, int> refcnt;   // shared block allocations
+  std::set<void*> big;                      // cudaMallocAsync allocations
   char* slab_ptr = nullptr;
   size_t slab_off = 0, slab_cap = 0, pool_bytes = 0;
   // host-side accounting: [alloc, sync-wait, plan, api]
   double host_ms[16] = {0};
-  int64_t n_allocs = 0, n_syncs = 0, n_kernels = 0;
+  int64_t n_allocs = 0, n_syncs = 0, n_kernels = 0, n_ring_overflow = 0;
   std::vector<cudaEvent_t> marks;
   std::vector<cudaEvent_t> ev_pool;
   // compiled solve-chain programs: 0 apply_qt, 1 solve_w, 2 apply_w
@@ -210,8 +213,18 @@ size_t size_class(size_t b) {
   return (c + 255) & ~(size_t)255;
 }
 
+constexpr size_t BIG_ALLOC = (size_t)8 << 20;   // >= 8 MB: driver stream-ordered pool
+
 double* dalloc(spq_ctx* c, size_t bytes) {
   auto t0 = std::chrono::steady_clock::now();
+  if (bytes >= BIG_ALLOC) {
+    void* p = nullptr;
+    CUDA_TRY(cudaMallocAsync(&p, bytes, c->st));
+    c->big.insert(p);
+    c->n_allocs++;
+    c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return (double*)p;
+  }
   const size_t cls = size_class(bytes == 0 ? 8 : bytes);
   void* p = nullptr;
   auto& fl = c->pool_free[cls];
@@ -220,7 +233,7 @@ double* dalloc(spq_ctx* c, size_t bytes) {
     fl.pop_back();
   } else {
     if (c->slab_ptr == nullptr || c->slab_off + cls > c->slab_cap) {
-      size_t cap = std::max<size_t>(cls, (size_t)512 << 20);
+      size_t cap = std::max<size_t>(cls, (size_t)128 << 20);
       void* s = nullptr;
       {
         auto& g = gcache();
@@ -251,6 +264,12 @@ double* dalloc(spq_ctx* c, size_t bytes) {
 }
 void dfree(spq_ctx* c, void* p) {
   if (!p) return;
+  auto bi = c->big.find(p);
+  if (bi != c->big.end()) {
+    CUDA_TRY(cudaFreeAsync(p, c->st));
+    c->big.erase(bi);
+    return;
+  }
   auto it = c->pool_size.find(p);
   if (it == c->pool_size.end()) throw std::runtime_error("dfree of unknown pointer");
   c->pool_free[it->second].push_back(p);
@@ -298,7 +317,15 @@ T* upload(spq_ctx* c, const T* src, size_t n) {
     c->deferred.push_back((double*)d);
     return d;
   }
-  if (c->ring_off + aligned > c->ring_cap) sync(c);
+  if (c->ring_off + aligned > c->ring_cap) {
+    // never wrap mid-sequence: later launches may still reference earlier
+    // uploads, so overflow goes to a dedicated stream-ordered buffer
+    T* d = (T*)dalloc(c, bytes);
+    CUDA_TRY(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, c->st));
+    c->deferred.push_back((double*)d);
+    c->n_ring_overflow++;
+    return d;
+  }
   std::memcpy(c->pin + c->ring_off, src, bytes);
   T* d = (T*)(c->dring + c->ring_off);
   CUDA_TRY(cudaMemcpyAsync(d, c->pin + c->ring_off, bytes, cudaMemcpyHostToDevice, c->st));
@@ -508,79 +535,6 @@ struct QrProb {
   std::vector<CTarget> targets;
 };
 
-constexpr int NB = 32;
-constexpr size_t SLAB_BYTES = 200 * 1024;
-
-void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
-  if (probs.empty()) return;
-  double qr_flops = 0, wy_flops = 0;
-  int maxk = 0;
-  for (auto& q : probs) {
-    qr_flops += 2.0 * q.m * (double)q.k * q.k - 2.0 * q.k * (double)q.k * q.k / 3.0;
-    for (auto& t : q.targets) wy_flops += 4.0 * q.m * (double)t.n * q.k - (double)t.n * q.k * q.k;
-    maxk = std::max(maxk, q.k);
-  }
-  c->tm.flops[F_QR] += qr_flops;
-  c->tm.flops[F_WY] += wy_flops;
-  for (int j0 = 0; j0 < maxk; j0 += NB) {
-    std::map<std::pair<int, int>, std::pair<std::vector<PanelJob>, int64_t>> groups;
-    size_t wtot = 0;
-    for (auto& q : probs) {
-      if (j0 >= q.k) continue;
-      const int kb = std::min(NB, q.k - j0);
-      const int mh = q.m - j0;
-      int cl = (int)(((size_t)mh * kb * 8 + SLAB_BYTES - 1) / SLAB_BYTES);
-      cl = std::max(1, cl);
-      int smem = 1;
-      if (cl > 8) { cl = 8; smem = 0; }
-      while (cl > 1 && (mh + cl - 1) / cl < 64) --cl;
-      const int rpc = (mh + cl - 1) / cl;
-      auto& grp = groups[{cl, smem}];
-      grp.first.push_back(PanelJob{q.P, q.R, q.tau, q.T, q.m, q.k, j0, kb, 1});
-      grp.second = std::max<int64_t>(grp.second, (int64_t)(rpc | 1) * kb);
-      const int j1 = j0 + kb;
-      if (j1 < q.k) wtot += 2 * (size_t)kb * (q.k - j1);
-      for (auto& t : q.targets) wtot += 2 * (size_t)kb * t.n;
-    }
-    {
-      Scope s(c, F_QR);
-      for (auto& kv : groups) {
-        launch_panel_qr(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first.first,
-                        kv.second.second, kv.first.second != 0, NB, c->st);
-        c->tm.launches[F_QR]++;
-        c->n_kernels++;
-      }
-    }
-    if (wtot == 0) continue;
-    double* Ws = dalloc(c, wtot * sizeof(double));
-    size_t off = 0;
-    GemmBatch g1, g2, g3;
-    for (auto& q : probs) {
-      if (j0 >= q.k) continue;
-      const int kb = std::min(NB, q.k - j0);
-      const int mh = q.m - j0;
-      const int j1 = j0 + kb;
-      double* Vb = q.P + j0 + (int64_t)j0 * q.m;
-      const double* Tb = q.T + j0 + (int64_t)j0 * q.k;
-      auto add = [&](double* X, int ldx, int nx) {
-        if (nx <= 0 || mh <= 0) return;
-        double* W = Ws + off;
-        double* W2 = W + (size_t)kb * nx;
-        off += 2 * (size_t)kb * nx;
-        g1.add(Vb, q.m, X, ldx, W, kb, kb, nx, mh, 1.0, 0.0);
-        g2.add(Tb, q.k, W, kb, W2, kb, kb, nx, kb, 1.0, 0.0);
-        g3.add(Vb, q.m, W2, kb, X, ldx, mh, nx, kb, -1.0, 1.0);
-      };
-      if (j1 < q.k) add(q.P + j0 + (int64_t)j1 * q.m, q.m, q.k - j1);
-      for (auto& t : q.targets) add(t.C + j0, t.ldc, t.n);
-    }
-    g1.run(c, true, 0);
-    g2.run(c, true, 0);
-    g3.run(c, false, 0);
-    dfree(c, Ws);
-  }
-}
-
 // full k x k T for a batch of (V, tau, T) triples: G = V^T V, blocked larft
 struct TProb {
   const double* V;
@@ -590,20 +544,29 @@ struct TProb {
 };
 
 void build_full_T(spq_ctx* c, const std::vector<TProb>& tp) {
+  // G = V^T V (batched DMMA), the 32x32 diagonal blocks of T by the row
+  // recurrence (one CTA per job), then recursive doubling over block pairs
+  // A=[x, x+s), B=[x+s, x+2s):  T_AB = -T_AA (G_AB T_BB)   (batched GEMMs)
   size_t gsz = 0;
-  for (auto& t : tp) gsz += (size_t)t.k * t.k + (size_t)t.k * 32;
+  int maxk = 0;
+  for (auto& t : tp) {
+    gsz += 2 * (size_t)t.k * t.k;
+    maxk = std::max(maxk, t.k);
+  }
   if (gsz == 0) return;
   double* scr = dalloc(c, gsz * sizeof(double));
   GemmBatch gg;
   std::vector<LarftJob> lj;
+  std::vector<double*> Gp(tp.size()), Yp(tp.size());
   size_t off = 0;
-  for (auto& t : tp) {
+  for (size_t i = 0; i < tp.size(); ++i) {
+    const auto& t = tp[i];
     if (t.k <= 0) continue;
-    double* G = scr + off;
-    double* Y = G + (size_t)t.k * t.k;
-    off += (size_t)t.k * t.k + (size_t)t.k * 32;
-    gg.add(t.V, t.m, t.V, t.m, G, t.k, t.k, t.k, t.m, 1.0, 0.0);
-    lj.push_back(LarftJob{G, t.tau, t.T, Y, t.k, t.k, t.k, 0});
+    Gp[i] = scr + off;
+    Yp[i] = Gp[i] + (size_t)t.k * t.k;
+    off += 2 * (size_t)t.k * t.k;
+    gg.add(t.V, t.m, t.V, t.m, Gp[i], t.k, t.k, t.k, t.m, 1.0, 0.0);
+    lj.push_back(LarftJob{Gp[i], t.tau, t.T, nullptr, t.k, t.k, t.k, 0});
   }
   gg.run(c, true, 0);
   {
@@ -611,6 +574,25 @@ void build_full_T(spq_ctx* c, const std::vector<TProb>& tp) {
     launch_larft(upload(c, lj), (int)lj.size(), 0, c->st);
     c->tm.launches[F_QR]++;
     c->n_kernels++;
+  }
+  for (int sz = 32; sz < maxk; sz *= 2) {
+    GemmBatch g1, g2;
+    for (size_t i = 0; i < tp.size(); ++i) {
+      const auto& t = tp[i];
+      for (int x = 0; x + sz < t.k; x += 2 * sz) {
+        const int na = sz, nb = std::min(sz, t.k - x - sz);
+        const int xa = x, xb = x + sz;
+        double* Y = Yp[i] + (size_t)xa;                        // na x nb, ld k
+        // Y = G[A, B] T[B, B]
+        g1.add(Gp[i] + xa + (int64_t)xb * t.k, t.k, t.T + xb + (int64_t)xb * t.k, t.k,
+               Y + (int64_t)xb * t.k, t.k, na, nb, nb, 1.0, 0.0);
+        // T[A, B] = -T[A, A] Y
+        g2.add(t.T + xa + (int64_t)xa * t.k, t.k, Y + (int64_t)xb * t.k, t.k,
+               t.T + xa + (int64_t)xb * t.k, t.k, na, nb, na, -1.0, 0.0);
+      }
+    }
+    g1.run(c, false, 0);
+    g2.run(c, false, 0);
   }
   dfree(c, scr);
 }
@@ -649,6 +631,102 @@ void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs, bool transpose, int 
   g2.run(c, transpose, 0);
   g3.run(c, false, 0);
   dfree(c, scr);
+}
+
+constexpr int NB = 32;
+
+// debug/test switch: SPQ_PANEL_GLOBAL=1 forces the L2-resident panel path
+int env_flag(const char* name) {
+  const char* e = getenv(name);
+  return (e && e[0] == '1') ? 1 : 0;
+}
+
+bool force_global_panel() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPQ_PANEL_GLOBAL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+constexpr size_t SLAB_BYTES = 200 * 1024;
+
+void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
+  if (probs.empty()) return;
+  double qr_flops = 0, wy_flops = 0;
+  int maxk = 0;
+  for (auto& q : probs) {
+    qr_flops += 2.0 * q.m * (double)q.k * q.k - 2.0 * q.k * (double)q.k * q.k / 3.0;
+    maxk = std::max(maxk, q.k);
+  }
+  c->tm.flops[F_QR] += qr_flops;
+  for (int j0 = 0; j0 < maxk; j0 += NB) {
+    std::map<std::pair<int, int>, std::pair<std::vector<PanelJob>, int64_t>> groups;
+    size_t wtot = 0;
+    for (auto& q : probs) {
+      if (j0 >= q.k) continue;
+      const int kb = std::min(NB, q.k - j0);
+      const int mh = q.m - j0;
+      int cl = (int)(((size_t)mh * kb * 8 + SLAB_BYTES - 1) / SLAB_BYTES);
+      cl = std::max(1, cl);
+      int smem = 1;
+      if (cl > 16 || force_global_panel()) { cl = std::min(cl, 16); smem = 0; }
+      while (cl > 1 && (mh + cl - 1) / cl < 64) --cl;
+      const int rpc = (mh + cl - 1) / cl;
+      auto& grp = groups[{cl, smem}];
+      grp.first.push_back(PanelJob{q.P, q.R, q.tau, q.T, q.m, q.k, j0, kb, 1});
+      grp.second = std::max<int64_t>(grp.second, (int64_t)(rpc | 1) * kb);
+      const int j1 = j0 + kb;
+      if (j1 < q.k) wtot += 2 * (size_t)kb * (q.k - j1);
+    }
+    {
+      Scope s(c, F_QR);
+      for (auto& kv : groups) {
+        launch_panel_qr(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first.first,
+                        kv.second.second, kv.first.second != 0, NB, c->st);
+        c->tm.launches[F_QR]++;
+        c->n_kernels++;
+      }
+    }
+    if (wtot == 0) continue;
+    double* Ws = dalloc(c, wtot * sizeof(double));
+    size_t off = 0;
+    GemmBatch g1, g2, g3;
+    for (auto& q : probs) {
+      if (j0 >= q.k) continue;
+      const int kb = std::min(NB, q.k - j0);
+      const int mh = q.m - j0;
+      const int j1 = j0 + kb;
+      double* Vb = q.P + j0 + (int64_t)j0 * q.m;
+      const double* Tb = q.T + j0 + (int64_t)j0 * q.k;
+      auto add = [&](double* X, int ldx, int nx) {
+        if (nx <= 0 || mh <= 0) return;
+        double* W = Ws + off;
+        double* W2 = W + (size_t)kb * nx;
+        off += 2 * (size_t)kb * nx;
+        g1.add(Vb, q.m, X, ldx, W, kb, kb, nx, mh, 1.0, 0.0);
+        g2.add(Tb, q.k, W, kb, W2, kb, kb, nx, kb, 1.0, 0.0);
+        g3.add(Vb, q.m, W2, kb, X, ldx, mh, nx, kb, -1.0, 1.0);
+      };
+      if (j1 < q.k) add(q.P + j0 + (int64_t)j1 * q.m, q.m, q.k - j1);
+    }
+    g1.run(c, true, 0);
+    g2.run(c, true, 0);
+    g3.run(c, false, 0);
+    dfree(c, Ws);
+  }
+  // targets: one pass with the full compact WY (k-deep GEMMs, C read once)
+  std::vector<TProb> tp;
+  std::vector<WyProb> wp;
+  for (auto& q : probs) {
+    if (q.k <= 0 || q.targets.empty()) continue;
+    tp.push_back(TProb{q.P, q.m, q.k, q.tau, q.T});
+    for (auto& t : q.targets) wp.push_back(WyProb{q.P, q.T, q.m, q.k, t.C, t.ldc, t.n});
+  }
+  if (!tp.empty()) {
+    build_full_T(c, tp);
+    wy_batch(c, wp, true);
+  }
 }
 
 // pivot checks for a batch; returns the first failing job (in order) or -1
@@ -1008,6 +1086,7 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
     Record& rec = c->recs[f.rec];
     QrProb q{rec.V, f.m, f.k, rec.R, rec.tau, rec.T, {}};
     if (f.n > 0) q.targets.push_back(CTarget{scr + coff[fi], f.m, f.n});
+    rec.full_T = !q.targets.empty();
     qp.push_back(std::move(q));
   }
   qr_batch(c, qp);
@@ -1136,6 +1215,7 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
         bc->clean = false;
       }
     }
+    rec.full_T = !q.targets.empty();
     qp.push_back(std::move(q));
     recid.push_back((int)c->recs.size());
     c->recs.push_back(std::move(rec));
@@ -1278,7 +1358,8 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       g.add(x);
       off += b->nc;
     }
-    j.cta = cpqr_cta_smem(j.np, std::max(j.ncols, 1)) <= CPQR_CTA_MAX_SMEM;
+    j.cta = cpqr_cta_smem(j.np, std::max(j.ncols, 1)) <= CPQR_CTA_MAX_SMEM &&
+            !env_flag("SPQ_CPQR_COOP");
   }
   g.run(c);
   SpScal* dsc = (SpScal*)dalloc(c, std::max(nw, 1) * sizeof(SpScal));
@@ -1314,6 +1395,9 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       double* slots = dalloc(c, 2 * G * sizeof(double));
       int* slotp = (int*)dalloc(c, 2 * G * sizeof(int));
       CpqrArgs a{};
+      a.gmaps = (int*)dalloc(c, (size_t)G * 2 * std::max(j.ncols, 1) * sizeof(int));
+      a.force_gmaps = env_flag("SPQ_CPQR_GMAPS");
+      c->deferred.push_back((double*)a.gmaps);
       a.W = j.Wm; a.m = j.np; a.ncols_cap = std::max(j.ncols, 1); a.nk = &dsc[t].nk;
       a.eps = &dsc[t].ratio; a.min_rank = 0; a.V = j.V; a.tau = j.tau; a.beta = j.beta;
       a.rank = &dsc[t].rank; a.perm = j.perm; a.slot_val = slots; a.slot_pos = slotp;
@@ -1717,6 +1801,25 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
     P.cnt.back()++;
     P.kmax.back() = std::max(P.kmax.back(), ops[t].k);
   }
+  // ops too large for shared memory get a private global scratch
+  size_t scr = 0;
+  for (auto& o : ordered)
+    if ((size_t)10 * o.k * sizeof(double) > CHAIN_SMEM_MAX) scr += 10 * (size_t)o.k;
+  if (scr) {
+    double* base = dalloc(c, scr * sizeof(double));
+    size_t off = 0;
+    for (auto& o : ordered)
+      if ((size_t)10 * o.k * sizeof(double) > CHAIN_SMEM_MAX) {
+        o.scratch = base + off;
+        off += 10 * (size_t)o.k;
+      }
+  }
+  for (size_t w = 0; w < P.off.size(); ++w) {
+    int km = 0;
+    for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t)
+      if (!ordered[t].scratch) km = std::max(km, ordered[t].k);
+    P.kmax[w] = km;
+  }
   if (!ordered.empty()) {
     P.d_ops = (ChainOp*)dalloc(c, ordered.size() * sizeof(ChainOp));
     CUDA_TRY(cudaMemcpyAsync(P.d_ops, ordered.data(), ordered.size() * sizeof(ChainOp),
@@ -1732,7 +1835,7 @@ void compile_chains(spq_ctx* c) {
   // apply_qt: every record's panel on its rows, in chain order
   for (auto& r : c->recs) {
     if (r.k <= 0) continue;
-    ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_rows, nullptr, r.V, r.T, nullptr, nullptr});
+    ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_rows, nullptr, r.V, r.T, nullptr, nullptr, nullptr});
     wr.push_back(to_int(r.rows));
     rd.push_back({});
   }
@@ -1743,14 +1846,14 @@ void compile_chains(spq_ctx* c) {
     Record& r = *it;
     if (r.kind == REC_SPARSIFY) {
       if (r.k <= 0) continue;
-      ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr});
+      ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr});
       wr.push_back(to_int(r.cols_s));
       rd.push_back({});
     } else {
       if (r.k <= 0) continue;
       const bool bh = r.kind == REC_ELIM;
       ops.push_back(ChainOp{CH_TRI_SOLVE, r.k, r.k, bh ? r.n : 0, r.d_cols_s,
-                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr});
+                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr});
       wr.push_back(to_int(r.cols_s));
       rd.push_back(bh ? to_int(r.cols_n) : std::vector<int>());
     }
@@ -1761,13 +1864,13 @@ void compile_chains(spq_ctx* c) {
   for (auto& r : c->recs) {
     if (r.k <= 0) continue;
     if (r.kind == REC_SPARSIFY) {
-      ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr});
+      ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr});
       wr.push_back(to_int(r.cols_s));
       rd.push_back({});
     } else {
       const bool bh = r.kind == REC_ELIM;
       ops.push_back(ChainOp{CH_TRI_MUL, r.k, r.k, bh ? r.n : 0, r.d_cols_s,
-                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr});
+                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr});
       wr.push_back(to_int(r.cols_s));
       rd.push_back(bh ? to_int(r.cols_n) : std::vector<int>());
     }
@@ -1873,11 +1976,11 @@ int spq_create(spq_ctx** out, int device) {
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    c->ring_cap = 64u << 20;
+    c->ring_cap = env_flag("SPQ_RING_SMALL") ? (1u << 16) : (64u << 20);
     {
       auto& g = gcache();
       std::lock_guard<std::mutex> lk(g.mu);
-      if (!g.rings.empty()) {
+      if (!g.rings.empty() && !env_flag("SPQ_RING_SMALL")) {
         c->pin = g.rings.back().first;
         c->dring = g.rings.back().second;
         g.rings.pop_back();
@@ -1903,6 +2006,8 @@ void spq_destroy(spq_ctx* c) {
     for (int f = 0; f < F_NFAM; ++f)
       for (auto& e : c->tm.ev[f]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (void* p : c->big) cudaFreeAsync(p, c->st);
+    if (c->st) cudaStreamSynchronize(c->st);
     for (auto e : c->marks) cudaEventDestroy(e);
     for (auto& P : c->prog)
       for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);
@@ -1995,7 +2100,7 @@ int spq_finish(spq_ctx* c) {
     }
     std::vector<TProb> tp;
     for (auto& r : c->recs)
-      if (r.kind != REC_SPARSIFY && r.k > 0) tp.push_back(TProb{r.V, r.m, r.k, r.tau, r.T});
+      if (r.kind != REC_SPARSIFY && r.k > 0 && !r.full_T) tp.push_back(TProb{r.V, r.m, r.k, r.tau, r.T});
     build_full_T(c, tp);
     compile_chains(c);
     c->finished = true;
@@ -2265,6 +2370,8 @@ int spq_rrqr(spq_ctx* c, int64_t m, int64_t k, const double* M, double eps, int6
     CUDA_TRY(cudaMemcpyAsync(deps, &eps, sizeof(double), cudaMemcpyHostToDevice, c->st));
     sync(c);
     CpqrArgs a{};
+    a.gmaps = (int*)dalloc(c, (size_t)G * 2 * std::max<int64_t>(k, 1) * sizeof(int));
+    c->deferred.push_back((double*)a.gmaps);
     a.W = W; a.m = (int)m; a.ncols_cap = (int)std::max<int64_t>(k, 1); a.nk = dnk; a.eps = deps;
     a.min_rank = (int)min_rank; a.V = dV; a.tau = dtau; a.beta = dbeta; a.rank = drank;
     a.perm = dperm; a.slot_val = slots; a.slot_pos = slotp; a.finalize = 1;
