@@ -161,6 +161,7 @@ void launch_pivot_check(const PivotJob* d_jobs, int njobs, int64_t* d_err_idx,
                         double* d_err_val, cudaStream_t st);
 void launch_trsm_right(const TrsmJob* d_jobs, int njobs, int total_tiles, cudaStream_t st);
 int trsm_tiles(int n);
+void launch_trsm_diag(const TrsmJob* d_jobs, int njobs, int total_tiles, int j0, cudaStream_t st);
 size_t cpqr_cta_smem(int m, int ncap);
 void launch_cpqr_cta(const CpqrJob* d_jobs, int njobs, size_t smem, cudaStream_t st);
 void launch_chain_wave(const ChainOp* d_ops, int nops, int kmax, double* z, int64_t N, int nrhs,

@@ -344,6 +344,36 @@ __global__ void __launch_bounds__(TRSM_NT) trsm_right_kernel(const TrsmJob* __re
 
 int trsm_tiles(int n) { return (n + TRSM_NT - 1) / TRSM_NT; }
 
+// diagonal-block step of the blocked right TRSM: columns [j0, j0+w) of
+// X R = B, the contributions of columns < j0 already subtracted (GEMM)
+__global__ void __launch_bounds__(TRSM_NT) trsm_diag_kernel(const TrsmJob* __restrict__ jobs,
+                                                           int njobs, int j0) {
+  int lo = 0, hi = njobs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].tile0 <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const TrsmJob J = jobs[lo];
+  const int row = (blockIdx.x - J.tile0) * TRSM_NT + threadIdx.x;
+  if (row >= J.n || j0 >= J.k) return;
+  const int w = min(32, J.k - j0);
+  double* B = J.B + row;
+  double x[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (j >= w) break;
+    double s = B[(int64_t)(j0 + j) * J.ldb];
+    for (int i = 0; i < j; ++i) s -= x[i] * J.R[(j0 + i) + (int64_t)(j0 + j) * J.ldr];
+    x[j] = s / J.R[(j0 + j) + (int64_t)(j0 + j) * J.ldr];
+    B[(int64_t)(j0 + j) * J.ldb] = x[j];
+  }
+}
+
+void launch_trsm_diag(const TrsmJob* d_jobs, int njobs, int total_tiles, int j0, cudaStream_t st) {
+  if (njobs <= 0 || total_tiles <= 0) return;
+  trsm_diag_kernel<<<total_tiles, TRSM_NT, 0, st>>>(d_jobs, njobs, j0);
+}
+
 void launch_trsm_right(const TrsmJob* d_jobs, int njobs, int total_tiles, cudaStream_t st) {
   if (njobs <= 0 || total_tiles <= 0) return;
   trsm_right_kernel<<<total_tiles, TRSM_NT, 0, st>>>(d_jobs, njobs);

@@ -1248,11 +1248,28 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
       }
     }
   }
-  {
-    Scope s(c, F_TRSM);
-    launch_trsm_right(upload(c, tj), (int)tj.size(), ttiles, c->st);
-    c->tm.launches[F_TRSM]++;
-    c->n_kernels++;
+  // blocked right TRSM: per 32-column block, DMMA update from the solved
+  // columns then the diagonal-block substitution (thread per row)
+  if (!tj.empty()) {
+    int kmax = 0;
+    for (auto& t : tj) kmax = std::max(kmax, t.k);
+    const TrsmJob* dj = upload(c, tj);
+    for (int j0 = 0; j0 < kmax; j0 += 32) {
+      if (j0 > 0) {
+        GemmBatch gb;
+        for (auto& t : tj) {
+          if (j0 >= t.k) continue;
+          const int w = std::min(32, t.k - j0);
+          gb.add(t.B, t.ldb, t.R + (int64_t)j0 * t.ldr, t.ldr, t.B + (int64_t)j0 * t.ldb, t.ldb,
+                 t.n, w, j0, -1.0, 1.0);
+        }
+        gb.run(c, false, 0);
+      }
+      Scope s(c, F_TRSM);
+      launch_trsm_diag(dj, (int)tj.size(), ttiles, j0, c->st);
+      c->tm.launches[F_TRSM]++;
+      c->n_kernels++;
+    }
     c->tm.flops[F_TRSM] += trsm_flops;
   }
   CopyBatch id;
