@@ -142,7 +142,7 @@ class Context:
 
     def timings(self):
         nf = len(TIMING_FAMILIES)
-        buf = np.zeros(4 * nf + 20)
+        buf = np.zeros(4 * nf + 22)
         self.call("spq_timings", buf, int(buf.size))
         out = {f: {"ms": buf[4 * i], "flops": buf[4 * i + 1], "launches": int(buf[4 * i + 2]),
                    "bytes": buf[4 * i + 3]}
@@ -154,7 +154,7 @@ class Context:
                        "flags_ms": h[8], "flags_wait_ms": h[9], "front_struct_ms": h[10],
                        "wave_exec_ms": h[11], "sparsify_ms": h[12], "sparsify_wait_ms": h[13],
                        "merge_ms": h[14], "scale_ms": h[15], "pivot_wait_ms": h[16],
-                       "stats_ms": h[17]}
+                       "stats_ms": h[17], "live_bytes": int(h[20]), "peak_bytes": int(h[21])}
         return out
 
 

@@ -164,6 +164,9 @@ int trsm_tiles(int n);
 void launch_trsm_diag(const TrsmJob* d_jobs, int njobs, int total_tiles, int j0, cudaStream_t st);
 size_t cpqr_cta_smem(int m, int ncap);
 void launch_cpqr_cta(const CpqrJob* d_jobs, int njobs, size_t smem, cudaStream_t st);
+int cpqr_cluster_size(int m, int ncap);
+size_t cpqr_cluster_smem(int m, int ncap, int cl);
+void launch_cpqr_cluster(const CpqrJob* d_jobs, int njobs, int cl, size_t smem, cudaStream_t st);
 void launch_chain_wave(const ChainOp* d_ops, int nops, int kmax, double* z, int64_t N, int nrhs,
                        cudaStream_t st);
 }  // namespace spq

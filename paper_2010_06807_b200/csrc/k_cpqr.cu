@@ -529,3 +529,255 @@ void launch_cpqr_cta(const CpqrJob* d_jobs, int njobs, size_t smem, cudaStream_t
 }
 
 }  // namespace spq
+
+// ===================================================================== cluster
+// Cluster-resident threshold CPQR: one thread-block cluster (CL <= 16 CTAs)
+// per problem; CTA q owns physical columns [q*cpc, (q+1)*cpc) of the
+// compacted candidate matrix in SHARED memory.  Per pivot step: one
+// barrier.cluster; the CL local candidates and the winning column travel
+// over DSMEM; swaps are logical (identical position maps in every CTA), so
+// ties go to the lowest current position exactly as in the reference.
+namespace spq {
+
+constexpr int CC_NT = 512;
+constexpr int CC_NW = CC_NT / 32;
+
+struct CcLayout {
+  int lds, cpc, n1, m1;
+  __host__ __device__ CcLayout(int m, int ncap, int CL)
+      : lds(m | 1), cpc((ncap + CL - 1) / CL), n1(ncap > 0 ? ncap : 1), m1(m > 0 ? m : 1) {}
+  // doubles: S (lds*cpc) | nrm (cpc) | v (m1) | part (8*cpc) | red (CC_NW) | xch (2*2)
+  // ints:    lpos (cpc) | phys (n1) | redp (CC_NW)
+  __host__ __device__ size_t doubles() const {
+    return (size_t)lds * cpc + cpc + m1 + 8 * (size_t)cpc + CC_NW + 4;
+  }
+  __host__ __device__ size_t bytes() const {
+    return doubles() * 8 + ((size_t)cpc + n1 + CC_NW) * 4 + 16;
+  }
+};
+
+__global__ void __launch_bounds__(CC_NT) cpqr_cluster_kernel(const CpqrJob* __restrict__ jobs) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int q = (int)cluster.block_rank();
+  const CpqrJob J = jobs[blockIdx.x / CL];
+  const int m = J.m;
+  const int n = J.nk ? *J.nk : J.n;
+  const double eps = *J.eps;
+  const int kmax = min(m, n);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const CcLayout L(m, J.ncap, CL);
+  const int lds = L.lds, cpc = L.cpc;
+  const int c0 = min(n, q * cpc), c1 = min(n, c0 + cpc), nloc = c1 - c0;
+  extern __shared__ __align__(16) double cs[];
+  double* S = cs;
+  double* nrm = S + (size_t)lds * cpc;
+  double* v = nrm + cpc;
+  double* part = v + L.m1;
+  double* red = part + 8 * (size_t)cpc;
+  double* xch = red + CC_NW;                   // [2][2]: best value, best position
+  int* lpos = reinterpret_cast<int*>(xch + 4);
+  int* phys = lpos + cpc;
+  int* redp = phys + L.n1;
+  __shared__ double sc[4];
+  __shared__ int si[2];
+
+  for (int e = tid; e < m * nloc; e += CC_NT) {
+    const int a = e % m, j = e / m;
+    S[a + j * lds] = J.W[a + (int64_t)(c0 + j) * J.ldw];
+  }
+  for (int j = tid; j < nloc; j += CC_NT) lpos[j] = c0 + j;
+  for (int j = tid; j < n; j += CC_NT) phys[j] = j;
+  int P = CC_NT / max(nloc, 1);
+  P = P >= 8 ? 8 : (P >= 4 ? 4 : (P >= 2 ? 2 : 1));
+  __syncthreads();
+  for (int t = tid; t < nloc * P; t += CC_NT) {
+    const int j = t % nloc, pr = t / nloc;
+    double s = 0.0;
+    for (int a = pr; a < m; a += P) s += S[a + j * lds] * S[a + j * lds];
+    part[pr * cpc + j] = s;
+  }
+  __syncthreads();
+  for (int j = tid; j < nloc; j += CC_NT) {
+    double s = 0.0;
+    for (int pr = 0; pr < P; ++pr) s += part[pr * cpc + j];
+    nrm[j] = sqrt(s);
+  }
+  __syncthreads();
+
+  // local candidate (largest norm among own columns with position >= i)
+  auto local_best = [&](int i, int parity) {
+    double bv = -1.0;
+    int bp = 0x7fffffff;
+    for (int j = tid; j < nloc; j += CC_NT)
+      if (lpos[j] >= i && better(nrm[j], lpos[j], bv, bp)) { bv = nrm[j]; bp = lpos[j]; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (better(ov, op, bv, bp)) { bv = ov; bp = op; }
+    }
+    if (lane == 0) { red[warp] = bv; redp[warp] = bp; }
+    __syncthreads();
+    if (tid == 0) {
+      double b1 = -1.0; int p1 = 0x7fffffff;
+      for (int w = 0; w < CC_NW; ++w) if (better(red[w], redp[w], b1, p1)) { b1 = red[w]; p1 = redp[w]; }
+      xch[parity * 2] = b1;
+      xch[parity * 2 + 1] = (double)p1;
+    }
+  };
+  local_best(0, 0);
+
+  double norm0 = 0.0;
+  int r = kmax;
+  for (int i = 0; i < kmax; ++i) {
+    const int par = i & 1;
+    cluster.sync();
+    // global argmax over the CL candidates (identical in every CTA)
+    if (warp == 0) {
+      double bv = -1.0;
+      int bp = 0x7fffffff;
+      if (lane < CL) {
+        const double* X = cluster.map_shared_rank(xch, lane);
+        bv = X[par * 2];
+        bp = (int)X[par * 2 + 1];
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (better(ov, op, bv, bp)) { bv = ov; bp = op; }
+      }
+      if (lane == 0) { sc[0] = bv; si[0] = bp; }
+    }
+    __syncthreads();
+    const double best = sc[0];
+    const int lp = si[0];
+    if (i == 0) {
+      norm0 = best;
+      if (norm0 == 0.0) { r = 0; break; }
+    } else if (best < eps * norm0 && i >= J.min_rank) {
+      r = i;
+      break;
+    }
+    const int pp = phys[lp], pi = phys[i];
+    const int qo = pp / cpc, jo = pp - qo * cpc;
+    // the pivot column from its owner's shared memory (rows i..m-1)
+    const double* X = cluster.map_shared_rank(S, qo) + (size_t)jo * lds;
+    double s = 0.0;
+    for (int a = i + tid; a < m; a += CC_NT) {
+      const double xa = X[a];
+      v[a] = xa;
+      if (a > i) s += xa * xa;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double sigma = 0.0;
+      for (int w = 0; w < CC_NW; ++w) sigma += red[w];
+      const double alpha = v[i];
+      double tau, beta, v0 = 1.0, zero = 0.0;
+      if (sigma == 0.0) {
+        zero = 1.0;
+        if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+      } else {
+        beta = sqrt(alpha * alpha + sigma);
+        v0 = (alpha <= 0.0) ? alpha - beta : -sigma / (alpha + beta);
+        tau = -v0 / beta;
+      }
+      sc[1] = tau; sc[2] = v0; sc[3] = zero;
+      if (q == 0) { J.tau[i] = tau; J.beta[i] = beta; }
+      // logical swap of positions i and lp (identical in every CTA)
+      phys[i] = pp;
+      phys[lp] = pi;
+      if (pp >= c0 && pp < c1) lpos[pp - c0] = i;
+      if (pi >= c0 && pi < c1 && pi != pp) lpos[pi - c0] = lp;
+    }
+    __syncthreads();
+    const double tau = sc[1], v0 = sc[2];
+    const bool zero = sc[3] != 0.0;
+    for (int a = i + tid; a < m; a += CC_NT) {
+      const double va = (a == i) ? 1.0 : (zero ? 0.0 : v[a] / v0);
+      v[a] = va;
+      if (q == 0) J.V[a + (int64_t)i * J.ldv] = va;
+    }
+    __syncthreads();
+    // update own columns with position > i, norms over rows i+1..m-1
+    if (tau != 0.0) {
+      for (int t = tid; t < nloc * P; t += CC_NT) {
+        const int j = t % nloc, pr = t / nloc;
+        if (lpos[j] <= i) continue;
+        double d = 0.0;
+        for (int a = i + pr; a < m; a += P) d += v[a] * S[a + j * lds];
+        part[pr * cpc + j] = d;
+      }
+      __syncthreads();
+      for (int t = tid; t < nloc * P; t += CC_NT) {
+        const int j = t % nloc, pr = t / nloc;
+        if (lpos[j] <= i) continue;
+        double d = 0.0;
+        for (int u = 0; u < P; ++u) d += part[u * cpc + j];
+        const double w = tau * d;
+        for (int a = i + pr; a < m; a += P) S[a + j * lds] -= w * v[a];
+      }
+      __syncthreads();
+    }
+    for (int t = tid; t < nloc * P; t += CC_NT) {
+      const int j = t % nloc, pr = t / nloc;
+      if (lpos[j] <= i) continue;
+      double ns = 0.0;
+      for (int a = i + 1 + pr; a < m; a += P) ns += S[a + j * lds] * S[a + j * lds];
+      part[pr * cpc + j] = ns;
+    }
+    __syncthreads();
+    for (int j = tid; j < nloc; j += CC_NT) {
+      if (lpos[j] <= i) continue;
+      double ns = 0.0;
+      for (int u = 0; u < P; ++u) ns += part[u * cpc + j];
+      nrm[j] = sqrt(ns);
+    }
+    __syncthreads();
+    local_best(i + 1, par ^ 1);
+  }
+  if (q == 0 && tid == 0) *J.rank = r;
+  if (q == 0)
+    for (int j = tid; j < n; j += CC_NT) J.perm[j] = phys[j];
+  cluster.sync();   // no CTA leaves while others may read its shared memory
+}
+
+int cpqr_cluster_size(int m, int ncap) {
+  for (int cl = 1; cl <= 16; cl *= 2)
+    if (CcLayout(m, ncap, cl).bytes() <= (size_t)200 * 1024) return cl;
+  return 0;
+}
+
+size_t cpqr_cluster_smem(int m, int ncap, int cl) { return CcLayout(m, ncap, cl).bytes() + 64; }
+
+void launch_cpqr_cluster(const CpqrJob* d_jobs, int njobs, int cl, size_t smem, cudaStream_t st) {
+  if (njobs <= 0) return;
+  static bool init = false;
+  if (!init) {
+    CUDA_TRY(cudaFuncSetAttribute(cpqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  220 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(cpqr_cluster_kernel,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    init = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(njobs * cl));
+  cfg.blockDim = dim3(CC_NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_cluster_kernel, d_jobs));
+}
+
+}  // namespace spq

@@ -161,6 +161,8 @@ struct spq_ctx {
   std::vector<size_t> slab_caps;
   std::unordered_map<void*, int> refcnt;   // shared block allocations
   std::set<void*> big;                      // cudaMallocAsync allocations
+  std::unordered_map<void*, size_t> big_size;
+  size_t live_bytes = 0, peak_bytes = 0;
   char* slab_ptr = nullptr;
   size_t slab_off = 0, slab_cap = 0, pool_bytes = 0;
   // host-side accounting: [alloc, sync-wait, plan, api]
@@ -221,6 +223,9 @@ double* dalloc(spq_ctx* c, size_t bytes) {
     void* p = nullptr;
     CUDA_TRY(cudaMallocAsync(&p, bytes, c->st));
     c->big.insert(p);
+    c->big_size[p] = bytes;
+    c->live_bytes += bytes;
+    c->peak_bytes = std::max(c->peak_bytes, c->live_bytes);
     c->n_allocs++;
     c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return (double*)p;
@@ -258,6 +263,8 @@ double* dalloc(spq_ctx* c, size_t bytes) {
     c->slab_off += cls;
   }
   c->pool_size[p] = cls;
+  c->live_bytes += cls;
+  c->peak_bytes = std::max(c->peak_bytes, c->live_bytes);
   c->n_allocs++;
   c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return (double*)p;
@@ -268,11 +275,14 @@ void dfree(spq_ctx* c, void* p) {
   if (bi != c->big.end()) {
     CUDA_TRY(cudaFreeAsync(p, c->st));
     c->big.erase(bi);
+    c->live_bytes -= c->big_size[p];
+    c->big_size.erase(p);
     return;
   }
   auto it = c->pool_size.find(p);
   if (it == c->pool_size.end()) throw std::runtime_error("dfree of unknown pointer");
   c->pool_free[it->second].push_back(p);
+  c->live_bytes -= it->second;
   c->pool_size.erase(it);
 }
 
@@ -1123,6 +1133,8 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
   flush_deferred(c);
 }
 
+constexpr size_t kWaveBudget = (size_t)12 << 30;   // front scratch per wave
+
 void do_factor(spq_ctx* c, const std::vector<int>& ids) {
   size_t pos = 0;
   std::vector<int> stamp(c->N, -1);
@@ -1141,6 +1153,7 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
     ++wave_id;
     std::vector<Front> wave;
     CopyBatch zeros;
+    size_t wave_bytes = 0;
     while (pos < ids.size()) {
       const int s = ids[pos];
       if (!c->active[s]) throw SpqError(SPQ_ERR_BAD_INPUT, "factor of inactive cluster " + std::to_string(s));
@@ -1158,6 +1171,10 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
       for (int64_t r : f.stack_rows)
         if (stamp[r] == wave_id) { clash = true; break; }
       if (clash) break;
+      // memory budget for the wave's front scratch (C_all) and payloads
+      const size_t fbytes = 8 * ((size_t)f.m * f.n + (size_t)f.m * f.k + (size_t)f.k * f.n);
+      if (!wave.empty() && wave_bytes + fbytes > kWaveBudget) break;
+      wave_bytes += fbytes;
       for (int64_t r : f.stack_rows) stamp[r] = wave_id;
       apply_front_structure(c, f, zeros);
       wave.push_back(std::move(f));
@@ -1314,6 +1331,7 @@ struct SpJob {
   double *V = nullptr, *tau = nullptr, *beta = nullptr, *T = nullptr;
   int *keep = nullptr, *perm = nullptr;
   bool cta = false;
+  int cl = 0;        // cluster size for the cluster-resident CPQR (0: cooperative)
   int rank = -1;
 };
 
@@ -1376,7 +1394,8 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       off += b->nc;
     }
     j.cta = cpqr_cta_smem(j.np, std::max(j.ncols, 1)) <= CPQR_CTA_MAX_SMEM &&
-            !env_flag("SPQ_CPQR_COOP");
+            !env_flag("SPQ_CPQR_COOP") && !env_flag("SPQ_CPQR_CLUSTER");
+    j.cl = (j.cta || env_flag("SPQ_CPQR_COOP")) ? 0 : cpqr_cluster_size(j.np, std::max(j.ncols, 1));
   }
   g.run(c);
   SpScal* dsc = (SpScal*)dalloc(c, std::max(nw, 1) * sizeof(SpScal));
@@ -1405,9 +1424,27 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       c->tm.launches[F_CPQR]++;
       c->n_kernels++;
     }
+    std::map<int, std::pair<std::vector<CpqrJob>, size_t>> by_cl;
     for (int t = 0; t < nw; ++t) {
       SpJob& j = J[t];
-      if (j.np == 0 || j.cta) continue;
+      if (j.np == 0 || j.cta || j.cl == 0) continue;
+      CpqrJob q{};
+      q.W = j.Wm; q.m = j.np; q.n = j.ncols; q.ncap = std::max(j.ncols, 1); q.ldw = j.np;
+      q.nk = &dsc[t].nk; q.eps = &dsc[t].ratio; q.min_rank = 0; q.V = j.V; q.ldv = j.np;
+      q.tau = j.tau; q.beta = j.beta; q.rank = &dsc[t].rank; q.perm = j.perm; q.write_back = 0;
+      auto& g2 = by_cl[j.cl];
+      g2.first.push_back(q);
+      g2.second = std::max(g2.second, cpqr_cluster_smem(j.np, std::max(j.ncols, 1), j.cl));
+    }
+    for (auto& kv : by_cl) {
+      launch_cpqr_cluster(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first,
+                          kv.second.second, c->st);
+      c->tm.launches[F_CPQR]++;
+      c->n_kernels++;
+    }
+    for (int t = 0; t < nw; ++t) {
+      SpJob& j = J[t];
+      if (j.np == 0 || j.cta || j.cl > 0) continue;
       const int G = cpqr_grid(std::max(j.ncols, 1), c->nsm);
       double* slots = dalloc(c, 2 * G * sizeof(double));
       int* slotp = (int*)dalloc(c, 2 * G * sizeof(int));
@@ -2190,6 +2227,10 @@ int spq_timings(spq_ctx* c, double* out, int n) {
                              (double)c->n_kernels};
     for (int i = 0; i < 8 && 4 * F_NFAM + i < n; ++i) out[4 * F_NFAM + i] = extra[i];
     for (int i = 4; i < 16 && 4 * F_NFAM + 8 + (i - 4) < n; ++i) out[4 * F_NFAM + 8 + (i - 4)] = c->host_ms[i];
+    if (4 * F_NFAM + 21 < n) {
+      out[4 * F_NFAM + 20] = (double)c->live_bytes;
+      out[4 * F_NFAM + 21] = (double)c->peak_bytes;
+    }
   });
 }
 

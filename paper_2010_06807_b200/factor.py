@@ -279,7 +279,7 @@ def _cluster_lists(clusters, attr):
 def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=True,
               scale_every=1, skip=2, sparsify_min=40, mode="scaled",
               row_heuristic="same-as-columns", equilibrate=True, observer=None, device=0,
-              _marks=False):
+              _marks=False, _memstats=False):
     """Run the multilevel factorization on the B200 (signature of the reference
     `factorize`, `factor.py:771-803`)."""
     if mode not in MODES:
@@ -385,6 +385,9 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
         nb, nz = C.c_int64(), C.c_int64()
         ctx.call("spq_trailing_stats", C.byref(nb), C.byref(nz))
         st["trailing_nnz"], st["trailing_blocks"] = int(nz.value), int(nb.value)
+        if _memstats:
+            h = ctx.timings()["host"]
+            st["_live_gb"], st["_peak_gb"] = h["live_bytes"] / 1e9, h["peak_bytes"] / 1e9
         on_lv = getattr(observer, "on_level", None)
         if on_lv is not None:
             on_lv(state, lev, st)
