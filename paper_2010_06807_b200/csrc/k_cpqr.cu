@@ -546,10 +546,10 @@ struct CcLayout {
   int lds, cpc, n1, m1;
   __host__ __device__ CcLayout(int m, int ncap, int CL)
       : lds(m | 1), cpc((ncap + CL - 1) / CL), n1(ncap > 0 ? ncap : 1), m1(m > 0 ? m : 1) {}
-  // doubles: S (lds*cpc) | nrm (cpc) | v (m1) | part (8*cpc) | red (CC_NW) | xch (2*2)
+  // doubles: S (lds*cpc) | x (m1) | dpart (8*cpc) | npart (8*cpc) | arow (cpc) | red (CC_NW) | xch (2*2)
   // ints:    lpos (cpc) | phys (n1) | redp (CC_NW)
   __host__ __device__ size_t doubles() const {
-    return (size_t)lds * cpc + cpc + m1 + 8 * (size_t)cpc + CC_NW + 4;
+    return (size_t)lds * cpc + m1 + 17 * (size_t)cpc + CC_NW + 4;
   }
   __host__ __device__ size_t bytes() const {
     return doubles() * 8 + ((size_t)cpc + n1 + CC_NW) * 4 + 16;
@@ -571,16 +571,15 @@ __global__ void __launch_bounds__(CC_NT) cpqr_cluster_kernel(const CpqrJob* __re
   const int c0 = min(n, q * cpc), c1 = min(n, c0 + cpc), nloc = c1 - c0;
   extern __shared__ __align__(16) double cs[];
   double* S = cs;
-  double* nrm = S + (size_t)lds * cpc;
-  double* v = nrm + cpc;
-  double* part = v + L.m1;
-  double* red = part + 8 * (size_t)cpc;
+  double* x = S + (size_t)lds * cpc;           // raw pivot column (rows i..m-1)
+  double* dpart = x + L.m1;
+  double* npart = dpart + 8 * (size_t)cpc;
+  double* arow = npart + 8 * (size_t)cpc;      // row i of the own columns, this step
+  double* red = arow + cpc;
   double* xch = red + CC_NW;                   // [2][2]: best value, best position
   int* lpos = reinterpret_cast<int*>(xch + 4);
   int* phys = lpos + cpc;
   int* redp = phys + L.n1;
-  __shared__ double sc[4];
-  __shared__ int si[2];
 
   for (int e = tid; e < m * nloc; e += CC_NT) {
     const int a = e % m, j = e / m;
@@ -591,26 +590,27 @@ __global__ void __launch_bounds__(CC_NT) cpqr_cluster_kernel(const CpqrJob* __re
   int P = CC_NT / max(nloc, 1);
   P = P >= 8 ? 8 : (P >= 4 ? 4 : (P >= 2 ? 2 : 1));
   __syncthreads();
+  // initial column norms -> local candidate
   for (int t = tid; t < nloc * P; t += CC_NT) {
     const int j = t % nloc, pr = t / nloc;
     double s = 0.0;
     for (int a = pr; a < m; a += P) s += S[a + j * lds] * S[a + j * lds];
-    part[pr * cpc + j] = s;
+    npart[pr * cpc + j] = s;
   }
   __syncthreads();
-  for (int j = tid; j < nloc; j += CC_NT) {
-    double s = 0.0;
-    for (int pr = 0; pr < P; ++pr) s += part[pr * cpc + j];
-    nrm[j] = sqrt(s);
-  }
-  __syncthreads();
-
-  // local candidate (largest norm among own columns with position >= i)
-  auto local_best = [&](int i, int parity) {
+  auto publish_best = [&](int from, int parity, int pp_over, int pi_over, int i_over, int lp_over) {
     double bv = -1.0;
     int bp = 0x7fffffff;
-    for (int j = tid; j < nloc; j += CC_NT)
-      if (lpos[j] >= i && better(nrm[j], lpos[j], bv, bp)) { bv = nrm[j]; bp = lpos[j]; }
+    for (int j = tid; j < nloc; j += CC_NT) {
+      int pj = lpos[j];
+      if (c0 + j == pp_over) pj = i_over;
+      else if (c0 + j == pi_over) pj = lp_over;
+      if (pj < from) continue;
+      double s = 0.0;
+      for (int pr = 0; pr < P; ++pr) s += npart[pr * cpc + j];
+      const double nv = sqrt(s);
+      if (better(nv, pj, bv, bp)) { bv = nv; bp = pj; }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -626,33 +626,27 @@ __global__ void __launch_bounds__(CC_NT) cpqr_cluster_kernel(const CpqrJob* __re
       xch[parity * 2 + 1] = (double)p1;
     }
   };
-  local_best(0, 0);
+  publish_best(0, 0, -1, -1, 0, 0);
 
   double norm0 = 0.0;
   int r = kmax;
   for (int i = 0; i < kmax; ++i) {
     const int par = i & 1;
     cluster.sync();
-    // global argmax over the CL candidates (identical in every CTA)
-    if (warp == 0) {
-      double bv = -1.0;
-      int bp = 0x7fffffff;
-      if (lane < CL) {
-        const double* X = cluster.map_shared_rank(xch, lane);
-        bv = X[par * 2];
-        bp = (int)X[par * 2 + 1];
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-        if (better(ov, op, bv, bp)) { bv = ov; bp = op; }
-      }
-      if (lane == 0) { sc[0] = bv; si[0] = bp; }
+    // every warp: argmax over the CL candidates (DSMEM), identical everywhere
+    double best = -1.0;
+    int lp = 0x7fffffff;
+    if (lane < CL) {
+      const double* X = cluster.map_shared_rank(xch, lane);
+      best = X[par * 2];
+      lp = (int)X[par * 2 + 1];
     }
-    __syncthreads();
-    const double best = sc[0];
-    const int lp = si[0];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, lp, o);
+      if (better(ov, op, best, lp)) { best = ov; lp = op; }
+    }
     if (i == 0) {
       norm0 = best;
       if (norm0 == 0.0) { r = 0; break; }
@@ -662,86 +656,83 @@ __global__ void __launch_bounds__(CC_NT) cpqr_cluster_kernel(const CpqrJob* __re
     }
     const int pp = phys[lp], pi = phys[i];
     const int qo = pp / cpc, jo = pp - qo * cpc;
-    // the pivot column from its owner's shared memory (rows i..m-1)
-    const double* X = cluster.map_shared_rank(S, qo) + (size_t)jo * lds;
+    // raw pivot column from its owner (DSMEM), partial sigma
+    const double* Xo = cluster.map_shared_rank(S, qo) + (size_t)jo * lds;
     double s = 0.0;
     for (int a = i + tid; a < m; a += CC_NT) {
-      const double xa = X[a];
-      v[a] = xa;
+      const double xa = Xo[a];
+      x[a] = xa;
       if (a > i) s += xa * xa;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) red[warp] = s;
-    __syncthreads();
-    if (tid == 0) {
-      double sigma = 0.0;
-      for (int w = 0; w < CC_NW; ++w) sigma += red[w];
-      const double alpha = v[i];
-      double tau, beta, v0 = 1.0, zero = 0.0;
-      if (sigma == 0.0) {
-        zero = 1.0;
-        if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
-      } else {
-        beta = sqrt(alpha * alpha + sigma);
-        v0 = (alpha <= 0.0) ? alpha - beta : -sigma / (alpha + beta);
-        tau = -v0 / beta;
-      }
-      sc[1] = tau; sc[2] = v0; sc[3] = zero;
-      if (q == 0) { J.tau[i] = tau; J.beta[i] = beta; }
-      // logical swap of positions i and lp (identical in every CTA)
+    __syncthreads();                                           // (1)
+    double sigma = 0.0;
+    for (int w = 0; w < CC_NW; ++w) sigma += red[w];
+    const double alpha = x[i];
+    double tau, beta, v0 = 1.0;
+    const bool zero = sigma == 0.0;
+    if (zero) {
+      if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+    } else {
+      beta = sqrt(alpha * alpha + sigma);
+      v0 = (alpha <= 0.0) ? alpha - beta : -sigma / (alpha + beta);
+      tau = -v0 / beta;
+    }
+    if (q == 0) {
+      for (int a = i + tid; a < m; a += CC_NT)
+        J.V[a + (int64_t)i * J.ldv] = (a == i) ? 1.0 : (zero ? 0.0 : x[a] / v0);
+      if (tid == 0) { J.tau[i] = tau; J.beta[i] = beta; }
+    }
+    // dot partials over rows > i with the raw pivot column
+    for (int t = tid; t < nloc * P; t += CC_NT) {
+      const int j = t % nloc, pr = t / nloc;
+      int pj = lpos[j];
+      if (c0 + j == pp) pj = i; else if (c0 + j == pi) pj = lp;
+      if (pj <= i) continue;
+      double d = 0.0;
+      for (int a = i + 1 + pr; a < m; a += P) d += x[a] * S[a + j * lds];
+      dpart[pr * cpc + j] = d;
+      if (pr == 0) arow[j] = S[i + j * lds];
+    }
+    __syncthreads();                                           // (2)
+    if (tid == 0) {   // logical swap of positions i and lp (identical in every CTA)
       phys[i] = pp;
       phys[lp] = pi;
       if (pp >= c0 && pp < c1) lpos[pp - c0] = i;
       if (pi >= c0 && pi < c1 && pi != pp) lpos[pi - c0] = lp;
     }
-    __syncthreads();
-    const double tau = sc[1], v0 = sc[2];
-    const bool zero = sc[3] != 0.0;
-    for (int a = i + tid; a < m; a += CC_NT) {
-      const double va = (a == i) ? 1.0 : (zero ? 0.0 : v[a] / v0);
-      v[a] = va;
-      if (q == 0) J.V[a + (int64_t)i * J.ldv] = va;
-    }
-    __syncthreads();
-    // update own columns with position > i, norms over rows i+1..m-1
-    if (tau != 0.0) {
-      for (int t = tid; t < nloc * P; t += CC_NT) {
-        const int j = t % nloc, pr = t / nloc;
-        if (lpos[j] <= i) continue;
-        double d = 0.0;
-        for (int a = i + pr; a < m; a += P) d += v[a] * S[a + j * lds];
-        part[pr * cpc + j] = d;
-      }
-      __syncthreads();
-      for (int t = tid; t < nloc * P; t += CC_NT) {
-        const int j = t % nloc, pr = t / nloc;
-        if (lpos[j] <= i) continue;
-        double d = 0.0;
-        for (int u = 0; u < P; ++u) d += part[u * cpc + j];
-        const double w = tau * d;
-        for (int a = i + pr; a < m; a += P) S[a + j * lds] -= w * v[a];
-      }
-      __syncthreads();
-    }
+    // update + norm partials over rows > i
     for (int t = tid; t < nloc * P; t += CC_NT) {
       const int j = t % nloc, pr = t / nloc;
-      if (lpos[j] <= i) continue;
+      int pj = lpos[j];
+      if (c0 + j == pp) pj = i; else if (c0 + j == pi) pj = lp;
+      if (pj <= i) continue;
+      double* col = S + j * lds;
       double ns = 0.0;
-      for (int a = i + 1 + pr; a < m; a += P) ns += S[a + j * lds] * S[a + j * lds];
-      part[pr * cpc + j] = ns;
+      if (tau != 0.0) {
+        double D = 0.0;
+        for (int u = 0; u < P; ++u) D += dpart[u * cpc + j];
+        const double aij = arow[j];
+        const double w = zero ? tau * aij : tau * (aij + D / v0);   // w = tau v^T a_j
+        const double coef = zero ? 0.0 : w / v0;                      // v_a = x_a / v0
+        if (pr == 0) col[i] = aij - w;
+        for (int a = i + 1 + pr; a < m; a += P) {
+          const double nv = col[a] - coef * x[a];
+          col[a] = nv;
+          ns += nv * nv;
+        }
+      } else {
+        for (int a = i + 1 + pr; a < m; a += P) ns += col[a] * col[a];
+      }
+      npart[pr * cpc + j] = ns;
     }
-    __syncthreads();
-    for (int j = tid; j < nloc; j += CC_NT) {
-      if (lpos[j] <= i) continue;
-      double ns = 0.0;
-      for (int u = 0; u < P; ++u) ns += part[u * cpc + j];
-      nrm[j] = sqrt(ns);
-    }
-    __syncthreads();
-    local_best(i + 1, par ^ 1);
+    __syncthreads();                                           // (3)
+    publish_best(i + 1, par ^ 1, pp, pi, i, lp);               // (4) inside
   }
   if (q == 0 && tid == 0) *J.rank = r;
+  __syncthreads();
   if (q == 0)
     for (int j = tid; j < n; j += CC_NT) J.perm[j] = phys[j];
   cluster.sync();   // no CTA leaves while others may read its shared memory
