@@ -154,7 +154,8 @@ class Context:
                        "flags_ms": h[8], "flags_wait_ms": h[9], "front_struct_ms": h[10],
                        "wave_exec_ms": h[11], "sparsify_ms": h[12], "sparsify_wait_ms": h[13],
                        "merge_ms": h[14], "scale_ms": h[15], "pivot_wait_ms": h[16],
-                       "stats_ms": h[17], "live_bytes": int(h[20]), "peak_bytes": int(h[21])}
+                       "stats_ms": h[17], "load_ms": h[18], "finish_ms": h[19],
+                       "live_bytes": int(h[20]), "peak_bytes": int(h[21])}
         return out
 
 

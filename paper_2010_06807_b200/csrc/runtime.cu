@@ -140,6 +140,7 @@ struct spq_ctx {
   int* d_roc = nullptr;
   int* d_index_pack = nullptr;
   bool finished = false;
+  bool compiled = false;
   // device error slots for pivot checks
   int64_t* d_err_idx = nullptr;
   double* d_err_val = nullptr;
@@ -920,11 +921,13 @@ bool plan_front(spq_ctx* c, int s, Front& f) {
     f.parts.push_back(std::move(p));
   }
   f.m = off;
-  // candidate trailing columns
-  std::set<int> cand;
+  // candidate trailing columns (sorted, unique)
+  std::vector<int> cand;
   for (auto& p : f.parts)
     for (int cc : c->rix[p.r])
-      if (cc != s) cand.insert(cc);
+      if (cc != s) cand.push_back(cc);
+  std::sort(cand.begin(), cand.end());
+  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
   int w = 0;
   for (int cc : cand) {
     bool present = false;
@@ -1062,6 +1065,21 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
   double* scr = tot ? dalloc(c, tot * sizeof(double)) : nullptr;
   for (size_t i = 0; i < wave.size(); ++i) zeros.zero(scr + coff[i], (int64_t)wave[i].m * wave[i].n);
   zeros.run(c);
+  // all partial row lists of the wave in ONE upload
+  std::vector<int> ixpack;
+  std::vector<std::vector<size_t>> ixoff(wave.size());
+  for (size_t fi = 0; fi < wave.size(); ++fi) {
+    Front& f = wave[fi];
+    ixoff[fi].assign(f.parts.size(), (size_t)-1);
+    for (size_t pi = 0; pi < f.parts.size(); ++pi) {
+      auto& p = f.parts[pi];
+      if (p.r != f.s && !p.full) {
+        ixoff[fi][pi] = ixpack.size();
+        ixpack.insert(ixpack.end(), p.ix.begin(), p.ix.end());
+      }
+    }
+  }
+  const int* d_ixpack = ixpack.empty() ? nullptr : upload(c, ixpack);
   // gather
   CopyBatch g;
   for (size_t fi = 0; fi < wave.size(); ++fi) {
@@ -1069,10 +1087,8 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
     Record& rec = c->recs[f.rec];
     double* C = scr + coff[fi];
     f.d_ix.assign(f.parts.size(), nullptr);
-    for (size_t pi = 0; pi < f.parts.size(); ++pi) {
-      auto& p = f.parts[pi];
-      if (p.r != f.s && !p.full) f.d_ix[pi] = upload(c, p.ix);
-    }
+    for (size_t pi = 0; pi < f.parts.size(); ++pi)
+      if (ixoff[fi][pi] != (size_t)-1) f.d_ix[pi] = d_ixpack + ixoff[fi][pi];
     for (auto& sp : f.psrc) {
       auto& p = f.parts[sp.part];
       CopyTask t{};
@@ -1940,6 +1956,10 @@ void run_prog(spq_ctx* c, int which, double* z, int nrhs) {
 
 // full application on c->d_vec (result in d_vec), captured once per nrhs
 void run_chain(spq_ctx* c, int which, int nrhs) {
+  if (!c->compiled) {   // solve programs are built on first use (not part of factorize)
+    compile_chains(c);
+    c->compiled = true;
+  }
   auto& P = c->prog[which];
   auto it = P.graphs.find(nrhs);
   if (it == P.graphs.end()) {
@@ -2091,6 +2111,7 @@ int spq_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
              const int32_t* leaf_ids, const int64_t* rows_ptr, const int64_t* rows,
              const int64_t* cols_ptr, const int64_t* cols) {
   return guarded(c, [&] {
+    HostTimer ht(&c->host_ms[14]);
     do_load(c, N, indptr, indices, data, equilibrate, n_clusters_total, n_leaf, leaf_ids,
             rows_ptr, rows, cols_ptr, cols);
   });
@@ -2128,6 +2149,7 @@ int spq_merge(spq_ctx* c, int n_parents, const int32_t* parent_ids, const int32_
 
 int spq_finish(spq_ctx* c) {
   return guarded(c, [&] {
+    HostTimer ht(&c->host_ms[15]);
     for (int64_t j = 0; j < c->N; ++j)
       if (c->row_of_col[j] < 0) {
         int64_t miss = 0;
@@ -2156,7 +2178,6 @@ int spq_finish(spq_ctx* c) {
     for (auto& r : c->recs)
       if (r.kind != REC_SPARSIFY && r.k > 0 && !r.full_T) tp.push_back(TProb{r.V, r.m, r.k, r.tau, r.T});
     build_full_T(c, tp);
-    compile_chains(c);
     c->finished = true;
     sync(c);
   });
