@@ -89,6 +89,8 @@ int spq_finish(spq_ctx* ctx);
 
 /* ------------------------------------------------------ queries / stats */
 int spq_cluster_size(spq_ctx* ctx, int id, int64_t* nrows, int64_t* ncols);
+/* |cols| of n clusters in one call */
+int spq_cluster_sizes(spq_ctx* ctx, int n, const int32_t* ids, int64_t* ncols);
 int spq_total_cols(spq_ctx* ctx, int64_t* out);
 /* trailing_blocks and trailing_nnz (exact nonzero count, device reduction) */
 int spq_trailing_stats(spq_ctx* ctx, int64_t* nblocks, int64_t* nnz);

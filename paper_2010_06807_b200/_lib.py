@@ -40,6 +40,7 @@ SIGNATURES = {
     "spq_merge": (C.c_int, [_ctx, C.c_int, _i32p, _i32p, _i32p]),
     "spq_finish": (C.c_int, [_ctx]),
     "spq_cluster_size": (C.c_int, [_ctx, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "spq_cluster_sizes": (C.c_int, [_ctx, C.c_int, _i32p, _i64p]),
     "spq_total_cols": (C.c_int, [_ctx, C.POINTER(C.c_int64)]),
     "spq_trailing_stats": (C.c_int, [_ctx, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "spq_row_of_col": (C.c_int, [_ctx, _i64p]),

@@ -105,6 +105,13 @@ struct CpqrArgs {
   int force_gmaps;      // test switch: use gmaps even when shared memory would fit
 };
 
+// sigma_max of a dropped block through its Gram G = E E^T (f x f, ld f)
+struct PowerJob {
+  const double* G;
+  int f;
+  double* out;
+};
+
 // one record operation of a solve-chain wave
 enum ChainKind { CH_WY_T = 1, CH_WY_N = 2, CH_TRI_SOLVE = 3, CH_TRI_MUL = 4 };
 struct ChainOp {
@@ -164,6 +171,7 @@ int trsm_tiles(int n);
 void launch_trsm_diag(const TrsmJob* d_jobs, int njobs, int total_tiles, int j0, cudaStream_t st);
 size_t cpqr_cta_smem(int m, int ncap);
 void launch_cpqr_cta(const CpqrJob* d_jobs, int njobs, size_t smem, cudaStream_t st);
+void launch_power_iter(const PowerJob* d_jobs, int njobs, int fmax, cudaStream_t st);
 int cpqr_cluster_size(int m, int ncap);
 size_t cpqr_cluster_smem(int m, int ncap, int cl);
 void launch_cpqr_cluster(const CpqrJob* d_jobs, int njobs, int cl, size_t smem, cudaStream_t st);

@@ -772,3 +772,70 @@ void launch_cpqr_cluster(const CpqrJob* d_jobs, int njobs, int cl, size_t smem, 
 }
 
 }  // namespace spq
+
+// ============================================================ spectral norms
+// sigma_max of dropped blocks (`spectral_norm`, kernels/__init__.py:236-241;
+// stats only, factor.py:643): power iteration on the Gram G = E E^T
+// (f x f, ld f), one CTA per matrix, Rayleigh quotient to relative 1e-14.
+namespace spq {
+
+constexpr int PI_NT = 256;
+
+__global__ void __launch_bounds__(PI_NT) power_iter_kernel(const PowerJob* __restrict__ jobs) {
+  const PowerJob J = jobs[blockIdx.x];
+  const int f = J.f, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(16) double pv[];
+  double* x = pv;          // f
+  double* y = pv + f;      // f
+  __shared__ double red[PI_NT / 32];
+  __shared__ double sc[3];
+  if (f <= 0) { if (tid == 0) *J.out = 0.0; return; }
+  for (int a = tid; a < f; a += PI_NT) x[a] = 1.0 + 0.001 * (a % 7);
+  __syncthreads();
+  double lam_prev = -1.0, lam = 0.0;
+  for (int it = 0; it < 1000; ++it) {
+    // y = G x ; lam = x^T y / x^T x ; x = y / ||y||
+    double xy = 0.0, xx = 0.0, yy = 0.0;
+    for (int a = tid; a < f; a += PI_NT) {
+      double s = 0.0;
+      for (int b = 0; b < f; ++b) s += J.G[a + (int64_t)b * f] * x[b];
+      y[a] = s;
+      xy += x[a] * s; xx += x[a] * x[a]; yy += s * s;
+    }
+    double vals[3] = {xy, xx, yy};
+    for (int t = 0; t < 3; ++t) {
+      double v = vals[t];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp] = v;
+      __syncthreads();
+      if (tid == 0) {
+        double sum = 0.0;
+        for (int w = 0; w < PI_NT / 32; ++w) sum += red[w];
+        sc[t] = sum;
+      }
+      __syncthreads();
+    }
+    lam = sc[1] > 0.0 ? sc[0] / sc[1] : 0.0;
+    const double ny = sqrt(sc[2]);
+    if (ny == 0.0) { lam = 0.0; break; }
+    for (int a = tid; a < f; a += PI_NT) x[a] = y[a] / ny;
+    __syncthreads();
+    if (fabs(lam - lam_prev) <= 1e-14 * fabs(lam)) break;
+    lam_prev = lam;
+  }
+  if (tid == 0) *J.out = sqrt(fmax(lam, 0.0));
+}
+
+void launch_power_iter(const PowerJob* d_jobs, int njobs, int fmax, cudaStream_t st) {
+  if (njobs <= 0) return;
+  const size_t smem = 2 * (size_t)(fmax > 0 ? fmax : 1) * sizeof(double);
+  static size_t conf = 0;
+  if (smem > 48 * 1024 && smem > conf) {
+    CUDA_TRY(cudaFuncSetAttribute(power_iter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    conf = smem;
+  }
+  power_iter_kernel<<<njobs, PI_NT, smem, st>>>(d_jobs);
+}
+
+}  // namespace spq

@@ -136,6 +136,7 @@ struct spq_ctx {
   // transform chain
   std::vector<Record> recs;
   double* d_scale = nullptr;
+  double* d_dropped = nullptr;
   bool equil = false;
   int* d_roc = nullptr;
   int* d_index_pack = nullptr;
@@ -1358,7 +1359,7 @@ constexpr size_t CPQR_CTA_MAX_SMEM = 220 * 1024;
 // sparsify_interface for a WAVE of mutually independent interfaces (no
 // shared block): identical to running them one after another in order.
 void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
-                      std::vector<SparsifyOut>& outs) {
+                      std::vector<SparsifyOut>& outs, int drop_base) {
   HostTimer ht(&c->host_ms[8]);
   const int nw = (int)wave.size();
   std::vector<SpJob> J(nw);
@@ -1502,6 +1503,56 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
   }
   build_full_T(c, tp);
   wy_batch(c, wp, true);
+  // dropped = max(||E1||_2, ||E2||_2), E1^T = QtM[r:, :nu], E2 = QtM[r:, nu:]
+  // (factor.py:634-643): Gram matrices by DMMA, batched power iteration
+  {
+    std::vector<size_t> eoff;
+    size_t etot = 0, gtot = 0;
+    for (int t = 0; t < nw; ++t) {
+      SpJob& j = J[t];
+      if (j.np == 0 || j.rank >= j.np || j.rank <= 0) continue;
+      const int fdim = j.np - j.rank;
+      etot += (size_t)fdim * std::max(j.ncols, 1);
+      gtot += 2 * (size_t)fdim * fdim;
+    }
+    if (gtot > 0) {
+      double* Et = dalloc(c, etot * sizeof(double));
+      double* Gs = dalloc(c, gtot * sizeof(double));
+      CopyBatch tcb;
+      GemmBatch gg;
+      std::vector<PowerJob> pj;
+      size_t eo = 0, go = 0;
+      int fmax = 0;
+      for (int t = 0; t < nw; ++t) {
+        SpJob& j = J[t];
+        if (j.np == 0 || j.rank >= j.np || j.rank <= 0) continue;
+        const int fdim = j.np - j.rank;
+        fmax = std::max(fmax, fdim);
+        double* E = Et + eo;              // E^T: ncols x fdim (ld ncols)
+        eo += (size_t)fdim * std::max(j.ncols, 1);
+        CopyTask x{};
+        x.src = j.M + j.rank; x.dst = E; x.nr = fdim; x.nc = j.ncols; x.lds = j.np;
+        x.ldd = std::max(j.ncols, 1); x.trans = 1;
+        tcb.add(x);
+        const int nu = j.nu, nc = j.ncols - j.nu;
+        double* G1 = Gs + go;
+        double* G2 = G1 + (size_t)fdim * fdim;
+        go += 2 * (size_t)fdim * fdim;
+        // G = E E^T = (E^T)^T (E^T) over the column ranges [0,nu) and [nu,ncols)
+        gg.add(E, std::max(j.ncols, 1), E, std::max(j.ncols, 1), G1, fdim, fdim, fdim, nu, 1.0, 0.0);
+        gg.add(E + nu, std::max(j.ncols, 1), E + nu, std::max(j.ncols, 1), G2, fdim, fdim, fdim,
+               nc, 1.0, 0.0);
+        pj.push_back(PowerJob{G1, fdim, c->d_dropped + 2 * (drop_base + t)});
+        pj.push_back(PowerJob{G2, fdim, c->d_dropped + 2 * (drop_base + t) + 1});
+      }
+      tcb.run(c);
+      gg.run(c, true, 0);
+      launch_power_iter(upload(c, pj), (int)pj.size(), fmax, c->st);
+      c->n_kernels++;
+      c->deferred.push_back(Et);
+      c->deferred.push_back(Gs);
+    }
+  }
   // split back + structure, in order (factor.py:617-658)
   CopyBatch sc;
   for (int t = 0; t < nw; ++t) {
@@ -1582,7 +1633,6 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     c->cols_of[p].assign(j.cols_p.begin(), j.cols_p.begin() + r);
     c->recs.push_back(std::move(rec));
     outs[t].done = 1;
-    outs[t].dropped = std::nan("");
     release();   // M etc. are read by the queued copies: stream order keeps them valid
   }
   sc.run(c);
@@ -1592,6 +1642,8 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
 void do_sparsify(spq_ctx* c, const std::vector<int>& ids, double eps,
                  std::vector<SparsifyOut>& outs) {
   outs.assign(ids.size(), SparsifyOut{-1, 0, 0.0, 0});
+  c->d_dropped = dalloc(c, 2 * std::max<size_t>(ids.size(), 1) * sizeof(double));
+  CUDA_TRY(cudaMemsetAsync(c->d_dropped, 0, 2 * std::max<size_t>(ids.size(), 1) * sizeof(double), c->st));
   size_t pos = 0;
   while (pos < ids.size()) {
     std::vector<int> wave;
@@ -1609,9 +1661,17 @@ void do_sparsify(spq_ctx* c, const std::vector<int>& ids, double eps,
       ++pos;
     }
     std::vector<SparsifyOut> wo(wave.size());
-    do_sparsify_wave(c, wave, eps, wo);
+    do_sparsify_wave(c, wave, eps, wo, (int)(pos - wave.size()));
     std::copy(wo.begin(), wo.end(), outs.begin() + (pos - wave.size()));
   }
+  // dropped norms of all compressed interfaces: one read at the end
+  std::vector<double> hd(2 * ids.size());
+  CUDA_TRY(cudaMemcpyAsync(hd.data(), c->d_dropped, hd.size() * 8, cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  for (size_t t = 0; t < ids.size(); ++t)
+    if (outs[t].done) outs[t].dropped = std::max(hd[2 * t], hd[2 * t + 1]);
+  dfree(c, c->d_dropped);
+  c->d_dropped = nullptr;
 }
 
 // ================================================================ (d) merge
@@ -1654,20 +1714,25 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
   for (auto& kv : old) keys.push_back(kv.first);
   std::sort(keys.begin(), keys.end());
   // parent blocks needed, grouped by parent row: one zeroed allocation per row
-  std::map<int, std::vector<int>> prow;   // Pi -> sorted Pj
+  std::vector<std::vector<int>> prow_v(c->ncl);   // Pi -> Pj list
   for (uint64_t key : keys) {
     Block& B = old[key];
     if ((int64_t)B.nr * B.nc == 0) continue;
     const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
     const int Pi = parent_of[i], Pj = parent_of[j];
     if (Pi < 0 || Pj < 0) throw SpqError(SPQ_ERR_BAD_INPUT, "merge: block of unmerged cluster");
-    prow[Pi].push_back(Pj);
+    prow_v[Pi].push_back(Pj);
   }
-  for (auto& kv : prow) {
-    auto& v = kv.second;
+  size_t nparent_blocks = 0;
+  for (auto& v : prow_v) {
     std::sort(v.begin(), v.end());
     v.erase(std::unique(v.begin(), v.end()), v.end());
-    const int Pi = kv.first;
+    nparent_blocks += v.size();
+  }
+  c->blk.reserve(nparent_blocks * 2 + 16);
+  for (int Pi = 0; Pi < c->ncl; ++Pi) {
+    auto& v = prow_v[Pi];
+    if (v.empty()) continue;
     const int R = (int)c->rows_of[Pi].size();
     size_t tot = 0;
     for (int Pj : v) tot += (size_t)R * c->cols_of[Pj].size();
@@ -2188,6 +2253,15 @@ int spq_cluster_size(spq_ctx* c, int id, int64_t* nr, int64_t* nc) {
     if (id < 0 || id >= c->ncl) throw SpqError(SPQ_ERR_BAD_INPUT, "cluster id out of range");
     *nr = (int64_t)c->rows_of[id].size();
     *nc = (int64_t)c->cols_of[id].size();
+  });
+}
+
+int spq_cluster_sizes(spq_ctx* c, int n, const int32_t* ids, int64_t* ncols) {
+  return guarded(c, [&] {
+    for (int t = 0; t < n; ++t) {
+      if (ids[t] < 0 || ids[t] >= c->ncl) throw SpqError(SPQ_ERR_BAD_INPUT, "cluster id out of range");
+      ncols[t] = (int64_t)c->cols_of[ids[t]].size();
+    }
   });
 }
 

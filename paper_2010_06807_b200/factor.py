@@ -317,6 +317,13 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
         ctx.call("spq_cluster_size", int(cid), C.byref(r), C.byref(c))
         return int(c.value)
 
+    def sizes_of(ids):
+        ids = np.asarray(ids, np.int32)
+        out = np.zeros(len(ids), np.int64)
+        if len(ids):
+            ctx.call("spq_cluster_sizes", len(ids), ids, out)
+        return out
+
     state = _StateView(ctx)
     stats = []
     ranks_log = []
@@ -334,7 +341,7 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
               "t_factor": 0.0, "t_scale": 0.0, "t_sparsify": 0.0, "t_merge": 0.0}
         t0 = time.perf_counter()
         ids = by_level[lev]
-        st["factored_cols"] = sum(size_of(s) for s in ids)
+        st["factored_cols"] = int(sizes_of(ids).sum())
         if ids:
             ctx.call("spq_factor", len(ids), np.asarray(ids, np.int32))
         st["n_factored"] = len(ids)
@@ -343,7 +350,8 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
         run_sparsify = sparsify and (L - lev + 1) > skip and lev >= 2 and pending[lev]
         if run_sparsify:
             n_sparsified_levels += 1
-            todo = [p for p in pending[lev] if size_of(p) >= sparsify_min]
+            psz = sizes_of(pending[lev])
+            todo = [p for p, z in zip(pending[lev], psz) if z >= sparsify_min]
             if todo:
                 ids_t = np.asarray(todo, np.int32)
                 t0 = time.perf_counter()
@@ -376,7 +384,7 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
                 st["t_sparsify"] = time.perf_counter() - t0
                 ranks_log.extend((lev, int(p), int(b), int(r)) for p, b, r in zip(todo, before, rank))
 
-        sizes = [size_of(p) for p in pending[lev]]
+        sizes = [int(z) for z in sizes_of(pending[lev])]
         if sizes:
             q1, q2, q3 = np.percentile(sizes, [25, 50, 75])
             st["iface_q1"], st["iface_q2"], st["iface_q3"] = float(q1), float(q2), float(q3)

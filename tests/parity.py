@@ -7,6 +7,8 @@
 * diag(R_ss) of every elimination record within max(1e-10, 10 x the
   reference's own numba-vs-numpy envelope for that record) relative to the
   block's max |R| — levels near the root accumulate rounding (F3);
+* dropped_max (largest spectral norm of the discarded blocks) within 1e-5
+  relative (power iteration on the device vs the reference's LAPACK SVD);
 * GMRES iteration count within +-1 and final residual within 10x.
 """
 
@@ -46,6 +48,9 @@ def compare_structure(stats, log, row_of_col, g):
             a, b = float(st[k]), float(ref[li, keys.index(k)])
             if a != b:
                 problems.append(f"level {st['level']} {k}: ours {a} ref {b}")
+        a, b = float(st["dropped_max"]), float(ref[li, keys.index("dropped_max")])
+        if abs(a - b) > 1e-5 * max(abs(b), 1e-300) and abs(a - b) > 1e-12:
+            problems.append(f"level {st['level']} dropped_max: ours {a} ref {b}")
         a, b = float(st["trailing_nnz"]), float(ref[li, keys.index("trailing_nnz")])
         if abs(a - b) > 1e-2 * max(b, 1.0):
             problems.append(f"level {st['level']} trailing_nnz: ours {a} ref {b}")
