@@ -159,6 +159,7 @@ void launch_csc_scatter(const int64_t* indptr, const int64_t* indices, const dou
                         const int* entry_blk, cudaStream_t st);
 void launch_gemm(const GemmProb* d_probs, int nprob, int total_tiles, bool transA, cudaStream_t st);
 int gemm_tiles(int m, int n);
+void gemm_set_variant(int v);   // 0 default, 1: 64x64 tiles, 2: 128x64 tiles
 void launch_splitk_reduce(const SplitRed* d_tasks, int ntasks, int64_t max_mn, cudaStream_t st);
 void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t slab_elems,
                      bool smem, int kbmax, cudaStream_t st);

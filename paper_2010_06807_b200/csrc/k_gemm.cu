@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(NT2) gemm_dmma2_kernel(const GemmProb* __restr
   }
 }
 
-static int gemm_variant() {
+static int gemm_env_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SPQ_GEMM");
@@ -275,6 +275,11 @@ static int gemm_variant() {
   }
   return v;
 }
+// per-batch choice (set by the host before tiling a batch): small batches use
+// the 64x64 kernel so more CTAs cover the SMs
+static thread_local int g_variant = 0;
+static int gemm_variant() { return g_variant ? g_variant : gemm_env_variant(); }
+void gemm_set_variant(int v) { g_variant = v; }
 
 int gemm_tiles(int m, int n) {
   if (m <= 0 || n <= 0) return 0;

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
   const int r0 = min(mh, q * rpc);
   const int r1 = min(mh, r0 + rpc);
   const int nloc = r1 - r0;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   extern __shared__ __align__(16) double sm[];
   double* xch = sm;                        // [2][XCH]
@@ -107,10 +107,27 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
     }
     cluster.sync();
     const int own = min(CL - 1, jj / rpc);
-    // every thread forms the reflector scalars itself (no extra barrier)
-    double sigma = 0.0;
-    for (int r = 0; r < CL; ++r) sigma += cluster.map_shared_rank(X, r)[1 + jj];
-    const double alpha = cluster.map_shared_rank(X, own)[1 + QR_NB + jj];
+    // cluster totals: lane r of a warp loads CTA r's partial (parallel DSMEM
+    // loads), fixed shuffle tree -> identical sums in every CTA
+    const double* dsrc = X + 1;                 // CL == 1: the local exchange is the total
+    const double* asrc = X + 1 + QR_NB;
+    if (CL > 1) {
+      for (int c = warp; c < kb; c += QR_NT / 32) {
+        double v = lane < CL ? cluster.map_shared_rank(X, lane)[1 + c] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+          dtot[c] = v;
+          apiv[c] = cluster.map_shared_rank(X, own)[1 + QR_NB + c];
+        }
+      }
+      __syncthreads();
+      dsrc = dtot;
+      asrc = apiv;
+    }
+    // every thread forms the reflector scalars itself
+    const double sigma = dsrc[jj];
+    const double alpha = asrc[jj];
     double tau, beta, v0 = 1.0;
     const bool zero = sigma == 0.0;
     if (zero) {
@@ -122,9 +139,8 @@ __global__ void __launch_bounds__(QR_NT) panel_qr_kernel(const PanelJob* __restr
     }
     if (q == 0 && tid == 0) J.tau[j0 + jj] = tau;
     if (tid < kb && tid != jj) {
-      double s = 0.0;
-      for (int r = 0; r < CL; ++r) s += cluster.map_shared_rank(X, r)[1 + tid];
-      const double ap = cluster.map_shared_rank(X, own)[1 + QR_NB + tid];
+      const double s = dsrc[tid];
+      const double ap = asrc[tid];
       const double gv = zero ? ap : ap + s / v0;      // V_c^T v_jj
       if (tid < jj) Gs[tid + jj * (QR_NB + 1)] = gv;
       else wv[tid] = tau * gv;                        // w_c = tau v^T a_c
@@ -294,7 +310,7 @@ void launch_larft(const LarftJob* d_jobs, int njobs, int /*total_tiles*/, cudaSt
 // ------------------------------------------------------------ pivot check
 __global__ void pivot_check_kernel(const PivotJob* __restrict__ jobs, int njobs,
                                    int64_t* err_idx, double* err_val) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (j >= njobs) return;
   const PivotJob J = jobs[j];
   int64_t bad = -1;
@@ -305,20 +321,28 @@ __global__ void pivot_check_kernel(const PivotJob* __restrict__ jobs, int njobs,
       bad = 0;
     } else {
       const double floor = 1e-14 * d0;
-      for (int i = 0; i < J.k; ++i) {
-        const double r = J.R[i + (int64_t)i * J.ld];
-        if (fabs(r) <= floor) { bad = i; val = r; break; }
+      for (int i0 = 0; i0 < J.k && bad < 0; i0 += 32) {   // first failing index wins
+        const int i = i0 + lane;
+        const double r = i < J.k ? J.R[i + (int64_t)i * J.ld] : 1.0;
+        const unsigned b = __ballot_sync(0xffffffffu, i < J.k && fabs(r) <= floor);
+        if (b) {
+          const int first = __ffs(b) - 1;
+          bad = i0 + first;
+          val = __shfl_sync(0xffffffffu, r, first);
+        }
       }
     }
   }
-  err_idx[J.slot] = bad;
-  err_val[J.slot] = val;
+  if (lane == 0) {
+    err_idx[J.slot] = bad;
+    err_val[J.slot] = val;
+  }
 }
 
 void launch_pivot_check(const PivotJob* d_jobs, int njobs, int64_t* d_err_idx, double* d_err_val,
                         cudaStream_t st) {
   if (njobs <= 0) return;
-  pivot_check_kernel<<<(njobs + 127) / 128, 128, 0, st>>>(d_jobs, njobs, d_err_idx, d_err_val);
+  pivot_check_kernel<<<(njobs * 32 + 255) / 256, 256, 0, st>>>(d_jobs, njobs, d_err_idx, d_err_val);
 }
 
 // ------------------------------------------------------------- right TRSM

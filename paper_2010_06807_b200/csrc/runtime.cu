@@ -162,7 +162,8 @@ struct spq_ctx {
   std::vector<void*> slabs;
   std::vector<size_t> slab_caps;
   std::unordered_map<void*, int> refcnt;   // shared block allocations
-  std::set<void*> big;                      // cudaMallocAsync allocations
+  std::set<void*> big;                      // large buffers (arena)
+  std::vector<void*> big_pending;           // freed, awaiting a stream sync
   std::unordered_map<void*, size_t> big_size;
   size_t live_bytes = 0, peak_bytes = 0;
   char* slab_ptr = nullptr;
@@ -185,9 +186,65 @@ namespace {
 // ------------------------------------------------------------ utilities
 // Process-wide caches: device slabs and the pinned upload ring outlive a
 // context, so repeated factorizations do not pay cudaMalloc/cudaMallocHost.
+// Best-fit arena with coalescing for large buffers (one reservation per
+// process; no driver calls in steady state).
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0;
+  std::map<size_t, size_t> free_off;             // offset -> size
+  std::multimap<size_t, size_t> free_size;       // size -> offset
+  std::unordered_map<size_t, size_t> used;       // offset -> size
+  void add_free(size_t off, size_t sz) {
+    auto nx = free_off.lower_bound(off);
+    if (nx != free_off.end() && off + sz == nx->first) {   // merge with the next block
+      erase_size(nx->second, nx->first);
+      sz += nx->second;
+      nx = free_off.erase(nx);
+    }
+    if (nx != free_off.begin()) {                            // merge with the previous block
+      auto pv = std::prev(nx);
+      if (pv->first + pv->second == off) {
+        erase_size(pv->second, pv->first);
+        off = pv->first;
+        sz += pv->second;
+        free_off.erase(pv);
+      }
+    }
+    free_off[off] = sz;
+    free_size.emplace(sz, off);
+  }
+  void erase_size(size_t sz, size_t off) {
+    auto range = free_size.equal_range(sz);
+    for (auto it = range.first; it != range.second; ++it)
+      if (it->second == off) { free_size.erase(it); return; }
+  }
+  void* alloc(size_t bytes) {
+    bytes = (bytes + 4095) & ~(size_t)4095;
+    auto it = free_size.lower_bound(bytes);
+    if (it == free_size.end()) return nullptr;
+    const size_t sz = it->first, off = it->second;
+    free_size.erase(it);
+    free_off.erase(off);
+    if (sz > bytes) add_free(off + bytes, sz - bytes);
+    used[off] = bytes;
+    return base + off;
+  }
+  bool owns(void* p) const { return base && (char*)p >= base && (char*)p < base + cap; }
+  size_t size_of(void* p) const { return used.at((size_t)((char*)p - base)); }
+  void release(void* p) {
+    const size_t off = (size_t)((char*)p - base);
+    auto it = used.find(off);
+    if (it == used.end()) return;
+    const size_t sz = it->second;
+    used.erase(it);
+    add_free(off, sz);
+  }
+};
+
 struct GlobalCache {
   std::mutex mu;
   std::vector<std::pair<void*, size_t>> slabs;   // (ptr, bytes)
+  Arena arena;
   std::vector<std::pair<char*, char*>> rings;    // (pinned, device) of RING_BYTES
 };
 GlobalCache& gcache() {
@@ -222,11 +279,34 @@ constexpr size_t BIG_ALLOC = (size_t)8 << 20;   // >= 8 MB: driver stream-ordere
 double* dalloc(spq_ctx* c, size_t bytes) {
   auto t0 = std::chrono::steady_clock::now();
   if (bytes >= BIG_ALLOC) {
+    // large buffers: process-wide best-fit arena
     void* p = nullptr;
-    CUDA_TRY(cudaMallocAsync(&p, bytes, c->st));
+    size_t got = 0;
+    {
+      auto& g = gcache();
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (!g.arena.base) {
+        size_t fr = 0, tot = 0;
+        CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+        size_t cap = (size_t)(fr * 0.55) & ~(((size_t)1 << 21) - 1);
+        void* b = nullptr;
+        if (cudaMalloc(&b, cap) != cudaSuccess) { (void)cudaGetLastError(); cap = 0; b = nullptr; }
+        g.arena.base = (char*)b;
+        g.arena.cap = cap;
+        if (cap) g.arena.add_free(0, cap);
+      }
+      if (g.arena.base) {
+        p = g.arena.alloc(bytes);
+        if (p) got = g.arena.size_of(p);
+      }
+    }
+    if (!p) {   // arena exhausted: dedicated allocation
+      CUDA_TRY(cudaMalloc(&p, bytes));
+      got = bytes;
+    }
     c->big.insert(p);
-    c->big_size[p] = bytes;
-    c->live_bytes += bytes;
+    c->big_size[p] = got;
+    c->live_bytes += got;
     c->peak_bytes = std::max(c->peak_bytes, c->live_bytes);
     c->n_allocs++;
     c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -275,10 +355,11 @@ void dfree(spq_ctx* c, void* p) {
   if (!p) return;
   auto bi = c->big.find(p);
   if (bi != c->big.end()) {
-    CUDA_TRY(cudaFreeAsync(p, c->st));
+    // published to the shared arena at this context's next stream sync
     c->big.erase(bi);
     c->live_bytes -= c->big_size[p];
     c->big_size.erase(p);
+    c->big_pending.push_back(p);
     return;
   }
   auto it = c->pool_size.find(p);
@@ -309,9 +390,21 @@ double* shared_alloc(spq_ctx* c, size_t elems, int nref) {
   return base;
 }
 
+void publish_big(spq_ctx* c) {
+  if (c->big_pending.empty()) return;
+  auto& g = gcache();
+  std::lock_guard<std::mutex> lk(g.mu);
+  for (void* p : c->big_pending) {
+    if (g.arena.owns(p)) g.arena.release(p);
+    else cudaFree(p);
+  }
+  c->big_pending.clear();
+}
+
 void sync(spq_ctx* c) {
   auto t0 = std::chrono::steady_clock::now();
   CUDA_TRY(cudaStreamSynchronize(c->st));
+  publish_big(c);
   c->ring_off = 0;
   c->n_syncs++;
   c->host_ms[1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -463,6 +556,13 @@ struct GemmBatch {
   }
   void run(spq_ctx* c, bool transA, double flops) {
     if (p.empty()) return;
+    // few output tiles: switch to the 64x64 kernel (4x the CTAs per area)
+    int small = 0;
+    gemm_set_variant(2);
+    for (auto& g : p) small += gemm_tiles(g.m, g.n);
+    gemm_set_variant(small < c->nsm ? 1 : 2);
+    tiles = 0;
+    for (auto& g : p) tiles += gemm_tiles(g.m, g.n);
     const int target = 2 * c->nsm;
     std::vector<GemmProb> q;
     std::vector<SplitRed> red;
@@ -472,8 +572,8 @@ struct GemmBatch {
     if (tiles < target) {
       for (size_t i = 0; i < p.size(); ++i) {
         const GemmProb& g = p[i];
-        if (g.k < 1024) continue;
-        int sp = std::min((g.k + 511) / 512, std::max(1, target / std::max(tiles, 1)));
+        if (g.k < 512) continue;
+        int sp = std::min((g.k + 255) / 256, std::max(1, target / std::max(tiles, 1)));
         splits[i] = std::max(1, sp);
         if (splits[i] > 1) part_tot += (size_t)splits[i] * g.m * g.n;
       }
@@ -519,6 +619,7 @@ struct GemmBatch {
     }
     c->tm.launches[F_WY] += 1 + (red.empty() ? 0 : 1);
     c->n_kernels += 1 + (red.empty() ? 0 : 1);
+    gemm_set_variant(0);
     c->tm.flops[F_WY] += flops;
     if (part) dfree(c, part);
     p.clear();
@@ -2145,8 +2246,10 @@ void spq_destroy(spq_ctx* c) {
     for (int f = 0; f < F_NFAM; ++f)
       for (auto& e : c->tm.ev[f]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
-    for (void* p : c->big) cudaFreeAsync(p, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
+    for (void* p : c->big) c->big_pending.push_back(p);
+    c->big.clear();
+    publish_big(c);
     for (auto e : c->marks) cudaEventDestroy(e);
     for (auto& P : c->prog)
       for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);
