@@ -120,6 +120,8 @@ int spq_apply_w_host(spq_ctx* ctx, const double* in, double* out, int nrhs);
 int spq_apply_qt_dev(spq_ctx* ctx, double* d_inout, int nrhs);
 int spq_solve_w_dev(spq_ctx* ctx, double* d_inout, int nrhs);
 int spq_synchronize(spq_ctx* ctx);
+/* compiled solve program (0 apply_qt, 1 solve_w, 2 apply_w): [waves, ops, max ops/wave, max k] */
+int spq_chain_info(spq_ctx* ctx, int which, int64_t* info4);
 /* CUDA events on the context stream (device timing of any call sequence) */
 int spq_mark(spq_ctx* ctx, int slot);
 int spq_mark_elapsed(spq_ctx* ctx, int slot_a, int slot_b, float* ms);

@@ -56,6 +56,7 @@ SIGNATURES = {
     "spq_apply_qt_dev": (C.c_int, [_ctx, _vp, C.c_int]),
     "spq_solve_w_dev": (C.c_int, [_ctx, _vp, C.c_int]),
     "spq_synchronize": (C.c_int, [_ctx]),
+    "spq_chain_info": (C.c_int, [_ctx, C.c_int, _i64p]),
     "spq_mark": (C.c_int, [_ctx, C.c_int]),
     "spq_mark_elapsed": (C.c_int, [_ctx, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "spq_qr_house": (C.c_int, [_ctx, C.c_int64, C.c_int64, _f64p, _f64p, _f64p, _f64p, _f64p]),

@@ -123,7 +123,10 @@ struct ChainOp {
   const double* T;
   const double* R;
   const double* Rsn;
-  double* scratch;      // 10*k doubles of global scratch when k is too big for shared memory
+  double* scratch;      // per chunk 3*k doubles of global scratch when k is too big for shared memory
+  int nchunk;           // CTAs working on this op
+  int per;              // rows (WY) or R_sn columns (TRI) per chunk
+  int64_t part_off;     // offset of this op's partials in the wave scratch (x nrhs)
 };
 constexpr size_t CHAIN_SMEM_MAX = 200 * 1024;
 
@@ -176,8 +179,8 @@ void launch_power_iter(const PowerJob* d_jobs, int njobs, int fmax, cudaStream_t
 int cpqr_cluster_size(int m, int ncap);
 size_t cpqr_cluster_smem(int m, int ncap, int cl);
 void launch_cpqr_cluster(const CpqrJob* d_jobs, int njobs, int cl, size_t smem, cudaStream_t st);
-void launch_chain_wave(const ChainOp* d_ops, int nops, int kmax, double* z, int64_t N, int nrhs,
-                       cudaStream_t st);
+void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax,
+                       double* part, double* z, int64_t N, int nrhs, cudaStream_t st);
 }  // namespace spq
 
 #define CUDA_TRY(x)                                                        \

@@ -174,34 +174,92 @@ void chain_perm(const double* z, const int* roc, int64_t N, int nrhs, double* ou
 }  // namespace spq
 
 // ======================================================= wave-batched chain
-// One launch per wave of data-independent record operations (disjoint index
-// sets, planned at spq_finish); one CTA per operation; z is N x nrhs.
+// Two launches per wave of data-independent record operations (disjoint
+// index sets, planned at spq_finish).  Large operations are split into
+// chunks, one CTA per (op, chunk):
+//   phase A: partial products  w_chunk = V[rows_chunk]^T z[rows_chunk]  (WY)
+//                              s_chunk = R_sn[:, cols_chunk] y[cols_chunk] (TRI)
+//   phase B: every chunk-CTA of a WY op reduces the partials (fixed order),
+//            forms T^T w / T w and updates its rows; the TRI ops finish in
+//            chunk 0 (R_ss back substitution with 32x32 diagonal blocks staged
+//            in shared memory, or the R y product).
 namespace spq {
 
-constexpr int CW_NT = 1024;
+constexpr int CW_NT = 512;
 constexpr int CW_NW = CW_NT / 32;
 
-__global__ void __launch_bounds__(CW_NT) chain_wave_kernel(const ChainOp* __restrict__ ops,
-                                                           double* __restrict__ z, int64_t N,
-                                                           int nrhs) {
-  const ChainOp o = ops[blockIdx.x];
-  extern __shared__ __align__(16) double cw[];
+__global__ void __launch_bounds__(CW_NT) chain_phaseA_kernel(const ChainOp* __restrict__ ops,
+                                                             const int2* __restrict__ tasks,
+                                                             double* __restrict__ part,
+                                                             const double* __restrict__ z,
+                                                             int64_t N, int nrhs) {
+  const int2 tk = tasks[blockIdx.x];
+  const ChainOp o = ops[tk.x];
+  const int chunk = tk.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int k = o.k, m = o.m;
-  // w | w2 | 8 partial rows: shared memory, or this op's global scratch
-  double* w = o.scratch ? o.scratch : cw;   // k
-  double* w2 = w + k;                       // k
-  double* part = w2 + k;                    // 8 x k (rsn partials)
-  for (int r = 0; r < nrhs; ++r) {
-    double* zr = z + (int64_t)r * N;
-    if (o.kind == CH_WY_T || o.kind == CH_WY_N) {
+  const int k = o.k;
+  if (o.kind == CH_WY_T || o.kind == CH_WY_N) {
+    const int i0 = chunk * o.per, i1 = min(o.m, i0 + o.per);
+    for (int r = 0; r < nrhs; ++r) {
+      const double* zr = z + (int64_t)r * N;
       for (int c = warp; c < k; c += CW_NW) {
-        const double* vc = o.V + (int64_t)c * m;
+        const double* vc = o.V + (int64_t)c * o.m;
         double s = 0.0;
-        for (int i = lane; i < m; i += 32) s += vc[i] * zr[o.idx[i]];
+        for (int i = i0 + lane; i < i1; i += 32) s += vc[i] * zr[o.idx[i]];
 #pragma unroll
         for (int q = 16; q; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
-        if (lane == 0) w[c] = s;
+        if (lane == 0) part[o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k + c] = s;
+      }
+    }
+  } else if (o.n > 0) {
+    // R_sn[:, chunk] y[chunk]: rows a split over threads, columns over P partitions
+    __shared__ double redA[CW_NT];
+    const int j0 = chunk * o.per, j1 = min(o.n, j0 + o.per);
+    int P = CW_NT / max(k, 1);
+    P = P >= 16 ? 16 : (P >= 8 ? 8 : (P >= 4 ? 4 : (P >= 2 ? 2 : 1)));
+    const int rows_per_pass = CW_NT / P;
+    for (int r = 0; r < nrhs; ++r) {
+      const double* zr = z + (int64_t)r * N;
+      for (int a0 = 0; a0 < k; a0 += rows_per_pass) {
+        const int a = a0 + tid % rows_per_pass, jp = tid / rows_per_pass;
+        double s = 0.0;
+        if (a < k)
+          for (int j = j0 + jp; j < j1; j += P) s += o.Rsn[a + (int64_t)j * k] * zr[o.idx_n[j]];
+        redA[tid] = s;
+        __syncthreads();
+        if (tid < rows_per_pass && a0 + tid < k) {
+          double t = 0.0;
+          for (int q = 0; q < P; ++q) t += redA[tid + q * rows_per_pass];
+          part[o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k + a0 + tid] = t;
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __restrict__ ops,
+                                                             const int2* __restrict__ tasks,
+                                                             const double* __restrict__ part,
+                                                             double* __restrict__ z, int64_t N,
+                                                             int nrhs) {
+  const int2 tk = tasks[blockIdx.x];
+  const ChainOp o = ops[tk.x];
+  const int chunk = tk.y;
+  extern __shared__ __align__(16) double cw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = o.k;
+  double* w = o.scratch ? o.scratch + (int64_t)chunk * 3 * k : cw;   // k
+  double* w2 = w + k;                                                   // k
+  __shared__ double Rd[32 * 33];
+  for (int r = 0; r < nrhs; ++r) {
+    double* zr = z + (int64_t)r * N;
+    const double* pr = part + o.part_off * nrhs + (int64_t)r * o.nchunk * k;
+    if (o.kind == CH_WY_T || o.kind == CH_WY_N) {
+      for (int c = tid; c < k; c += CW_NT) {
+        double s = 0.0;
+        for (int q = 0; q < o.nchunk; ++q) s += pr[(int64_t)q * k + c];
+        w[c] = s;
       }
       __syncthreads();
       for (int a = tid; a < k; a += CW_NT) {
@@ -213,26 +271,18 @@ __global__ void __launch_bounds__(CW_NT) chain_wave_kernel(const ChainOp* __rest
         w2[a] = s;
       }
       __syncthreads();
-      for (int i = tid; i < m; i += CW_NT) {
+      const int i0 = chunk * o.per, i1 = min(o.m, i0 + o.per);
+      for (int i = i0 + tid; i < i1; i += CW_NT) {
         double s = 0.0;
-        for (int c = 0; c < k; ++c) s += o.V[i + (int64_t)c * m] * w2[c];
+        for (int c = 0; c < k; ++c) s += o.V[i + (int64_t)c * o.m] * w2[c];
         zr[o.idx[i]] -= s;
       }
       __syncthreads();
     } else {
-      // triangular ops on y[idx] (k entries), coupling R_sn (k x n) to y[idx_n]
-      const int n = o.n;
-      const int P = 8;
-      for (int t = tid; t < k * P; t += CW_NT) {
-        const int a = t % k, pr = t / k;
-        double s = 0.0;
-        for (int j = pr; j < n; j += P) s += o.Rsn[a + (int64_t)j * k] * zr[o.idx_n[j]];
-        part[pr * k + a] = s;
-      }
-      __syncthreads();
+      if (chunk != 0) return;
       for (int a = tid; a < k; a += CW_NT) {
         double s = 0.0;
-        for (int pr = 0; pr < P; ++pr) s += part[pr * k + a];
+        for (int q = 0; q < o.nchunk && o.n > 0; ++q) s += pr[(int64_t)q * k + a];
         if (o.kind == CH_TRI_SOLVE) {
           w[a] = zr[o.idx[a]] - s;
         } else {   // CH_TRI_MUL: R y_s + R_sn y_n
@@ -243,19 +293,21 @@ __global__ void __launch_bounds__(CW_NT) chain_wave_kernel(const ChainOp* __rest
       }
       __syncthreads();
       if (o.kind == CH_TRI_SOLVE) {
-        // blocked back substitution: 32-row diagonal blocks solved by warp 0,
-        // the rows above updated by all threads
         for (int i1 = k; i1 > 0; i1 -= 32) {
-          const int i0 = max(0, i1 - 32);
+          const int i0 = max(0, i1 - 32), wd = i1 - i0;
+          for (int e = tid; e < wd * wd; e += CW_NT) {     // stage the diagonal block
+            const int a = e % wd, b = e / wd;
+            Rd[a + b * 33] = o.R[(i0 + a) + (int64_t)(i0 + b) * k];
+          }
+          __syncthreads();
           if (warp == 0) {
-            for (int i = i1 - 1; i >= i0; --i) {
-              double xi = 0.0;
-              if (lane == 0) { xi = w[i] / o.R[i + (int64_t)i * k]; w[i] = xi; }
-              xi = __shfl_sync(0xffffffffu, xi, 0);
-              const int a = i0 + lane;
-              if (a < i) w[a] -= o.R[a + (int64_t)i * k] * xi;
-              __syncwarp();
+            double wl = lane < wd ? w[i0 + lane] : 0.0;
+            for (int i = wd - 1; i >= 0; --i) {
+              const double xi = __shfl_sync(0xffffffffu, wl, i) / Rd[i + i * 33];
+              if (lane == i) wl = xi;
+              if (lane < i) wl -= Rd[lane + i * 33] * xi;
             }
+            if (lane < wd) w[i0 + lane] = wl;
           }
           __syncthreads();
           for (int a = tid; a < i0; a += CW_NT) {
@@ -273,21 +325,22 @@ __global__ void __launch_bounds__(CW_NT) chain_wave_kernel(const ChainOp* __rest
 }
 
 size_t chain_wave_smem(int kmax) {
-  const size_t b = (size_t)10 * (kmax > 0 ? kmax : 1) * sizeof(double);
-  return b <= CHAIN_SMEM_MAX ? b : 0;   // bigger ops carry global scratch
+  const size_t b = (size_t)2 * (kmax > 0 ? kmax : 1) * sizeof(double);
+  return b <= CHAIN_SMEM_MAX ? b : 0;
 }
 
-void launch_chain_wave(const ChainOp* d_ops, int nops, int kmax, double* z, int64_t N, int nrhs,
-                       cudaStream_t st) {
-  if (nops <= 0) return;
+void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax,
+                       double* part, double* z, int64_t N, int nrhs, cudaStream_t st) {
+  if (ntasks <= 0) return;
   const size_t smem = chain_wave_smem(kmax);
   static size_t conf = 0;
   if (smem > 48 * 1024 && smem > conf) {
-    CUDA_TRY(cudaFuncSetAttribute(chain_wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(chain_phaseB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     conf = smem;
   }
-  chain_wave_kernel<<<nops, CW_NT, smem, st>>>(d_ops, z, N, nrhs);
+  chain_phaseA_kernel<<<ntasks, CW_NT, 0, st>>>(d_ops, d_tasks, part, z, N, nrhs);
+  chain_phaseB_kernel<<<ntasks, CW_NT, smem, st>>>(d_ops, d_tasks, part, z, N, nrhs);
 }
 
 }  // namespace spq

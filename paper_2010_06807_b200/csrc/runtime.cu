@@ -176,6 +176,10 @@ struct spq_ctx {
   // compiled solve-chain programs: 0 apply_qt, 1 solve_w, 2 apply_w
   struct Prog {
     ChainOp* d_ops = nullptr;
+    int2* d_tasks = nullptr;
+    std::vector<int> toff, tcnt;          // per wave: task range
+    std::vector<int64_t> part_sz;         // per wave: partial-sum doubles (x nrhs)
+    std::map<int, double*> part_buf;      // nrhs -> wave scratch (max over waves)
     std::vector<int> off, cnt, kmax;
     std::map<int, cudaGraphExec_t> graphs;   // nrhs -> executable graph (z = d_vec)
   } prog[3];
@@ -2037,28 +2041,50 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
     P.cnt.back()++;
     P.kmax.back() = std::max(P.kmax.back(), ops[t].k);
   }
-  // ops too large for shared memory get a private global scratch
+  // chunking: ~64K multiply-adds per CTA, at most 64 CTAs per op
+  std::vector<int2> tasks;
+  P.toff.clear(); P.tcnt.clear(); P.part_sz.clear();
   size_t scr = 0;
-  for (auto& o : ordered)
-    if ((size_t)10 * o.k * sizeof(double) > CHAIN_SMEM_MAX) scr += 10 * (size_t)o.k;
-  if (scr) {
+  for (auto& o : ordered) {
+    const bool wy = o.kind == CH_WY_T || o.kind == CH_WY_N;
+    const int64_t len = wy ? o.m : o.n;           // the dimension that is split
+    const int64_t work = (int64_t)std::max(len, (int64_t)1) * std::max(o.k, 1);
+    int nch = (int)std::min<int64_t>(64, std::max<int64_t>(1, work / 65536));
+    if (!wy && o.n == 0) nch = 1;
+    o.per = (int)std::max<int64_t>(1, (len + nch - 1) / nch);
+    o.nchunk = (int)std::max<int64_t>(1, (len + o.per - 1) / o.per);
+    if ((size_t)2 * o.k * sizeof(double) > CHAIN_SMEM_MAX) scr += 3 * (size_t)o.k * o.nchunk;
+  }
+  if (scr) {   // ops too large for shared memory: private global scratch per chunk
     double* base = dalloc(c, scr * sizeof(double));
     size_t off = 0;
     for (auto& o : ordered)
-      if ((size_t)10 * o.k * sizeof(double) > CHAIN_SMEM_MAX) {
+      if ((size_t)2 * o.k * sizeof(double) > CHAIN_SMEM_MAX) {
         o.scratch = base + off;
-        off += 10 * (size_t)o.k;
+        off += 3 * (size_t)o.k * o.nchunk;
       }
   }
   for (size_t w = 0; w < P.off.size(); ++w) {
     int km = 0;
-    for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t)
-      if (!ordered[t].scratch) km = std::max(km, ordered[t].k);
+    int64_t psz = 0;
+    P.toff.push_back((int)tasks.size());
+    for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
+      ChainOp& o = ordered[t];
+      if (!o.scratch) km = std::max(km, o.k);
+      o.part_off = psz;
+      psz += (int64_t)o.nchunk * std::max(o.k, 1);
+      for (int q = 0; q < o.nchunk; ++q) tasks.push_back(make_int2(t - P.off[w], q));
+    }
+    P.tcnt.push_back((int)tasks.size() - P.toff.back());
     P.kmax[w] = km;
+    P.part_sz.push_back(psz);
   }
   if (!ordered.empty()) {
     P.d_ops = (ChainOp*)dalloc(c, ordered.size() * sizeof(ChainOp));
     CUDA_TRY(cudaMemcpyAsync(P.d_ops, ordered.data(), ordered.size() * sizeof(ChainOp),
+                             cudaMemcpyHostToDevice, c->st));
+    P.d_tasks = (int2*)dalloc(c, std::max<size_t>(tasks.size(), 1) * sizeof(int2));
+    CUDA_TRY(cudaMemcpyAsync(P.d_tasks, tasks.data(), tasks.size() * sizeof(int2),
                              cudaMemcpyHostToDevice, c->st));
     sync(c);
   }
@@ -2071,7 +2097,7 @@ void compile_chains(spq_ctx* c) {
   // apply_qt: every record's panel on its rows, in chain order
   for (auto& r : c->recs) {
     if (r.k <= 0) continue;
-    ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_rows, nullptr, r.V, r.T, nullptr, nullptr, nullptr});
+    ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_rows, nullptr, r.V, r.T, nullptr, nullptr, nullptr, 1, 1, 0});
     wr.push_back(to_int(r.rows));
     rd.push_back({});
   }
@@ -2082,14 +2108,14 @@ void compile_chains(spq_ctx* c) {
     Record& r = *it;
     if (r.kind == REC_SPARSIFY) {
       if (r.k <= 0) continue;
-      ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr});
+      ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, 1, 1, 0});
       wr.push_back(to_int(r.cols_s));
       rd.push_back({});
     } else {
       if (r.k <= 0) continue;
       const bool bh = r.kind == REC_ELIM;
       ops.push_back(ChainOp{CH_TRI_SOLVE, r.k, r.k, bh ? r.n : 0, r.d_cols_s,
-                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr});
+                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr, 1, 1, 0});
       wr.push_back(to_int(r.cols_s));
       rd.push_back(bh ? to_int(r.cols_n) : std::vector<int>());
     }
@@ -2100,13 +2126,13 @@ void compile_chains(spq_ctx* c) {
   for (auto& r : c->recs) {
     if (r.k <= 0) continue;
     if (r.kind == REC_SPARSIFY) {
-      ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr});
+      ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, 1, 1, 0});
       wr.push_back(to_int(r.cols_s));
       rd.push_back({});
     } else {
       const bool bh = r.kind == REC_ELIM;
       ops.push_back(ChainOp{CH_TRI_MUL, r.k, r.k, bh ? r.n : 0, r.d_cols_s,
-                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr});
+                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr, 1, 1, 0});
       wr.push_back(to_int(r.cols_s));
       rd.push_back(bh ? to_int(r.cols_n) : std::vector<int>());
     }
@@ -2114,10 +2140,24 @@ void compile_chains(spq_ctx* c) {
   build_prog(c, 2, ops, wr, rd);
 }
 
+double* ensure_part(spq_ctx* c, int which, int nrhs) {   // call outside graph capture
+  auto& P = c->prog[which];
+  auto it = P.part_buf.find(nrhs);
+  if (it == P.part_buf.end()) {
+    int64_t mx = 1;
+    for (auto v : P.part_sz) mx = std::max(mx, v);
+    it = P.part_buf.emplace(nrhs, dalloc(c, (size_t)mx * nrhs * sizeof(double))).first;
+  }
+  return it->second;
+}
+
 void run_prog(spq_ctx* c, int which, double* z, int nrhs) {
   auto& P = c->prog[which];
+  auto it = P.part_buf.find(nrhs);
+  if (it == P.part_buf.end()) throw SpqError(SPQ_ERR_INTERNAL, "chain scratch missing");
   for (size_t w = 0; w < P.off.size(); ++w)
-    launch_chain_wave(P.d_ops + P.off[w], P.cnt[w], P.kmax[w], z, c->N, nrhs, c->st);
+    launch_chain_wave(P.d_ops + P.off[w], P.d_tasks + P.toff[w], P.tcnt[w], P.kmax[w],
+                      it->second, z, c->N, nrhs, c->st);
 }
 
 // full application on c->d_vec (result in d_vec), captured once per nrhs
@@ -2129,6 +2169,7 @@ void run_chain(spq_ctx* c, int which, int nrhs) {
   auto& P = c->prog[which];
   auto it = P.graphs.find(nrhs);
   if (it == P.graphs.end()) {
+    ensure_part(c, which, nrhs);
     cudaGraph_t g;
     CUDA_TRY(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
     if (which == 0) {
@@ -2523,6 +2564,21 @@ int spq_mark_elapsed(spq_ctx* c, int a, int b, float* ms) {
       throw SpqError(SPQ_ERR_BAD_INPUT, "mark slot");
     CUDA_TRY(cudaEventSynchronize(c->marks[b]));
     CUDA_TRY(cudaEventElapsedTime(ms, c->marks[a], c->marks[b]));
+  });
+}
+
+int spq_chain_info(spq_ctx* c, int which, int64_t* info4) {
+  return guarded(c, [&] {
+    if (which < 0 || which > 2) throw SpqError(SPQ_ERR_BAD_INPUT, "chain index");
+    if (!c->compiled) { compile_chains(c); c->compiled = true; }
+    auto& P = c->prog[which];
+    int64_t ops = 0, maxw = 0, kmax = 0;
+    for (size_t w = 0; w < P.cnt.size(); ++w) {
+      ops += P.cnt[w];
+      maxw = std::max<int64_t>(maxw, P.cnt[w]);
+      kmax = std::max<int64_t>(kmax, P.kmax[w]);
+    }
+    info4[0] = (int64_t)P.cnt.size(); info4[1] = ops; info4[2] = maxw; info4[3] = kmax;
   });
 }
 

@@ -16,6 +16,10 @@ A, dims, L, eps, b, tol = make_config(cfg)
 F = factorize(A, partition_geometric(dims, L), eps=eps)
 y = np.random.default_rng(0).standard_normal(A.ncols)
 out = {}
+for w, name in enumerate(("apply_qt", "solve_w", "apply_w")):
+    info = np.zeros(4, np.int64)
+    F._ctx.call("spq_chain_info", w, info)
+    out[name + "_program"] = {"waves": int(info[0]), "ops": int(info[1]), "max_ops_per_wave": int(info[2]), "kmax": int(info[3])}
 for fn in ("apply_qt", "solve_w", "apply_w"):
     getattr(F, fn)(y)                    # first call compiles the wave program + graph
     F._ctx.call("spq_reset_timings")
