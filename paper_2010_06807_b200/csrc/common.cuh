@@ -191,6 +191,10 @@ void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, in
     }                                                                      \
   } while (0)
 
+// every <<<>>> launch is followed by this: launch-configuration errors
+// (grid limits, shared-memory attributes) must never pass silently
+#define SPQ_LAUNCH_CHECK() CUDA_TRY(cudaGetLastError())
+
 #include <stdexcept>
 #include <string>
 namespace spq {

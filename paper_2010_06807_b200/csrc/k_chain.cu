@@ -10,6 +10,8 @@
 //     partial sums + one reduction CTA), then R_ss back substitution.
 //   apply_w: y_s = R_ss x_s + R_sn x_n ; DiagonalScaling ; Permutation.
 // All HBM-bound (~0.4 flop/byte).
+#include <string>
+
 #include "common.cuh"
 
 namespace spq {
@@ -133,9 +135,9 @@ __global__ void permute_kernel(const double* __restrict__ z, const int* __restri
 void chain_wy(const double* V, const double* T, int m, int k, double* z, const int* rows,
               int64_t N, int nrhs, bool transpose, double* w, double* w2, cudaStream_t st) {
   if (k <= 0 || m <= 0) return;
-  wy_dot_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(V, m, k, z, rows, N, nrhs, w);
-  tri_mv_kernel<<<1, 256, 0, st>>>(T, k, w, nrhs, transpose ? 1 : 0, w2);
-  wy_update_kernel<<<(m + 127) / 128, 128, 0, st>>>(V, m, k, z, rows, N, nrhs, w2);
+  wy_dot_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(V, m, k, z, rows, N, nrhs, w); SPQ_LAUNCH_CHECK();
+  tri_mv_kernel<<<1, 256, 0, st>>>(T, k, w, nrhs, transpose ? 1 : 0, w2); SPQ_LAUNCH_CHECK();
+  wy_update_kernel<<<(m + 127) / 128, 128, 0, st>>>(V, m, k, z, rows, N, nrhs, w2); SPQ_LAUNCH_CHECK();
 }
 
 int chain_rsn_chunks(int n) { return n <= 0 ? 0 : (n + 127) / 128; }
@@ -146,29 +148,29 @@ void chain_tri(const double* R, int k, const double* Rsn, int n, double* y, cons
   const int nch = chain_rsn_chunks(n);
   if (nch > 0)
     rsn_partial_kernel<<<dim3((k + 127) / 128, nch), 128, 0, st>>>(Rsn, k, n, y, cols_n, N, nrhs,
-                                                                   128, part);
+                                                                   128, part); SPQ_LAUNCH_CHECK();
   const size_t smem = (size_t)k * sizeof(double);
   static size_t conf = 0;
-  if (smem > 48 * 1024 && smem > conf) {
+  if (smem > conf) {   // the default 48 KB cap counts static + dynamic
     CUDA_TRY(cudaFuncSetAttribute(tri_solve_vec_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     conf = smem;
   }
   tri_solve_vec_kernel<<<1, 1024, smem, st>>>(R, k, y, cols_s, N, nrhs, nch ? part : nullptr, nch,
-                                              mode);
+                                              mode); SPQ_LAUNCH_CHECK();
 }
 
 void chain_diag(double* y, const double* s, int64_t N, int nrhs, bool divide, cudaStream_t st) {
   const int64_t t = N * nrhs;
   if (t <= 0) return;
-  diag_scale_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(y, s, N, nrhs, divide ? 1 : 0);
+  diag_scale_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(y, s, N, nrhs, divide ? 1 : 0); SPQ_LAUNCH_CHECK();
 }
 
 void chain_perm(const double* z, const int* roc, int64_t N, int nrhs, double* out,
                 cudaStream_t st) {
   const int64_t t = N * nrhs;
   if (t <= 0) return;
-  permute_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(z, roc, N, nrhs, out);
+  permute_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(z, roc, N, nrhs, out); SPQ_LAUNCH_CHECK();
 }
 
 }  // namespace spq
@@ -334,13 +336,24 @@ void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, in
   if (ntasks <= 0) return;
   const size_t smem = chain_wave_smem(kmax);
   static size_t conf = 0;
-  if (smem > 48 * 1024 && smem > conf) {
+  if (smem > conf) {   // the default 48 KB cap counts static + dynamic
     CUDA_TRY(cudaFuncSetAttribute(chain_phaseB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     conf = smem;
   }
+  auto fail = [&](const char* where) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+      throw std::runtime_error(std::string(cudaGetErrorString(e)) + " " + where +
+                               " (ntasks=" + std::to_string(ntasks) + " kmax=" +
+                               std::to_string(kmax) + " smem=" + std::to_string(smem) +
+                               " conf=" + std::to_string(conf) + ")");
+  };
+  fail("pending before chain wave");
   chain_phaseA_kernel<<<ntasks, CW_NT, 0, st>>>(d_ops, d_tasks, part, z, N, nrhs);
+  fail("at chain phase A launch");
   chain_phaseB_kernel<<<ntasks, CW_NT, smem, st>>>(d_ops, d_tasks, part, z, N, nrhs);
+  fail("at chain phase B launch");
 }
 
 }  // namespace spq

@@ -44,7 +44,7 @@ void launch_copy(const CopyTask* d_tasks, int ntasks, int64_t max_elems, cudaStr
   if (y > 512) y = 512;
   // grid.x limit is 2^31-1; y <= 512 stays far below the 65535 limit
   dim3 grid((unsigned)ntasks, (unsigned)y);
-  copy_tasks_kernel<<<grid, 256, 0, st>>>(d_tasks);
+  copy_tasks_kernel<<<grid, 256, 0, st>>>(d_tasks); SPQ_LAUNCH_CHECK();
 }
 
 // one CTA per block; thread per row; flag = any nonzero in the row
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) rowflags_kernel(const double* const* __re
 void launch_rowflags(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
                      const int64_t* d_off, unsigned char* d_out, int nblk, cudaStream_t st) {
   if (nblk <= 0) return;
-  rowflags_kernel<<<nblk, 128, 0, st>>>(d_ptrs, d_nr, d_nc, d_off, d_out);
+  rowflags_kernel<<<nblk, 128, 0, st>>>(d_ptrs, d_nr, d_nc, d_off, d_out); SPQ_LAUNCH_CHECK();
 }
 
 __global__ void __launch_bounds__(256) count_nnz_kernel(const double* const* __restrict__ ptrs,
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) count_nnz_kernel(const double* const* __r
 void launch_count_nnz(const double* const* d_ptrs, const int64_t* d_sizes, int nblk,
                       unsigned long long* d_count, cudaStream_t st) {
   if (nblk <= 0) return;
-  count_nnz_kernel<<<nblk, 256, 0, st>>>(d_ptrs, d_sizes, d_count);
+  count_nnz_kernel<<<nblk, 256, 0, st>>>(d_ptrs, d_sizes, d_count); SPQ_LAUNCH_CHECK();
 }
 
 // Column 2-norms accumulated sequentially in CSC entry order, no FMA
@@ -113,7 +113,7 @@ void launch_colnorms_scale(const int64_t* indptr, const int64_t* /*indices*/, do
                            cudaStream_t st) {
   if (N <= 0) return;
   colnorms_scale_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(indptr, data, N, scale,
-                                                                      zero_col, equilibrate);
+                                                                      zero_col, equilibrate); SPQ_LAUNCH_CHECK();
 }
 
 // entry e of the CSC goes to blk_base[entry_blk[e]][dest_off[e]]
@@ -132,7 +132,7 @@ void launch_csc_scatter(const int64_t* indptr, const int64_t* /*indices*/, const
   (void)indptr;
   if (nnz <= 0) return;
   csc_scatter_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(data, nnz, dest_off,
-                                                                     blk_base, entry_blk);
+                                                                     blk_base, entry_blk); SPQ_LAUNCH_CHECK();
 }
 
 }  // namespace spq

@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -224,8 +225,17 @@ size_t cpqr_smem_bytes(int ncols_cap, int m, bool force_gmaps) {
 }
 
 int cpqr_grid(int ncols, int nsm) {
-  int g = (ncols + 7) / 8;
+  static int gmax = -1, per = -1;
+  if (gmax < 0) {
+    const char* e = getenv("SPQ_CPQR_GMAX");
+    gmax = e ? atoi(e) : 0;
+    const char* f = getenv("SPQ_CPQR_COLS_PER_CTA");
+    per = f ? atoi(f) : 8;
+    if (per < 1) per = 8;
+  }
+  int g = (ncols + per - 1) / per;
   if (g > nsm) g = nsm;
+  if (gmax > 0 && g > gmax) g = gmax;
   if (g < 1) g = 1;
   return g;
 }
@@ -233,7 +243,7 @@ int cpqr_grid(int ncols, int nsm) {
 void launch_cpqr(const CpqrArgs& a, int G, cudaStream_t st) {
   const size_t bytes = cpqr_smem_bytes(a.ncols_cap, a.m, a.force_gmaps != 0);
   static size_t configured = 0;
-  if (bytes > 48 * 1024 && bytes > configured) {
+  if (bytes > configured) {   // the default 48 KB cap counts static + dynamic
     CUDA_TRY(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)bytes));
     configured = bytes;
@@ -304,21 +314,23 @@ __global__ void __launch_bounds__(1024) sparsify_select_kernel(const double* __r
 }
 
 // W[:, t] = M[:, keep_idx[t]] for t < *nk
+// (column index on grid x: candidate counts exceed gridDim.y's 65535 limit
+// on 3D problems)
 __global__ void gather_cols_kernel(const double* __restrict__ M, int m, const int* __restrict__ idx,
                                    const int* nk, double* __restrict__ W) {
-  const int t = blockIdx.y;
+  const int t = blockIdx.x;
   if (t >= *nk) return;
   const double* src = M + (int64_t)idx[t] * m;
   double* dst = W + (int64_t)t * m;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x)
+  for (int r = blockIdx.y * blockDim.x + threadIdx.x; r < m; r += gridDim.y * blockDim.x)
     dst[r] = src[r];
 }
 
 void launch_sparsify_prep(const double* M, int m, int n, double eps, double* sq, int* keep_idx,
                           int* nk, double* ratio, double* maxcol, double* W, cudaStream_t st) {
-  if (n > 0) colsq_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(M, m, n, sq);
-  sparsify_select_kernel<<<1, 1024, 0, st>>>(sq, m, n, eps, keep_idx, nk, ratio, maxcol);
-  if (n > 0) gather_cols_kernel<<<dim3((m + 255) / 256, n), 256, 0, st>>>(M, m, keep_idx, nk, W);
+  if (n > 0) colsq_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(M, m, n, sq); SPQ_LAUNCH_CHECK();
+  sparsify_select_kernel<<<1, 1024, 0, st>>>(sq, m, n, eps, keep_idx, nk, ratio, maxcol); SPQ_LAUNCH_CHECK();
+  if (n > 0) gather_cols_kernel<<<dim3(n, (unsigned)std::min((m + 255) / 256, 64)), 256, 0, st>>>(M, m, keep_idx, nk, W); SPQ_LAUNCH_CHECK();
 }
 
 }  // namespace spq
@@ -525,7 +537,7 @@ void launch_cpqr_cta(const CpqrJob* d_jobs, int njobs, size_t smem, cudaStream_t
                                   (int)std::max<size_t>(smem, 48 * 1024)));
     conf = smem;
   }
-  cpqr_cta_kernel<<<njobs, CB_NT, smem, st>>>(d_jobs);
+  cpqr_cta_kernel<<<njobs, CB_NT, smem, st>>>(d_jobs); SPQ_LAUNCH_CHECK();
 }
 
 }  // namespace spq
@@ -739,7 +751,12 @@ __global__ void __launch_bounds__(CC_NT) cpqr_cluster_kernel(const CpqrJob* __re
 }
 
 int cpqr_cluster_size(int m, int ncap) {
-  for (int cl = 1; cl <= 16; cl *= 2)
+  static int clmax = -1;
+  if (clmax < 0) {
+    const char* e = getenv("SPQ_CPQR_CLMAX");
+    clmax = e ? atoi(e) : 16;
+  }
+  for (int cl = 1; cl <= clmax; cl *= 2)
     if (CcLayout(m, ncap, cl).bytes() <= (size_t)200 * 1024) return cl;
   return 0;
 }
@@ -831,11 +848,11 @@ void launch_power_iter(const PowerJob* d_jobs, int njobs, int fmax, cudaStream_t
   if (njobs <= 0) return;
   const size_t smem = 2 * (size_t)(fmax > 0 ? fmax : 1) * sizeof(double);
   static size_t conf = 0;
-  if (smem > 48 * 1024 && smem > conf) {
+  if (smem > conf) {   // the default 48 KB cap counts static + dynamic
     CUDA_TRY(cudaFuncSetAttribute(power_iter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     conf = smem;
   }
-  power_iter_kernel<<<njobs, PI_NT, smem, st>>>(d_jobs);
+  power_iter_kernel<<<njobs, PI_NT, smem, st>>>(d_jobs); SPQ_LAUNCH_CHECK();
 }
 
 }  // namespace spq

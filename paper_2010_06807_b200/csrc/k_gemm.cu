@@ -148,7 +148,7 @@ void launch_splitk_reduce(const SplitRed* d_tasks, int ntasks, int64_t max_mn, c
   int64_t y = (max_mn + 2047) / 2048;
   if (y < 1) y = 1;
   if (y > 256) y = 256;
-  splitk_reduce_kernel<<<dim3(ntasks, (unsigned)y), 256, 0, st>>>(d_tasks);
+  splitk_reduce_kernel<<<dim3(ntasks, (unsigned)y), 256, 0, st>>>(d_tasks); SPQ_LAUNCH_CHECK();
 }
 
 
@@ -302,12 +302,14 @@ void launch_gemm(const GemmProb* d_probs, int nprob, int total_tiles, bool trans
       gemm_dmma2_kernel<true><<<total_tiles, NT2, smem, st>>>(d_probs, nprob);
     else
       gemm_dmma2_kernel<false><<<total_tiles, NT2, smem, st>>>(d_probs, nprob);
+    SPQ_LAUNCH_CHECK();
     return;
   }
   if (transA)
     gemm_dmma_kernel<true><<<total_tiles, NT, 0, st>>>(d_probs, nprob);
   else
     gemm_dmma_kernel<false><<<total_tiles, NT, 0, st>>>(d_probs, nprob);
+  SPQ_LAUNCH_CHECK();
 }
 
 }  // namespace spq

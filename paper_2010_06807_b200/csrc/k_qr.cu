@@ -304,7 +304,7 @@ int larft_tiles(int) { return 1; }
 
 void launch_larft(const LarftJob* d_jobs, int njobs, int /*total_tiles*/, cudaStream_t st) {
   if (njobs <= 0) return;
-  larft_kernel<<<njobs, LARFT_NT, 0, st>>>(d_jobs);
+  larft_kernel<<<njobs, LARFT_NT, 0, st>>>(d_jobs); SPQ_LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------------ pivot check
@@ -342,7 +342,7 @@ __global__ void pivot_check_kernel(const PivotJob* __restrict__ jobs, int njobs,
 void launch_pivot_check(const PivotJob* d_jobs, int njobs, int64_t* d_err_idx, double* d_err_val,
                         cudaStream_t st) {
   if (njobs <= 0) return;
-  pivot_check_kernel<<<(njobs * 32 + 255) / 256, 256, 0, st>>>(d_jobs, njobs, d_err_idx, d_err_val);
+  pivot_check_kernel<<<(njobs * 32 + 255) / 256, 256, 0, st>>>(d_jobs, njobs, d_err_idx, d_err_val); SPQ_LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------------- right TRSM
@@ -395,12 +395,12 @@ __global__ void __launch_bounds__(TRSM_NT) trsm_diag_kernel(const TrsmJob* __res
 
 void launch_trsm_diag(const TrsmJob* d_jobs, int njobs, int total_tiles, int j0, cudaStream_t st) {
   if (njobs <= 0 || total_tiles <= 0) return;
-  trsm_diag_kernel<<<total_tiles, TRSM_NT, 0, st>>>(d_jobs, njobs, j0);
+  trsm_diag_kernel<<<total_tiles, TRSM_NT, 0, st>>>(d_jobs, njobs, j0); SPQ_LAUNCH_CHECK();
 }
 
 void launch_trsm_right(const TrsmJob* d_jobs, int njobs, int total_tiles, cudaStream_t st) {
   if (njobs <= 0 || total_tiles <= 0) return;
-  trsm_right_kernel<<<total_tiles, TRSM_NT, 0, st>>>(d_jobs, njobs);
+  trsm_right_kernel<<<total_tiles, TRSM_NT, 0, st>>>(d_jobs, njobs); SPQ_LAUNCH_CHECK();
 }
 
 }  // namespace spq

@@ -146,3 +146,21 @@ def test_c5_full_size_properties():
     assert np.linalg.norm(F.apply_w(F.solve_w(y)) - y) <= 1e-8 * np.linalg.norm(y)
     z = F.apply_qt(y)
     assert abs(np.linalg.norm(z) - np.linalg.norm(y)) <= 1e-10 * np.linalg.norm(y)
+
+
+@pytest.mark.slow
+def test_n48_3d_top_levels_match_oracle(golden_dir):
+    """3D 48^3 with the C5 generator: every sparsified interface on levels
+    11..8 has the oracle's rank (tests/golden/make_n48_ranks.py).  Level 8
+    has candidate matrices with > 65,535 columns (grid-limit regression)."""
+    import os
+    from paper_2010_06807_b200.factor import factorize
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    g = np.load(os.path.join(golden_dir, "ranks_C5_n48_L8.npz"))["ranks"]
+    A, dims, L, eps, b, tol = make_config("C5", n=48)
+    F = factorize(A, partition_geometric(dims, L), eps=eps)
+    got = {(int(l), int(p)): (int(r), int(bf)) for l, p, bf, r in F.sparsify_log}
+    bad = [(int(l), int(p), int(r), int(bf), got.get((int(l), int(p))))
+           for l, p, r, bf in g if got.get((int(l), int(p))) != (int(r), int(bf))]
+    assert not bad, f"{len(bad)} of {len(g)} interfaces differ, e.g. {bad[:5]}"
