@@ -157,10 +157,15 @@ struct spq_ctx {
   double* d_part = nullptr;
   size_t vec_cap = 0, w_cap = 0, part_cap = 0;
   // device memory pool
-  std::unordered_map<size_t, std::vector<void*>> pool_free;
-  std::unordered_map<void*, size_t> pool_size;
-  std::vector<void*> slabs;
+  std::unordered_map<size_t, std::vector<std::pair<void*, int>>> pool_free;   // (ptr, slab)
+  bool counted = false;   // included in gcache().n_ctx
+  const char* stage = "";   // innermost runtime stage (OOM reports)
+  struct PoolEnt { size_t cls; int slab; };
+  std::unordered_map<void*, PoolEnt> pool_size;
+  std::vector<void*> slabs;          // nullptr once reclaimed
   std::vector<size_t> slab_caps;
+  std::vector<int64_t> slab_live;    // live pool buffers per slab
+  int cur_slab = -1;
   std::unordered_map<void*, int> refcnt;   // shared block allocations
   std::set<void*> big;                      // large buffers (arena)
   std::vector<void*> big_pending;           // freed, awaiting a stream sync
@@ -250,6 +255,7 @@ struct GlobalCache {
   std::vector<std::pair<void*, size_t>> slabs;   // (ptr, bytes)
   Arena arena;
   std::vector<std::pair<char*, char*>> rings;    // (pinned, device) of RING_BYTES
+  int n_ctx = 0;                                 // live contexts (1 => frees reusable at once)
 };
 GlobalCache& gcache() {
   static GlobalCache* g = new GlobalCache();   // leaked on purpose (process lifetime)
@@ -264,6 +270,13 @@ struct HostTimer {
     *acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
 };
+struct Stage {   // tags allocations with the runtime stage making them
+  spq_ctx* c;
+  const char* prev;
+  Stage(spq_ctx* cc, const char* name) : c(cc), prev(cc->stage) { c->stage = name; }
+  ~Stage() { c->stage = prev; }
+};
+
 // Size-class pool over large cudaMalloc slabs.  All device work of a context
 // is ordered on ONE stream, so a buffer released after its last use has been
 // enqueued can be handed out again immediately (the same guarantee
@@ -280,6 +293,101 @@ size_t size_class(size_t b) {
 
 constexpr size_t BIG_ALLOC = (size_t)8 << 20;   // >= 8 MB: driver stream-ordered pool
 
+// out-of-memory: report where the memory is (live vs. pooled vs. arena
+// fragmentation) instead of a bare cudaMalloc failure
+[[noreturn]] void throw_oom(spq_ctx* c, size_t bytes, const char* what) {
+  (void)cudaGetLastError();
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  size_t afree = 0, alarge = 0, anfree = 0;
+  {
+    auto& g = gcache();
+    std::lock_guard<std::mutex> lk(g.mu);
+    for (auto& kv : g.arena.free_off) { afree += kv.second; alarge = std::max(alarge, kv.second); ++anfree; }
+  }
+  size_t pooled_free = 0;
+  for (auto& kv : c->pool_free) pooled_free += kv.first * kv.second.size();
+  const double G = 1.0 / (1 << 30);
+  char buf[768];
+  snprintf(buf, sizeof buf,
+           "out of memory (%s, %.3f GB requested): live %.2f GB, peak %.2f GB, slabs %.2f GB "
+           "(%.2f GB in free lists), arena %.2f GB with %.2f GB free in %zu ranges (largest %.3f GB), "
+           "device free %.2f of %.2f GB, stage %s",
+           what, bytes * G, c->live_bytes * G, c->peak_bytes * G, c->pool_bytes * G,
+           pooled_free * G, gcache().arena.cap * G, afree * G, anfree, alarge * G, fr * G, tot * G,
+           c->stage);
+  throw spq::CudaFailure(cudaErrorMemoryAllocation, buf, __FILE__, __LINE__);
+}
+
+void publish_big(spq_ctx* c);
+
+constexpr size_t kSlabBytes = (size_t)32 << 20;
+
+// Pool slabs whose buffers are all free go back to the arena (after one
+// stream sync, so no queued work still touches them), together with the
+// process cache of slabs left by destroyed contexts.  The recovery path of
+// an arena miss: a level's merge frees most small blocks at once, leaving
+// whole slabs empty.  Returns the bytes reclaimed.
+size_t reclaim_slabs(spq_ctx* c) {
+  std::vector<char> dead(c->slabs.size(), 0);
+  bool any = false;
+  for (size_t i = 0; i < c->slabs.size(); ++i)
+    if (c->slabs[i] && c->slab_live[i] == 0) { dead[i] = 1; any = true; }
+  auto& g = gcache();
+  {
+    std::lock_guard<std::mutex> lk(g.mu);
+    any = any || !g.slabs.empty();
+  }
+  if (!any) return 0;
+  // not sync(): that also recycles the upload ring, and this runs inside
+  // dalloc, possibly between an upload and the launch that reads it
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  publish_big(c);
+  for (auto& kv : c->pool_free) {
+    auto& v = kv.second;
+    v.erase(std::remove_if(v.begin(), v.end(), [&](const std::pair<void*, int>& e) { return dead[e.second] != 0; }),
+            v.end());
+  }
+  size_t freed = 0;
+  std::lock_guard<std::mutex> lk(g.mu);
+  for (size_t i = 0; i < c->slabs.size(); ++i) {
+    if (!dead[i]) continue;
+    if ((int)i == c->cur_slab) { c->slab_ptr = nullptr; c->cur_slab = -1; }
+    if (g.arena.owns(c->slabs[i])) g.arena.release(c->slabs[i]);
+    else cudaFree(c->slabs[i]);
+    freed += c->slab_caps[i];
+    c->pool_bytes -= c->slab_caps[i];
+    c->slabs[i] = nullptr;
+    c->slab_caps[i] = 0;
+  }
+  for (auto& e : g.slabs) {
+    if (g.arena.owns(e.first)) g.arena.release(e.first);
+    else cudaFree(e.first);
+    freed += e.second;
+  }
+  g.slabs.clear();
+  return freed;
+}
+
+// The process-wide arena takes all free HBM but a reserve (for torch and
+// other libraries in the process) at first use; SPQ_ARENA_RESERVE_GB
+// overrides the reserve.  Caller holds g.mu.
+void ensure_arena(GlobalCache& g) {
+  if (g.arena.base) return;
+  size_t fr = 0, tot = 0;
+  CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+  const char* e = getenv("SPQ_ARENA_RESERVE_GB");
+  size_t reserve = e ? (size_t)(atof(e) * (double)(1ull << 30))
+                     : std::max<size_t>((size_t)6 << 30, fr / 20);
+  size_t cap = fr > reserve ? fr - reserve : fr / 2;
+  cap &= ~(((size_t)1 << 21) - 1);
+  void* b = nullptr;
+  if (cudaMalloc(&b, cap) != cudaSuccess) { (void)cudaGetLastError(); cap = 0; b = nullptr; }
+  g.arena.base = (char*)b;
+  g.arena.cap = cap;
+  if (cap) g.arena.add_free(0, cap);
+}
+
 double* dalloc(spq_ctx* c, size_t bytes) {
   auto t0 = std::chrono::steady_clock::now();
   if (bytes >= BIG_ALLOC) {
@@ -289,23 +397,20 @@ double* dalloc(spq_ctx* c, size_t bytes) {
     {
       auto& g = gcache();
       std::lock_guard<std::mutex> lk(g.mu);
-      if (!g.arena.base) {
-        size_t fr = 0, tot = 0;
-        CUDA_TRY(cudaMemGetInfo(&fr, &tot));
-        size_t cap = (size_t)(fr * 0.55) & ~(((size_t)1 << 21) - 1);
-        void* b = nullptr;
-        if (cudaMalloc(&b, cap) != cudaSuccess) { (void)cudaGetLastError(); cap = 0; b = nullptr; }
-        g.arena.base = (char*)b;
-        g.arena.cap = cap;
-        if (cap) g.arena.add_free(0, cap);
-      }
+      ensure_arena(g);
       if (g.arena.base) {
         p = g.arena.alloc(bytes);
         if (p) got = g.arena.size_of(p);
       }
     }
+    if (!p && reclaim_slabs(c) > 0) {   // empty pool slabs back to the arena, retry
+      auto& g = gcache();
+      std::lock_guard<std::mutex> lk(g.mu);
+      p = g.arena.alloc(bytes);
+      if (p) got = g.arena.size_of(p);
+    }
     if (!p) {   // arena exhausted: dedicated allocation
-      CUDA_TRY(cudaMalloc(&p, bytes));
+      if (cudaMalloc(&p, bytes) != cudaSuccess) throw_oom(c, bytes, "large buffer");
       got = bytes;
     }
     c->big.insert(p);
@@ -318,15 +423,18 @@ double* dalloc(spq_ctx* c, size_t bytes) {
   }
   const size_t cls = size_class(bytes == 0 ? 8 : bytes);
   void* p = nullptr;
+  int sid = -1;
   auto& fl = c->pool_free[cls];
   if (!fl.empty()) {
-    p = fl.back();
+    p = fl.back().first;
+    sid = fl.back().second;
     fl.pop_back();
   } else {
     if (c->slab_ptr == nullptr || c->slab_off + cls > c->slab_cap) {
-      size_t cap = std::max<size_t>(cls, (size_t)128 << 20);
+      size_t cap = std::max<size_t>(cls, kSlabBytes);
       void* s = nullptr;
-      {
+      for (int attempt = 0; attempt < 2 && !s; ++attempt) {
+        if (attempt == 1 && reclaim_slabs(c) == 0) break;
         auto& g = gcache();
         std::lock_guard<std::mutex> lk(g.mu);
         for (size_t i = 0; i < g.slabs.size(); ++i)
@@ -336,40 +444,93 @@ double* dalloc(spq_ctx* c, size_t bytes) {
             g.slabs.erase(g.slabs.begin() + i);
             break;
           }
+        if (!s) {   // carve the slab from the arena
+          ensure_arena(g);
+          if (g.arena.base) s = g.arena.alloc(cap);
+        }
       }
-      if (!s) CUDA_TRY(cudaMalloc(&s, cap));
+      if (!s && cudaMalloc(&s, cap) != cudaSuccess) throw_oom(c, cap, "pool slab");
       c->slabs.push_back(s);
       c->slab_caps.push_back(cap);
+      c->slab_live.push_back(0);
+      c->cur_slab = (int)c->slabs.size() - 1;
       c->slab_ptr = (char*)s;
       c->slab_off = 0;
       c->slab_cap = cap;
       c->pool_bytes += cap;
     }
     p = c->slab_ptr + c->slab_off;
+    sid = c->cur_slab;
     c->slab_off += cls;
   }
-  c->pool_size[p] = cls;
+  c->pool_size[p] = spq_ctx::PoolEnt{cls, sid};
+  c->slab_live[sid]++;
   c->live_bytes += cls;
   c->peak_bytes = std::max(c->peak_bytes, c->live_bytes);
   c->n_allocs++;
   c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return (double*)p;
 }
+// Scratch whose size is a free parameter (chunk widths, WY batches): the
+// largest power-of-two fraction of `want` (>= `floor`) the arena can give
+// right now; `got` receives the size.  Falls back to dalloc at the floor.
+double* dalloc_flex(spq_ctx* c, size_t want, size_t floor, size_t* got) {
+  floor = std::min(floor, want);
+  if (want < BIG_ALLOC) {
+    *got = std::max<size_t>(want, 8);
+    return dalloc(c, *got);
+  }
+  {
+    auto& g = gcache();
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (attempt == 1 && reclaim_slabs(c) == 0) break;
+      std::lock_guard<std::mutex> lk(g.mu);
+      ensure_arena(g);
+      if (!g.arena.base) break;
+      for (size_t b = want; b >= std::max(floor, BIG_ALLOC); b /= 2) {
+        void* p = g.arena.alloc(b);
+        if (!p) continue;
+        const size_t sz = g.arena.size_of(p);
+        c->big.insert(p);
+        c->big_size[p] = sz;
+        c->live_bytes += sz;
+        c->peak_bytes = std::max(c->peak_bytes, c->live_bytes);
+        c->n_allocs++;
+        *got = b;
+        return (double*)p;
+      }
+    }
+  }
+  *got = std::max<size_t>(floor, 8);
+  return dalloc(c, *got);
+}
+
 void dfree(spq_ctx* c, void* p) {
   if (!p) return;
   auto bi = c->big.find(p);
   if (bi != c->big.end()) {
-    // published to the shared arena at this context's next stream sync
     c->big.erase(bi);
     c->live_bytes -= c->big_size[p];
     c->big_size.erase(p);
+    {
+      // sole context: all device work is ordered on its one stream, so the
+      // range can be handed out again at once (stream-ordered reuse);
+      // otherwise it is published at this context's next stream sync
+      auto& g = gcache();
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (g.n_ctx <= 1 && g.arena.owns(p)) {
+        g.arena.release(p);
+        return;
+      }
+    }
     c->big_pending.push_back(p);
     return;
   }
   auto it = c->pool_size.find(p);
   if (it == c->pool_size.end()) throw std::runtime_error("dfree of unknown pointer");
-  c->pool_free[it->second].push_back(p);
-  c->live_bytes -= it->second;
+  c->pool_free[it->second.cls].push_back({p, it->second.slab});
+  c->slab_live[it->second.slab]--;
+  c->live_bytes -= it->second.cls;
   c->pool_size.erase(it);
 }
 
@@ -650,6 +811,7 @@ struct QrProb {
   double* tau;
   double* T;  // k x k (diagonal 32-blocks written)
   std::vector<CTarget> targets;
+  bool want_T = false;   // full T even without targets (targets applied later, in chunks)
 };
 
 // full k x k T for a batch of (V, tau, T) triples: G = V^T V, blocked larft
@@ -661,6 +823,7 @@ struct TProb {
 };
 
 void build_full_T(spq_ctx* c, const std::vector<TProb>& tp) {
+  Stage stage_(c, "build_full_T");
   // G = V^T V (batched DMMA), the 32x32 diagonal blocks of T by the row
   // recurrence (one CTA per job), then recursive doubling over block pairs
   // A=[x, x+s), B=[x+s, x+2s):  T_AB = -T_AA (G_AB T_BB)   (batched GEMMs)
@@ -723,30 +886,65 @@ struct WyProb {
   int ldc, n;
 };
 
-void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs, bool transpose, int fam = F_WY) {
-  size_t tot = 0;
-  double flops = 0;
-  for (auto& p : probs) {
-    if (p.k > 0 && p.n > 0 && p.m > 0) tot += 2 * (size_t)p.k * p.n;
-    flops += 4.0 * p.m * (double)p.n * p.k - (double)p.n * p.k * p.k;
+size_t chunk_bytes() {   // SPQ_CHUNK_BYTES overrides (tests force the chunked path)
+  static size_t v = 0;
+  if (!v) {
+    const char* e = getenv("SPQ_CHUNK_BYTES");
+    v = e ? std::max<size_t>(4096, strtoull(e, nullptr, 10)) : ((size_t)2 << 30);
   }
+  return v;
+}
+
+// The (W, W2) scratch of a batch is bounded by chunk_bytes(): problems are
+// split by columns (the update is column-independent) and the batch runs in
+// consecutive groups that reuse one scratch buffer (stream order).  A level
+// of interface scalings otherwise needs 2 k n doubles for ALL its targets
+// at once (~100 GB at 64^3).
+void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs_in, bool transpose, int fam = F_WY) {
+  Stage stage_(c, "wy_batch");
   (void)fam;
-  if (tot == 0) return;
-  double* scr = dalloc(c, tot * sizeof(double));
-  GemmBatch g1, g2, g3;
-  size_t off = 0;
-  for (auto& p : probs) {
+  const size_t budget = std::max<size_t>(chunk_bytes() / sizeof(double), 2);
+  std::vector<WyProb> probs;
+  size_t tot = 0;
+  for (auto& p : probs_in) {
     if (p.k <= 0 || p.n <= 0 || p.m <= 0) continue;
-    double* W = scr + off;
-    double* W2 = W + (size_t)p.k * p.n;
-    off += 2 * (size_t)p.k * p.n;
-    g1.add(p.V, p.m, p.C, p.ldc, W, p.k, p.k, p.n, p.m, 1.0, 0.0);
-    g2.add(p.T, p.k, W, p.k, W2, p.k, p.k, p.n, p.k, 1.0, 0.0);
-    g3.add(p.V, p.m, W2, p.k, p.C, p.ldc, p.m, p.n, p.k, -1.0, 1.0);
+    const int64_t maxn = (int64_t)std::max<size_t>(1, budget / (2 * (size_t)p.k));
+    for (int64_t j0 = 0; j0 < p.n; j0 += maxn) {
+      WyProb q = p;
+      q.C = p.C + j0 * (int64_t)p.ldc;
+      q.n = (int)std::min<int64_t>(maxn, p.n - j0);
+      probs.push_back(q);
+      tot += 2 * (size_t)q.k * q.n;
+    }
   }
-  g1.run(c, true, flops);
-  g2.run(c, transpose, 0);
-  g3.run(c, false, 0);
+  if (tot == 0) return;
+  size_t need1 = 0;   // the largest single (split) problem
+  for (auto& p : probs) need1 = std::max(need1, 2 * (size_t)p.k * p.n);
+  size_t got = 0;
+  double* scr = dalloc_flex(c, std::min(tot, std::max(budget, need1)) * sizeof(double),
+                            need1 * sizeof(double), &got);
+  const size_t cap = got / sizeof(double);
+  size_t i = 0;
+  while (i < probs.size()) {
+    GemmBatch g1, g2, g3;
+    size_t off = 0;
+    double flops = 0;
+    for (; i < probs.size(); ++i) {
+      const WyProb& p = probs[i];
+      const size_t need = 2 * (size_t)p.k * p.n;
+      if (off > 0 && off + need > cap) break;
+      double* W = scr + off;
+      double* W2 = W + (size_t)p.k * p.n;
+      off += need;
+      flops += 4.0 * p.m * (double)p.n * p.k - (double)p.n * p.k * p.k;
+      g1.add(p.V, p.m, p.C, p.ldc, W, p.k, p.k, p.n, p.m, 1.0, 0.0);
+      g2.add(p.T, p.k, W, p.k, W2, p.k, p.k, p.n, p.k, 1.0, 0.0);
+      g3.add(p.V, p.m, W2, p.k, p.C, p.ldc, p.m, p.n, p.k, -1.0, 1.0);
+    }
+    g1.run(c, true, flops);
+    g2.run(c, transpose, 0);
+    g3.run(c, false, 0);
+  }
   dfree(c, scr);
 }
 
@@ -769,6 +967,7 @@ bool force_global_panel() {
 constexpr size_t SLAB_BYTES = 200 * 1024;
 
 void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
+  Stage stage_(c, "qr_batch");
   if (probs.empty()) return;
   double qr_flops = 0, wy_flops = 0;
   int maxk = 0;
@@ -836,7 +1035,7 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
   std::vector<TProb> tp;
   std::vector<WyProb> wp;
   for (auto& q : probs) {
-    if (q.k <= 0 || q.targets.empty()) continue;
+    if (q.k <= 0 || (q.targets.empty() && !q.want_T)) continue;
     tp.push_back(TProb{q.P, q.m, q.k, q.tau, q.T});
     for (auto& t : q.targets) wp.push_back(WyProb{q.P, q.T, q.m, q.k, t.C, t.ldc, t.n});
   }
@@ -918,6 +1117,7 @@ double* new_block_mem(spq_ctx* c, int nr, int nc) {
 
 // refresh row flags of every non-clean block in the given row clusters
 void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
+  Stage stage_(c, "refresh_flags");
   HostTimer ht(&c->host_ms[4]);
   std::vector<const double*> ptrs;
   std::vector<int> nr, nc;
@@ -1075,6 +1275,7 @@ bool plan_front(spq_ctx* c, int s, Front& f) {
 }
 
 void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
+  Stage stage_(c, "apply_front_structure");
   HostTimer ht(&c->host_ms[6]);
   const int s = f.s;
   // gather sources (current blocks, before any replacement)
@@ -1159,17 +1360,87 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
   retire(c, s);
 }
 
+// Fronts whose target scratch C (m x n) would exceed kChunkBytes stream
+// their targets in column chunks after the panel QR (gather -> compact-WY
+// Q^T -> scatter per chunk).  Q^T acts column by column, so the result is
+// the same as the one-shot C_all path; chunks follow column-cluster
+// boundaries, so no block is both written by one chunk and read by another.
+bool front_chunked(const Front& f) { return (size_t)f.m * f.n * sizeof(double) > chunk_bytes(); }
+size_t front_scratch_bytes(const Front& f) {
+  return front_chunked(f) ? chunk_bytes() : (size_t)f.m * f.n * sizeof(double);
+}
+
+void run_front_chunked(spq_ctx* c, Front& f) {
+  Stage stage_(c, "run_front_chunked");
+  Record& rec = c->recs[f.rec];
+  const int nct = (int)f.cols_t.size();
+  auto cend = [&](int ci) { return ci + 1 < nct ? f.woff[ci + 1] : f.n; };
+  // one chunk buffer for the whole front, as large as the arena allows
+  // (>= the widest column cluster); chunks are packed to its width
+  size_t wmin = 1;
+  for (int ci = 0; ci < nct; ++ci) wmin = std::max<size_t>(wmin, cend(ci) - f.woff[ci]);
+  const size_t colb = sizeof(double) * (size_t)f.m;
+  size_t got = 0;
+  double* Cbuf = dalloc_flex(c, std::max(chunk_bytes(), wmin * colb), wmin * colb, &got);
+  const size_t maxw = std::max<size_t>(wmin, got / colb);
+  int ci0 = 0;
+  while (ci0 < nct) {
+    int ci1 = ci0 + 1;
+    while (ci1 < nct && (size_t)(cend(ci1) - f.woff[ci0]) <= maxw) ++ci1;
+    const int a = f.woff[ci0], b = cend(ci1 - 1), w = b - a;
+    ci0 = ci1;
+    if (w <= 0) continue;
+    double* C = Cbuf;
+    CopyBatch g;
+    g.zero(C, (int64_t)f.m * w);
+    g.run(c);
+    CopyBatch g2;
+    for (auto& sg : f.gsrc) {
+      if (sg.col_off < a || sg.col_off >= b) continue;
+      auto& p = f.parts[sg.part];
+      CopyTask t{};
+      t.src = sg.p; t.dst = C + p.o0 + (int64_t)(sg.col_off - a) * f.m; t.src_rows = f.d_ix[sg.part];
+      t.nr = p.o1 - p.o0; t.nc = sg.ncols; t.lds = sg.nr; t.ldd = f.m;
+      g2.add(t);
+    }
+    g2.run(c);
+    wy_batch(c, {WyProb{rec.V, rec.T, f.m, f.k, C, f.m, w}}, true);
+    CopyBatch sc;
+    CopyTask t{};
+    t.src = C; t.dst = rec.Rsn + (int64_t)a * f.k; t.nr = f.k; t.nc = w; t.lds = f.m; t.ldd = f.k;
+    sc.add(t);
+    for (auto& d : f.dsts) {
+      const int x0 = std::max(d.col_off, a), x1 = std::min(d.col_off + d.ncols, b);
+      if (x0 >= x1) continue;
+      auto& p = f.parts[d.part];
+      CopyTask u{};
+      u.src = C + p.o0 + (int64_t)(x0 - a) * f.m;
+      u.dst = d.p + (int64_t)(x0 - d.col_off) * d.nr;
+      u.nr = p.o1 - p.o0;
+      u.nc = x1 - x0;
+      u.lds = f.m;
+      u.ldd = d.nr;
+      u.dst_rows = d.full ? nullptr : f.d_ix[d.part];
+      sc.add(u);
+    }
+    sc.run(c);
+  }
+  dfree(c, Cbuf);
+}
+
 void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotSet& ps) {
+  Stage stage_(c, "execute_wave");
   HostTimer ht(&c->host_ms[7]);
-  // scratch per front: C (m x n)
+  // scratch per (one-shot) front: C (m x n)
   size_t tot = 0;
   std::vector<size_t> coff(wave.size());
   for (size_t i = 0; i < wave.size(); ++i) {
     coff[i] = tot;
-    tot += (size_t)wave[i].m * wave[i].n;
+    if (!front_chunked(wave[i])) tot += (size_t)wave[i].m * wave[i].n;
   }
   double* scr = tot ? dalloc(c, tot * sizeof(double)) : nullptr;
-  for (size_t i = 0; i < wave.size(); ++i) zeros.zero(scr + coff[i], (int64_t)wave[i].m * wave[i].n);
+  for (size_t i = 0; i < wave.size(); ++i)
+    if (!front_chunked(wave[i])) zeros.zero(scr + coff[i], (int64_t)wave[i].m * wave[i].n);
   zeros.run(c);
   // all partial row lists of the wave in ONE upload
   std::vector<int> ixpack;
@@ -1203,6 +1474,7 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
       g.add(t);
     }
     for (auto& sg : f.gsrc) {
+      if (front_chunked(f)) break;
       auto& p = f.parts[sg.part];
       CopyTask t{};
       t.src = sg.p; t.dst = C + p.o0 + (int64_t)sg.col_off * f.m; t.src_rows = f.d_ix[sg.part];
@@ -1217,8 +1489,9 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
     Front& f = wave[fi];
     Record& rec = c->recs[f.rec];
     QrProb q{rec.V, f.m, f.k, rec.R, rec.tau, rec.T, {}};
-    if (f.n > 0) q.targets.push_back(CTarget{scr + coff[fi], f.m, f.n});
-    rec.full_T = !q.targets.empty();
+    if (f.n > 0 && !front_chunked(f)) q.targets.push_back(CTarget{scr + coff[fi], f.m, f.n});
+    q.want_T = f.n > 0 && front_chunked(f);
+    rec.full_T = f.n > 0;
     qp.push_back(std::move(q));
   }
   qr_batch(c, qp);
@@ -1231,6 +1504,7 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
   CopyBatch sc;
   for (size_t fi = 0; fi < wave.size(); ++fi) {
     Front& f = wave[fi];
+    if (front_chunked(f)) continue;
     Record& rec = c->recs[f.rec];
     double* C = scr + coff[fi];
     CopyTask t{};
@@ -1250,8 +1524,10 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
     }
   }
   sc.run(c);
+  if (scr) dfree(c, scr);
+  for (auto& f : wave)
+    if (front_chunked(f)) run_front_chunked(c, f);
   pivot_launch(c, ps);
-  dfree(c, scr);
   flush_deferred(c);
 }
 
@@ -1294,7 +1570,7 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
         if (stamp[r] == wave_id) { clash = true; break; }
       if (clash) break;
       // memory budget for the wave's front scratch (C_all) and payloads
-      const size_t fbytes = 8 * ((size_t)f.m * f.n + (size_t)f.m * f.k + (size_t)f.k * f.n);
+      const size_t fbytes = front_scratch_bytes(f) + 8 * ((size_t)f.m * f.k + (size_t)f.k * f.n);
       if (!wave.empty() && wave_bytes + fbytes > kWaveBudget) break;
       wave_bytes += fbytes;
       for (int64_t r : f.stack_rows) stamp[r] = wave_id;
@@ -1314,6 +1590,7 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
 
 // ================================================================ (b) scale
 void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
+  Stage stage_(c, "do_scale");
   HostTimer ht(&c->host_ms[11]);
   std::vector<int> todo;
   for (size_t t = 0; t < ids.size(); ++t) {
@@ -1465,6 +1742,7 @@ constexpr size_t CPQR_CTA_MAX_SMEM = 220 * 1024;
 // shared block): identical to running them one after another in order.
 void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
                       std::vector<SparsifyOut>& outs, int drop_base) {
+  Stage stage_(c, "do_sparsify_wave");
   HostTimer ht(&c->host_ms[8]);
   const int nw = (int)wave.size();
   std::vector<SpJob> J(nw);
@@ -1753,6 +2031,7 @@ void do_sparsify(spq_ctx* c, const std::vector<int>& ids, double eps,
   while (pos < ids.size()) {
     std::vector<int> wave;
     std::set<int> members;
+    size_t wave_bytes = 0;
     while (pos < ids.size()) {
       const int p = ids[pos];
       if (!c->active[p]) throw SpqError(SPQ_ERR_BAD_INPUT, "sparsify of inactive cluster");
@@ -1761,6 +2040,13 @@ void do_sparsify(spq_ctx* c, const std::vector<int>& ids, double eps,
       if (!clash)
         for (int q : c->rix[p]) if (q != p && members.count(q)) { clash = true; break; }
       if (clash) break;
+      // device scratch of the job (M and its compacted copy, np x ncols each)
+      size_t nc = 0;
+      for (int q : c->rix[p]) if (q != p) nc += c->cols_of[q].size();
+      for (int q : c->cix[p]) if (q != p) nc += c->rows_of[q].size();
+      const size_t est = 2 * sizeof(double) * c->cols_of[p].size() * nc;
+      if (!wave.empty() && wave_bytes + est > 4 * chunk_bytes()) break;
+      wave_bytes += est;
       wave.push_back(p);
       members.insert(p);
       ++pos;
@@ -1781,6 +2067,7 @@ void do_sparsify(spq_ctx* c, const std::vector<int>& ids, double eps,
 
 // ================================================================ (d) merge
 void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, const int32_t* cid) {
+  Stage stage_(c, "do_merge");
   HostTimer ht(&c->host_ms[10]);
   std::vector<int> parent_of(c->ncl, -1), roff(c->ncl, 0), coff(c->ncl, 0);
   std::vector<std::vector<int64_t>> nrows(np_), ncols(np_);
@@ -1835,47 +2122,66 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
     nparent_blocks += v.size();
   }
   c->blk.reserve(nparent_blocks * 2 + 16);
-  for (int Pi = 0; Pi < c->ncl; ++Pi) {
-    auto& v = prow_v[Pi];
-    if (v.empty()) continue;
-    const int R = (int)c->rows_of[Pi].size();
-    size_t tot = 0;
-    for (int Pj : v) tot += (size_t)R * c->cols_of[Pj].size();
-    double* slab = shared_alloc(c, tot, (int)v.size());
-    zeros.zero(slab, (int64_t)tot);
-    size_t off = 0;
-    for (int Pj : v) {
-      const int C = (int)c->cols_of[Pj].size();
-      Block& nb = put_block(c, Pi, Pj, slab + off, R, C, slab);
-      nb.clean = false;
-      off += (size_t)R * C;
-    }
-  }
+  // old blocks by parent row; a shared slab only ever holds blocks of one
+  // row cluster, so releasing a parent row's children frees whole slabs
+  std::vector<std::vector<uint64_t>> by_prow(c->ncl);
   for (uint64_t key : keys) {
     Block& B = old[key];
-    const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
-    if ((int64_t)B.nr * B.nc == 0) {
-      release_mem(c, B);
-      continue;
-    }
-    const int Pi = parent_of[i], Pj = parent_of[j];
-    Block* tgt = find_block(c, Pi, Pj);
-    const int R = (int)c->rows_of[Pi].size();
-    CopyTask x{};
-    x.src = B.p; x.dst = tgt->p + roff[i] + (int64_t)coff[j] * R; x.nr = B.nr; x.nc = B.nc;
-    x.lds = B.nr; x.ldd = R;
-    cp.add(x);
-    release_mem(c, B);
+    if ((int64_t)B.nr * B.nc == 0) { release_mem(c, B); continue; }
+    by_prow[parent_of[(int)(key >> 32)]].push_back(key);
   }
-  zeros.run(c);
-  cp.run(c);
   flush_deferred(c);
+  // parent rows in groups of bounded new storage: allocate + zero the
+  // group's slabs, copy its children in, release them (reused by the next
+  // group in stream order) -- the transient is one group, not the level
+  const size_t budget = 4 * chunk_bytes();
+  int Pi = 0;
+  while (Pi < c->ncl) {
+    CopyBatch zeros, cp;
+    size_t group = 0;
+    const int g0 = Pi;
+    for (; Pi < c->ncl; ++Pi) {
+      auto& v = prow_v[Pi];
+      if (v.empty()) continue;
+      const int R = (int)c->rows_of[Pi].size();
+      size_t tot = 0;
+      for (int Pj : v) tot += (size_t)R * c->cols_of[Pj].size();
+      if (Pi > g0 && group > 0 && (group + tot) * sizeof(double) > budget) break;
+      group += tot;
+      double* slab = shared_alloc(c, tot, (int)v.size());
+      zeros.zero(slab, (int64_t)tot);
+      size_t off = 0;
+      for (int Pj : v) {
+        const int C = (int)c->cols_of[Pj].size();
+        Block& nb = put_block(c, Pi, Pj, slab + off, R, C, slab);
+        nb.clean = false;
+        off += (size_t)R * C;
+      }
+    }
+    for (int q = g0; q < Pi; ++q)
+      for (uint64_t key : by_prow[q]) {
+        Block& B = old[key];
+        const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
+        const int Pj = parent_of[j];
+        Block* tgt = find_block(c, q, Pj);
+        const int R = (int)c->rows_of[q].size();
+        CopyTask x{};
+        x.src = B.p; x.dst = tgt->p + roff[i] + (int64_t)coff[j] * R; x.nr = B.nr; x.nc = B.nc;
+        x.lds = B.nr; x.ldd = R;
+        cp.add(x);
+        release_mem(c, B);
+      }
+    zeros.run(c);
+    cp.run(c);
+    flush_deferred(c);
+  }
 }
 
 // ================================================================== load
 void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indices,
              const double* data, int equilibrate, int ncl, int nleaf, const int32_t* leaf_ids,
              const int64_t* rptr, const int64_t* rows, const int64_t* cptr, const int64_t* cols) {
+  Stage stage_(c, "do_load");
   c->N = N;
   c->ncl = ncl;
   c->rows_of.assign(ncl, {});
@@ -2261,6 +2567,8 @@ int spq_create(spq_ctx** out, int device) {
     {
       auto& g = gcache();
       std::lock_guard<std::mutex> lk(g.mu);
+      ++g.n_ctx;
+      c->counted = true;
       if (!g.rings.empty() && !env_flag("SPQ_RING_SMALL")) {
         c->pin = g.rings.back().first;
         c->dring = g.rings.back().second;
@@ -2297,8 +2605,10 @@ void spq_destroy(spq_ctx* c) {
     {
       auto& g = gcache();
       std::lock_guard<std::mutex> lk(g.mu);
-      for (size_t i = 0; i < c->slabs.size(); ++i) g.slabs.push_back({c->slabs[i], c->slab_caps[i]});
+      for (size_t i = 0; i < c->slabs.size(); ++i)
+        if (c->slabs[i]) g.slabs.push_back({c->slabs[i], c->slab_caps[i]});
       if (c->pin && c->dring) g.rings.push_back({c->pin, c->dring});
+      if (c->counted) --g.n_ctx;
     }
     if (c->st) cudaStreamDestroy(c->st);
   } catch (...) {

@@ -4,7 +4,7 @@ sys.path.insert(0, ".")
 from paper_2010_06807_b200.factor import factorize          # noqa: E402
 from paper_2010_06807_b200.ordering import partition_geometric  # noqa: E402
 from paper_2010_06807_b200.problems import make_config      # noqa: E402
-cfg, n = sys.argv[1], int(sys.argv[2])
+cfg, n = sys.argv[1], (None if sys.argv[2] == "-" else int(sys.argv[2]))
 A, dims, L, eps, b, tol = make_config(cfg, n=n)
 class Obs:
     def on_level(self, state, lev, st):
