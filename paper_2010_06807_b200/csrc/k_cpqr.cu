@@ -856,3 +856,309 @@ void launch_power_iter(const PowerJob* d_jobs, int njobs, int fmax, cudaStream_t
 }
 
 }  // namespace spq
+
+// ============================================================ register-resident
+// Cluster threshold CPQR with the candidate matrix held in REGISTERS.
+//
+// The smem-resident kernels stream the whole m x n matrix through shared
+// memory three times per pivot step (dot, update, norm), which bounds a
+// sparsify wave at ~2 us per step.  Here a group of TPC lanes owns C
+// columns, lane s of the group holding rows s, s+TPC, ... (R per lane):
+// the per-step work is register FMAs plus log2(TPC) shuffles per column.
+// One step:
+//   cluster.sync -> every warp reads the CL per-CTA candidates (DSMEM) and
+//   picks the winner identically -> the CTA copies the winner's column
+//   (published by its owner at the end of the previous step) from the
+//   winning CTA into shared memory -> every warp forms sigma, alpha, tau,
+//   v0 identically -> v = x / v0 (a thread per row) -> each group updates
+//   its columns and their norms -> CTA argmax -> the owner group publishes
+//   the CTA's best column for the next step.
+// Logical swaps as in the other kernels (owners update the position of
+// the pivot and of the column it displaces).  Semantics: `cpqr_threshold`
+// (kernels/_numba.py:120-167), v = x / v0 like the reference.
+namespace spq {
+
+constexpr int RG_NT = 512;
+constexpr int RG_NW = RG_NT / 32;
+
+__device__ __forceinline__ unsigned long long rg_pack(int pos, int phys) {
+  return ((unsigned long long)(unsigned)pos << 32) | (unsigned)phys;
+}
+__device__ __forceinline__ bool rg_better(double v, unsigned long long k, double bv,
+                                          unsigned long long bk) {
+  return v > bv || (v == bv && (int)(k >> 32) < (int)(bk >> 32));
+}
+
+struct RgLayout {   // shared memory (doubles then keys); rows padded to mp = tpc * R
+  int m1;
+  __host__ __device__ explicit RgLayout(int mp) : m1(mp > 0 ? mp : 1) {}
+  // vbuf (m1) | candcol [2][m1] | cval [2] | wv [RG_NW] | ckey [2] | wk [RG_NW]
+  __host__ __device__ size_t bytes() const { return (size_t)(3 * m1 + 2 + RG_NW) * 8 + (2 + RG_NW) * 8 + 64; }
+};
+
+template <int R, int C>
+__global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __restrict__ jobs,
+                                                            int tpc) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int q = (int)cluster.block_rank();
+  const CpqrJob J = jobs[blockIdx.x / CL];
+  const int m = J.m;
+  const int n = J.nk ? *J.nk : J.n;
+  const double eps = *J.eps;
+  const int kmax = min(m, n);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = tid % tpc;                 // lane within the column group
+  const int grp = tid / tpc;                 // group within the CTA
+  const int cpc = (RG_NT / tpc) * C;         // columns per CTA
+  const int mp = tpc * R;                    // padded rows
+  const int ph0 = q * cpc + grp * C;         // first own physical column
+  extern __shared__ __align__(16) double rs[];
+  const RgLayout L(mp);
+  double* vbuf = rs;                         // v (zero outside rows i..m-1)
+  double* candcol = vbuf + L.m1;             // [2][m1]
+  double* cval = candcol + 2 * L.m1;         // [2]
+  double* wv = cval + 2;                     // [RG_NW]
+  unsigned long long* ckey = reinterpret_cast<unsigned long long*>(wv + RG_NW);   // [2]
+  unsigned long long* wk = ckey + 2;         // [RG_NW]
+
+  // own columns: rows sub + tpc*r (zero beyond m / beyond n)
+  double x[C][R];
+  int pos[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    pos[c] = ph0 + c;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int a = sub + tpc * r;
+      x[c][r] = (ph0 + c < n && a < m) ? J.W[a + (int64_t)(ph0 + c) * J.ldw] : 0.0;
+    }
+  }
+  for (int a = tid; a < L.m1; a += RG_NT) vbuf[a] = 0.0;
+
+  // CTA argmax over every group's (norm, position); the owner group
+  // publishes that column into candcol[slot]
+  auto publish = [&](double bv, unsigned long long bk, int slot) {
+#pragma unroll
+    for (int o = 16; o >= tpc; o >>= 1) {    // lanes of a group agree already
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      if (rg_better(ov, ok, bv, bk)) { bv = ov; bk = ok; }
+    }
+    if (lane == 0) { wv[warp] = bv; wk[warp] = bk; }
+    __syncthreads();
+    double cv = lane < RG_NW ? wv[lane] : -1.0;
+    unsigned long long ck = lane < RG_NW ? wk[lane] : rg_pack(0x7fffffff, 0);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {   // full warp: every lane must agree
+      const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, ck, o);
+      if (rg_better(ov, ok, cv, ck)) { cv = ov; ck = ok; }
+    }
+    const int cph = (int)(ck & 0xffffffffu);
+    if (cv >= 0.0 && cph >= ph0 && cph < ph0 + C) {
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (ph0 + c == cph)
+#pragma unroll
+          for (int r = 0; r < R; ++r) candcol[slot * L.m1 + sub + tpc * r] = x[c][r];
+    }
+    if (tid == 0) { cval[slot] = cv; ckey[slot] = ck; }
+  };
+
+  // initial norms (all rows)
+  {
+    double bv = -1.0;
+    unsigned long long bk = rg_pack(0x7fffffff, 0);
+    double ns[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      ns[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) ns[c] = fma(x[c][r], x[c][r], ns[c]);
+    }
+    for (int o = tpc >> 1; o; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < C; ++c) ns[c] += __shfl_xor_sync(0xffffffffu, ns[c], o);
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (ph0 + c < n) {
+        const double nv = sqrt(ns[c]);
+        const unsigned long long k = rg_pack(pos[c], ph0 + c);
+        if (rg_better(nv, k, bv, bk)) { bv = nv; bk = k; }
+      }
+    publish(bv, bk, 0);
+  }
+
+  double norm0 = 0.0;
+  int r_out = kmax;
+  for (int i = 0; i < kmax; ++i) {
+    const int slot = i & 1;
+    cluster.sync();
+    // ---- winner over the CL CTA candidates (identical in every warp)
+    double best = -1.0;
+    unsigned long long bk = rg_pack(0x7fffffff, 0);
+    int wr = 0;
+    if (lane < CL) {
+      best = cluster.map_shared_rank(cval, lane)[slot];
+      bk = cluster.map_shared_rank(ckey, lane)[slot];
+      wr = lane;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {   // full warp: every lane must agree (stop test)
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int orr = __shfl_xor_sync(0xffffffffu, wr, o);
+      if (rg_better(ov, ok, best, bk)) { best = ov; bk = ok; wr = orr; }
+    }
+    if (i == 0) {
+      norm0 = best;
+      if (norm0 == 0.0) { r_out = 0; break; }
+    } else if (best < eps * norm0 && i >= J.min_rank) {
+      r_out = i;
+      break;
+    }
+    const int lp = (int)(bk >> 32), pp = (int)(bk & 0xffffffffu);
+    // ---- winner's column rows i..m-1 into vbuf (row i-1 no longer used)
+    {
+      const double* Xr = cluster.map_shared_rank(candcol, wr) + slot * L.m1;
+      for (int a = i + tid; a < m; a += RG_NT) vbuf[a] = Xr[a];
+      if (tid == 0 && i > 0) vbuf[i - 1] = 0.0;
+    }
+    __syncthreads();
+    double sg = 0.0;
+    for (int a = i + 1 + lane; a < m; a += 32) sg = fma(vbuf[a], vbuf[a], sg);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
+    const double alpha = vbuf[i];
+    double tau, beta, v0 = 1.0;
+    const bool zero = sg == 0.0;
+    if (zero) {
+      if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+    } else {
+      beta = sqrt(alpha * alpha + sg);
+      v0 = (alpha <= 0.0) ? alpha - beta : -sg / (alpha + beta);
+      tau = -v0 / beta;
+    }
+    __syncthreads();   // every warp has read alpha / sigma from the raw column
+    for (int a = i + tid; a < m; a += RG_NT) {
+      const double va = (a == i) ? 1.0 : (zero ? 0.0 : vbuf[a] / v0);
+      vbuf[a] = va;
+      if (q == 0) J.V[a + (int64_t)i * J.ldv] = va;
+    }
+    if (q == 0 && tid == 0) { J.tau[i] = tau; J.beta[i] = beta; }
+    __syncthreads();
+    // ---- own columns: swap bookkeeping, update, norms over rows > i
+    double vr[R], mk[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      vr[r] = vbuf[sub + tpc * r];                    // zero outside rows i..m-1
+      mk[r] = (sub + tpc * r > i) ? 1.0 : 0.0;
+    }
+    bool act[C];
+    double d[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      if (ph0 + c == pp) pos[c] = i;                 // the pivot retires at position i
+      else if (pos[c] == i) pos[c] = lp;             // displaced by the swap
+      act[c] = ph0 + c < n && ph0 + c != pp && pos[c] > i;
+      d[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) d[c] = fma(vr[r], x[c][r], d[c]);
+    }
+    for (int o = tpc >> 1; o; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < C; ++c) d[c] += __shfl_xor_sync(0xffffffffu, d[c], o);
+    double ns[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const double w = act[c] ? tau * d[c] : 0.0;
+      ns[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        x[c][r] = fma(-w, vr[r], x[c][r]);
+        ns[c] = fma(mk[r] * x[c][r], x[c][r], ns[c]);
+      }
+    }
+    for (int o = tpc >> 1; o; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < C; ++c) ns[c] += __shfl_xor_sync(0xffffffffu, ns[c], o);
+    double bv = -1.0;
+    unsigned long long bkk = rg_pack(0x7fffffff, 0);
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (act[c]) {
+        const double nv = sqrt(ns[c]);
+        const unsigned long long k = rg_pack(pos[c], ph0 + c);
+        if (rg_better(nv, k, bv, bkk)) { bv = nv; bkk = k; }
+      }
+    publish(bv, bkk, slot ^ 1);
+  }
+  if (q == 0 && tid == 0) *J.rank = r_out;
+  if (sub == 0)
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (ph0 + c < n) J.perm[pos[c]] = ph0 + c;
+  cluster.sync();   // no CTA leaves while others may read its shared memory
+}
+
+// variant v: (R, C) = (16,2), (8,4), (4,8); returns cluster size or 0
+int cpqr_reg_plan(int m, int n, int v, int* tpc_out) {
+  static const int RR[3] = {16, 8, 4}, CC[3] = {2, 4, 8};
+  static int clmax = -1;
+  if (clmax < 0) {
+    const char* e = getenv("SPQ_CPQR_CLMAX");
+    clmax = e ? atoi(e) : 16;
+  }
+  if (m <= 0 || n <= 0) return 0;
+  const int R = RR[v], C = CC[v];
+  int tpc = 1;
+  while (tpc * R < m) tpc *= 2;
+  if (tpc > 32) return 0;
+  const int cpc = (RG_NT / tpc) * C;
+  int cl = 1;
+  while (cl * cpc < n) cl *= 2;
+  if (cl > clmax || cl > 16) return 0;
+  *tpc_out = tpc;
+  return cl;
+}
+
+size_t cpqr_reg_smem(int mp) { return RgLayout(mp).bytes(); }   // mp = tpc * R
+
+template <int R, int C>
+static void launch_rg(const CpqrJob* d_jobs, int njobs, int cl, int tpc, size_t smem, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    CUDA_TRY(cudaFuncSetAttribute(cpqr_reg_kernel<R, C>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(cpqr_reg_kernel<R, C>,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    init = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(njobs * cl));
+  cfg.blockDim = dim3(RG_NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg_kernel<R, C>, d_jobs, tpc));
+}
+
+void launch_cpqr_reg(const CpqrJob* d_jobs, int njobs, int v, int cl, int tpc, size_t smem,
+                     cudaStream_t st) {
+  if (njobs <= 0) return;
+  switch (v) {
+    case 0: launch_rg<16, 2>(d_jobs, njobs, cl, tpc, smem, st); break;
+    case 1: launch_rg<8, 4>(d_jobs, njobs, cl, tpc, smem, st); break;
+    case 2: launch_rg<4, 8>(d_jobs, njobs, cl, tpc, smem, st); break;
+    default: throw std::runtime_error("cpqr_reg: bad variant");
+  }
+}
+
+}  // namespace spq

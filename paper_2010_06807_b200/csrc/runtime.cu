@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -159,6 +160,9 @@ struct spq_ctx {
   // device memory pool
   std::unordered_map<size_t, std::vector<std::pair<void*, int>>> pool_free;   // (ptr, slab)
   bool counted = false;   // included in gcache().n_ctx
+  static constexpr int NAUX = 4;
+  cudaStream_t aux[NAUX] = {};               // fork-join streams for independent launches
+  cudaEvent_t ev_fork = nullptr, ev_join[NAUX] = {};
   const char* stage = "";   // innermost runtime stage (OOM reports)
   struct PoolEnt { size_t cls; int slab; };
   std::unordered_map<void*, PoolEnt> pool_size;
@@ -611,6 +615,37 @@ void flush_deferred(spq_ctx* c) {
   for (double* p : c->deferred) dfree(c, p);
   c->deferred.clear();
 }
+
+// fork-join: independent launches on auxiliary streams that start after
+// everything queued so far on the context stream and are joined back
+// before anything after them (all buffers they touch stay stream-ordered)
+struct Fork {
+  spq_ctx* c;
+  int used = 0;
+  explicit Fork(spq_ctx* cc) : c(cc) {
+    if (!c->ev_fork) {
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      for (int k = 0; k < spq_ctx::NAUX; ++k) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming));
+      }
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_fork, c->st));
+  }
+  cudaStream_t next() {
+    const int k = used % spq_ctx::NAUX;
+    if (used < spq_ctx::NAUX) CUDA_TRY(cudaStreamWaitEvent(c->aux[k], c->ev_fork, 0));
+    ++used;
+    return c->aux[k];
+  }
+  void join() {
+    for (int k = 0; k < std::min(used, spq_ctx::NAUX); ++k) {
+      CUDA_TRY(cudaEventRecord(c->ev_join[k], c->aux[k]));
+      CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_join[k], 0));
+    }
+    used = 0;
+  }
+};
 
 struct Scope {
   spq_ctx* c;
@@ -1793,14 +1828,9 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       g.add(x);
       off += b->nc;
     }
-    j.cta = cpqr_cta_smem(j.np, std::max(j.ncols, 1)) <= CPQR_CTA_MAX_SMEM &&
-            !env_flag("SPQ_CPQR_COOP") && !env_flag("SPQ_CPQR_CLUSTER");
-    j.cl = (j.cta || env_flag("SPQ_CPQR_COOP")) ? 0 : cpqr_cluster_size(j.np, std::max(j.ncols, 1));
   }
   g.run(c);
   SpScal* dsc = (SpScal*)dalloc(c, std::max(nw, 1) * sizeof(SpScal));
-  std::vector<CpqrJob> cj;
-  size_t cta_smem = 0;
   {
     Scope s(c, F_CPQR);
     for (int t = 0; t < nw; ++t) {
@@ -1810,49 +1840,106 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
                            &dsc[t].maxcol, j.Wm, c->st);
       c->tm.launches[F_CPQR] += 3;
       c->n_kernels += 3;
-      if (j.cta) {
-        CpqrJob q{};
-        q.W = j.Wm; q.m = j.np; q.n = j.ncols; q.ncap = std::max(j.ncols, 1); q.ldw = j.np;
-        q.nk = &dsc[t].nk; q.eps = &dsc[t].ratio; q.min_rank = 0; q.V = j.V; q.ldv = j.np;
-        q.tau = j.tau; q.beta = j.beta; q.rank = &dsc[t].rank; q.perm = j.perm; q.write_back = 0;
-        cj.push_back(q);
-        cta_smem = std::max(cta_smem, cpqr_cta_smem(j.np, std::max(j.ncols, 1)));
+    }
+  }
+  // the kept column counts (one read per wave) size every CPQR exactly
+  std::vector<SpScal> hk(std::max(nw, 1));
+  {
+    HostTimer hw(&c->host_ms[9]);
+    CUDA_TRY(cudaMemcpyAsync(hk.data(), dsc, nw * sizeof(SpScal), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+  }
+  const bool coop_only = env_flag("SPQ_CPQR_COOP"), no_ws = env_flag("SPQ_CPQR_NOWS");
+  auto job_of = [&](int t, int ncap) {
+    SpJob& j = J[t];
+    CpqrJob q{};
+    q.W = j.Wm; q.m = j.np; q.n = j.ncols; q.ncap = ncap; q.ldw = j.np;
+    q.nk = &dsc[t].nk; q.eps = &dsc[t].ratio; q.min_rank = 0; q.V = j.V; q.ldv = j.np;
+    q.tau = j.tau; q.beta = j.beta; q.rank = &dsc[t].rank; q.perm = j.perm; q.write_back = 0;
+    return q;
+  };
+  std::map<std::tuple<int, int, int>, std::pair<std::vector<CpqrJob>, size_t>> rg_groups;   // (variant, cl, tpc)
+  std::map<int, std::pair<std::vector<CpqrJob>, size_t>> by_cl;
+  std::vector<CpqrJob> cj;
+  std::vector<int> coop;
+  size_t cta_smem = 0;
+  for (int t = 0; t < nw; ++t) {
+    SpJob& j = J[t];
+    if (j.np == 0) continue;
+    const int ncap = std::max(hk[t].nk, 1);
+    // register-resident kernel: smallest cluster, then least row padding
+    int bv = -1, bcl = 0, btpc = 0;
+    if (!coop_only && !no_ws)
+      for (int v = 0; v < 3; ++v) {
+        int tpc = 0;
+        const int cl = cpqr_reg_plan(j.np, ncap, v, &tpc);
+        if (cl == 0) continue;
+        static const int RR[3] = {16, 8, 4};
+        if (bv < 0 || cl < bcl || (cl == bcl && tpc * RR[v] < btpc * RR[bv])) { bv = v; bcl = cl; btpc = tpc; }
       }
+    if (bv >= 0) {
+      auto& g = rg_groups[std::make_tuple(bv, bcl, btpc)];
+      g.first.push_back(job_of(t, ncap));
+      static const int RRv[3] = {16, 8, 4};
+      g.second = std::max(g.second, cpqr_reg_smem(btpc * RRv[bv]));
+      continue;
     }
-    if (!cj.empty()) {
-      launch_cpqr_cta(upload(c, cj), (int)cj.size(), cta_smem, c->st);
+    if (!coop_only && !env_flag("SPQ_CPQR_CLUSTER") && cpqr_cta_smem(j.np, ncap) <= CPQR_CTA_MAX_SMEM) {
+      cj.push_back(job_of(t, ncap));
+      cta_smem = std::max(cta_smem, cpqr_cta_smem(j.np, ncap));
+      continue;
+    }
+    const int cl = coop_only ? 0 : cpqr_cluster_size(j.np, ncap);
+    if (cl > 0) {
+      auto& g2 = by_cl[cl];
+      g2.first.push_back(job_of(t, ncap));
+      g2.second = std::max(g2.second, cpqr_cluster_smem(j.np, ncap, cl));
+      continue;
+    }
+    coop.push_back(t);
+  }
+  {
+    Scope s(c, F_CPQR);
+    // upload every job list first (the ring), then fork
+    std::vector<std::tuple<const CpqrJob*, int, std::tuple<int, int, int>, size_t>> wl;
+    for (auto& kv : rg_groups)
+      wl.emplace_back(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first,
+                      kv.second.second);
+    std::vector<std::tuple<const CpqrJob*, int, int, size_t>> cl_l;
+    for (auto& kv : by_cl)
+      cl_l.emplace_back(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first,
+                        kv.second.second);
+    const CpqrJob* d_cj = cj.empty() ? nullptr : upload(c, cj);
+    Fork fk(c);
+    for (auto& w : wl) {
+      const auto& key = std::get<2>(w);
+      launch_cpqr_reg(std::get<0>(w), std::get<1>(w), std::get<0>(key), std::get<1>(key),
+                      std::get<2>(key), std::get<3>(w), fk.next());
       c->tm.launches[F_CPQR]++;
       c->n_kernels++;
     }
-    std::map<int, std::pair<std::vector<CpqrJob>, size_t>> by_cl;
-    for (int t = 0; t < nw; ++t) {
-      SpJob& j = J[t];
-      if (j.np == 0 || j.cta || j.cl == 0) continue;
-      CpqrJob q{};
-      q.W = j.Wm; q.m = j.np; q.n = j.ncols; q.ncap = std::max(j.ncols, 1); q.ldw = j.np;
-      q.nk = &dsc[t].nk; q.eps = &dsc[t].ratio; q.min_rank = 0; q.V = j.V; q.ldv = j.np;
-      q.tau = j.tau; q.beta = j.beta; q.rank = &dsc[t].rank; q.perm = j.perm; q.write_back = 0;
-      auto& g2 = by_cl[j.cl];
-      g2.first.push_back(q);
-      g2.second = std::max(g2.second, cpqr_cluster_smem(j.np, std::max(j.ncols, 1), j.cl));
-    }
-    for (auto& kv : by_cl) {
-      launch_cpqr_cluster(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first,
-                          kv.second.second, c->st);
+    for (auto& w : cl_l) {
+      launch_cpqr_cluster(std::get<0>(w), std::get<1>(w), std::get<2>(w), std::get<3>(w), fk.next());
       c->tm.launches[F_CPQR]++;
       c->n_kernels++;
     }
-    for (int t = 0; t < nw; ++t) {
+    if (d_cj) {
+      launch_cpqr_cta(d_cj, (int)cj.size(), cta_smem, fk.next());
+      c->tm.launches[F_CPQR]++;
+      c->n_kernels++;
+    }
+    fk.join();
+    for (int t : coop) {
       SpJob& j = J[t];
-      if (j.np == 0 || j.cta || j.cl > 0) continue;
-      const int G = cpqr_grid(std::max(j.ncols, 1), c->nsm);
+      const int ncap = std::max(hk[t].nk, 1);
+      const int G = cpqr_grid(ncap, c->nsm);
       double* slots = dalloc(c, 2 * G * sizeof(double));
       int* slotp = (int*)dalloc(c, 2 * G * sizeof(int));
       CpqrArgs a{};
-      a.gmaps = (int*)dalloc(c, (size_t)G * 2 * std::max(j.ncols, 1) * sizeof(int));
+      a.gmaps = (int*)dalloc(c, (size_t)G * 2 * ncap * sizeof(int));
       a.force_gmaps = env_flag("SPQ_CPQR_GMAPS");
       c->deferred.push_back((double*)a.gmaps);
-      a.W = j.Wm; a.m = j.np; a.ncols_cap = std::max(j.ncols, 1); a.nk = &dsc[t].nk;
+      a.W = j.Wm; a.m = j.np; a.ncols_cap = ncap; a.nk = &dsc[t].nk;
       a.eps = &dsc[t].ratio; a.min_rank = 0; a.V = j.V; a.tau = j.tau; a.beta = j.beta;
       a.rank = &dsc[t].rank; a.perm = j.perm; a.slot_val = slots; a.slot_pos = slotp;
       a.finalize = 0;
@@ -2610,6 +2697,11 @@ void spq_destroy(spq_ctx* c) {
       if (c->pin && c->dring) g.rings.push_back({c->pin, c->dring});
       if (c->counted) --g.n_ctx;
     }
+    for (int k = 0; k < spq_ctx::NAUX; ++k) {
+      if (c->aux[k]) { cudaStreamSynchronize(c->aux[k]); cudaStreamDestroy(c->aux[k]); }
+      if (c->ev_join[k]) cudaEventDestroy(c->ev_join[k]);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->st) cudaStreamDestroy(c->st);
   } catch (...) {
   }

@@ -21,6 +21,8 @@ SWITCHES = {
     "cooperative_cpqr": {"SPQ_CPQR_COOP": "1"},
     "cooperative_cpqr_global_maps": {"SPQ_CPQR_COOP": "1", "SPQ_CPQR_GMAPS": "1"},
     "no_cluster_cpqr": {"SPQ_CPQR_CLMAX": "0"},
+    "legacy_cpqr_kernels": {"SPQ_CPQR_NOWS": "1"},
+    "legacy_cpqr_no_cta": {"SPQ_CPQR_NOWS": "1", "SPQ_CPQR_CLUSTER": "1"},
     "small_upload_ring": {"SPQ_RING_SMALL": "1"},
     "gemm_v1": {"SPQ_GEMM": "1"},
 }
