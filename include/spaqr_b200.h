@@ -10,7 +10,8 @@
  *
  * Status codes mirror the reference's exit codes (pkg/src/nestqr/errors.py:3-6):
  *   SPQ_OK 0, SPQ_ERR_SINGULAR 3 (SingularPivotError), SPQ_ERR_BAD_INPUT 4
- *   (NestqrError), SPQ_ERR_CUDA 5, SPQ_ERR_INTERNAL 6.  Details of the last
+ *   (NestqrError), SPQ_ERR_CUDA 5, SPQ_ERR_INTERNAL 6, SPQ_ERR_SPECULATION 7
+ *   (speculative row flags were wrong: redo with speculate=0).  Details of the last
  *   failure via spq_last_error().
  * Ownership: the context owns all device memory; host arrays are borrowed
  * for the duration of a call.  Threading: one context per host thread; all
@@ -30,6 +31,7 @@ extern "C" {
 #define SPQ_ERR_BAD_INPUT 4
 #define SPQ_ERR_CUDA 5
 #define SPQ_ERR_INTERNAL 6
+#define SPQ_ERR_SPECULATION 7
 
 typedef struct spq_ctx spq_ctx;
 
@@ -43,6 +45,15 @@ void spq_destroy(spq_ctx* ctx);
 /* last error: code, pivot index, pivot value, message (context string) */
 int spq_last_error(spq_ctx* ctx, int* code, int64_t* index, double* value,
                    char* msg, int msglen);
+/* options (before spq_load):
+ *   "speculate" (default 1): the host PREDICTS the per-row nonzero flags that
+ *   decide panel row subsets and present column clusters (factor.py:422,
+ *   454: np.any) from the symbolic effect of each update instead of reading
+ *   them back after every factor wave; the device checks every prediction
+ *   in stream order at the point it is used and spq_finish returns
+ *   SPQ_ERR_SPECULATION if any was wrong (the host then redoes the
+ *   factorization with speculate=0, which reads the flags back exactly). */
+int spq_set_option(spq_ctx* ctx, const char* key, int64_t value);
 
 /* -------------------------------------------------- (d) state construction
  * Replaces TrailingState.__init__ (factor.py:328-374) and
@@ -94,6 +105,11 @@ int spq_cluster_sizes(spq_ctx* ctx, int n, const int32_t* ids, int64_t* ncols);
 int spq_total_cols(spq_ctx* ctx, int64_t* out);
 /* trailing_blocks and trailing_nnz (exact nonzero count, device reduction) */
 int spq_trailing_stats(spq_ctx* ctx, int64_t* nblocks, int64_t* nnz);
+/* same statistics without a host round trip: trailing_blocks is returned at
+ * once, trailing_nnz is counted on the device into `slot` (0..4095) and read
+ * for slots [0, n) by spq_trailing_nnz (one synchronization). */
+int spq_trailing_stats_async(spq_ctx* ctx, int slot, int64_t* nblocks);
+int spq_trailing_nnz(spq_ctx* ctx, int n, int64_t* out);
 int spq_row_of_col(spq_ctx* ctx, int64_t* out);
 int spq_payload_scalars(spq_ctx* ctx, int64_t* out);
 /* per kernel family [ms, algorithmic flops, launches, bytes] x 7 families

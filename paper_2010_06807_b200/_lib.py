@@ -12,7 +12,7 @@ import os
 
 import numpy as np
 
-from .errors import (SPQ_ERR_BAD_INPUT, SPQ_ERR_SINGULAR, DeviceError, NestqrError,
+from .errors import (SPQ_ERR_BAD_INPUT, SPQ_ERR_SINGULAR, SPQ_ERR_SPECULATION, SpeculationError, DeviceError, NestqrError,
                      SingularPivotError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -32,6 +32,7 @@ SIGNATURES = {
     "spq_destroy": (None, [_ctx]),
     "spq_last_error": (C.c_int, [_ctx, C.POINTER(C.c_int), C.POINTER(C.c_int64),
                                  C.POINTER(C.c_double), C.c_char_p, C.c_int]),
+    "spq_set_option": (C.c_int, [_ctx, C.c_char_p, C.c_int64]),
     "spq_load": (C.c_int, [_ctx, C.c_int64, _i64p, _i64p, _f64p, C.c_int, C.c_int, C.c_int,
                            _i32p, _i64p, _i64p, _i64p, _i64p]),
     "spq_factor": (C.c_int, [_ctx, C.c_int, _i32p]),
@@ -43,6 +44,8 @@ SIGNATURES = {
     "spq_cluster_sizes": (C.c_int, [_ctx, C.c_int, _i32p, _i64p]),
     "spq_total_cols": (C.c_int, [_ctx, C.POINTER(C.c_int64)]),
     "spq_trailing_stats": (C.c_int, [_ctx, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "spq_trailing_stats_async": (C.c_int, [_ctx, C.c_int, C.POINTER(C.c_int64)]),
+    "spq_trailing_nnz": (C.c_int, [_ctx, C.c_int, _i64p]),
     "spq_row_of_col": (C.c_int, [_ctx, _i64p]),
     "spq_payload_scalars": (C.c_int, [_ctx, C.POINTER(C.c_int64)]),
     "spq_timings": (C.c_int, [_ctx, _f64p, C.c_int]),
@@ -120,6 +123,8 @@ class Context:
             raise SingularPivotError(int(idx.value), float(val.value), text)
         if rc == SPQ_ERR_BAD_INPUT:
             raise NestqrError(text)
+        if rc == SPQ_ERR_SPECULATION:
+            raise SpeculationError(text)
         raise DeviceError(f"native error {rc}: {text}")
 
     def call(self, name, *args):
@@ -144,7 +149,7 @@ class Context:
 
     def timings(self):
         nf = len(TIMING_FAMILIES)
-        buf = np.zeros(4 * nf + 22)
+        buf = np.zeros(4 * nf + 25)
         self.call("spq_timings", buf, int(buf.size))
         out = {f: {"ms": buf[4 * i], "flops": buf[4 * i + 1], "launches": int(buf[4 * i + 2]),
                    "bytes": buf[4 * i + 3]}
@@ -157,7 +162,9 @@ class Context:
                        "wave_exec_ms": h[11], "sparsify_ms": h[12], "sparsify_wait_ms": h[13],
                        "merge_ms": h[14], "scale_ms": h[15], "pivot_wait_ms": h[16],
                        "stats_ms": h[17], "load_ms": h[18], "finish_ms": h[19],
-                       "live_bytes": int(h[20]), "peak_bytes": int(h[21])}
+                       "live_bytes": int(h[20]), "peak_bytes": int(h[21]),
+                       "speculate": int(h[22]), "verified_blocks": int(h[23]),
+                       "spec_mismatch": int(h[24])}
         return out
 
 

@@ -153,6 +153,9 @@ namespace spq {
 void launch_copy(const CopyTask* d_tasks, int ntasks, int64_t max_elems, cudaStream_t st);
 void launch_rowflags(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
                      const int64_t* d_off, unsigned char* d_out, int nblk, cudaStream_t st);
+void launch_rowflags_verify(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
+                            const int64_t* d_off, const unsigned char* d_pred, int nblk, int* d_bad,
+                            cudaStream_t st);
 void launch_count_nnz(const double* const* d_ptrs, const int64_t* d_sizes, int nblk,
                       unsigned long long* d_count, cudaStream_t st);
 void launch_colnorms_scale(const int64_t* indptr, const int64_t* indices, double* data,
@@ -166,6 +169,9 @@ void gemm_set_variant(int v);   // 0 default, 1: 64x64 tiles, 2: 128x64 tiles
 void launch_splitk_reduce(const SplitRed* d_tasks, int ntasks, int64_t max_mn, cudaStream_t st);
 void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t slab_elems,
                      bool smem, int kbmax, cudaStream_t st);
+void launch_panel_qr_reg(const PanelJob* d_jobs, int njobs, int cluster, int rows_per_thread,
+                         int kbmax, cudaStream_t st);
+int panel_reg_kbmax(int kb);
 void launch_larft(const LarftJob* d_jobs, int njobs, int total_tiles, cudaStream_t st);
 int larft_tiles(int k);
 void launch_pivot_check(const PivotJob* d_jobs, int njobs, int64_t* d_err_idx,

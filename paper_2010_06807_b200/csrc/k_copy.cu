@@ -72,6 +72,38 @@ void launch_rowflags(const double* const* d_ptrs, const int* d_nr, const int* d_
   rowflags_kernel<<<nblk, 128, 0, st>>>(d_ptrs, d_nr, d_nc, d_off, d_out); SPQ_LAUNCH_CHECK();
 }
 
+// Speculative-mode check: the row flags the host PREDICTED (pred) against
+// the block values; every mismatching row adds one to *bad.
+__global__ void __launch_bounds__(128) rowflags_verify_kernel(const double* const* __restrict__ ptrs,
+                                                              const int* __restrict__ nr,
+                                                              const int* __restrict__ nc,
+                                                              const int64_t* __restrict__ off,
+                                                              const unsigned char* __restrict__ pred,
+                                                              int* bad) {
+  const int b = blockIdx.x;
+  const double* p = ptrs[b];
+  const int R = nr[b], C = nc[b];
+  const unsigned char* q = pred + off[b];
+  int miss = 0;
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    unsigned char f = 0;
+    for (int j = 0; j < C; ++j) {
+      if (p[i + (int64_t)j * R] != 0.0) { f = 1; break; }
+    }
+    miss += (f != q[i]);
+  }
+  for (int o = 16; o; o >>= 1) miss += __shfl_xor_sync(0xffffffffu, miss, o);
+  if ((threadIdx.x & 31) == 0 && miss) atomicAdd(bad, miss);
+}
+
+void launch_rowflags_verify(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
+                            const int64_t* d_off, const unsigned char* d_pred, int nblk, int* d_bad,
+                            cudaStream_t st) {
+  if (nblk <= 0) return;
+  rowflags_verify_kernel<<<nblk, 128, 0, st>>>(d_ptrs, d_nr, d_nc, d_off, d_pred, d_bad);
+  SPQ_LAUNCH_CHECK();
+}
+
 __global__ void __launch_bounds__(256) count_nnz_kernel(const double* const* __restrict__ ptrs,
                                                         const int64_t* __restrict__ sizes,
                                                         unsigned long long* count) {

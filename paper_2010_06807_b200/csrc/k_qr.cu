@@ -233,6 +233,277 @@ void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t sla
     CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_qr_kernel<false>, d_jobs));
 }
 
+// ------------------------------------------------------- register panel QR
+// Same algorithm and conventions as panel_qr_kernel, with the 32-column
+// block held in REGISTERS: thread t of CTA q owns local rows t + 256 r
+// (r < R) of the CTA's row range, all 32 columns.  Per column step:
+//   * partial dots x.a_c for all 32 columns are thread-local FMAs,
+//   * a warp reduce-scatter (31 shuffles) leaves lane l with the warp sum of
+//     column l, 8 warp partials are summed through shared memory, CTA
+//     partials over DSMEM (one barrier.cluster),
+//   * the rank-1 update is thread-local.
+// No shared-memory traffic proportional to the panel (the smem kernel
+// streams the slab through shared memory twice per column).  Requires
+// rows-per-CTA >= 32 so every pivot row lives in CTA 0 (thread jj).
+constexpr int QRR_NT = 256;
+
+struct QrrShared {
+  double X[2][1 + 2 * QR_NB];       // [1+c]: CTA partial dot, [33+c]: pivot row
+  double red[QRR_NT / 32][QR_NB];
+  double dtot[QR_NB], apiv[QR_NB];
+  double Gs[QR_NB * (QR_NB + 1)];
+};
+
+struct QrrCtx {
+  int q, CL, nloc, tid, lane, warp, kb, j0;
+  double* tau;
+};
+
+// one column step (JJ is a compile-time column so the register block is
+// indexed statically)
+template <int R, int JJ>
+__device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB], QrrShared& sh,
+                                         cg::cluster_group& cluster) {
+  const int q = x.q, CL = x.CL, nloc = x.nloc, tid = x.tid, lane = x.lane, warp = x.warp;
+  double* Xb = sh.X[JJ & 1];
+  (void)q;
+  // ---- partial dots of the pivot column (rows strictly below the pivot)
+  double d[QR_NB];
+#pragma unroll
+  for (int c = 0; c < QR_NB; ++c) d[c] = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + QRR_NT * r;
+    if (i < nloc && (q > 0 || i > JJ)) {
+      const double xv = a[r][JJ];
+#pragma unroll
+      for (int c = 0; c < QR_NB; ++c) d[c] = fma(xv, a[r][c], d[c]);
+    }
+  }
+  // ---- warp reduce-scatter: lane l ends with the warp sum of column l
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool hi = (lane & h) != 0;
+#pragma unroll
+    for (int t = 0; t < h; ++t) {
+      const double send = hi ? d[t] : d[t + h];
+      const double keep = hi ? d[t + h] : d[t];
+      d[t] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  sh.red[warp][lane] = d[0];
+  if (q == 0 && tid == JJ) {
+#pragma unroll
+    for (int c = 0; c < QR_NB; ++c) Xb[1 + QR_NB + c] = a[0][c];
+  }
+  __syncthreads();
+  if (tid < QR_NB) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < QRR_NT / 32; ++w) s += sh.red[w][tid];
+    Xb[1 + tid] = s;
+  }
+  // CTA partials over DSMEM (a 1-CTA cluster reads its own shared memory);
+  // branch-free so the shuffles are not lowered as collectives
+  cluster.sync();
+  {
+    const double* src = cluster.map_shared_rank(Xb, lane < CL ? lane : 0);
+    const double* piv = cluster.map_shared_rank(Xb, 0);
+#pragma unroll
+    for (int cc = 0; cc < QR_NB / (QRR_NT / 32); ++cc) {
+      const int c = warp + cc * (QRR_NT / 32);
+      double v = src[1 + c];
+      v = lane < CL ? v : 0.0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        sh.dtot[c] = v;
+        sh.apiv[c] = piv[1 + QR_NB + c];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- reflector scalars (every thread, identical inputs)
+  const double sigma = sh.dtot[JJ];
+  const double alpha = sh.apiv[JJ];
+  double tau, beta, v0 = 1.0;
+  const bool zero = sigma == 0.0;
+  if (zero) {
+    if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+  } else {
+    beta = sqrt(alpha * alpha + sigma);
+    v0 = (alpha <= 0.0) ? alpha - beta : -sigma / (alpha + beta);
+    tau = -v0 / beta;
+  }
+  // one reciprocal per step (x / v0 -> x * (1/v0): within an ulp of the
+  // reference's division, far inside the parity tolerance)
+  const double inv0 = zero ? 0.0 : 1.0 / v0;
+  if (q == 0 && tid == 0 && JJ < x.kb) x.tau[x.j0 + JJ] = tau;
+  if (tid < JJ) sh.Gs[tid + JJ * (QR_NB + 1)] = sh.apiv[tid] + sh.dtot[tid] * inv0;
+  // ---- v below the pivot, rank-1 update of the columns right of it
+  double v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + QRR_NT * r;
+    v[r] = 0.0;
+    if (q == 0 && r == 0 && i == JJ) {
+      v[r] = 1.0;
+      a[r][JJ] = beta;
+    } else if (i < nloc && (q > 0 || i > JJ)) {
+      v[r] = a[r][JJ] * inv0;
+      a[r][JJ] = v[r];
+    }
+  }
+  if (tau != 0.0) {
+#pragma unroll
+    for (int c = JJ + 1; c < QR_NB; ++c) {
+      const double wc = tau * fma(sh.dtot[c], inv0, sh.apiv[c]);
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r][c] = fma(-wc, v[r], a[r][c]);
+    }
+  }
+}
+
+// Steps JJ in [0, KBMAX) run unconditionally (a branch around the
+// shuffles would make the compiler lower every shuffle as a collective);
+// steps JJ >= kb see an all-zero column: tau = 0, no update, nothing stored.
+template <int R, int JJ, int KBMAX>
+struct QrrSteps {
+  static __device__ __forceinline__ void run(const QrrCtx& x, double (&a)[R][QR_NB], QrrShared& sh,
+                                             cg::cluster_group& cluster) {
+    qrr_step<R, JJ>(x, a, sh, cluster);
+    QrrSteps<R, JJ + 1, KBMAX>::run(x, a, sh, cluster);
+  }
+};
+template <int R, int KBMAX>
+struct QrrSteps<R, KBMAX, KBMAX> {
+  static __device__ __forceinline__ void run(const QrrCtx&, double (&)[R][QR_NB], QrrShared&,
+                                             cg::cluster_group&) {}
+};
+
+template <int R, int KBMAX>
+__global__ void __launch_bounds__(QRR_NT, 1) panel_qr_reg_kernel(const PanelJob* __restrict__ jobs) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int q = (int)cluster.block_rank();
+  const PanelJob J = jobs[blockIdx.x / CL];
+  const int m = J.m, k = J.k, j0 = J.j0, kb = J.kb;
+  const int mh = m - j0;
+  const int rpc = (mh + CL - 1) / CL;
+  const int r0 = min(mh, q * rpc);
+  const int r1 = min(mh, r0 + rpc);
+  const int nloc = r1 - r0;
+  const int tid = threadIdx.x;
+  __shared__ QrrShared sh;
+
+  double* P0 = J.P + (int64_t)j0 * m + j0 + r0;
+  double a[R][QR_NB];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + QRR_NT * r;
+#pragma unroll
+    for (int c = 0; c < QR_NB; ++c)
+      a[r][c] = (i < nloc && c < kb) ? P0[i + (int64_t)c * m] : 0.0;
+  }
+  if (q == 0 && j0 > 0) {   // finished R entries above the block
+    for (int e = tid; e < j0 * kb; e += QRR_NT) {
+      const int i = e % j0, c = e / j0;
+      double* src = J.P + i + (int64_t)(j0 + c) * m;
+      J.R[i + (int64_t)(j0 + c) * k] = *src;
+      *src = 0.0;
+    }
+  }
+  const QrrCtx x{q, CL, nloc, tid, tid & 31, tid >> 5, kb, j0, J.tau};
+  QrrSteps<R, 0, KBMAX>::run(x, a, sh, cluster);
+
+  // R entries of the diagonal block out, explicit unit-lower V in
+  if (q == 0 && tid < kb) {
+#pragma unroll
+    for (int c = 0; c < QR_NB; ++c) {
+      if (c >= tid && c < kb) {
+        J.R[(j0 + tid) + (int64_t)(j0 + c) * k] = a[0][c];
+        a[0][c] = (c == tid) ? 1.0 : 0.0;
+      }
+    }
+  }
+  __syncthreads();
+  // T_b from the Gram columns: row-parallel recurrence (trow in shared
+  // memory: a register array indexed by the thread's row would spill)
+  if (q == 0 && tid < kb) {
+    const int ar = tid;
+    double tr[QR_NB];
+#pragma unroll
+    for (int b = 0; b < QR_NB; ++b) tr[b] = (b == ar) ? J.tau[j0 + ar] : 0.0;
+#pragma unroll
+    for (int i = 1; i < QR_NB; ++i) {
+      if (i > ar && i < kb) {
+        const double ti = J.tau[j0 + i];
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < i; ++b)
+          if (b >= ar) s += tr[b] * sh.Gs[b + i * (QR_NB + 1)];
+        tr[i] = (ti != 0.0) ? -ti * s : 0.0;
+      }
+    }
+    double* Tg = J.T + j0 + (int64_t)j0 * k;
+#pragma unroll
+    for (int i = 0; i < QR_NB; ++i)
+      if (i < kb) Tg[ar + (int64_t)i * k] = tr[i];
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + QRR_NT * r;
+    if (i < nloc) {
+#pragma unroll
+      for (int c = 0; c < QR_NB; ++c)
+        if (c < kb) P0[i + (int64_t)c * m] = a[r][c];
+    }
+  }
+  cluster.sync();   // no CTA leaves while others may read its shared memory
+}
+
+template <int R, int KBMAX>
+void launch_qrr(const cudaLaunchConfig_t& cfg, const PanelJob* d_jobs) {
+  static bool init = false;
+  if (!init) {
+    CUDA_TRY(cudaFuncSetAttribute(panel_qr_reg_kernel<R, KBMAX>,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    init = true;
+  }
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_qr_reg_kernel<R, KBMAX>, d_jobs));
+}
+
+int panel_reg_kbmax(int kb) { return kb <= 8 ? 8 : kb <= 16 ? 16 : kb <= 24 ? 24 : 32; }
+
+void launch_panel_qr_reg(const PanelJob* d_jobs, int njobs, int cluster, int rows_per_thread,
+                         int kbmax, cudaStream_t st) {
+  if (njobs <= 0) return;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(njobs * cluster));
+  cfg.blockDim = dim3(QRR_NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int kc = panel_reg_kbmax(kbmax);
+  if (rows_per_thread <= 1) {
+    if (kc == 8) launch_qrr<1, 8>(cfg, d_jobs);
+    else if (kc == 16) launch_qrr<1, 16>(cfg, d_jobs);
+    else if (kc == 24) launch_qrr<1, 24>(cfg, d_jobs);
+    else launch_qrr<1, 32>(cfg, d_jobs);
+  } else {
+    if (kc == 8) launch_qrr<2, 8>(cfg, d_jobs);
+    else if (kc == 16) launch_qrr<2, 16>(cfg, d_jobs);
+    else if (kc == 24) launch_qrr<2, 24>(cfg, d_jobs);
+    else launch_qrr<2, 32>(cfg, d_jobs);
+  }
+}
+
 // ------------------------------------------------------------------ larft
 // Full compact-WY T (k x k) from G = V^T V and tau, one CTA per job, in
 // 32-column block columns J:  T_JJ by the row recurrence (one warp),

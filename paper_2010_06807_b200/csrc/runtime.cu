@@ -64,6 +64,10 @@ struct Block {
   int nr = 0, nc = 0;
   std::vector<uint8_t> flags;  // per row: 0 zero, 1 nonzero, 2 unknown (written)
   bool clean = false;
+  // flags PREDICTED by the symbolic rules (speculative mode), not yet
+  // checked against the device values; checked at the next query
+  bool unverified = false;
+  uint8_t origin = 0;   // last predicting site (SPQ_SPEC_DEBUG reports)
 };
 
 // sorted small-vector set (cluster adjacency lists are short; iteration
@@ -83,6 +87,14 @@ struct FlatSet {
   std::vector<int>::const_iterator begin() const { return v.begin(); }
   std::vector<int>::const_iterator end() const { return v.end(); }
   size_t size() const { return v.size(); }
+};
+
+// pivot checks (factor.py:57-68) queued on the device, raised in order at
+// the next synchronization point
+struct PivotSet {
+  std::vector<PivotJob> jobs;
+  std::vector<std::string> ctx;
+  size_t launched = 0;   // jobs[0, launched) already checked on the device
 };
 
 enum RecKind { REC_ELIM = 1, REC_SCALE = 2, REC_SPARSIFY = 3 };
@@ -143,6 +155,14 @@ struct spq_ctx {
   int* d_index_pack = nullptr;
   bool finished = false;
   bool compiled = false;
+  // speculative row flags (no host sync per factor wave); mismatches found
+  // by the device verification are counted in d_spec_bad (mapped pinned)
+  bool spec = true;
+  int* h_spec_bad = nullptr;
+  int* d_spec_bad = nullptr;
+  int64_t n_verified = 0;
+  PivotSet piv;   // speculative mode: checks pending across calls
+  unsigned long long* d_nnz_slots = nullptr;   // per-level trailing_nnz counters
   // device error slots for pivot checks
   int64_t* d_err_idx = nullptr;
   double* d_err_val = nullptr;
@@ -692,11 +712,19 @@ void collect_timings(spq_ctx* c) {
 
 void ensure_err_slots(spq_ctx* c, int n) {
   if (n <= c->err_slots) return;
+  int cap = std::max(n, 2 * c->err_slots + 64);
+  int64_t* idx = (int64_t*)dalloc(c, cap * sizeof(int64_t));
+  double* val = dalloc(c, cap * sizeof(double));
+  if (c->err_slots > 0) {   // results of checks not yet raised survive the growth
+    CUDA_TRY(cudaMemcpyAsync(idx, c->d_err_idx, c->err_slots * sizeof(int64_t),
+                             cudaMemcpyDeviceToDevice, c->st));
+    CUDA_TRY(cudaMemcpyAsync(val, c->d_err_val, c->err_slots * sizeof(double),
+                             cudaMemcpyDeviceToDevice, c->st));
+  }
   dfree(c, c->d_err_idx);
   dfree(c, c->d_err_val);
-  int cap = std::max(n, 2 * c->err_slots + 64);
-  c->d_err_idx = (int64_t*)dalloc(c, cap * sizeof(int64_t));
-  c->d_err_val = dalloc(c, cap * sizeof(double));
+  c->d_err_idx = idx;
+  c->d_err_val = val;
   c->err_slots = cap;
 }
 
@@ -1000,6 +1028,18 @@ bool force_global_panel() {
   return v == 1;
 }
 constexpr size_t SLAB_BYTES = 200 * 1024;
+bool legacy_panel() {
+  static const bool v = env_flag("SPQ_PANEL_LEGACY") || force_global_panel();
+  return v;
+}
+int panel_rows() {   // target rows per CTA of the register panel kernel
+  static const int v = [] {
+    const char* e = getenv("SPQ_PANEL_ROWS");
+    const int r = e ? atoi(e) : 256;
+    return std::max(32, std::min(512, r));
+  }();
+  return v;
+}
 
 void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
   Stage stage_(c, "qr_batch");
@@ -1013,11 +1053,23 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
   c->tm.flops[F_QR] += qr_flops;
   for (int j0 = 0; j0 < maxk; j0 += NB) {
     std::map<std::pair<int, int>, std::pair<std::vector<PanelJob>, int64_t>> groups;
+    std::map<std::tuple<int, int, int>, std::vector<PanelJob>> rgroups;   // (cl, R, kbmax)
     size_t wtot = 0;
     for (auto& q : probs) {
       if (j0 >= q.k) continue;
       const int kb = std::min(NB, q.k - j0);
       const int mh = q.m - j0;
+      if (!legacy_panel() && mh <= 16 * 2 * 256) {
+        // register-resident block: ~panel_rows() rows per CTA, R rows per thread
+        int cl = std::max(1, std::min(16, (mh + panel_rows() - 1) / panel_rows()));
+        int rpc = (mh + cl - 1) / cl;
+        while (cl > 1 && rpc < 32) { --cl; rpc = (mh + cl - 1) / cl; }
+        const int R = rpc <= 256 ? 1 : 2;
+        rgroups[{cl, R, panel_reg_kbmax(kb)}].push_back(PanelJob{q.P, q.R, q.tau, q.T, q.m, q.k, j0, kb, 1});
+        const int j1 = j0 + kb;
+        if (j1 < q.k) wtot += 2 * (size_t)kb * (q.k - j1);
+        continue;
+      }
       int cl = (int)(((size_t)mh * kb * 8 + SLAB_BYTES - 1) / SLAB_BYTES);
       cl = std::max(1, cl);
       int smem = 1;
@@ -1035,6 +1087,12 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
       for (auto& kv : groups) {
         launch_panel_qr(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first.first,
                         kv.second.second, kv.first.second != 0, NB, c->st);
+        c->tm.launches[F_QR]++;
+        c->n_kernels++;
+      }
+      for (auto& kv : rgroups) {
+        launch_panel_qr_reg(upload(c, kv.second), (int)kv.second.size(), std::get<0>(kv.first),
+                            std::get<1>(kv.first), std::get<2>(kv.first), c->st);
         c->tm.launches[F_QR]++;
         c->n_kernels++;
       }
@@ -1081,16 +1139,16 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
 }
 
 // pivot checks for a batch; returns the first failing job (in order) or -1
-struct PivotSet {
-  std::vector<PivotJob> jobs;
-  std::vector<std::string> ctx;
-};
-
+// checks the jobs added since the last launch; results accumulate in the
+// error slots until pivot_raise reads them (one read per set, in order)
 void pivot_launch(spq_ctx* c, PivotSet& ps) {
-  if (ps.jobs.empty()) return;
+  if (ps.jobs.size() <= ps.launched) return;
   ensure_err_slots(c, (int)ps.jobs.size());
-  for (int i = 0; i < (int)ps.jobs.size(); ++i) ps.jobs[i].slot = i;
-  launch_pivot_check(upload(c, ps.jobs), (int)ps.jobs.size(), c->d_err_idx, c->d_err_val, c->st);
+  for (size_t i = ps.launched; i < ps.jobs.size(); ++i) ps.jobs[i].slot = (int)i;
+  const int n = (int)(ps.jobs.size() - ps.launched);
+  launch_pivot_check(upload(c, ps.jobs.data() + ps.launched, n), n, c->d_err_idx, c->d_err_val,
+                     c->st);
+  ps.launched = ps.jobs.size();
   c->n_kernels++;
 }
 
@@ -1109,6 +1167,7 @@ void pivot_raise(spq_ctx* c, PivotSet& ps) {
     if (idx[i] >= 0) throw SpqError(SPQ_ERR_SINGULAR, ps.ctx[i], idx[i], val[i]);
   ps.jobs.clear();
   ps.ctx.clear();
+  ps.launched = 0;
 }
 
 // ----------------------------------------------------- block bookkeeping
@@ -1150,19 +1209,37 @@ double* new_block_mem(spq_ctx* c, int nr, int nc) {
   return dalloc(c, (size_t)std::max(1, nr) * std::max(1, nc) * sizeof(double));
 }
 
-// refresh row flags of every non-clean block in the given row clusters
+// refresh row flags of every non-clean block in the given row clusters.
+// Speculative mode: blocks whose flags were PREDICTED (clean, unverified)
+// are checked on the device in stream order -- the check sees exactly the
+// values the prediction describes -- without a host round trip; only
+// blocks with unknown flags still need the synchronous exact refresh.
 void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
   Stage stage_(c, "refresh_flags");
   HostTimer ht(&c->host_ms[4]);
-  std::vector<const double*> ptrs;
-  std::vector<int> nr, nc;
-  std::vector<int64_t> off;
+  std::vector<const double*> ptrs, vptrs;
+  std::vector<int> nr, nc, vnr, vnc;
+  std::vector<int64_t> off, voff;
+  std::vector<unsigned char> vpred;
   std::vector<Block*> which;
   int64_t tot = 0;
   for (int r : row_clusters) {
     for (int cc : c->rix[r]) {
       Block* b = find_block(c, r, cc);
-      if (!b || b->clean) continue;
+      if (!b) continue;
+      if (b->clean) {
+        if (b->unverified) {
+          b->unverified = false;
+          if ((int64_t)b->nr * b->nc == 0) continue;
+          vptrs.push_back(b->p);
+          vnr.push_back(b->nr);
+          vnc.push_back(b->nc);
+          voff.push_back((int64_t)vpred.size());
+          vpred.insert(vpred.end(), b->flags.begin(), b->flags.end());
+        }
+        continue;
+      }
+      b->unverified = false;
       if (b->nr == 0) { b->flags.clear(); b->clean = true; continue; }
       if (b->nc == 0) { b->flags.assign(b->nr, 0); b->clean = true; continue; }
       ptrs.push_back(b->p);
@@ -1172,6 +1249,42 @@ void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
       which.push_back(b);
       tot += b->nr;
     }
+  }
+  static const bool spec_debug = env_flag("SPQ_SPEC_DEBUG");
+  if (spec_debug && !vptrs.empty()) {   // exact read-back of every prediction, report mismatches
+    std::vector<int64_t> noff(vptrs.size());
+    for (size_t t = 0; t < vptrs.size(); ++t) noff[t] = voff[t];
+    unsigned char* d_o = (unsigned char*)dalloc(c, vpred.size());
+    launch_rowflags(upload(c, vptrs), upload(c, vnr), upload(c, vnc), upload(c, noff), d_o,
+                    (int)vptrs.size(), c->st);
+    std::vector<unsigned char> hh(vpred.size());
+    CUDA_TRY(cudaMemcpyAsync(hh.data(), d_o, hh.size(), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    dfree(c, d_o);
+    for (size_t t = 0; t < vptrs.size(); ++t) {
+      int bad = 0, first = -1;
+      for (int i = 0; i < vnr[t]; ++i)
+        if (hh[voff[t] + i] != vpred[voff[t] + i]) { ++bad; if (first < 0) first = i; }
+      if (bad) {
+        Block* hit = nullptr;
+        int hr = -1, hc = -1;
+        for (auto& kv : c->blk)
+          if (kv.second.p == vptrs[t]) { hit = &kv.second; hr = (int)(kv.first >> 32); hc = (int)(kv.first & 0xffffffffu); }
+        fprintf(stderr, "[spec] block (%d,%d) %dx%d origin %d: %d rows differ, first %d pred %d actual %d\n",
+                hr, hc, vnr[t], vnc[t], hit ? hit->origin : -1, bad, first,
+                (int)vpred[voff[t] + first], (int)hh[voff[t] + first]);
+      }
+    }
+  }
+  if (!vptrs.empty()) {
+    static const bool sabotage = env_flag("SPQ_SPEC_TEST_FAIL");   // tests: force the retry path
+    if (sabotage) vpred[0] ^= 1;
+    Scope s(c, F_FLAGS);
+    launch_rowflags_verify(upload(c, vptrs), upload(c, vnr), upload(c, vnc), upload(c, voff),
+                           upload(c, vpred), (int)vptrs.size(), c->d_spec_bad, c->st);
+    c->tm.launches[F_FLAGS]++;
+    c->n_kernels++;
+    c->n_verified += (int64_t)vptrs.size();
   }
   if (which.empty()) return;
   unsigned char* d_out = (unsigned char*)dalloc(c, tot);
@@ -1194,6 +1307,31 @@ void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
     b->flags.assign(h.begin() + off[t], h.begin() + off[t] + b->nr);
     b->clean = true;
   }
+}
+
+// speculative-mode prediction helpers
+inline bool any_nonzero(const Block& b) {
+  for (uint8_t f : b.flags) if (f == 1) return true;
+  return false;
+}
+// every row becomes a combination of all rows (left orthogonal transform)
+void predict_mixed_rows(spq_ctx* c, Block& b, bool nonzero, int new_nr) {
+  if (!c->spec) { b.clean = false; b.flags.clear(); return; }
+  b.flags.assign(new_nr, nonzero ? 1 : 0);
+  b.clean = true;
+  b.unverified = true;
+}
+// rows keep their zero/nonzero pattern (right transform by a nonsingular factor)
+void predict_same_rows(spq_ctx* c, Block& b) {
+  if (!c->spec || !b.clean) { b.clean = false; return; }
+  b.unverified = true;
+}
+// exact identity
+void set_identity_flags(spq_ctx* c, Block& b, int n) {
+  if (!c->spec) { b.clean = false; b.flags.clear(); return; }
+  b.flags.assign(n, 1);
+  b.clean = true;
+  b.unverified = false;
 }
 
 int* upload_idx32(spq_ctx* c, const std::vector<int64_t>& v) {
@@ -1346,8 +1484,12 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
         if (old) release_mem(c, *old);
         Block& b = put_block(c, p.r, cc, full_slab[pi] + (int64_t)f.woff[ci] * nr, nr, ncol,
                              full_slab[pi]);
-        b.flags.assign(nr, 2);
-        b.clean = false;
+        // speculative: every row is a panel row and receives a row of
+        // H^T C_all with cc present -- nonzero (verified at the next query)
+        b.flags.assign(nr, c->spec ? 1 : 2);
+        b.clean = c->spec;
+        b.unverified = c->spec;
+        b.origin = 1;
       } else {
         Block* b = find_block(c, p.r, cc);
         if (!b) {
@@ -1355,13 +1497,20 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
           zeros.zero(mem, (int64_t)nr * ncol);
           Block& nb = put_block(c, p.r, cc, mem, nr, ncol);
           nb.flags.assign(nr, 0);
-          nb.clean = false;
+          nb.clean = true;
           b = &nb;
         } else if (b->flags.size() != (size_t)nr) {
           b->flags.assign(nr, 2);
+          b->clean = false;
         }
-        for (int i : p.ix) b->flags[i] = 2;
-        b->clean = false;
+        const uint8_t w = c->spec ? 1 : 2;
+        for (int i : p.ix) b->flags[i] = w;
+        b->origin = 2;
+        if (c->spec) {
+          b->unverified = true;   // rows outside the panel keep their (known or unknown) flags
+        } else {
+          b->clean = false;
+        }
         f.dsts.push_back({b->p, nr, pi, f.woff[ci], ncol, false});
       }
     }
@@ -1572,7 +1721,8 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
   size_t pos = 0;
   std::vector<int> stamp(c->N, -1);
   int wave_id = 0;
-  PivotSet ps;
+  PivotSet& ps = c->piv;
+  if (!c->spec) pivot_raise(c, ps);
   while (pos < ids.size()) {
     // refresh flags of every row cluster any pending op may query
     std::set<int> rows;
@@ -1582,7 +1732,9 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
       for (int r : c->cix[s]) rows.insert(r);
     }
     refresh_flags(c, std::vector<int>(rows.begin(), rows.end()));
-    pivot_raise(c, ps);   // previous wave (synced by refresh)
+    // exact mode: the refresh synchronized, so reading the previous waves'
+    // pivot checks is free; speculative mode defers them to the end of the call
+    if (!c->spec) pivot_raise(c, ps);
     ++wave_id;
     std::vector<Front> wave;
     CopyBatch zeros;
@@ -1619,7 +1771,7 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
     }
     execute_wave(c, wave, zeros, ps);
   }
-  pivot_raise(c, ps);
+  if (!c->spec) pivot_raise(c, ps);
   flush_deferred(c);
 }
 
@@ -1663,7 +1815,13 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
       Block* bc = find_block(c, p, cc);
       if (bc && bc->nc > 0 && bc->nr == np) {
         q.targets.push_back(CTarget{bc->p, bc->nr, bc->nc});
+        // U_pp^T mixes rows only within the coupled groups of A_pp (merged
+        // child fragments can be decoupled: block-diagonal U) -- no
+        // prediction, the next query reads these flags back exactly
+        bc->origin = 3;
         bc->clean = false;
+        bc->unverified = false;
+        bc->flags.clear();
       }
     }
     rec.full_T = !q.targets.empty();
@@ -1674,7 +1832,7 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
   zeros.run(c);
   g.run(c);
   qr_batch(c, qp);
-  PivotSet ps;
+  PivotSet& ps = c->piv;
   for (size_t t = 0; t < todo.size(); ++t) {
     Record& rec = c->recs[recid[t]];
     ps.jobs.push_back(PivotJob{rec.R, rec.k, rec.k, 0});
@@ -1695,7 +1853,8 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
         tj.push_back(TrsmJob{rec.R, b->p, b->nr, rec.k, rec.k, b->nr, ttiles});
         ttiles += trsm_tiles(b->nr);
         trsm_flops += (double)b->nr * rec.k * rec.k;
-        b->clean = false;
+        b->origin = 4;
+        predict_same_rows(c, *b);
       }
     }
   }
@@ -1736,13 +1895,13 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
       (void)nb;
       b = find_block(c, p, p);
     }
-    b->clean = false;
+    set_identity_flags(c, *b, np);
     CopyTask t{};
     t.dst = mem; t.nr = np; t.nc = np; t.ldd = np; t.ident = 1;
     id.add(t);
   }
   id.run(c);
-  pivot_raise(c, ps);
+  if (!c->spec) pivot_raise(c, ps);
   flush_deferred(c);
 }
 
@@ -1849,6 +2008,7 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     CUDA_TRY(cudaMemcpyAsync(hk.data(), dsc, nw * sizeof(SpScal), cudaMemcpyDeviceToHost, c->st));
     sync(c);
   }
+  pivot_raise(c, c->piv);   // checks queued by this level's factor/scale calls
   const bool coop_only = env_flag("SPQ_CPQR_COOP"), no_ws = env_flag("SPQ_CPQR_NOWS");
   auto job_of = [&](int t, int ncap) {
     SpJob& j = J[t];
@@ -2043,6 +2203,10 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     for (size_t q = 0; q < j.us.size(); ++q) {
       const int u = j.us[q], h_u = j.hu[q];
       Block* old = find_block(c, u, p);
+      // rows of u keep their zero pattern under the right rotation
+      std::vector<uint8_t> keep_fl;
+      const bool known = c->spec && old && old->clean && old->flags.size() == (size_t)h_u;
+      if (known) keep_fl = old->flags;
       if (old) release_mem(c, *old);
       if ((int64_t)h_u * r > 0) {
         double* mem = new_block_mem(c, h_u, r);
@@ -2051,8 +2215,15 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
         x.ldd = h_u; x.trans = 1;
         sc.add(x);
         Block& b = put_block(c, u, p, mem, h_u, r);
-        b.clean = false;
-        b.flags.clear();
+        b.origin = 5;
+        if (known) {
+          b.flags = std::move(keep_fl);
+          b.clean = true;
+          b.unverified = true;
+        } else {
+          b.clean = false;
+          b.flags.clear();
+        }
       } else {
         drop_block(c, u, p);
       }
@@ -2061,6 +2232,8 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     for (size_t q = 0; q < j.cs.size(); ++q) {
       const int cc = j.cs[q], w = j.wc[q];
       Block* old = find_block(c, p, cc);
+      const bool known = c->spec && old && old->clean;
+      const bool nz = known && any_nonzero(*old);
       if (old) release_mem(c, *old);
       if ((int64_t)w * r > 0) {
         double* mem = new_block_mem(c, r, w);
@@ -2068,8 +2241,13 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
         x.src = j.M + (int64_t)off * np; x.dst = mem; x.nr = r; x.nc = w; x.lds = np; x.ldd = r;
         sc.add(x);
         Block& b = put_block(c, p, cc, mem, r, w);
-        b.clean = false;
-        b.flags.clear();
+        b.origin = 6;
+        if (known) {
+          predict_mixed_rows(c, b, nz, r);
+        } else {
+          b.clean = false;
+          b.flags.clear();
+        }
       } else {
         drop_block(c, p, cc);
       }
@@ -2083,8 +2261,7 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       x.dst = mem; x.nr = r; x.nc = r; x.ldd = r; x.ident = 1;
       sc.add(x);
       Block& b = put_block(c, p, p, mem, r, r);
-      b.clean = false;
-      b.flags.clear();
+      set_identity_flags(c, b, r);
     } else {
       drop_block(c, p, p);
       for (int u : j.us) drop_block(c, u, p);
@@ -2241,7 +2418,13 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
       for (int Pj : v) {
         const int C = (int)c->cols_of[Pj].size();
         Block& nb = put_block(c, Pi, Pj, slab + off, R, C, slab);
-        nb.clean = false;
+        // merged values are copies: the parent's row flags are the OR of its
+        // children's (exact given theirs; unverified if any child is)
+        if (c->spec) nb.flags.assign(R, 0);
+        else nb.flags.clear();
+        nb.clean = c->spec;
+        nb.unverified = false;
+        nb.origin = 7;
         off += (size_t)R * C;
       }
     }
@@ -2256,6 +2439,18 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
         x.src = B.p; x.dst = tgt->p + roff[i] + (int64_t)coff[j] * R; x.nr = B.nr; x.nc = B.nc;
         x.lds = B.nr; x.ldd = R;
         cp.add(x);
+        if (tgt->clean) {
+          if (B.clean && B.flags.size() == (size_t)B.nr) {
+            for (int t = 0; t < B.nr; ++t)
+              if (B.flags[t] == 1) tgt->flags[roff[i] + t] = 1;
+            if (B.unverified && !tgt->unverified) tgt->origin = (uint8_t)(10 + B.origin % 10);
+            tgt->unverified = tgt->unverified || B.unverified;
+          } else {
+            tgt->clean = false;
+            tgt->unverified = false;
+            tgt->flags.clear();
+          }
+        }
         release_mem(c, B);
       }
     zeros.run(c);
@@ -2337,6 +2532,21 @@ void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
     Block& B = put_block(c, i, j, mem, nr, nc);
     B.clean = false;
     bases[b] = mem;
+  }
+  // exact initial row flags from the stored values (equilibration divides
+  // by positive norms: zero stays zero, nonzero stays nonzero)
+  if (c->spec) {
+    std::vector<Block*> bp(bkeys.size());
+    for (size_t b = 0; b < bkeys.size(); ++b) {
+      bp[b] = find_block(c, bkeys[b].first, bkeys[b].second);
+      bp[b]->flags.assign(bp[b]->nr, 0);
+      bp[b]->clean = true;
+      bp[b]->unverified = true;
+      bp[b]->origin = 8;
+    }
+    for (int64_t j = 0; j < N; ++j)
+      for (int64_t e = indptr[j]; e < indptr[j + 1]; ++e)
+        if (data[e] != 0.0) bp[eb[e]]->flags[rpos[indices[e]]] = 1;
   }
   zeros.run(c);
   int64_t* d_indptr = (int64_t*)dalloc(c, (N + 1) * sizeof(int64_t));
@@ -2666,6 +2876,10 @@ int spq_create(spq_ctx** out, int device) {
       CUDA_TRY(cudaMallocHost(&c->pin, c->ring_cap));
       CUDA_TRY(cudaMalloc(&c->dring, c->ring_cap));
     }
+    c->spec = !env_flag("SPQ_NO_SPEC");
+    CUDA_TRY(cudaHostAlloc(&c->h_spec_bad, sizeof(int), cudaHostAllocMapped));
+    *c->h_spec_bad = 0;
+    CUDA_TRY(cudaHostGetDevicePointer(&c->d_spec_bad, c->h_spec_bad, 0));
   });
   if (rc != SPQ_OK) {
     *out = c;  // caller may query the error, then destroy
@@ -2703,6 +2917,7 @@ void spq_destroy(spq_ctx* c) {
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->st) cudaStreamDestroy(c->st);
+    if (c->h_spec_bad) cudaFreeHost(c->h_spec_bad);
   } catch (...) {
   }
   delete c;
@@ -2761,6 +2976,7 @@ int spq_merge(spq_ctx* c, int n_parents, const int32_t* parent_ids, const int32_
 int spq_finish(spq_ctx* c) {
   return guarded(c, [&] {
     HostTimer ht(&c->host_ms[15]);
+    pivot_raise(c, c->piv);
     for (int64_t j = 0; j < c->N; ++j)
       if (c->row_of_col[j] < 0) {
         int64_t miss = 0;
@@ -2791,6 +3007,23 @@ int spq_finish(spq_ctx* c) {
     build_full_T(c, tp);
     c->finished = true;
     sync(c);
+    if (*c->h_spec_bad)
+      throw SpqError(SPQ_ERR_SPECULATION, std::to_string(*c->h_spec_bad) +
+                     " predicted row flags differed from the device values; "
+                     "re-run with speculation off");
+  });
+}
+
+int spq_set_option(spq_ctx* c, const char* key, int64_t value) {
+  return guarded(c, [&] {
+    const std::string k = key ? key : "";
+    if (k == "speculate") {
+      if (!c->blk.empty() || !c->recs.empty())
+        throw SpqError(SPQ_ERR_BAD_INPUT, "speculate must be set before spq_load");
+      c->spec = value != 0;
+    } else {
+      throw SpqError(SPQ_ERR_BAD_INPUT, "unknown option '" + k + "'");
+    }
   });
 }
 
@@ -2841,6 +3074,43 @@ int spq_trailing_stats(spq_ctx* c, int64_t* nblocks, int64_t* nnz) {
   });
 }
 
+// trailing_blocks now, trailing_nnz counted on the device into a slot read
+// later (spq_trailing_nnz): no host round trip per level
+int spq_trailing_stats_async(spq_ctx* c, int slot, int64_t* nblocks) {
+  return guarded(c, [&] {
+    HostTimer ht(&c->host_ms[13]);
+    if (slot < 0 || slot >= 4096) throw SpqError(SPQ_ERR_BAD_INPUT, "stats slot out of range");
+    if (!c->d_nnz_slots) {
+      c->d_nnz_slots = (unsigned long long*)dalloc(c, 4096 * sizeof(unsigned long long));
+      CUDA_TRY(cudaMemsetAsync(c->d_nnz_slots, 0, 4096 * sizeof(unsigned long long), c->st));
+    }
+    *nblocks = (int64_t)c->blk.size();
+    std::vector<const double*> ptrs;
+    std::vector<int64_t> sizes;
+    for (auto& kv : c->blk) {
+      const int64_t n = (int64_t)kv.second.nr * kv.second.nc;
+      if (n > 0) { ptrs.push_back(kv.second.p); sizes.push_back(n); }
+    }
+    unsigned long long* d = c->d_nnz_slots + slot;
+    CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->st));
+    if (!ptrs.empty())
+      launch_count_nnz(upload(c, ptrs), upload(c, sizes), (int)ptrs.size(), d, c->st);
+    c->n_kernels++;
+  });
+}
+
+int spq_trailing_nnz(spq_ctx* c, int n, int64_t* out) {
+  return guarded(c, [&] {
+    if (n < 0 || n > 4096) throw SpqError(SPQ_ERR_BAD_INPUT, "stats slot count out of range");
+    if (!c->d_nnz_slots || n == 0) { std::fill(out, out + n, 0); return; }
+    std::vector<unsigned long long> h(n);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), c->d_nnz_slots, n * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    for (int i = 0; i < n; ++i) out[i] = (int64_t)h[i];
+  });
+}
+
 int spq_row_of_col(spq_ctx* c, int64_t* out) {
   return guarded(c, [&] { std::copy(c->row_of_col.begin(), c->row_of_col.end(), out); });
 }
@@ -2871,6 +3141,11 @@ int spq_timings(spq_ctx* c, double* out, int n) {
     if (4 * F_NFAM + 21 < n) {
       out[4 * F_NFAM + 20] = (double)c->live_bytes;
       out[4 * F_NFAM + 21] = (double)c->peak_bytes;
+    }
+    if (4 * F_NFAM + 24 < n) {
+      out[4 * F_NFAM + 22] = c->spec ? 1.0 : 0.0;
+      out[4 * F_NFAM + 23] = (double)c->n_verified;
+      out[4 * F_NFAM + 24] = c->h_spec_bad ? (double)*c->h_spec_bad : 0.0;
     }
   });
 }

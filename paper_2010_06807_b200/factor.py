@@ -23,7 +23,7 @@ import time
 import numpy as np
 
 from ._lib import Context
-from .errors import NestqrError
+from .errors import NestqrError, SpeculationError
 from .sparse import as_csc
 
 MODES = ("scaled", "unscaled", "variant1", "variant2")
@@ -279,7 +279,7 @@ def _cluster_lists(clusters, attr):
 def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=True,
               scale_every=1, skip=2, sparsify_min=40, mode="scaled",
               row_heuristic="same-as-columns", equilibrate=True, observer=None, device=0,
-              _marks=False, _memstats=False):
+              _marks=False, _memstats=False, _speculate=True):
     """Run the multilevel factorization on the B200 (signature of the reference
     `factorize`, `factor.py:771-803`)."""
     if mode not in MODES:
@@ -302,6 +302,8 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
         assign_rows_same_as_columns(tree)
     L = tree.L
     ctx = Context(device)
+    if not _speculate:
+        ctx.call("spq_set_option", b"speculate", 0)
     leaf_ids = np.array([c.id for c in leaves], np.int32)
     rptr, rows = _cluster_lists(leaves, "rows")
     cptr, cols = _cluster_lists(leaves, "cols")
@@ -390,13 +392,18 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
             st["iface_q1"], st["iface_q2"], st["iface_q3"] = float(q1), float(q2), float(q3)
             st["iface_max"] = int(max(sizes))
         st["cols_after"] = ctx.i64("spq_total_cols")
-        nb, nz = C.c_int64(), C.c_int64()
-        ctx.call("spq_trailing_stats", C.byref(nb), C.byref(nz))
-        st["trailing_nnz"], st["trailing_blocks"] = int(nz.value), int(nb.value)
+        nb = C.c_int64()
+        on_lv = getattr(observer, "on_level", None)
+        if on_lv is None:   # nnz read once after the last level (no per-level sync)
+            ctx.call("spq_trailing_stats_async", len(stats), C.byref(nb))
+        else:
+            nz = C.c_int64()
+            ctx.call("spq_trailing_stats", C.byref(nb), C.byref(nz))
+            st["trailing_nnz"] = int(nz.value)
+        st["trailing_blocks"] = int(nb.value)
         if _memstats:
             h = ctx.timings()["host"]
             st["_live_gb"], st["_peak_gb"] = h["live_bytes"] / 1e9, h["peak_bytes"] / 1e9
-        on_lv = getattr(observer, "on_level", None)
         if on_lv is not None:
             on_lv(state, lev, st)
         if lev >= 2:
@@ -412,7 +419,22 @@ def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tru
             st["t_merge"] = time.perf_counter() - t0
         stats.append(st)
 
-    ctx.call("spq_finish")
+    try:
+        ctx.call("spq_finish")
+    except SpeculationError:
+        # a predicted row-nonzero flag was wrong (an exact cancellation the
+        # symbolic rules cannot see): redo with flags read back exactly
+        ctx.close()
+        return factorize(A, tree, eps, levels=levels, sparsify=sparsify, scaling=scaling,
+                         scale_every=scale_every, skip=skip, sparsify_min=sparsify_min,
+                         mode=mode, row_heuristic=row_heuristic, equilibrate=equilibrate,
+                         observer=observer, device=device, _marks=_marks,
+                         _memstats=_memstats, _speculate=False)
+    if getattr(observer, "on_level", None) is None and stats:
+        nnz = np.zeros(len(stats), np.int64)
+        ctx.call("spq_trailing_nnz", len(stats), nnz)
+        for st, z in zip(stats, nnz):
+            st["trailing_nnz"] = int(z)
     device_ms = None
     if _marks:
         ctx.call("spq_mark", 1)
