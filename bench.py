@@ -257,6 +257,20 @@ def main():
                     a[key] += v.get(key, 0)
             del F
     barrier()
+    # solve phase (reported beside the metric): device GMRES on one factorization
+    solve = None
+    if b is not None:
+        from paper_2010_06807_b200.solve import gmres
+        F = FZ.factorize(A, tree, eps=eps, device=local)
+        gmres(A, b, F, tol=tol)                       # warm (chain graphs, CSR upload)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, rep = gmres(A, b, F, tol=tol)
+        ts = time.perf_counter() - t0
+        solve = {"gmres_s": ts, "iterations": int(rep.iterations),
+                 "final_residual": float(rep.final_residual), "tol": tol,
+                 "where": "device (spq_gmres: chains + CSR SpMV + MGS in HBM)"}
+        del F
     T = float(np.sum(dev_ms))
     Te = float(np.sum(e2e_ms))
     T, Te = reduce_max([T, Te], dist)
@@ -301,6 +315,7 @@ def main():
                         "gflop_per_step": v["flops"] / args.steps / 1e9,
                         "launches_per_step": v["launches"] / args.steps} for k, v in fams.items()},
         "roofline": roof,
+        "solve": solve,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": csc_bytes(A, tree),
                 "d2h_bytes_per_step": 8 * int(A.ncols)},
         "gpu_launches": launches,

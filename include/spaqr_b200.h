@@ -130,6 +130,22 @@ int spq_record_get(spq_ctx* ctx, int idx, int which, void* out);
  * Factorization.apply_qt / solve_w / apply_w (factor.py:281-300) on an
  * N x nrhs column-major block.  *_host: host in/out (copies inside);
  * *_dev: device pointer, in place. */
+/* ------------------------------------------------------- device GMRES
+ * Right-preconditioned GMRES of pkg/src/nestqr/solve.py:66-209 on the device
+ * (operator v -> apply_qt(A solve_w(v)), modified Gram-Schmidt with the
+ * 1e-8 re-orthogonalisation test, Givens updates, the TRUE residual of every
+ * iterate, best iterate returned).  spq_set_matrix uploads A (the original,
+ * unscaled CSC matrix, stored as CSR on the device) once; spq_gmres takes
+ * host b (N), optional host x0 (NULL = 0), writes x (N), the relative
+ * residual history hist (room for maxit+1; its+1 entries written), the
+ * iteration count, the converged flag and the best residual.
+ * restart <= 0 means full GMRES. */
+int spq_set_matrix(spq_ctx* ctx, int64_t N, const int64_t* indptr, const int64_t* indices,
+                   const double* data);
+int spq_gmres(spq_ctx* ctx, const double* b, const double* x0, double tol, int maxit,
+              int restart, double* x, double* hist, int* its, int* converged,
+              double* best_residual);
+
 int spq_apply_qt_host(spq_ctx* ctx, const double* in, double* out, int nrhs);
 int spq_solve_w_host(spq_ctx* ctx, const double* in, double* out, int nrhs);
 int spq_apply_w_host(spq_ctx* ctx, const double* in, double* out, int nrhs);

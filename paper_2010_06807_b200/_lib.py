@@ -53,6 +53,9 @@ SIGNATURES = {
     "spq_num_records": (C.c_int, [_ctx]),
     "spq_record_info": (C.c_int, [_ctx, C.c_int, _i64p]),
     "spq_record_get": (C.c_int, [_ctx, C.c_int, C.c_int, _vp]),
+    "spq_set_matrix": (C.c_int, [_ctx, C.c_int64, _i64p, _i64p, _f64p]),
+    "spq_gmres": (C.c_int, [_ctx, _f64p, _vp, C.c_double, C.c_int, C.c_int, _f64p, _f64p,
+                            C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "spq_apply_qt_host": (C.c_int, [_ctx, _f64p, _f64p, C.c_int]),
     "spq_solve_w_host": (C.c_int, [_ctx, _f64p, _f64p, C.c_int]),
     "spq_apply_w_host": (C.c_int, [_ctx, _f64p, _f64p, C.c_int]),

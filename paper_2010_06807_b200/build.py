@@ -15,9 +15,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libspaqr_b200.so")
-SOURCES = ["k_copy.cu", "k_gemm.cu", "k_qr.cu", "k_cpqr.cu", "k_chain.cu", "runtime.cu"]
+SOURCES = ["k_copy.cu", "k_gemm.cu", "k_qr.cu", "k_cpqr.cu", "k_chain.cu", "runtime.cu", "hostprof.cu", "k_krylov.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+         "-Xcompiler", "-g", "-Xcompiler", "-fno-omit-frame-pointer",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
          "-Xptxas", "-v" if os.environ.get("SPQ_PTXAS_V") else "-O3"]
 
@@ -56,7 +57,7 @@ def build(force=False, verbose=False):
         if verbose and (r.stdout or r.stderr):
             sys.stderr.write(r.stdout + r.stderr)
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT + ".tmp",
-           *[o for o, _ in results], "-lcudart"]
+           *[o for o, _ in results], "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

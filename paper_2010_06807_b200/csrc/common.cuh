@@ -213,4 +213,22 @@ struct CudaFailure : std::runtime_error {
       : std::runtime_error(std::string(cudaGetErrorString(e)) + " at " + f + ":" +
                            std::to_string(l) + " (" + what + ")") {}
 };
+// ---------------------------------------------------- Krylov (k_krylov.cu)
+constexpr int KRY_G = 296;   // fixed grid of the deterministic reductions (2 x 148 SMs)
+void kry_spmv(const int64_t* ptr, const int* idx, const double* val, const double* x,
+              const double* b, double* y, int64_t n, int mode, cudaStream_t st);
+void kry_dot_part(const double* x, const double* y, int64_t n, double* part, cudaStream_t st);
+void kry_finish(const double* part, double* out, bool sqrt_it, cudaStream_t st);
+void kry_mgs_step(const double* qi, const double* q_next, double* w, int64_t n,
+                  const double* part_in, double* part_out, double* h_out, cudaStream_t st);
+void kry_multi_dot(const double* Q, int64_t ldq, int j, const double* w, int64_t n, double* part,
+                   double* cvec, cudaStream_t st);
+void kry_reorth(const double* Q, int64_t ldq, int j, const double* cvec, const double* wn,
+                double thr, double* w, int64_t n, double* Hcol, int* flag, double* part_out,
+                cudaStream_t st);
+void kry_scale_div(const double* src, const double* den, double* dst, int64_t n, cudaStream_t st);
+void kry_gemv(const double* Q, int64_t ldq, int j, const double* y, double* out, int64_t n,
+              cudaStream_t st);
+void kry_add(const double* x, const double* y, double* z, int64_t n, cudaStream_t st);
+
 }  // namespace spq

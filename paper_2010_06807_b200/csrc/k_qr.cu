@@ -246,12 +246,44 @@ void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t sla
 // streams the slab through shared memory twice per column).  Requires
 // rows-per-CTA >= 32 so every pivot row lives in CTA 0 (thread jj).
 constexpr int QRR_NT = 256;
+constexpr int QRR_CLMAX = 16;
+
+// ---- DSMEM push exchange (st.async + mbarrier complete_tx): no cluster
+// barrier per column step.  A cluster barrier with release/acquire
+// semantics compiles to MEMBAR.ALL.GPU + L1 invalidation on sm_100a.
+__device__ __forceinline__ uint32_t qrr_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t qrr_mapa(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void qrr_st_async(uint32_t raddr, double v, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+               :: "r"(raddr), "d"(v), "r"(rmbar) : "memory");
+}
+__device__ __forceinline__ void qrr_arm(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void qrr_wait(uint32_t mbar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                 "selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(mbar), "r"(parity) : "memory");
+  }
+}
 
 struct QrrShared {
-  double X[2][1 + 2 * QR_NB];       // [1+c]: CTA partial dot, [33+c]: pivot row
+  double XR[2][QRR_CLMAX][QR_NB];   // per source CTA: partial dots (pushed)
+  double PR[2][QR_NB];              // pivot row (pushed by CTA 0)
+  double Xp[QR_NB];                 // CTA 0: pivot row staging
   double red[QRR_NT / 32][QR_NB];
   double dtot[QR_NB], apiv[QR_NB];
   double Gs[QR_NB * (QR_NB + 1)];
+  alignas(8) uint64_t mbar[2];
 };
 
 struct QrrCtx {
@@ -259,73 +291,91 @@ struct QrrCtx {
   double* tau;
 };
 
-// one column step (JJ is a compile-time column so the register block is
-// indexed statically)
-template <int R, int JJ>
+// One column step.  The loop over columns is NOT unrolled (a 32x unrolled
+// step sequence overflows the instruction cache: ncu showed 58% of warp
+// samples stalled on "no instructions"); the register block is indexed
+// with compile-time columns only, so the dynamic column jj is selected
+// with predicated moves.
+template <int R>
 __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB], QrrShared& sh,
-                                         cg::cluster_group& cluster) {
+                                         const int jj) {
   const int q = x.q, CL = x.CL, nloc = x.nloc, tid = x.tid, lane = x.lane, warp = x.warp;
-  double* Xb = sh.X[JJ & 1];
-  (void)q;
-  // ---- partial dots of the pivot column (rows strictly below the pivot)
-  double d[QR_NB];
-#pragma unroll
-  for (int c = 0; c < QR_NB; ++c) d[c] = 0.0;
+  const int B = jj & 1;
+  // ---- this thread's entries of the pivot column
+  double xv[R];
+  bool part[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int i = tid + QRR_NT * r;
-    if (i < nloc && (q > 0 || i > JJ)) {
-      const double xv = a[r][JJ];
+    part[r] = i < nloc && (q > 0 || i > jj);
+    double t = 0.0;
 #pragma unroll
-      for (int c = 0; c < QR_NB; ++c) d[c] = fma(xv, a[r][c], d[c]);
-    }
+    for (int c = 0; c < QR_NB; ++c) t = (c == jj) ? a[r][c] : t;
+    xv[r] = t;
   }
-  // ---- warp reduce-scatter: lane l ends with the warp sum of column l
+  // ---- partial dots of the pivot column (rows strictly below the pivot),
+  // in two halves of 16 columns (register pressure); a warp reduce-scatter
+  // per half leaves lane l with the warp sum of column (l & 15) of the half
+  double mine = 0.0;
 #pragma unroll
-  for (int h = 16; h >= 1; h >>= 1) {
-    const bool hi = (lane & h) != 0;
+  for (int half = 0; half < 2; ++half) {
+    double d[QR_NB / 2];
 #pragma unroll
-    for (int t = 0; t < h; ++t) {
-      const double send = hi ? d[t] : d[t + h];
-      const double keep = hi ? d[t + h] : d[t];
-      d[t] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    for (int c = 0; c < QR_NB / 2; ++c) d[c] = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double xr = part[r] ? xv[r] : 0.0;
+#pragma unroll
+      for (int c = 0; c < QR_NB / 2; ++c) d[c] = fma(xr, a[r][half * (QR_NB / 2) + c], d[c]);
     }
-  }
-  sh.red[warp][lane] = d[0];
-  if (q == 0 && tid == JJ) {
 #pragma unroll
-    for (int c = 0; c < QR_NB; ++c) Xb[1 + QR_NB + c] = a[0][c];
+    for (int h = 8; h >= 1; h >>= 1) {
+      const bool hi = (lane & h) != 0;
+#pragma unroll
+      for (int t = 0; t < h; ++t) {
+        const double send = hi ? d[t] : d[t + h];
+        const double keep = hi ? d[t + h] : d[t];
+        d[t] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+      }
+    }
+    const double tot = d[0] + __shfl_xor_sync(0xffffffffu, d[0], 16);
+    if ((lane >> 4) == half) mine = tot;
+  }
+  sh.red[warp][lane] = mine;
+  if (q == 0 && tid == jj) {
+#pragma unroll
+    for (int c = 0; c < QR_NB; ++c) sh.Xp[c] = a[0][c];
   }
   __syncthreads();
-  if (tid < QR_NB) {
+  // ---- push the CTA partials (and CTA 0's pivot row) to every CTA
+  for (int t = tid; t < QR_NB * CL; t += QRR_NT) {
+    const int dst = t >> 5, c = t & 31;
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < QRR_NT / 32; ++w) s += sh.red[w][tid];
-    Xb[1 + tid] = s;
+    for (int w = 0; w < QRR_NT / 32; ++w) s += sh.red[w][c];
+    const uint32_t mb = qrr_mapa(qrr_smem(&sh.mbar[B]), dst);
+    qrr_st_async(qrr_mapa(qrr_smem(&sh.XR[B][q][c]), dst), s, mb);
+    if (q == 0) qrr_st_async(qrr_mapa(qrr_smem(&sh.PR[B][c]), dst), sh.Xp[c], mb);
   }
-  // CTA partials over DSMEM (a 1-CTA cluster reads its own shared memory);
-  // branch-free so the shuffles are not lowered as collectives
-  cluster.sync();
-  {
-    const double* src = cluster.map_shared_rank(Xb, lane < CL ? lane : 0);
-    const double* piv = cluster.map_shared_rank(Xb, 0);
+  qrr_wait(qrr_smem(&sh.mbar[B]), (uint32_t)((jj >> 1) & 1));
+  if (tid == 0)   // re-arm this buffer for step jj + 2 (before anyone can push it)
+    qrr_arm(qrr_smem(&sh.mbar[B]), (uint32_t)((CL + 1) * QR_NB * sizeof(double)));
+  // ---- totals over the CTAs in rank order (identical in every CTA)
 #pragma unroll
-    for (int cc = 0; cc < QR_NB / (QRR_NT / 32); ++cc) {
-      const int c = warp + cc * (QRR_NT / 32);
-      double v = src[1 + c];
-      v = lane < CL ? v : 0.0;
+  for (int cc = 0; cc < QR_NB / (QRR_NT / 32); ++cc) {
+    const int c = warp + cc * (QRR_NT / 32);
+    double v = lane < CL ? sh.XR[B][lane < CL ? lane : 0][c] : 0.0;
 #pragma unroll
-      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) {
-        sh.dtot[c] = v;
-        sh.apiv[c] = piv[1 + QR_NB + c];
-      }
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      sh.dtot[c] = v;
+      sh.apiv[c] = sh.PR[B][c];
     }
   }
   __syncthreads();
   // ---- reflector scalars (every thread, identical inputs)
-  const double sigma = sh.dtot[JJ];
-  const double alpha = sh.apiv[JJ];
+  const double sigma = sh.dtot[jj];
+  const double alpha = sh.apiv[jj];
   double tau, beta, v0 = 1.0;
   const bool zero = sigma == 0.0;
   if (zero) {
@@ -338,48 +388,28 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
   // one reciprocal per step (x / v0 -> x * (1/v0): within an ulp of the
   // reference's division, far inside the parity tolerance)
   const double inv0 = zero ? 0.0 : 1.0 / v0;
-  if (q == 0 && tid == 0 && JJ < x.kb) x.tau[x.j0 + JJ] = tau;
-  if (tid < JJ) sh.Gs[tid + JJ * (QR_NB + 1)] = sh.apiv[tid] + sh.dtot[tid] * inv0;
+  if (q == 0 && tid == 0 && jj < x.kb) x.tau[x.j0 + jj] = tau;
+  if (tid < jj) sh.Gs[tid + jj * (QR_NB + 1)] = sh.apiv[tid] + sh.dtot[tid] * inv0;
   // ---- v below the pivot, rank-1 update of the columns right of it
-  double v[R];
+  double v[R], nj[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int i = tid + QRR_NT * r;
-    v[r] = 0.0;
-    if (q == 0 && r == 0 && i == JJ) {
-      v[r] = 1.0;
-      a[r][JJ] = beta;
-    } else if (i < nloc && (q > 0 || i > JJ)) {
-      v[r] = a[r][JJ] * inv0;
-      a[r][JJ] = v[r];
-    }
+    const bool piv = q == 0 && r == 0 && i == jj;
+    v[r] = piv ? 1.0 : (part[r] ? xv[r] * inv0 : 0.0);
+    nj[r] = piv ? beta : (part[r] ? v[r] : xv[r]);   // new value of column jj
   }
-  if (tau != 0.0) {
+  const double ts = tau != 0.0 ? tau : 0.0;
 #pragma unroll
-    for (int c = JJ + 1; c < QR_NB; ++c) {
-      const double wc = tau * fma(sh.dtot[c], inv0, sh.apiv[c]);
+  for (int c = 0; c < QR_NB; ++c) {
+    const double wc = c > jj ? ts * fma(sh.dtot[c], inv0, sh.apiv[c]) : 0.0;
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[r][c] = fma(-wc, v[r], a[r][c]);
+    for (int r = 0; r < R; ++r) {
+      const double u = fma(-wc, v[r], a[r][c]);
+      a[r][c] = (c == jj) ? nj[r] : u;
     }
   }
 }
-
-// Steps JJ in [0, KBMAX) run unconditionally (a branch around the
-// shuffles would make the compiler lower every shuffle as a collective);
-// steps JJ >= kb see an all-zero column: tau = 0, no update, nothing stored.
-template <int R, int JJ, int KBMAX>
-struct QrrSteps {
-  static __device__ __forceinline__ void run(const QrrCtx& x, double (&a)[R][QR_NB], QrrShared& sh,
-                                             cg::cluster_group& cluster) {
-    qrr_step<R, JJ>(x, a, sh, cluster);
-    QrrSteps<R, JJ + 1, KBMAX>::run(x, a, sh, cluster);
-  }
-};
-template <int R, int KBMAX>
-struct QrrSteps<R, KBMAX, KBMAX> {
-  static __device__ __forceinline__ void run(const QrrCtx&, double (&)[R][QR_NB], QrrShared&,
-                                             cg::cluster_group&) {}
-};
 
 template <int R, int KBMAX>
 __global__ void __launch_bounds__(QRR_NT, 1) panel_qr_reg_kernel(const PanelJob* __restrict__ jobs) {
@@ -396,6 +426,13 @@ __global__ void __launch_bounds__(QRR_NT, 1) panel_qr_reg_kernel(const PanelJob*
   const int tid = threadIdx.x;
   __shared__ QrrShared sh;
 
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(qrr_smem(&sh.mbar[b])) : "memory");
+      qrr_arm(qrr_smem(&sh.mbar[b]), (uint32_t)((CL + 1) * QR_NB * sizeof(double)));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   double* P0 = J.P + (int64_t)j0 * m + j0 + r0;
   double a[R][QR_NB];
 #pragma unroll
@@ -413,8 +450,13 @@ __global__ void __launch_bounds__(QRR_NT, 1) panel_qr_reg_kernel(const PanelJob*
       *src = 0.0;
     }
   }
+  cluster.sync();   // every CTA's barriers are initialised and armed before any push
   const QrrCtx x{q, CL, nloc, tid, tid & 31, tid >> 5, kb, j0, J.tau};
-  QrrSteps<R, 0, KBMAX>::run(x, a, sh, cluster);
+  // KBMAX steps run unconditionally (a data-dependent trip count would make
+  // the compiler lower the shuffles as collectives); steps jj >= kb see an
+  // all-zero column: tau = 0, no update, nothing stored
+#pragma unroll 1
+  for (int jj = 0; jj < KBMAX; ++jj) qrr_step<R>(x, a, sh, jj);
 
   // R entries of the diagonal block out, explicit unit-lower V in
   if (q == 0 && tid < kb) {
@@ -427,8 +469,7 @@ __global__ void __launch_bounds__(QRR_NT, 1) panel_qr_reg_kernel(const PanelJob*
     }
   }
   __syncthreads();
-  // T_b from the Gram columns: row-parallel recurrence (trow in shared
-  // memory: a register array indexed by the thread's row would spill)
+  // T_b from the Gram columns: row-parallel recurrence
   if (q == 0 && tid < kb) {
     const int ar = tid;
     double tr[QR_NB];
@@ -459,7 +500,9 @@ __global__ void __launch_bounds__(QRR_NT, 1) panel_qr_reg_kernel(const PanelJob*
         if (c < kb) P0[i + (int64_t)c * m] = a[r][c];
     }
   }
-  cluster.sync();   // no CTA leaves while others may read its shared memory
+  // every push addressed to this CTA has landed (waited above); a relaxed
+  // cluster barrier keeps CTAs resident until all pushes were issued
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
 template <int R, int KBMAX>

@@ -163,6 +163,10 @@ struct spq_ctx {
   int64_t n_verified = 0;
   PivotSet piv;   // speculative mode: checks pending across calls
   unsigned long long* d_nnz_slots = nullptr;   // per-level trailing_nnz counters
+  // device GMRES: the original (unscaled) matrix in CSR
+  int64_t* d_csr_ptr = nullptr;
+  int* d_csr_idx = nullptr;
+  double* d_csr_val = nullptr;
   // device error slots for pivot checks
   int64_t* d_err_idx = nullptr;
   double* d_err_val = nullptr;
@@ -3222,6 +3226,205 @@ static int chain_dev(spq_ctx* c, double* d, int nrhs, int which) {
 
 int spq_apply_qt_dev(spq_ctx* c, double* d, int nrhs) { return chain_dev(c, d, nrhs, 0); }
 int spq_solve_w_dev(spq_ctx* c, double* d, int nrhs) { return chain_dev(c, d, nrhs, 1); }
+
+// ================================================================ GMRES
+// Right-preconditioned GMRES entirely on the device (reference
+// pkg/src/nestqr/solve.py:66-209): the operator v -> apply_qt(A solve_w(v))
+// runs as chain graphs + a CSR SpMV, Arnoldi with modified Gram-Schmidt (one
+// fused launch per step) and the conditional re-orthogonalisation test on
+// the device; only the Hessenberg column (j+2 scalars) and the true residual
+// norm come back per iteration for the Givens / least-squares update, which
+// the host does exactly like the reference.
+int spq_set_matrix(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indices,
+                   const double* data) {
+  return guarded(c, [&] {
+    if (N != c->N) throw SpqError(SPQ_ERR_BAD_INPUT, "matrix size does not match the factorization");
+    const int64_t nnz = indptr[N];
+    std::vector<int64_t> rp(N + 1, 0);
+    for (int64_t e = 0; e < nnz; ++e) {
+      if (indices[e] < 0 || indices[e] >= N) throw SpqError(SPQ_ERR_BAD_INPUT, "row index out of range");
+      rp[indices[e] + 1]++;
+    }
+    for (int64_t i = 0; i < N; ++i) rp[i + 1] += rp[i];
+    std::vector<int> ci(std::max<int64_t>(nnz, 1));
+    std::vector<double> cv(std::max<int64_t>(nnz, 1));
+    std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
+    for (int64_t j = 0; j < N; ++j)
+      for (int64_t e = indptr[j]; e < indptr[j + 1]; ++e) {
+        const int64_t at = fill[indices[e]]++;
+        ci[at] = (int)j;
+        cv[at] = data[e];
+      }
+    dfree(c, c->d_csr_ptr);
+    dfree(c, c->d_csr_idx);
+    dfree(c, c->d_csr_val);
+    c->d_csr_ptr = (int64_t*)dalloc(c, (N + 1) * sizeof(int64_t));
+    c->d_csr_idx = (int*)dalloc(c, ci.size() * sizeof(int));
+    c->d_csr_val = dalloc(c, cv.size() * sizeof(double));
+    CUDA_TRY(cudaMemcpyAsync(c->d_csr_ptr, rp.data(), (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+    CUDA_TRY(cudaMemcpyAsync(c->d_csr_idx, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    CUDA_TRY(cudaMemcpyAsync(c->d_csr_val, cv.data(), cv.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    sync(c);
+  });
+}
+
+int spq_gmres(spq_ctx* c, const double* b_h, const double* x0_h, double tol, int maxit,
+              int restart, double* x_h, double* hist_h, int* its_out, int* conv_out,
+              double* best_out) {
+  return guarded(c, [&] {
+    if (!c->finished) throw SpqError(SPQ_ERR_BAD_INPUT, "factorization not finished");
+    if (!c->d_csr_ptr) throw SpqError(SPQ_ERR_BAD_INPUT, "spq_set_matrix was not called");
+    if (maxit < 0) throw SpqError(SPQ_ERR_BAD_INPUT, "maxit must be >= 0");
+    const int64_t n = c->N;
+    const size_t vb = (size_t)n * sizeof(double);
+    const double thr = 1e-8;   // solve.py:25
+    ensure_chain_scratch(c, 1);
+    const int mcap = std::max(1, restart > 0 ? std::min(restart, std::max(maxit, 1)) : std::max(maxit, 1));
+    // device workspace: Q (n x (mcap+1)) | b | x | xn | best | w | t
+    double* Q = dalloc(c, (size_t)n * (mcap + 1) * sizeof(double));
+    double* vecs = dalloc(c, 6 * vb);
+    double *b = vecs, *x = b + n, *xn = x + n, *best = xn + n, *w = best + n, *t = w + n;
+    double* part = dalloc(c, (size_t)(mcap + 3) * KRY_G * sizeof(double));
+    double* scal = dalloc(c, (size_t)(3 * (mcap + 2) + 8) * sizeof(double));
+    double* Hcol = scal;                  // mcap + 2
+    double* cvec = Hcol + (mcap + 2);     // mcap + 2
+    double* ydev = cvec + (mcap + 2);     // mcap + 2
+    double* sc = ydev + (mcap + 2);       // [0] norm, [1] norm2
+    int* flag = (int*)dalloc(c, sizeof(int));
+    double* partA = part;
+    double* partB = part + KRY_G;
+    double* partM = part + 2 * KRY_G;
+    auto norm_of = [&](const double* v, double* out) {
+      kry_dot_part(v, v, n, partA, c->st);
+      kry_finish(partA, out, true, c->st);
+    };
+    auto fetch = [&](const double* d, double* h, int cnt) {
+      CUDA_TRY(cudaMemcpyAsync(h, d, cnt * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+    };
+    // preconditioned operator pieces on c->d_vec
+    auto apply_qt_into = [&](const double* src, double* dst) {
+      CUDA_TRY(cudaMemcpyAsync(c->d_vec, src, vb, cudaMemcpyDeviceToDevice, c->st));
+      run_chain(c, 0, 1);
+      CUDA_TRY(cudaMemcpyAsync(dst, c->d_vec, vb, cudaMemcpyDeviceToDevice, c->st));
+    };
+    CUDA_TRY(cudaMemcpyAsync(b, b_h, vb, cudaMemcpyHostToDevice, c->st));
+    if (x0_h) CUDA_TRY(cudaMemcpyAsync(x, x0_h, vb, cudaMemcpyHostToDevice, c->st));
+    else CUDA_TRY(cudaMemsetAsync(x, 0, vb, c->st));
+    double h2[2];
+    norm_of(b, sc);
+    fetch(sc, h2, 1);
+    const double bnorm = h2[0];
+    int nh = 0;
+    if (bnorm == 0.0) {
+      std::fill(x_h, x_h + n, 0.0);
+      hist_h[0] = 0.0;
+      *its_out = 0;
+      *conv_out = 1;
+      *best_out = 0.0;
+    } else {
+      kry_spmv(c->d_csr_ptr, c->d_csr_idx, c->d_csr_val, x, b, t, n, 1, c->st);
+      norm_of(t, sc);
+      fetch(sc, h2, 1);
+      hist_h[nh++] = h2[0] / bnorm;
+      bool done = hist_h[0] <= tol;
+      double best_r = hist_h[0];
+      CUDA_TRY(cudaMemcpyAsync(best, x, vb, cudaMemcpyDeviceToDevice, c->st));
+      int its = 0;
+      std::vector<double> H, cs, sn, g, hc(mcap + 2), y;
+      while (!done && its < maxit) {
+        // z = apply_qt(b - A x), beta = ||z||
+        kry_spmv(c->d_csr_ptr, c->d_csr_idx, c->d_csr_val, x, b, t, n, 1, c->st);
+        apply_qt_into(t, Q);
+        norm_of(Q, sc);
+        fetch(sc, h2, 1);
+        const double beta = h2[0];
+        if (beta == 0.0) { done = true; break; }
+        const int m = restart > 0 ? std::min(restart, maxit - its) : maxit - its;
+        H.assign((size_t)(m + 1) * m, 0.0);   // column-major (m+1) x m
+        cs.assign(m, 0.0); sn.assign(m, 0.0); g.assign(m + 1, 0.0);
+        g[0] = beta;
+        kry_scale_div(Q, sc, Q, n, c->st);
+        CUDA_TRY(cudaMemcpyAsync(xn, x, vb, cudaMemcpyDeviceToDevice, c->st));
+        auto Hij = [&](int i, int j) -> double& { return H[(size_t)j * (m + 1) + i]; };
+        for (int j = 0; j < m; ++j) {
+          const double* qj = Q + (size_t)j * n;
+          // w = apply_qt(A solve_w(q_j))
+          CUDA_TRY(cudaMemcpyAsync(c->d_vec, qj, vb, cudaMemcpyDeviceToDevice, c->st));
+          run_chain(c, 1, 1);
+          kry_spmv(c->d_csr_ptr, c->d_csr_idx, c->d_csr_val, c->d_vec, nullptr, t, n, 0, c->st);
+          apply_qt_into(t, w);
+          // modified Gram-Schmidt, one fused launch per step
+          kry_dot_part(Q, w, n, partA, c->st);
+          for (int i = 0; i <= j; ++i) {
+            const double* qn = i < j ? Q + (size_t)(i + 1) * n : nullptr;
+            kry_mgs_step(Q + (size_t)i * n, qn, w, n, (i & 1) ? partB : partA,
+                         (i & 1) ? partA : partB, Hcol + i, c->st);
+          }
+          double* pw = ((j + 1) & 1) ? partB : partA;   // w.w partials of the last step
+          kry_finish(pw, sc, true, c->st);
+          // conditional re-orthogonalisation against Q[:, 0:j+1]
+          kry_multi_dot(Q, n, j + 1, w, n, partM, cvec, c->st);
+          kry_reorth(Q, n, j + 1, cvec, sc, thr, w, n, Hcol, flag, partA, c->st);
+          kry_finish(partA, sc + 1, true, c->st);
+          CUDA_TRY(cudaMemcpyAsync(hc.data(), Hcol, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+          fetch(sc, h2, 2);
+          for (int i = 0; i <= j; ++i) Hij(i, j) = hc[i];
+          const double wn = h2[1];
+          Hij(j + 1, j) = wn;
+          for (int i = 0; i < j; ++i) {     // previous rotations
+            const double a = Hij(i, j), bb = Hij(i + 1, j);
+            Hij(i, j) = cs[i] * a + sn[i] * bb;
+            Hij(i + 1, j) = -sn[i] * a + cs[i] * bb;
+          }
+          const double den = std::hypot(Hij(j, j), Hij(j + 1, j));
+          if (den == 0.0) { cs[j] = 1.0; sn[j] = 0.0; }
+          else { cs[j] = Hij(j, j) / den; sn[j] = Hij(j + 1, j) / den; }
+          Hij(j, j) = cs[j] * Hij(j, j) + sn[j] * Hij(j + 1, j);
+          Hij(j + 1, j) = 0.0;
+          g[j + 1] = -sn[j] * g[j];
+          g[j] = cs[j] * g[j];
+          // y = H[0:j+1, 0:j+1]^{-1} g[0:j+1] (upper triangular)
+          y.assign(j + 1, 0.0);
+          for (int i = j; i >= 0; --i) {
+            double s = g[i];
+            for (int l = i + 1; l <= j; ++l) s -= Hij(i, l) * y[l];
+            y[i] = s / Hij(i, i);
+          }
+          // x_new = x + solve_w(Q y); true residual
+          CUDA_TRY(cudaMemcpyAsync(ydev, y.data(), (j + 1) * sizeof(double), cudaMemcpyHostToDevice, c->st));
+          kry_gemv(Q, n, j + 1, ydev, c->d_vec, n, c->st);
+          run_chain(c, 1, 1);
+          kry_add(x, c->d_vec, xn, n, c->st);
+          kry_spmv(c->d_csr_ptr, c->d_csr_idx, c->d_csr_val, xn, b, t, n, 1, c->st);
+          norm_of(t, sc);
+          fetch(sc, h2, 1);
+          ++its;
+          hist_h[nh++] = h2[0] / bnorm;
+          if (hist_h[nh - 1] < best_r) {
+            best_r = hist_h[nh - 1];
+            CUDA_TRY(cudaMemcpyAsync(best, xn, vb, cudaMemcpyDeviceToDevice, c->st));
+          }
+          if (std::fabs(g[j + 1]) / bnorm <= tol || hist_h[nh - 1] <= tol) { done = true; break; }
+          if (wn <= 1e-300) break;
+          kry_scale_div(w, sc + 1, Q + (size_t)(j + 1) * n, n, c->st);
+        }
+        CUDA_TRY(cudaMemcpyAsync(x, xn, vb, cudaMemcpyDeviceToDevice, c->st));
+      }
+      CUDA_TRY(cudaMemcpyAsync(x_h, best, vb, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      *its_out = its;
+      *conv_out = done ? 1 : 0;
+      *best_out = best_r;
+    }
+    dfree(c, Q);
+    dfree(c, vecs);
+    dfree(c, part);
+    dfree(c, scal);
+    dfree(c, flag);
+    sync(c);
+  });
+}
 
 int spq_mark(spq_ctx* c, int slot) {
   return guarded(c, [&] {

@@ -230,6 +230,30 @@ class Factorization:
         """W^{-1} y (reference `factor.py:295-300`)."""
         return self._run("spq_solve_w_host", y)
 
+    def gmres_device(self, A, b, tol=1e-12, maxit=300, restart=None, x0=None):
+        """GMRES of `solve.py:66-209` run entirely on the device (spq_gmres);
+        returns (x, iterations, history, converged, best_residual)."""
+        import ctypes as C
+        from .sparse import as_csc
+        n, m, indptr, indices, data = as_csc(A)
+        if n != self.N or m != self.N:
+            raise NestqrError("factorization size does not match the matrix")
+        key = (id(A), int(indptr[-1]))
+        if getattr(self, "_matrix_key", None) != key:
+            self._ctx.call("spq_set_matrix", n, indptr, indices, data)
+            self._matrix_key = key
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(n)
+        hist = np.empty(max(int(maxit), 0) + 1)
+        its, conv, best = C.c_int(), C.c_int(), C.c_double()
+        x0a = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+        self._ctx.call("spq_gmres", b, None if x0a is None else x0a.ctypes.data, float(tol),
+                       int(maxit), 0 if restart is None else int(restart), x, hist,
+                       C.byref(its), C.byref(conv), C.byref(best))
+        k = int(its.value)
+        nh = k + 1 if float(np.linalg.norm(b)) != 0.0 else 1
+        return x, k, hist[:nh].copy(), bool(conv.value), float(best.value)
+
     def materialize_preconditioned(self):
         X = self.solve_w(np.eye(self.N))
         from .sparse import matvec

@@ -195,3 +195,35 @@ def test_speculative_flags_verified_and_equal_exact_mode():
     assert len(bs) == len(be)
     for x, y in zip(bs, be):
         assert np.abs(x.R_ss - y.R_ss).max() <= 1e-10 * np.abs(y.R_ss).max()
+
+
+def test_device_gmres_matches_host_loop():
+    """spq_gmres (whole Arnoldi loop in HBM) against the host loop of
+    solve.py:66-209 on the same factorization: iterations within 1, final
+    residual within 10x, solutions agreeing; restarted GMRES, an initial
+    guess and a zero right-hand side too."""
+    from paper_2010_06807_b200.factor import factorize
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    from paper_2010_06807_b200.solve import gmres, gmres_host
+    from paper_2010_06807_b200.sparse import matvec
+    A, dims, L, eps, b, tol = make_config("C3", n=48)
+    tree = partition_geometric(dims, L)
+    F = factorize(A, tree, eps=eps)
+    for kw in ({}, {"restart": 2}, {"x0": np.full(A.ncols, 0.5)}):
+        xd, rd = gmres(A, b, F, tol=tol, **kw)
+        xh, rh = gmres_host(A, b, F, tol=tol, **kw)
+        assert rd.meta.get("device")
+        assert abs(rd.iterations - rh.iterations) <= 1, kw
+        assert len(rd.residuals) == rd.iterations + 1
+        assert rd.converged == rh.converged
+        assert rd.final_residual <= 10 * max(rh.final_residual, 1e-16), kw
+        np.testing.assert_allclose(rd.residuals[:2], rh.residuals[:2], rtol=1e-6)
+        r = np.linalg.norm(b - matvec(A, xd)) / np.linalg.norm(b)
+        assert r <= 10 * max(rh.final_residual, 1e-16)
+        assert np.abs(xd - xh).max() <= 1e-8 * np.abs(xh).max()
+    x0, r0 = gmres(A, np.zeros(A.ncols), F, tol=tol)
+    assert r0.iterations == 0 and r0.converged and not x0.any()
+    # maxit cap honoured, not converged
+    x1, r1 = gmres(A, b, F, tol=1e-30, maxit=3)
+    assert r1.iterations == 3 and not r1.converged and len(r1.residuals) == 4
