@@ -124,6 +124,9 @@ struct ChainOp {
   const double* R;
   const double* Rsn;
   double* scratch;      // per chunk 3*k doubles of global scratch when k is too big for shared memory
+  const double* W;      // WY: precomputed V T^T (WY_T) or V T (WY_N), m x k (ld m), or nullptr
+  int* cnt;             // WY: chunk arrival counter (last chunk of phase A reduces)
+  int64_t u_off;        // WY: offset of the reduced vector u (k) in the wave scratch (x nrhs)
   int nchunk;           // CTAs working on this op
   int per;              // rows (WY) or R_sn columns (TRI) per chunk
   int64_t part_off;     // offset of this op's partials in the wave scratch (x nrhs)

@@ -190,6 +190,31 @@ namespace spq {
 constexpr int CW_NT = 512;
 constexpr int CW_NW = CW_NT / 32;
 
+// out[c] = sum_q part[q*k + c], q < nq: g lanes per column (g = power of two
+// ~ nq/4, so each lane has a few independent loads), fixed shuffle tree
+__device__ __forceinline__ void chain_reduce_partials(const double* part, int nq, int k,
+                                                      double* out) {
+  int g = 1;
+  while (g < 32 && g * 4 < nq) g <<= 1;
+  const int tid = threadIdx.x, sub = tid & (g - 1);
+  const int per_pass = CW_NT / g;
+  for (int c0 = 0; c0 < k; c0 += per_pass) {
+    const int c = c0 + tid / g;
+    double s0 = 0.0, s1 = 0.0;
+    if (c < k) {
+      int q = sub;
+      for (; q + g < nq; q += 2 * g) {
+        s0 += __ldcg(part + (int64_t)q * k + c);
+        s1 += __ldcg(part + (int64_t)(q + g) * k + c);
+      }
+      if (q < nq) s0 += __ldcg(part + (int64_t)q * k + c);
+    }
+    double s = s0 + s1;
+    for (int sh = g >> 1; sh; sh >>= 1) s += __shfl_xor_sync(0xffffffffu, s, sh);
+    if (sub == 0 && c < k) out[c] = s;
+  }
+}
+
 __global__ void __launch_bounds__(CW_NT) chain_phaseA_kernel(const ChainOp* __restrict__ ops,
                                                              const int2* __restrict__ tasks,
                                                              double* __restrict__ part,
@@ -204,15 +229,83 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseA_kernel(const ChainOp* __re
     const int i0 = chunk * o.per, i1 = min(o.m, i0 + o.per);
     for (int r = 0; r < nrhs; ++r) {
       const double* zr = z + (int64_t)r * N;
-      for (int c = warp; c < k; c += CW_NW) {
+      // z rows of the chunk staged once in shared memory (gathered)
+      __shared__ double zs[CW_NT * 2];
+      const int nrow = i1 - i0;
+      const bool staged = nrow <= CW_NT * 2;
+      if (staged)
+        for (int i = tid; i < nrow; i += CW_NT) zs[i] = zr[o.idx[i0 + i]];
+      __syncthreads();
+      // two columns per warp pass, four independent accumulators (the loads
+      // are latency-bound: keep several in flight per lane)
+      for (int c = warp; c < k; c += 2 * CW_NW) {
+        const int c2 = c + CW_NW;
         const double* vc = o.V + (int64_t)c * o.m;
-        double s = 0.0;
-        for (int i = i0 + lane; i < i1; i += 32) s += vc[i] * zr[o.idx[i]];
+        const double* vd = o.V + (int64_t)(c2 < k ? c2 : c) * o.m;
+        double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
+        int i = i0 + lane;
+        for (; i + 32 < i1; i += 64) {
+          const double z0 = staged ? zs[i - i0] : zr[o.idx[i]];
+          const double z1 = staged ? zs[i + 32 - i0] : zr[o.idx[i + 32]];
+          s0 = fma(vc[i], z0, s0);
+          s1 = fma(vc[i + 32], z1, s1);
+          t0 = fma(vd[i], z0, t0);
+          t1 = fma(vd[i + 32], z1, t1);
+        }
+        if (i < i1) {
+          const double z0 = staged ? zs[i - i0] : zr[o.idx[i]];
+          s0 = fma(vc[i], z0, s0);
+          t0 = fma(vd[i], z0, t0);
+        }
+        double s = s0 + s1, t = t0 + t1;
 #pragma unroll
-        for (int q = 16; q; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
-        if (lane == 0) part[o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k + c] = s;
+        for (int q = 16; q; q >>= 1) {
+          s += __shfl_xor_sync(0xffffffffu, s, q);
+          t += __shfl_xor_sync(0xffffffffu, t, q);
+        }
+        if (lane == 0) {
+          part[o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k + c] = s;
+          if (c2 < k) part[o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k + c2] = t;
+        }
       }
+      __syncthreads();
     }
+    // the last chunk to arrive reduces the partials (fixed chunk order) and
+    // forms u = w (W precomputed) or T^T w / T w, once per operation
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(o.cnt, 1) == o.nchunk - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    __shared__ double wred[CW_NT * 2];
+    for (int r = 0; r < nrhs; ++r) {
+      const double* pr = part + o.part_off * nrhs + (int64_t)r * o.nchunk * k;
+      double* u = part + o.u_off * nrhs + (int64_t)r * 2 * k;   // u (k) | global w (k)
+      const bool sm = k <= CW_NT * 2;
+      double* wv = o.W ? u : (sm ? wred : u + k);
+      chain_reduce_partials(pr, o.nchunk, k, wv);
+      __syncthreads();
+      if (!o.W && o.kind == CH_WY_T) {   // (T^T w)_a = sum_{b<=a} T[b,a] w_b: warp per a (coalesced)
+        for (int a = warp; a < k; a += CW_NW) {
+          double s = 0.0;
+          for (int b = lane; b <= a; b += 32) s = fma(o.T[b + (int64_t)a * k], sm ? wv[b] : __ldcg(wv + b), s);
+#pragma unroll
+          for (int q = 16; q; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
+          if (lane == 0) u[a] = s;
+        }
+      } else if (!o.W) {                 // (T w)_a = sum_{b>=a} T[a,b] w_b: thread per a (coalesced)
+        for (int a = tid; a < k; a += CW_NT) {
+          double s = 0.0;
+          for (int b = a; b < k; ++b) s = fma(o.T[a + (int64_t)b * k], sm ? wv[b] : __ldcg(wv + b), s);
+          u[a] = s;
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) *o.cnt = 0;   // ready for the next application
+    return;
   } else if (o.n > 0) {
     // R_sn[:, chunk] y[chunk]: rows a split over threads, columns over P partitions
     __shared__ double redA[CW_NT];
@@ -258,33 +351,36 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __re
     double* zr = z + (int64_t)r * N;
     const double* pr = part + o.part_off * nrhs + (int64_t)r * o.nchunk * k;
     if (o.kind == CH_WY_T || o.kind == CH_WY_N) {
-      for (int c = tid; c < k; c += CW_NT) {
-        double s = 0.0;
-        for (int q = 0; q < o.nchunk; ++q) s += pr[(int64_t)q * k + c];
-        w[c] = s;
-      }
+      // u (reduced by the last chunk of phase A) into shared memory, then
+      // z[rows] -= M u with M = W (= V T^T / V T, precomputed) or V
+      const double* u = part + o.u_off * nrhs + (int64_t)r * 2 * k;
+      for (int c = tid; c < k; c += CW_NT) w[c] = __ldcg(u + c);
       __syncthreads();
-      for (int a = tid; a < k; a += CW_NT) {
-        double s = 0.0;
-        if (o.kind == CH_WY_T)
-          for (int b = 0; b <= a; ++b) s += o.T[b + (int64_t)a * k] * w[b];
-        else
-          for (int b = a; b < k; ++b) s += o.T[a + (int64_t)b * k] * w[b];
-        w2[a] = s;
-      }
-      __syncthreads();
+      const double* M = o.W ? o.W : o.V;
       const int i0 = chunk * o.per, i1 = min(o.m, i0 + o.per);
       for (int i = i0 + tid; i < i1; i += CW_NT) {
-        double s = 0.0;
-        for (int c = 0; c < k; ++c) s += o.V[i + (int64_t)c * o.m] * w2[c];
-        zr[o.idx[i]] -= s;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int c = 0;
+        for (; c + 3 < k; c += 4) {
+          s0 = fma(M[i + (int64_t)c * o.m], w[c], s0);
+          s1 = fma(M[i + (int64_t)(c + 1) * o.m], w[c + 1], s1);
+          s2 = fma(M[i + (int64_t)(c + 2) * o.m], w[c + 2], s2);
+          s3 = fma(M[i + (int64_t)(c + 3) * o.m], w[c + 3], s3);
+        }
+        for (; c < k; ++c) s0 = fma(M[i + (int64_t)c * o.m], w[c], s0);
+        zr[o.idx[i]] -= (s0 + s1) + (s2 + s3);
       }
       __syncthreads();
     } else {
       if (chunk != 0) return;
+      if (o.n > 0) {
+        chain_reduce_partials(pr, o.nchunk, k, w);   // R_sn y_n partials
+      } else {
+        for (int a = tid; a < k; a += CW_NT) w[a] = 0.0;
+      }
+      __syncthreads();
       for (int a = tid; a < k; a += CW_NT) {
-        double s = 0.0;
-        for (int q = 0; q < o.nchunk && o.n > 0; ++q) s += pr[(int64_t)q * k + a];
+        const double s = w[a];
         if (o.kind == CH_TRI_SOLVE) {
           w[a] = zr[o.idx[a]] - s;
         } else {   // CH_TRI_MUL: R y_s + R_sn y_n

@@ -108,6 +108,8 @@ struct Record {
   int *d_rows = nullptr, *d_cols_s = nullptr, *d_cols_n = nullptr;
   int64_t payload_scalars = 0;
   bool full_T = false;   // T already complete (built for a target update)
+  double* WT = nullptr;  // chain: V T^T (m x k), built at chain compile time
+  double* WN = nullptr;  // chain: V T (sparsifiers, solve_w direction)
 };
 
 // families for device timing / flop accounting
@@ -288,6 +290,14 @@ struct GlobalCache {
 GlobalCache& gcache() {
   static GlobalCache* g = new GlobalCache();   // leaked on purpose (process lifetime)
   return *g;
+}
+
+size_t arena_free_bytes() {
+  auto& g = gcache();
+  std::lock_guard<std::mutex> lk(g.mu);
+  size_t t = 0;
+  for (auto& kv : g.arena.free_off) t += kv.second;
+  return t;
 }
 
 struct HostTimer {
@@ -2648,19 +2658,33 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
     P.cnt.back()++;
     P.kmax.back() = std::max(P.kmax.back(), ops[t].k);
   }
-  // chunking: ~64K multiply-adds per CTA, at most 64 CTAs per op
+  // chunking: per wave, the operations split into chunks so the wave fills
+  // ~2 CTAs per SM (the chain is latency-bound wave by wave), at least 64
+  // rows (WY) / columns (R_sn) per chunk
   std::vector<int2> tasks;
   P.toff.clear(); P.tcnt.clear(); P.part_sz.clear();
   size_t scr = 0;
-  for (auto& o : ordered) {
-    const bool wy = o.kind == CH_WY_T || o.kind == CH_WY_N;
-    const int64_t len = wy ? o.m : o.n;           // the dimension that is split
-    const int64_t work = (int64_t)std::max(len, (int64_t)1) * std::max(o.k, 1);
-    int nch = (int)std::min<int64_t>(64, std::max<int64_t>(1, work / 65536));
-    if (!wy && o.n == 0) nch = 1;
-    o.per = (int)std::max<int64_t>(1, (len + nch - 1) / nch);
-    o.nchunk = (int)std::max<int64_t>(1, (len + o.per - 1) / o.per);
-    if ((size_t)2 * o.k * sizeof(double) > CHAIN_SMEM_MAX) scr += 3 * (size_t)o.k * o.nchunk;
+  for (size_t w = 0; w < P.off.size(); ++w) {
+    double wave_work = 0;
+    for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
+      const ChainOp& o = ordered[t];
+      const bool wy = o.kind == CH_WY_T || o.kind == CH_WY_N;
+      wave_work += (double)std::max<int64_t>(wy ? o.m : o.n, 1) * std::max(o.k, 1);
+    }
+    const double per_cta = std::max(4096.0, wave_work / (2.0 * c->nsm));
+    for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
+      ChainOp& o = ordered[t];
+      const bool wy = o.kind == CH_WY_T || o.kind == CH_WY_N;
+      const int64_t len = wy ? o.m : o.n;           // the dimension that is split
+      const double work = (double)std::max(len, (int64_t)1) * std::max(o.k, 1);
+      int64_t nch = (int64_t)std::ceil(work / per_cta);
+      nch = std::max<int64_t>(1, std::min<int64_t>(nch, (len + 63) / 64));
+      nch = std::min<int64_t>(nch, 512);
+      if (!wy && o.n == 0) nch = 1;
+      o.per = (int)std::max<int64_t>(1, (len + nch - 1) / nch);
+      o.nchunk = (int)std::max<int64_t>(1, (len + o.per - 1) / o.per);
+      if ((size_t)2 * o.k * sizeof(double) > CHAIN_SMEM_MAX) scr += 3 * (size_t)o.k * o.nchunk;
+    }
   }
   if (scr) {   // ops too large for shared memory: private global scratch per chunk
     double* base = dalloc(c, scr * sizeof(double));
@@ -2671,6 +2695,9 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
         off += 3 * (size_t)o.k * o.nchunk;
       }
   }
+  // arrival counters of the WY operations (reset by the last chunk)
+  int* cnts = ordered.empty() ? nullptr : (int*)dalloc(c, ordered.size() * sizeof(int));
+  if (cnts) CUDA_TRY(cudaMemsetAsync(cnts, 0, ordered.size() * sizeof(int), c->st));
   for (size_t w = 0; w < P.off.size(); ++w) {
     int km = 0;
     int64_t psz = 0;
@@ -2680,7 +2707,13 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
       if (!o.scratch) km = std::max(km, o.k);
       o.part_off = psz;
       psz += (int64_t)o.nchunk * std::max(o.k, 1);
+      o.cnt = cnts + t;
       for (int q = 0; q < o.nchunk; ++q) tasks.push_back(make_int2(t - P.off[w], q));
+    }
+    for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {   // reduced vectors after the partials
+      ChainOp& o = ordered[t];
+      o.u_off = psz;
+      psz += 2 * (int64_t)std::max(o.k, 1);
     }
     P.tcnt.push_back((int)tasks.size() - P.toff.back());
     P.kmax[w] = km;
@@ -2697,14 +2730,54 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
   }
 }
 
+// W = V T^T (transposed) or V T for every WY record: the chain update
+// becomes z -= W (V^T z) with no triangular product per chunk.  Built with
+// the batched DMMA GEMM at chain compile time; skipped (kernels fall back
+// to the T path) when the extra payload would not fit comfortably.
+constexpr int CHAIN_W_KMIN = 192;   // below: T w in the reducing chunk is cheaper
+void build_chain_W(spq_ctx* c) {
+  const int kmin = env_flag("SPQ_CHAIN_W") ? 1 : CHAIN_W_KMIN;
+  size_t need = 0;
+  for (auto& r : c->recs)
+    if (r.k >= kmin) need += (size_t)r.m * r.k * (r.kind == REC_SPARSIFY ? 2 : 1);
+  if (need == 0 || env_flag("SPQ_CHAIN_NO_W")) return;
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  if (need * sizeof(double) * 3 > fr + arena_free_bytes()) return;
+  CopyBatch cp;
+  GemmBatch gT, gN;
+  std::vector<double*> tts;
+  for (auto& r : c->recs) {
+    if (r.k < kmin) continue;
+    const size_t mk = (size_t)r.m * r.k, kk = (size_t)r.k * r.k;
+    const bool sp = r.kind == REC_SPARSIFY;
+    r.WT = dalloc(c, mk * sizeof(double));
+    double* Tt = dalloc(c, kk * sizeof(double));
+    tts.push_back(Tt);
+    CopyTask x{};
+    x.src = r.T; x.dst = Tt; x.nr = r.k; x.nc = r.k; x.lds = r.k; x.ldd = r.k; x.trans = 1;
+    cp.add(x);
+    gT.add(r.V, r.m, Tt, r.k, r.WT, r.m, r.m, r.k, r.k, 1.0, 0.0);
+    if (sp) {
+      r.WN = dalloc(c, mk * sizeof(double));
+      gN.add(r.V, r.m, r.T, r.k, r.WN, r.m, r.m, r.k, r.k, 1.0, 0.0);
+    }
+  }
+  cp.run(c);
+  gT.run(c, false, 0);
+  gN.run(c, false, 0);
+  for (double* p : tts) dfree(c, p);
+}
+
 void compile_chains(spq_ctx* c) {
+  build_chain_W(c);
   std::vector<ChainOp> ops;
   std::vector<std::vector<int>> wr, rd;
   auto to_int = [](const std::vector<int64_t>& v) { return std::vector<int>(v.begin(), v.end()); };
   // apply_qt: every record's panel on its rows, in chain order
   for (auto& r : c->recs) {
     if (r.k <= 0) continue;
-    ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_rows, nullptr, r.V, r.T, nullptr, nullptr, nullptr, 1, 1, 0});
+    ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_rows, nullptr, r.V, r.T, nullptr, nullptr, nullptr, r.WT, nullptr, 0, 1, 1, 0});
     wr.push_back(to_int(r.rows));
     rd.push_back({});
   }
@@ -2715,14 +2788,14 @@ void compile_chains(spq_ctx* c) {
     Record& r = *it;
     if (r.kind == REC_SPARSIFY) {
       if (r.k <= 0) continue;
-      ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, 1, 1, 0});
+      ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, r.WN, nullptr, 0, 1, 1, 0});
       wr.push_back(to_int(r.cols_s));
       rd.push_back({});
     } else {
       if (r.k <= 0) continue;
       const bool bh = r.kind == REC_ELIM;
       ops.push_back(ChainOp{CH_TRI_SOLVE, r.k, r.k, bh ? r.n : 0, r.d_cols_s,
-                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr, 1, 1, 0});
+                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr, nullptr, nullptr, 0, 1, 1, 0});
       wr.push_back(to_int(r.cols_s));
       rd.push_back(bh ? to_int(r.cols_n) : std::vector<int>());
     }
@@ -2733,13 +2806,13 @@ void compile_chains(spq_ctx* c) {
   for (auto& r : c->recs) {
     if (r.k <= 0) continue;
     if (r.kind == REC_SPARSIFY) {
-      ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, 1, 1, 0});
+      ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, r.WT, nullptr, 0, 1, 1, 0});
       wr.push_back(to_int(r.cols_s));
       rd.push_back({});
     } else {
       const bool bh = r.kind == REC_ELIM;
       ops.push_back(ChainOp{CH_TRI_MUL, r.k, r.k, bh ? r.n : 0, r.d_cols_s,
-                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr, 1, 1, 0});
+                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr, nullptr, nullptr, 0, 1, 1, 0});
       wr.push_back(to_int(r.cols_s));
       rd.push_back(bh ? to_int(r.cols_n) : std::vector<int>());
     }
