@@ -189,7 +189,7 @@ int cpqr_cluster_size(int m, int ncap);
 size_t cpqr_cluster_smem(int m, int ncap, int cl);
 void launch_cpqr_cluster(const CpqrJob* d_jobs, int njobs, int cl, size_t smem, cudaStream_t st);
 int cpqr_reg_plan(int m, int n, int variant, int* tpc);
-size_t cpqr_reg_smem(int padded_rows);
+size_t cpqr_reg_smem(int padded_rows, int cl);
 void launch_cpqr_reg(const CpqrJob* d_jobs, int njobs, int variant, int cl, int tpc, size_t smem,
                      cudaStream_t st);
 void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax,

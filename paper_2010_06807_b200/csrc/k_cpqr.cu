@@ -889,11 +889,41 @@ __device__ __forceinline__ bool rg_better(double v, unsigned long long k, double
   return v > bv || (v == bv && (int)(k >> 32) < (int)(bk >> 32));
 }
 
-struct RgLayout {   // shared memory (doubles then keys); rows padded to mp = tpc * R
-  int m1;
-  __host__ __device__ explicit RgLayout(int mp) : m1(mp > 0 ? mp : 1) {}
-  // vbuf (m1) | candcol [2][m1] | cval [2] | wv [RG_NW] | ckey [2] | wk [RG_NW]
-  __host__ __device__ size_t bytes() const { return (size_t)(3 * m1 + 2 + RG_NW) * 8 + (2 + RG_NW) * 8 + 64; }
+// DSMEM push exchange: at the end of every step each CTA pushes its best
+// candidate (value, key, column) with ONE bulk copy per destination
+// (cp.async.bulk shared::cta -> shared::cluster, completing on the
+// destination's mbarrier).  After its wait, every CTA holds all CL
+// candidates locally: no cluster barrier (which compiles to MEMBAR.GPU +
+// L1 invalidation per step on sm_100a) and no remote loads.
+__device__ __forceinline__ uint32_t rg_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t rg_mapa(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void rg_arm(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void rg_wait(uint32_t mbar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                 "selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(mbar), "r"(parity) : "memory");
+  }
+}
+
+struct RgLayout {   // shared memory in doubles; rows padded to mp = tpc * R
+  int m1, cl, rec;  // rec = one candidate record: [value, key, column (m1)]
+  __host__ __device__ RgLayout(int mp, int cl_) : m1(mp > 0 ? ((mp + 1) & ~1) : 2), cl(cl_), rec(m1 + 2) {}
+  // vbuf (m1) | SX [2][rec] | RX [2][cl][rec] | wv [RG_NW] | wk [RG_NW] | mbar [2]
+  __host__ __device__ size_t sx() const { return (size_t)m1; }
+  __host__ __device__ size_t rx() const { return sx() + 2 * (size_t)rec; }
+  __host__ __device__ size_t wvo() const { return rx() + 2 * (size_t)cl * rec; }
+  __host__ __device__ size_t bytes() const { return (wvo() + 2 * RG_NW + 2) * 8 + 64; }
 };
 
 template <int R, int C>
@@ -914,13 +944,22 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
   const int mp = tpc * R;                    // padded rows
   const int ph0 = q * cpc + grp * C;         // first own physical column
   extern __shared__ __align__(16) double rs[];
-  const RgLayout L(mp);
+  const RgLayout L(mp, CL);
   double* vbuf = rs;                         // v (zero outside rows i..m-1)
-  double* candcol = vbuf + L.m1;             // [2][m1]
-  double* cval = candcol + 2 * L.m1;         // [2]
-  double* wv = cval + 2;                     // [RG_NW]
-  unsigned long long* ckey = reinterpret_cast<unsigned long long*>(wv + RG_NW);   // [2]
-  unsigned long long* wk = ckey + 2;         // [RG_NW]
+  double* SX = rs + L.sx();                  // [2][rec] own candidate, staged for the push
+  double* RX = rs + L.rx();                  // [2][CL][rec] every CTA's candidate
+  double* wv = rs + L.wvo();                 // [RG_NW]
+  unsigned long long* wk = reinterpret_cast<unsigned long long*>(wv + RG_NW);   // [RG_NW]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(wk + RG_NW);                     // [2]
+  const uint32_t rec_bytes = (uint32_t)(L.rec * sizeof(double));
+
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(rg_smem(&mbar[b])) : "memory");
+      rg_arm(rg_smem(&mbar[b]), rec_bytes * CL);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
 
   // own columns: rows sub + tpc*r (zero beyond m / beyond n)
   double x[C][R];
@@ -935,9 +974,10 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
     }
   }
   for (int a = tid; a < L.m1; a += RG_NT) vbuf[a] = 0.0;
+  cluster.sync();   // barriers initialised and armed everywhere before the first push
 
-  // CTA argmax over every group's (norm, position); the owner group
-  // publishes that column into candcol[slot]
+  // CTA argmax over every group's (norm, position); the owner group stages
+  // that column, then one thread pushes the record to every CTA
   auto publish = [&](double bv, unsigned long long bk, int slot) {
 #pragma unroll
     for (int o = 16; o >= tpc; o >>= 1) {    // lanes of a group agree already
@@ -955,15 +995,30 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
       const unsigned long long ok = __shfl_xor_sync(0xffffffffu, ck, o);
       if (rg_better(ov, ok, cv, ck)) { cv = ov; ck = ok; }
     }
+    double* sx = SX + slot * L.rec;
     const int cph = (int)(ck & 0xffffffffu);
     if (cv >= 0.0 && cph >= ph0 && cph < ph0 + C) {
 #pragma unroll
       for (int c = 0; c < C; ++c)
         if (ph0 + c == cph)
 #pragma unroll
-          for (int r = 0; r < R; ++r) candcol[slot * L.m1 + sub + tpc * r] = x[c][r];
+          for (int r = 0; r < R; ++r) sx[2 + sub + tpc * r] = x[c][r];
     }
-    if (tid == 0) { cval[slot] = cv; ckey[slot] = ck; }
+    if (tid == 0) { sx[0] = cv; sx[1] = __longlong_as_double((long long)ck); }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk copy
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t src = rg_smem(sx);
+      for (int d = 0; d < CL; ++d) {
+        const uint32_t dst = rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec), d);
+        const uint32_t mb = rg_mapa(rg_smem(&mbar[slot]), d);
+        asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes "
+                     "[%0], [%1], %2, [%3];" :: "r"(dst), "r"(src), "r"(rec_bytes), "r"(mb)
+                     : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
+    }
   };
 
   // initial norms (all rows)
@@ -994,14 +1049,16 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
   int r_out = kmax;
   for (int i = 0; i < kmax; ++i) {
     const int slot = i & 1;
-    cluster.sync();
+    rg_wait(rg_smem(&mbar[slot]), (uint32_t)((i >> 1) & 1));
+    if (tid == 0) rg_arm(rg_smem(&mbar[slot]), rec_bytes * CL);   // for step i + 2
+    const double* rx = RX + (size_t)slot * CL * L.rec;
     // ---- winner over the CL CTA candidates (identical in every warp)
     double best = -1.0;
     unsigned long long bk = rg_pack(0x7fffffff, 0);
     int wr = 0;
     if (lane < CL) {
-      best = cluster.map_shared_rank(cval, lane)[slot];
-      bk = cluster.map_shared_rank(ckey, lane)[slot];
+      best = rx[(size_t)lane * L.rec];
+      bk = (unsigned long long)__double_as_longlong(rx[(size_t)lane * L.rec + 1]);
       wr = lane;
     }
 #pragma unroll
@@ -1021,7 +1078,7 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
     const int lp = (int)(bk >> 32), pp = (int)(bk & 0xffffffffu);
     // ---- winner's column rows i..m-1 into vbuf (row i-1 no longer used)
     {
-      const double* Xr = cluster.map_shared_rank(candcol, wr) + slot * L.m1;
+      const double* Xr = rx + (size_t)wr * L.rec + 2;
       for (int a = i + tid; a < m; a += RG_NT) vbuf[a] = Xr[a];
       if (tid == 0 && i > 0) vbuf[i - 1] = 0.0;
     }
@@ -1099,7 +1156,9 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
 #pragma unroll
     for (int c = 0; c < C; ++c)
       if (ph0 + c < n) J.perm[pos[c]] = ph0 + c;
-  cluster.sync();   // no CTA leaves while others may read its shared memory
+  // every push addressed to this CTA was waited for; keep the CTAs resident
+  // until all of them issued theirs
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
 // variant v: (R, C) = (16,2), (8,4), (4,8); returns cluster size or 0
@@ -1123,14 +1182,14 @@ int cpqr_reg_plan(int m, int n, int v, int* tpc_out) {
   return cl;
 }
 
-size_t cpqr_reg_smem(int mp) { return RgLayout(mp).bytes(); }   // mp = tpc * R
+size_t cpqr_reg_smem(int mp, int cl) { return RgLayout(mp, cl).bytes(); }   // mp = tpc * R
 
 template <int R, int C>
 static void launch_rg(const CpqrJob* d_jobs, int njobs, int cl, int tpc, size_t smem, cudaStream_t st) {
   static bool init = false;
   if (!init) {
     CUDA_TRY(cudaFuncSetAttribute(cpqr_reg_kernel<R, C>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CUDA_TRY(cudaFuncSetAttribute(cpqr_reg_kernel<R, C>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     init = true;

@@ -2055,7 +2055,7 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       auto& g = rg_groups[std::make_tuple(bv, bcl, btpc)];
       g.first.push_back(job_of(t, ncap));
       static const int RRv[3] = {16, 8, 4};
-      g.second = std::max(g.second, cpqr_reg_smem(btpc * RRv[bv]));
+      g.second = std::max(g.second, cpqr_reg_smem(btpc * RRv[bv], bcl));
       continue;
     }
     if (!coop_only && !env_flag("SPQ_CPQR_CLUSTER") && cpqr_cta_smem(j.np, ncap) <= CPQR_CTA_MAX_SMEM) {
