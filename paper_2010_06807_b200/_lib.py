@@ -152,7 +152,7 @@ class Context:
 
     def timings(self):
         nf = len(TIMING_FAMILIES)
-        buf = np.zeros(4 * nf + 25)
+        buf = np.zeros(4 * nf + 26)
         self.call("spq_timings", buf, int(buf.size))
         out = {f: {"ms": buf[4 * i], "flops": buf[4 * i + 1], "launches": int(buf[4 * i + 2]),
                    "bytes": buf[4 * i + 3]}
@@ -167,7 +167,7 @@ class Context:
                        "stats_ms": h[17], "load_ms": h[18], "finish_ms": h[19],
                        "live_bytes": int(h[20]), "peak_bytes": int(h[21]),
                        "speculate": int(h[22]), "verified_blocks": int(h[23]),
-                       "spec_mismatch": int(h[24])}
+                       "spec_mismatch": int(h[24]), "sparsify_waves": int(h[25])}
         return out
 
 

@@ -163,6 +163,7 @@ struct spq_ctx {
   int* h_spec_bad = nullptr;
   int* d_spec_bad = nullptr;
   int64_t n_verified = 0;
+  int64_t n_sparsify_waves = 0;
   PivotSet piv;   // speculative mode: checks pending across calls
   unsigned long long* d_nnz_slots = nullptr;   // per-level trailing_nnz counters
   // device GMRES: the original (unscaled) matrix in CSR
@@ -1069,11 +1070,17 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
     std::map<std::pair<int, int>, std::pair<std::vector<PanelJob>, int64_t>> groups;
     std::map<std::tuple<int, int, int>, std::vector<PanelJob>> rgroups;   // (cl, R, kbmax)
     size_t wtot = 0;
+    // the register kernel (1 CTA/SM, 255 registers) minimises the latency of
+    // few large panels; many small panels run at higher occupancy in the
+    // shared-memory kernel (throughput: BASELINE config 2's 4096 blocks)
+    int njobs = 0;
+    for (auto& q : probs) njobs += j0 < q.k;
+    const bool many = njobs > 2 * c->nsm;
     for (auto& q : probs) {
       if (j0 >= q.k) continue;
       const int kb = std::min(NB, q.k - j0);
       const int mh = q.m - j0;
-      if (!legacy_panel() && mh <= 16 * 2 * 256) {
+      if (!legacy_panel() && !many && mh <= 16 * 2 * 256) {
         // register-resident block: ~panel_rows() rows per CTA, R rows per thread
         int cl = std::max(1, std::min(16, (mh + panel_rows() - 1) / panel_rows()));
         int rpc = (mh + cl - 1) / cl;
@@ -1949,7 +1956,7 @@ constexpr size_t CPQR_CTA_MAX_SMEM = 220 * 1024;
 // sparsify_interface for a WAVE of mutually independent interfaces (no
 // shared block): identical to running them one after another in order.
 void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
-                      std::vector<SparsifyOut>& outs, int drop_base) {
+                      std::vector<SparsifyOut>& outs, const std::vector<int>& drop_idx) {
   Stage stage_(c, "do_sparsify_wave");
   HostTimer ht(&c->host_ms[8]);
   const int nw = (int)wave.size();
@@ -2186,8 +2193,8 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
         gg.add(E, std::max(j.ncols, 1), E, std::max(j.ncols, 1), G1, fdim, fdim, fdim, nu, 1.0, 0.0);
         gg.add(E + nu, std::max(j.ncols, 1), E + nu, std::max(j.ncols, 1), G2, fdim, fdim, fdim,
                nc, 1.0, 0.0);
-        pj.push_back(PowerJob{G1, fdim, c->d_dropped + 2 * (drop_base + t)});
-        pj.push_back(PowerJob{G2, fdim, c->d_dropped + 2 * (drop_base + t) + 1});
+        pj.push_back(PowerJob{G1, fdim, c->d_dropped + 2 * drop_idx[t]});
+        pj.push_back(PowerJob{G2, fdim, c->d_dropped + 2 * drop_idx[t] + 1});
       }
       tcb.run(c);
       gg.run(c, true, 0);
@@ -2305,33 +2312,73 @@ void do_sparsify(spq_ctx* c, const std::vector<int>& ids, double eps,
   outs.assign(ids.size(), SparsifyOut{-1, 0, 0.0, 0});
   c->d_dropped = dalloc(c, 2 * std::max<size_t>(ids.size(), 1) * sizeof(double));
   CUDA_TRY(cudaMemsetAsync(c->d_dropped, 0, 2 * std::max<size_t>(ids.size(), 1) * sizeof(double), c->st));
-  size_t pos = 0;
-  while (pos < ids.size()) {
-    std::vector<int> wave;
+  // Waves of pairwise non-adjacent interfaces (no shared block).  The
+  // reference sparsifies in ascending id; two interfaces commute unless
+  // they share a block, so each interface goes one wave after the latest
+  // EARLIER (in id order) interface adjacent to it: every adjacent pair
+  // keeps its order, everything else is batched (fewer waves than a greedy
+  // prefix split, hence fewer rank read-backs).  SPQ_SPARSIFY_PREFIX=1:
+  // the greedy prefix split.
+  const int nid = (int)ids.size();
+  std::vector<int> lvl(nid, 0);
+  {
+    std::unordered_map<int, int> where;
+    where.reserve(nid * 2);
+    for (int t = 0; t < nid; ++t) where[ids[t]] = t;
+    static const bool prefix = env_flag("SPQ_SPARSIFY_PREFIX");
+    int cur = 0;
     std::set<int> members;
-    size_t wave_bytes = 0;
-    while (pos < ids.size()) {
-      const int p = ids[pos];
+    for (int t = 0; t < nid; ++t) {
+      const int p = ids[t];
       if (!c->active[p]) throw SpqError(SPQ_ERR_BAD_INPUT, "sparsify of inactive cluster");
-      bool clash = false;
-      for (int q : c->cix[p]) if (q != p && members.count(q)) { clash = true; break; }
-      if (!clash)
-        for (int q : c->rix[p]) if (q != p && members.count(q)) { clash = true; break; }
-      if (clash) break;
-      // device scratch of the job (M and its compacted copy, np x ncols each)
-      size_t nc = 0;
-      for (int q : c->rix[p]) if (q != p) nc += c->cols_of[q].size();
-      for (int q : c->cix[p]) if (q != p) nc += c->rows_of[q].size();
-      const size_t est = 2 * sizeof(double) * c->cols_of[p].size() * nc;
-      if (!wave.empty() && wave_bytes + est > 4 * chunk_bytes()) break;
-      wave_bytes += est;
-      wave.push_back(p);
-      members.insert(p);
-      ++pos;
+      int L = 0;
+      if (prefix) {
+        bool clash = false;
+        for (int q : c->cix[p]) if (q != p && members.count(q)) { clash = true; break; }
+        if (!clash) for (int q : c->rix[p]) if (q != p && members.count(q)) { clash = true; break; }
+        if (clash) { ++cur; members.clear(); }
+        members.insert(p);
+        L = cur;
+      } else {
+        auto dep = [&](int q) {
+          if (q == p) return;
+          auto it = where.find(q);
+          if (it != where.end() && it->second < t) L = std::max(L, lvl[it->second] + 1);
+        };
+        for (int q : c->cix[p]) dep(q);
+        for (int q : c->rix[p]) dep(q);
+      }
+      lvl[t] = L;
     }
-    std::vector<SparsifyOut> wo(wave.size());
-    do_sparsify_wave(c, wave, eps, wo, (int)(pos - wave.size()));
-    std::copy(wo.begin(), wo.end(), outs.begin() + (pos - wave.size()));
+  }
+  int nlev = 0;
+  for (int t = 0; t < nid; ++t) nlev = std::max(nlev, lvl[t] + 1);
+  for (int L = 0; L < nlev; ++L) {
+    std::vector<int> members_t;
+    for (int t = 0; t < nid; ++t) if (lvl[t] == L) members_t.push_back(t);
+    size_t pos = 0;
+    while (pos < members_t.size()) {   // memory-bounded groups, ascending id
+      std::vector<int> wave, didx;
+      size_t wave_bytes = 0;
+      while (pos < members_t.size()) {
+        const int t = members_t[pos];
+        const int p = ids[t];
+        // device scratch of the job (M and its compacted copy, np x ncols each)
+        size_t nc = 0;
+        for (int q : c->rix[p]) if (q != p) nc += c->cols_of[q].size();
+        for (int q : c->cix[p]) if (q != p) nc += c->rows_of[q].size();
+        const size_t est = 2 * sizeof(double) * c->cols_of[p].size() * nc;
+        if (!wave.empty() && wave_bytes + est > 4 * chunk_bytes()) break;
+        wave_bytes += est;
+        wave.push_back(p);
+        didx.push_back(t);
+        ++pos;
+      }
+      std::vector<SparsifyOut> wo(wave.size());
+      do_sparsify_wave(c, wave, eps, wo, didx);
+      for (size_t u = 0; u < wave.size(); ++u) outs[didx[u]] = wo[u];
+      c->n_sparsify_waves++;
+    }
   }
   // dropped norms of all compressed interfaces: one read at the end
   std::vector<double> hd(2 * ids.size());
@@ -3224,6 +3271,7 @@ int spq_timings(spq_ctx* c, double* out, int n) {
       out[4 * F_NFAM + 23] = (double)c->n_verified;
       out[4 * F_NFAM + 24] = c->h_spec_bad ? (double)*c->h_spec_bad : 0.0;
     }
+    if (4 * F_NFAM + 25 < n) out[4 * F_NFAM + 25] = (double)c->n_sparsify_waves;
   });
 }
 

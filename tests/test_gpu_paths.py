@@ -26,6 +26,7 @@ SWITCHES = {
     "small_upload_ring": {"SPQ_RING_SMALL": "1"},
     "gemm_v1": {"SPQ_GEMM": "1"},
     "exact_row_flags": {"SPQ_NO_SPEC": "1"},
+    "sparsify_prefix_waves": {"SPQ_SPARSIFY_PREFIX": "1"},
     "legacy_panel_smem": {"SPQ_PANEL_LEGACY": "1"},
     "register_panel_512_rows": {"SPQ_PANEL_ROWS": "512"},
     "speculation_failure_retry": {"SPQ_SPEC_TEST_FAIL": "1"},
