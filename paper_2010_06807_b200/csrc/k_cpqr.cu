@@ -1042,7 +1042,7 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
         const unsigned long long k = rg_pack(pos[c], ph0 + c);
         if (rg_better(nv, k, bv, bk)) { bv = nv; bk = k; }
       }
-    publish(bv, bk, 0);
+    if (kmax > 0) publish(bv, bk, 0);
   }
 
   double norm0 = 0.0;
@@ -1149,7 +1149,10 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
         const unsigned long long k = rg_pack(pos[c], ph0 + c);
         if (rg_better(nv, k, bv, bkk)) { bv = nv; bkk = k; }
       }
-    publish(bv, bkk, slot ^ 1);
+    // no push after the last step: nobody would wait for it, and a bulk
+    // copy still in flight when its destination CTA exits lands in shared
+    // memory that may already belong to another CTA
+    if (i + 1 < kmax) publish(bv, bkk, slot ^ 1);
   }
   if (q == 0 && tid == 0) *J.rank = r_out;
   if (sub == 0)
