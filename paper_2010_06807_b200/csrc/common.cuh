@@ -62,6 +62,18 @@ struct PanelJob {
   int want_T;
 };
 
+// ------------------------------------------- fused shallow compact-WY (k <= 64)
+// C (m x n) <- C - V op(T) V^T C ; op(T) = T^T when trans (Q^T C), else T
+struct WyfJob {
+  const double* V;   // m x k (ldv), explicit (zeros above the unit diagonal)
+  const double* T;   // k x k upper triangular (ldt)
+  double* C;         // m x n (ldc)
+  int ldv, ldt, ldc;
+  int m, n, k;
+  int trans;
+  int tile0;         // first 32-column tile of this job in the launch
+};
+
 // ------------------------------------------------------ pivot check
 struct PivotJob {
   const double* R;
@@ -169,6 +181,9 @@ void launch_csc_scatter(const int64_t* indptr, const int64_t* indices, const dou
 void launch_gemm(const GemmProb* d_probs, int nprob, int total_tiles, bool transA, cudaStream_t st);
 int gemm_tiles(int m, int n);
 void gemm_set_variant(int v);   // 0 default, 1: 64x64 tiles, 2: 128x64 tiles
+void launch_wyf(const WyfJob* d_jobs, int njobs, int tiles, int kmax, int cl, cudaStream_t st);
+int wyf_kmax();
+int wyf_cluster(int m);
 void launch_splitk_reduce(const SplitRed* d_tasks, int ntasks, int64_t max_mn, cudaStream_t st);
 void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t slab_elems,
                      bool smem, int kbmax, cudaStream_t st);
@@ -177,6 +192,8 @@ void launch_panel_qr_reg(const PanelJob* d_jobs, int njobs, int cluster, int row
 int panel_reg_kbmax(int kb);
 void launch_larft(const LarftJob* d_jobs, int njobs, int total_tiles, cudaStream_t st);
 int larft_tiles(int k);
+void launch_larft_full(const LarftJob* d_jobs, int njobs, int kmax, cudaStream_t st);
+int larft_full_max();
 void launch_pivot_check(const PivotJob* d_jobs, int njobs, int64_t* d_err_idx,
                         double* d_err_val, cudaStream_t st);
 void launch_trsm_right(const TrsmJob* d_jobs, int njobs, int total_tiles, cudaStream_t st);

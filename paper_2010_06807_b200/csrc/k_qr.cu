@@ -614,6 +614,78 @@ __global__ void __launch_bounds__(LARFT_NT) larft_kernel(const LarftJob* __restr
   }
 }
 
+// Full T in ONE launch for k <= LARFT_FULL_MAX (replaces the 32-block
+// larft + 2 log2(k/32) doubling GEMM launches, ~15 us each, on the panels
+// of the sequential upper-level fronts).  G is staged in shared memory; row
+// a of T is an independent recurrence (thread a):
+//   T[a,i] = -tau_i sum_{b=a}^{i-1} T[a,b] G[b,i]
+// with T[a,b] (b > a) kept in the strictly LOWER triangle of the same
+// buffer (G is only read above the diagonal): no second k x k array.
+constexpr int LARFT_FULL_MAX = 160;
+
+__global__ void __launch_bounds__(LARFT_NT) larft_full_kernel(const LarftJob* __restrict__ jobs) {
+  const LarftJob J = jobs[blockIdx.x];
+  const int k = J.k, tid = threadIdx.x;
+  const int ld = (k + 1) & ~1;   // even: column reads and the (ld+1) row stride are conflict-free
+  extern __shared__ double S[];
+  // G (upper triangle) in batches of 8 independent loads per thread: their
+  // latencies overlap (a plain strided loop serialises one L2 round trip
+  // per iteration)
+  for (int e0 = 0; e0 < k * k; e0 += 8 * LARFT_NT) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + tid + u * LARFT_NT;
+      const int a = e % k, b = e / k;
+      t[u] = (e < k * k && a < b) ? __ldg(J.G + a + (int64_t)b * J.ldg) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + tid + u * LARFT_NT;
+      const int a = e % k, b = e / k;
+      if (e < k * k && a < b) S[a + b * ld] = t[u];
+    }
+  }
+  __syncthreads();
+  if (tid < k) {
+    const int a = tid;
+    const double ta = J.tau[a];
+    double* Ta = S + a * ld;   // Ta[b] = T[a,b] for b > a (lower triangle, column a)
+    for (int i = a + 1; i < k; ++i) {
+      const double* Gi = S + i * ld;   // Gi[b] = G[b,i], b < i
+      double s0 = ta * Gi[a], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int b = a + 1;
+      for (; b + 3 < i; b += 4) {
+        s0 = fma(Ta[b], Gi[b], s0);
+        s1 = fma(Ta[b + 1], Gi[b + 1], s1);
+        s2 = fma(Ta[b + 2], Gi[b + 2], s2);
+        s3 = fma(Ta[b + 3], Gi[b + 3], s3);
+      }
+      for (; b < i; ++b) s0 = fma(Ta[b], Gi[b], s0);
+      const double ti = J.tau[i];
+      Ta[i] = (ti != 0.0) ? -ti * ((s0 + s1) + (s2 + s3)) : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += LARFT_NT) {
+    const int a = e % k, i = e / k;
+    J.T[a + (int64_t)i * J.ldt] = a < i ? S[i + a * ld] : (a == i ? J.tau[a] : 0.0);
+  }
+}
+
+int larft_full_max() { return LARFT_FULL_MAX; }
+
+void launch_larft_full(const LarftJob* d_jobs, int njobs, int kmax, cudaStream_t st) {
+  if (njobs <= 0) return;
+  const size_t smem = (size_t)kmax * ((kmax + 1) & ~1) * sizeof(double);
+  static size_t conf = 0;
+  if (smem > conf) {
+    CUDA_TRY(cudaFuncSetAttribute(larft_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    conf = smem;
+  }
+  larft_full_kernel<<<njobs, LARFT_NT, smem, st>>>(d_jobs); SPQ_LAUNCH_CHECK();
+}
+
 int larft_tiles(int) { return 1; }
 
 void launch_larft(const LarftJob* d_jobs, int njobs, int /*total_tiles*/, cudaStream_t st) {

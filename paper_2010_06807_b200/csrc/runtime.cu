@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <tuple>
 #include <memory>
@@ -70,23 +71,196 @@ struct Block {
   uint8_t origin = 0;   // last predicting site (SPQ_SPEC_DEBUG reports)
 };
 
+// 64-bit key -> small value, open addressing with linear probing (the
+// allocator's pointer tables: one probe instead of a node allocation and two
+// cache misses per dalloc/dfree)
+template <class V>
+class FlatMap {
+  static constexpr uint64_t EMPTY = ~0ull, TOMB = ~1ull;
+  std::vector<uint64_t> keys_;
+  std::vector<V> vals_;
+  size_t live_ = 0, used_ = 0;
+  static size_t mix(uint64_t k) {
+    k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ull; k ^= k >> 33;
+    return (size_t)k;
+  }
+  void rehash(size_t cap) {
+    std::vector<uint64_t> ok;
+    std::vector<V> ov;
+    ok.swap(keys_);
+    ov.swap(vals_);
+    keys_.assign(cap, EMPTY);
+    vals_.assign(cap, V());
+    used_ = live_;
+    for (size_t t = 0; t < ok.size(); ++t)
+      if (ok[t] < TOMB) {
+        size_t h = mix(ok[t]) & (cap - 1);
+        while (keys_[h] != EMPTY) h = (h + 1) & (cap - 1);
+        keys_[h] = ok[t];
+        vals_[h] = ov[t];
+      }
+  }
+  size_t slot_of(uint64_t k) const {
+    const size_t m = keys_.size() - 1;
+    for (size_t h = mix(k) & m;; h = (h + 1) & m) {
+      if (keys_[h] == k) return h;
+      if (keys_[h] == EMPTY) return SIZE_MAX;
+    }
+  }
+
+ public:
+  FlatMap() { rehash(1024); }
+  size_t size() const { return live_; }
+  V* find(uint64_t k) {
+    const size_t h = slot_of(k);
+    return h == SIZE_MAX ? nullptr : &vals_[h];
+  }
+  V& operator[](uint64_t k) {
+    if (V* v = find(k)) return *v;
+    if (2 * (used_ + 1) > keys_.size()) rehash(keys_.size() * (2 * (live_ + 1) > keys_.size() / 2 ? 2 : 1));
+    const size_t m = keys_.size() - 1;
+    size_t h = mix(k) & m;
+    while (keys_[h] < TOMB) h = (h + 1) & m;
+    if (keys_[h] == EMPTY) ++used_;
+    keys_[h] = k;
+    vals_[h] = V();
+    ++live_;
+    return vals_[h];
+  }
+  bool erase(uint64_t k) {
+    const size_t h = slot_of(k);
+    if (h == SIZE_MAX) return false;
+    keys_[h] = TOMB;
+    --live_;
+    return true;
+  }
+  void clear() { keys_.assign(keys_.size(), EMPTY); live_ = used_ = 0; }
+};
+inline uint64_t pkey(const void* p) { return (uint64_t)(uintptr_t)p; }
+
+// (row cluster, col cluster) -> Block.  Open addressing with linear probing
+// over 64-bit keys; Blocks live in a deque (stable references across
+// inserts) recycled through a free list.  The planner does ~10^5 lookups per
+// factorization: a node-based unordered_map costs two cache misses each.
+class BlockMap {
+  static constexpr uint64_t EMPTY = ~0ull, TOMB = ~1ull;
+  std::vector<uint64_t> keys_;
+  std::vector<uint32_t> idx_;
+  std::deque<Block> pool_;
+  std::vector<uint32_t> free_;
+  size_t live_ = 0, used_ = 0;   // used_ = live + tombstones
+  static size_t mix(uint64_t k) {
+    k ^= k >> 31; k *= 0x7fb5d329728ea185ull; k ^= k >> 27; k *= 0x81dadef4bc2dd44dull; k ^= k >> 33;
+    return (size_t)k;
+  }
+  void rehash(size_t cap) {
+    std::vector<uint64_t> ok;
+    std::vector<uint32_t> oi;
+    ok.swap(keys_);
+    oi.swap(idx_);
+    keys_.assign(cap, EMPTY);
+    idx_.assign(cap, 0);
+    used_ = live_;
+    for (size_t t = 0; t < ok.size(); ++t)
+      if (ok[t] < TOMB) {
+        size_t h = mix(ok[t]) & (cap - 1);
+        while (keys_[h] != EMPTY) h = (h + 1) & (cap - 1);
+        keys_[h] = ok[t];
+        idx_[h] = oi[t];
+      }
+  }
+  size_t slot_of(uint64_t k) const {   // slot holding k, or SIZE_MAX
+    if (keys_.empty()) return SIZE_MAX;
+    const size_t m = keys_.size() - 1;
+    for (size_t h = mix(k) & m;; h = (h + 1) & m) {
+      if (keys_[h] == k) return h;
+      if (keys_[h] == EMPTY) return SIZE_MAX;
+    }
+  }
+
+ public:
+  BlockMap() { rehash(1024); }
+  size_t size() const { return live_; }
+  bool empty() const { return live_ == 0; }
+  void reserve(size_t n) {
+    size_t cap = keys_.size();
+    while (cap < 2 * n) cap <<= 1;
+    if (cap != keys_.size()) rehash(cap);
+  }
+  Block* find(uint64_t k) {
+    const size_t h = slot_of(k);
+    return h == SIZE_MAX ? nullptr : &pool_[idx_[h]];
+  }
+  Block& at(uint64_t k) {
+    Block* b = find(k);
+    if (!b) throw std::out_of_range("block map: missing key");
+    return *b;
+  }
+  Block& get_or_create(uint64_t k) {
+    if (Block* b = find(k)) return *b;
+    if (2 * (used_ + 1) > keys_.size()) rehash(keys_.size() * (2 * (live_ + 1) > keys_.size() / 2 ? 2 : 1));
+    const size_t m = keys_.size() - 1;
+    size_t h = mix(k) & m;
+    while (keys_[h] < TOMB) h = (h + 1) & m;
+    if (keys_[h] == EMPTY) ++used_;
+    uint32_t id;
+    if (!free_.empty()) { id = free_.back(); free_.pop_back(); }
+    else { id = (uint32_t)pool_.size(); pool_.emplace_back(); }
+    keys_[h] = k;
+    idx_[h] = id;
+    ++live_;
+    return pool_[id];
+  }
+  bool erase(uint64_t k) {
+    const size_t h = slot_of(k);
+    if (h == SIZE_MAX) return false;
+    pool_[idx_[h]] = Block();
+    free_.push_back(idx_[h]);
+    keys_[h] = TOMB;
+    --live_;
+    return true;
+  }
+  void swap(BlockMap& o) {
+    keys_.swap(o.keys_); idx_.swap(o.idx_); pool_.swap(o.pool_); free_.swap(o.free_);
+    std::swap(live_, o.live_); std::swap(used_, o.used_);
+  }
+  template <class F> void for_each(F&& f) {   // f(key, Block&), unspecified order
+    for (size_t t = 0; t < keys_.size(); ++t)
+      if (keys_[t] < TOMB) f(keys_[t], pool_[idx_[t]]);
+  }
+};
+
 // sorted small-vector set (cluster adjacency lists are short; iteration
-// must be ascending like the reference's sorted(...) calls)
+// must be ascending like the reference's sorted(...) calls).  Each entry
+// also carries the Block it stands for, so the planner's block lookups are a
+// binary search in a short, cache-resident row list instead of a hash probe.
 struct FlatSet {
   std::vector<int> v;
-  void insert(int x) {
+  std::vector<Block*> b;
+  void insert(int x, Block* blk = nullptr) {
     auto it = std::lower_bound(v.begin(), v.end(), x);
-    if (it == v.end() || *it != x) v.insert(it, x);
+    const size_t i = (size_t)(it - v.begin());
+    if (it == v.end() || *it != x) {
+      v.insert(it, x);
+      b.insert(b.begin() + i, blk);
+    } else if (blk) {
+      b[i] = blk;
+    }
   }
   void erase(int x) {
     auto it = std::lower_bound(v.begin(), v.end(), x);
-    if (it != v.end() && *it == x) v.erase(it);
+    if (it != v.end() && *it == x) {
+      b.erase(b.begin() + (it - v.begin()));
+      v.erase(it);
+    }
   }
-  size_t count(int x) const { return std::binary_search(v.begin(), v.end(), x) ? 1 : 0; }
-  void clear() { v.clear(); }
+  Block* find(int x) const {
+    auto it = std::lower_bound(v.begin(), v.end(), x);
+    return (it != v.end() && *it == x) ? b[it - v.begin()] : nullptr;
+  }
+  void clear() { v.clear(); b.clear(); }
   std::vector<int>::const_iterator begin() const { return v.begin(); }
   std::vector<int>::const_iterator end() const { return v.end(); }
-  size_t size() const { return v.size(); }
 };
 
 // pivot checks (factor.py:57-68) queued on the device, raised in order at
@@ -117,6 +291,7 @@ enum Fam { F_COPY = 0, F_QR, F_WY, F_TRSM, F_CPQR, F_FLAGS, F_CHAIN, F_NFAM };
 
 struct FamTimer {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[F_NFAM];
+  std::vector<std::string> tag[F_NFAM];   // SPQ_SCOPE_LOG only
   double ms[F_NFAM] = {0};
   double flops[F_NFAM] = {0};
   double bytes[F_NFAM] = {0};
@@ -145,7 +320,7 @@ struct spq_ctx {
   std::vector<std::vector<int64_t>> rows_of, cols_of;
   std::vector<char> active;
   std::vector<FlatSet> rix, cix;
-  std::unordered_map<uint64_t, Block> blk;
+  BlockMap blk;
   std::vector<int64_t> row_of_col;
   std::vector<double*> deferred;
   // transform chain
@@ -192,12 +367,12 @@ struct spq_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join[NAUX] = {};
   const char* stage = "";   // innermost runtime stage (OOM reports)
   struct PoolEnt { size_t cls; int slab; };
-  std::unordered_map<void*, PoolEnt> pool_size;
+  FlatMap<PoolEnt> pool_size;
   std::vector<void*> slabs;          // nullptr once reclaimed
   std::vector<size_t> slab_caps;
   std::vector<int64_t> slab_live;    // live pool buffers per slab
   int cur_slab = -1;
-  std::unordered_map<void*, int> refcnt;   // shared block allocations
+  FlatMap<int> refcnt;   // shared block allocations
   std::set<void*> big;                      // large buffers (arena)
   std::vector<void*> big_pending;           // freed, awaiting a stream sync
   std::unordered_map<void*, size_t> big_size;
@@ -428,8 +603,8 @@ void ensure_arena(GlobalCache& g) {
 }
 
 double* dalloc(spq_ctx* c, size_t bytes) {
-  auto t0 = std::chrono::steady_clock::now();
   if (bytes >= BIG_ALLOC) {
+    auto t0 = std::chrono::steady_clock::now();
     // large buffers: process-wide best-fit arena
     void* p = nullptr;
     size_t got = 0;
@@ -502,12 +677,11 @@ double* dalloc(spq_ctx* c, size_t bytes) {
     sid = c->cur_slab;
     c->slab_off += cls;
   }
-  c->pool_size[p] = spq_ctx::PoolEnt{cls, sid};
+  c->pool_size[pkey(p)] = spq_ctx::PoolEnt{cls, sid};
   c->slab_live[sid]++;
   c->live_bytes += cls;
   c->peak_bytes = std::max(c->peak_bytes, c->live_bytes);
-  c->n_allocs++;
-  c->host_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  c->n_allocs++;   // (small path untimed: two clock reads would cost as much as the pool op)
   return (double*)p;
 }
 // Scratch whose size is a free parameter (chunk widths, WY batches): the
@@ -565,21 +739,22 @@ void dfree(spq_ctx* c, void* p) {
     c->big_pending.push_back(p);
     return;
   }
-  auto it = c->pool_size.find(p);
-  if (it == c->pool_size.end()) throw std::runtime_error("dfree of unknown pointer");
-  c->pool_free[it->second.cls].push_back({p, it->second.slab});
-  c->slab_live[it->second.slab]--;
-  c->live_bytes -= it->second.cls;
-  c->pool_size.erase(it);
+  spq_ctx::PoolEnt* it = c->pool_size.find(pkey(p));
+  if (!it) throw std::runtime_error("dfree of unknown pointer");
+  const spq_ctx::PoolEnt e = *it;
+  c->pool_size.erase(pkey(p));
+  c->pool_free[e.cls].push_back({p, e.slab});
+  c->slab_live[e.slab]--;
+  c->live_bytes -= e.cls;
 }
 
 // stream-ordered release of a block's memory (shared allocations refcounted)
 void release_mem(spq_ctx* c, Block& b) {
   if (b.base) {
-    auto it = c->refcnt.find(b.base);
-    if (it != c->refcnt.end() && --it->second == 0) {
+    int* rc = c->refcnt.find(pkey(b.base));
+    if (rc && --*rc == 0) {
       c->deferred.push_back((double*)b.base);
-      c->refcnt.erase(it);
+      c->refcnt.erase(pkey(b.base));
     }
   } else if (b.p) {
     c->deferred.push_back(b.p);
@@ -590,7 +765,7 @@ void release_mem(spq_ctx* c, Block& b) {
 
 double* shared_alloc(spq_ctx* c, size_t elems, int nref) {
   double* base = dalloc(c, std::max<size_t>(elems, 1) * sizeof(double));
-  c->refcnt[base] = nref;
+  c->refcnt[pkey(base)] = nref;
   return base;
 }
 
@@ -696,10 +871,11 @@ struct Scope {
     CUDA_TRY(cudaEventCreate(&e));
     return e;
   }
-  Scope(spq_ctx* c_, int f) : c(c_), fam(f) {
+  Scope(spq_ctx* c_, int f, std::string tag = std::string()) : c(c_), fam(f) {
     if (c->timing) {
       a = get(c);
       CUDA_TRY(cudaEventRecord(a, c->st));
+      if (scope_log()) c->tm.tag[fam].push_back(std::move(tag));
     }
   }
   ~Scope() {
@@ -709,19 +885,32 @@ struct Scope {
       c->tm.ev[fam].push_back({a, b});
     }
   }
+  // SPQ_SCOPE_LOG=<path>: every timed scope (family, ms, tag) appended at
+  // the next timing collection (diagnostic)
+  static FILE* scope_log() {
+    static FILE* f = [] {
+      const char* e = getenv("SPQ_SCOPE_LOG");
+      return (e && *e) ? fopen(e, "a") : (FILE*)nullptr;
+    }();
+    return f;
+  }
 };
 
 void collect_timings(spq_ctx* c) {
   for (int f = 0; f < F_NFAM; ++f) {
-    for (auto& e : c->tm.ev[f]) {
+    FILE* lg = Scope::scope_log();
+    for (size_t t = 0; t < c->tm.ev[f].size(); ++t) {
+      auto& e = c->tm.ev[f][t];
       float ms = 0.f;
       CUDA_TRY(cudaEventSynchronize(e.second));
       CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
       c->tm.ms[f] += ms;
+      if (lg) fprintf(lg, "%d %.4f %s\n", f, ms, t < c->tm.tag[f].size() ? c->tm.tag[f][t].c_str() : "");
       c->ev_pool.push_back(e.first);
       c->ev_pool.push_back(e.second);
     }
     c->tm.ev[f].clear();
+    c->tm.tag[f].clear();
   }
 }
 
@@ -856,7 +1045,20 @@ struct GemmBatch {
       poff += (size_t)S * g.m * g.n;
     }
     {
-      Scope s(c, F_WY);
+      std::string tag;
+      if (Scope::scope_log()) {
+        int mm = 0, nn = 0, kk = 0;
+        double fl = 0;
+        for (auto& g : p) {
+          mm = std::max(mm, g.m); nn = std::max(nn, g.n); kk = std::max(kk, g.k);
+          fl += 2.0 * g.m * g.n * (double)g.k;
+        }
+        char b[200];
+        snprintf(b, sizeof b, "gemm %s np=%zu tiles=%d split=%zu tA=%d max_mnk=%d,%d,%d gflop=%.4f",
+                 c->stage, p.size(), t0, red.size(), (int)transA, mm, nn, kk, fl / 1e9);
+        tag = b;
+      }
+      Scope s(c, F_WY, tag);
       launch_gemm(upload(c, q), (int)q.size(), t0, transA, c->st);
       if (!red.empty()) launch_splitk_reduce(upload(c, red), (int)red.size(), red_max, c->st);
     }
@@ -900,6 +1102,8 @@ struct TProb {
   double* T;
 };
 
+int env_flag(const char* name);
+
 void build_full_T(spq_ctx* c, const std::vector<TProb>& tp) {
   Stage stage_(c, "build_full_T");
   // G = V^T V (batched DMMA), the 32x32 diagonal blocks of T by the row
@@ -927,6 +1131,14 @@ void build_full_T(spq_ctx* c, const std::vector<TProb>& tp) {
     lj.push_back(LarftJob{Gp[i], t.tau, t.T, nullptr, t.k, t.k, t.k, 0});
   }
   gg.run(c, true, 0);
+  if (maxk <= larft_full_max() && !env_flag("SPQ_LARFT_DOUBLING")) {   // whole T in one launch
+    Scope s(c, F_QR);
+    launch_larft_full(upload(c, lj), (int)lj.size(), maxk, c->st);
+    c->tm.launches[F_QR]++;
+    c->n_kernels++;
+    dfree(c, scr);
+    return;
+  }
   {
     Scope s(c, F_QR);
     launch_larft(upload(c, lj), (int)lj.size(), 0, c->st);
@@ -964,6 +1176,26 @@ struct WyProb {
   int ldc, n;
 };
 
+// fused shallow-WY kernel on (SPQ_NO_WYF=1: the three-GEMM path, A/B tests)
+bool use_wyf() {
+  static const bool v = !env_flag("SPQ_NO_WYF");
+  return v;
+}
+
+std::string wyf_tag(spq_ctx* c, const std::vector<WyfJob>& wj, int tiles, int cl) {
+  if (!Scope::scope_log()) return std::string();
+  int mm = 0, nn = 0, kk = 0;
+  double fl = 0;
+  for (auto& w : wj) {
+    mm = std::max(mm, w.m); nn = std::max(nn, w.n); kk = std::max(kk, w.k);
+    fl += 4.0 * w.m * (double)w.n * w.k;
+  }
+  char b[200];
+  snprintf(b, sizeof b, "wyf %s np=%zu tiles=%d cl=%d max_mnk=%d,%d,%d gflop=%.4f", c->stage,
+           wj.size(), tiles, cl, mm, nn, kk, fl / 1e9);
+  return b;
+}
+
 size_t chunk_bytes() {   // SPQ_CHUNK_BYTES overrides (tests force the chunked path)
   static size_t v = 0;
   if (!v) {
@@ -996,6 +1228,41 @@ void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs_in, bool transpose, i
     }
   }
   if (tot == 0) return;
+  {
+    // shallow reflector blocks (every k <= 64) with little total work: one
+    // fused launch (k_wyf.cu) instead of three GEMM launches + split-K
+    // (big batches -- the leaf levels' thousands of fronts -- stay on the
+    // GEMM engine, which runs several CTAs per SM)
+    bool shallow = use_wyf();
+    double fl = 0;
+    int64_t ctas = 0;
+    int clm = 1;
+    for (auto& p : probs) {
+      shallow = shallow && p.k <= wyf_kmax();
+      fl += 4.0 * p.m * (double)p.n * p.k;
+      ctas += (p.n + 31) / 32;
+      clm = std::max(clm, wyf_cluster(p.m));
+    }
+    if (shallow && fl <= 8e9 && ctas * clm <= 4 * c->nsm) {
+      std::vector<WyfJob> wj;
+      int tiles = 0, cl = 1, kmax = 1;
+      for (auto& p : probs) {
+        WyfJob w{};
+        w.V = p.V; w.ldv = p.m; w.T = p.T; w.ldt = p.k; w.C = p.C; w.ldc = p.ldc;
+        w.m = p.m; w.n = p.n; w.k = p.k; w.trans = transpose ? 1 : 0; w.tile0 = tiles;
+        tiles += (p.n + 31) / 32;
+        cl = std::max(cl, wyf_cluster(p.m));
+        kmax = std::max(kmax, p.k);
+        c->tm.flops[F_WY] += 4.0 * p.m * (double)p.n * p.k - (double)p.n * p.k * p.k;
+        wj.push_back(w);
+      }
+      Scope s(c, F_WY, wyf_tag(c, wj, tiles, cl));
+      launch_wyf(upload(c, wj), (int)wj.size(), tiles, kmax, cl, c->st);
+      c->tm.launches[F_WY]++;
+      c->n_kernels++;
+      return;
+    }
+  }
   size_t need1 = 0;   // the largest single (split) problem
   for (auto& p : probs) need1 = std::max(need1, 2 * (size_t)p.k * p.n);
   size_t got = 0;
@@ -1119,6 +1386,30 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
       }
     }
     if (wtot == 0) continue;
+    if (use_wyf()) {   // the block's compact WY on the trailing panel columns: one fused launch
+      std::vector<WyfJob> wj;
+      int tiles = 0, cl = 1;
+      for (auto& q : probs) {
+        if (j0 >= q.k) continue;
+        const int kb = std::min(NB, q.k - j0);
+        const int j1 = j0 + kb;
+        if (j1 >= q.k) continue;
+        WyfJob w{};
+        w.V = q.P + j0 + (int64_t)j0 * q.m; w.ldv = q.m;
+        w.T = q.T + j0 + (int64_t)j0 * q.k; w.ldt = q.k;
+        w.C = q.P + j0 + (int64_t)j1 * q.m; w.ldc = q.m;
+        w.m = q.m - j0; w.n = q.k - j1; w.k = kb; w.trans = 1; w.tile0 = tiles;
+        tiles += (w.n + 31) / 32;
+        cl = std::max(cl, wyf_cluster(w.m));
+        c->tm.flops[F_WY] += 4.0 * w.m * (double)w.n * w.k - (double)w.n * w.k * w.k;
+        wj.push_back(w);
+      }
+      Scope s(c, F_WY, wyf_tag(c, wj, tiles, cl));
+      launch_wyf(upload(c, wj), (int)wj.size(), tiles, NB, cl, c->st);
+      c->tm.launches[F_WY]++;
+      c->n_kernels++;
+      continue;
+    }
     double* Ws = dalloc(c, wtot * sizeof(double));
     size_t off = 0;
     GemmBatch g1, g2, g3;
@@ -1192,27 +1483,23 @@ void pivot_raise(spq_ctx* c, PivotSet& ps) {
 }
 
 // ----------------------------------------------------- block bookkeeping
-Block* find_block(spq_ctx* c, int i, int j) {
-  auto it = c->blk.find(bkey(i, j));
-  return it == c->blk.end() ? nullptr : &it->second;
-}
+inline Block* find_block(spq_ctx* c, int i, int j) { return c->rix[i].find(j); }
 
 Block& put_block(spq_ctx* c, int i, int j, double* p, int nr, int nc, void* base = nullptr) {
-  Block& b = c->blk[bkey(i, j)];
+  Block& b = c->blk.get_or_create(bkey(i, j));
   b.p = p;
   b.base = base;
   b.nr = nr;
   b.nc = nc;
-  c->rix[i].insert(j);
-  c->cix[j].insert(i);
+  c->rix[i].insert(j, &b);
+  c->cix[j].insert(i, &b);
   return b;
 }
 
 void drop_block(spq_ctx* c, int i, int j) {
-  auto it = c->blk.find(bkey(i, j));
-  if (it != c->blk.end()) {
-    release_mem(c, it->second);
-    c->blk.erase(it);
+  if (Block* b = c->blk.find(bkey(i, j))) {
+    release_mem(c, *b);
+    c->blk.erase(bkey(i, j));
   }
   c->rix[i].erase(j);
   c->cix[j].erase(i);
@@ -1289,8 +1576,9 @@ void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
       if (bad) {
         Block* hit = nullptr;
         int hr = -1, hc = -1;
-        for (auto& kv : c->blk)
-          if (kv.second.p == vptrs[t]) { hit = &kv.second; hr = (int)(kv.first >> 32); hc = (int)(kv.first & 0xffffffffu); }
+        c->blk.for_each([&](uint64_t key, Block& bb) {
+          if (bb.p == vptrs[t]) { hit = &bb; hr = (int)(key >> 32); hc = (int)(key & 0xffffffffu); }
+        });
         fprintf(stderr, "[spec] block (%d,%d) %dx%d origin %d: %d rows differ, first %d pred %d actual %d\n",
                 hr, hc, vnr[t], vnc[t], hit ? hit->origin : -1, bad, first,
                 (int)vpred[voff[t] + first], (int)hh[voff[t] + first]);
@@ -2410,7 +2698,7 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
       ncols[t].insert(ncols[t].end(), c->cols_of[k].begin(), c->cols_of[k].end());
     }
   }
-  std::unordered_map<uint64_t, Block> old;
+  BlockMap old;
   old.swap(c->blk);
   for (int s = 0; s < c->ncl; ++s) {
     if (c->active[s]) { c->rows_of[s].clear(); c->cols_of[s].clear(); }
@@ -2428,12 +2716,12 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
   // deterministic order: sort old keys
   std::vector<uint64_t> keys;
   keys.reserve(old.size());
-  for (auto& kv : old) keys.push_back(kv.first);
+  old.for_each([&](uint64_t key, Block&) { keys.push_back(key); });
   std::sort(keys.begin(), keys.end());
   // parent blocks needed, grouped by parent row: one zeroed allocation per row
   std::vector<std::vector<int>> prow_v(c->ncl);   // Pi -> Pj list
   for (uint64_t key : keys) {
-    Block& B = old[key];
+    Block& B = old.at(key);
     if ((int64_t)B.nr * B.nc == 0) continue;
     const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
     const int Pi = parent_of[i], Pj = parent_of[j];
@@ -2451,7 +2739,7 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
   // row cluster, so releasing a parent row's children frees whole slabs
   std::vector<std::vector<uint64_t>> by_prow(c->ncl);
   for (uint64_t key : keys) {
-    Block& B = old[key];
+    Block& B = old.at(key);
     if ((int64_t)B.nr * B.nc == 0) { release_mem(c, B); continue; }
     by_prow[parent_of[(int)(key >> 32)]].push_back(key);
   }
@@ -2491,7 +2779,7 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
     }
     for (int q = g0; q < Pi; ++q)
       for (uint64_t key : by_prow[q]) {
-        Block& B = old[key];
+        Block& B = old.at(key);
         const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
         const int Pj = parent_of[j];
         Block* tgt = find_block(c, q, Pj);
@@ -3182,10 +3470,10 @@ int spq_trailing_stats(spq_ctx* c, int64_t* nblocks, int64_t* nnz) {
     *nblocks = (int64_t)c->blk.size();
     std::vector<const double*> ptrs;
     std::vector<int64_t> sizes;
-    for (auto& kv : c->blk) {
-      const int64_t n = (int64_t)kv.second.nr * kv.second.nc;
-      if (n > 0) { ptrs.push_back(kv.second.p); sizes.push_back(n); }
-    }
+    c->blk.for_each([&](uint64_t, Block& b) {
+      const int64_t n = (int64_t)b.nr * b.nc;
+      if (n > 0) { ptrs.push_back(b.p); sizes.push_back(n); }
+    });
     unsigned long long* d = (unsigned long long*)dalloc(c, sizeof(unsigned long long));
     CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->st));
     if (!ptrs.empty())
@@ -3211,10 +3499,10 @@ int spq_trailing_stats_async(spq_ctx* c, int slot, int64_t* nblocks) {
     *nblocks = (int64_t)c->blk.size();
     std::vector<const double*> ptrs;
     std::vector<int64_t> sizes;
-    for (auto& kv : c->blk) {
-      const int64_t n = (int64_t)kv.second.nr * kv.second.nc;
-      if (n > 0) { ptrs.push_back(kv.second.p); sizes.push_back(n); }
-    }
+    c->blk.for_each([&](uint64_t, Block& b) {
+      const int64_t n = (int64_t)b.nr * b.nc;
+      if (n > 0) { ptrs.push_back(b.p); sizes.push_back(n); }
+    });
     unsigned long long* d = c->d_nnz_slots + slot;
     CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->st));
     if (!ptrs.empty())

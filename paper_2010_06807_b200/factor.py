@@ -23,7 +23,7 @@ import time
 import numpy as np
 
 from ._lib import Context
-from .errors import NestqrError, SpeculationError
+from .errors import DeviceError, NestqrError, SpeculationError
 from .sparse import as_csc
 
 MODES = ("scaled", "unscaled", "variant1", "variant2")
@@ -54,14 +54,16 @@ class _RecordView:
     kind = 0
 
     def __init__(self, F, idx, info):
-        self._F, self._idx = F, idx
+        # the context, not the Factorization: no reference cycle, so the
+        # device memory is released as soon as the last user drops F
+        self._ctx, self._idx = F._ctx, idx
         self._m, self._k, self._n, self._rank = (int(x) for x in info[1:5])
         self._cache = {}
 
     def _get(self, which):
         if which in self._cache:
             return self._cache[which]
-        ctx = self._F._ctx
+        ctx = self._ctx
         m, k, n = self._m, self._k, self._n
         if which in (0, 1, 2):
             size = {0: m, 1: self._ncols(), 2: self._ncolsn()}[which]
@@ -300,12 +302,28 @@ def _cluster_lists(clusters, attr):
     return ptr, (np.concatenate(vals) if vals else np.zeros(0, np.int64))
 
 
-def factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=True,
-              scale_every=1, skip=2, sparsify_min=40, mode="scaled",
-              row_heuristic="same-as-columns", equilibrate=True, observer=None, device=0,
-              _marks=False, _memstats=False, _speculate=True):
+def factorize(A, tree=None, eps=1e-3, **kw):
     """Run the multilevel factorization on the B200 (signature of the reference
-    `factorize`, `factor.py:771-803`)."""
+    `factorize`, `factor.py:771-803`).
+
+    Device memory of contexts that are unreachable but not yet collected
+    (reference cycles) is only returned when the garbage collector runs: on an
+    out-of-memory failure the context is released, garbage is collected and
+    the factorization runs once more."""
+    try:
+        return _factorize(A, tree, eps, **kw)
+    except DeviceError as e:
+        if "out of memory" not in str(e):
+            raise
+    import gc
+    gc.collect()
+    return _factorize(A, tree, eps, **kw)
+
+
+def _factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=True,
+               scale_every=1, skip=2, sparsify_min=40, mode="scaled",
+               row_heuristic="same-as-columns", equilibrate=True, observer=None, device=0,
+               _marks=False, _memstats=False, _speculate=True):
     if mode not in MODES:
         raise NestqrError(f"unknown sparsification mode {mode!r}")
     if mode == "unscaled":

@@ -28,23 +28,48 @@ t_last = [time.perf_counter()]
 
 
 class Obs:
+    F = None
+    prev = {}
+
     def on_level(self, state, lev, st):
         t = time.perf_counter()
+        dev = ""
+        if Obs.ctx is not None:
+            tm = Obs.ctx.timings()
+            cur = {k: v["ms"] for k, v in tm.items() if k != "host"}
+            d = {k: cur[k] - Obs.prev.get(k, 0.0) for k in cur}
+            Obs.prev = cur
+            dev = " dev[" + " ".join(f"{k}={v:.1f}" for k, v in d.items() if v > 0.05) + \
+                f"] sum={sum(d.values()):.1f}ms"
         keys = ("n_factored", "n_scaled", "n_sparsified", "fine_retired", "cols_after",
                 "trailing_blocks", "t_factor", "t_scale", "t_sparsify")
         print(f"  level {lev}: {t - t_last[0]:.3f} s "
               + " ".join(f"{k}={st[k]:.3f}" if isinstance(st.get(k), float) else f"{k}={st.get(k)}"
-                         for k in keys if k in st), flush=True)
+                         for k in keys if k in st) + dev, flush=True)
         t_last[0] = t
 
 
 obs = Obs()
+Obs.ctx = None
+_Ctx = None
+import paper_2010_06807_b200.factor as _FZ  # noqa: E402
+_orig_ctx = _FZ.Context
+
+
+class _SpyCtx(_orig_ctx):
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        Obs.ctx = self
+        Obs.prev = {}
+
+
+_FZ.Context = _SpyCtx
 
 
 for r in range(reps):
     t0 = time.perf_counter()
     t_last[0] = t0
-    F = factorize(A, tree, eps=eps, observer=obs if r == 0 else None)
+    F = factorize(A, tree, eps=eps, observer=obs if r == reps - 1 else None)
     t1 = time.perf_counter()
     print(f"factor {t1 - t0:.3f} s", flush=True)
 x, rep = gmres(A, b, F, tol=tol)
