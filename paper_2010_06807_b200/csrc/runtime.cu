@@ -59,11 +59,70 @@ struct SpqError : std::runtime_error {
 
 inline uint64_t bkey(int i, int j) { return ((uint64_t)(uint32_t)i << 32) | (uint32_t)j; }
 
+// Per-row flags of one block with inline storage for short blocks: the
+// planner creates ~10^4 blocks per level on the leaf levels, most with
+// fewer than 56 rows -- no heap allocation for those.
+class RowFlags {
+  static constexpr int INL = 56;
+  uint8_t* p_ = inl_;
+  int n_ = 0, cap_ = INL;
+  uint8_t inl_[INL];
+  void reserve_(int n) {
+    if (n <= cap_) return;
+    uint8_t* q = new uint8_t[n];
+    if (p_ != inl_) delete[] p_;
+    p_ = q;
+    cap_ = n;
+  }
+
+ public:
+  RowFlags() = default;
+  RowFlags(const RowFlags& o) { assign(o.begin(), o.end()); }
+  RowFlags& operator=(const RowFlags& o) {
+    if (this != &o) assign(o.begin(), o.end());
+    return *this;
+  }
+  RowFlags(RowFlags&& o) noexcept { *this = std::move(o); }
+  RowFlags& operator=(RowFlags&& o) noexcept {
+    if (this == &o) return *this;
+    if (o.p_ != o.inl_) {   // steal the heap buffer
+      if (p_ != inl_) delete[] p_;
+      p_ = o.p_; cap_ = o.cap_; n_ = o.n_;
+      o.p_ = o.inl_; o.cap_ = INL; o.n_ = 0;
+    } else {
+      n_ = 0;
+      assign(o.begin(), o.end());
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  ~RowFlags() { if (p_ != inl_) delete[] p_; }
+  void assign(size_t n, uint8_t v) {
+    reserve_((int)n);
+    n_ = (int)n;
+    std::memset(p_, v, n);
+  }
+  template <class It, class = typename std::enable_if<!std::is_integral<It>::value>::type>
+  void assign(It a, It b) {
+    const int n = (int)(b - a);
+    reserve_(n);
+    n_ = n;
+    std::copy(a, b, p_);
+  }
+  void clear() { n_ = 0; }
+  bool empty() const { return n_ == 0; }
+  size_t size() const { return (size_t)n_; }
+  uint8_t& operator[](size_t i) { return p_[i]; }
+  const uint8_t& operator[](size_t i) const { return p_[i]; }
+  const uint8_t* begin() const { return p_; }
+  const uint8_t* end() const { return p_ + n_; }
+};
+
 struct Block {
   double* p = nullptr;
   void* base = nullptr;        // shared (refcounted) allocation this block lives in
   int nr = 0, nc = 0;
-  std::vector<uint8_t> flags;  // per row: 0 zero, 1 nonzero, 2 unknown (written)
+  RowFlags flags;              // per row: 0 zero, 1 nonzero, 2 unknown (written)
   bool clean = false;
   // flags PREDICTED by the symbolic rules (speculative mode), not yet
   // checked against the device values; checked at the next query
@@ -552,7 +611,14 @@ size_t reclaim_slabs(spq_ctx* c) {
     std::lock_guard<std::mutex> lk(g.mu);
     any = any || !g.slabs.empty();
   }
-  if (!any) return 0;
+  // large frees deferred while other contexts live (published at a stream
+  // sync) are the other recoverable reserve
+  size_t pending = 0;
+  for (void* p : c->big_pending) {
+    auto it = c->big_size.find(p);
+    pending += it != c->big_size.end() ? it->second : 1;
+  }
+  if (!any && pending == 0) return 0;
   // not sync(): that also recycles the upload ring, and this runs inside
   // dalloc, possibly between an upload and the launch that reads it
   CUDA_TRY(cudaStreamSynchronize(c->st));
@@ -580,7 +646,7 @@ size_t reclaim_slabs(spq_ctx* c) {
     freed += e.second;
   }
   g.slabs.clear();
-  return freed;
+  return freed + pending;
 }
 
 // The process-wide arena takes all free HBM but a reserve (for torch and
@@ -905,7 +971,14 @@ void collect_timings(spq_ctx* c) {
       CUDA_TRY(cudaEventSynchronize(e.second));
       CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
       c->tm.ms[f] += ms;
-      if (lg) fprintf(lg, "%d %.4f %s\n", f, ms, t < c->tm.tag[f].size() ? c->tm.tag[f][t].c_str() : "");
+      if (lg) {
+        float t0 = -1.f;   // start, relative to mark 0 (the factorization start) when recorded
+        if (!c->marks.empty() && cudaEventElapsedTime(&t0, c->marks[0], e.first) != cudaSuccess) {
+          (void)cudaGetLastError();
+          t0 = -1.f;
+        }
+        fprintf(lg, "%d %.4f %.4f %s\n", f, ms, t0, t < c->tm.tag[f].size() ? c->tm.tag[f][t].c_str() : "");
+      }
       c->ev_pool.push_back(e.first);
       c->ev_pool.push_back(e.second);
     }
@@ -1716,11 +1789,22 @@ bool plan_front(spq_ctx* c, int s, Front& f) {
       if (cc != s) cand.push_back(cc);
   std::sort(cand.begin(), cand.end());
   cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
-  int w = 0;
-  for (int cc : cand) {
-    bool present = false;
-    for (auto& p : f.parts) {
-      Block* b = find_block(c, p.r, cc);
+  // presence of each candidate (factor.py:454): parts in order until a
+  // nonzero row is found.  Walked part-major over each part's row list
+  // (block pointers at hand, no lookups); for every candidate the parts and
+  // rows examined -- hence the unknown-flag bail-out -- are exactly those of
+  // the candidate-major loop.
+  std::vector<char> present(cand.size(), 0);
+  for (auto& p : f.parts) {
+    const FlatSet& row = c->rix[p.r];
+    size_t q = 0;
+    for (size_t t = 0; t < row.v.size(); ++t) {
+      const int cc = row.v[t];
+      if (cc == s) continue;
+      while (q < cand.size() && cand[q] < cc) ++q;
+      if (q == cand.size()) break;
+      if (present[q]) continue;
+      const Block* b = row.b[t];
       if (!b || b->nr == 0 || b->nc == 0) continue;
       const auto& fl = b->flags;
       const bool known = b->clean || !fl.empty();
@@ -1728,18 +1812,21 @@ bool plan_front(spq_ctx* c, int s, Front& f) {
         for (int i = 0; i < b->nr; ++i) {
           const uint8_t v = known ? fl[i] : 2;
           if (v == 2) return false;
-          if (v == 1) { present = true; break; }
+          if (v == 1) { present[q] = 1; break; }
         }
       } else {
         for (int i : p.ix) {
           const uint8_t v = known ? fl[i] : 2;
           if (v == 2) return false;
-          if (v == 1) { present = true; break; }
+          if (v == 1) { present[q] = 1; break; }
         }
       }
-      if (present) break;
     }
-    if (present) {
+  }
+  int w = 0;
+  for (size_t q = 0; q < cand.size(); ++q) {
+    if (present[q]) {
+      const int cc = cand[q];
       f.cols_t.push_back(cc);
       f.woff.push_back(w);
       w += (int)c->cols_of[cc].size();
@@ -1765,8 +1852,15 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
     auto& p = f.parts[pi];
     Block* b = find_block(c, p.r, s);
     if (b && b->nc > 0 && b->nr > 0) f.psrc.push_back({b->p, b->nr, pi, 0, b->nc, p.full});
+    // blocks (p.r, cols_t[ci]): merge-walk of the sorted row list and cols_t
+    const FlatSet& row = c->rix[p.r];
+    size_t t = 0;
     for (int ci = 0; ci < (int)f.cols_t.size(); ++ci) {
-      Block* bc = find_block(c, p.r, f.cols_t[ci]);
+      const int cc = f.cols_t[ci];
+      while (t < row.v.size() && row.v[t] < cc) ++t;
+      if (t == row.v.size()) break;
+      if (row.v[t] != cc) continue;
+      Block* bc = row.b[t];
       if (bc && bc->nr > 0 && bc->nc > 0)
         f.gsrc.push_back({bc->p, bc->nr, pi, f.woff[ci], bc->nc, p.full});
     }
@@ -2513,7 +2607,7 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       const int u = j.us[q], h_u = j.hu[q];
       Block* old = find_block(c, u, p);
       // rows of u keep their zero pattern under the right rotation
-      std::vector<uint8_t> keep_fl;
+      RowFlags keep_fl;
       const bool known = c->spec && old && old->clean && old->flags.size() == (size_t)h_u;
       if (known) keep_fl = old->flags;
       if (old) release_mem(c, *old);
@@ -2714,14 +2808,18 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
   }
   CopyBatch zeros, cp;
   // deterministic order: sort old keys
-  std::vector<uint64_t> keys;
+  std::vector<std::pair<uint64_t, Block*>> keys;   // (key, block): no lookups below
   keys.reserve(old.size());
-  old.for_each([&](uint64_t key, Block&) { keys.push_back(key); });
-  std::sort(keys.begin(), keys.end());
+  old.for_each([&](uint64_t key, Block& B) { keys.push_back({key, &B}); });
+  std::sort(keys.begin(), keys.end(),
+            [](const std::pair<uint64_t, Block*>& x, const std::pair<uint64_t, Block*>& y) {
+              return x.first < y.first;
+            });
   // parent blocks needed, grouped by parent row: one zeroed allocation per row
   std::vector<std::vector<int>> prow_v(c->ncl);   // Pi -> Pj list
-  for (uint64_t key : keys) {
-    Block& B = old.at(key);
+  for (auto& kb : keys) {
+    const uint64_t key = kb.first;
+    Block& B = *kb.second;
     if ((int64_t)B.nr * B.nc == 0) continue;
     const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
     const int Pi = parent_of[i], Pj = parent_of[j];
@@ -2737,11 +2835,11 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
   c->blk.reserve(nparent_blocks * 2 + 16);
   // old blocks by parent row; a shared slab only ever holds blocks of one
   // row cluster, so releasing a parent row's children frees whole slabs
-  std::vector<std::vector<uint64_t>> by_prow(c->ncl);
-  for (uint64_t key : keys) {
-    Block& B = old.at(key);
+  std::vector<std::vector<std::pair<uint64_t, Block*>>> by_prow(c->ncl);
+  for (auto& kb : keys) {
+    Block& B = *kb.second;
     if ((int64_t)B.nr * B.nc == 0) { release_mem(c, B); continue; }
-    by_prow[parent_of[(int)(key >> 32)]].push_back(key);
+    by_prow[parent_of[(int)(kb.first >> 32)]].push_back(kb);
   }
   flush_deferred(c);
   // parent rows in groups of bounded new storage: allocate + zero the
@@ -2778,8 +2876,9 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
       }
     }
     for (int q = g0; q < Pi; ++q)
-      for (uint64_t key : by_prow[q]) {
-        Block& B = old.at(key);
+      for (auto& kb : by_prow[q]) {
+        const uint64_t key = kb.first;
+        Block& B = *kb.second;
         const int i = (int)(key >> 32), j = (int)(key & 0xffffffffu);
         const int Pj = parent_of[j];
         Block* tgt = find_block(c, q, Pj);
@@ -2848,7 +2947,7 @@ void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
   for (int64_t i = 0; i < N; ++i)
     if (rown[i] < 0 || coln[i] < 0) throw SpqError(SPQ_ERR_BAD_INPUT, "leaf clusters do not cover all rows/columns");
   // block structure of the entries
-  std::unordered_map<uint64_t, int> bidx;
+  FlatMap<int> bidx;
   std::vector<std::pair<int, int>> bkeys;
   std::vector<int> eb(nnz);
   std::vector<int64_t> eoff(nnz);
@@ -2858,14 +2957,14 @@ void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
       const int64_t r = indices[e];
       const int ri = rown[r];
       const uint64_t key = bkey(ri, cj);
-      auto it = bidx.find(key);
+      const int* hit = bidx.find(key);
       int b;
-      if (it == bidx.end()) {
+      if (!hit) {
         b = (int)bkeys.size();
-        bidx.emplace(key, b);
+        bidx[key] = b;
         bkeys.push_back({ri, cj});
       } else {
-        b = it->second;
+        b = *hit;
       }
       eb[e] = b;
       eoff[e] = rpos[r] + (int64_t)cpos[j] * (int64_t)c->rows_of[ri].size();
