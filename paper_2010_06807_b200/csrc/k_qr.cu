@@ -623,53 +623,59 @@ __global__ void __launch_bounds__(LARFT_NT) larft_kernel(const LarftJob* __restr
 // buffer (G is only read above the diagonal): no second k x k array.
 constexpr int LARFT_FULL_MAX = 160;
 
-__global__ void __launch_bounds__(LARFT_NT) larft_full_kernel(const LarftJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(4 * LARFT_FULL_MAX) larft_full_kernel(const LarftJob* __restrict__ jobs) {
   const LarftJob J = jobs[blockIdx.x];
-  const int k = J.k, tid = threadIdx.x;
+  const int k = J.k, tid = threadIdx.x, nt = blockDim.x;
   const int ld = (k + 1) & ~1;   // even: column reads and the (ld+1) row stride are conflict-free
   extern __shared__ double S[];
   // G (upper triangle) in batches of 8 independent loads per thread: their
   // latencies overlap (a plain strided loop serialises one L2 round trip
   // per iteration)
-  for (int e0 = 0; e0 < k * k; e0 += 8 * LARFT_NT) {
+  for (int e0 = 0; e0 < k * k; e0 += 8 * nt) {
     double t[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int e = e0 + tid + u * LARFT_NT;
+      const int e = e0 + tid + u * nt;
       const int a = e % k, b = e / k;
       t[u] = (e < k * k && a < b) ? __ldg(J.G + a + (int64_t)b * J.ldg) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int e = e0 + tid + u * LARFT_NT;
+      const int e = e0 + tid + u * nt;
       const int a = e % k, b = e / k;
       if (e < k * k && a < b) S[a + b * ld] = t[u];
     }
   }
   __syncthreads();
-  if (tid < k) {
-    const int a = tid;
+  // row a of T by four lanes (the long rows near the top set the kernel's
+  // duration): lane `sub` sums b = a+1+sub, a+5+sub, ...; two shuffles
+  // combine; lane 0 stores and the group syncs before the next entry
+  const int a = tid >> 2, sub = tid & 3;
+  const unsigned gm = 0xFu << ((tid & 31) & 28);
+  if (a < k) {
     const double ta = J.tau[a];
     double* Ta = S + a * ld;   // Ta[b] = T[a,b] for b > a (lower triangle, column a)
     for (int i = a + 1; i < k; ++i) {
       const double* Gi = S + i * ld;   // Gi[b] = G[b,i], b < i
-      double s0 = ta * Gi[a], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int b = a + 1;
-      for (; b + 3 < i; b += 4) {
+      double s0 = sub == 0 ? ta * Gi[a] : 0.0, s1 = 0.0;
+      int b = a + 1 + sub;
+      for (; b + 4 < i; b += 8) {
         s0 = fma(Ta[b], Gi[b], s0);
-        s1 = fma(Ta[b + 1], Gi[b + 1], s1);
-        s2 = fma(Ta[b + 2], Gi[b + 2], s2);
-        s3 = fma(Ta[b + 3], Gi[b + 3], s3);
+        s1 = fma(Ta[b + 4], Gi[b + 4], s1);
       }
-      for (; b < i; ++b) s0 = fma(Ta[b], Gi[b], s0);
+      if (b < i) s0 = fma(Ta[b], Gi[b], s0);
+      double sv = s0 + s1;
+      sv += __shfl_xor_sync(gm, sv, 1);
+      sv += __shfl_xor_sync(gm, sv, 2);
       const double ti = J.tau[i];
-      Ta[i] = (ti != 0.0) ? -ti * ((s0 + s1) + (s2 + s3)) : 0.0;
+      if (sub == 0) Ta[i] = (ti != 0.0) ? -ti * sv : 0.0;
+      __syncwarp(gm);
     }
   }
   __syncthreads();
-  for (int e = tid; e < k * k; e += LARFT_NT) {
-    const int a = e % k, i = e / k;
-    J.T[a + (int64_t)i * J.ldt] = a < i ? S[i + a * ld] : (a == i ? J.tau[a] : 0.0);
+  for (int e = tid; e < k * k; e += nt) {
+    const int a2 = e % k, i = e / k;
+    J.T[a2 + (int64_t)i * J.ldt] = a2 < i ? S[i + a2 * ld] : (a2 == i ? J.tau[a2] : 0.0);
   }
 }
 
@@ -683,7 +689,8 @@ void launch_larft_full(const LarftJob* d_jobs, int njobs, int kmax, cudaStream_t
     CUDA_TRY(cudaFuncSetAttribute(larft_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     conf = smem;
   }
-  larft_full_kernel<<<njobs, LARFT_NT, smem, st>>>(d_jobs); SPQ_LAUNCH_CHECK();
+  const int nt = ((4 * kmax + 31) / 32) * 32;
+  larft_full_kernel<<<njobs, nt, smem, st>>>(d_jobs); SPQ_LAUNCH_CHECK();
 }
 
 int larft_tiles(int) { return 1; }
