@@ -421,6 +421,14 @@ struct spq_ctx {
   // device memory pool
   std::unordered_map<size_t, std::vector<std::pair<void*, int>>> pool_free;   // (ptr, slab)
   bool counted = false;   // included in gcache().n_ctx
+  // side stream: work off the critical path whose result is only read at a
+  // later join (the sparsifiers' dropped-norm statistic).  While `on_side`,
+  // launches go to the side stream, uploads bypass the ring and every free
+  // is held in side_free until side_join() orders it after the side work.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_side_a = nullptr, ev_side_b = nullptr;
+  bool on_side = false, side_pending = false;
+  std::vector<void*> side_free;
   static constexpr int NAUX = 4;
   cudaStream_t aux[NAUX] = {};               // fork-join streams for independent launches
   cudaEvent_t ev_fork = nullptr, ev_join[NAUX] = {};
@@ -786,6 +794,10 @@ double* dalloc_flex(spq_ctx* c, size_t want, size_t floor, size_t* got) {
 
 void dfree(spq_ctx* c, void* p) {
   if (!p) return;
+  if (c->on_side) {   // still used by queued side work: released at side_join
+    c->side_free.push_back(p);
+    return;
+  }
   auto bi = c->big.find(p);
   if (bi != c->big.end()) {
     c->big.erase(bi);
@@ -855,11 +867,52 @@ void sync(spq_ctx* c) {
   c->host_ms[1] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// enter/leave the side stream (see spq_ctx::side)
+struct SideScope {
+  spq_ctx* c;
+  cudaStream_t main;
+  explicit SideScope(spq_ctx* cc) : c(cc), main(cc->st) {
+    if (!c->side) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side_a, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side_b, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_side_a, main));
+    CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_side_a, 0));
+    c->st = c->side;
+    c->on_side = true;
+  }
+  ~SideScope() {
+    c->st = main;
+    c->on_side = false;
+    c->side_pending = true;
+  }
+};
+
+void dfree(spq_ctx* c, void* p);
+// the main stream waits for all side work; its buffers are released in
+// stream order after that point
+void side_join(spq_ctx* c) {
+  if (!c->side_pending) return;
+  CUDA_TRY(cudaEventRecord(c->ev_side_b, c->side));
+  CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_side_b, 0));
+  c->side_pending = false;
+  std::vector<void*> f;
+  f.swap(c->side_free);
+  for (void* p : f) dfree(c, p);
+}
+
 template <class T>
 T* upload(spq_ctx* c, const T* src, size_t n) {
   const size_t bytes = n * sizeof(T);
   if (bytes == 0) return nullptr;
   size_t aligned = (bytes + 255) & ~(size_t)255;
+  if (c->on_side) {   // the ring is recycled at main-stream syncs: side work owns its buffers
+    T* d = (T*)dalloc(c, bytes);
+    CUDA_TRY(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, c->st));
+    c->side_free.push_back(d);
+    return d;
+  }
   if (aligned > c->ring_cap) {
     // oversize: dedicated allocation, freed stream-ordered after use by caller
     T* d = (T*)dalloc(c, bytes);
@@ -2326,6 +2379,7 @@ struct SpJob {
   double *M = nullptr, *Wm = nullptr, *sq = nullptr, *pay = nullptr;
   double *V = nullptr, *tau = nullptr, *beta = nullptr, *T = nullptr;
   int *keep = nullptr, *perm = nullptr;
+  bool m_on_side = false;   // M read by queued side-stream work (freed at side_join)
   bool cta = false;
   int cl = 0;        // cluster size for the cluster-resident CPQR (0: cooperative)
   int rank = -1;
@@ -2404,12 +2458,18 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       c->n_kernels += 3;
     }
   }
-  // the kept column counts (one read per wave) size every CPQR exactly
+  // the kept column counts (one read per wave) size every CPQR exactly.
+  // SPQ_SPARSIFY_NO_NKSYNC=1 sizes them by the pre-filter count instead (no
+  // read-back; measured slower on C3: the larger clusters cost more per
+  // pivot step than the sync saves)
   std::vector<SpScal> hk(std::max(nw, 1));
-  {
+  static const bool nk_sync = !env_flag("SPQ_SPARSIFY_NO_NKSYNC");
+  if (nk_sync) {
     HostTimer hw(&c->host_ms[9]);
     CUDA_TRY(cudaMemcpyAsync(hk.data(), dsc, nw * sizeof(SpScal), cudaMemcpyDeviceToHost, c->st));
     sync(c);
+  } else {
+    for (int t = 0; t < nw; ++t) hk[t].nk = J[t].ncols;
   }
   pivot_raise(c, c->piv);   // checks queued by this level's factor/scale calls
   const bool coop_only = env_flag("SPQ_CPQR_COOP"), no_ws = env_flag("SPQ_CPQR_NOWS");
@@ -2549,6 +2609,9 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       gtot += 2 * (size_t)fdim * fdim;
     }
     if (gtot > 0) {
+      // only the level's statistic reads the result (after side_join at the
+      // end of do_sparsify): off the critical path, on the side stream
+      SideScope side_(c);
       double* Et = dalloc(c, etot * sizeof(double));
       double* Gs = dalloc(c, gtot * sizeof(double));
       CopyBatch tcb;
@@ -2582,8 +2645,11 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
       gg.run(c, true, 0);
       launch_power_iter(upload(c, pj), (int)pj.size(), fmax, c->st);
       c->n_kernels++;
-      c->deferred.push_back(Et);
-      c->deferred.push_back(Gs);
+      c->side_free.push_back(Et);
+      c->side_free.push_back(Gs);
+      // the side work reads M (= Q^T M): keep every M of this wave until the join
+      for (int t = 0; t < nw; ++t)
+        if (J[t].np > 0 && J[t].rank > 0 && J[t].rank < J[t].np) J[t].m_on_side = true;
     }
   }
   // split back + structure, in order (factor.py:617-658)
@@ -2594,8 +2660,10 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     const int p = j.p, r = j.rank, np = j.np;
     // M is still read by the queued split-back copies: free after sc.run
     auto release = [&]() {
-      for (void* q : {(void*)j.M, (void*)j.Wm, (void*)j.sq, (void*)j.keep, (void*)j.perm})
+      for (void* q : {(void*)j.Wm, (void*)j.sq, (void*)j.keep, (void*)j.perm})
         c->deferred.push_back((double*)q);
+      if (j.m_on_side) c->side_free.push_back(j.M);
+      else c->deferred.push_back(j.M);
     };
     if (r >= np) {   // factor.py:630-631
       release();
@@ -2763,6 +2831,7 @@ void do_sparsify(spq_ctx* c, const std::vector<int>& ids, double eps,
     }
   }
   // dropped norms of all compressed interfaces: one read at the end
+  side_join(c);
   std::vector<double> hd(2 * ids.size());
   CUDA_TRY(cudaMemcpyAsync(hd.data(), c->d_dropped, hd.size() * 8, cudaMemcpyDeviceToHost, c->st));
   sync(c);
@@ -3403,6 +3472,7 @@ int spq_create(spq_ctx** out, int device) {
 void spq_destroy(spq_ctx* c) {
   if (!c) return;
   try {
+    if (c->side) cudaStreamSynchronize(c->side);
     if (c->st) cudaStreamSynchronize(c->st);
     for (int f = 0; f < F_NFAM; ++f)
       for (auto& e : c->tm.ev[f]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
