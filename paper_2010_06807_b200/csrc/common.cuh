@@ -29,6 +29,22 @@ struct CopyTask {
   int ident;
 };
 
+// ---------------------------------------------------- job lists in params
+// Short job lists travel IN the kernel launch parameters (__grid_constant__,
+// read through a generic pointer into parameter space) instead of through
+// an H2D copy of the upload ring: a small pinned copy between two dependent
+// kernels costs ~2.3 us of device time (measured, tools/memcpy_probe.py),
+// and ~4000 launches per C3 factorization carried one or more.
+template <class T, int N>
+struct PList {
+  T v[N];
+};
+constexpr int PL_GEMM = 24;
+constexpr int PL_RED = 24;
+constexpr int PL_COPY = 48;
+constexpr int PL_WYF = 48;
+constexpr int PL_SMALL = 8;   // panel / larft / CPQR job lists (one front or interface per wave, mostly)
+
 // ------------------------------------------------------------- gemm
 // C = alpha * op(A) * B + beta * C ; op(A) = A (m x k, lda) or A^T (A is k x m)
 struct GemmProb {
@@ -165,7 +181,9 @@ struct CpqrJob {
 
 // ---------------------------------------------------------------- launchers
 namespace spq {
-void launch_copy(const CopyTask* d_tasks, int ntasks, int64_t max_elems, cudaStream_t st);
+// d_* == nullptr: the list is passed in the launch parameters from h_* (n <= PL_*)
+void launch_copy(const CopyTask* d_tasks, const CopyTask* h_tasks, int ntasks, int64_t max_elems,
+                 cudaStream_t st);
 void launch_rowflags(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
                      const int64_t* d_off, unsigned char* d_out, int nblk, cudaStream_t st);
 void launch_rowflags_verify(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
@@ -178,21 +196,25 @@ void launch_colnorms_scale(const int64_t* indptr, const int64_t* indices, double
 void launch_csc_scatter(const int64_t* indptr, const int64_t* indices, const double* data,
                         int64_t N, const int64_t* dest_off, double* const* blk_base,
                         const int* entry_blk, cudaStream_t st);
-void launch_gemm(const GemmProb* d_probs, int nprob, int total_tiles, bool transA, cudaStream_t st);
+void launch_gemm(const GemmProb* d_probs, const GemmProb* h_probs, int nprob, int total_tiles,
+                 bool transA, cudaStream_t st);
 int gemm_tiles(int m, int n);
 void gemm_set_variant(int v);   // 0 default, 1: 64x64 tiles, 2: 128x64 tiles
-void launch_wyf(const WyfJob* d_jobs, int njobs, int tiles, int kmax, int cl, cudaStream_t st);
+void launch_wyf(const WyfJob* d_jobs, const WyfJob* h_jobs, int njobs, int tiles, int kmax, int cl,
+                cudaStream_t st);
 int wyf_kmax();
 int wyf_cluster(int m);
-void launch_splitk_reduce(const SplitRed* d_tasks, int ntasks, int64_t max_mn, cudaStream_t st);
+void launch_splitk_reduce(const SplitRed* d_tasks, const SplitRed* h_tasks, int ntasks,
+                          int64_t max_mn, cudaStream_t st);
 void launch_panel_qr(const PanelJob* d_jobs, int njobs, int cluster, int64_t slab_elems,
                      bool smem, int kbmax, cudaStream_t st);
-void launch_panel_qr_reg(const PanelJob* d_jobs, int njobs, int cluster, int rows_per_thread,
+void launch_panel_qr_reg(const PanelJob* d_jobs, const PanelJob* h_jobs, int njobs, int cluster, int rows_per_thread,
                          int kbmax, cudaStream_t st);
 int panel_reg_kbmax(int kb);
 void launch_larft(const LarftJob* d_jobs, int njobs, int total_tiles, cudaStream_t st);
 int larft_tiles(int k);
-void launch_larft_full(const LarftJob* d_jobs, int njobs, int kmax, cudaStream_t st);
+void launch_larft_full(const LarftJob* d_jobs, const LarftJob* h_jobs, int njobs, int kmax,
+                       cudaStream_t st);
 int larft_full_max();
 void launch_pivot_check(const PivotJob* d_jobs, int njobs, int64_t* d_err_idx,
                         double* d_err_val, cudaStream_t st);
@@ -207,7 +229,7 @@ size_t cpqr_cluster_smem(int m, int ncap, int cl);
 void launch_cpqr_cluster(const CpqrJob* d_jobs, int njobs, int cl, size_t smem, cudaStream_t st);
 int cpqr_reg_plan(int m, int n, int variant, int* tpc);
 size_t cpqr_reg_smem(int padded_rows, int cl);
-void launch_cpqr_reg(const CpqrJob* d_jobs, int njobs, int variant, int cl, int tpc, size_t smem,
+void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int variant, int cl, int tpc, size_t smem,
                      cudaStream_t st);
 void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax,
                        double* part, double* z, int64_t N, int nrhs, cudaStream_t st);

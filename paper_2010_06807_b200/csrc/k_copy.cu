@@ -32,8 +32,10 @@ struct FastDiv {
   }
 };
 
-__global__ void __launch_bounds__(256) copy_tasks_kernel(const CopyTask* __restrict__ tasks) {
-  const CopyTask t = tasks[blockIdx.x];
+template <int NP>
+__global__ void __launch_bounds__(256) copy_tasks_kernel(const CopyTask* __restrict__ tasks_g,
+                                                         const __grid_constant__ PList<CopyTask, NP> pl) {
+  const CopyTask t = NP > 1 ? pl.v[blockIdx.x] : tasks_g[blockIdx.x];
   const int64_t total = (int64_t)t.nr * t.nc;
   const int64_t stride = (int64_t)gridDim.y * blockDim.x;
   const bool small = total + stride < ((int64_t)1 << 32);
@@ -66,14 +68,23 @@ __global__ void __launch_bounds__(256) copy_tasks_kernel(const CopyTask* __restr
   }
 }
 
-void launch_copy(const CopyTask* d_tasks, int ntasks, int64_t max_elems, cudaStream_t st) {
+void launch_copy(const CopyTask* d_tasks, const CopyTask* h_tasks, int ntasks, int64_t max_elems,
+                 cudaStream_t st) {
   if (ntasks <= 0) return;
   int64_t y = (max_elems + 256 * 8 - 1) / (256 * 8);
   if (y < 1) y = 1;
   if (y > 512) y = 512;
   // grid.x limit is 2^31-1; y <= 512 stays far below the 65535 limit
   dim3 grid((unsigned)ntasks, (unsigned)y);
-  copy_tasks_kernel<<<grid, 256, 0, st>>>(d_tasks); SPQ_LAUNCH_CHECK();
+  if (d_tasks == nullptr) {
+    if (ntasks > PL_COPY) throw std::runtime_error("launch_copy: parameter list too long");
+    PList<CopyTask, PL_COPY> pl;
+    for (int i = 0; i < ntasks; ++i) pl.v[i] = h_tasks[i];
+    copy_tasks_kernel<PL_COPY><<<grid, 256, 0, st>>>(nullptr, pl);
+  } else {
+    copy_tasks_kernel<1><<<grid, 256, 0, st>>>(d_tasks, PList<CopyTask, 1>{});
+  }
+  SPQ_LAUNCH_CHECK();
 }
 
 // one CTA per block; thread per row; flag = any nonzero in the row

@@ -927,8 +927,10 @@ struct RgLayout {   // shared memory in doubles; rows padded to mp = tpc * R
 };
 
 template <int R, int C>
-__global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __restrict__ jobs,
-                                                            int tpc) {
+__global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __restrict__ jobs_g,
+                                                            int tpc,
+                                                            const __grid_constant__ PList<CpqrJob, PL_SMALL> pl) {
+  const CpqrJob* jobs = jobs_g ? jobs_g : pl.v;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int q = (int)cluster.block_rank();
@@ -1188,7 +1190,8 @@ int cpqr_reg_plan(int m, int n, int v, int* tpc_out) {
 size_t cpqr_reg_smem(int mp, int cl) { return RgLayout(mp, cl).bytes(); }   // mp = tpc * R
 
 template <int R, int C>
-static void launch_rg(const CpqrJob* d_jobs, int njobs, int cl, int tpc, size_t smem, cudaStream_t st) {
+static void launch_rg(const CpqrJob* d_jobs, const PList<CpqrJob, PL_SMALL>& pl, int njobs, int cl,
+                      int tpc, size_t smem, cudaStream_t st) {
   static bool init = false;
   if (!init) {
     CUDA_TRY(cudaFuncSetAttribute(cpqr_reg_kernel<R, C>,
@@ -1209,16 +1212,21 @@ static void launch_rg(const CpqrJob* d_jobs, int njobs, int cl, int tpc, size_t 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg_kernel<R, C>, d_jobs, tpc));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg_kernel<R, C>, d_jobs, tpc, pl));
 }
 
-void launch_cpqr_reg(const CpqrJob* d_jobs, int njobs, int v, int cl, int tpc, size_t smem,
-                     cudaStream_t st) {
+void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int v, int cl, int tpc,
+                     size_t smem, cudaStream_t st) {
   if (njobs <= 0) return;
+  PList<CpqrJob, PL_SMALL> pl;
+  if (!d_jobs) {
+    if (njobs > PL_SMALL) throw std::runtime_error("launch_cpqr_reg: parameter list too long");
+    for (int i = 0; i < njobs; ++i) pl.v[i] = h_jobs[i];
+  }
   switch (v) {
-    case 0: launch_rg<16, 2>(d_jobs, njobs, cl, tpc, smem, st); break;
-    case 1: launch_rg<8, 4>(d_jobs, njobs, cl, tpc, smem, st); break;
-    case 2: launch_rg<4, 8>(d_jobs, njobs, cl, tpc, smem, st); break;
+    case 0: launch_rg<16, 2>(d_jobs, pl, njobs, cl, tpc, smem, st); break;
+    case 1: launch_rg<8, 4>(d_jobs, pl, njobs, cl, tpc, smem, st); break;
+    case 2: launch_rg<4, 8>(d_jobs, pl, njobs, cl, tpc, smem, st); break;
     default: throw std::runtime_error("cpqr_reg: bad variant");
   }
 }

@@ -60,9 +60,11 @@ __device__ __forceinline__ void gemm_epilogue(const GemmProb& p, const double (&
       }
 }
 
-template <bool TA>
-__global__ void __launch_bounds__(NT) gemm_dmma_kernel(const GemmProb* __restrict__ probs,
-                                                       int nprob) {
+template <bool TA, int NP>
+__global__ void __launch_bounds__(NT) gemm_dmma_kernel(const GemmProb* __restrict__ probs_g,
+                                                       int nprob,
+                                                       const __grid_constant__ PList<GemmProb, NP> pl) {
+  const GemmProb* probs = NP > 1 ? pl.v : probs_g;
   int lo = 0, hi = nprob - 1;
   const int bid = blockIdx.x;
   while (lo < hi) {
@@ -147,8 +149,10 @@ __global__ void __launch_bounds__(NT) gemm_dmma_kernel(const GemmProb* __restric
 
 // C = alpha * sum_s P_s + beta * C over split-K partials P_s (m x n, ld m,
 // stride m*n), fixed summation order -> deterministic
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const SplitRed* __restrict__ tasks) {
-  const SplitRed t = tasks[blockIdx.x];
+template <int NP>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const SplitRed* __restrict__ tasks_g,
+                                                            const __grid_constant__ PList<SplitRed, NP> pl) {
+  const SplitRed t = NP > 1 ? pl.v[blockIdx.x] : tasks_g[blockIdx.x];
   const int64_t mn = (int64_t)t.m * t.n;
   for (int64_t e = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; e < mn;
        e += (int64_t)gridDim.y * blockDim.x) {
@@ -161,12 +165,22 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const SplitRed* __re
   }
 }
 
-void launch_splitk_reduce(const SplitRed* d_tasks, int ntasks, int64_t max_mn, cudaStream_t st) {
+void launch_splitk_reduce(const SplitRed* d_tasks, const SplitRed* h_tasks, int ntasks,
+                          int64_t max_mn, cudaStream_t st) {
   if (ntasks <= 0) return;
   int64_t y = (max_mn + 2047) / 2048;
   if (y < 1) y = 1;
   if (y > 256) y = 256;
-  splitk_reduce_kernel<<<dim3(ntasks, (unsigned)y), 256, 0, st>>>(d_tasks); SPQ_LAUNCH_CHECK();
+  const dim3 grid(ntasks, (unsigned)y);
+  if (d_tasks == nullptr) {
+    if (ntasks > PL_RED) throw std::runtime_error("launch_splitk_reduce: parameter list too long");
+    PList<SplitRed, PL_RED> pl;
+    for (int i = 0; i < ntasks; ++i) pl.v[i] = h_tasks[i];
+    splitk_reduce_kernel<PL_RED><<<grid, 256, 0, st>>>(nullptr, pl);
+  } else {
+    splitk_reduce_kernel<1><<<grid, 256, 0, st>>>(d_tasks, PList<SplitRed, 1>{});
+  }
+  SPQ_LAUNCH_CHECK();
 }
 
 
@@ -187,9 +201,11 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 }  // namespace
 
-template <bool TA>
-__global__ void __launch_bounds__(NT2) gemm_dmma2_kernel(const GemmProb* __restrict__ probs,
-                                                         int nprob) {
+template <bool TA, int NP>
+__global__ void __launch_bounds__(NT2) gemm_dmma2_kernel(const GemmProb* __restrict__ probs_g,
+                                                         int nprob,
+                                                         const __grid_constant__ PList<GemmProb, NP> pl) {
+  const GemmProb* probs = NP > 1 ? pl.v : probs_g;
   int lo = 0, hi = nprob - 1;
   const int bid = blockIdx.x;
   while (lo < hi) {
@@ -290,29 +306,42 @@ int gemm_tiles(int m, int n) {
   return ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
 }
 
-void launch_gemm(const GemmProb* d_probs, int nprob, int total_tiles, bool transA,
-                 cudaStream_t st) {
-  if (nprob <= 0 || total_tiles <= 0) return;
+template <int NP>
+static void launch_gemm_t(const GemmProb* d_probs, const PList<GemmProb, NP>& pl, int nprob,
+                          int total_tiles, bool transA, cudaStream_t st) {
   if (gemm_variant() == 2) {
     const size_t smem = (size_t)ST2 * BK2 * (PA2 + PB2) * sizeof(double);
     static bool init = false;
     if (!init) {
-      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<true, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<false, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       init = true;
     }
     if (transA)
-      gemm_dmma2_kernel<true><<<total_tiles, NT2, smem, st>>>(d_probs, nprob);
+      gemm_dmma2_kernel<true, NP><<<total_tiles, NT2, smem, st>>>(d_probs, nprob, pl);
     else
-      gemm_dmma2_kernel<false><<<total_tiles, NT2, smem, st>>>(d_probs, nprob);
+      gemm_dmma2_kernel<false, NP><<<total_tiles, NT2, smem, st>>>(d_probs, nprob, pl);
     SPQ_LAUNCH_CHECK();
     return;
   }
   if (transA)
-    gemm_dmma_kernel<true><<<total_tiles, NT, 0, st>>>(d_probs, nprob);
+    gemm_dmma_kernel<true, NP><<<total_tiles, NT, 0, st>>>(d_probs, nprob, pl);
   else
-    gemm_dmma_kernel<false><<<total_tiles, NT, 0, st>>>(d_probs, nprob);
+    gemm_dmma_kernel<false, NP><<<total_tiles, NT, 0, st>>>(d_probs, nprob, pl);
   SPQ_LAUNCH_CHECK();
+}
+
+void launch_gemm(const GemmProb* d_probs, const GemmProb* h_probs, int nprob, int total_tiles,
+                 bool transA, cudaStream_t st) {
+  if (nprob <= 0 || total_tiles <= 0) return;
+  if (d_probs == nullptr) {
+    if (nprob > PL_GEMM) throw std::runtime_error("launch_gemm: parameter list too long");
+    PList<GemmProb, PL_GEMM> pl;
+    for (int i = 0; i < nprob; ++i) pl.v[i] = h_probs[i];
+    launch_gemm_t<PL_GEMM>(nullptr, pl, nprob, total_tiles, transA, st);
+  } else {
+    launch_gemm_t<1>(d_probs, PList<GemmProb, 1>{}, nprob, total_tiles, transA, st);
+  }
 }
 
 }  // namespace spq

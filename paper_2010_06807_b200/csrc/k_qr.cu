@@ -412,10 +412,12 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
 }
 
 template <int R, int KBMAX>
-__global__ void __launch_bounds__(QRR_NT, 1) panel_qr_reg_kernel(const PanelJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(QRR_NT, 1) panel_qr_reg_kernel(const PanelJob* __restrict__ jobs_g,
+                                                                 const __grid_constant__ PList<PanelJob, PL_SMALL> pl) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int q = (int)cluster.block_rank();
+  const PanelJob* jobs = jobs_g ? jobs_g : pl.v;
   const PanelJob J = jobs[blockIdx.x / CL];
   const int m = J.m, k = J.k, j0 = J.j0, kb = J.kb;
   const int mh = m - j0;
@@ -506,21 +508,27 @@ __global__ void __launch_bounds__(QRR_NT, 1) panel_qr_reg_kernel(const PanelJob*
 }
 
 template <int R, int KBMAX>
-void launch_qrr(const cudaLaunchConfig_t& cfg, const PanelJob* d_jobs) {
+void launch_qrr(const cudaLaunchConfig_t& cfg, const PanelJob* d_jobs,
+                const PList<PanelJob, PL_SMALL>& pl) {
   static bool init = false;
   if (!init) {
     CUDA_TRY(cudaFuncSetAttribute(panel_qr_reg_kernel<R, KBMAX>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     init = true;
   }
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_qr_reg_kernel<R, KBMAX>, d_jobs));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, panel_qr_reg_kernel<R, KBMAX>, d_jobs, pl));
 }
 
 int panel_reg_kbmax(int kb) { return kb <= 8 ? 8 : kb <= 16 ? 16 : kb <= 24 ? 24 : 32; }
 
-void launch_panel_qr_reg(const PanelJob* d_jobs, int njobs, int cluster, int rows_per_thread,
-                         int kbmax, cudaStream_t st) {
+void launch_panel_qr_reg(const PanelJob* d_jobs, const PanelJob* h_jobs, int njobs, int cluster,
+                         int rows_per_thread, int kbmax, cudaStream_t st) {
   if (njobs <= 0) return;
+  PList<PanelJob, PL_SMALL> pl;
+  if (!d_jobs) {
+    if (njobs > PL_SMALL) throw std::runtime_error("launch_panel_qr_reg: parameter list too long");
+    for (int i = 0; i < njobs; ++i) pl.v[i] = h_jobs[i];
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(njobs * cluster));
   cfg.blockDim = dim3(QRR_NT);
@@ -535,15 +543,15 @@ void launch_panel_qr_reg(const PanelJob* d_jobs, int njobs, int cluster, int row
   cfg.numAttrs = 1;
   const int kc = panel_reg_kbmax(kbmax);
   if (rows_per_thread <= 1) {
-    if (kc == 8) launch_qrr<1, 8>(cfg, d_jobs);
-    else if (kc == 16) launch_qrr<1, 16>(cfg, d_jobs);
-    else if (kc == 24) launch_qrr<1, 24>(cfg, d_jobs);
-    else launch_qrr<1, 32>(cfg, d_jobs);
+    if (kc == 8) launch_qrr<1, 8>(cfg, d_jobs, pl);
+    else if (kc == 16) launch_qrr<1, 16>(cfg, d_jobs, pl);
+    else if (kc == 24) launch_qrr<1, 24>(cfg, d_jobs, pl);
+    else launch_qrr<1, 32>(cfg, d_jobs, pl);
   } else {
-    if (kc == 8) launch_qrr<2, 8>(cfg, d_jobs);
-    else if (kc == 16) launch_qrr<2, 16>(cfg, d_jobs);
-    else if (kc == 24) launch_qrr<2, 24>(cfg, d_jobs);
-    else launch_qrr<2, 32>(cfg, d_jobs);
+    if (kc == 8) launch_qrr<2, 8>(cfg, d_jobs, pl);
+    else if (kc == 16) launch_qrr<2, 16>(cfg, d_jobs, pl);
+    else if (kc == 24) launch_qrr<2, 24>(cfg, d_jobs, pl);
+    else launch_qrr<2, 32>(cfg, d_jobs, pl);
   }
 }
 
@@ -623,8 +631,9 @@ __global__ void __launch_bounds__(LARFT_NT) larft_kernel(const LarftJob* __restr
 // buffer (G is only read above the diagonal): no second k x k array.
 constexpr int LARFT_FULL_MAX = 160;
 
-__global__ void __launch_bounds__(4 * LARFT_FULL_MAX) larft_full_kernel(const LarftJob* __restrict__ jobs) {
-  const LarftJob J = jobs[blockIdx.x];
+__global__ void __launch_bounds__(4 * LARFT_FULL_MAX) larft_full_kernel(const LarftJob* __restrict__ jobs_g,
+                                                                       const __grid_constant__ PList<LarftJob, PL_SMALL> pl) {
+  const LarftJob J = jobs_g ? jobs_g[blockIdx.x] : pl.v[blockIdx.x];
   const int k = J.k, tid = threadIdx.x, nt = blockDim.x;
   const int ld = (k + 1) & ~1;   // even: column reads and the (ld+1) row stride are conflict-free
   extern __shared__ double S[];
@@ -681,8 +690,14 @@ __global__ void __launch_bounds__(4 * LARFT_FULL_MAX) larft_full_kernel(const La
 
 int larft_full_max() { return LARFT_FULL_MAX; }
 
-void launch_larft_full(const LarftJob* d_jobs, int njobs, int kmax, cudaStream_t st) {
+void launch_larft_full(const LarftJob* d_jobs, const LarftJob* h_jobs, int njobs, int kmax,
+                       cudaStream_t st) {
   if (njobs <= 0) return;
+  PList<LarftJob, PL_SMALL> pl;
+  if (!d_jobs) {
+    if (njobs > PL_SMALL) throw std::runtime_error("launch_larft_full: parameter list too long");
+    for (int i = 0; i < njobs; ++i) pl.v[i] = h_jobs[i];
+  }
   const size_t smem = (size_t)kmax * ((kmax + 1) & ~1) * sizeof(double);
   static size_t conf = 0;
   if (smem > conf) {
@@ -690,7 +705,7 @@ void launch_larft_full(const LarftJob* d_jobs, int njobs, int kmax, cudaStream_t
     conf = smem;
   }
   const int nt = ((4 * kmax + 31) / 32) * 32;
-  larft_full_kernel<<<njobs, nt, smem, st>>>(d_jobs); SPQ_LAUNCH_CHECK();
+  larft_full_kernel<<<njobs, nt, smem, st>>>(d_jobs, pl); SPQ_LAUNCH_CHECK();
 }
 
 int larft_tiles(int) { return 1; }

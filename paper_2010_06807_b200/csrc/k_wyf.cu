@@ -88,8 +88,10 @@ __device__ __forceinline__ void wyf_load(WyfSmem<KM>& sh, const WyfJob& J, int r
   wyf_load_mat<WYF_TC, WYF_LDS>(sh.Cs, J.C + (int64_t)c0 * J.ldc, J.ldc, r0, nr, nc);
 }
 
-template <int KM>
-__global__ void __launch_bounds__(WYF_NT, 1) wyf_kernel(const WyfJob* __restrict__ jobs, int njobs) {
+template <int KM, int NP>
+__global__ void __launch_bounds__(WYF_NT, 1) wyf_kernel(const WyfJob* __restrict__ jobs_g, int njobs,
+                                                        const __grid_constant__ PList<WyfJob, NP> pl) {
+  const WyfJob* jobs = NP > 1 ? pl.v : jobs_g;
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = (int)cluster.num_blocks();
   const int q = (int)cluster.block_rank();
@@ -200,13 +202,14 @@ int wyf_cluster(int m) {   // CTAs per tile: rows resident in one chunk when pos
   return cl < 1 ? 1 : (cl > 16 ? 16 : cl);
 }
 
-template <int KM>
-static void launch_wyf_t(const WyfJob* d_jobs, int njobs, int tiles, int cl, cudaStream_t st) {
+template <int KM, int NP>
+static void launch_wyf_t(const WyfJob* d_jobs, const PList<WyfJob, NP>& pl, int njobs, int tiles,
+                         int cl, cudaStream_t st) {
   const size_t smem = sizeof(WyfSmem<KM>);
   static bool init = false;
   if (!init) {
-    CUDA_TRY(cudaFuncSetAttribute(wyf_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CUDA_TRY(cudaFuncSetAttribute(wyf_kernel<KM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CUDA_TRY(cudaFuncSetAttribute(wyf_kernel<KM, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_TRY(cudaFuncSetAttribute(wyf_kernel<KM, NP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     init = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -221,13 +224,27 @@ static void launch_wyf_t(const WyfJob* d_jobs, int njobs, int tiles, int cl, cud
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, wyf_kernel<KM>, d_jobs, njobs));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, wyf_kernel<KM, NP>, d_jobs, njobs, pl));
 }
 
-void launch_wyf(const WyfJob* d_jobs, int njobs, int tiles, int kmax, int cl, cudaStream_t st) {
+template <int KM>
+static void launch_wyf_k(const WyfJob* d_jobs, const WyfJob* h_jobs, int njobs, int tiles, int cl,
+                         cudaStream_t st) {
+  if (d_jobs == nullptr) {
+    if (njobs > PL_WYF) throw std::runtime_error("launch_wyf: parameter list too long");
+    PList<WyfJob, PL_WYF> pl;
+    for (int i = 0; i < njobs; ++i) pl.v[i] = h_jobs[i];
+    launch_wyf_t<KM, PL_WYF>(nullptr, pl, njobs, tiles, cl, st);
+  } else {
+    launch_wyf_t<KM, 1>(d_jobs, PList<WyfJob, 1>{}, njobs, tiles, cl, st);
+  }
+}
+
+void launch_wyf(const WyfJob* d_jobs, const WyfJob* h_jobs, int njobs, int tiles, int kmax, int cl,
+                cudaStream_t st) {
   if (njobs <= 0 || tiles <= 0) return;
-  if (kmax <= 32) launch_wyf_t<32>(d_jobs, njobs, tiles, cl, st);
-  else if (kmax <= 64) launch_wyf_t<64>(d_jobs, njobs, tiles, cl, st);
+  if (kmax <= 32) launch_wyf_k<32>(d_jobs, h_jobs, njobs, tiles, cl, st);
+  else if (kmax <= 64) launch_wyf_k<64>(d_jobs, h_jobs, njobs, tiles, cl, st);
   else throw std::runtime_error("wyf: k > 64");
 }
 

@@ -939,6 +939,15 @@ template <class T>
 T* upload(spq_ctx* c, const std::vector<T>& v) {
   return upload(c, v.data(), v.size());
 }
+// nullptr (the launcher carries the list in its parameters) for short
+// lists, an uploaded copy otherwise; SPQ_NO_PARAM_LISTS=1 always uploads
+int env_flag(const char* name);
+template <class T>
+const T* up_or_param(spq_ctx* c, const std::vector<T>& v, int pmax) {
+  static const bool off = env_flag("SPQ_NO_PARAM_LISTS");
+  if (!off && (int)v.size() <= pmax) return nullptr;
+  return upload(c, v);
+}
 
 void flush_deferred(spq_ctx* c) {
   for (double* p : c->deferred) dfree(c, p);
@@ -1086,8 +1095,7 @@ struct CopyBatch {
   void run(spq_ctx* c) {
     if (t.empty()) return;
     Scope s(c, F_COPY);
-    const CopyTask* d = upload(c, t);
-    launch_copy(d, (int)t.size(), maxe, c->st);
+    launch_copy(up_or_param(c, t, PL_COPY), t.data(), (int)t.size(), maxe, c->st);
     c->tm.launches[F_COPY]++;
     c->n_kernels++;
     double by = 0;
@@ -1185,8 +1193,9 @@ struct GemmBatch {
         tag = b;
       }
       Scope s(c, F_WY, tag);
-      launch_gemm(upload(c, q), (int)q.size(), t0, transA, c->st);
-      if (!red.empty()) launch_splitk_reduce(upload(c, red), (int)red.size(), red_max, c->st);
+      launch_gemm(up_or_param(c, q, PL_GEMM), q.data(), (int)q.size(), t0, transA, c->st);
+      if (!red.empty())
+        launch_splitk_reduce(up_or_param(c, red, PL_RED), red.data(), (int)red.size(), red_max, c->st);
     }
     c->tm.launches[F_WY] += 1 + (red.empty() ? 0 : 1);
     c->n_kernels += 1 + (red.empty() ? 0 : 1);
@@ -1259,7 +1268,7 @@ void build_full_T(spq_ctx* c, const std::vector<TProb>& tp) {
   gg.run(c, true, 0);
   if (maxk <= larft_full_max() && !env_flag("SPQ_LARFT_DOUBLING")) {   // whole T in one launch
     Scope s(c, F_QR);
-    launch_larft_full(upload(c, lj), (int)lj.size(), maxk, c->st);
+    launch_larft_full(up_or_param(c, lj, PL_SMALL), lj.data(), (int)lj.size(), maxk, c->st);
     c->tm.launches[F_QR]++;
     c->n_kernels++;
     dfree(c, scr);
@@ -1383,7 +1392,7 @@ void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs_in, bool transpose, i
         wj.push_back(w);
       }
       Scope s(c, F_WY, wyf_tag(c, wj, tiles, cl));
-      launch_wyf(upload(c, wj), (int)wj.size(), tiles, kmax, cl, c->st);
+      launch_wyf(up_or_param(c, wj, PL_WYF), wj.data(), (int)wj.size(), tiles, kmax, cl, c->st);
       c->tm.launches[F_WY]++;
       c->n_kernels++;
       return;
@@ -1505,7 +1514,8 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
         c->n_kernels++;
       }
       for (auto& kv : rgroups) {
-        launch_panel_qr_reg(upload(c, kv.second), (int)kv.second.size(), std::get<0>(kv.first),
+        launch_panel_qr_reg(up_or_param(c, kv.second, PL_SMALL), kv.second.data(),
+                            (int)kv.second.size(), std::get<0>(kv.first),
                             std::get<1>(kv.first), std::get<2>(kv.first), c->st);
         c->tm.launches[F_QR]++;
         c->n_kernels++;
@@ -1531,7 +1541,7 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
         wj.push_back(w);
       }
       Scope s(c, F_WY, wyf_tag(c, wj, tiles, cl));
-      launch_wyf(upload(c, wj), (int)wj.size(), tiles, NB, cl, c->st);
+      launch_wyf(up_or_param(c, wj, PL_WYF), wj.data(), (int)wj.size(), tiles, NB, cl, c->st);
       c->tm.launches[F_WY]++;
       c->n_kernels++;
       continue;
@@ -2524,10 +2534,10 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
   {
     Scope s(c, F_CPQR);
     // upload every job list first (the ring), then fork
-    std::vector<std::tuple<const CpqrJob*, int, std::tuple<int, int, int>, size_t>> wl;
+    std::vector<std::tuple<const CpqrJob*, int, std::tuple<int, int, int>, size_t, const CpqrJob*>> wl;
     for (auto& kv : rg_groups)
-      wl.emplace_back(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first,
-                      kv.second.second);
+      wl.emplace_back(up_or_param(c, kv.second.first, PL_SMALL), (int)kv.second.first.size(), kv.first,
+                      kv.second.second, kv.second.first.data());
     std::vector<std::tuple<const CpqrJob*, int, int, size_t>> cl_l;
     for (auto& kv : by_cl)
       cl_l.emplace_back(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first,
@@ -2536,7 +2546,7 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     Fork fk(c);
     for (auto& w : wl) {
       const auto& key = std::get<2>(w);
-      launch_cpqr_reg(std::get<0>(w), std::get<1>(w), std::get<0>(key), std::get<1>(key),
+      launch_cpqr_reg(std::get<0>(w), std::get<4>(w), std::get<1>(w), std::get<0>(key), std::get<1>(key),
                       std::get<2>(key), std::get<3>(w), fk.next());
       c->tm.launches[F_CPQR]++;
       c->n_kernels++;
