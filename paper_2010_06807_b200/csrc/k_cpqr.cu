@@ -1009,15 +1009,17 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
     if (tid == 0) { sx[0] = cv; sx[1] = __longlong_as_double((long long)ck); }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk copy
     __syncthreads();
-    if (tid == 0) {
+    // one bulk copy per destination, issued by CL threads of warp 0 in
+    // parallel (serial issue from one thread put CL copy set-ups in a row on
+    // every pivot step's critical path)
+    if (tid < CL) {
       const uint32_t src = rg_smem(sx);
-      for (int d = 0; d < CL; ++d) {
-        const uint32_t dst = rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec), d);
-        const uint32_t mb = rg_mapa(rg_smem(&mbar[slot]), d);
-        asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes "
-                     "[%0], [%1], %2, [%3];" :: "r"(dst), "r"(src), "r"(rec_bytes), "r"(mb)
-                     : "memory");
-      }
+      const int d = tid;
+      const uint32_t dst = rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec), d);
+      const uint32_t mb = rg_mapa(rg_smem(&mbar[slot]), d);
+      asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes "
+                   "[%0], [%1], %2, [%3];" :: "r"(dst), "r"(src), "r"(rec_bytes), "r"(mb)
+                   : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
     }
