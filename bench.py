@@ -165,12 +165,18 @@ def family_line(name, v, steps, peak64, hbm):
          "launches_per_step": v["launches"] / steps}
     if v["ms"] <= 0:
         return d
+    t_roof = 0.0     # roofline time: the slower of fp64 peak and HBM for the family's work
     if v["flops"] > 0:
         ach = v["flops"] / (v["ms"] * 1e-3) / 1e12
         d.update({"achieved_tflops": ach, "frac_fp64_peak": ach / peak64 if peak64 else None})
-    elif v.get("bytes", 0) > 0:
+        if peak64:
+            t_roof = max(t_roof, v["flops"] / (peak64 * 1e12))
+    if v.get("bytes", 0) > 0:
         ach = v["bytes"] / (v["ms"] * 1e-3) / 1e9
         d.update({"achieved_gbs": ach, "frac_hbm": ach / hbm})
+        t_roof = max(t_roof, v["bytes"] / (hbm * 1e9))
+    if t_roof > 0:
+        d["frac_roofline"] = t_roof / (v["ms"] * 1e-3)
     return d
 
 
@@ -302,7 +308,9 @@ def main():
     roof = None
     if dom is not None:
         d = fams[dom]
-        if dom in ("copy", "flags", "chain"):
+        t_f = d["flops"] / (peak64 * 1e12) if (peak64 and d["flops"]) else 0.0
+        t_b = d.get("bytes", 0.0) / (hbm * 1e9)
+        if dom in ("copy", "flags", "chain") or t_b > t_f:
             ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                     "frac": ach / hbm, "traffic": None, "kernel_family": dom,
@@ -313,6 +321,19 @@ def main():
                     "peak": peak64, "unit": "TFLOP/s", "frac": ach / peak64, "traffic": None,
                     "kernel_family": dom,
                     "peak_source": "measured cuBLAS DGEMM 8192^3 (torch.matmul fp64) on this box"}
+    if roof is not None:
+        # DRAM bytes per launch of the same family from the committed ncu launch list
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            ft = tr["families"][dom]
+            roof["traffic"] = ft["dram_bytes_per_launch"]
+            roof["traffic_unit"] = "bytes/launch (dram read+write)"
+            roof["traffic_source"] = "profiles/ncu_traffic.json (" + tr["source"] + ")"
+            # algorithmic bytes per launch of the family, for comparison with traffic
+            if d.get("launches"):
+                roof["algorithmic_bytes_per_launch"] = d.get("bytes", 0.0) / d["launches"]
+        except (OSError, KeyError, ValueError):
+            pass
     qr_fams = [f for f in ("qr", "wy", "trsm", "cpqr") if f in fams]
     qflops = sum(fams[f]["flops"] for f in qr_fams)
     qms = sum(fams[f]["ms"] for f in qr_fams)

@@ -1363,6 +1363,8 @@ void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs_in, bool transpose, i
     }
   }
   if (tot == 0) return;
+  for (auto& p : probs)   // algorithmic bytes of the WY apply: 8(2mn + mk + k^2)
+    c->tm.bytes[F_WY] += 8.0 * (2.0 * p.m * (double)p.n + (double)p.m * p.k + (double)p.k * p.k);
   {
     // shallow reflector blocks (every k <= 64) with little total work: one
     // fused launch (k_wyf.cu) instead of three GEMM launches + split-K
@@ -1465,6 +1467,7 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
   int maxk = 0;
   for (auto& q : probs) {
     qr_flops += 2.0 * q.m * (double)q.k * q.k - 2.0 * q.k * (double)q.k * q.k / 3.0;
+    c->tm.bytes[F_QR] += 8.0 * (2.0 * q.m * (double)q.k + (double)q.k * q.k);
     maxk = std::max(maxk, q.k);
   }
   c->tm.flops[F_QR] += qr_flops;
@@ -1538,6 +1541,7 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
         tiles += (w.n + 31) / 32;
         cl = std::max(cl, wyf_cluster(w.m));
         c->tm.flops[F_WY] += 4.0 * w.m * (double)w.n * w.k - (double)w.n * w.k * w.k;
+        c->tm.bytes[F_WY] += 8.0 * (2.0 * w.m * (double)w.n + (double)w.m * w.k + (double)w.k * w.k);
         wj.push_back(w);
       }
       Scope s(c, F_WY, wyf_tag(c, wj, tiles, cl));
@@ -2600,6 +2604,7 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     outs[t].rank = j.rank;
     const double mm = j.np, nn = h[t].nk, rr = j.rank;
     c->tm.flops[F_CPQR] += 4.0 * mm * nn * rr - 2.0 * rr * rr * (mm + nn) + 4.0 * rr * rr * rr / 3.0;
+    c->tm.bytes[F_CPQR] += 16.0 * mm * nn;
     if (j.rank >= j.np || j.rank <= 0) continue;
     tp.push_back(TProb{j.V, j.np, j.rank, j.tau, j.T});
     wp.push_back(WyProb{j.V, j.T, j.np, j.rank, j.M, j.np, j.ncols});
