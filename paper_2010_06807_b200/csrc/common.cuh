@@ -27,6 +27,8 @@ struct CopyTask {
   int lds, ldd;
   int trans;
   int ident;
+  int cta0;   // first CTA of the task in a flattened (1-D) copy grid
+  int ncta;   // CTAs of the task in that grid
 };
 
 // ---------------------------------------------------- job lists in params
@@ -183,7 +185,7 @@ struct CpqrJob {
 namespace spq {
 // d_* == nullptr: the list is passed in the launch parameters from h_* (n <= PL_*)
 void launch_copy(const CopyTask* d_tasks, const CopyTask* h_tasks, int ntasks, int64_t max_elems,
-                 cudaStream_t st);
+                 int64_t total_ctas, cudaStream_t st);
 void launch_rowflags(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
                      const int64_t* d_off, unsigned char* d_out, int nblk, cudaStream_t st);
 void launch_rowflags_verify(const double* const* d_ptrs, const int* d_nr, const int* d_nc,

@@ -32,15 +32,13 @@ struct FastDiv {
   }
 };
 
-template <int NP>
-__global__ void __launch_bounds__(256) copy_tasks_kernel(const CopyTask* __restrict__ tasks_g,
-                                                         const __grid_constant__ PList<CopyTask, NP> pl) {
-  const CopyTask t = NP > 1 ? pl.v[blockIdx.x] : tasks_g[blockIdx.x];
+// Element loop of one task: CTA `cb` of `nb` CTAs assigned to it.
+__device__ __forceinline__ void copy_task_elems(const CopyTask& t, int64_t cb, int64_t nb) {
   const int64_t total = (int64_t)t.nr * t.nc;
-  const int64_t stride = (int64_t)gridDim.y * blockDim.x;
+  const int64_t stride = nb * blockDim.x;
   const bool small = total + stride < ((int64_t)1 << 32);
   const FastDiv fd((uint32_t)(t.nr > 0 ? t.nr : 1));
-  for (int64_t e = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; e < total; e += stride) {
+  for (int64_t e = cb * blockDim.x + threadIdx.x; e < total; e += stride) {
     int i, j;
     if (small) {
       const uint32_t q = fd.div((uint32_t)e);
@@ -68,12 +66,55 @@ __global__ void __launch_bounds__(256) copy_tasks_kernel(const CopyTask* __restr
   }
 }
 
+// Rectangular grid (task, CTA within task): used when the tasks have similar
+// sizes (the rectangle wastes at most a few empty CTAs per task).
+template <int NP>
+__global__ void __launch_bounds__(256) copy_tasks_kernel(const CopyTask* __restrict__ tasks_g,
+                                                         const __grid_constant__ PList<CopyTask, NP> pl) {
+  const CopyTask t = NP > 1 ? pl.v[blockIdx.x] : tasks_g[blockIdx.x];
+  copy_task_elems(t, blockIdx.y, gridDim.y);
+}
+
+// Flattened grid: task k owns CTAs [cta0, cta0 + ncta).  Mixed batches (one
+// huge front buffer among 10^5 small blocks) would otherwise launch
+// ntasks x max-CTAs mostly empty CTAs (C5 level 8: seconds of empty CTA
+// scheduling).  Warp 0 finds the task by a 32-ary search over cta0.
+__global__ void __launch_bounds__(256) copy_tasks_flat_kernel(const CopyTask* __restrict__ tasks,
+                                                              int ntasks) {
+  __shared__ int s_task;
+  const int bid = (int)blockIdx.x;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int lo = 0, n = ntasks;   // invariant: tasks[lo].cta0 <= bid
+    while (n > 1) {
+      const int seg = (n + 31) / 32;
+      const int idx = lo + lane * seg;
+      const bool ok = lane * seg < n && tasks[idx].cta0 <= bid;
+      const unsigned msk = __ballot_sync(0xffffffffu, ok);
+      const int last = 31 - __clz(msk);
+      lo += last * seg;
+      n = min(seg, n - last * seg);
+    }
+    if (lane == 0) s_task = lo;
+  }
+  __syncthreads();
+  const CopyTask t = tasks[s_task];
+  copy_task_elems(t, bid - t.cta0, t.ncta);
+}
+
+// h_tasks carry cta0/ncta (set by the caller for the flattened grid);
+// total_ctas = their sum; max_elems = the largest task.
 void launch_copy(const CopyTask* d_tasks, const CopyTask* h_tasks, int ntasks, int64_t max_elems,
-                 cudaStream_t st) {
+                 int64_t total_ctas, cudaStream_t st) {
   if (ntasks <= 0) return;
   int64_t y = (max_elems + 256 * 8 - 1) / (256 * 8);
   if (y < 1) y = 1;
   if (y > 512) y = 512;
+  if (d_tasks != nullptr && total_ctas > 0 && (int64_t)ntasks * y > 4 * total_ctas + 4096) {
+    copy_tasks_flat_kernel<<<(unsigned)total_ctas, 256, 0, st>>>(d_tasks, ntasks);
+    SPQ_LAUNCH_CHECK();
+    return;
+  }
   // grid.x limit is 2^31-1; y <= 512 stays far below the 65535 limit
   dim3 grid((unsigned)ntasks, (unsigned)y);
   if (d_tasks == nullptr) {

@@ -1080,18 +1080,17 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
       break;
     }
     const int lp = (int)(bk >> 32), pp = (int)(bk & 0xffffffffu);
-    // ---- winner's column rows i..m-1 into vbuf (row i-1 no longer used)
-    {
-      const double* Xr = rx + (size_t)wr * L.rec + 2;
-      for (int a = i + tid; a < m; a += RG_NT) vbuf[a] = Xr[a];
-      if (tid == 0 && i > 0) vbuf[i - 1] = 0.0;
-    }
-    __syncthreads();
+    // ---- reflector straight from the winner's record in local shared
+    // memory (every warp redundantly: no CTA barrier).  The record's slot is
+    // overwritten only by pushes for step i + 2, which other CTAs issue after
+    // waiting for this CTA's step-(i+1) push, i.e. after every warp here
+    // passed publish()'s first barrier -- after these reads.
+    const double* Xr = rx + (size_t)wr * L.rec + 2;
     double sg = 0.0;
-    for (int a = i + 1 + lane; a < m; a += 32) sg = fma(vbuf[a], vbuf[a], sg);
+    for (int a = i + 1 + lane; a < m; a += 32) sg = fma(Xr[a], Xr[a], sg);
 #pragma unroll
     for (int o = 16; o; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
-    const double alpha = vbuf[i];
+    const double alpha = Xr[i];
     double tau, beta, v0 = 1.0;
     const bool zero = sg == 0.0;
     if (zero) {
@@ -1101,12 +1100,14 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
       v0 = (alpha <= 0.0) ? alpha - beta : -sg / (alpha + beta);
       tau = -v0 / beta;
     }
-    __syncthreads();   // every warp has read alpha / sigma from the raw column
+    // v once per row (the reference's division x / v0) into vbuf, zero at
+    // row i-1; the previous step's vbuf reads ended before publish()'s barriers
     for (int a = i + tid; a < m; a += RG_NT) {
-      const double va = (a == i) ? 1.0 : (zero ? 0.0 : vbuf[a] / v0);
+      const double va = (a == i) ? 1.0 : (zero ? 0.0 : Xr[a] / v0);
       vbuf[a] = va;
       if (q == 0) J.V[a + (int64_t)i * J.ldv] = va;
     }
+    if (tid == 0 && i > 0) vbuf[i - 1] = 0.0;
     if (q == 0 && tid == 0) { J.tau[i] = tau; J.beta[i] = beta; }
     __syncthreads();
     // ---- own columns: swap bookkeeping, update, norms over rows > i

@@ -1094,8 +1094,23 @@ struct CopyBatch {
   }
   void run(spq_ctx* c) {
     if (t.empty()) return;
-    Scope s(c, F_COPY);
-    launch_copy(up_or_param(c, t, PL_COPY), t.data(), (int)t.size(), maxe, c->st);
+    std::string tag;
+    if (Scope::scope_log()) {
+      double by = 0;
+      for (auto& x : t) by += (double)x.nr * x.nc * ((x.src && !x.ident) ? 16.0 : 8.0);
+      char b[160];
+      snprintf(b, sizeof b, "copy %s nt=%zu maxe=%lld gb=%.4f", c->stage, t.size(), (long long)maxe, by / 1e9);
+      tag = b;
+    }
+    Scope s(c, F_COPY, tag);
+    int64_t ctas = 0;   // flattened-grid assignment (used for mixed task sizes)
+    for (auto& x : t) {
+      const int64_t nb = std::min<int64_t>(512, std::max<int64_t>(1, ((int64_t)x.nr * x.nc + 2047) / 2048));
+      x.cta0 = (int)ctas;
+      x.ncta = (int)nb;
+      ctas += nb;
+    }
+    launch_copy(up_or_param(c, t, PL_COPY), t.data(), (int)t.size(), maxe, ctas, c->st);
     c->tm.launches[F_COPY]++;
     c->n_kernels++;
     double by = 0;
