@@ -919,9 +919,9 @@ __device__ __forceinline__ void rg_wait(uint32_t mbar, uint32_t parity) {
 struct RgLayout {   // shared memory in doubles; rows padded to mp = tpc * R
   int m1, cl, rec;  // rec = one candidate record: [value, key, column (m1)]
   __host__ __device__ RgLayout(int mp, int cl_) : m1(mp > 0 ? ((mp + 1) & ~1) : 2), cl(cl_), rec(m1 + 2) {}
-  // vbuf (m1) | SX [2][rec] | RX [2][cl][rec] | wv [RG_NW] | wk [RG_NW] | mbar [2]
+  // vbuf (m1) | ST [RG_NW][rec] | RX [2][cl][rec] | wv [RG_NW] | wk [RG_NW] | mbar [2]
   __host__ __device__ size_t sx() const { return (size_t)m1; }
-  __host__ __device__ size_t rx() const { return sx() + 2 * (size_t)rec; }
+  __host__ __device__ size_t rx() const { return sx() + (size_t)RG_NW * rec; }
   __host__ __device__ size_t wvo() const { return rx() + 2 * (size_t)cl * rec; }
   __host__ __device__ size_t bytes() const { return (wvo() + 2 * RG_NW + 2) * 8 + 64; }
 };
@@ -948,7 +948,7 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
   extern __shared__ __align__(16) double rs[];
   const RgLayout L(mp, CL);
   double* vbuf = rs;                         // v (zero outside rows i..m-1)
-  double* SX = rs + L.sx();                  // [2][rec] own candidate, staged for the push
+  double* ST = rs + L.sx();                  // [RG_NW][rec] every warp's candidate, staged for the push
   double* RX = rs + L.rx();                  // [2][CL][rec] every CTA's candidate
   double* wv = rs + L.wvo();                 // [RG_NW]
   unsigned long long* wk = reinterpret_cast<unsigned long long*>(wv + RG_NW);   // [RG_NW]
@@ -978,8 +978,13 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
   for (int a = tid; a < L.m1; a += RG_NT) vbuf[a] = 0.0;
   cluster.sync();   // barriers initialised and armed everywhere before the first push
 
-  // CTA argmax over every group's (norm, position); the owner group stages
-  // that column, then one thread pushes the record to every CTA
+  // Every warp stages its best candidate record [value, key, column] (the
+  // owner group writes the column); ONE CTA barrier; warp 0 picks the CTA
+  // winner among the RG_NW records and bulk-copies that record to every CTA
+  // (cp.async.bulk shared::cta -> shared::cluster on the destination's
+  // mbarrier), CL lanes issuing in parallel.  A staged record is rewritten
+  // only in the next step's publish, after the next step's vbuf barrier,
+  // which warp 0 reaches after its copies have read their source.
   auto publish = [&](double bv, unsigned long long bk, int slot) {
 #pragma unroll
     for (int o = 16; o >= tpc; o >>= 1) {    // lanes of a group agree already
@@ -987,41 +992,42 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
       const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
       if (rg_better(ov, ok, bv, bk)) { bv = ov; bk = ok; }
     }
-    if (lane == 0) { wv[warp] = bv; wk[warp] = bk; }
-    __syncthreads();
-    double cv = lane < RG_NW ? wv[lane] : -1.0;
-    unsigned long long ck = lane < RG_NW ? wk[lane] : rg_pack(0x7fffffff, 0);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {   // full warp: every lane must agree
-      const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, ck, o);
-      if (rg_better(ov, ok, cv, ck)) { cv = ov; ck = ok; }
-    }
-    double* sx = SX + slot * L.rec;
-    const int cph = (int)(ck & 0xffffffffu);
-    if (cv >= 0.0 && cph >= ph0 && cph < ph0 + C) {
+    double* st = ST + (size_t)warp * L.rec;
+    const int cph = (int)(bk & 0xffffffffu);
+    if (bv >= 0.0 && cph >= ph0 && cph < ph0 + C) {
 #pragma unroll
       for (int c = 0; c < C; ++c)
         if (ph0 + c == cph)
 #pragma unroll
-          for (int r = 0; r < R; ++r) sx[2 + sub + tpc * r] = x[c][r];
+          for (int r = 0; r < R; ++r) st[2 + sub + tpc * r] = x[c][r];
     }
-    if (tid == 0) { sx[0] = cv; sx[1] = __longlong_as_double((long long)ck); }
+    if (lane == 0) { st[0] = bv; st[1] = __longlong_as_double((long long)bk); }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk copy
     __syncthreads();
-    // one bulk copy per destination, issued by CL threads of warp 0 in
-    // parallel (serial issue from one thread put CL copy set-ups in a row on
-    // every pivot step's critical path)
-    if (tid < CL) {
-      const uint32_t src = rg_smem(sx);
-      const int d = tid;
-      const uint32_t dst = rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec), d);
-      const uint32_t mb = rg_mapa(rg_smem(&mbar[slot]), d);
-      asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes "
-                   "[%0], [%1], %2, [%3];" :: "r"(dst), "r"(src), "r"(rec_bytes), "r"(mb)
-                   : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
+    if (warp == 0) {
+      double cv = lane < RG_NW ? ST[(size_t)lane * L.rec] : -1.0;
+      unsigned long long ck = lane < RG_NW
+          ? (unsigned long long)__double_as_longlong(ST[(size_t)lane * L.rec + 1])
+          : rg_pack(0x7fffffff, 0);
+      int cw = lane < RG_NW ? lane : 0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {   // full warp: every lane must agree
+        const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
+        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, ck, o);
+        const int ow = __shfl_xor_sync(0xffffffffu, cw, o);
+        if (rg_better(ov, ok, cv, ck)) { cv = ov; ck = ok; cw = ow; }
+      }
+      if (lane < CL) {
+        const uint32_t src = rg_smem(ST + (size_t)cw * L.rec);
+        const int d = lane;
+        const uint32_t dst = rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec), d);
+        const uint32_t mb = rg_mapa(rg_smem(&mbar[slot]), d);
+        asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes "
+                     "[%0], [%1], %2, [%3];" :: "r"(dst), "r"(src), "r"(rec_bytes), "r"(mb)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
+      }
     }
   };
 

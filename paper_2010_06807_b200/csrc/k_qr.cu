@@ -347,6 +347,16 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
     for (int c = 0; c < QR_NB; ++c) sh.Xp[c] = a[0][c];
   }
   __syncthreads();
+  if (CL == 1) {   // single CTA: totals straight into shared memory, no DSMEM round trip
+    if (tid < QR_NB) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < QRR_NT / 32; ++w) s += sh.red[w][tid];
+      sh.dtot[tid] = s;
+      sh.apiv[tid] = sh.Xp[tid];
+    }
+    __syncthreads();
+  } else {
   // ---- push the CTA partials (and CTA 0's pivot row) to every CTA
   for (int t = tid; t < QR_NB * CL; t += QRR_NT) {
     const int dst = t >> 5, c = t & 31;
@@ -373,6 +383,7 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
     }
   }
   __syncthreads();
+  }
   // ---- reflector scalars (every thread, identical inputs)
   const double sigma = sh.dtot[jj];
   const double alpha = sh.apiv[jj];
