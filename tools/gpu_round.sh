@@ -15,4 +15,8 @@ CMD1="python tools/run_config.py C3 - 1"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_dmma2 -s 20 -c 1 -o $O/gemm $CMD1 > $O/ncu_gemm.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:wyf -s 100 -c 1 -o $O/wyf $CMD1 > $O/ncu_wyf.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:copy_tasks -s 200 -c 1 -o $O/copy $CMD1 > $O/ncu_copy.log 2>&1
-echo done >> $O/ncu_copy.log
+
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:cpqr_reg -s 60 -c 1 -o $O/cpqr $CMD1 > $O/ncu_cpqr.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:panel_qr_reg -s 200 -c 1 -o $O/panel $CMD1 > $O/ncu_panel.log 2>&1
+SPQ_SCOPE_LOG=$O/c3_scopes.txt timeout 300 python tools/c3_timeline.py C3 > $O/c3tl.log 2>&1
+echo done >> $O/ncu_panel.log
