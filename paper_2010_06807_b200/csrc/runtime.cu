@@ -2891,8 +2891,28 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
       ncols[t].insert(ncols[t].end(), c->cols_of[k].begin(), c->cols_of[k].end());
     }
   }
+  // old blocks in ascending (i, j) key order: the row adjacency lists are
+  // sorted by column and carry the block pointers, so walking rows in
+  // ascending id yields the sorted key list without a sort.  Any mismatch
+  // with the map (a list entry without its block) falls back to sorting.
+  std::vector<std::pair<uint64_t, Block*>> keys;   // (key, block): no lookups below
+  keys.reserve(c->blk.size());
+  for (int i = 0; i < c->ncl; ++i) {
+    const FlatSet& row = c->rix[i];
+    for (size_t t = 0; t < row.v.size(); ++t) keys.push_back({bkey(i, row.v[t]), row.b[t]});
+  }
+  bool walk_ok = keys.size() == c->blk.size();
+  for (size_t t = 0; walk_ok && t < keys.size(); ++t) walk_ok = keys[t].second != nullptr;
   BlockMap old;
   old.swap(c->blk);
+  if (!walk_ok) {
+    keys.clear();
+    old.for_each([&](uint64_t key, Block& B) { keys.push_back({key, &B}); });
+    std::sort(keys.begin(), keys.end(),
+              [](const std::pair<uint64_t, Block*>& x, const std::pair<uint64_t, Block*>& y) {
+                return x.first < y.first;
+              });
+  }
   for (int s = 0; s < c->ncl; ++s) {
     if (c->active[s]) { c->rows_of[s].clear(); c->cols_of[s].clear(); }
     c->active[s] = 0;
@@ -2906,14 +2926,6 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
     c->active[P] = 1;
   }
   CopyBatch zeros, cp;
-  // deterministic order: sort old keys
-  std::vector<std::pair<uint64_t, Block*>> keys;   // (key, block): no lookups below
-  keys.reserve(old.size());
-  old.for_each([&](uint64_t key, Block& B) { keys.push_back({key, &B}); });
-  std::sort(keys.begin(), keys.end(),
-            [](const std::pair<uint64_t, Block*>& x, const std::pair<uint64_t, Block*>& y) {
-              return x.first < y.first;
-            });
   // parent blocks needed, grouped by parent row: one zeroed allocation per row
   std::vector<std::vector<int>> prow_v(c->ncl);   // Pi -> Pj list
   for (auto& kb : keys) {
