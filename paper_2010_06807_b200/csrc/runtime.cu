@@ -528,6 +528,7 @@ struct GlobalCache {
   std::vector<std::pair<void*, size_t>> slabs;   // (ptr, bytes)
   Arena arena;
   std::vector<std::pair<char*, char*>> rings;    // (pinned, device) of RING_BYTES
+  std::vector<int*> spec_flags;                  // mapped pinned ints of closed contexts
   int n_ctx = 0;                                 // live contexts (1 => frees reusable at once)
 };
 GlobalCache& gcache() {
@@ -3473,10 +3474,13 @@ int spq_create(spq_ctx** out, int device) {
   int rc = guarded(c, [&] {
     c->dev = device;
     CUDA_TRY(cudaSetDevice(device));
-    cudaDeviceProp p;
-    CUDA_TRY(cudaGetDeviceProperties(&p, device));
-    if (p.major < 10) throw SpqError(SPQ_ERR_CUDA, "sm_100a device required");
-    c->nsm = p.multiProcessorCount;
+    // two attribute queries (cudaGetDeviceProperties fills the whole struct:
+    // milliseconds per context)
+    int major = 0, nsm = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    if (major < 10) throw SpqError(SPQ_ERR_CUDA, "sm_100a device required");
+    c->nsm = nsm;
     CUDA_TRY(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     cudaMemPool_t pool;
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -3499,7 +3503,16 @@ int spq_create(spq_ctx** out, int device) {
       CUDA_TRY(cudaMalloc(&c->dring, c->ring_cap));
     }
     c->spec = !env_flag("SPQ_NO_SPEC");
-    CUDA_TRY(cudaHostAlloc(&c->h_spec_bad, sizeof(int), cudaHostAllocMapped));
+    {   // mapped speculation flag, reused across contexts (pinned allocations
+        // and their frees cost milliseconds and cudaFreeHost synchronizes)
+      auto& g = gcache();
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (!g.spec_flags.empty()) {
+        c->h_spec_bad = g.spec_flags.back();
+        g.spec_flags.pop_back();
+      }
+    }
+    if (!c->h_spec_bad) CUDA_TRY(cudaHostAlloc(&c->h_spec_bad, sizeof(int), cudaHostAllocMapped));
     *c->h_spec_bad = 0;
     CUDA_TRY(cudaHostGetDevicePointer(&c->d_spec_bad, c->h_spec_bad, 0));
   });
@@ -3540,7 +3553,12 @@ void spq_destroy(spq_ctx* c) {
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->st) cudaStreamDestroy(c->st);
-    if (c->h_spec_bad) cudaFreeHost(c->h_spec_bad);
+    if (c->h_spec_bad) {   // every stream of the context is drained: back to the pool
+      auto& g = gcache();
+      std::lock_guard<std::mutex> lk(g.mu);
+      g.spec_flags.push_back(c->h_spec_bad);
+      c->h_spec_bad = nullptr;
+    }
   } catch (...) {
   }
   delete c;
