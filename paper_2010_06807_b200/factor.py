@@ -290,16 +290,17 @@ class _StateView:
 
 
 def _cluster_lists(clusters, attr):
-    ptr = np.zeros(len(clusters) + 1, np.int64)
+    """CSR-style (ptr, values) of the clusters' row or column index lists
+    (one concatenate: a per-cluster conversion loop cost ~2 ms per call at C3)."""
     vals = []
-    for i, c in enumerate(clusters):
+    for c in clusters:
         a = getattr(c, attr)
-        if a is None:
-            a = c.cols
-        a = np.asarray(a, np.int64)
-        vals.append(a)
-        ptr[i + 1] = ptr[i] + len(a)
-    return ptr, (np.concatenate(vals) if vals else np.zeros(0, np.int64))
+        vals.append(c.cols if a is None else a)
+    ptr = np.zeros(len(vals) + 1, np.int64)
+    if not vals:
+        return ptr, np.zeros(0, np.int64)
+    np.cumsum([len(a) for a in vals], out=ptr[1:])
+    return ptr, np.concatenate(vals).astype(np.int64, copy=False)
 
 
 def factorize(A, tree=None, eps=1e-3, **kw):
