@@ -529,6 +529,8 @@ struct GlobalCache {
   Arena arena;
   std::vector<std::pair<char*, char*>> rings;    // (pinned, device) of RING_BYTES
   std::vector<int*> spec_flags;                  // mapped pinned ints of closed contexts
+  std::vector<cudaEvent_t> events;               // timing events of closed contexts
+  int events_dev = -1;                           // device those events belong to
   int n_ctx = 0;                                 // live contexts (1 => frees reusable at once)
 };
 GlobalCache& gcache() {
@@ -3511,6 +3513,7 @@ int spq_create(spq_ctx** out, int device) {
         c->h_spec_bad = g.spec_flags.back();
         g.spec_flags.pop_back();
       }
+      if (g.events_dev == device) c->ev_pool.swap(g.events);
     }
     if (!c->h_spec_bad) CUDA_TRY(cudaHostAlloc(&c->h_spec_bad, sizeof(int), cudaHostAllocMapped));
     *c->h_spec_bad = 0;
@@ -3529,8 +3532,20 @@ void spq_destroy(spq_ctx* c) {
   try {
     if (c->side) cudaStreamSynchronize(c->side);
     if (c->st) cudaStreamSynchronize(c->st);
+    // scope events go back to the process pool (the streams are drained:
+    // every recorded event has completed); the next context reuses them
+    // instead of creating ~5000 events per factorization
     for (int f = 0; f < F_NFAM; ++f)
-      for (auto& e : c->tm.ev[f]) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+      for (auto& e : c->tm.ev[f]) { c->ev_pool.push_back(e.first); c->ev_pool.push_back(e.second); }
+    {
+      auto& g = gcache();
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (g.events.empty()) g.events_dev = c->dev;
+      while (!c->ev_pool.empty() && g.events_dev == c->dev && g.events.size() < ((size_t)1 << 16)) {
+        g.events.push_back(c->ev_pool.back());
+        c->ev_pool.pop_back();
+      }
+    }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->st) cudaStreamSynchronize(c->st);
     for (void* p : c->big) c->big_pending.push_back(p);
