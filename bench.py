@@ -38,7 +38,15 @@ sys.path.insert(0, ROOT)
 
 METRIC = "spaQR factor time + batched-QR fp64 GFLOP/s (% roofline), 2D N=256^2, 1 B200"
 UNIT = "factorizations/s"
-WORKLOAD = "C3: 2D var-coef upwind conv-diff 256^2 (N=65536), L=10, eps=1e-3, scaled sparsification"
+WORKLOADS = {
+    "C1": "C1: 2D upwind conv-diff 64^2 (N=4096), beta=(20,20), L=6, eps=1e-2",
+    "C3": "C3: 2D var-coef upwind conv-diff 256^2 (N=65536), L=10, eps=1e-3, scaled sparsification",
+    "C4": "C4: 3D upwind conv-diff 32^3 (N=32768), beta=(10,10,10), L=9, eps=1e-2",
+    "C5": "C5: 3D var-coef upwind conv-diff 64^3 (N=262144), L=11, eps=1e-2",
+    "C2": "C2: batched QR+Q^T apply of 4096 blocks (m~U{32..256}, k~U{16..128}, k<=m) and "
+          "batched threshold RRQR of 4096 64x192 blocks at eps 1e-2 and 1e-4",
+}
+WORKLOAD = WORKLOADS["C3"]
 
 
 def parse():
@@ -47,9 +55,25 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
+
+
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: re-run this script under torchrun with N
+    ranks (one process per GPU, rendezvous on 127.0.0.1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def dist_setup(n):
@@ -63,6 +87,14 @@ def dist_setup(n):
         dist.init_process_group("nccl" if os.environ.get("SPQ_BENCH_BACKEND") != "gloo" else "gloo")
         pg = dist
     return rank, world, local, pg
+
+
+def config_dict(cfg, A, tree, eps, world):
+    """The workload description, identical in both arms."""
+    d = {"workload": WORKLOADS[cfg], "config": cfg, "N": int(A.ncols), "levels": int(tree.L),
+         "eps": eps, "parallelism": f"replicas x{world}" if world > 1 else "single device",
+         "l2": "256 MB buffer written between timed steps (L2 flush)"}
+    return d
 
 
 def problem(cfg):
@@ -191,7 +223,7 @@ def cpu_baseline(A, tree, eps, budget_s=30.0):
     O.factorize(A, tree, eps=eps)
     dt = time.perf_counter() - t0
     return {"value": 1.0 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"1 full {WORKLOAD.split(':')[0]} factorization by oracle/spaqr_oracle.py "
+            "sample": f"1 full factorization of the same workload by oracle/spaqr_oracle.py "
                       f"({dt:.1f} s, numpy/OpenBLAS threads={os.cpu_count()})",
             "seconds_per_factorization": dt}
 
@@ -219,16 +251,126 @@ def run_reference(args, rank, world):
             "steps_run": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD, "parallelism": "host cores"},
+            "config": config_dict(args.config, A, tree, eps, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                              "sample": f"{len(times)} full factorizations by the CPU oracle"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     return line
 
 
+def run_c2(args, rank, world, local, dist):
+    """BASELINE config 2: the isolated batched kernels (one step = batched QR +
+    Q^T apply of the 4096 QR blocks, then batched threshold RRQR of the 4096
+    RRQR blocks at eps 1e-2 and at 1e-4).  value = algorithmic GFLOP/s of the
+    step (SURVEY §8d counts) from device time; e2e = the same through the
+    host-buffer C-ABI calls (H2D + D2H inside)."""
+    from paper_2010_06807_b200.batched import batched_qr, batched_rrqr, config2_inputs
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle import spaqr_oracle as O
+        Bs, Cs, Ms = config2_inputs(n_qr=256, n_rrqr=256)
+        fl = c2_flops(Bs, Cs, None)
+        t0 = time.perf_counter()
+        fl_rr = 0.0
+        for B, Cc in zip(Bs, Cs):
+            V, tau, R = O.house_qr(B)
+            O.wy_apply(V, O.larft(V, tau), Cc, True)
+        for eps in (1e-2, 1e-4):
+            for M in Ms:
+                r = O.rrqr_threshold(M, eps)["rank"]
+                fl_rr += 4 * 64 * 192 * r - 2 * r * r * (64 + 192) + 4 * r ** 3 / 3
+        dt = time.perf_counter() - t0
+        v = (fl + fl_rr) / dt / 1e9
+        line = {"metric": "config-2 batched QR+apply / RRQR fp64 GFLOP/s", "value": v,
+                "unit": "GFLOP/s", "n_gpus": world, "steps": 1, "warmup": 0,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": WORKLOADS["C2"], "config": "C2"},
+                "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": os.cpu_count(),
+                                 "kind": "port", "sample": "256 QR + 2x256 RRQR blocks"},
+                "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    Bs, Cs, Ms = config2_inputs()
+    peak64 = fp64_peak_tflops()
+    fl_qr = c2_flops(Bs, Cs, None)
+    for _ in range(max(args.warmup, 0)):
+        batched_qr(Bs, Cs)
+        for eps in (1e-2, 1e-4):
+            batched_rrqr(Ms, eps)
+    dev = {"qr": 0.0, "rrqr_1e-2": 0.0, "rrqr_1e-4": 0.0}
+    fl = {"qr": fl_qr, "rrqr_1e-2": 0.0, "rrqr_1e-4": 0.0}
+    wall = 0.0
+    ranks = {}
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    with clocks:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            _, _, ms = batched_qr(Bs, Cs)
+            dev["qr"] += ms
+            for eps in (1e-2, 1e-4):
+                rk, _, ms = batched_rrqr(Ms, eps)
+                key = f"rrqr_{eps:g}"
+                dev[key] += ms
+                fl[key] = float(sum(4 * 64 * 192 * r - 2 * r * r * (64 + 192) + 4 * r ** 3 / 3
+                                    for r in rk))
+                ranks[key] = [int(rk.min()), int(np.median(rk)), int(rk.max())]
+            wall += time.perf_counter() - t0
+    torch.cuda.synchronize()
+    T = sum(dev.values())
+    T, wall = reduce_max([T, wall], dist)
+    if rank != 0:
+        return
+    total = (fl["qr"] + fl["rrqr_1e-2"] + fl["rrqr_1e-4"]) * args.steps * world
+    value = total / (T * 1e-3) / 1e9
+    kern = {}
+    for k in dev:
+        ach = fl[k] * args.steps / (dev[k] * 1e-3) / 1e12 if dev[k] else 0.0
+        kern[k] = {"ms_per_step": dev[k] / args.steps, "gflop_per_step": fl[k] / 1e9,
+                   "achieved_tflops": ach, "frac_fp64_peak": ach / peak64}
+    dom = max(dev, key=dev.get)
+    in_bytes = 8 * (sum(b.size for b in Bs) + 2 * sum(c.size for c in Cs) + 2 * Ms.size)
+    line = {"metric": "config-2 batched QR+apply / RRQR fp64 GFLOP/s", "value": value,
+            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": T / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS["C2"], "config": "C2", "n_qr": len(Bs),
+                       "n_rrqr": int(Ms.shape[0]),
+                       "l2": "inputs 0.75 GB per step > 126 MB L2"},
+            "kernels": kern, "ranks": ranks,
+            "roofline": {"bound": "fp64", "achieved": kern[dom]["achieved_tflops"],
+                         "peak": peak64, "unit": "TFLOP/s",
+                         "frac": kern[dom]["frac_fp64_peak"], "traffic": None,
+                         "kernel_family": dom,
+                         "peak_source": "measured cuBLAS DGEMM 8192^3 on this box"},
+            "e2e": {"value": total / wall / 1e9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": int(in_bytes // 2)},
+            "fp64_peak_tflops_measured": peak64, "clocks": clocks.summary()}
+    print(json.dumps(line), flush=True)
+
+
+def c2_flops(Bs, Cs, _):
+    f = 0.0
+    for b, c in zip(Bs, Cs):
+        m, k = b.shape
+        n = c.shape[1]
+        f += 2 * m * k * k - 2 * k ** 3 / 3 + 4 * m * n * k - n * k * k
+    return f
+
+
 def main():
     args = parse()
+    spawn_ranks(args)
     rank, world, local, dist = dist_setup(args.gpus)
+    if args.config == "C2":
+        return run_c2(args, rank, world, local, dist)
     if args.impl == "reference":
         line = run_reference(args, rank, world)
         if line is not None:
@@ -256,6 +398,7 @@ def main():
         torch.cuda.synchronize()
 
     dev_ms, e2e_ms = [], []
+    spec_retries = 0
     agg = {}
     launches = 0
     barrier()
@@ -271,6 +414,7 @@ def main():
             torch.cuda.synchronize()
             e2e_ms.append(e0.elapsed_time(e1))
             dev_ms.append(F.device_ms)
+            spec_retries += int(getattr(F, "spec_retries", 0))
             tm = F.device_timings()
             host = tm.pop("host")
             launches += int(host.get("kernels", 0))
@@ -342,9 +486,11 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": T / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "N": int(A.ncols), "levels": int(tree.L), "eps": eps,
-                   "parallelism": f"replicas x{world}",
-                   "l2": "256 MB buffer written between timed steps (L2 flush)"},
+        "config": config_dict(args.config, A, tree, eps, world),
+        "timed_region": "device: mark before spq_load (CSC upload, equilibration, block scatter "
+                        "included) -> end of spq_finish; e2e: the public factorize(A_host, tree) "
+                        "call",
+        "spec_retries": spec_retries,
         "factor_time_s": T / args.steps / 1e3,
         "step_ms": [round(float(x), 3) for x in dev_ms],
         "batched_qr_gflops": bqr,
@@ -358,7 +504,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.config in ("C1", "C3"):
         line["cpu_baseline"] = cpu_baseline(A, tree, eps)
     print(json.dumps(line), flush=True)
     if dist is not None:

@@ -262,6 +262,7 @@ class RecSparsify:
         self.rows, self.cols, self.panel, self.rank = rows, cols, panel, rank
 
     payload = property(lambda s: s.panel.size)
+    q_panel = property(lambda s: s.panel)
 
     def qt(self, z):
         z[self.rows] = _apply(self.panel, z[self.rows], True)

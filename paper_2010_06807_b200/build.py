@@ -15,7 +15,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libspaqr_b200.so")
-SOURCES = ["k_copy.cu", "k_gemm.cu", "k_qr.cu", "k_cpqr.cu", "k_chain.cu", "runtime.cu", "hostprof.cu", "k_krylov.cu", "k_wyf.cu"]
+SOURCES = ["k_copy.cu", "k_gemm.cu", "k_qr.cu", "k_cpqr.cu", "k_chain.cu", "runtime.cu", "k_krylov.cu",
+           "k_wyf.cu"]
+# diagnostic host sampling profiler (tools/hostprof.cu): linked in only when
+# SPQ_BUILD_HOSTPROF=1, never part of the shipped library
+EXTRA = ([os.path.join(os.path.dirname(HERE), "tools", "hostprof.cu")]
+         if os.environ.get("SPQ_BUILD_HOSTPROF") == "1" else [])
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-g", "-Xcompiler", "-fno-omit-frame-pointer",
@@ -42,14 +47,14 @@ def build(force=False, verbose=False):
     cflags = [f for f in FLAGS if f != "-shared"]
 
     def compile_one(src):
-        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
         cmd = [NVCC, *cflags, "-c", "-o", obj, os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd), flush=True)
         return obj, subprocess.run(cmd, capture_output=True, text=True)
 
-    with ThreadPoolExecutor(len(SOURCES)) as ex:
-        results = list(ex.map(compile_one, SOURCES))
+    with ThreadPoolExecutor(len(SOURCES) + len(EXTRA)) as ex:
+        results = list(ex.map(compile_one, SOURCES + EXTRA))
     for obj, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

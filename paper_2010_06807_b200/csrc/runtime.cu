@@ -533,13 +533,21 @@ struct GlobalCache {
   int events_dev = -1;                           // device those events belong to
   int n_ctx = 0;                                 // live contexts (1 => frees reusable at once)
 };
-GlobalCache& gcache() {
-  static GlobalCache* g = new GlobalCache();   // leaked on purpose (process lifetime)
-  return *g;
+// One cache per device: slabs, arena ranges, rings, mapped flags and events
+// belong to the device they were allocated on, and a context only ever draws
+// from its own device's cache.
+constexpr int kMaxDevices = 64;
+GlobalCache& gcache(int dev) {
+  static std::mutex mu;
+  static GlobalCache* g[kMaxDevices] = {};   // leaked on purpose (process lifetime)
+  if (dev < 0 || dev >= kMaxDevices) throw SpqError(SPQ_ERR_BAD_INPUT, "device ordinal out of range");
+  std::lock_guard<std::mutex> lk(mu);
+  if (!g[dev]) g[dev] = new GlobalCache();
+  return *g[dev];
 }
 
-size_t arena_free_bytes() {
-  auto& g = gcache();
+size_t arena_free_bytes(int dev) {
+  auto& g = gcache(dev);
   std::lock_guard<std::mutex> lk(g.mu);
   size_t t = 0;
   for (auto& kv : g.arena.free_off) t += kv.second;
@@ -585,7 +593,7 @@ constexpr size_t BIG_ALLOC = (size_t)8 << 20;   // >= 8 MB: driver stream-ordere
   cudaMemGetInfo(&fr, &tot);
   size_t afree = 0, alarge = 0, anfree = 0;
   {
-    auto& g = gcache();
+    auto& g = gcache(c->dev);
     std::lock_guard<std::mutex> lk(g.mu);
     for (auto& kv : g.arena.free_off) { afree += kv.second; alarge = std::max(alarge, kv.second); ++anfree; }
   }
@@ -598,7 +606,7 @@ constexpr size_t BIG_ALLOC = (size_t)8 << 20;   // >= 8 MB: driver stream-ordere
            "(%.2f GB in free lists), arena %.2f GB with %.2f GB free in %zu ranges (largest %.3f GB), "
            "device free %.2f of %.2f GB, stage %s",
            what, bytes * G, c->live_bytes * G, c->peak_bytes * G, c->pool_bytes * G,
-           pooled_free * G, gcache().arena.cap * G, afree * G, anfree, alarge * G, fr * G, tot * G,
+           pooled_free * G, gcache(c->dev).arena.cap * G, afree * G, anfree, alarge * G, fr * G, tot * G,
            c->stage);
   throw spq::CudaFailure(cudaErrorMemoryAllocation, buf, __FILE__, __LINE__);
 }
@@ -617,7 +625,7 @@ size_t reclaim_slabs(spq_ctx* c) {
   bool any = false;
   for (size_t i = 0; i < c->slabs.size(); ++i)
     if (c->slabs[i] && c->slab_live[i] == 0) { dead[i] = 1; any = true; }
-  auto& g = gcache();
+  auto& g = gcache(c->dev);
   {
     std::lock_guard<std::mutex> lk(g.mu);
     any = any || !g.slabs.empty();
@@ -686,7 +694,7 @@ double* dalloc(spq_ctx* c, size_t bytes) {
     void* p = nullptr;
     size_t got = 0;
     {
-      auto& g = gcache();
+      auto& g = gcache(c->dev);
       std::lock_guard<std::mutex> lk(g.mu);
       ensure_arena(g);
       if (g.arena.base) {
@@ -695,7 +703,7 @@ double* dalloc(spq_ctx* c, size_t bytes) {
       }
     }
     if (!p && reclaim_slabs(c) > 0) {   // empty pool slabs back to the arena, retry
-      auto& g = gcache();
+      auto& g = gcache(c->dev);
       std::lock_guard<std::mutex> lk(g.mu);
       p = g.arena.alloc(bytes);
       if (p) got = g.arena.size_of(p);
@@ -726,7 +734,7 @@ double* dalloc(spq_ctx* c, size_t bytes) {
       void* s = nullptr;
       for (int attempt = 0; attempt < 2 && !s; ++attempt) {
         if (attempt == 1 && reclaim_slabs(c) == 0) break;
-        auto& g = gcache();
+        auto& g = gcache(c->dev);
         std::lock_guard<std::mutex> lk(g.mu);
         for (size_t i = 0; i < g.slabs.size(); ++i)
           if (g.slabs[i].second >= cap) {
@@ -771,7 +779,7 @@ double* dalloc_flex(spq_ctx* c, size_t want, size_t floor, size_t* got) {
     return dalloc(c, *got);
   }
   {
-    auto& g = gcache();
+    auto& g = gcache(c->dev);
     for (int attempt = 0; attempt < 2; ++attempt) {
       if (attempt == 1 && reclaim_slabs(c) == 0) break;
       std::lock_guard<std::mutex> lk(g.mu);
@@ -810,7 +818,7 @@ void dfree(spq_ctx* c, void* p) {
       // sole context: all device work is ordered on its one stream, so the
       // range can be handed out again at once (stream-ordered reuse);
       // otherwise it is published at this context's next stream sync
-      auto& g = gcache();
+      auto& g = gcache(c->dev);
       std::lock_guard<std::mutex> lk(g.mu);
       if (g.n_ctx <= 1 && g.arena.owns(p)) {
         g.arena.release(p);
@@ -852,7 +860,7 @@ double* shared_alloc(spq_ctx* c, size_t elems, int nref) {
 
 void publish_big(spq_ctx* c) {
   if (c->big_pending.empty()) return;
-  auto& g = gcache();
+  auto& g = gcache(c->dev);
   std::lock_guard<std::mutex> lk(g.mu);
   for (void* p : c->big_pending) {
     if (g.arena.owns(p)) g.arena.release(p);
@@ -1622,6 +1630,15 @@ void pivot_launch(spq_ctx* c, PivotSet& ps) {
   c->n_kernels++;
 }
 
+// after a stream sync: raise SPQ_ERR_SPECULATION if the device found a
+// predicted row flag wrong (speculative mode only)
+void spec_raise(spq_ctx* c) {
+  if (c->spec && c->h_spec_bad && *c->h_spec_bad)
+    throw SpqError(SPQ_ERR_SPECULATION, std::to_string(*c->h_spec_bad) +
+                   " predicted row flags differed from the device values; "
+                   "re-run with speculation off");
+}
+
 void pivot_raise(spq_ctx* c, PivotSet& ps) {
   if (ps.jobs.empty()) return;
   HostTimer ht(&c->host_ms[12]);
@@ -1633,6 +1650,9 @@ void pivot_raise(spq_ctx* c, PivotSet& ps) {
   CUDA_TRY(cudaMemcpyAsync(val.data(), c->d_err_val, n * sizeof(double), cudaMemcpyDeviceToHost,
                            c->st));
   sync(c);
+  // a pivot failure that follows a wrong row-flag prediction is an artefact
+  // of the speculation: report that first, so the host retries exactly
+  spec_raise(c);
   for (int i = 0; i < n; ++i)
     if (idx[i] >= 0) throw SpqError(SPQ_ERR_SINGULAR, ps.ctx[i], idx[i], val[i]);
   ps.jobs.clear();
@@ -3291,7 +3311,7 @@ void build_chain_W(spq_ctx* c) {
   if (need == 0 || env_flag("SPQ_CHAIN_NO_W")) return;
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  if (need * sizeof(double) * 3 > fr + arena_free_bytes()) return;
+  if (need * sizeof(double) * 3 > fr + arena_free_bytes(c->dev)) return;
   CopyBatch cp;
   GemmBatch gT, gN;
   std::vector<double*> tts;
@@ -3489,9 +3509,11 @@ int spq_create(spq_ctx** out, int device) {
     uint64_t thr = UINT64_MAX;
     CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     c->ring_cap = env_flag("SPQ_RING_SMALL") ? (1u << 16) : (64u << 20);
+    bool others_live = false;
     {
-      auto& g = gcache();
+      auto& g = gcache(c->dev);
       std::lock_guard<std::mutex> lk(g.mu);
+      others_live = g.n_ctx > 0;
       ++g.n_ctx;
       c->counted = true;
       if (!g.rings.empty() && !env_flag("SPQ_RING_SMALL")) {
@@ -3500,6 +3522,12 @@ int spq_create(spq_ctx** out, int device) {
         g.rings.pop_back();
       }
     }
+    // A sole live context hands freed arena ranges back at once, ordered only
+    // by its own stream (dfree).  Once this context is counted, the others
+    // defer their frees to a stream sync; ranges they released before that
+    // may still be read by their queued kernels, so drain the device once
+    // before this context can allocate any of them.
+    if (others_live) CUDA_TRY(cudaDeviceSynchronize());
     if (!c->pin) {
       CUDA_TRY(cudaMallocHost(&c->pin, c->ring_cap));
       CUDA_TRY(cudaMalloc(&c->dring, c->ring_cap));
@@ -3507,7 +3535,7 @@ int spq_create(spq_ctx** out, int device) {
     c->spec = !env_flag("SPQ_NO_SPEC");
     {   // mapped speculation flag, reused across contexts (pinned allocations
         // and their frees cost milliseconds and cudaFreeHost synchronizes)
-      auto& g = gcache();
+      auto& g = gcache(c->dev);
       std::lock_guard<std::mutex> lk(g.mu);
       if (!g.spec_flags.empty()) {
         c->h_spec_bad = g.spec_flags.back();
@@ -3515,7 +3543,8 @@ int spq_create(spq_ctx** out, int device) {
       }
       if (g.events_dev == device) c->ev_pool.swap(g.events);
     }
-    if (!c->h_spec_bad) CUDA_TRY(cudaHostAlloc(&c->h_spec_bad, sizeof(int), cudaHostAllocMapped));
+    if (!c->h_spec_bad)
+      CUDA_TRY(cudaHostAlloc(&c->h_spec_bad, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
     *c->h_spec_bad = 0;
     CUDA_TRY(cudaHostGetDevicePointer(&c->d_spec_bad, c->h_spec_bad, 0));
   });
@@ -3538,7 +3567,7 @@ void spq_destroy(spq_ctx* c) {
     for (int f = 0; f < F_NFAM; ++f)
       for (auto& e : c->tm.ev[f]) { c->ev_pool.push_back(e.first); c->ev_pool.push_back(e.second); }
     {
-      auto& g = gcache();
+      auto& g = gcache(c->dev);
       std::lock_guard<std::mutex> lk(g.mu);
       if (g.events.empty()) g.events_dev = c->dev;
       while (!c->ev_pool.empty() && g.events_dev == c->dev && g.events.size() < ((size_t)1 << 16)) {
@@ -3555,7 +3584,7 @@ void spq_destroy(spq_ctx* c) {
     for (auto& P : c->prog)
       for (auto& kv : P.graphs) cudaGraphExecDestroy(kv.second);
     {
-      auto& g = gcache();
+      auto& g = gcache(c->dev);
       std::lock_guard<std::mutex> lk(g.mu);
       for (size_t i = 0; i < c->slabs.size(); ++i)
         if (c->slabs[i]) g.slabs.push_back({c->slabs[i], c->slab_caps[i]});
@@ -3569,7 +3598,7 @@ void spq_destroy(spq_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->st) cudaStreamDestroy(c->st);
     if (c->h_spec_bad) {   // every stream of the context is drained: back to the pool
-      auto& g = gcache();
+      auto& g = gcache(c->dev);
       std::lock_guard<std::mutex> lk(g.mu);
       g.spec_flags.push_back(c->h_spec_bad);
       c->h_spec_bad = nullptr;
@@ -3635,6 +3664,8 @@ int spq_finish(spq_ctx* c) {
     pivot_raise(c, c->piv);
     for (int64_t j = 0; j < c->N; ++j)
       if (c->row_of_col[j] < 0) {
+        sync(c);
+        spec_raise(c);
         int64_t miss = 0;
         for (int64_t t = 0; t < c->N; ++t) miss += c->row_of_col[t] < 0;
         throw SpqError(SPQ_ERR_BAD_INPUT, std::to_string(miss) + " columns were never factored (inconsistent tree?)");
@@ -3663,10 +3694,7 @@ int spq_finish(spq_ctx* c) {
     build_full_T(c, tp);
     c->finished = true;
     sync(c);
-    if (*c->h_spec_bad)
-      throw SpqError(SPQ_ERR_SPECULATION, std::to_string(*c->h_spec_bad) +
-                     " predicted row flags differed from the device values; "
-                     "re-run with speculation off");
+    spec_raise(c);
   });
 }
 

@@ -10,9 +10,14 @@ Outputs (committed, small):
   kernels.npz   known-answer cases for qr_house / rrqr_threshold / tri_solve
                 (reference `kernels/__init__.py:147-233`, numba backend)
   factor_<case>.npz  per-case factorization results: per-level stats, the
-                per-interface rank sequence, row_of_col, diag(R_ss) of every
-                elimination record, full R_ss of a few records, GMRES history;
-                plus the numpy-backend R_ss divergence envelope per level (F3)
+                per-interface rank sequence, row_of_col; diag(R_ss), max|R_sn|
+                and ||R_sn||_F of every elimination record, full R_ss / R_sn of
+                picked records; diag(R_pp) of every interface scaling, full R_pp
+                of picks; rank and tau of every sparsifier, V/T of picks (and
+                R_ff / R_fc / H_f tau in the unscaled branch); the reference's
+                own apply_qt / solve_w / apply_w of a seeded vector; GMRES
+                history; plus the numpy-backend divergence envelope of every
+                one of those quantities, per record
   trees.json    tree digests of the reference's partition_geometric per config
 --big adds the full C3 (256^2) and C4 (32^3) runs (minutes of CPU).
 """
@@ -40,13 +45,23 @@ from paper_2010_06807_b200.ordering import tree_digest         # noqa: E402
 from paper_2010_06807_b200.problems import make_config         # noqa: E402
 
 CASES = {
-    # name: (config, n override)
-    "C1_n24": ("C1", 24),
-    "C1": ("C1", None),
-    "C3_n48": ("C3", 48),
-    "C4_n12": ("C4", 12),
+    # name: (config, n override, factorize options)
+    "C1_n24": ("C1", 24, {}),
+    "C1": ("C1", None, {}),
+    "C3_n48": ("C3", 48, {}),
+    "C4_n12": ("C4", 12, {}),
+    # the unscaled sparsification branch and alternating scaling
+    # (factor.py:557-566, 660-709, 849-850)
+    "C1_unscaled": ("C1", None, {"mode": "unscaled"}),
+    "C3_n48_unscaled": ("C3", 48, {"mode": "unscaled"}),
+    "C1_se2": ("C1", None, {"scale_every": 2}),
+    "C3_n48_se2": ("C3", 48, {"scale_every": 2}),
+    "C4_n12_unscaled": ("C4", 12, {"mode": "unscaled"}),
+    "C3_n96_unscaled": ("C3", 96, {"mode": "unscaled"}),
+    "C3_n96_se2": ("C3", 96, {"scale_every": 2}),
 }
-BIG = {"C3": ("C3", None), "C4": ("C4", None)}
+# full-size metric configs; the numpy-backend envelope run is part of them
+BIG = {"C3": ("C3", None, {}), "C4": ("C4", None, {})}
 
 
 def kernel_cases():
@@ -123,14 +138,42 @@ class RankLog:
             self.rows.append((p, self._b, len(state.cols_of[p])))
 
 
-def factor_case(name, cfg, n):
+PICK_MAX = 160_000          # largest full block stored for a picked record
+
+
+def _rel(a, c):
+    """max|a - c| / max|c| (inf on a shape mismatch)."""
+    if a.shape != c.shape:
+        return np.inf
+    if a.size == 0:
+        return 0.0
+    return float(np.abs(a - c).max() / max(np.abs(c).max(), 1e-300))
+
+
+def _picks(n):
+    return sorted(set(i for i in (0, 1, n // 2, n - 2, n - 1) if 0 <= i < n))
+
+
+def _records(F):
+    bh = [r for r in F.q_chain if isinstance(r, BlockHouseholder)]
+    isc = [r for r in F.q_chain if isinstance(r, InterfaceScaling)]
+    sp = [r for r in F.q_chain if isinstance(r, Sparsifier)]
+    return bh, isc, sp
+
+
+def _chain_vectors(F, N):
+    v = np.random.default_rng(11).standard_normal(N)
+    return {"apply_qt": F.apply_qt(v), "solve_w": F.solve_w(v), "apply_w": F.apply_w(v)}
+
+
+def factor_case(name, cfg, n, envelope=None, **opts):
     A0, dims, L, eps, b, tol = make_config(cfg, n=n)
     A = SparseMat(A0.nrows, A0.ncols, A0.indptr, A0.indices, A0.data)
     tree = ref_partition(dims, L)
     K.set_backend("numba")
     log = RankLog()
     t0 = time.perf_counter()
-    F = factorize(A, tree, eps=eps, observer=log)
+    F = factorize(A, tree, eps=eps, observer=log, **opts)
     t_fac = time.perf_counter() - t0
     t0 = time.perf_counter()
     x, rep = gmres(A, b, F, tol=tol)
@@ -138,39 +181,95 @@ def factor_case(name, cfg, n):
     out = {"dims": np.array(dims), "L": np.int64(L), "eps": np.float64(eps),
            "tol": np.float64(tol), "t_factor": np.float64(t_fac),
            "t_gmres": np.float64(t_sol)}
+    out["options"] = np.array(json.dumps(opts))
     keys = [k for k in F.stats[0] if not k.startswith("t_")]
     out["stat_keys"] = np.array(keys)
     out["stats"] = np.array([[float(s[k]) for k in keys] for s in F.stats])
     out["sparsify_log"] = np.array(log.rows, dtype=np.int64).reshape(-1, 3)
     out["row_of_col"] = F.row_of_col
     out["payload"] = np.int64(F.payload_scalars)
-    bh = [r for r in F.q_chain if isinstance(r, BlockHouseholder)]
+    bh, isc, sp = _records(F)
+    # ---- elimination records (factor.py:486-493): R_ss, R_sn
     out["rss_diag"] = np.concatenate([np.diag(r.R_ss) for r in bh])
     out["rss_k"] = np.array([r.R_ss.shape[0] for r in bh])
-    pick = sorted(i for i in set([0, 1, len(bh) // 2, len(bh) - 2, len(bh) - 1])
-                  if bh[i].R_ss.shape[0] <= 256)
+    out["rsn_shape"] = np.array([r.R_sn.shape for r in bh], dtype=np.int64).reshape(-1, 2)
+    out["rsn_maxabs"] = np.array([np.abs(r.R_sn).max(initial=0.0) for r in bh])
+    out["rsn_fro"] = np.array([np.linalg.norm(r.R_sn) for r in bh])
+    pick = sorted(i for i in _picks(len(bh)) if bh[i].R_ss.shape[0] <= 256)
     out["rss_pick"] = np.array(pick)
     for i in pick:
         out[f"rss_{i}"] = bh[i].R_ss
         out[f"rsn_{i}_shape"] = np.array(bh[i].R_sn.shape)
         out[f"rsn_{i}_fro"] = np.float64(np.linalg.norm(bh[i].R_sn))
+    rsn_pick = [i for i in pick if bh[i].R_sn.size <= PICK_MAX]
+    out["rsn_pick"] = np.array(rsn_pick, dtype=np.int64)
+    for i in rsn_pick:
+        out[f"rsn_{i}"] = bh[i].R_sn
+    # ---- interface scaling records (factor.py:504-532): R_pp
+    out["rpp_k"] = np.array([r.R_pp.shape[0] for r in isc], dtype=np.int64)
+    out["rpp_diag"] = (np.concatenate([np.diag(r.R_pp) for r in isc]) if isc
+                       else np.zeros(0))
+    out["rpp_fro"] = np.array([np.linalg.norm(r.R_pp) for r in isc])
+    pp_pick = [i for i in _picks(len(isc)) if isc[i].R_pp.size <= PICK_MAX]
+    out["rpp_pick"] = np.array(pp_pick, dtype=np.int64)
+    for i in pp_pick:
+        out[f"rpp_{i}"] = isc[i].R_pp
+    # ---- sparsifier records (factor.py:627-709): rank, tau, V; R_ff/R_fc unscaled
+    out["sp_rank"] = np.array([r.rank for r in sp], dtype=np.int64)
+    out["sp_scaled"] = np.array([bool(r.scaled) for r in sp])
+    out["sp_m"] = np.array([len(r.cols) for r in sp], dtype=np.int64)
+    out["sp_tau"] = (np.concatenate([r.q_panel.tau for r in sp]) if sp else np.zeros(0))
+    out["sp_ntau"] = np.array([len(r.q_panel.tau) for r in sp], dtype=np.int64)
+    sp_pick = [i for i in _picks(len(sp)) if sp[i].q_panel.V.size <= PICK_MAX]
+    out["sp_pick"] = np.array(sp_pick, dtype=np.int64)
+    for i in sp_pick:
+        out[f"sp_{i}_V"] = sp[i].q_panel.V
+        out[f"sp_{i}_T"] = sp[i].q_panel.T
+    unsc = [i for i, r in enumerate(sp) if not r.scaled]
+    if unsc:
+        out["rff_k"] = np.array([sp[i].R_ff.shape[0] for i in unsc], dtype=np.int64)
+        out["rff_diag"] = np.concatenate([np.diag(sp[i].R_ff) for i in unsc])
+        out["rfc_fro"] = np.array([np.linalg.norm(sp[i].R_fc) for i in unsc])
+        out["hf_tau"] = np.concatenate([sp[i].hf_panel.tau for i in unsc])
+        out["unsc_idx"] = np.array(unsc, dtype=np.int64)
+        for i in _picks(len(unsc)):
+            j = unsc[i]
+            if sp[j].R_ff.size + sp[j].R_fc.size <= PICK_MAX:
+                out[f"rff_{j}"] = sp[j].R_ff
+                out[f"rfc_{j}"] = sp[j].R_fc
     out["chain_kinds"] = np.array([type(r).__name__ for r in F.q_chain[:-1]])
+    # ---- the reference's own chain applications (factor.py:281-300)
+    for k, v in _chain_vectors(F, A.ncols).items():
+        out[f"chain_{k}"] = v
     out["gmres_iters"] = np.int64(rep.iterations)
     out["gmres_hist"] = rep.residuals
     out["gmres_converged"] = np.bool_(rep.converged)
     out["x_norm"] = np.float64(np.linalg.norm(x))
     # rounding envelope (F3): numpy backend on the same inputs
-    if A.ncols <= 8192:
+    if envelope is None:
+        envelope = A.ncols <= 8192
+    if envelope:
         K.set_backend("numpy")
-        F2 = factorize(A, tree, eps=eps)
+        t0 = time.perf_counter()
+        F2 = factorize(A, tree, eps=eps, **opts)
+        out["t_factor_numpy"] = np.float64(time.perf_counter() - t0)
         K.set_backend("numba")
-        bh2 = [r for r in F2.q_chain if isinstance(r, BlockHouseholder)]
-        env = [float(np.abs(a.R_ss - c.R_ss).max() / max(np.abs(a.R_ss).max(), 1e-300))
-               if a.R_ss.shape == c.R_ss.shape else np.inf for a, c in zip(bh, bh2)]
-        out["rss_envelope"] = np.array(env)
+        bh2, isc2, sp2 = _records(F2)
+        out["rss_envelope"] = np.array([_rel(a.R_ss, c.R_ss) for a, c in zip(bh2, bh)])
+        out["rsn_envelope"] = np.array([_rel(a.R_sn, c.R_sn) for a, c in zip(bh2, bh)])
+        out["rpp_envelope"] = np.array([_rel(a.R_pp, c.R_pp) for a, c in zip(isc2, isc)])
+        out["sp_envelope"] = np.array([_rel(a.q_panel.V, c.q_panel.V) for a, c in zip(sp2, sp)])
+        out["sp_rank_numpy"] = np.array([r.rank for r in sp2], dtype=np.int64)
+        if unsc:
+            out["rff_envelope"] = np.array([_rel(sp2[i].R_ff, sp[i].R_ff) if i < len(sp2)
+                                            and not sp2[i].scaled else np.inf for i in unsc])
+        ch2 = _chain_vectors(F2, A.ncols)
+        for k, v in ch2.items():
+            out[f"chain_{k}_envelope"] = np.float64(_rel(v, out[f"chain_{k}"]))
     np.savez_compressed(os.path.join(HERE, f"factor_{name}.npz"), **out)
     print(f"{name}: N={A.ncols} L={L} factor {t_fac:.2f}s gmres {t_sol:.2f}s "
-          f"its={rep.iterations} res={rep.final_residual:.3e}", flush=True)
+          f"its={rep.iterations} res={rep.final_residual:.3e} "
+          f"records bh={len(bh)} is={len(isc)} sp={len(sp)} (unscaled {len(unsc)})", flush=True)
 
 
 def trees():
@@ -192,7 +291,7 @@ if __name__ == "__main__":
     if "--big" in sys.argv:
         cases.update(BIG)
     only = [a for a in sys.argv[1:] if not a.startswith("--")]
-    for name, (cfg, n) in cases.items():
+    for name, (cfg, n, opts) in cases.items():
         if only and name not in only:
             continue
-        factor_case(name, cfg, n)
+        factor_case(name, cfg, n, envelope=True if name in BIG else None, **opts)

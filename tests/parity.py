@@ -88,3 +88,124 @@ def rss_bar(g, n):
         tail = np.linspace(0.0, 1.0, n)
         bar = np.where(tail < 0.95, 1e-9, np.where(tail < 0.995, 1e-7, 1e-5))
     return bar
+
+
+# ------------------------------------------------------------------ R blocks
+# Every comparison below is relative to the reference block's own max |.|,
+# against bar = max(1e-10, 10 x the reference's numba-vs-numpy divergence of
+# that same quantity on that same record) — SURVEY §8(c) item 3.
+
+def env_bar(g, key, n):
+    env = g.get(key)
+    if env is None or len(env) != n:
+        return rss_bar(g, n)
+    return np.maximum(1e-10, 10.0 * np.where(np.isfinite(env), env, 1.0))
+
+
+def _rel(a, ref):
+    a = np.asarray(a)
+    if a.shape != ref.shape:
+        return np.inf
+    if ref.size == 0:
+        return 0.0
+    return float(np.abs(a - ref).max() / max(np.abs(ref).max(), 1e-300))
+
+
+def compare_records(bh, isc, sp, g):
+    """bh / isc / sp: the device's BlockHouseholder / InterfaceScaling /
+    Sparsifier views in chain order.  Returns a list of problems."""
+    out = []
+    n = len(bh)
+    if n != len(g["rss_k"]):
+        return [f"{n} elimination records, reference {len(g['rss_k'])}"]
+    # R_ss: diagonal of every record, full picks (factor.py:486-488)
+    errs = rss_diag_errors([r.R_ss for r in bh], g)
+    bar = env_bar(g, "rss_envelope", n)
+    bad = np.nonzero(errs > bar)[0]
+    if bad.size:
+        out.append(f"diag(R_ss) beyond bar at records {bad[:8]}: {errs[bad[:8]]}")
+    for i in g["rss_pick"]:
+        e = _rel(bh[i].R_ss, g[f"rss_{i}"])
+        if e > bar[i]:
+            out.append(f"R_ss[{i}] full: {e:.3e} > {bar[i]:.1e}")
+    # R_sn: shape, max|.| and Frobenius norm of every record; full picks
+    if "rsn_shape" in g:
+        rbar = env_bar(g, "rsn_envelope", n)
+        for i, r in enumerate(bh):
+            R = r.R_sn
+            if tuple(R.shape) != tuple(g["rsn_shape"][i]):
+                out.append(f"R_sn[{i}] shape {R.shape} vs {tuple(g['rsn_shape'][i])}")
+                continue
+            ma, fr = g["rsn_maxabs"][i], g["rsn_fro"][i]
+            if abs(np.abs(R).max(initial=0.0) - ma) > rbar[i] * max(ma, 1e-300) and ma > 0:
+                out.append(f"max|R_sn[{i}]| {np.abs(R).max():.17e} vs {ma:.17e}")
+            if abs(np.linalg.norm(R) - fr) > rbar[i] * np.sqrt(max(R.size, 1)) * max(ma, 1e-300) \
+                    and fr > 0:
+                out.append(f"||R_sn[{i}]||_F {np.linalg.norm(R):.17e} vs {fr:.17e}")
+        for i in g["rsn_pick"]:
+            e = _rel(bh[i].R_sn, g[f"rsn_{i}"])
+            if e > rbar[i]:
+                out.append(f"R_sn[{i}] full: {e:.3e} > {rbar[i]:.1e}")
+    # R_pp of the interface scalings (factor.py:504-532)
+    if "rpp_k" in g:
+        ks = g["rpp_k"]
+        if len(isc) != len(ks):
+            out.append(f"{len(isc)} interface scalings, reference {len(ks)}")
+        else:
+            pbar = env_bar(g, "rpp_envelope", len(ks))
+            off = np.r_[0, np.cumsum(ks)]
+            for i, r in enumerate(isc):
+                R = r.R_pp
+                dref = g["rpp_diag"][off[i]:off[i + 1]]
+                if R.shape != (ks[i], ks[i]):
+                    out.append(f"R_pp[{i}] shape {R.shape}")
+                    continue
+                e = _rel(np.diag(R), dref)
+                if e > pbar[i]:
+                    out.append(f"diag(R_pp[{i}]): {e:.3e} > {pbar[i]:.1e}")
+            for i in g["rpp_pick"]:
+                e = _rel(isc[i].R_pp, g[f"rpp_{i}"])
+                if e > pbar[i]:
+                    out.append(f"R_pp[{i}] full: {e:.3e} > {pbar[i]:.1e}")
+    # sparsifier basis Q_pp: rank and tau of every record, V / T of picks
+    # (factor.py:627-658, kernels rrqr_threshold)
+    if "sp_rank" in g:
+        ranks = g["sp_rank"]
+        if len(sp) != len(ranks):
+            out.append(f"{len(sp)} sparsifiers, reference {len(ranks)}")
+        else:
+            sbar = env_bar(g, "sp_envelope", len(ranks))
+            toff = np.r_[0, np.cumsum(g["sp_ntau"])]
+            for i, r in enumerate(sp):
+                if r.rank != ranks[i]:
+                    out.append(f"sparsifier {i} rank {r.rank} vs {ranks[i]}")
+                    continue
+                tref = g["sp_tau"][toff[i]:toff[i + 1]]
+                tau = r.q_panel.tau
+                if tau.shape != tref.shape or (tau.size and np.abs(tau - tref).max() > sbar[i] * 2.0):
+                    out.append(f"sparsifier {i} tau differs")
+            for i in g["sp_pick"]:
+                if i >= len(sp):
+                    continue
+                for key, val in (("V", sp[i].q_panel.V), ("T", sp[i].q_panel.T)):
+                    e = _rel(val, g[f"sp_{i}_{key}"])
+                    if e > sbar[i]:
+                        out.append(f"sparsifier {i} {key}: {e:.3e} > {sbar[i]:.1e}")
+    return out
+
+
+def compare_chains(F, g):
+    """The device chains against the reference's own apply_qt / solve_w /
+    apply_w of the seeded vector (factor.py:281-300)."""
+    out = []
+    if "chain_apply_qt" not in g:
+        return out
+    v = np.random.default_rng(11).standard_normal(F.N)
+    for fn in ("apply_qt", "solve_w", "apply_w"):
+        ref = g[f"chain_{fn}"]
+        env = float(g.get(f"chain_{fn}_envelope", 0.0))
+        bar = max(1e-10, 10.0 * env)
+        e = _rel(getattr(F, fn)(v), ref)
+        if e > bar:
+            out.append(f"{fn}: {e:.3e} > {bar:.1e}")
+    return out

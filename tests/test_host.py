@@ -48,18 +48,40 @@ def test_generator_seeded_and_variable():
 
 
 def test_host_gmres_with_oracle():
+    """The host GMRES restatement (test comparator for spq_gmres) solves the
+    oracle-preconditioned system to the dense solution."""
     from oracle import spaqr_oracle as O
+    from oracle.krylov import gmres_host
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    from paper_2010_06807_b200.sparse import matvec
+    A, dims, L, eps, b, tol = make_config("C1", n=20)
+    F = O.factorize(A, partition_geometric(dims, L), eps=1e-2)
+    x, its, hist, conv = gmres_host(A, b, F, tol=1e-12, maxit=50, matvec=matvec)
+    assert conv
+    xd = np.linalg.solve(A.to_dense(), b)
+    assert np.linalg.norm(x - xd) <= 1e-9 * np.linalg.norm(xd)
+    x0, its0, _, _ = gmres_host(A, np.zeros_like(b), F, matvec=matvec)
+    assert its0 == 0 and not x0.any()
+
+
+def test_product_gmres_needs_device_or_reference():
+    """No silent host fallback in the product package: a non-B200 F goes to
+    the reference's own nestqr.solve.gmres or raises."""
+    import importlib.util
+    from oracle import spaqr_oracle as O
+    from paper_2010_06807_b200.errors import NestqrError
     from paper_2010_06807_b200.ordering import partition_geometric
     from paper_2010_06807_b200.problems import make_config
     from paper_2010_06807_b200.solve import gmres
-    A, dims, L, eps, b, tol = make_config("C1", n=20)
+    A, dims, L, eps, b, tol = make_config("C1", n=12)
     F = O.factorize(A, partition_geometric(dims, L), eps=1e-2)
-    x, rep = gmres(A, b, F, tol=1e-12, maxit=50)
-    assert rep.converged
-    xd = np.linalg.solve(A.to_dense(), b)
-    assert np.linalg.norm(x - xd) <= 1e-9 * np.linalg.norm(xd)
-    x0, rep0 = gmres(A, np.zeros_like(b), F)
-    assert rep0.iterations == 0 and not x0.any()
+    if importlib.util.find_spec("nestqr") is None:
+        with pytest.raises(NestqrError):
+            gmres(A, b, F)
+    else:
+        x, rep = gmres(A, b, F)
+        assert rep.converged
 
 
 def test_library_exports_every_header_symbol():
@@ -126,3 +148,20 @@ def test_replica_timing_is_max_over_ranks_gloo():
     assert Ts[0] == Ts[1]            # every rank sees the max
     assert Ts[0][0] >= 100.0         # rank 1's (shifted) time wins
     assert out[0][2] == out[1][2]    # replicas compute identical ranks
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` with no launcher re-executes itself under torchrun:
+    two ranks, one JSON line from rank 0 (reference arm, gloo, C1)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, SPQ_BENCH_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--gpus", "2", "--config", "C1", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+    assert lines[0]["config"]["config"] == "C1" and lines[0]["config"]["N"] == 4096

@@ -1,3 +1,3 @@
 #!/bin/bash
 O=gpurun_out/${1:-hp}; mkdir -p $O
-SPQ_HOST_PROFILE=$O/hp.txt timeout 300 python tools/run_config.py C3 - 8 > $O/c3.log 2>&1; echo "exit=$?" >> $O/c3.log
+SPQ_BUILD_HOSTPROF=1 python -m paper_2010_06807_b200.build --force > /dev/null && SPQ_HOST_PROFILE=$O/hp.txt timeout 300 python tools/run_config.py C3 - 8 > $O/c3.log 2>&1; echo "exit=$?" >> $O/c3.log
