@@ -10,7 +10,8 @@
  *
  * Status codes mirror the reference's exit codes (pkg/src/nestqr/errors.py:3-6):
  *   SPQ_OK 0, SPQ_ERR_SINGULAR 3 (SingularPivotError), SPQ_ERR_BAD_INPUT 4
- *   (NestqrError), SPQ_ERR_CUDA 5, SPQ_ERR_INTERNAL 6, SPQ_ERR_SPECULATION 7
+ *   (NestqrError), SPQ_ERR_CUDA 5, SPQ_ERR_INTERNAL 6, SPQ_ERR_SPECULATION 7,
+ *   SPQ_ERR_ILL_CONDITIONED 8 (IllConditionedInterfaceError)
  *   (speculative row flags were wrong: redo with speculate=0).  Details of the last
  *   failure via spq_last_error().
  * Ownership: the context owns all device memory; host arrays are borrowed
@@ -32,6 +33,8 @@ extern "C" {
 #define SPQ_ERR_CUDA 5
 #define SPQ_ERR_INTERNAL 6
 #define SPQ_ERR_SPECULATION 7
+#define SPQ_ERR_ILL_CONDITIONED 8   /* IllConditionedInterfaceError: index = interface,
+                                       value = sigma_min, message = the floor */
 
 typedef struct spq_ctx spq_ctx;
 
@@ -88,6 +91,18 @@ int spq_sparsify(spq_ctx* ctx, int n, const int32_t* ids, double eps,
                  int32_t* out_rank, int32_t* out_before, double* out_dropped,
                  int32_t* out_done);
 
+/* sparsify_interface(p, eps, mode, scaled_now) for every id, in order
+ * (factor.py:569-709): mode 0 'scaled', 1 'unscaled', 2 'variant1',
+ * 3 'variant2'; scaled_now = whether this level was scaled (the driver's
+ * do_scale, factor.py:849-850).  mode 0 with scaled_now runs the batched
+ * wave path (= spq_sparsify); every other combination the reference's
+ * sequential route, including the sigma-weighted unscaled target with its
+ * IllConditionedInterfaceError (SPQ_ERR_ILL_CONDITIONED) and the
+ * min_rank escalation loop. */
+int spq_sparsify_ex(spq_ctx* ctx, int n, const int32_t* ids, double eps, int mode,
+                    int scaled_now, int32_t* out_rank, int32_t* out_before,
+                    double* out_dropped, int32_t* out_done);
+
 /* ------------------------------------------------------ (d) merge
  * merge_level (factor.py:713-748): parent k takes the children
  * child_ids[child_ptr[k]:child_ptr[k+1]] in that order. */
@@ -120,10 +135,13 @@ int spq_reset_timings(spq_ctx* ctx);
 
 /* ------------------------------------------------------ records (audit) */
 int spq_num_records(spq_ctx* ctx);
-/* info: [kind(1 elim,2 scale,3 sparsify), m(rows), k, n(cols_n), rank] */
-int spq_record_info(spq_ctx* ctx, int idx, int64_t* info5);
-/* which: 0 rows, 1 cols_s/cols, 2 cols_n, 3 V, 4 tau, 5 T, 6 R (R_ss/R_pp),
- * 7 R_sn.  Copies to host (int64 for index arrays, double otherwise). */
+/* info (8 slots): [kind(1 elim,2 scale,3 sparsify), m(rows), k, n(cols_n), rank,
+ * cluster id, unscaled-sparsifier flag, fine count f] */
+int spq_record_info(spq_ctx* ctx, int idx, int64_t* info8);
+/* which: 0 rows, 1 cols_s/cols, 2 cols_n, 3 V, 4 tau, 5 T, 6 R (R_ss/R_pp;
+ * R_ff f x f of an unscaled sparsifier), 7 R_sn (R_fc f x rank of an
+ * unscaled sparsifier), 8/9/10 the H_f panel V (m x f) / tau / T (f x f).
+ * Copies to host (int64 for index arrays, double otherwise). */
 int spq_record_get(spq_ctx* ctx, int idx, int which, void* out);
 
 /* ------------------------------------------------------ (e) solve chains

@@ -478,6 +478,7 @@ class BlockState:
                   else np.empty(0, np.int64))
         self.row_of_col[cols_s] = rows_s
         rec = RecElim(stack_rows, panel, cols_s.copy(), R_ss, cols_n, C[:ns].copy())
+        rec.cid = s
         self.retire(s)
         return rec
 
@@ -495,7 +496,9 @@ class BlockState:
         for r in sorted(self.cix[p] - {p}):
             self.blk[(r, p)] = tri_solve_right(R_pp, self.blk[(r, p)])
         self.put(p, p, np.eye(npp))
-        return RecScale(self.rows_of[p].copy(), panel, self.cols_of[p].copy(), R_pp)
+        rec = RecScale(self.rows_of[p].copy(), panel, self.cols_of[p].copy(), R_pp)
+        rec.cid = p
+        return rec
 
     # ---------------------------------------------------------------- (c)
     def sparsify_iface(self, p, eps):
@@ -545,6 +548,7 @@ class BlockState:
                 self.drop(p, c)
         dropped = max(spectral_norm(E1), spectral_norm(E2))
         rec = RecSparsify(rows_p.copy(), cols_p.copy(), panel, r)
+        rec.cid = p
         self.row_of_col[cols_p[r:]] = rows_p[r:]
         self.rows_of[p] = rows_p[:r].copy()
         self.cols_of[p] = cols_p[:r].copy()

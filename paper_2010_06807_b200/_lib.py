@@ -12,7 +12,8 @@ import os
 
 import numpy as np
 
-from .errors import (SPQ_ERR_BAD_INPUT, SPQ_ERR_SINGULAR, SPQ_ERR_SPECULATION, SpeculationError, DeviceError, NestqrError,
+from .errors import (SPQ_ERR_BAD_INPUT, SPQ_ERR_ILL_CONDITIONED, SPQ_ERR_SINGULAR, SPQ_ERR_SPECULATION,
+                     IllConditionedInterfaceError, SpeculationError, DeviceError, NestqrError,
                      SingularPivotError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -38,6 +39,8 @@ SIGNATURES = {
     "spq_factor": (C.c_int, [_ctx, C.c_int, _i32p]),
     "spq_scale": (C.c_int, [_ctx, C.c_int, _i32p, _i32p]),
     "spq_sparsify": (C.c_int, [_ctx, C.c_int, _i32p, C.c_double, _i32p, _i32p, _f64p, _i32p]),
+    "spq_sparsify_ex": (C.c_int, [_ctx, C.c_int, _i32p, C.c_double, C.c_int, C.c_int, _i32p,
+                                  _i32p, _f64p, _i32p]),
     "spq_merge": (C.c_int, [_ctx, C.c_int, _i32p, _i32p, _i32p]),
     "spq_finish": (C.c_int, [_ctx]),
     "spq_cluster_size": (C.c_int, [_ctx, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -128,6 +131,8 @@ class Context:
             raise NestqrError(text)
         if rc == SPQ_ERR_SPECULATION:
             raise SpeculationError(text)
+        if rc == SPQ_ERR_ILL_CONDITIONED:
+            raise IllConditionedInterfaceError(int(idx.value), float(val.value), float(text))
         raise DeviceError(f"native error {rc}: {text}")
 
     def call(self, name, *args):

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libspaqr_b200.so")
 SOURCES = ["k_copy.cu", "k_gemm.cu", "k_qr.cu", "k_cpqr.cu", "k_chain.cu", "runtime.cu", "k_krylov.cu",
-           "k_wyf.cu"]
+           "k_wyf.cu", "k_svd.cu"]
 # diagnostic host sampling profiler (tools/hostprof.cu): linked in only when
 # SPQ_BUILD_HOSTPROF=1, never part of the shipped library
 EXTRA = ([os.path.join(os.path.dirname(HERE), "tools", "hostprof.cu")]

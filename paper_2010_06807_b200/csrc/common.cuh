@@ -163,6 +163,15 @@ struct ChainOp {
 };
 constexpr size_t CHAIN_SMEM_MAX = 200 * 1024;
 
+// one block of the batched one-sided Jacobi (k_svd.cu): A (m x n, lda) is
+// overwritten; smax / smin receive the extreme singular values
+struct SvJob {
+  double* A;
+  int m, n, lda;
+  double* smax;
+  double* smin;
+};
+
 // one problem of the batched CTA-resident CPQR
 struct CpqrJob {
   double* W;           // m x n (ldw), candidate columns (compacted), read (and written back)

@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(1024) sparsify_select_kernel(const double* __r
                                                                int m, int n, double eps_user,
                                                                int* __restrict__ keep_idx,
                                                                int* nk, double* ratio_out,
-                                                               double* maxcol_out) {
+                                                               double* maxcol_out, int allow_filter) {
   __shared__ double red[32];
   __shared__ int cnt[33];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -290,7 +290,9 @@ __global__ void __launch_bounds__(1024) sparsify_select_kernel(const double* __r
   __syncthreads();
   const double maxcol = red[0];
   const double ratio = (maxcol == 0.0) ? 0.0 : fmin(eps_user / maxcol, 0.999999);
-  const bool filter = maxcol > 0.0 && n > 4 * m;
+  // scaled route only (factor.py:600-604); the unscaled route runs the CPQR
+  // on the full target (factor.py:606-611)
+  const bool filter = allow_filter && maxcol > 0.0 && n > 4 * m;
   const double thr = ratio * maxcol;
   // ordered compaction in chunks of blockDim
   int base = 0;
@@ -327,9 +329,10 @@ __global__ void gather_cols_kernel(const double* __restrict__ M, int m, const in
 }
 
 void launch_sparsify_prep(const double* M, int m, int n, double eps, double* sq, int* keep_idx,
-                          int* nk, double* ratio, double* maxcol, double* W, cudaStream_t st) {
+                          int* nk, double* ratio, double* maxcol, double* W, cudaStream_t st,
+                          int allow_filter) {
   if (n > 0) colsq_kernel<<<(n * 32 + 255) / 256, 256, 0, st>>>(M, m, n, sq); SPQ_LAUNCH_CHECK();
-  sparsify_select_kernel<<<1, 1024, 0, st>>>(sq, m, n, eps, keep_idx, nk, ratio, maxcol); SPQ_LAUNCH_CHECK();
+  sparsify_select_kernel<<<1, 1024, 0, st>>>(sq, m, n, eps, keep_idx, nk, ratio, maxcol, allow_filter); SPQ_LAUNCH_CHECK();
   if (n > 0) gather_cols_kernel<<<dim3(n, (unsigned)std::min((m + 255) / 256, 64)), 256, 0, st>>>(M, m, keep_idx, nk, W); SPQ_LAUNCH_CHECK();
 }
 

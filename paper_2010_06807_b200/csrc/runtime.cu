@@ -34,7 +34,9 @@ namespace spq {
 void launch_cpqr(const CpqrArgs& a, int G, cudaStream_t st);
 int cpqr_grid(int ncols, int nsm);
 void launch_sparsify_prep(const double* M, int m, int n, double eps, double* sq, int* keep_idx,
-                          int* nk, double* ratio, double* maxcol, double* W, cudaStream_t st);
+                          int* nk, double* ratio, double* maxcol, double* W, cudaStream_t st,
+                          int allow_filter = 1);
+void launch_jacobi_sv(const SvJob* d_jobs, int n, cudaStream_t st);
 void chain_wy(const double* V, const double* T, int m, int k, double* z, const int* rows,
               int64_t N, int nrhs, bool transpose, double* w, double* w2, cudaStream_t st);
 void chain_tri(const double* R, int k, const double* Rsn, int n, double* y, const int* cols_s,
@@ -335,6 +337,14 @@ enum RecKind { REC_ELIM = 1, REC_SCALE = 2, REC_SPARSIFY = 3 };
 struct Record {
   int kind = 0;
   int m = 0, k = 0, n = 0, rank = 0;
+  int cid = -1;          // cluster the record eliminates / scales / compresses
+  // unscaled sparsifier (factor.py:660-709): H_f panel (m x f) + R_ff (f x f, in R)
+  // + R_fc (f x rank, in Rsn); fine / coarse column lists for the W-side ops
+  bool unscaled = false;
+  int f = 0;
+  double *hV = nullptr, *htau = nullptr, *hT = nullptr;
+  std::vector<int64_t> cols_f, cols_c;
+  int *d_cols_f = nullptr, *d_cols_c = nullptr;
   std::vector<int64_t> rows, cols_s, cols_n;
   double* payload = nullptr;
   double *V = nullptr, *tau = nullptr, *T = nullptr, *R = nullptr, *Rsn = nullptr;
@@ -2031,6 +2041,7 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
   // record + bookkeeping (factor.py:486-492)
   Record rec;
   rec.kind = REC_ELIM;
+  rec.cid = s;
   rec.m = f.m;
   rec.k = f.k;
   rec.n = f.n;
@@ -2302,6 +2313,7 @@ void do_scale(spq_ctx* c, const std::vector<int>& ids, int32_t* done) {
     const int np = (int)c->cols_of[p].size();
     Record rec;
     rec.kind = REC_SCALE;
+    rec.cid = p;
     rec.m = np; rec.k = np; rec.n = 0;
     rec.rows = c->rows_of[p];
     rec.cols_s = c->cols_of[p];
@@ -2441,6 +2453,104 @@ struct SpScal { int nk; int rank; double ratio; double maxcol; };
 
 constexpr size_t CPQR_CTA_MAX_SMEM = 220 * 1024;
 
+// Threshold CPQR of a list of independent problems (job.ncap = column
+// capacity, job.nk = device live column count).  Per problem: the
+// register-resident cluster kernel when a plan exists (smallest cluster,
+// then least row padding), else the CTA shared-memory kernel, the cluster
+// shared-memory kernel, or the cooperative grid kernel.  Everything but the
+// cooperative jobs runs concurrently on the fork streams.
+void run_cpqr_jobs(spq_ctx* c, const std::vector<CpqrJob>& jobs) {
+  const bool coop_only = env_flag("SPQ_CPQR_COOP"), no_ws = env_flag("SPQ_CPQR_NOWS");
+  std::map<std::tuple<int, int, int>, std::pair<std::vector<CpqrJob>, size_t>> rg_groups;   // (variant, cl, tpc)
+  std::map<int, std::pair<std::vector<CpqrJob>, size_t>> by_cl;
+  std::vector<CpqrJob> cj;
+  std::vector<CpqrJob> coop;
+  size_t cta_smem = 0;
+  for (const CpqrJob& q : jobs) {
+    const int np = q.m, ncap = std::max(q.ncap, 1);
+    int bv = -1, bcl = 0, btpc = 0;
+    if (!coop_only && !no_ws)
+      for (int v = 0; v < 3; ++v) {
+        int tpc = 0;
+        const int cl = cpqr_reg_plan(np, ncap, v, &tpc);
+        if (cl == 0) continue;
+        static const int RR[3] = {16, 8, 4};
+        if (bv < 0 || cl < bcl || (cl == bcl && tpc * RR[v] < btpc * RR[bv])) { bv = v; bcl = cl; btpc = tpc; }
+      }
+    if (bv >= 0) {
+      auto& g = rg_groups[std::make_tuple(bv, bcl, btpc)];
+      g.first.push_back(q);
+      static const int RRv[3] = {16, 8, 4};
+      g.second = std::max(g.second, cpqr_reg_smem(btpc * RRv[bv], bcl));
+      continue;
+    }
+    if (!coop_only && !env_flag("SPQ_CPQR_CLUSTER") && cpqr_cta_smem(np, ncap) <= CPQR_CTA_MAX_SMEM) {
+      cj.push_back(q);
+      cta_smem = std::max(cta_smem, cpqr_cta_smem(np, ncap));
+      continue;
+    }
+    const int cl = coop_only ? 0 : cpqr_cluster_size(np, ncap);
+    if (cl > 0) {
+      auto& g2 = by_cl[cl];
+      g2.first.push_back(q);
+      g2.second = std::max(g2.second, cpqr_cluster_smem(np, ncap, cl));
+      continue;
+    }
+    coop.push_back(q);
+  }
+  Scope s(c, F_CPQR);
+  // upload every job list first (the ring), then fork
+  std::vector<std::tuple<const CpqrJob*, int, std::tuple<int, int, int>, size_t, const CpqrJob*>> wl;
+  for (auto& kv : rg_groups)
+    wl.emplace_back(up_or_param(c, kv.second.first, PL_SMALL), (int)kv.second.first.size(), kv.first,
+                    kv.second.second, kv.second.first.data());
+  std::vector<std::tuple<const CpqrJob*, int, int, size_t>> cl_l;
+  for (auto& kv : by_cl)
+    cl_l.emplace_back(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first,
+                      kv.second.second);
+  const CpqrJob* d_cj = cj.empty() ? nullptr : upload(c, cj);
+  {
+    Fork fk(c);
+    for (auto& w : wl) {
+      const auto& key = std::get<2>(w);
+      launch_cpqr_reg(std::get<0>(w), std::get<4>(w), std::get<1>(w), std::get<0>(key), std::get<1>(key),
+                      std::get<2>(key), std::get<3>(w), fk.next());
+      c->tm.launches[F_CPQR]++;
+      c->n_kernels++;
+    }
+    for (auto& w : cl_l) {
+      launch_cpqr_cluster(std::get<0>(w), std::get<1>(w), std::get<2>(w), std::get<3>(w), fk.next());
+      c->tm.launches[F_CPQR]++;
+      c->n_kernels++;
+    }
+    if (d_cj) {
+      launch_cpqr_cta(d_cj, (int)cj.size(), cta_smem, fk.next());
+      c->tm.launches[F_CPQR]++;
+      c->n_kernels++;
+    }
+    fk.join();
+  }
+  for (const CpqrJob& q : coop) {
+    const int ncap = std::max(q.ncap, 1);
+    const int G = cpqr_grid(ncap, c->nsm);
+    double* slots = dalloc(c, 2 * G * sizeof(double));
+    int* slotp = (int*)dalloc(c, 2 * G * sizeof(int));
+    CpqrArgs a{};
+    a.gmaps = (int*)dalloc(c, (size_t)G * 2 * ncap * sizeof(int));
+    a.force_gmaps = env_flag("SPQ_CPQR_GMAPS");
+    c->deferred.push_back((double*)a.gmaps);
+    a.W = q.W; a.m = q.m; a.ncols_cap = ncap; a.nk = q.nk;
+    a.eps = q.eps; a.min_rank = q.min_rank; a.V = q.V; a.tau = q.tau; a.beta = q.beta;
+    a.rank = q.rank; a.perm = q.perm; a.slot_val = slots; a.slot_pos = slotp;
+    a.finalize = 0;
+    launch_cpqr(a, G, c->st);
+    c->tm.launches[F_CPQR]++;
+    c->n_kernels++;
+    dfree(c, slots);
+    dfree(c, slotp);
+  }
+}
+
 // sparsify_interface for a WAVE of mutually independent interfaces (no
 // shared block): identical to running them one after another in order.
 void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
@@ -2524,7 +2634,6 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     for (int t = 0; t < nw; ++t) hk[t].nk = J[t].ncols;
   }
   pivot_raise(c, c->piv);   // checks queued by this level's factor/scale calls
-  const bool coop_only = env_flag("SPQ_CPQR_COOP"), no_ws = env_flag("SPQ_CPQR_NOWS");
   auto job_of = [&](int t, int ncap) {
     SpJob& j = J[t];
     CpqrJob q{};
@@ -2533,98 +2642,10 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     q.tau = j.tau; q.beta = j.beta; q.rank = &dsc[t].rank; q.perm = j.perm; q.write_back = 0;
     return q;
   };
-  std::map<std::tuple<int, int, int>, std::pair<std::vector<CpqrJob>, size_t>> rg_groups;   // (variant, cl, tpc)
-  std::map<int, std::pair<std::vector<CpqrJob>, size_t>> by_cl;
-  std::vector<CpqrJob> cj;
-  std::vector<int> coop;
-  size_t cta_smem = 0;
-  for (int t = 0; t < nw; ++t) {
-    SpJob& j = J[t];
-    if (j.np == 0) continue;
-    const int ncap = std::max(hk[t].nk, 1);
-    // register-resident kernel: smallest cluster, then least row padding
-    int bv = -1, bcl = 0, btpc = 0;
-    if (!coop_only && !no_ws)
-      for (int v = 0; v < 3; ++v) {
-        int tpc = 0;
-        const int cl = cpqr_reg_plan(j.np, ncap, v, &tpc);
-        if (cl == 0) continue;
-        static const int RR[3] = {16, 8, 4};
-        if (bv < 0 || cl < bcl || (cl == bcl && tpc * RR[v] < btpc * RR[bv])) { bv = v; bcl = cl; btpc = tpc; }
-      }
-    if (bv >= 0) {
-      auto& g = rg_groups[std::make_tuple(bv, bcl, btpc)];
-      g.first.push_back(job_of(t, ncap));
-      static const int RRv[3] = {16, 8, 4};
-      g.second = std::max(g.second, cpqr_reg_smem(btpc * RRv[bv], bcl));
-      continue;
-    }
-    if (!coop_only && !env_flag("SPQ_CPQR_CLUSTER") && cpqr_cta_smem(j.np, ncap) <= CPQR_CTA_MAX_SMEM) {
-      cj.push_back(job_of(t, ncap));
-      cta_smem = std::max(cta_smem, cpqr_cta_smem(j.np, ncap));
-      continue;
-    }
-    const int cl = coop_only ? 0 : cpqr_cluster_size(j.np, ncap);
-    if (cl > 0) {
-      auto& g2 = by_cl[cl];
-      g2.first.push_back(job_of(t, ncap));
-      g2.second = std::max(g2.second, cpqr_cluster_smem(j.np, ncap, cl));
-      continue;
-    }
-    coop.push_back(t);
-  }
-  {
-    Scope s(c, F_CPQR);
-    // upload every job list first (the ring), then fork
-    std::vector<std::tuple<const CpqrJob*, int, std::tuple<int, int, int>, size_t, const CpqrJob*>> wl;
-    for (auto& kv : rg_groups)
-      wl.emplace_back(up_or_param(c, kv.second.first, PL_SMALL), (int)kv.second.first.size(), kv.first,
-                      kv.second.second, kv.second.first.data());
-    std::vector<std::tuple<const CpqrJob*, int, int, size_t>> cl_l;
-    for (auto& kv : by_cl)
-      cl_l.emplace_back(upload(c, kv.second.first), (int)kv.second.first.size(), kv.first,
-                        kv.second.second);
-    const CpqrJob* d_cj = cj.empty() ? nullptr : upload(c, cj);
-    Fork fk(c);
-    for (auto& w : wl) {
-      const auto& key = std::get<2>(w);
-      launch_cpqr_reg(std::get<0>(w), std::get<4>(w), std::get<1>(w), std::get<0>(key), std::get<1>(key),
-                      std::get<2>(key), std::get<3>(w), fk.next());
-      c->tm.launches[F_CPQR]++;
-      c->n_kernels++;
-    }
-    for (auto& w : cl_l) {
-      launch_cpqr_cluster(std::get<0>(w), std::get<1>(w), std::get<2>(w), std::get<3>(w), fk.next());
-      c->tm.launches[F_CPQR]++;
-      c->n_kernels++;
-    }
-    if (d_cj) {
-      launch_cpqr_cta(d_cj, (int)cj.size(), cta_smem, fk.next());
-      c->tm.launches[F_CPQR]++;
-      c->n_kernels++;
-    }
-    fk.join();
-    for (int t : coop) {
-      SpJob& j = J[t];
-      const int ncap = std::max(hk[t].nk, 1);
-      const int G = cpqr_grid(ncap, c->nsm);
-      double* slots = dalloc(c, 2 * G * sizeof(double));
-      int* slotp = (int*)dalloc(c, 2 * G * sizeof(int));
-      CpqrArgs a{};
-      a.gmaps = (int*)dalloc(c, (size_t)G * 2 * ncap * sizeof(int));
-      a.force_gmaps = env_flag("SPQ_CPQR_GMAPS");
-      c->deferred.push_back((double*)a.gmaps);
-      a.W = j.Wm; a.m = j.np; a.ncols_cap = ncap; a.nk = &dsc[t].nk;
-      a.eps = &dsc[t].ratio; a.min_rank = 0; a.V = j.V; a.tau = j.tau; a.beta = j.beta;
-      a.rank = &dsc[t].rank; a.perm = j.perm; a.slot_val = slots; a.slot_pos = slotp;
-      a.finalize = 0;
-      launch_cpqr(a, G, c->st);
-      c->tm.launches[F_CPQR]++;
-      c->n_kernels++;
-      dfree(c, slots);
-      dfree(c, slotp);
-    }
-  }
+  std::vector<CpqrJob> jobs;
+  for (int t = 0; t < nw; ++t)
+    if (J[t].np > 0) jobs.push_back(job_of(t, std::max(hk[t].nk, 1)));
+  run_cpqr_jobs(c, jobs);
   std::vector<SpScal> h(std::max(nw, 1));
   {
     HostTimer hw(&c->host_ms[9]);
@@ -2793,6 +2814,7 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     }
     Record rec;
     rec.kind = REC_SPARSIFY;
+    rec.cid = p;
     rec.m = np; rec.k = r; rec.n = 0; rec.rank = r;
     rec.rows = j.rows_p;
     rec.cols_s = j.cols_p;
@@ -2810,9 +2832,485 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
   flush_deferred(c);
 }
 
+// ------------------------------------------------------------------------
+// Sequential route for the sparsification variants the wave path does not
+// cover (factor.py:536-709): the UNSCALED route (mode 'unscaled', and every
+// level on which scale_every > 1 skips the scaling) and the one-sided /
+// Gram targets of 'variant1' / 'variant2'.  One interface at a time in the
+// reference's ascending order; every numeric step runs on the device, the
+// host reads only the scalars that steer the control flow (sigma_min, the
+// accepted rank, ||R_fn||_2).
+enum SpMode { SPM_SCALED = 0, SPM_UNSCALED = 1, SPM_VARIANT1 = 2, SPM_VARIANT2 = 3 };
+constexpr double SIGMA_FLOOR = 1e-14;   // factor.py:53
+
+// extreme singular values of A (m x n, lda) by one-sided Jacobi on a copy
+void jacobi_extremes(spq_ctx* c, const double* A, int m, int n, int lda, double* smax,
+                     double* smin) {
+  *smax = 0.0;
+  *smin = 0.0;
+  if ((int64_t)m * n == 0) return;
+  double* W = dalloc(c, ((size_t)m * n + 2) * sizeof(double));
+  CopyBatch cb;
+  CopyTask x{};
+  x.src = A; x.dst = W; x.nr = m; x.nc = n; x.lds = lda; x.ldd = m;
+  cb.add(x);
+  cb.run(c);
+  SvJob j{W, m, n, m, W + (size_t)m * n, W + (size_t)m * n + 1};
+  launch_jacobi_sv(upload(c, &j, 1), 1, c->st);
+  c->n_kernels++;
+  double h[2];
+  CUDA_TRY(cudaMemcpyAsync(h, W + (size_t)m * n, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  *smax = h[0];
+  *smin = h[1];
+  dfree(c, W);
+}
+
+// ||X||_2 (X rows x cols, ldx): the largest eigenvalue of the smaller Gram
+// matrix (full relative accuracy for the largest singular value)
+double spectral_norm_dev(spq_ctx* c, const double* X, int rows, int cols, int ldx) {
+  if ((int64_t)rows * cols == 0) return 0.0;
+  const int g = std::min(rows, cols);
+  double* G = dalloc(c, (size_t)g * g * sizeof(double));
+  double* Xt = nullptr;
+  GemmBatch gb;
+  if (cols <= rows) {   // X^T X
+    gb.add(X, ldx, X, ldx, G, g, g, g, rows, 1.0, 0.0);
+  } else {              // X X^T = (X^T)^T (X^T)
+    Xt = dalloc(c, (size_t)rows * cols * sizeof(double));
+    CopyBatch cb;
+    CopyTask x{};
+    x.src = X; x.dst = Xt; x.nr = rows; x.nc = cols; x.lds = ldx; x.ldd = cols; x.trans = 1;
+    cb.add(x);
+    cb.run(c);
+    gb.add(Xt, cols, Xt, cols, G, g, g, g, cols, 1.0, 0.0);
+  }
+  gb.run(c, true, 2.0 * g * g * (double)std::max(rows, cols));
+  double smax, smin;
+  jacobi_extremes(c, G, g, g, g, &smax, &smin);
+  dfree(c, G);
+  if (Xt) dfree(c, Xt);
+  return std::sqrt(smax);
+}
+
+void do_sparsify_seq(spq_ctx* c, int p, double eps, int mode, bool scaled_now,
+                     SparsifyOut& out) {
+  Stage stage_(c, "do_sparsify_seq");
+  HostTimer ht(&c->host_ms[8]);
+  const std::vector<int64_t> rows_p = c->rows_of[p], cols_p = c->cols_of[p];
+  const int np = (int)cols_p.size();
+  out = SparsifyOut{-1, np, 0.0, 0};
+  if (np == 0) return;
+  std::vector<int> us, cs, hu, wc;
+  for (int u : c->cix[p]) if (u != p) us.push_back(u);
+  for (int cc : c->rix[p]) if (cc != p) cs.push_back(cc);
+  int nu = 0, ncl = 0;
+  for (int u : us) { hu.push_back(find_block(c, u, p)->nr); nu += hu.back(); }
+  for (int cc : cs) { wc.push_back(find_block(c, p, cc)->nc); ncl += wc.back(); }
+  const size_t pp = (size_t)np * np;
+  // ---- operands: A_pp (np x np), A_np^T (np x nu), A_pn (np x ncl); col-major
+  double* App = dalloc(c, std::max<size_t>(pp, 1) * sizeof(double));
+  double* AnpT = dalloc(c, std::max<size_t>((size_t)np * nu, 1) * sizeof(double));
+  double* Apn = dalloc(c, std::max<size_t>((size_t)np * ncl, 1) * sizeof(double));
+  {
+    CopyBatch g;
+    Block* bp = find_block(c, p, p);
+    if (bp && bp->nr == np && bp->nc == np) {
+      CopyTask x{};
+      x.src = bp->p; x.dst = App; x.nr = np; x.nc = np; x.lds = np; x.ldd = np;
+      g.add(x);
+    } else {
+      g.zero(App, (int64_t)pp);   // a missing block reads as zeros (factor.py:389-392)
+    }
+    int off = 0;
+    for (size_t q = 0; q < us.size(); ++q) {
+      Block* b = find_block(c, us[q], p);
+      CopyTask x{};
+      x.src = b->p; x.dst = AnpT + (int64_t)off * np; x.nr = b->nr; x.nc = np; x.lds = b->nr;
+      x.ldd = np; x.trans = 1;
+      g.add(x);
+      off += b->nr;
+    }
+    off = 0;
+    for (size_t q = 0; q < cs.size(); ++q) {
+      Block* b = find_block(c, p, cs[q]);
+      CopyTask x{};
+      x.src = b->p; x.dst = Apn + (int64_t)off * np; x.nr = np; x.nc = b->nc; x.lds = np;
+      x.ldd = np;
+      g.add(x);
+      off += b->nc;
+    }
+    g.run(c);
+  }
+  // ---- compression target M (factor.py:536-567)
+  int mcols = 0;
+  double* M = nullptr;
+  if (mode == SPM_VARIANT1) {
+    mcols = nu;
+    M = AnpT;
+  } else if (mode == SPM_VARIANT2) {
+    // M = [sum_{r in col_index[p] & col_index[c]} A_rp^T A_rc  for c in c_list]
+    mcols = ncl;
+    M = dalloc(c, std::max<size_t>((size_t)np * ncl, 1) * sizeof(double));
+    CopyBatch z;
+    z.zero(M, (int64_t)np * ncl);
+    z.run(c);
+    int off = 0;
+    for (size_t q = 0; q < cs.size(); ++q) {
+      const int cc = cs[q];
+      for (int r : c->cix[p]) {
+        Block* brc = find_block(c, r, cc);
+        if (!brc) continue;
+        Block* brp = find_block(c, r, p);
+        GemmBatch gb;
+        gb.add(brp->p, brp->nr, brc->p, brc->nr, M + (int64_t)off * np, np, np, brc->nc, brp->nr,
+               1.0, 1.0);
+        gb.run(c, true, 2.0 * np * brc->nc * (double)brp->nr);
+      }
+      off += wc[q];
+    }
+  } else if (scaled_now) {
+    mcols = nu + ncl;
+    M = dalloc(c, std::max<size_t>((size_t)np * mcols, 1) * sizeof(double));
+    CopyBatch g;
+    CopyTask x{};
+    x.src = AnpT; x.dst = M; x.nr = np; x.nc = nu; x.lds = np; x.ldd = np;
+    g.add(x);
+    x.src = Apn; x.dst = M + (int64_t)nu * np; x.nc = ncl;
+    g.add(x);
+    g.run(c);
+  } else {
+    // sigma-weighted route: sigma_min of [A_pp; A_np] from the R of its QR
+    const int ms = np + nu;
+    double* CS = dalloc(c, ((size_t)ms * np + 2 * pp + np) * sizeof(double));
+    double* Rcs = CS + (size_t)ms * np;
+    double* tcs = Rcs + pp;
+    double* Tcs = tcs + np;
+    CopyBatch g;
+    g.zero(Rcs, (int64_t)(2 * pp + np));
+    CopyTask x{};
+    x.src = App; x.dst = CS; x.nr = np; x.nc = np; x.lds = np; x.ldd = ms;
+    g.add(x);
+    x.src = AnpT; x.dst = CS + np; x.nr = np; x.nc = nu; x.lds = np; x.ldd = ms; x.trans = 1;
+    g.add(x);
+    g.run(c);
+    qr_batch(c, {QrProb{CS, ms, np, Rcs, tcs, Tcs, {}}});
+    double smax, smin;
+    jacobi_extremes(c, Rcs, np, np, np, &smax, &smin);
+    dfree(c, CS);
+    if (smin <= SIGMA_FLOOR * std::max(smax, 1e-300)) {
+      char fl[64];
+      snprintf(fl, sizeof fl, "%.17g", SIGMA_FLOOR * smax);
+      throw SpqError(SPQ_ERR_ILL_CONDITIONED, fl, p, smin);
+    }
+    const double sigma = 1.0 / smin;
+    mcols = nu + ncl;
+    M = dalloc(c, std::max<size_t>((size_t)np * mcols, 1) * sizeof(double));
+    CopyBatch g2;
+    CopyTask y{};
+    y.src = AnpT; y.dst = M; y.nr = np; y.nc = nu; y.lds = np; y.ldd = np;
+    g2.add(y);
+    g2.run(c);
+    GemmBatch gb;   // sigma * A_pp^T A_pn
+    gb.add(App, np, Apn, np, M + (int64_t)nu * np, np, np, ncl, np, sigma, 0.0);
+    gb.run(c, true, 2.0 * np * ncl * (double)np);
+  }
+  // ---- threshold CPQR (scaled: column filter; unscaled: full target)
+  const int kmax = std::min(np, mcols);
+  const int rank_max = kmax;
+  const size_t msz = (size_t)np * std::max(mcols, 1);
+  double* Wm = dalloc(c, msz * sizeof(double));
+  double* sq = dalloc(c, std::max(mcols, 1) * sizeof(double));
+  int* keep = (int*)dalloc(c, std::max(mcols, 1) * sizeof(int));
+  int* perm = (int*)dalloc(c, std::max(mcols, 1) * sizeof(int));
+  const int k1 = std::max(kmax, 1);
+  double* Vq = dalloc(c, ((size_t)np * k1 + 2 * (size_t)k1) * sizeof(double));
+  double* tq = Vq + (size_t)np * k1;
+  double* bq = tq + k1;
+  SpScal* dsc = (SpScal*)dalloc(c, sizeof(SpScal));
+  auto cpqr = [&](int min_rank) {
+    CopyBatch z;
+    z.zero(Vq, (int64_t)np * k1 + 2 * k1);
+    z.run(c);
+    {
+      Scope s(c, F_CPQR);
+      launch_sparsify_prep(M, np, mcols, eps, sq, keep, &dsc->nk, &dsc->ratio, &dsc->maxcol, Wm,
+                           c->st, scaled_now ? 1 : 0);
+      c->tm.launches[F_CPQR] += 3;
+      c->n_kernels += 3;
+    }
+    SpScal h{};
+    CUDA_TRY(cudaMemcpyAsync(&h, dsc, sizeof(SpScal), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    CpqrJob q{};
+    q.W = Wm; q.m = np; q.n = mcols; q.ncap = std::max(h.nk, 1); q.ldw = np;
+    q.nk = &dsc->nk; q.eps = &dsc->ratio; q.min_rank = std::min(min_rank, kmax); q.V = Vq;
+    q.ldv = np; q.tau = tq; q.beta = bq; q.rank = &dsc->rank; q.perm = perm; q.write_back = 0;
+    if (mcols > 0) run_cpqr_jobs(c, {q});
+    else CUDA_TRY(cudaMemsetAsync(&dsc->rank, 0, sizeof(int), c->st));
+    CUDA_TRY(cudaMemcpyAsync(&h, dsc, sizeof(SpScal), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    const double mm = np, nn = h.nk, rr = h.rank;
+    c->tm.flops[F_CPQR] += 4.0 * mm * nn * rr - 2.0 * rr * rr * (mm + nn) + 4.0 * rr * rr * rr / 3.0;
+    c->tm.bytes[F_CPQR] += 16.0 * mm * nn;
+    return h.rank;
+  };
+  int r = cpqr(0);
+  auto free_all = [&]() {
+    for (void* q : {(void*)App, (void*)AnpT, (void*)Apn, (void*)Wm, (void*)sq, (void*)keep,
+                    (void*)perm, (void*)Vq, (void*)dsc})
+      dfree(c, q);
+    if (M && M != AnpT) dfree(c, M);
+  };
+  out.rank = r;
+  CopyBatch sc;            // split-back copies, in order
+  std::vector<std::pair<int, int>> drops;
+  auto put_new = [&](int i, int j, int nr, int nc, const double* src, int lds, bool trans) {
+    Block* old = find_block(c, i, j);
+    if (old) release_mem(c, *old);
+    if ((int64_t)nr * nc <= 0) {
+      drop_block(c, i, j);
+      return;
+    }
+    double* mem = new_block_mem(c, nr, nc);
+    CopyTask x{};
+    x.src = src; x.dst = mem; x.lds = lds;
+    if (trans) { x.nr = nc; x.nc = nr; x.ldd = nr; x.trans = 1; }
+    else { x.nr = nr; x.nc = nc; x.ldd = nr; }
+    sc.add(x);
+    Block& b = put_block(c, i, j, mem, nr, nc);
+    b.clean = false;            // values of a new rotation: flags read back on demand
+    b.unverified = false;
+    b.flags.clear();
+  };
+  auto drop_all = [&]() {
+    drop_block(c, p, p);
+    for (int u : us) drop_block(c, u, p);
+    for (int cc : cs) drop_block(c, p, cc);
+  };
+  Record rec;
+  rec.kind = REC_SPARSIFY;
+  rec.cid = p;
+  rec.rows = rows_p;
+  rec.cols_s = cols_p;
+  if (scaled_now) {
+    // ---------------- scaled apply (factor.py:627-658) on [A_np^T, A_pn]
+    if (r >= np) { free_all(); return; }
+    double* X = dalloc(c, std::max<size_t>((size_t)np * (nu + ncl), 1) * sizeof(double));
+    {
+      CopyBatch g;
+      CopyTask x{};
+      x.src = AnpT; x.dst = X; x.nr = np; x.nc = nu; x.lds = np; x.ldd = np;
+      g.add(x);
+      x.src = Apn; x.dst = X + (int64_t)nu * np; x.nc = ncl;
+      g.add(x);
+      g.run(c);
+    }
+    const int rk = std::max(r, 1);
+    rec.m = np; rec.k = r; rec.rank = r;
+    rec.payload = dalloc(c, ((size_t)np * rk + 2 * (size_t)rk + (size_t)rk * rk) * sizeof(double));
+    rec.V = rec.payload; rec.tau = rec.V + (size_t)np * rk; rec.T = rec.tau + rk;
+    {
+      CopyBatch g;
+      g.zero(rec.T, (int64_t)rk * rk);
+      CopyTask x{};
+      x.src = Vq; x.dst = rec.V; x.nr = np; x.nc = r; x.lds = np; x.ldd = np;
+      g.add(x);
+      x.src = tq; x.dst = rec.tau; x.nr = r; x.nc = 1; x.lds = r; x.ldd = r;
+      g.add(x);
+      g.run(c);
+    }
+    if (r > 0) {
+      build_full_T(c, {TProb{rec.V, np, r, rec.tau, rec.T}});
+      wy_batch(c, {WyProb{rec.V, rec.T, np, r, X, np, nu + ncl}}, true);
+    }
+    rec.full_T = true;
+    rec.payload_scalars = (int64_t)np * r + r + (int64_t)r * r;
+    const double e1 = spectral_norm_dev(c, X + r, np - r, nu, np);
+    const double e2 = spectral_norm_dev(c, X + r + (int64_t)nu * np, np - r, ncl, np);
+    out.dropped = std::max(e1, e2);
+    int off = 0;
+    for (size_t q = 0; q < us.size(); ++q) {   // (u,p) <- (X[:r, u cols])^T
+      put_new(us[q], p, hu[q], r, X + (int64_t)off * np, np, true);
+      off += hu[q];
+    }
+    for (size_t q = 0; q < cs.size(); ++q) {   // (p,c) <- X[:r, c cols]
+      put_new(p, cs[q], r, wc[q], X + (int64_t)off * np, np, false);
+      off += wc[q];
+    }
+    {
+      Block* dp = find_block(c, p, p);
+      if (dp) release_mem(c, *dp);
+      if (r > 0) {
+        double* mem = new_block_mem(c, r, r);
+        CopyTask x{};
+        x.dst = mem; x.nr = r; x.nc = r; x.ldd = r; x.ident = 1;
+        sc.add(x);
+        Block& b = put_block(c, p, p, mem, r, r);
+        set_identity_flags(c, b, r);
+      } else {
+        drop_all();
+      }
+    }
+    for (int i = r; i < np; ++i) c->row_of_col[cols_p[i]] = rows_p[i];
+    c->rows_of[p].assign(rows_p.begin(), rows_p.begin() + r);
+    c->cols_of[p].assign(cols_p.begin(), cols_p.begin() + r);
+    sc.run(c);
+    c->recs.push_back(std::move(rec));
+    out.done = 1;
+    dfree(c, X);
+    free_all();
+    flush_deferred(c);
+    return;
+  }
+  // ---------------- unscaled apply with rank escalation (factor.py:660-709)
+  const bool enforce = mode == SPM_SCALED || mode == SPM_UNSCALED;
+  double* G = dalloc(c, std::max<size_t>(pp, 1) * sizeof(double));
+  double* Gt = dalloc(c, std::max<size_t>(pp, 1) * sizeof(double));
+  double* ApnT = dalloc(c, std::max<size_t>((size_t)np * ncl, 1) * sizeof(double));
+  double* Tq = dalloc(c, (size_t)k1 * k1 * sizeof(double));
+  double* Rff = dalloc(c, (std::max<size_t>(pp, 1) * 2 + np) * sizeof(double));
+  double* Tf = Rff + pp;
+  double* tf = Tf + pp;
+  double nrm_fn = 0.0;
+  int f = 0;
+  for (;;) {
+    f = np - r;
+    if (f == 0) {   // factor.py:665-666: every direction coarse, no transform
+      for (void* q : {(void*)G, (void*)Gt, (void*)ApnT, (void*)Tq, (void*)Rff}) dfree(c, q);
+      free_all();
+      out.rank = r;
+      return;
+    }
+    CopyBatch g;
+    g.zero(Tq, (int64_t)k1 * k1);
+    g.zero(Rff, (int64_t)2 * pp + np);
+    CopyTask x{};
+    x.src = App; x.dst = Gt; x.nr = np; x.nc = np; x.lds = np; x.ldd = np; x.trans = 1;
+    g.add(x);   // Gt = A_pp^T
+    CopyTask y{};
+    y.src = Apn; y.dst = ApnT; y.nr = np; y.nc = ncl; y.lds = np; y.ldd = np;
+    g.add(y);
+    g.run(c);
+    if (r > 0) {   // Gt <- Q^T A_pp^T = (A_pp Q)^T
+      build_full_T(c, {TProb{Vq, np, r, tq, Tq}});
+      wy_batch(c, {WyProb{Vq, Tq, np, r, Gt, np, np}}, true);
+    }
+    CopyBatch g2;
+    CopyTask z{};
+    z.src = Gt; z.dst = G; z.nr = np; z.nc = np; z.lds = np; z.ldd = np; z.trans = 1;
+    g2.add(z);   // G = A_pp Q
+    g2.run(c);
+    // H_f, R_ff = qr_house(G[:, r:]); H_f^T on G[:, :r] and on A_pn
+    QrProb qf{G + (int64_t)r * np, np, f, Rff, tf, Tf, {}};
+    if (r > 0) qf.targets.push_back(CTarget{G, np, r});
+    if (ncl > 0) qf.targets.push_back(CTarget{ApnT, np, ncl});
+    qr_batch(c, {qf});
+    nrm_fn = spectral_norm_dev(c, ApnT, f, ncl, np);    // ||R_fn||_2, R_fn = (H_f^T A_pn)[:f]
+    if (!enforce || nrm_fn <= eps * (1.0 + 1e-8) || r >= rank_max) break;
+    r = cpqr(r + 1);                                       // rank escalation (factor.py:676)
+  }
+  out.rank = r;
+  // pivot floor of R_ff (factor.py:677)
+  {
+    PivotSet ps;
+    ps.jobs.push_back(PivotJob{Rff, f, f, 0});
+    ps.ctx.push_back("fine block of interface " + std::to_string(p));
+    pivot_launch(c, ps);
+    pivot_raise(c, ps);
+  }
+  // A_np Q: (A_np Q)^T = Q^T A_np^T in place of AnpT (factor.py:679-680)
+  double* Tqr = Tq;
+  if (r > 0) {
+    CopyBatch g;
+    g.zero(Tq, (int64_t)k1 * k1);
+    g.run(c);
+    build_full_T(c, {TProb{Vq, np, r, tq, Tq}});
+    wy_batch(c, {WyProb{Vq, Tq, np, r, AnpT, np, nu}}, true);
+  }
+  const double e1 = spectral_norm_dev(c, AnpT + r, f, nu, np);   // E1^T = rows r: of (A_np Q)^T
+  out.dropped = std::max(e1, nrm_fn);
+  // record: Q panel | H_f panel | R_ff | R_fc
+  const int rk = std::max(r, 1);
+  const size_t nq = (size_t)np * rk + 2 * (size_t)rk + (size_t)rk * rk;
+  const size_t nh = (size_t)np * f + f + (size_t)f * f;
+  const size_t nr_ = (size_t)f * f + (size_t)f * rk;
+  rec.m = np; rec.k = r; rec.rank = r; rec.unscaled = true; rec.f = f;
+  rec.payload = dalloc(c, (nq + nh + nr_) * sizeof(double));
+  rec.V = rec.payload; rec.tau = rec.V + (size_t)np * rk; rec.T = rec.tau + 2 * (size_t)rk;
+  rec.hV = rec.payload + nq; rec.htau = rec.hV + (size_t)np * f; rec.hT = rec.htau + f;
+  rec.R = rec.hT + (size_t)f * f; rec.Rsn = rec.R + (size_t)f * f;
+  {
+    CopyBatch g;
+    g.zero(rec.payload, (int64_t)(nq + nh + nr_));
+    g.run(c);
+    CopyTask x{};
+    x.src = Vq; x.dst = rec.V; x.nr = np; x.nc = r; x.lds = np; x.ldd = np;
+    g.add(x);
+    x.src = tq; x.dst = rec.tau; x.nr = r; x.nc = 1; x.lds = r; x.ldd = r;
+    g.add(x);
+    x.src = Tqr; x.dst = rec.T; x.nr = r; x.nc = r; x.lds = r; x.ldd = r;
+    g.add(x);
+    x.src = G + (int64_t)r * np; x.dst = rec.hV; x.nr = np; x.nc = f; x.lds = np; x.ldd = np;
+    g.add(x);
+    x.src = tf; x.dst = rec.htau; x.nr = f; x.nc = 1; x.lds = f; x.ldd = f;
+    g.add(x);
+    x.src = Rff; x.dst = rec.R; x.nr = f; x.nc = f; x.lds = f; x.ldd = f;
+    g.add(x);
+    x.src = G; x.dst = rec.Rsn; x.nr = f; x.nc = r; x.lds = np; x.ldd = f;   // R_fc = G2[:f, :r]
+    g.add(x);
+    g.run(c);
+    build_full_T(c, {TProb{rec.hV, np, f, rec.htau, rec.hT}});
+  }
+  rec.n = 0;
+  rec.full_T = true;
+  rec.payload_scalars = (int64_t)np * r + r + (int64_t)r * r + (int64_t)np * f + f +
+                        (int64_t)f * f + (int64_t)f * f + (int64_t)f * r;
+  rec.cols_c.assign(cols_p.begin(), cols_p.begin() + r);
+  rec.cols_f.assign(cols_p.begin() + r, cols_p.end());
+  // split back (factor.py:682-685) and the new diagonal block G2[f:, :r]
+  int off = 0;
+  for (size_t q = 0; q < us.size(); ++q) {
+    put_new(us[q], p, hu[q], r, AnpT + (int64_t)off * np, np, true);
+    off += hu[q];
+  }
+  off = 0;
+  for (size_t q = 0; q < cs.size(); ++q) {
+    put_new(p, cs[q], r, wc[q], ApnT + f + (int64_t)off * np, np, false);
+    off += wc[q];
+  }
+  if (r > 0) {
+    put_new(p, p, r, r, G + f, np, false);
+  } else {
+    Block* dp = find_block(c, p, p);
+    if (dp) release_mem(c, *dp);
+    drop_all();
+  }
+  // fine rows are the first f slots after H_f; they pair with the fine
+  // columns (last f slots after the basis rotation), factor.py:690-693
+  for (int i = 0; i < f; ++i) c->row_of_col[cols_p[r + i]] = rows_p[i];
+  c->rows_of[p].assign(rows_p.begin() + f, rows_p.end());
+  c->cols_of[p].assign(cols_p.begin(), cols_p.begin() + r);
+  sc.run(c);
+  c->recs.push_back(std::move(rec));
+  out.done = 1;
+  sync(c);   // the scratch below is read by the queued split-back copies
+  for (void* q : {(void*)G, (void*)Gt, (void*)ApnT, (void*)Tq, (void*)Rff}) dfree(c, q);
+  free_all();
+  flush_deferred(c);
+}
+
 void do_sparsify(spq_ctx* c, const std::vector<int>& ids, double eps,
-                 std::vector<SparsifyOut>& outs) {
+                 std::vector<SparsifyOut>& outs, int mode = SPM_SCALED, bool scaled_now = true) {
   outs.assign(ids.size(), SparsifyOut{-1, 0, 0.0, 0});
+  if (mode != SPM_SCALED || !scaled_now) {
+    // unscaled route / variant targets: the reference's sequential loop
+    for (size_t t = 0; t < ids.size(); ++t) {
+      if (!c->active[ids[t]]) throw SpqError(SPQ_ERR_BAD_INPUT, "sparsify of inactive cluster");
+      do_sparsify_seq(c, ids[t], eps, mode, scaled_now, outs[t]);
+    }
+    return;
+  }
   c->d_dropped = dalloc(c, 2 * std::max<size_t>(ids.size(), 1) * sizeof(double));
   CUDA_TRY(cudaMemsetAsync(c->d_dropped, 0, 2 * std::max<size_t>(ids.size(), 1) * sizeof(double), c->st));
   // Waves of pairwise non-adjacent interfaces (no shared block).  The
@@ -3170,6 +3668,8 @@ void ensure_chain_scratch(spq_ctx* c, int nrhs) {
   for (auto& r : c->recs) {
     maxk = std::max<size_t>(maxk, (size_t)std::max(r.k, r.m));
     maxp = std::max<size_t>(maxp, (size_t)chain_rsn_chunks(r.n) * std::max(r.k, 1));
+    if (r.unscaled)   // TRI op with R_ff (f x f) and R_fc (f x rank)
+      maxp = std::max<size_t>(maxp, (size_t)chain_rsn_chunks(r.k) * std::max(r.f, 1));
   }
   const size_t vneed = (size_t)c->N * nrhs;
   if (vneed > c->vec_cap) {
@@ -3307,7 +3807,7 @@ void build_chain_W(spq_ctx* c) {
   const int kmin = env_flag("SPQ_CHAIN_W") ? 1 : CHAIN_W_KMIN;
   size_t need = 0;
   for (auto& r : c->recs)
-    if (r.k >= kmin) need += (size_t)r.m * r.k * (r.kind == REC_SPARSIFY ? 2 : 1);
+    if (r.k >= kmin && !r.unscaled) need += (size_t)r.m * r.k * (r.kind == REC_SPARSIFY ? 2 : 1);
   if (need == 0 || env_flag("SPQ_CHAIN_NO_W")) return;
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
@@ -3316,7 +3816,7 @@ void build_chain_W(spq_ctx* c) {
   GemmBatch gT, gN;
   std::vector<double*> tts;
   for (auto& r : c->recs) {
-    if (r.k < kmin) continue;
+    if (r.k < kmin || r.unscaled) continue;
     const size_t mk = (size_t)r.m * r.k, kk = (size_t)r.k * r.k;
     const bool sp = r.kind == REC_SPARSIFY;
     r.WT = dalloc(c, mk * sizeof(double));
@@ -3342,8 +3842,15 @@ void compile_chains(spq_ctx* c) {
   std::vector<ChainOp> ops;
   std::vector<std::vector<int>> wr, rd;
   auto to_int = [](const std::vector<int64_t>& v) { return std::vector<int>(v.begin(), v.end()); };
-  // apply_qt: every record's panel on its rows, in chain order
+  // apply_qt: every record's panel on its rows, in chain order (an unscaled
+  // sparsifier's Q-side is its H_f panel, factor.py:183-186)
   for (auto& r : c->recs) {
+    if (r.unscaled) {
+      ops.push_back(ChainOp{CH_WY_T, r.m, r.f, 0, r.d_rows, nullptr, r.hV, r.hT, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 1, 1, 0});
+      wr.push_back(to_int(r.rows));
+      rd.push_back({});
+      continue;
+    }
     if (r.k <= 0) continue;
     ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_rows, nullptr, r.V, r.T, nullptr, nullptr, nullptr, r.WT, nullptr, 0, 1, 1, 0});
     wr.push_back(to_int(r.rows));
@@ -3354,6 +3861,19 @@ void compile_chains(spq_ctx* c) {
   ops.clear(); wr.clear(); rd.clear();
   for (auto it = c->recs.rbegin(); it != c->recs.rend(); ++it) {
     Record& r = *it;
+    if (r.unscaled) {
+      // v = y[cols]; v[r:] = R_ff^{-1}(v[r:] - R_fc v[:r]); y[cols] = Q v  (factor.py:195-203)
+      ops.push_back(ChainOp{CH_TRI_SOLVE, r.f, r.f, r.k, r.d_cols_f, r.d_cols_c, nullptr, nullptr,
+                            r.R, r.Rsn, nullptr, nullptr, nullptr, 0, 1, 1, 0});
+      wr.push_back(to_int(r.cols_f));
+      rd.push_back(to_int(r.cols_c));
+      if (r.k > 0) {
+        ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 1, 1, 0});
+        wr.push_back(to_int(r.cols_s));
+        rd.push_back({});
+      }
+      continue;
+    }
     if (r.kind == REC_SPARSIFY) {
       if (r.k <= 0) continue;
       ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, r.WN, nullptr, 0, 1, 1, 0});
@@ -3372,6 +3892,19 @@ void compile_chains(spq_ctx* c) {
   // apply_w: forward W-chain (after the diagonal scaling)
   ops.clear(); wr.clear(); rd.clear();
   for (auto& r : c->recs) {
+    if (r.unscaled) {
+      // v = Q^T x[cols]; v[r:] = R_ff v[r:] + R_fc v[:r]  (factor.py:188-193)
+      if (r.k > 0) {
+        ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 1, 1, 0});
+        wr.push_back(to_int(r.cols_s));
+        rd.push_back({});
+      }
+      ops.push_back(ChainOp{CH_TRI_MUL, r.f, r.f, r.k, r.d_cols_f, r.d_cols_c, nullptr, nullptr,
+                            r.R, r.Rsn, nullptr, nullptr, nullptr, 0, 1, 1, 0});
+      wr.push_back(to_int(r.cols_f));
+      rd.push_back(to_int(r.cols_c));
+      continue;
+    }
     if (r.k <= 0) continue;
     if (r.kind == REC_SPARSIFY) {
       ops.push_back(ChainOp{CH_WY_T, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, r.WT, nullptr, 0, 1, 1, 0});
@@ -3638,12 +4171,20 @@ int spq_scale(spq_ctx* c, int n, const int32_t* ids, int32_t* out_done) {
 
 int spq_sparsify(spq_ctx* c, int n, const int32_t* ids, double eps, int32_t* out_rank,
                  int32_t* out_before, double* out_dropped, int32_t* out_done) {
+  return spq_sparsify_ex(c, n, ids, eps, SPM_SCALED, 1, out_rank, out_before, out_dropped,
+                         out_done);
+}
+
+int spq_sparsify_ex(spq_ctx* c, int n, const int32_t* ids, double eps, int mode, int scaled_now,
+                    int32_t* out_rank, int32_t* out_before, double* out_dropped,
+                    int32_t* out_done) {
   return guarded(c, [&] {
+    if (mode < SPM_SCALED || mode > SPM_VARIANT2) throw SpqError(SPQ_ERR_BAD_INPUT, "sparsify mode");
     for (int t = 0; t < n; ++t) {
       out_rank[t] = -1; out_before[t] = 0; out_dropped[t] = 0.0; out_done[t] = 0;
     }
     std::vector<SparsifyOut> outs;
-    do_sparsify(c, std::vector<int>(ids, ids + n), eps, outs);
+    do_sparsify(c, std::vector<int>(ids, ids + n), eps, outs, mode, scaled_now != 0);
     for (int t = 0; t < n; ++t) {
       out_rank[t] = outs[t].rank;
       out_before[t] = outs[t].before;
@@ -3674,7 +4215,7 @@ int spq_finish(spq_ctx* c) {
     std::vector<int> pack(c->row_of_col.begin(), c->row_of_col.end());
     std::vector<size_t> offs;
     for (auto& r : c->recs)
-      for (auto* v : {&r.rows, &r.cols_s, &r.cols_n}) {
+      for (auto* v : {&r.rows, &r.cols_s, &r.cols_n, &r.cols_f, &r.cols_c}) {
         offs.push_back(pack.size());
         pack.insert(pack.end(), v->begin(), v->end());
       }
@@ -3687,6 +4228,8 @@ int spq_finish(spq_ctx* c) {
       r.d_rows = d + offs[q++];
       r.d_cols_s = d + offs[q++];
       r.d_cols_n = d + offs[q++];
+      r.d_cols_f = d + offs[q++];
+      r.d_cols_c = d + offs[q++];
     }
     std::vector<TProb> tp;
     for (auto& r : c->recs)
@@ -3853,6 +4396,9 @@ int spq_record_info(spq_ctx* c, int idx, int64_t* info) {
     if (idx < 0 || idx >= (int)c->recs.size()) throw SpqError(SPQ_ERR_BAD_INPUT, "record index");
     Record& r = c->recs[idx];
     info[0] = r.kind; info[1] = r.m; info[2] = r.k; info[3] = r.n; info[4] = r.rank;
+    info[5] = r.cid;
+    info[6] = r.unscaled ? 1 : 0;
+    info[7] = r.f;
   });
 }
 
@@ -3871,8 +4417,17 @@ int spq_record_get(spq_ctx* c, int idx, int which, void* out) {
       case 3: cp(r.V, (size_t)r.m * r.k); break;
       case 4: cp(r.tau, r.k); break;
       case 5: cp(r.T, (size_t)r.k * r.k); break;
-      case 6: if (r.R) cp(r.R, (size_t)r.k * r.k); break;
-      case 7: if (r.Rsn) cp(r.Rsn, (size_t)r.k * r.n); break;
+      case 6:
+        if (r.unscaled) cp(r.R, (size_t)r.f * r.f);        // R_ff
+        else if (r.R) cp(r.R, (size_t)r.k * r.k);
+        break;
+      case 7:
+        if (r.unscaled) cp(r.Rsn, (size_t)r.f * r.k);      // R_fc
+        else if (r.Rsn) cp(r.Rsn, (size_t)r.k * r.n);
+        break;
+      case 8: if (r.unscaled) cp(r.hV, (size_t)r.m * r.f); break;
+      case 9: if (r.unscaled) cp(r.htau, r.f); break;
+      case 10: if (r.unscaled) cp(r.hT, (size_t)r.f * r.f); break;
       default: throw SpqError(SPQ_ERR_BAD_INPUT, "record field");
     }
   });

@@ -58,6 +58,8 @@ class _RecordView:
         # device memory is released as soon as the last user drops F
         self._ctx, self._idx = F._ctx, idx
         self._m, self._k, self._n, self._rank = (int(x) for x in info[1:5])
+        self.cid = int(info[5])          # cluster eliminated / scaled / compressed
+        self._unscaled, self._f = bool(info[6]), int(info[7])
         self._cache = {}
 
     def _get(self, which):
@@ -125,12 +127,16 @@ class InterfaceScaling(_RecordView):
 
 
 class Sparsifier(_RecordView):
-    """Scaled sparsifier record (reference `factor.py:145-205`)."""
+    """Sparsifier record (reference `factor.py:145-205`): scaled flavour
+    (Q panel only) or unscaled flavour (Q panel + H_f panel, R_ff, R_fc)."""
     kind = 3
-    scaled = True
 
     cols = property(lambda s: s._get(1))
     rank = property(lambda s: s._rank)
+
+    @property
+    def scaled(self):
+        return not self._unscaled
 
     @property
     def fine(self):
@@ -140,9 +146,37 @@ class Sparsifier(_RecordView):
     def q_panel(self):
         return self.panel
 
+    def _getu(self, which, shape):
+        if which not in self._cache:
+            out = np.empty(shape[::-1] if len(shape) == 2 else shape)
+            if out.size:
+                self._ctx.call("spq_record_get", self._idx, which, out.ctypes.data)
+            self._cache[which] = np.ascontiguousarray(out.T) if len(shape) == 2 else out
+        return self._cache[which]
+
+    @property
+    def hf_panel(self):
+        if self.scaled:
+            return None
+        f, m = self._f, self._m
+        return HouseholderPanel(self._getu(8, (m, f)), self._getu(9, (f,)),
+                                self._getu(10, (f, f)), self.rows)
+
+    @property
+    def R_ff(self):
+        return None if self.scaled else self._getu(6, (self._f, self._f))
+
+    @property
+    def R_fc(self):
+        return None if self.scaled else self._getu(7, (self._f, self._rank))
+
     @property
     def payload_scalars(self):
-        return self._m * self._k + self._k + self._k * self._k
+        n = self._m * self._k + self._k + self._k * self._k
+        if not self.scaled:
+            f = self._f
+            n += self._m * f + f + f * f + f * f + f * self._rank
+        return n
 
 
 class Permutation:
@@ -185,7 +219,7 @@ class Factorization:
         if self._records is None:
             n = self._ctx.lib.spq_num_records(self._ctx.h)
             recs = []
-            info = np.zeros(5, np.int64)
+            info = np.zeros(8, np.int64)
             for i in range(n):
                 self._ctx.call("spq_record_info", i, info)
                 recs.append(_VIEW[int(info[0])](self, i, info.copy()))
@@ -312,26 +346,57 @@ def factorize(A, tree=None, eps=1e-3, **kw):
     out-of-memory failure the context is released, garbage is collected and
     the factorization runs once more."""
     try:
-        return _factorize(A, tree, eps, **kw)
+        return _factorize_spec(A, tree, eps, **kw)
     except DeviceError as e:
         if "out of memory" not in str(e):
             raise
     import gc
     gc.collect()
-    return _factorize(A, tree, eps, **kw)
+    return _factorize_spec(A, tree, eps, **kw)
+
+
+def _factorize_spec(A, tree, eps, **kw):
+    """A predicted row-nonzero flag that the device finds wrong (an exact
+    cancellation the symbolic rules cannot see) surfaces as SpeculationError
+    at the next synchronisation point, anywhere in the level loop: redo the
+    factorization with flags read back exactly.  The failed attempt's device
+    time stays in the measured total."""
+    held = {}
+    try:
+        return _factorize(A, tree, eps, _held=held, **kw)
+    except SpeculationError:
+        if not kw.get("_speculate", True):
+            raise
+    ctx = held.get("ctx")
+    lost_ms = 0.0
+    if ctx is not None:
+        if kw.get("_marks"):
+            import ctypes as C
+            ms = C.c_float()
+            ctx.call("spq_mark", 1)
+            ctx.call("spq_synchronize")
+            ctx.call("spq_mark_elapsed", 0, 1, C.byref(ms))
+            lost_ms = float(ms.value)
+        ctx.close()
+    kw = dict(kw, _speculate=False)
+    F = _factorize(A, tree, eps, **kw)
+    F.spec_retries = 1
+    if F.device_ms is not None:
+        F.device_ms += lost_ms
+    return F
 
 
 def _factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=True,
                scale_every=1, skip=2, sparsify_min=40, mode="scaled",
                row_heuristic="same-as-columns", equilibrate=True, observer=None, device=0,
-               _marks=False, _memstats=False, _speculate=True):
+               _marks=False, _memstats=False, _speculate=True, _held=None):
     if mode not in MODES:
         raise NestqrError(f"unknown sparsification mode {mode!r}")
     if mode == "unscaled":
         scaling = False
-    if sparsify and (mode != "scaled" or not scaling or scale_every != 1):
-        raise NestqrError("the B200 path implements scaled-mode sparsification with "
-                          "scale_every=1 (unscaled/variant modes are a later row, SURVEY §8f)")
+    if int(scale_every) < 1:
+        raise NestqrError(f"scale_every must be >= 1, got {scale_every}")
+    mode_id = MODES.index(mode)
     if tree is None:
         raise NestqrError("the B200 path needs a cluster tree (e.g. ordering.partition_geometric)")
     n, m, indptr, indices, data = as_csc(A)
@@ -345,6 +410,8 @@ def _factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tr
         assign_rows_same_as_columns(tree)
     L = tree.L
     ctx = Context(device)
+    if _held is not None:
+        _held["ctx"] = ctx
     if not _speculate:
         ctx.call("spq_set_option", b"speculate", 0)
     leaf_ids = np.array([c.id for c in leaves], np.int32)
@@ -400,13 +467,16 @@ def _factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tr
             n_sparsified_levels += 1
             psz = sizes_of(pending[lev])
             todo = [p for p, z in zip(pending[lev], psz) if z >= sparsify_min]
+            # scaling on every scale_every-th sparsified level (factor.py:847-861)
+            do_scale = bool(scaling) and (n_sparsified_levels - 1) % int(scale_every) == 0
             if todo:
                 ids_t = np.asarray(todo, np.int32)
-                t0 = time.perf_counter()
-                done = np.zeros(len(todo), np.int32)
-                ctx.call("spq_scale", len(todo), ids_t, done)
-                st["n_scaled"] = int(done.sum())
-                st["t_scale"] = time.perf_counter() - t0
+                if do_scale:
+                    t0 = time.perf_counter()
+                    done = np.zeros(len(todo), np.int32)
+                    ctx.call("spq_scale", len(todo), ids_t, done)
+                    st["n_scaled"] = int(done.sum())
+                    st["t_scale"] = time.perf_counter() - t0
                 on_sp = getattr(observer, "on_sparsify", None)
                 t0 = time.perf_counter()
                 rank = np.zeros(len(todo), np.int32)
@@ -414,14 +484,15 @@ def _factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tr
                 dropped = np.zeros(len(todo))
                 done = np.zeros(len(todo), np.int32)
                 if on_sp is None:
-                    ctx.call("spq_sparsify", len(todo), ids_t, float(eps), rank, before,
-                             dropped, done)
+                    ctx.call("spq_sparsify_ex", len(todo), ids_t, float(eps), mode_id,
+                             int(do_scale), rank, before, dropped, done)
                 else:
                     for t, p in enumerate(todo):
                         on_sp(state, p, "before")
                         r1, b1 = np.zeros(1, np.int32), np.zeros(1, np.int32)
                         d1, k1 = np.zeros(1), np.zeros(1, np.int32)
-                        ctx.call("spq_sparsify", 1, ids_t[t:t + 1], float(eps), r1, b1, d1, k1)
+                        ctx.call("spq_sparsify_ex", 1, ids_t[t:t + 1], float(eps), mode_id,
+                                 int(do_scale), r1, b1, d1, k1)
                         rank[t], before[t], dropped[t], done[t] = r1[0], b1[0], d1[0], k1[0]
                         on_sp(state, p, "after")
                 for t in range(len(todo)):
@@ -465,29 +536,7 @@ def _factorize(A, tree=None, eps=1e-3, *, levels=None, sparsify=True, scaling=Tr
             st["t_merge"] = time.perf_counter() - t0
         stats.append(st)
 
-    try:
-        ctx.call("spq_finish")
-    except SpeculationError:
-        # a predicted row-nonzero flag was wrong (an exact cancellation the
-        # symbolic rules cannot see): redo with flags read back exactly; the
-        # failed attempt's device time stays in the measured total
-        lost_ms = 0.0
-        if _marks:
-            ctx.call("spq_mark", 1)
-            ms = C.c_float()
-            ctx.call("spq_synchronize")
-            ctx.call("spq_mark_elapsed", 0, 1, C.byref(ms))
-            lost_ms = float(ms.value)
-        ctx.close()
-        F = factorize(A, tree, eps, levels=levels, sparsify=sparsify, scaling=scaling,
-                      scale_every=scale_every, skip=skip, sparsify_min=sparsify_min,
-                      mode=mode, row_heuristic=row_heuristic, equilibrate=equilibrate,
-                      observer=observer, device=device, _marks=_marks,
-                      _memstats=_memstats, _speculate=False)
-        F.spec_retries = getattr(F, "spec_retries", 0) + 1
-        if F.device_ms is not None:
-            F.device_ms += lost_ms
-        return F
+    ctx.call("spq_finish")
     if getattr(observer, "on_level", None) is None and stats:
         nnz = np.zeros(len(stats), np.int64)
         ctx.call("spq_trailing_nnz", len(stats), nnz)

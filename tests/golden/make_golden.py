@@ -59,6 +59,11 @@ CASES = {
     "C4_n12_unscaled": ("C4", 12, {"mode": "unscaled"}),
     "C3_n96_unscaled": ("C3", 96, {"mode": "unscaled"}),
     "C3_n96_se2": ("C3", 96, {"scale_every": 2}),
+    # one-sided / Gram compression targets (factor.py:541-551)
+    "C3_n48_variant1": ("C3", 48, {"mode": "variant1"}),
+    "C3_n48_variant2": ("C3", 48, {"mode": "variant2"}),
+    "C1_variant1_se2": ("C1", None, {"mode": "variant1", "scale_every": 2}),
+    "C1_variant2_se2": ("C1", None, {"mode": "variant2", "scale_every": 2}),
 }
 # full-size metric configs; the numpy-backend envelope run is part of them
 BIG = {"C3": ("C3", None, {}), "C4": ("C4", None, {})}
@@ -166,14 +171,56 @@ def _chain_vectors(F, N):
     return {"apply_qt": F.apply_qt(v), "solve_w": F.solve_w(v), "apply_w": F.apply_w(v)}
 
 
+class KeyLog:
+    """Cluster id of every record, per kind, in chain order (wraps the
+    reference's TrailingState level operations; results untouched)."""
+
+    def __init__(self):
+        import nestqr.factor as NF
+        self.keys = {"bh": [], "is": [], "sp": []}
+        TS = NF.TrailingState
+        self._orig = (TS.factor_interior, TS.scale_interface, TS.sparsify_interface)
+        log = self.keys
+        fi, si, spi = self._orig
+
+        def factor_interior(st, s):
+            rec = fi(st, s)
+            if rec is not None:
+                log["bh"].append(s)
+            return rec
+
+        def scale_interface(st, p):
+            rec = si(st, p)
+            if rec is not None:
+                log["is"].append(p)
+            return rec
+
+        def sparsify_interface(st, p, *a, **k):
+            rec, dropped = spi(st, p, *a, **k)
+            if rec is not None:
+                log["sp"].append(p)
+            return rec, dropped
+
+        TS.factor_interior, TS.scale_interface = factor_interior, scale_interface
+        TS.sparsify_interface = sparsify_interface
+        self._TS = TS
+
+    def close(self):
+        self._TS.factor_interior, self._TS.scale_interface, self._TS.sparsify_interface = self._orig
+
+
 def factor_case(name, cfg, n, envelope=None, **opts):
     A0, dims, L, eps, b, tol = make_config(cfg, n=n)
     A = SparseMat(A0.nrows, A0.ncols, A0.indptr, A0.indices, A0.data)
     tree = ref_partition(dims, L)
     K.set_backend("numba")
     log = RankLog()
+    klog = KeyLog()
     t0 = time.perf_counter()
-    F = factorize(A, tree, eps=eps, observer=log, **opts)
+    try:
+        F = factorize(A, tree, eps=eps, observer=log, **opts)
+    finally:
+        klog.close()
     t_fac = time.perf_counter() - t0
     t0 = time.perf_counter()
     x, rep = gmres(A, b, F, tol=tol)
@@ -189,6 +236,13 @@ def factor_case(name, cfg, n, envelope=None, **opts):
     out["row_of_col"] = F.row_of_col
     out["payload"] = np.int64(F.payload_scalars)
     bh, isc, sp = _records(F)
+    # cluster id of every record (records of independent clusters commute, so
+    # the device's chain order may differ; the comparison matches by id)
+    out["bh_key"] = np.array(klog.keys["bh"], dtype=np.int64)
+    out["rpp_key"] = np.array(klog.keys["is"], dtype=np.int64)
+    out["sp_key"] = np.array(klog.keys["sp"], dtype=np.int64)
+    assert len(out["bh_key"]) == len(bh) and len(out["rpp_key"]) == len(isc)
+    assert len(out["sp_key"]) == len(sp)
     # ---- elimination records (factor.py:486-493): R_ss, R_sn
     out["rss_diag"] = np.concatenate([np.diag(r.R_ss) for r in bh])
     out["rss_k"] = np.array([r.R_ss.shape[0] for r in bh])
@@ -247,12 +301,16 @@ def factor_case(name, cfg, n, envelope=None, **opts):
     out["x_norm"] = np.float64(np.linalg.norm(x))
     # rounding envelope (F3): numpy backend on the same inputs
     if envelope is None:
-        envelope = A.ncols <= 8192
+        envelope = A.ncols <= 16384
     if envelope:
         K.set_backend("numpy")
         t0 = time.perf_counter()
         F2 = factorize(A, tree, eps=eps, **opts)
         out["t_factor_numpy"] = np.float64(time.perf_counter() - t0)
+        # structure decided by exact zeros (panel rows with any nonzero,
+        # trailing_nnz) is itself rounding-dependent: the numpy twin's values
+        out["payload_numpy"] = np.int64(F2.payload_scalars)
+        out["stats_numpy"] = np.array([[float(s_[k]) for k in keys] for s_ in F2.stats])
         K.set_backend("numba")
         bh2, isc2, sp2 = _records(F2)
         out["rss_envelope"] = np.array([_rel(a.R_ss, c.R_ss) for a, c in zip(bh2, bh)])
