@@ -242,7 +242,7 @@ int cpqr_reg_plan(int m, int n, int variant, int* tpc);
 size_t cpqr_reg_smem(int padded_rows, int cl);
 void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int variant, int cl, int tpc, size_t smem,
                      cudaStream_t st);
-void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax,
+void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax, int slab_k,
                        double* part, double* z, int64_t N, int nrhs, cudaStream_t st);
 }  // namespace spq
 

@@ -10,6 +10,7 @@
 //     partial sums + one reduction CTA), then R_ss back substitution.
 //   apply_w: y_s = R_ss x_s + R_sn x_n ; DiagonalScaling ; Permutation.
 // All HBM-bound (~0.4 flop/byte).
+#include <algorithm>
 #include <string>
 
 #include "common.cuh"
@@ -295,21 +296,27 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseA_kernel(const ChainOp* __re
           for (int q = 16; q; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
           if (lane == 0) u[a] = s;
         }
-      } else if (!o.W) {                 // (T w)_a = sum_{b>=a} T[a,b] w_b: thread per a (coalesced)
-        for (int a = tid; a < k; a += CW_NT) {
+      } else if (!o.W) {                 // (T w)_a = sum_{b>=a} T[a,b] w_b: warp per a, lanes over b
+        for (int a = warp; a < k; a += CW_NW) {
           double s = 0.0;
-          for (int b = a; b < k; ++b) s = fma(o.T[a + (int64_t)b * k], sm ? wv[b] : __ldcg(wv + b), s);
-          u[a] = s;
+          for (int b = a + lane; b < k; b += 32) s = fma(o.T[a + (int64_t)b * k], sm ? wv[b] : __ldcg(wv + b), s);
+#pragma unroll
+          for (int q = 16; q; q >>= 1) s += __shfl_xor_sync(0xffffffffu, s, q);
+          if (lane == 0) u[a] = s;
         }
       }
       __syncthreads();
     }
     if (tid == 0) *o.cnt = 0;   // ready for the next application
     return;
-  } else if (o.n > 0) {
-    // R_sn[:, chunk] y[chunk]: rows a split over threads, columns over P partitions
+  } else if (o.n > 0 || o.kind == CH_TRI_MUL) {
+    // [R | R_sn][:, chunk] [y_s; y_n][chunk] (TRI_MUL: the whole product, R
+    // upper triangular; TRI_SOLVE: the R_sn part only): rows a split over
+    // threads, columns over P partitions
     __shared__ double redA[CW_NT];
-    const int j0 = chunk * o.per, j1 = min(o.n, j0 + o.per);
+    const bool mul = o.kind == CH_TRI_MUL;
+    const int ncol = mul ? k + o.n : o.n;
+    const int j0 = chunk * o.per, j1 = min(ncol, j0 + o.per);
     int P = CW_NT / max(k, 1);
     P = P >= 16 ? 16 : (P >= 8 ? 8 : (P >= 4 ? 4 : (P >= 2 ? 2 : 1)));
     const int rows_per_pass = CW_NT / P;
@@ -318,8 +325,19 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseA_kernel(const ChainOp* __re
       for (int a0 = 0; a0 < k; a0 += rows_per_pass) {
         const int a = a0 + tid % rows_per_pass, jp = tid / rows_per_pass;
         double s = 0.0;
-        if (a < k)
-          for (int j = j0 + jp; j < j1; j += P) s += o.Rsn[a + (int64_t)j * k] * zr[o.idx_n[j]];
+        if (a < k) {
+          if (mul) {
+            for (int j = j0 + jp; j < j1; j += P) {
+              if (j < k) {
+                if (a <= j) s += o.R[a + (int64_t)j * k] * zr[o.idx[j]];
+              } else {
+                s += o.Rsn[a + (int64_t)(j - k) * k] * zr[o.idx_n[j - k]];
+              }
+            }
+          } else {
+            for (int j = j0 + jp; j < j1; j += P) s += o.Rsn[a + (int64_t)j * k] * zr[o.idx_n[j]];
+          }
+        }
         redA[tid] = s;
         __syncthreads();
         if (tid < rows_per_pass && a0 + tid < k) {
@@ -333,11 +351,34 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseA_kernel(const ChainOp* __re
   }
 }
 
+// Back substitution of one (wd <= 32) upper-triangular diagonal block by a
+// single warp: lane l holds row l of the block in registers and its
+// reciprocal pivot, so each of the wd sequential steps is one shuffle and one
+// FMA (the pivot division -- a long multi-instruction sequence -- is off the
+// dependency chain; x * (1/d) differs from x / d by at most one rounding).
+__device__ __forceinline__ void tri32_backsolve(const double* D, int ldd, int wd, double* wv,
+                                                int lane) {
+  double rrow[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) rrow[j] = (j < wd && lane < j) ? D[lane + (int64_t)j * ldd] : 0.0;
+  const double dinv = lane < wd ? 1.0 / D[lane + (int64_t)lane * ldd] : 0.0;
+  double wl = lane < wd ? wv[lane] : 0.0;
+#pragma unroll
+  for (int i = 31; i >= 0; --i) {
+    if (i < wd) {
+      if (lane == i) wl *= dinv;
+      const double xi = __shfl_sync(0xffffffffu, wl, i);
+      if (lane < i) wl = fma(-rrow[i], xi, wl);
+    }
+  }
+  if (lane < wd) wv[lane] = wl;
+}
+
 __global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __restrict__ ops,
                                                              const int2* __restrict__ tasks,
                                                              const double* __restrict__ part,
                                                              double* __restrict__ z, int64_t N,
-                                                             int nrhs) {
+                                                             int nrhs, int slab_k) {
   const int2 tk = tasks[blockIdx.x];
   const ChainOp o = ops[tk.x];
   const int chunk = tk.y;
@@ -357,40 +398,99 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __re
       for (int c = tid; c < k; c += CW_NT) w[c] = __ldcg(u + c);
       __syncthreads();
       const double* M = o.W ? o.W : o.V;
-      const int i0 = chunk * o.per, i1 = min(o.m, i0 + o.per);
-      for (int i = i0 + tid; i < i1; i += CW_NT) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int c = 0;
-        for (; c + 3 < k; c += 4) {
-          s0 = fma(M[i + (int64_t)c * o.m], w[c], s0);
-          s1 = fma(M[i + (int64_t)(c + 1) * o.m], w[c + 1], s1);
-          s2 = fma(M[i + (int64_t)(c + 2) * o.m], w[c + 2], s2);
-          s3 = fma(M[i + (int64_t)(c + 3) * o.m], w[c + 3], s3);
+      const int i0 = chunk * o.per, i1 = min(o.m, i0 + o.per), nrow = i1 - i0;
+      if (nrow <= CW_NT / 2) {
+        // few rows: TPR threads per row split the k columns (every thread
+        // keeps independent loads in flight; rows stay coalesced per column),
+        // partial sums reduced in a fixed order through shared memory
+        __shared__ double redB[CW_NT];
+        int rp = 1;
+        while (rp < nrow) rp <<= 1;
+        const int tpr = CW_NT / rp, row = tid % rp, cs = tid / rp;
+        double s0 = 0.0, s1 = 0.0;
+        if (row < nrow) {
+          const double* Mi = M + i0 + row;
+          int c = cs;
+          for (; c + tpr < k; c += 2 * tpr) {
+            s0 = fma(Mi[(int64_t)c * o.m], w[c], s0);
+            s1 = fma(Mi[(int64_t)(c + tpr) * o.m], w[c + tpr], s1);
+          }
+          if (c < k) s0 = fma(Mi[(int64_t)c * o.m], w[c], s0);
         }
-        for (; c < k; ++c) s0 = fma(M[i + (int64_t)c * o.m], w[c], s0);
-        zr[o.idx[i]] -= (s0 + s1) + (s2 + s3);
+        redB[tid] = s0 + s1;
+        __syncthreads();
+        if (cs == 0 && row < nrow) {
+          double t = 0.0;
+          for (int q = 0; q < tpr; ++q) t += redB[row + q * rp];
+          zr[o.idx[i0 + row]] -= t;
+        }
+        __syncthreads();
+      } else {
+        for (int i = i0 + tid; i < i1; i += CW_NT) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          int c = 0;
+          for (; c + 3 < k; c += 4) {
+            s0 = fma(M[i + (int64_t)c * o.m], w[c], s0);
+            s1 = fma(M[i + (int64_t)(c + 1) * o.m], w[c + 1], s1);
+            s2 = fma(M[i + (int64_t)(c + 2) * o.m], w[c + 2], s2);
+            s3 = fma(M[i + (int64_t)(c + 3) * o.m], w[c + 3], s3);
+          }
+          for (; c < k; ++c) s0 = fma(M[i + (int64_t)c * o.m], w[c], s0);
+          zr[o.idx[i]] -= (s0 + s1) + (s2 + s3);
+        }
+        __syncthreads();
       }
-      __syncthreads();
     } else {
       if (chunk != 0) return;
-      if (o.n > 0) {
-        chain_reduce_partials(pr, o.nchunk, k, w);   // R_sn y_n partials
+      if (o.n > 0 || o.kind == CH_TRI_MUL) {
+        // R_sn y_n partials (TRI_SOLVE) / R y_s + R_sn y_n partials (TRI_MUL)
+        chain_reduce_partials(pr, o.nchunk, k, w);
       } else {
         for (int a = tid; a < k; a += CW_NT) w[a] = 0.0;
       }
       __syncthreads();
-      for (int a = tid; a < k; a += CW_NT) {
-        const double s = w[a];
-        if (o.kind == CH_TRI_SOLVE) {
-          w[a] = zr[o.idx[a]] - s;
-        } else {   // CH_TRI_MUL: R y_s + R_sn y_n
-          double t2 = 0.0;
-          for (int b = a; b < k; ++b) t2 += o.R[a + (int64_t)b * k] * zr[o.idx[b]];
-          w[a] = t2 + s;
-        }
-      }
+      if (o.kind == CH_TRI_SOLVE)
+        for (int a = tid; a < k; a += CW_NT) w[a] = zr[o.idx[a]] - w[a];
       __syncthreads();
-      if (o.kind == CH_TRI_SOLVE) {
+      if (o.kind == CH_TRI_SOLVE && k > 32 && k <= slab_k) {
+        // blocked back substitution, 32 columns per block from the bottom;
+        // the R slab of the next block (rows 0..i1, its 32 columns) streams
+        // into shared memory (cp.async, double buffered) while the current
+        // block is solved, so the solve never waits on a global load
+        double* slab = cw + 2 * (int64_t)slab_k;     // two buffers of slab_k x 32
+        const int nb = (k + 31) / 32;
+        auto issue = [&](int t) {
+          const int i1 = k - 32 * t, i0 = max(0, i1 - 32), wd = i1 - i0;
+          double* dst = slab + (int64_t)(t & 1) * slab_k * 32;
+          for (int e = tid; e < i1 * wd; e += CW_NT) {
+            const int a = e % i1, b = e / i1;
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + a + (int64_t)b * i1);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa),
+                         "l"(o.R + (i0 + b) * (int64_t)k + a) : "memory");
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        issue(0);
+        for (int t = 0; t < nb; ++t) {
+          if (t + 1 < nb) {
+            issue(t + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+          } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+          }
+          __syncthreads();
+          const int i1 = k - 32 * t, i0 = max(0, i1 - 32), wd = i1 - i0;
+          const double* S = slab + (int64_t)(t & 1) * slab_k * 32;   // i1 x wd, ld i1
+          if (warp == 0) tri32_backsolve(S + i0, i1, wd, w + i0, lane);
+          __syncthreads();
+          for (int a = tid; a < i0; a += CW_NT) {
+            double s = 0.0;
+            for (int b = 0; b < wd; ++b) s = fma(S[a + (int64_t)b * i1], w[i0 + b], s);
+            w[a] -= s;
+          }
+          __syncthreads();
+        }
+      } else if (o.kind == CH_TRI_SOLVE) {
         for (int i1 = k; i1 > 0; i1 -= 32) {
           const int i0 = max(0, i1 - 32), wd = i1 - i0;
           for (int e = tid; e < wd * wd; e += CW_NT) {     // stage the diagonal block
@@ -398,15 +498,7 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __re
             Rd[a + b * 33] = o.R[(i0 + a) + (int64_t)(i0 + b) * k];
           }
           __syncthreads();
-          if (warp == 0) {
-            double wl = lane < wd ? w[i0 + lane] : 0.0;
-            for (int i = wd - 1; i >= 0; --i) {
-              const double xi = __shfl_sync(0xffffffffu, wl, i) / Rd[i + i * 33];
-              if (lane == i) wl = xi;
-              if (lane < i) wl -= Rd[lane + i * 33] * xi;
-            }
-            if (lane < wd) w[i0 + lane] = wl;
-          }
+          if (warp == 0) tri32_backsolve(Rd, 33, wd, w + i0, lane);
           __syncthreads();
           for (int a = tid; a < i0; a += CW_NT) {
             double s = 0.0;
@@ -422,15 +514,16 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __re
   }
 }
 
-size_t chain_wave_smem(int kmax) {
-  const size_t b = (size_t)2 * (kmax > 0 ? kmax : 1) * sizeof(double);
+size_t chain_wave_smem(int kmax, int slab_k) {
+  const size_t b = (size_t)2 * (kmax > 0 ? kmax : 1) * sizeof(double) +
+                   (size_t)64 * slab_k * sizeof(double);
   return b <= CHAIN_SMEM_MAX ? b : 0;
 }
 
-void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax,
+void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax, int slab_k,
                        double* part, double* z, int64_t N, int nrhs, cudaStream_t st) {
   if (ntasks <= 0) return;
-  const size_t smem = chain_wave_smem(kmax);
+  const size_t smem = chain_wave_smem(std::max(kmax, slab_k), slab_k);
   static size_t conf = 0;
   if (smem > conf) {   // the default 48 KB cap counts static + dynamic
     CUDA_TRY(cudaFuncSetAttribute(chain_phaseB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -448,7 +541,7 @@ void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, in
   fail("pending before chain wave");
   chain_phaseA_kernel<<<ntasks, CW_NT, 0, st>>>(d_ops, d_tasks, part, z, N, nrhs);
   fail("at chain phase A launch");
-  chain_phaseB_kernel<<<ntasks, CW_NT, smem, st>>>(d_ops, d_tasks, part, z, N, nrhs);
+  chain_phaseB_kernel<<<ntasks, CW_NT, smem, st>>>(d_ops, d_tasks, part, z, N, nrhs, slab_k);
   fail("at chain phase B launch");
 }
 

@@ -45,6 +45,7 @@ int chain_rsn_chunks(int n);
 void chain_diag(double* y, const double* s, int64_t N, int nrhs, bool divide, cudaStream_t st);
 void chain_perm(const double* z, const int* roc, int64_t N, int nrhs, double* out,
                 cudaStream_t st);
+constexpr int CHAIN_SLAB_KMAX = 320;
 }  // namespace spq
 
 using namespace spq;
@@ -468,8 +469,9 @@ struct spq_ctx {
     std::vector<int> toff, tcnt;          // per wave: task range
     std::vector<int64_t> part_sz;         // per wave: partial-sum doubles (x nrhs)
     std::map<int, double*> part_buf;      // nrhs -> wave scratch (max over waves)
-    std::vector<int> off, cnt, kmax;
+    std::vector<int> off, cnt, kmax, slabk;   // slabk: back-substitution slab width (0: none)
     std::map<int, cudaGraphExec_t> graphs;   // nrhs -> executable graph (z = d_vec)
+    std::vector<ChainOp> hops;               // host copy of the ordered ops (diagnostics)
   } prog[3];
 };
 
@@ -3704,51 +3706,63 @@ void ensure_chain_scratch(spq_ctx* c, int nrhs) {
 void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
                 const std::vector<std::vector<int>>& wr, const std::vector<std::vector<int>>& rd) {
   auto& P = c->prog[which];
-  std::vector<int> ws(c->N, -1), rs(c->N, -1);
-  int wave = 0;
+  // dependency levels: an op goes one wave after the latest earlier op it
+  // conflicts with (read-after-write, write-after-read, write-after-write on
+  // any index); ops of one level commute, so the chain is applied level by
+  // level -- the critical path of the record DAG, not a greedy in-order split
+  std::vector<int> lw(c->N, -1), lr(c->N, -1), lev(ops.size(), 0);
+  int nlev = 0;
+  for (size_t t = 0; t < ops.size(); ++t) {
+    int L = 0;
+    for (int i : wr[t]) L = std::max(L, std::max(lw[i], lr[i]) + 1);
+    for (int i : rd[t]) L = std::max(L, lw[i] + 1);
+    for (int i : wr[t]) lw[i] = L;
+    for (int i : rd[t]) lr[i] = std::max(lr[i], L);
+    lev[t] = L;
+    nlev = std::max(nlev, L + 1);
+  }
   std::vector<ChainOp> ordered;
   P.off.clear(); P.cnt.clear(); P.kmax.clear();
-  for (size_t t = 0; t < ops.size(); ++t) {
-    bool clash = P.off.empty();
-    if (!clash) {
-      for (int i : wr[t]) if (ws[i] == wave || rs[i] == wave) { clash = true; break; }
-      if (!clash) for (int i : rd[t]) if (ws[i] == wave) { clash = true; break; }
-    }
-    if (clash) {
-      ++wave;
+  {
+    std::vector<std::vector<int>> by(nlev);
+    for (size_t t = 0; t < ops.size(); ++t) by[lev[t]].push_back((int)t);
+    for (int L = 0; L < nlev; ++L) {
       P.off.push_back((int)ordered.size());
       P.cnt.push_back(0);
       P.kmax.push_back(0);
+      for (int t : by[L]) {
+        ordered.push_back(ops[t]);
+        P.cnt.back()++;
+        P.kmax.back() = std::max(P.kmax.back(), ops[t].k);
+      }
     }
-    for (int i : wr[t]) ws[i] = wave;
-    for (int i : rd[t]) rs[i] = wave;
-    ordered.push_back(ops[t]);
-    P.cnt.back()++;
-    P.kmax.back() = std::max(P.kmax.back(), ops[t].k);
   }
   // chunking: per wave, the operations split into chunks so the wave fills
-  // ~2 CTAs per SM (the chain is latency-bound wave by wave), at least 64
+  // ~4 CTAs per SM (the chain is latency-bound wave by wave), at least 32
   // rows (WY) / columns (R_sn) per chunk
   std::vector<int2> tasks;
-  P.toff.clear(); P.tcnt.clear(); P.part_sz.clear();
+  P.toff.clear(); P.tcnt.clear(); P.part_sz.clear(); P.slabk.clear();
   size_t scr = 0;
   for (size_t w = 0; w < P.off.size(); ++w) {
     double wave_work = 0;
     for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
       const ChainOp& o = ordered[t];
       const bool wy = o.kind == CH_WY_T || o.kind == CH_WY_N;
-      wave_work += (double)std::max<int64_t>(wy ? o.m : o.n, 1) * std::max(o.k, 1);
+      const int64_t len = wy ? o.m : (o.kind == CH_TRI_MUL ? (int64_t)o.k + o.n : o.n);
+      wave_work += (double)std::max<int64_t>(len, 1) * std::max(o.k, 1);
     }
-    const double per_cta = std::max(4096.0, wave_work / (2.0 * c->nsm));
+    const double per_cta = std::max(2048.0, wave_work / (4.0 * c->nsm));
     for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
       ChainOp& o = ordered[t];
       const bool wy = o.kind == CH_WY_T || o.kind == CH_WY_N;
-      const int64_t len = wy ? o.m : o.n;           // the dimension that is split
+      // the dimension that is split: WY rows; TRI_MUL the columns of [R | R_sn];
+      // TRI_SOLVE the R_sn columns (the back substitution stays in one CTA)
+      const int64_t len = wy ? o.m : (o.kind == CH_TRI_MUL ? (int64_t)o.k + o.n : o.n);
       const double work = (double)std::max(len, (int64_t)1) * std::max(o.k, 1);
       int64_t nch = (int64_t)std::ceil(work / per_cta);
-      nch = std::max<int64_t>(1, std::min<int64_t>(nch, (len + 63) / 64));
+      nch = std::max<int64_t>(1, std::min<int64_t>(nch, (len + 31) / 32));
       nch = std::min<int64_t>(nch, 512);
-      if (!wy && o.n == 0) nch = 1;
+      if (!wy && len == 0) nch = 1;
       o.per = (int)std::max<int64_t>(1, (len + nch - 1) / nch);
       o.nchunk = (int)std::max<int64_t>(1, (len + o.per - 1) / o.per);
       if ((size_t)2 * o.k * sizeof(double) > CHAIN_SMEM_MAX) scr += 3 * (size_t)o.k * o.nchunk;
@@ -3785,8 +3799,16 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
     }
     P.tcnt.push_back((int)tasks.size() - P.toff.back());
     P.kmax[w] = km;
+    int sk = 0;   // TRI_SOLVE ops whose R slabs stream through shared memory
+    for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
+      const ChainOp& o = ordered[t];
+      if (o.kind == CH_TRI_SOLVE && !o.scratch && o.k > 32 && o.k <= CHAIN_SLAB_KMAX) sk = std::max(sk, o.k);
+    }
+    if ((size_t)(2 * std::max(km, sk) + 64 * sk) * sizeof(double) > CHAIN_SMEM_MAX) sk = 0;
+    P.slabk.push_back(sk);
     P.part_sz.push_back(psz);
   }
+  if (env_flag("SPQ_CHAIN_PROFILE")) P.hops = ordered;
   if (!ordered.empty()) {
     P.d_ops = (ChainOp*)dalloc(c, ordered.size() * sizeof(ChainOp));
     CUDA_TRY(cudaMemcpyAsync(P.d_ops, ordered.data(), ordered.size() * sizeof(ChainOp),
@@ -3937,7 +3959,7 @@ void run_prog(spq_ctx* c, int which, double* z, int nrhs) {
   auto it = P.part_buf.find(nrhs);
   if (it == P.part_buf.end()) throw SpqError(SPQ_ERR_INTERNAL, "chain scratch missing");
   for (size_t w = 0; w < P.off.size(); ++w)
-    launch_chain_wave(P.d_ops + P.off[w], P.d_tasks + P.toff[w], P.tcnt[w], P.kmax[w],
+    launch_chain_wave(P.d_ops + P.off[w], P.d_tasks + P.toff[w], P.tcnt[w], P.kmax[w], P.slabk[w],
                       it->second, z, c->N, nrhs, c->st);
 }
 
@@ -3948,6 +3970,35 @@ void run_chain(spq_ctx* c, int which, int nrhs) {
     c->compiled = true;
   }
   auto& P = c->prog[which];
+  if (env_flag("SPQ_CHAIN_PROFILE") && which != 0) {
+    // diagnostics: every wave timed on its own (no graph), one line per wave
+    double* part = ensure_part(c, which, nrhs);
+    if (which == 2 && c->equil) chain_diag(c->d_vec, c->d_scale, c->N, nrhs, false, c->st);
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    for (size_t w = 0; w < P.off.size(); ++w) {
+      CUDA_TRY(cudaEventRecord(e0, c->st));
+      launch_chain_wave(P.d_ops + P.off[w], P.d_tasks + P.toff[w], P.tcnt[w], P.kmax[w], P.slabk[w], part,
+                        c->d_vec, c->N, nrhs, c->st);
+      CUDA_TRY(cudaEventRecord(e1, c->st));
+      CUDA_TRY(cudaEventSynchronize(e1));
+      float ms = 0;
+      CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      int nwy = 0, ntri = 0, kmx = 0, mmx = 0, nmx = 0;
+      for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
+        const ChainOp& o = P.hops[t];
+        (o.kind == CH_WY_T || o.kind == CH_WY_N ? nwy : ntri)++;
+        kmx = std::max(kmx, o.k); mmx = std::max(mmx, o.m); nmx = std::max(nmx, o.n);
+      }
+      fprintf(stderr, "chain %d wave %zu: %.1f us ops %d (wy %d tri %d) tasks %d kmax %d mmax %d nmax %d\n",
+              which, w, 1e3 * ms, P.cnt[w], nwy, ntri, P.tcnt[w], kmx, mmx, nmx);
+    }
+    if (which == 1 && c->equil) chain_diag(c->d_vec, c->d_scale, c->N, nrhs, true, c->st);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return;
+  }
   auto it = P.graphs.find(nrhs);
   if (it == P.graphs.end()) {
     ensure_part(c, which, nrhs);
