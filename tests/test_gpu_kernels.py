@@ -125,3 +125,32 @@ def test_build_t_matches_golden(K, gk):
         T = K.build_t(gk[f"qr{t}_V"], gk[f"qr{t}_tau"])
         Tr = gk[f"qr{t}_T"]
         assert np.abs(T - Tr).max() <= 1e-11 * max(1, np.abs(Tr).max())
+
+
+def test_nestqr_backend_module_contract(golden_dir):
+    """The `nestqr.kernels._impl` drop-in (paper_2010_06807_b200.nestqr_backend)
+    returns what the reference's numba backend returned on the golden inputs:
+    house_qr's (V, tau, R), build_t's T, cpqr_threshold's (V, tau, perm, r)
+    and both triangular solves."""
+    import os
+    from paper_2010_06807_b200 import nestqr_backend as NB
+    g = dict(np.load(os.path.join(golden_dir, "kernels.npz")))
+    for t in range(int(g["n_qr"])):
+        V, tau, R = NB.house_qr(g[f"qr{t}_B"])
+        sc = max(1.0, np.abs(g[f"qr{t}_R"]).max())
+        assert np.abs(R - g[f"qr{t}_R"]).max() <= 1e-12 * sc
+        assert np.abs(tau - g[f"qr{t}_tau"]).max() <= 1e-12
+        assert np.abs(V - g[f"qr{t}_V"]).max() <= 1e-10
+        T = NB.build_t(V, tau)
+        assert np.abs(T - g[f"qr{t}_T"]).max() <= 1e-10 * max(1.0, np.abs(T).max())
+    for key in g["rr_keys"]:
+        t = key.split("_")[0]
+        V, tau, Tred, perm, r = NB.cpqr_threshold(g[f"{t}_M"], float(g[key + "_eps"]), 0)
+        assert r == int(g[key + "_rank"]), key
+        assert V.shape[1] == r and tau.shape == (r,) and perm.dtype == np.int64
+    for t in range(int(g["n_ts"])):
+        R = g[f"ts{t}_R"]
+        X = NB.tri_solve_left(R, g[f"ts{t}_C"])
+        assert np.abs(X - g[f"ts{t}_left"]).max() <= 1e-12 * max(1.0, np.abs(X).max())
+        Y = NB.tri_solve_right(R, g[f"ts{t}_Cr"])
+        assert np.abs(Y - g[f"ts{t}_right"]).max() <= 1e-12 * max(1.0, np.abs(Y).max())
