@@ -31,6 +31,19 @@ struct CopyTask {
   int ncta;   // CTAs of the task in that grid
 };
 
+// one interface of a sparsify wave: column norms, keep filter, compaction
+struct PrepJob {
+  const double* M;   // m x n candidates (ld m)
+  double* sq;        // [n] squared column norms
+  int* keep_idx;     // [n] kept column indices (ascending)
+  int* nk;           // kept count
+  double* ratio;     // min(eps / maxcol, 0.999999)
+  double* maxcol;
+  double* W;         // m x nk gathered columns (ld m)
+  int m, n;
+  int allow_filter, pad_;
+};
+
 // ---------------------------------------------------- job lists in params
 // Short job lists travel IN the kernel launch parameters (__grid_constant__,
 // read through a generic pointer into parameter space) instead of through

@@ -336,6 +336,113 @@ void launch_sparsify_prep(const double* M, int m, int n, double eps, double* sq,
   if (n > 0) gather_cols_kernel<<<dim3(n, (unsigned)std::min((m + 255) / 256, 64)), 256, 0, st>>>(M, m, keep_idx, nk, W); SPQ_LAUNCH_CHECK();
 }
 
+// ---- the same three steps for every interface of a wave in three launches
+// (a wave launched them per interface: 3 dependent ~5 us launches each).
+// Per column / per interface the arithmetic is that of the kernels above.
+constexpr int PL_PREP = 16;
+
+__global__ void colsq_batch_kernel(const PrepJob* __restrict__ jobs_g,
+                                   const __grid_constant__ PList<PrepJob, PL_PREP> pl) {
+  const PrepJob& J = (jobs_g ? jobs_g : pl.v)[blockIdx.y];
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= J.n) return;
+  const double* col = J.M + (int64_t)w * J.m;
+  double s = 0.0;
+  for (int r = lane; r < J.m; r += 32) s += col[r] * col[r];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) J.sq[w] = s;
+}
+
+__global__ void __launch_bounds__(1024) select_batch_kernel(const PrepJob* __restrict__ jobs_g,
+                                                            double eps_user,
+                                                            const __grid_constant__ PList<PrepJob, PL_PREP> pl) {
+  const PrepJob& J = (jobs_g ? jobs_g : pl.v)[blockIdx.x];
+  const double* sq = J.sq;
+  const int m = J.m, n = J.n;
+  __shared__ double red[32];
+  __shared__ int cnt[33];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double mx = 0.0;
+  for (int j = tid; j < n; j += blockDim.x) mx = fmax(mx, sqrt(sq[j]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    red[0] = v;
+  }
+  __syncthreads();
+  const double maxcol = red[0];
+  const double ratio = (maxcol == 0.0) ? 0.0 : fmin(eps_user / maxcol, 0.999999);
+  const bool filter = J.allow_filter && maxcol > 0.0 && n > 4 * m;
+  const double thr = ratio * maxcol;
+  int base = 0;
+  for (int j0 = 0; j0 < n; j0 += blockDim.x) {
+    const int j = j0 + tid;
+    const bool keep = j < n && (!filter || sqrt(sq[j]) >= thr);
+    const unsigned ball = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) cnt[warp] = __popc(ball);
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { const int c = cnt[w]; cnt[w] = acc; acc += c; }
+      cnt[32] = acc;
+    }
+    __syncthreads();
+    if (keep) J.keep_idx[base + cnt[warp] + __popc(ball & ((1u << lane) - 1u))] = j;
+    base += cnt[32];
+    __syncthreads();
+  }
+  if (tid == 0) { *J.nk = base; *J.ratio = ratio; *J.maxcol = maxcol; }
+}
+
+__global__ void gather_cols_batch_kernel(const PrepJob* __restrict__ jobs_g,
+                                         const __grid_constant__ PList<PrepJob, PL_PREP> pl) {
+  const PrepJob& J = (jobs_g ? jobs_g : pl.v)[blockIdx.z];
+  const int t = blockIdx.x;
+  if (t >= *J.nk) return;
+  const int m = J.m;
+  const double* src = J.M + (int64_t)J.keep_idx[t] * m;
+  double* dst = J.W + (int64_t)t * m;
+  for (int r = blockIdx.y * blockDim.x + threadIdx.x; r < m; r += gridDim.y * blockDim.x)
+    dst[r] = src[r];
+}
+
+int sparsify_prep_plist_max() { return PL_PREP; }
+
+// d_jobs == nullptr: the list travels in the launch parameters (njobs <= PL_PREP)
+void launch_sparsify_prep_batch(const PrepJob* d_jobs, const PrepJob* h_jobs, int njobs, double eps,
+                                cudaStream_t st) {
+  if (njobs <= 0) return;
+  PList<PrepJob, PL_PREP> pl;
+  if (!d_jobs) {
+    if (njobs > PL_PREP) throw std::runtime_error("launch_sparsify_prep_batch: parameter list too long");
+    for (int i = 0; i < njobs; ++i) pl.v[i] = h_jobs[i];
+  }
+  constexpr int CHUNK = 16384;   // grid y / z limits (65535)
+  for (int j0 = 0; j0 < njobs; j0 += CHUNK) {
+    const int nj = std::min(CHUNK, njobs - j0);
+    const PrepJob* dj = d_jobs ? d_jobs + j0 : nullptr;
+    int nmax = 0, mmax = 0;
+    for (int i = j0; i < j0 + nj; ++i) {
+      nmax = std::max(nmax, h_jobs[i].n);
+      mmax = std::max(mmax, h_jobs[i].m);
+    }
+    if (nmax > 0) {
+      colsq_batch_kernel<<<dim3((nmax * 32 + 255) / 256, nj), 256, 0, st>>>(dj, pl);
+      SPQ_LAUNCH_CHECK();
+    }
+    select_batch_kernel<<<nj, 1024, 0, st>>>(dj, eps, pl); SPQ_LAUNCH_CHECK();
+    if (nmax > 0) {
+      gather_cols_batch_kernel<<<dim3(nmax, (unsigned)std::min((mmax + 255) / 256, 64), nj), 256, 0, st>>>(dj, pl);
+      SPQ_LAUNCH_CHECK();
+    }
+  }
+}
+
 }  // namespace spq
 
 // ===================================================================== batched
@@ -1178,6 +1285,285 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
+// ---- v2 of the register-resident kernel: a shorter dependent chain per
+// pivot step.  Differences from cpqr_reg_kernel:
+//   * the CTA winner among the RG_NW staged warp records is found by EVERY
+//     warp (lanes mirror the 16 records, 4 butterfly stages): no warp-0
+//     stage behind a second CTA barrier;
+//   * single-CTA problems (the common case at 2D sizes) read the winner's
+//     column straight from the staging area -- no mbarrier, no copy;
+//   * cluster problems push the winner record with st.async from all
+//     threads (8-byte remote stores completing on the destination's
+//     mbarrier: no async-proxy fence, no bulk-copy issue latency);
+//   * the winner over the CL candidates takes log2(CL) butterfly stages;
+//   * v = x * (1 / v0): one division per step instead of one per row
+//     (within an ulp of the reference's x / v0, like the panel QR kernel).
+__device__ __forceinline__ void rg_st_async(uint32_t raddr, double v, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+               :: "r"(raddr), "d"(v), "r"(rmbar) : "memory");
+}
+// total order on candidate records: larger norm, then lower logical
+// position, then lower record index (all lanes of a butterfly must agree)
+__device__ __forceinline__ bool rg_better3(double v, unsigned long long k, int w, double bv,
+                                           unsigned long long bk, int bw) {
+  if (v != bv) return v > bv;
+  const int p = (int)(k >> 32), bp = (int)(bk >> 32);
+  if (p != bp) return p < bp;
+  return w < bw;
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __restrict__ jobs_g,
+                                                             int tpc,
+                                                             const __grid_constant__ PList<CpqrJob, PL_SMALL> pl) {
+  const CpqrJob* jobs = jobs_g ? jobs_g : pl.v;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks();
+  const int q = (int)cluster.block_rank();
+  const bool multi = CL > 1;
+  const CpqrJob J = jobs[blockIdx.x / CL];
+  const int m = J.m;
+  const int n = J.nk ? *J.nk : J.n;
+  const double eps = *J.eps;
+  const int kmax = min(m, n);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = tid % tpc;
+  const int grp = tid / tpc;
+  const int cpc = (RG_NT / tpc) * C;
+  const int mp = tpc * R;
+  const int ph0 = q * cpc + grp * C;
+  extern __shared__ __align__(16) double rs[];
+  const RgLayout L(mp, CL);
+  double* vbuf = rs;
+  double* ST = rs + L.sx();
+  double* RX = rs + L.rx();
+  double* wv = rs + L.wvo();
+  unsigned long long* wk = reinterpret_cast<unsigned long long*>(wv + RG_NW);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(wk + RG_NW);
+  const uint32_t rec_bytes = (uint32_t)(L.rec * sizeof(double));
+
+  if (multi && tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(rg_smem(&mbar[b])) : "memory");
+      rg_arm(rg_smem(&mbar[b]), rec_bytes * CL);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double x[C][R];
+  int pos[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    pos[c] = ph0 + c;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int a = sub + tpc * r;
+      x[c][r] = (ph0 + c < n && a < m) ? J.W[a + (int64_t)(ph0 + c) * J.ldw] : 0.0;
+    }
+  }
+  for (int a = tid; a < L.m1; a += RG_NT) vbuf[a] = 0.0;
+  if (multi) cluster.sync(); else __syncthreads();
+
+  // winner among the RG_NW staged records; identical in every lane of every warp
+  auto cta_winner = [&](double& bv, unsigned long long& bk) -> int {
+    int cw = lane & (RG_NW - 1);
+    double v = ST[(size_t)cw * L.rec];
+    unsigned long long k = (unsigned long long)__double_as_longlong(ST[(size_t)cw * L.rec + 1]);
+#pragma unroll
+    for (int o = RG_NW / 2; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, k, o);
+      const int ow = __shfl_xor_sync(0xffffffffu, cw, o);
+      if (rg_better3(ov, ok, ow, v, k, cw)) { v = ov; k = ok; cw = ow; }
+    }
+    bv = v; bk = k;
+    return cw;
+  };
+  // every warp stages its best candidate record [value, key, column]; one CTA
+  // barrier.  A record is rewritten only by the next step's stage(), after
+  // that step's vbuf barrier, which every thread reaches after its reads
+  // (winner scan, reflector, pushes) of this step's records.
+  auto stage = [&](double bv, unsigned long long bk) {
+#pragma unroll
+    for (int o = 16; o >= tpc; o >>= 1) {    // lanes of a group agree already
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      if (rg_better(ov, ok, bv, bk)) { bv = ov; bk = ok; }
+    }
+    double* st = ST + (size_t)warp * L.rec;
+    const int cph = (int)(bk & 0xffffffffu);
+    if (bv >= 0.0 && cph >= ph0 && cph < ph0 + C) {
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (ph0 + c == cph)
+#pragma unroll
+          for (int r = 0; r < R; ++r) st[2 + sub + tpc * r] = x[c][r];
+    }
+    if (lane == 0) { st[0] = bv; st[1] = __longlong_as_double((long long)bk); }
+    __syncthreads();
+  };
+  // cluster problems: all threads push the CTA winner's record to every CTA
+  auto push = [&](int slot) {
+    double bv;
+    unsigned long long bk;
+    const int cw = cta_winner(bv, bk);
+    const double* src = ST + (size_t)cw * L.rec;
+    const int ne = L.rec * CL;
+    for (int e = tid; e < ne; e += RG_NT) {
+      const int d = e / L.rec, idx = e - d * L.rec;
+      rg_st_async(rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec + idx), d), src[idx],
+                  rg_mapa(rg_smem(&mbar[slot]), d));
+    }
+  };
+
+  {   // initial norms (all rows)
+    double bv = -1.0;
+    unsigned long long bk = rg_pack(0x7fffffff, 0);
+    double ns[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      ns[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) ns[c] = fma(x[c][r], x[c][r], ns[c]);
+    }
+    for (int o = tpc >> 1; o; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < C; ++c) ns[c] += __shfl_xor_sync(0xffffffffu, ns[c], o);
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (ph0 + c < n) {
+        const double nv = sqrt(ns[c]);
+        const unsigned long long k = rg_pack(pos[c], ph0 + c);
+        if (rg_better(nv, k, bv, bk)) { bv = nv; bk = k; }
+      }
+    if (kmax > 0) {
+      stage(bv, bk);
+      if (multi) push(0);
+    }
+  }
+
+  double norm0 = 0.0;
+  int r_out = kmax;
+  for (int i = 0; i < kmax; ++i) {
+    double best;
+    unsigned long long bk;
+    const double* Xr;
+    if (multi) {
+      const int slot = i & 1;
+      rg_wait(rg_smem(&mbar[slot]), (uint32_t)((i >> 1) & 1));
+      if (tid == 0) rg_arm(rg_smem(&mbar[slot]), rec_bytes * CL);   // for step i + 2
+      const double* rx = RX + (size_t)slot * CL * L.rec;
+      int wr = lane & (CL - 1);   // lanes mirror the CL candidates
+      best = rx[(size_t)wr * L.rec];
+      bk = (unsigned long long)__double_as_longlong(rx[(size_t)wr * L.rec + 1]);
+      auto stage_x = [&](int o) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        const int orr = __shfl_xor_sync(0xffffffffu, wr, o);
+        if (rg_better3(ov, ok, orr, best, bk, wr)) { best = ov; bk = ok; wr = orr; }
+      };
+      if (CL > 4) { stage_x(8); stage_x(4); }
+      if (CL > 2) stage_x(2);
+      stage_x(1);
+      Xr = rx + (size_t)wr * L.rec + 2;
+    } else {
+      const int cw = cta_winner(best, bk);
+      Xr = ST + (size_t)cw * L.rec + 2;
+    }
+    if (i == 0) {
+      norm0 = best;
+      if (norm0 == 0.0) { r_out = 0; break; }
+    } else if (best < eps * norm0 && i >= J.min_rank) {
+      r_out = i;
+      break;
+    }
+    const int lp = (int)(bk >> 32), pp = (int)(bk & 0xffffffffu);
+    // ---- reflector from the winner's record (every warp redundantly)
+    double sg = 0.0;
+    for (int a = i + 1 + lane; a < m; a += 32) sg = fma(Xr[a], Xr[a], sg);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
+    const double alpha = Xr[i];
+    double tau, beta, v0 = 1.0;
+    const bool zero = sg == 0.0;
+    if (zero) {
+      if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+    } else {
+      beta = sqrt(alpha * alpha + sg);
+      v0 = (alpha <= 0.0) ? alpha - beta : -sg / (alpha + beta);
+      tau = -v0 / beta;
+    }
+    const double inv0 = zero ? 0.0 : 1.0 / v0;
+    for (int a = i + tid; a < m; a += RG_NT) {
+      const double va = (a == i) ? 1.0 : Xr[a] * inv0;
+      vbuf[a] = va;
+      if (q == 0) J.V[a + (int64_t)i * J.ldv] = va;
+    }
+    if (tid == 0 && i > 0) vbuf[i - 1] = 0.0;
+    if (q == 0 && tid == 0) { J.tau[i] = tau; J.beta[i] = beta; }
+    __syncthreads();
+    // ---- own columns: swap bookkeeping, update, norms over rows > i
+    double vr[R], mk[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      vr[r] = vbuf[sub + tpc * r];                    // zero outside rows i..m-1
+      mk[r] = (sub + tpc * r > i) ? 1.0 : 0.0;
+    }
+    bool act[C];
+    double d[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      if (ph0 + c == pp) pos[c] = i;                 // the pivot retires at position i
+      else if (pos[c] == i) pos[c] = lp;             // displaced by the swap
+      act[c] = ph0 + c < n && ph0 + c != pp && pos[c] > i;
+      d[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) d[c] = fma(vr[r], x[c][r], d[c]);
+    }
+    for (int o = tpc >> 1; o; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < C; ++c) d[c] += __shfl_xor_sync(0xffffffffu, d[c], o);
+    double ns[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const double w = act[c] ? tau * d[c] : 0.0;
+      ns[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        x[c][r] = fma(-w, vr[r], x[c][r]);
+        ns[c] = fma(mk[r] * x[c][r], x[c][r], ns[c]);
+      }
+    }
+    for (int o = tpc >> 1; o; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < C; ++c) ns[c] += __shfl_xor_sync(0xffffffffu, ns[c], o);
+    double bv = -1.0;
+    unsigned long long bkk = rg_pack(0x7fffffff, 0);
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (act[c]) {
+        const double nv = sqrt(ns[c]);
+        const unsigned long long k = rg_pack(pos[c], ph0 + c);
+        if (rg_better(nv, k, bv, bkk)) { bv = nv; bkk = k; }
+      }
+    // no push after the last step: nobody would wait for it, and a remote
+    // store still in flight when its destination CTA exits lands in shared
+    // memory that may already belong to another CTA
+    if (i + 1 < kmax) {
+      stage(bv, bkk);
+      if (multi) push((i & 1) ^ 1);
+    }
+  }
+  if (q == 0 && tid == 0) *J.rank = r_out;
+  if (sub == 0)
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (ph0 + c < n) J.perm[pos[c]] = ph0 + c;
+  // every push addressed to this CTA was waited for; keep the CTAs resident
+  // until all of them issued theirs
+  if (multi)
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 // variant v: (R, C) = (16,2), (8,4), (4,8); returns cluster size or 0
 int cpqr_reg_plan(int m, int n, int v, int* tpc_out) {
   static const int RR[3] = {16, 8, 4}, CC[3] = {2, 4, 8};
@@ -1210,6 +1596,10 @@ static void launch_rg(const CpqrJob* d_jobs, const PList<CpqrJob, PL_SMALL>& pl,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CUDA_TRY(cudaFuncSetAttribute(cpqr_reg_kernel<R, C>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CUDA_TRY(cudaFuncSetAttribute(cpqr_reg2_kernel<R, C>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(cpqr_reg2_kernel<R, C>,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     init = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -1224,7 +1614,9 @@ static void launch_rg(const CpqrJob* d_jobs, const PList<CpqrJob, PL_SMALL>& pl,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg_kernel<R, C>, d_jobs, tpc, pl));
+  static const bool v1 = getenv("SPQ_CPQR_V1") && atoi(getenv("SPQ_CPQR_V1")) != 0;
+  if (v1) CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg_kernel<R, C>, d_jobs, tpc, pl));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg2_kernel<R, C>, d_jobs, tpc, pl));
 }
 
 void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int v, int cl, int tpc,

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <malloc.h>
 #include <map>
 #include <tuple>
 #include <memory>
@@ -36,6 +37,9 @@ int cpqr_grid(int ncols, int nsm);
 void launch_sparsify_prep(const double* M, int m, int n, double eps, double* sq, int* keep_idx,
                           int* nk, double* ratio, double* maxcol, double* W, cudaStream_t st,
                           int allow_filter = 1);
+void launch_sparsify_prep_batch(const PrepJob* d_jobs, const PrepJob* h_jobs, int njobs, double eps,
+                                cudaStream_t st);
+int sparsify_prep_plist_max();
 void launch_jacobi_sv(const SvJob* d_jobs, int n, cudaStream_t st);
 void chain_wy(const double* V, const double* T, int m, int k, double* z, const int* rows,
               int64_t N, int nrhs, bool transpose, double* w, double* w2, cudaStream_t st);
@@ -1722,8 +1726,9 @@ void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
   std::vector<Block*> which;
   int64_t tot = 0;
   for (int r : row_clusters) {
-    for (int cc : c->rix[r]) {
-      Block* b = find_block(c, r, cc);
+    const FlatSet& row = c->rix[r];
+    for (size_t t = 0; t < row.v.size(); ++t) {
+      Block* b = row.b[t] ? row.b[t] : find_block(c, r, row.v[t]);
       if (!b) continue;
       if (b->clean) {
         if (b->unverified) {
@@ -1901,11 +1906,16 @@ bool plan_front(spq_ctx* c, int s, Front& f) {
   f.m = off;
   // candidate trailing columns (sorted, unique)
   std::vector<int> cand;
-  for (auto& p : f.parts)
-    for (int cc : c->rix[p.r])
-      if (cc != s) cand.push_back(cc);
-  std::sort(cand.begin(), cand.end());
-  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+  {
+    static thread_local std::vector<int> mark;   // epoch stamps per cluster
+    static thread_local int epoch = 0;
+    if ((int)mark.size() < c->ncl) mark.assign(c->ncl, 0), epoch = 0;
+    if (++epoch == 0x7fffffff) { std::fill(mark.begin(), mark.end(), 0); epoch = 1; }
+    for (auto& p : f.parts)
+      for (int cc : c->rix[p.r])
+        if (cc != s && mark[cc] != epoch) { mark[cc] = epoch; cand.push_back(cc); }
+    std::sort(cand.begin(), cand.end());
+  }
   // presence of each candidate (factor.py:454): parts in order until a
   // nonzero row is found.  Walked part-major over each part's row list
   // (block pointers at hand, no lookups); for every candidate the parts and
@@ -2246,13 +2256,20 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
   if (!c->spec) pivot_raise(c, ps);
   while (pos < ids.size()) {
     // refresh flags of every row cluster any pending op may query
-    std::set<int> rows;
-    for (size_t t = pos; t < ids.size(); ++t) {
-      const int s = ids[t];
-      rows.insert(s);
-      for (int r : c->cix[s]) rows.insert(r);
+    // (ascending cluster ids, each once)
+    std::vector<int> rows;
+    {
+      static thread_local std::vector<char> seen;
+      seen.assign(c->ncl, 0);
+      auto take = [&](int r) { if (!seen[r]) { seen[r] = 1; rows.push_back(r); } };
+      for (size_t t = pos; t < ids.size(); ++t) {
+        const int s = ids[t];
+        take(s);
+        for (int r : c->cix[s]) take(r);
+      }
+      std::sort(rows.begin(), rows.end());
     }
-    refresh_flags(c, std::vector<int>(rows.begin(), rows.end()));
+    refresh_flags(c, rows);
     // exact mode: the refresh synchronized, so reading the previous waves'
     // pivot checks is free; speculative mode defers them to the end of the call
     if (!c->spec) pivot_raise(c, ps);
@@ -2479,6 +2496,8 @@ void run_cpqr_jobs(spq_ctx* c, const std::vector<CpqrJob>& jobs) {
         static const int RR[3] = {16, 8, 4};
         if (bv < 0 || cl < bcl || (cl == bcl && tpc * RR[v] < btpc * RR[bv])) { bv = v; bcl = cl; btpc = tpc; }
       }
+    static const bool cpqr_log = env_flag("SPQ_CPQR_LOG");   // diagnostics: problem sizes and plans
+    if (cpqr_log) fprintf(stderr, "[cpqr] m=%d ncap=%d n=%d variant=%d cl=%d tpc=%d\n", np, ncap, q.n, bv, bcl, btpc);
     if (bv >= 0) {
       auto& g = rg_groups[std::make_tuple(bv, bcl, btpc)];
       g.first.push_back(q);
@@ -2613,11 +2632,16 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
   SpScal* dsc = (SpScal*)dalloc(c, std::max(nw, 1) * sizeof(SpScal));
   {
     Scope s(c, F_CPQR);
+    std::vector<PrepJob> pj;
     for (int t = 0; t < nw; ++t) {
       SpJob& j = J[t];
       if (j.np == 0) continue;
-      launch_sparsify_prep(j.M, j.np, j.ncols, eps, j.sq, j.keep, &dsc[t].nk, &dsc[t].ratio,
-                           &dsc[t].maxcol, j.Wm, c->st);
+      pj.push_back(PrepJob{j.M, j.sq, j.keep, &dsc[t].nk, &dsc[t].ratio, &dsc[t].maxcol, j.Wm,
+                           j.np, j.ncols, 1, 0});
+    }
+    if (!pj.empty()) {
+      const PrepJob* d_pj = (int)pj.size() <= sparsify_prep_plist_max() ? nullptr : upload(c, pj);
+      launch_sparsify_prep_batch(d_pj, pj.data(), (int)pj.size(), eps, c->st);
       c->tm.launches[F_CPQR] += 3;
       c->n_kernels += 3;
     }
@@ -3585,20 +3609,28 @@ void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
   std::vector<std::pair<int, int>> bkeys;
   std::vector<int> eb(nnz);
   std::vector<int64_t> eoff(nnz);
+  uint64_t last_key = ~0ull;
+  int last_b = -1;
   for (int64_t j = 0; j < N; ++j) {
     const int cj = coln[j];
     for (int64_t e = indptr[j]; e < indptr[j + 1]; ++e) {
       const int64_t r = indices[e];
       const int ri = rown[r];
       const uint64_t key = bkey(ri, cj);
-      const int* hit = bidx.find(key);
       int b;
-      if (!hit) {
-        b = (int)bkeys.size();
-        bidx[key] = b;
-        bkeys.push_back({ri, cj});
+      if (key == last_key) {   // runs of entries of one block: no probe
+        b = last_b;
       } else {
-        b = *hit;
+        const int* hit = bidx.find(key);
+        if (!hit) {
+          b = (int)bkeys.size();
+          bidx[key] = b;
+          bkeys.push_back({ri, cj});
+        } else {
+          b = *hit;
+        }
+        last_key = key;
+        last_b = b;
       }
       eb[e] = b;
       eoff[e] = rpos[r] + (int64_t)cpos[j] * (int64_t)c->rows_of[ri].size();
@@ -4079,6 +4111,19 @@ int spq_create(spq_ctx** out, int device) {
   spq_ctx* c = new spq_ctx();
   int rc = guarded(c, [&] {
     c->dev = device;
+    // The planner builds and drops multi-megabyte task vectors many times per
+    // factorization; with glibc's defaults each of them is a fresh mmap (page
+    // faults on first touch, munmap on free).  Keep them in the heap.
+    // SPQ_NO_MALLOPT=1 leaves the process's malloc policy alone.
+    static const bool tuned = [] {
+      if (!env_flag("SPQ_NO_MALLOPT")) {
+        mallopt(M_MMAP_THRESHOLD, 256 << 20);
+        mallopt(M_TRIM_THRESHOLD, 512 << 20);
+        mallopt(M_TOP_PAD, 64 << 20);
+      }
+      return true;
+    }();
+    (void)tuned;
     CUDA_TRY(cudaSetDevice(device));
     // two attribute queries (cudaGetDeviceProperties fills the whole struct:
     // milliseconds per context)
