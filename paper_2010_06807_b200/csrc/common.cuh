@@ -251,9 +251,9 @@ void launch_power_iter(const PowerJob* d_jobs, int njobs, int fmax, cudaStream_t
 int cpqr_cluster_size(int m, int ncap);
 size_t cpqr_cluster_smem(int m, int ncap, int cl);
 void launch_cpqr_cluster(const CpqrJob* d_jobs, int njobs, int cl, size_t smem, cudaStream_t st);
-int cpqr_reg_plan(int m, int n, int variant, int* tpc);
-size_t cpqr_reg_smem(int padded_rows, int cl);
-void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int variant, int cl, int tpc, size_t smem,
+int cpqr_reg_plan(int m, int n, int variant, int* tpc, int* nt);
+size_t cpqr_reg_smem(int padded_rows, int cl, int nt);
+void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int variant, int cl, int tpc, int nt, size_t smem,
                      cudaStream_t st);
 void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax, int slab_k,
                        double* part, double* z, int64_t N, int nrhs, cudaStream_t st);

@@ -1285,32 +1285,62 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
-// ---- v2 of the register-resident kernel: a shorter dependent chain per
-// pivot step.  Differences from cpqr_reg_kernel:
-//   * the CTA winner among the RG_NW staged warp records is found by EVERY
-//     warp (lanes mirror the 16 records, 4 butterfly stages): no warp-0
-//     stage behind a second CTA barrier;
-//   * single-CTA problems (the common case at 2D sizes) read the winner's
-//     column straight from the staging area -- no mbarrier, no copy;
-//   * cluster problems push the winner record with st.async from all
-//     threads (8-byte remote stores completing on the destination's
-//     mbarrier: no async-proxy fence, no bulk-copy issue latency);
-//   * the winner over the CL candidates takes log2(CL) butterfly stages;
+// ---- v3 of the register-resident kernel.  clock64 stamps of v1/v2
+// (tools/cpqr_trace.py, profiles/r02c) showed a pivot step of ~7800 cycles that
+// is bound by one SM's ISSUE throughput, not by the exchange (the mbarrier
+// wait was ~200 cycles): 16 warps each repeated the winner scan, sigma, the
+// sqrt/div scalars and the CTA-winner scan (fp64 division and 64-bit
+// shuffles at 16x redundancy), and every CTA carried 16K matrix entries.
+// Here:
+//   * the CTA size is a launch parameter (128/256/512 threads, still 32
+//     entries per thread): the planner spreads a problem over up to 16 CTAs
+//     so each SM issues ~4x fewer fp64 / shuffle instructions per step;
+//   * warp 0 alone waits for the candidates, picks the winner, forms sigma,
+//     tau, v0 and writes v: the other warps sleep at the CTA barrier;
+//   * every argmax (across column groups of a warp, across the warp
+//     records of a CTA, across the CTA candidates) is three integer warp
+//     reductions (redux.sync on the norm's high word, low word, position)
+//     and a ballot instead of a 5-stage butterfly of 64-bit shuffles;
+//   * cluster problems push the winner record with st.async from a few
+//     warps (8-byte remote stores completing on the destination's mbarrier);
+//   * norms over rows > i by predicated FMAs (no mask multiply);
 //   * v = x * (1 / v0): one division per step instead of one per row
 //     (within an ulp of the reference's x / v0, like the panel QR kernel).
 __device__ __forceinline__ void rg_st_async(uint32_t raddr, double v, uint32_t rmbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
                :: "r"(raddr), "d"(v), "r"(rmbar) : "memory");
 }
-// total order on candidate records: larger norm, then lower logical
-// position, then lower record index (all lanes of a butterfly must agree)
-__device__ __forceinline__ bool rg_better3(double v, unsigned long long k, int w, double bv,
-                                           unsigned long long bk, int bw) {
-  if (v != bv) return v > bv;
-  const int p = (int)(k >> 32), bp = (int)(bk >> 32);
-  if (p != bp) return p < bp;
-  return w < bw;
+// lane holding the best candidate of the warp: largest norm v (v < 0: none),
+// then lowest position.  Every lane takes part; identical in every lane.
+__device__ __forceinline__ int rg_argbest(double v, int pos) {
+  const unsigned hi = v < 0.0 ? 0u : (unsigned)__double2hiint(v) + 1u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned lo = hi == mh ? (unsigned)__double2loint(v) : 0u;
+  const unsigned ml = __reduce_max_sync(0xffffffffu, lo);
+  const bool cand = hi == mh && lo == ml;
+  const unsigned mp = __reduce_min_sync(0xffffffffu, cand ? (unsigned)pos : 0xffffffffu);
+  return __ffs(__ballot_sync(0xffffffffu, cand && (unsigned)pos == mp)) - 1;
 }
+
+struct Rg3Layout {   // shared memory in doubles; rows padded to mp = tpc * R
+  int m1, cl, rec, nw;  // rec = one candidate record: [value, key, column (m1)]
+  __host__ __device__ Rg3Layout(int mp, int cl_, int nw_)
+      : m1(mp > 0 ? ((mp + 1) & ~1) : 2), cl(cl_), rec(m1 + 2), nw(nw_) {}
+  // vbuf (m1) | ST [nw][rec] | RX [2][cl][rec] | sc [4] | mbar [2]
+  __host__ __device__ size_t sx() const { return (size_t)m1; }
+  __host__ __device__ size_t rx() const { return sx() + (size_t)nw * rec; }
+  __host__ __device__ size_t sco() const { return rx() + 2 * (size_t)cl * rec; }
+  __host__ __device__ size_t bytes() const { return (sco() + 4 + 2) * 8 + 64; }
+};
+
+#ifdef SPQ_TRACE
+// diagnostic build only (SPQ_TRACE=1 python -m paper_2010_06807_b200.build):
+// per-step clock64 stamps of thread 0 / CTA 0, read by spq_debug_cpqr_trace
+__device__ long long g_cpqr_trace[64 * 12];
+#define RG_STAMP(slot) do { if (q == 0 && tid == 0 && i < 64) g_cpqr_trace[i * 12 + (slot)] = clock64(); } while (0)
+#else
+#define RG_STAMP(slot) do { } while (0)
+#endif
 
 template <int R, int C>
 __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __restrict__ jobs_g,
@@ -1321,6 +1351,7 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
   const int CL = (int)cluster.num_blocks();
   const int q = (int)cluster.block_rank();
   const bool multi = CL > 1;
+  const int NT = (int)blockDim.x, NW = NT >> 5;
   const CpqrJob J = jobs[blockIdx.x / CL];
   const int m = J.m;
   const int n = J.nk ? *J.nk : J.n;
@@ -1329,17 +1360,16 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int sub = tid % tpc;
   const int grp = tid / tpc;
-  const int cpc = (RG_NT / tpc) * C;
+  const int cpc = (NT / tpc) * C;
   const int mp = tpc * R;
   const int ph0 = q * cpc + grp * C;
   extern __shared__ __align__(16) double rs[];
-  const RgLayout L(mp, CL);
+  const Rg3Layout L(mp, CL, NW);
   double* vbuf = rs;
   double* ST = rs + L.sx();
   double* RX = rs + L.rx();
-  double* wv = rs + L.wvo();
-  unsigned long long* wk = reinterpret_cast<unsigned long long*>(wv + RG_NW);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(wk + RG_NW);
+  double* sc = rs + L.sco();   // [0] tau, [1] (lp << 32 | pp), [2] stop
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(sc + 4);
   const uint32_t rec_bytes = (uint32_t)(L.rec * sizeof(double));
 
   if (multi && tid == 0) {
@@ -1360,58 +1390,40 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
       x[c][r] = (ph0 + c < n && a < m) ? J.W[a + (int64_t)(ph0 + c) * J.ldw] : 0.0;
     }
   }
-  for (int a = tid; a < L.m1; a += RG_NT) vbuf[a] = 0.0;
+  for (int a = tid; a < L.m1; a += NT) vbuf[a] = 0.0;
   if (multi) cluster.sync(); else __syncthreads();
 
-  // winner among the RG_NW staged records; identical in every lane of every warp
-  auto cta_winner = [&](double& bv, unsigned long long& bk) -> int {
-    int cw = lane & (RG_NW - 1);
-    double v = ST[(size_t)cw * L.rec];
-    unsigned long long k = (unsigned long long)__double_as_longlong(ST[(size_t)cw * L.rec + 1]);
-#pragma unroll
-    for (int o = RG_NW / 2; o; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, k, o);
-      const int ow = __shfl_xor_sync(0xffffffffu, cw, o);
-      if (rg_better3(ov, ok, ow, v, k, cw)) { v = ov; k = ok; cw = ow; }
-    }
-    bv = v; bk = k;
-    return cw;
-  };
-  // every warp stages its best candidate record [value, key, column]; one CTA
-  // barrier.  A record is rewritten only by the next step's stage(), after
-  // that step's vbuf barrier, which every thread reaches after its reads
-  // (winner scan, reflector, pushes) of this step's records.
+  // Every warp stages its best candidate record [value, key, column]; one
+  // CTA barrier.  A record is rewritten only by the next step's stage(),
+  // after that step's vbuf barrier, which every warp reaches after its reads
+  // of this step's records (winner scan and reflector in warp 0, pushes).
   auto stage = [&](double bv, unsigned long long bk) {
-#pragma unroll
-    for (int o = 16; o >= tpc; o >>= 1) {    // lanes of a group agree already
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      if (rg_better(ov, ok, bv, bk)) { bv = ov; bk = ok; }
-    }
+    const int bl = rg_argbest(bv, (int)(bk >> 32));   // lanes of a group agree already
     double* st = ST + (size_t)warp * L.rec;
-    const int cph = (int)(bk & 0xffffffffu);
-    if (bv >= 0.0 && cph >= ph0 && cph < ph0 + C) {
+    if (lane / tpc == bl / tpc && bv >= 0.0) {       // the winning group writes its column
+      const int cph = (int)(bk & 0xffffffffu);
 #pragma unroll
       for (int c = 0; c < C; ++c)
         if (ph0 + c == cph)
 #pragma unroll
           for (int r = 0; r < R; ++r) st[2 + sub + tpc * r] = x[c][r];
     }
-    if (lane == 0) { st[0] = bv; st[1] = __longlong_as_double((long long)bk); }
+    if (lane == bl) { st[0] = bv; st[1] = __longlong_as_double((long long)bk); }
     __syncthreads();
   };
-  // cluster problems: all threads push the CTA winner's record to every CTA
+  // cluster problems: warp w pushes the CTA winner's record to the CTAs
+  // w, w + NW, ...
   auto push = [&](int slot) {
-    double bv;
-    unsigned long long bk;
-    const int cw = cta_winner(bv, bk);
+    if (warp >= CL) return;
+    const int w = lane < NW ? lane : 0;
+    const double v = lane < NW ? ST[(size_t)w * L.rec] : -1.0;
+    const unsigned long long k = (unsigned long long)__double_as_longlong(ST[(size_t)w * L.rec + 1]);
+    const int cw = rg_argbest(v, lane < NW ? (int)(k >> 32) : 0x7fffffff);
     const double* src = ST + (size_t)cw * L.rec;
-    const int ne = L.rec * CL;
-    for (int e = tid; e < ne; e += RG_NT) {
-      const int d = e / L.rec, idx = e - d * L.rec;
-      rg_st_async(rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec + idx), d), src[idx],
-                  rg_mapa(rg_smem(&mbar[slot]), d));
+    for (int d = warp; d < CL; d += NW) {
+      const uint32_t dst = rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec), d);
+      const uint32_t mb = rg_mapa(rg_smem(&mbar[slot]), d);
+      for (int idx = lane; idx < L.rec; idx += 32) rg_st_async(dst + 8u * (uint32_t)idx, src[idx], mb);
     }
   };
 
@@ -1441,72 +1453,87 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
     }
   }
 
-  double norm0 = 0.0;
+  double norm0 = 0.0;   // warp 0
   int r_out = kmax;
   for (int i = 0; i < kmax; ++i) {
-    double best;
-    unsigned long long bk;
-    const double* Xr;
-    if (multi) {
-      const int slot = i & 1;
-      rg_wait(rg_smem(&mbar[slot]), (uint32_t)((i >> 1) & 1));
-      if (tid == 0) rg_arm(rg_smem(&mbar[slot]), rec_bytes * CL);   // for step i + 2
-      const double* rx = RX + (size_t)slot * CL * L.rec;
-      int wr = lane & (CL - 1);   // lanes mirror the CL candidates
-      best = rx[(size_t)wr * L.rec];
-      bk = (unsigned long long)__double_as_longlong(rx[(size_t)wr * L.rec + 1]);
-      auto stage_x = [&](int o) {
-        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        const int orr = __shfl_xor_sync(0xffffffffu, wr, o);
-        if (rg_better3(ov, ok, orr, best, bk, wr)) { best = ov; bk = ok; wr = orr; }
-      };
-      if (CL > 4) { stage_x(8); stage_x(4); }
-      if (CL > 2) stage_x(2);
-      stage_x(1);
-      Xr = rx + (size_t)wr * L.rec + 2;
-    } else {
-      const int cw = cta_winner(best, bk);
-      Xr = ST + (size_t)cw * L.rec + 2;
-    }
-    if (i == 0) {
-      norm0 = best;
-      if (norm0 == 0.0) { r_out = 0; break; }
-    } else if (best < eps * norm0 && i >= J.min_rank) {
-      r_out = i;
-      break;
-    }
-    const int lp = (int)(bk >> 32), pp = (int)(bk & 0xffffffffu);
-    // ---- reflector from the winner's record (every warp redundantly)
-    double sg = 0.0;
-    for (int a = i + 1 + lane; a < m; a += 32) sg = fma(Xr[a], Xr[a], sg);
+    RG_STAMP(0);
+    if (warp == 0) {
+      // ---- candidates -> winner -> reflector scalars -> v (warp 0 only)
+      const double* recs;
+      int nrec;
+      if (multi) {
+        const int slot = i & 1;
+        rg_wait(rg_smem(&mbar[slot]), (uint32_t)((i >> 1) & 1));
+        if (lane == 0) rg_arm(rg_smem(&mbar[slot]), rec_bytes * CL);   // for step i + 2
+        recs = RX + (size_t)slot * CL * L.rec;
+        nrec = CL;
+      } else {
+        recs = ST;
+        nrec = NW;
+      }
+      RG_STAMP(1);
+      const int w = lane < nrec ? lane : 0;
+      const double cv = lane < nrec ? recs[(size_t)w * L.rec] : -1.0;
+      const unsigned long long ck = (unsigned long long)__double_as_longlong(recs[(size_t)w * L.rec + 1]);
+      const int wl = rg_argbest(cv, lane < nrec ? (int)(ck >> 32) : 0x7fffffff);
+      const double best = __shfl_sync(0xffffffffu, cv, wl);
+      const unsigned long long bk = __shfl_sync(0xffffffffu, ck, wl);
+      RG_STAMP(2);
+      bool stop = false;
+      if (i == 0) {
+        norm0 = best;
+        if (norm0 == 0.0) { r_out = 0; stop = true; }
+      } else if (best < eps * norm0 && i >= J.min_rank) {
+        r_out = i;
+        stop = true;
+      }
+      if (!stop) {
+        const double* Xr = recs + (size_t)wl * L.rec + 2;
+        double sg = 0.0;
+        for (int a = i + 1 + lane; a < m; a += 32) sg = fma(Xr[a], Xr[a], sg);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
-    const double alpha = Xr[i];
-    double tau, beta, v0 = 1.0;
-    const bool zero = sg == 0.0;
-    if (zero) {
-      if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
-    } else {
-      beta = sqrt(alpha * alpha + sg);
-      v0 = (alpha <= 0.0) ? alpha - beta : -sg / (alpha + beta);
-      tau = -v0 / beta;
+        for (int o = 16; o; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
+        RG_STAMP(3);
+        const double alpha = Xr[i];
+        double tau, beta, v0 = 1.0;
+        const bool zero = sg == 0.0;
+        if (zero) {
+          if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+        } else {
+          beta = sqrt(alpha * alpha + sg);
+          v0 = (alpha <= 0.0) ? alpha - beta : -sg / (alpha + beta);
+          tau = -v0 / beta;
+        }
+        const double inv0 = zero ? 0.0 : 1.0 / v0;
+        // v (zero outside rows i..m-1: row i-1 is cleared, rows < i-1 were)
+        for (int a = i + lane; a < m; a += 32) {
+          const double va = (a == i) ? 1.0 : Xr[a] * inv0;
+          vbuf[a] = va;
+          if (q == 0) J.V[a + (int64_t)i * J.ldv] = va;
+        }
+        if (lane == 0) {
+          if (i > 0) vbuf[i - 1] = 0.0;
+          sc[0] = tau;
+          sc[1] = __longlong_as_double((long long)bk);
+          if (q == 0) { J.tau[i] = tau; J.beta[i] = beta; }
+        }
+      }
+      if (lane == 0) sc[2] = stop ? 1.0 : 0.0;
     }
-    const double inv0 = zero ? 0.0 : 1.0 / v0;
-    for (int a = i + tid; a < m; a += RG_NT) {
-      const double va = (a == i) ? 1.0 : Xr[a] * inv0;
-      vbuf[a] = va;
-      if (q == 0) J.V[a + (int64_t)i * J.ldv] = va;
-    }
-    if (tid == 0 && i > 0) vbuf[i - 1] = 0.0;
-    if (q == 0 && tid == 0) { J.tau[i] = tau; J.beta[i] = beta; }
+    RG_STAMP(4);
     __syncthreads();
+    RG_STAMP(5);
+    if (sc[2] != 0.0) break;
+    const double tau = sc[0];
+    const unsigned long long bk = (unsigned long long)__double_as_longlong(sc[1]);
+    const int lp = (int)(bk >> 32), pp = (int)(bk & 0xffffffffu);
     // ---- own columns: swap bookkeeping, update, norms over rows > i
-    double vr[R], mk[R];
+    double vr[R];
+    bool below[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      vr[r] = vbuf[sub + tpc * r];                    // zero outside rows i..m-1
-      mk[r] = (sub + tpc * r > i) ? 1.0 : 0.0;
+      vr[r] = vbuf[sub + tpc * r];
+      below[r] = sub + tpc * r > i;
     }
     bool act[C];
     double d[C];
@@ -1522,6 +1549,7 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
     for (int o = tpc >> 1; o; o >>= 1)
 #pragma unroll
       for (int c = 0; c < C; ++c) d[c] += __shfl_xor_sync(0xffffffffu, d[c], o);
+    RG_STAMP(6);
     double ns[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -1530,7 +1558,7 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         x[c][r] = fma(-w, vr[r], x[c][r]);
-        ns[c] = fma(mk[r] * x[c][r], x[c][r], ns[c]);
+        if (below[r]) ns[c] = fma(x[c][r], x[c][r], ns[c]);
       }
     }
     for (int o = tpc >> 1; o; o >>= 1)
@@ -1545,12 +1573,15 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
         const unsigned long long k = rg_pack(pos[c], ph0 + c);
         if (rg_better(nv, k, bv, bkk)) { bv = nv; bkk = k; }
       }
+    RG_STAMP(7);
     // no push after the last step: nobody would wait for it, and a remote
     // store still in flight when its destination CTA exits lands in shared
     // memory that may already belong to another CTA
     if (i + 1 < kmax) {
       stage(bv, bkk);
+      RG_STAMP(8);
       if (multi) push((i & 1) ^ 1);
+      RG_STAMP(9);
     }
   }
   if (q == 0 && tid == 0) *J.rank = r_out;
@@ -1564,32 +1595,49 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
-// variant v: (R, C) = (16,2), (8,4), (4,8); returns cluster size or 0
-int cpqr_reg_plan(int m, int n, int v, int* tpc_out) {
+// variant v: (R, C) = (16,2), (8,4), (4,8).  Plan of one problem: lanes per
+// column tpc (power of two, tpc * R >= m), CTA size nt and cluster size (0:
+// no plan).  The smallest CTA (128, 256, 512 threads) whose cluster still
+// holds all n columns wins: a pivot step is bound by one SM's issue rate, so
+// the columns are spread as widely as the cluster limit allows
+// (SPQ_CPQR_NTMIN / SPQ_CPQR_CLMAX narrow the choice for A/B runs).
+int cpqr_reg_plan(int m, int n, int v, int* tpc_out, int* nt_out) {
   static const int RR[3] = {16, 8, 4}, CC[3] = {2, 4, 8};
-  static int clmax = -1;
+  static int clmax = -1, ntmin = 128;
+  static bool v1 = false;
   if (clmax < 0) {
     const char* e = getenv("SPQ_CPQR_CLMAX");
     clmax = e ? atoi(e) : 16;
+    const char* f = getenv("SPQ_CPQR_NTMIN");
+    if (f) ntmin = std::max(32, std::min(RG_NT, atoi(f)));
+    v1 = getenv("SPQ_CPQR_V1") && atoi(getenv("SPQ_CPQR_V1")) != 0;
+    if (v1) ntmin = RG_NT;   // the v1 kernel is compiled for 512 threads
   }
   if (m <= 0 || n <= 0) return 0;
   const int R = RR[v], C = CC[v];
   int tpc = 1;
   while (tpc * R < m) tpc *= 2;
   if (tpc > 32) return 0;
-  const int cpc = (RG_NT / tpc) * C;
-  int cl = 1;
-  while (cl * cpc < n) cl *= 2;
-  if (cl > clmax || cl > 16) return 0;
-  *tpc_out = tpc;
-  return cl;
+  for (int nt = ntmin; nt <= RG_NT; nt *= 2) {
+    if (nt < tpc || nt < 32) continue;
+    const int cpc = (nt / tpc) * C;
+    int cl = 1;
+    while (cl * cpc < n) cl *= 2;
+    if (cl > clmax || cl > 16) continue;
+    *tpc_out = tpc;
+    *nt_out = nt;
+    return cl;
+  }
+  return 0;
 }
 
-size_t cpqr_reg_smem(int mp, int cl) { return RgLayout(mp, cl).bytes(); }   // mp = tpc * R
+size_t cpqr_reg_smem(int mp, int cl, int nt) {   // mp = tpc * R
+  return std::max(RgLayout(mp, cl).bytes(), Rg3Layout(mp, cl, nt / 32).bytes());
+}
 
 template <int R, int C>
 static void launch_rg(const CpqrJob* d_jobs, const PList<CpqrJob, PL_SMALL>& pl, int njobs, int cl,
-                      int tpc, size_t smem, cudaStream_t st) {
+                      int tpc, int nt, size_t smem, cudaStream_t st) {
   static bool init = false;
   if (!init) {
     CUDA_TRY(cudaFuncSetAttribute(cpqr_reg_kernel<R, C>,
@@ -1602,9 +1650,10 @@ static void launch_rg(const CpqrJob* d_jobs, const PList<CpqrJob, PL_SMALL>& pl,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     init = true;
   }
+  static const bool v1 = getenv("SPQ_CPQR_V1") && atoi(getenv("SPQ_CPQR_V1")) != 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(njobs * cl));
-  cfg.blockDim = dim3(RG_NT);
+  cfg.blockDim = dim3(v1 ? RG_NT : nt);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1614,13 +1663,12 @@ static void launch_rg(const CpqrJob* d_jobs, const PList<CpqrJob, PL_SMALL>& pl,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static const bool v1 = getenv("SPQ_CPQR_V1") && atoi(getenv("SPQ_CPQR_V1")) != 0;
   if (v1) CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg_kernel<R, C>, d_jobs, tpc, pl));
   else CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg2_kernel<R, C>, d_jobs, tpc, pl));
 }
 
 void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int v, int cl, int tpc,
-                     size_t smem, cudaStream_t st) {
+                     int nt, size_t smem, cudaStream_t st) {
   if (njobs <= 0) return;
   PList<CpqrJob, PL_SMALL> pl;
   if (!d_jobs) {
@@ -1628,11 +1676,17 @@ void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, in
     for (int i = 0; i < njobs; ++i) pl.v[i] = h_jobs[i];
   }
   switch (v) {
-    case 0: launch_rg<16, 2>(d_jobs, pl, njobs, cl, tpc, smem, st); break;
-    case 1: launch_rg<8, 4>(d_jobs, pl, njobs, cl, tpc, smem, st); break;
-    case 2: launch_rg<4, 8>(d_jobs, pl, njobs, cl, tpc, smem, st); break;
+    case 0: launch_rg<16, 2>(d_jobs, pl, njobs, cl, tpc, nt, smem, st); break;
+    case 1: launch_rg<8, 4>(d_jobs, pl, njobs, cl, tpc, nt, smem, st); break;
+    case 2: launch_rg<4, 8>(d_jobs, pl, njobs, cl, tpc, nt, smem, st); break;
     default: throw std::runtime_error("cpqr_reg: bad variant");
   }
 }
 
 }  // namespace spq
+
+#ifdef SPQ_TRACE
+extern "C" int spq_debug_cpqr_trace(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, spq::g_cpqr_trace, sizeof(long long) * (size_t)(n < 64 * 12 ? n : 64 * 12));
+}
+#endif

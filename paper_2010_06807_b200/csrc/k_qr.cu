@@ -296,11 +296,20 @@ struct QrrCtx {
 // samples stalled on "no instructions"); the register block is indexed
 // with compile-time columns only, so the dynamic column jj is selected
 // with predicated moves.
+#ifdef SPQ_TRACE
+// diagnostic build only: clock64 stamps of thread 0 / CTA 0 per column step
+__device__ long long g_panel_trace[32 * 8];
+#define QRR_STAMP(slot) do { if (x.q == 0 && x.tid == 0) g_panel_trace[jj * 8 + (slot)] = clock64(); } while (0)
+#else
+#define QRR_STAMP(slot) do { } while (0)
+#endif
+
 template <int R>
 __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB], QrrShared& sh,
                                          const int jj) {
   const int q = x.q, CL = x.CL, nloc = x.nloc, tid = x.tid, lane = x.lane, warp = x.warp;
   const int B = jj & 1;
+  QRR_STAMP(0);
   // ---- this thread's entries of the pivot column
   double xv[R];
   bool part[R];
@@ -341,12 +350,14 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
     const double tot = d[0] + __shfl_xor_sync(0xffffffffu, d[0], 16);
     if ((lane >> 4) == half) mine = tot;
   }
+  QRR_STAMP(1);
   sh.red[warp][lane] = mine;
   if (q == 0 && tid == jj) {
 #pragma unroll
     for (int c = 0; c < QR_NB; ++c) sh.Xp[c] = a[0][c];
   }
   __syncthreads();
+  QRR_STAMP(2);
   if (CL == 1) {   // single CTA: totals straight into shared memory, no DSMEM round trip
     if (tid < QR_NB) {
       double s = 0.0;
@@ -367,7 +378,9 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
     qrr_st_async(qrr_mapa(qrr_smem(&sh.XR[B][q][c]), dst), s, mb);
     if (q == 0) qrr_st_async(qrr_mapa(qrr_smem(&sh.PR[B][c]), dst), sh.Xp[c], mb);
   }
+  QRR_STAMP(3);
   qrr_wait(qrr_smem(&sh.mbar[B]), (uint32_t)((jj >> 1) & 1));
+  QRR_STAMP(4);
   if (tid == 0)   // re-arm this buffer for step jj + 2 (before anyone can push it)
     qrr_arm(qrr_smem(&sh.mbar[B]), (uint32_t)((CL + 1) * QR_NB * sizeof(double)));
   // ---- totals over the CTAs in rank order (identical in every CTA)
@@ -384,6 +397,7 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
   }
   __syncthreads();
   }
+  QRR_STAMP(5);
   // ---- reflector scalars (every thread, identical inputs)
   const double sigma = sh.dtot[jj];
   const double alpha = sh.apiv[jj];
@@ -410,6 +424,7 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
     v[r] = piv ? 1.0 : (part[r] ? xv[r] * inv0 : 0.0);
     nj[r] = piv ? beta : (part[r] ? v[r] : xv[r]);   // new value of column jj
   }
+  QRR_STAMP(6);
   const double ts = tau != 0.0 ? tau : 0.0;
 #pragma unroll
   for (int c = 0; c < QR_NB; ++c) {
@@ -420,6 +435,7 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
       a[r][c] = (c == jj) ? nj[r] : u;
     }
   }
+  QRR_STAMP(7);
 }
 
 template <int R, int KBMAX>
@@ -823,3 +839,9 @@ void launch_trsm_right(const TrsmJob* d_jobs, int njobs, int total_tiles, cudaSt
 }
 
 }  // namespace spq
+
+#ifdef SPQ_TRACE
+extern "C" int spq_debug_panel_trace(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, spq::g_panel_trace, sizeof(long long) * (size_t)(n < 32 * 8 ? n : 32 * 8));
+}
+#endif

@@ -2480,29 +2480,31 @@ constexpr size_t CPQR_CTA_MAX_SMEM = 220 * 1024;
 // cooperative jobs runs concurrently on the fork streams.
 void run_cpqr_jobs(spq_ctx* c, const std::vector<CpqrJob>& jobs) {
   const bool coop_only = env_flag("SPQ_CPQR_COOP"), no_ws = env_flag("SPQ_CPQR_NOWS");
-  std::map<std::tuple<int, int, int>, std::pair<std::vector<CpqrJob>, size_t>> rg_groups;   // (variant, cl, tpc)
+  std::map<std::tuple<int, int, int, int>, std::pair<std::vector<CpqrJob>, size_t>> rg_groups;   // (variant, cl, tpc, nt)
   std::map<int, std::pair<std::vector<CpqrJob>, size_t>> by_cl;
   std::vector<CpqrJob> cj;
   std::vector<CpqrJob> coop;
   size_t cta_smem = 0;
   for (const CpqrJob& q : jobs) {
     const int np = q.m, ncap = std::max(q.ncap, 1);
-    int bv = -1, bcl = 0, btpc = 0;
+    // register plan: smallest CTA (widest spread), then fewest lanes per
+    // column (fewest shuffles per reduction), then least row padding
+    int bv = -1, bcl = 0, btpc = 0, bnt = 0;
+    static const int RR[3] = {16, 8, 4};
     if (!coop_only && !no_ws)
       for (int v = 0; v < 3; ++v) {
-        int tpc = 0;
-        const int cl = cpqr_reg_plan(np, ncap, v, &tpc);
+        int tpc = 0, nt = 0;
+        const int cl = cpqr_reg_plan(np, ncap, v, &tpc, &nt);
         if (cl == 0) continue;
-        static const int RR[3] = {16, 8, 4};
-        if (bv < 0 || cl < bcl || (cl == bcl && tpc * RR[v] < btpc * RR[bv])) { bv = v; bcl = cl; btpc = tpc; }
+        const auto key = std::make_tuple(nt, tpc * RR[v], tpc, cl);
+        if (bv < 0 || key < std::make_tuple(bnt, btpc * RR[bv], btpc, bcl)) { bv = v; bcl = cl; btpc = tpc; bnt = nt; }
       }
     static const bool cpqr_log = env_flag("SPQ_CPQR_LOG");   // diagnostics: problem sizes and plans
-    if (cpqr_log) fprintf(stderr, "[cpqr] m=%d ncap=%d n=%d variant=%d cl=%d tpc=%d\n", np, ncap, q.n, bv, bcl, btpc);
+    if (cpqr_log) fprintf(stderr, "[cpqr] m=%d ncap=%d n=%d variant=%d cl=%d tpc=%d nt=%d\n", np, ncap, q.n, bv, bcl, btpc, bnt);
     if (bv >= 0) {
-      auto& g = rg_groups[std::make_tuple(bv, bcl, btpc)];
+      auto& g = rg_groups[std::make_tuple(bv, bcl, btpc, bnt)];
       g.first.push_back(q);
-      static const int RRv[3] = {16, 8, 4};
-      g.second = std::max(g.second, cpqr_reg_smem(btpc * RRv[bv], bcl));
+      g.second = std::max(g.second, cpqr_reg_smem(btpc * RR[bv], bcl, bnt));
       continue;
     }
     if (!coop_only && !env_flag("SPQ_CPQR_CLUSTER") && cpqr_cta_smem(np, ncap) <= CPQR_CTA_MAX_SMEM) {
@@ -2521,7 +2523,7 @@ void run_cpqr_jobs(spq_ctx* c, const std::vector<CpqrJob>& jobs) {
   }
   Scope s(c, F_CPQR);
   // upload every job list first (the ring), then fork
-  std::vector<std::tuple<const CpqrJob*, int, std::tuple<int, int, int>, size_t, const CpqrJob*>> wl;
+  std::vector<std::tuple<const CpqrJob*, int, std::tuple<int, int, int, int>, size_t, const CpqrJob*>> wl;
   for (auto& kv : rg_groups)
     wl.emplace_back(up_or_param(c, kv.second.first, PL_SMALL), (int)kv.second.first.size(), kv.first,
                     kv.second.second, kv.second.first.data());
@@ -2535,7 +2537,7 @@ void run_cpqr_jobs(spq_ctx* c, const std::vector<CpqrJob>& jobs) {
     for (auto& w : wl) {
       const auto& key = std::get<2>(w);
       launch_cpqr_reg(std::get<0>(w), std::get<4>(w), std::get<1>(w), std::get<0>(key), std::get<1>(key),
-                      std::get<2>(key), std::get<3>(w), fk.next());
+                      std::get<2>(key), std::get<3>(key), std::get<3>(w), fk.next());
       c->tm.launches[F_CPQR]++;
       c->n_kernels++;
     }
