@@ -1495,16 +1495,25 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
         for (int o = 16; o; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
         RG_STAMP(3);
         const double alpha = Xr[i];
-        double tau, beta, v0 = 1.0;
-        const bool zero = sg == 0.0;
-        if (zero) {
+        // v0 = alpha - beta (alpha <= 0) or -sigma / (alpha + beta); 1 / v0 and
+        // tau = -v0 / beta are formed from alpha, beta, sigma directly so the
+        // two quotients do not wait for each other (within an ulp or two of
+        // the reference's values, kernels/_numba.py:15-35)
+        double tau, beta, inv0 = 0.0;
+        if (sg == 0.0) {
           if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
         } else {
           beta = sqrt(alpha * alpha + sg);
-          v0 = (alpha <= 0.0) ? alpha - beta : -sg / (alpha + beta);
-          tau = -v0 / beta;
+          if (alpha <= 0.0) {
+            const double v0 = alpha - beta;
+            inv0 = 1.0 / v0;
+            tau = -v0 / beta;
+          } else {
+            const double ab = alpha + beta;
+            inv0 = -ab / sg;
+            tau = sg / (ab * beta);
+          }
         }
-        const double inv0 = zero ? 0.0 : 1.0 / v0;
         // v (zero outside rows i..m-1: row i-1 is cleared, rows < i-1 were)
         for (int a = i + lane; a < m; a += 32) {
           const double va = (a == i) ? 1.0 : Xr[a] * inv0;
@@ -1618,16 +1627,20 @@ int cpqr_reg_plan(int m, int n, int v, int* tpc_out, int* nt_out) {
   int tpc = 1;
   while (tpc * R < m) tpc *= 2;
   if (tpc > 32) return 0;
-  for (int nt = ntmin; nt <= RG_NT; nt *= 2) {
-    if (nt < tpc || nt < 32) continue;
-    const int cpc = (nt / tpc) * C;
-    int cl = 1;
-    while (cl * cpc < n) cl *= 2;
-    if (cl > clmax || cl > 16) continue;
-    *tpc_out = tpc;
-    *nt_out = nt;
-    return cl;
-  }
+  // every CTA sends its candidate column to all CL CTAs each step (8-byte
+  // remote stores): prefer plans whose exchange cl * rows stays <= 2048
+  for (int pass = 0; pass < 2; ++pass)
+    for (int nt = ntmin; nt <= RG_NT; nt *= 2) {
+      if (nt < tpc || nt < 32) continue;
+      const int cpc = (nt / tpc) * C;
+      int cl = 1;
+      while (cl * cpc < n) cl *= 2;
+      if (cl > clmax || cl > 16) continue;
+      if (pass == 0 && cl * tpc * R > 2048) continue;
+      *tpc_out = tpc;
+      *nt_out = nt;
+      return cl;
+    }
   return 0;
 }
 

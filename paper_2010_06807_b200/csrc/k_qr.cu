@@ -358,63 +358,83 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
   }
   __syncthreads();
   QRR_STAMP(2);
-  if (CL == 1) {   // single CTA: totals straight into shared memory, no DSMEM round trip
-    if (tid < QR_NB) {
-      double s = 0.0;
+  // clock64 stamps (tools/panel_trace.py) showed this tail bound by fp64 ISSUE
+  // (one fp64 instruction per warp every ~14 cycles): every thread repeated
+  // the sqrt/div scalars and formed all 32 update coefficients itself (64
+  // fp64 operations), and the totals took 20 shuffle+add rounds per warp.
+  // Now warp 0 alone sums the CTA partials (lane c = column c, rank order),
+  // forms the scalars once and publishes the 32 coefficients; the other
+  // warps wait at one CTA barrier and read them.
+  if (CL > 1) {
+    // ---- push the CTA partials (and CTA 0's pivot row) to every CTA
+    for (int t = tid; t < QR_NB * CL; t += QRR_NT) {
+      const int dst = t >> 5, c = t & 31;
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int w = 0; w < QRR_NT / 32; ++w) s += sh.red[w][tid];
-      sh.dtot[tid] = s;
-      sh.apiv[tid] = sh.Xp[tid];
+      for (int w = 0; w < QRR_NT / 32; w += 2) { s0 += sh.red[w][c]; s1 += sh.red[w + 1][c]; }
+      const uint32_t mb = qrr_mapa(qrr_smem(&sh.mbar[B]), dst);
+      qrr_st_async(qrr_mapa(qrr_smem(&sh.XR[B][q][c]), dst), s0 + s1, mb);
+      if (q == 0) qrr_st_async(qrr_mapa(qrr_smem(&sh.PR[B][c]), dst), sh.Xp[c], mb);
     }
-    __syncthreads();
-  } else {
-  // ---- push the CTA partials (and CTA 0's pivot row) to every CTA
-  for (int t = tid; t < QR_NB * CL; t += QRR_NT) {
-    const int dst = t >> 5, c = t & 31;
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < QRR_NT / 32; ++w) s += sh.red[w][c];
-    const uint32_t mb = qrr_mapa(qrr_smem(&sh.mbar[B]), dst);
-    qrr_st_async(qrr_mapa(qrr_smem(&sh.XR[B][q][c]), dst), s, mb);
-    if (q == 0) qrr_st_async(qrr_mapa(qrr_smem(&sh.PR[B][c]), dst), sh.Xp[c], mb);
   }
   QRR_STAMP(3);
-  qrr_wait(qrr_smem(&sh.mbar[B]), (uint32_t)((jj >> 1) & 1));
-  QRR_STAMP(4);
-  if (tid == 0)   // re-arm this buffer for step jj + 2 (before anyone can push it)
-    qrr_arm(qrr_smem(&sh.mbar[B]), (uint32_t)((CL + 1) * QR_NB * sizeof(double)));
-  // ---- totals over the CTAs in rank order (identical in every CTA)
+  if (warp == 0) {
+    double dt, ap;
+    if (CL > 1) {
+      qrr_wait(qrr_smem(&sh.mbar[B]), (uint32_t)((jj >> 1) & 1));
+      QRR_STAMP(4);
+      if (lane == 0)   // re-arm this buffer for step jj + 2 (before anyone can push it)
+        qrr_arm(qrr_smem(&sh.mbar[B]), (uint32_t)((CL + 1) * QR_NB * sizeof(double)));
+      // totals over the CTAs in rank order (identical in every CTA)
+      double s0 = 0.0, s1 = 0.0;
+      for (int p = 0; p + 1 < CL; p += 2) { s0 += sh.XR[B][p][lane]; s1 += sh.XR[B][p + 1][lane]; }
+      if (CL & 1) s0 += sh.XR[B][CL - 1][lane];
+      dt = s0 + s1;
+      ap = sh.PR[B][lane];
+    } else {
+      QRR_STAMP(4);
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-  for (int cc = 0; cc < QR_NB / (QRR_NT / 32); ++cc) {
-    const int c = warp + cc * (QRR_NT / 32);
-    double v = lane < CL ? sh.XR[B][lane < CL ? lane : 0][c] : 0.0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      for (int w = 0; w < QRR_NT / 32; w += 2) { s0 += sh.red[w][lane]; s1 += sh.red[w + 1][lane]; }
+      dt = s0 + s1;
+      ap = sh.Xp[lane];
+    }
+    // ---- reflector scalars (kernels/_numba.py:15-35)
+    const double sigma = __shfl_sync(0xffffffffu, dt, jj);
+    const double alpha = __shfl_sync(0xffffffffu, ap, jj);
+    // v0 = alpha - beta (alpha <= 0) or -sigma / (alpha + beta); 1 / v0 and
+    // tau = -v0 / beta are formed from alpha, beta, sigma directly, so the two
+    // quotients do not wait for each other (x * (1 / v0) instead of x / v0 and
+    // these quotients are within an ulp or two of the reference's values, far
+    // inside the parity tolerance)
+    double tau, beta, inv0 = 0.0;
+    if (sigma == 0.0) {
+      if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
+    } else {
+      beta = sqrt(alpha * alpha + sigma);
+      if (alpha <= 0.0) {
+        const double v0 = alpha - beta;
+        inv0 = 1.0 / v0;
+        tau = -v0 / beta;
+      } else {
+        const double ab = alpha + beta;
+        inv0 = -ab / sigma;
+        tau = sigma / (ab * beta);
+      }
+    }
+    const double g = fma(dt, inv0, ap);           // v_jj^T (column lane): G entry / update dot
+    const double ts = tau != 0.0 ? tau : 0.0;
+    sh.dtot[lane] = lane > jj ? ts * g : 0.0;     // update coefficient of column lane
+    if (lane < jj) sh.Gs[lane + jj * (QR_NB + 1)] = g;
     if (lane == 0) {
-      sh.dtot[c] = v;
-      sh.apiv[c] = sh.PR[B][c];
+      sh.apiv[0] = inv0;
+      sh.apiv[1] = beta;
+      if (q == 0 && jj < x.kb) x.tau[x.j0 + jj] = tau;
     }
   }
   __syncthreads();
-  }
   QRR_STAMP(5);
-  // ---- reflector scalars (every thread, identical inputs)
-  const double sigma = sh.dtot[jj];
-  const double alpha = sh.apiv[jj];
-  double tau, beta, v0 = 1.0;
-  const bool zero = sigma == 0.0;
-  if (zero) {
-    if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
-  } else {
-    beta = sqrt(alpha * alpha + sigma);
-    v0 = (alpha <= 0.0) ? alpha - beta : -sigma / (alpha + beta);
-    tau = -v0 / beta;
-  }
-  // one reciprocal per step (x / v0 -> x * (1/v0): within an ulp of the
-  // reference's division, far inside the parity tolerance)
-  const double inv0 = zero ? 0.0 : 1.0 / v0;
-  if (q == 0 && tid == 0 && jj < x.kb) x.tau[x.j0 + jj] = tau;
-  if (tid < jj) sh.Gs[tid + jj * (QR_NB + 1)] = sh.apiv[tid] + sh.dtot[tid] * inv0;
+  const double inv0 = sh.apiv[0], beta = sh.apiv[1];
   // ---- v below the pivot, rank-1 update of the columns right of it
   double v[R], nj[R];
 #pragma unroll
@@ -425,10 +445,9 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
     nj[r] = piv ? beta : (part[r] ? v[r] : xv[r]);   // new value of column jj
   }
   QRR_STAMP(6);
-  const double ts = tau != 0.0 ? tau : 0.0;
 #pragma unroll
   for (int c = 0; c < QR_NB; ++c) {
-    const double wc = c > jj ? ts * fma(sh.dtot[c], inv0, sh.apiv[c]) : 0.0;
+    const double wc = sh.dtot[c];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const double u = fma(-wc, v[r], a[r][c]);

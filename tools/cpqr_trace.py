@@ -34,6 +34,6 @@ for cfg, n in (("C3", None), ("C3", 128), ("C4", 16)):
     print(f"{cfg} n={n}: last interface {F.sparsify_log[-1]}: cycles/step {per.mean():.0f} "
           f"({per.mean() / 1.965e3:.2f} us)", flush=True)
     for k, nm in enumerate(names):
-        print(f"   {nm:14s} {d[:, k].mean():8.0f}")
+        print(f"   {nm:22s} {d[:, k].mean():8.0f}")
     print(f"   {'loop back':14s} {(t[3:steps, 0] - t[2:steps - 1, 9]).mean():8.0f}", flush=True)
     del F
