@@ -127,7 +127,7 @@ class Clocks:
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "500"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
@@ -317,7 +317,7 @@ def run_c2(args, rank, world, local, dist):
             dev["qr"] += ms
             for eps in (1e-2, 1e-4):
                 rk, _, ms = batched_rrqr(Ms, eps)
-                key = f"rrqr_{eps:g}"
+                key = "rrqr_1e-2" if eps == 1e-2 else "rrqr_1e-4"
                 dev[key] += ms
                 fl[key] = float(sum(4 * 64 * 192 * r - 2 * r * r * (64 + 192) + 4 * r ** 3 / 3
                                     for r in rk))
@@ -403,6 +403,12 @@ def main():
     launches = 0
     barrier()
     clocks = Clocks(local)
+    if os.environ.get("SPQ_BENCH_NOCLOCKS") == "1":   # diagnostics: is the sampler perturbing the steps?
+        clocks.__enter__ = lambda: clocks
+    if os.environ.get("SPQ_BENCH_NOGC") == "1":       # diagnostics: are the outliers collector pauses?
+        import gc
+        gc.collect()
+        gc.disable()
     with clocks:
         for _ in range(args.steps):
             flush_l2(l2buf)
@@ -437,6 +443,22 @@ def main():
         solve = {"gmres_s": ts, "iterations": int(rep.iterations),
                  "final_residual": float(rep.final_residual), "tol": tol,
                  "where": "device (spq_gmres: chains + CSR SpMV + MGS in HBM)"}
+        # roofline of the chain applications (row (e)): one application reads the
+        # stored payload (V, T, R_ss, R_sn of every record) once -- algorithmic
+        # bytes = 8 * payload_scalars -- timed on the library stream
+        y = np.random.default_rng(0).standard_normal(A.ncols)
+        chain = {}
+        for fn in ("apply_qt", "solve_w"):
+            getattr(F, fn)(y)
+            F._ctx.call("spq_reset_timings")
+            reps = 10
+            for _ in range(reps):
+                getattr(F, fn)(y)
+            ms = F.device_timings()["chain"]["ms"] / reps
+            gb = 8.0 * int(F.payload_scalars) / 1e9
+            chain[fn] = {"device_ms": ms, "payload_gb": gb, "achieved_gbs": gb / (ms * 1e-3),
+                         "frac_hbm": gb / (ms * 1e-3) / hbm}
+        solve["chain"] = chain
         del F
     T = float(np.sum(dev_ms))
     Te = float(np.sum(e2e_ms))

@@ -1026,267 +1026,9 @@ __device__ __forceinline__ void rg_wait(uint32_t mbar, uint32_t parity) {
   }
 }
 
-struct RgLayout {   // shared memory in doubles; rows padded to mp = tpc * R
-  int m1, cl, rec;  // rec = one candidate record: [value, key, column (m1)]
-  __host__ __device__ RgLayout(int mp, int cl_) : m1(mp > 0 ? ((mp + 1) & ~1) : 2), cl(cl_), rec(m1 + 2) {}
-  // vbuf (m1) | ST [RG_NW][rec] | RX [2][cl][rec] | wv [RG_NW] | wk [RG_NW] | mbar [2]
-  __host__ __device__ size_t sx() const { return (size_t)m1; }
-  __host__ __device__ size_t rx() const { return sx() + (size_t)RG_NW * rec; }
-  __host__ __device__ size_t wvo() const { return rx() + 2 * (size_t)cl * rec; }
-  __host__ __device__ size_t bytes() const { return (wvo() + 2 * RG_NW + 2) * 8 + 64; }
-};
-
-template <int R, int C>
-__global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __restrict__ jobs_g,
-                                                            int tpc,
-                                                            const __grid_constant__ PList<CpqrJob, PL_SMALL> pl) {
-  const CpqrJob* jobs = jobs_g ? jobs_g : pl.v;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int CL = (int)cluster.num_blocks();
-  const int q = (int)cluster.block_rank();
-  const CpqrJob J = jobs[blockIdx.x / CL];
-  const int m = J.m;
-  const int n = J.nk ? *J.nk : J.n;
-  const double eps = *J.eps;
-  const int kmax = min(m, n);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int sub = tid % tpc;                 // lane within the column group
-  const int grp = tid / tpc;                 // group within the CTA
-  const int cpc = (RG_NT / tpc) * C;         // columns per CTA
-  const int mp = tpc * R;                    // padded rows
-  const int ph0 = q * cpc + grp * C;         // first own physical column
-  extern __shared__ __align__(16) double rs[];
-  const RgLayout L(mp, CL);
-  double* vbuf = rs;                         // v (zero outside rows i..m-1)
-  double* ST = rs + L.sx();                  // [RG_NW][rec] every warp's candidate, staged for the push
-  double* RX = rs + L.rx();                  // [2][CL][rec] every CTA's candidate
-  double* wv = rs + L.wvo();                 // [RG_NW]
-  unsigned long long* wk = reinterpret_cast<unsigned long long*>(wv + RG_NW);   // [RG_NW]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(wk + RG_NW);                     // [2]
-  const uint32_t rec_bytes = (uint32_t)(L.rec * sizeof(double));
-
-  if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(rg_smem(&mbar[b])) : "memory");
-      rg_arm(rg_smem(&mbar[b]), rec_bytes * CL);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-
-  // own columns: rows sub + tpc*r (zero beyond m / beyond n)
-  double x[C][R];
-  int pos[C];
-#pragma unroll
-  for (int c = 0; c < C; ++c) {
-    pos[c] = ph0 + c;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int a = sub + tpc * r;
-      x[c][r] = (ph0 + c < n && a < m) ? J.W[a + (int64_t)(ph0 + c) * J.ldw] : 0.0;
-    }
-  }
-  for (int a = tid; a < L.m1; a += RG_NT) vbuf[a] = 0.0;
-  cluster.sync();   // barriers initialised and armed everywhere before the first push
-
-  // Every warp stages its best candidate record [value, key, column] (the
-  // owner group writes the column); ONE CTA barrier; warp 0 picks the CTA
-  // winner among the RG_NW records and bulk-copies that record to every CTA
-  // (cp.async.bulk shared::cta -> shared::cluster on the destination's
-  // mbarrier), CL lanes issuing in parallel.  A staged record is rewritten
-  // only in the next step's publish, after the next step's vbuf barrier,
-  // which warp 0 reaches after its copies have read their source.
-  auto publish = [&](double bv, unsigned long long bk, int slot) {
-#pragma unroll
-    for (int o = 16; o >= tpc; o >>= 1) {    // lanes of a group agree already
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      if (rg_better(ov, ok, bv, bk)) { bv = ov; bk = ok; }
-    }
-    double* st = ST + (size_t)warp * L.rec;
-    const int cph = (int)(bk & 0xffffffffu);
-    if (bv >= 0.0 && cph >= ph0 && cph < ph0 + C) {
-#pragma unroll
-      for (int c = 0; c < C; ++c)
-        if (ph0 + c == cph)
-#pragma unroll
-          for (int r = 0; r < R; ++r) st[2 + sub + tpc * r] = x[c][r];
-    }
-    if (lane == 0) { st[0] = bv; st[1] = __longlong_as_double((long long)bk); }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk copy
-    __syncthreads();
-    if (warp == 0) {
-      double cv = lane < RG_NW ? ST[(size_t)lane * L.rec] : -1.0;
-      unsigned long long ck = lane < RG_NW
-          ? (unsigned long long)__double_as_longlong(ST[(size_t)lane * L.rec + 1])
-          : rg_pack(0x7fffffff, 0);
-      int cw = lane < RG_NW ? lane : 0;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {   // full warp: every lane must agree
-        const double ov = __shfl_xor_sync(0xffffffffu, cv, o);
-        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, ck, o);
-        const int ow = __shfl_xor_sync(0xffffffffu, cw, o);
-        if (rg_better(ov, ok, cv, ck)) { cv = ov; ck = ok; cw = ow; }
-      }
-      if (lane < CL) {
-        const uint32_t src = rg_smem(ST + (size_t)cw * L.rec);
-        const int d = lane;
-        const uint32_t dst = rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec), d);
-        const uint32_t mb = rg_mapa(rg_smem(&mbar[slot]), d);
-        asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes "
-                     "[%0], [%1], %2, [%3];" :: "r"(dst), "r"(src), "r"(rec_bytes), "r"(mb)
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
-      }
-    }
-  };
-
-  // initial norms (all rows)
-  {
-    double bv = -1.0;
-    unsigned long long bk = rg_pack(0x7fffffff, 0);
-    double ns[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      ns[c] = 0.0;
-#pragma unroll
-      for (int r = 0; r < R; ++r) ns[c] = fma(x[c][r], x[c][r], ns[c]);
-    }
-    for (int o = tpc >> 1; o; o >>= 1)
-#pragma unroll
-      for (int c = 0; c < C; ++c) ns[c] += __shfl_xor_sync(0xffffffffu, ns[c], o);
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-      if (ph0 + c < n) {
-        const double nv = sqrt(ns[c]);
-        const unsigned long long k = rg_pack(pos[c], ph0 + c);
-        if (rg_better(nv, k, bv, bk)) { bv = nv; bk = k; }
-      }
-    if (kmax > 0) publish(bv, bk, 0);
-  }
-
-  double norm0 = 0.0;
-  int r_out = kmax;
-  for (int i = 0; i < kmax; ++i) {
-    const int slot = i & 1;
-    rg_wait(rg_smem(&mbar[slot]), (uint32_t)((i >> 1) & 1));
-    if (tid == 0) rg_arm(rg_smem(&mbar[slot]), rec_bytes * CL);   // for step i + 2
-    const double* rx = RX + (size_t)slot * CL * L.rec;
-    // ---- winner over the CL CTA candidates (identical in every warp)
-    double best = -1.0;
-    unsigned long long bk = rg_pack(0x7fffffff, 0);
-    int wr = 0;
-    if (lane < CL) {
-      best = rx[(size_t)lane * L.rec];
-      bk = (unsigned long long)__double_as_longlong(rx[(size_t)lane * L.rec + 1]);
-      wr = lane;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {   // full warp: every lane must agree (stop test)
-      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      const int orr = __shfl_xor_sync(0xffffffffu, wr, o);
-      if (rg_better(ov, ok, best, bk)) { best = ov; bk = ok; wr = orr; }
-    }
-    if (i == 0) {
-      norm0 = best;
-      if (norm0 == 0.0) { r_out = 0; break; }
-    } else if (best < eps * norm0 && i >= J.min_rank) {
-      r_out = i;
-      break;
-    }
-    const int lp = (int)(bk >> 32), pp = (int)(bk & 0xffffffffu);
-    // ---- reflector straight from the winner's record in local shared
-    // memory (every warp redundantly: no CTA barrier).  The record's slot is
-    // overwritten only by pushes for step i + 2, which other CTAs issue after
-    // waiting for this CTA's step-(i+1) push, i.e. after every warp here
-    // passed publish()'s first barrier -- after these reads.
-    const double* Xr = rx + (size_t)wr * L.rec + 2;
-    double sg = 0.0;
-    for (int a = i + 1 + lane; a < m; a += 32) sg = fma(Xr[a], Xr[a], sg);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sg += __shfl_xor_sync(0xffffffffu, sg, o);
-    const double alpha = Xr[i];
-    double tau, beta, v0 = 1.0;
-    const bool zero = sg == 0.0;
-    if (zero) {
-      if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
-    } else {
-      beta = sqrt(alpha * alpha + sg);
-      v0 = (alpha <= 0.0) ? alpha - beta : -sg / (alpha + beta);
-      tau = -v0 / beta;
-    }
-    // v once per row (the reference's division x / v0) into vbuf, zero at
-    // row i-1; the previous step's vbuf reads ended before publish()'s barriers
-    for (int a = i + tid; a < m; a += RG_NT) {
-      const double va = (a == i) ? 1.0 : (zero ? 0.0 : Xr[a] / v0);
-      vbuf[a] = va;
-      if (q == 0) J.V[a + (int64_t)i * J.ldv] = va;
-    }
-    if (tid == 0 && i > 0) vbuf[i - 1] = 0.0;
-    if (q == 0 && tid == 0) { J.tau[i] = tau; J.beta[i] = beta; }
-    __syncthreads();
-    // ---- own columns: swap bookkeeping, update, norms over rows > i
-    double vr[R], mk[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      vr[r] = vbuf[sub + tpc * r];                    // zero outside rows i..m-1
-      mk[r] = (sub + tpc * r > i) ? 1.0 : 0.0;
-    }
-    bool act[C];
-    double d[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      if (ph0 + c == pp) pos[c] = i;                 // the pivot retires at position i
-      else if (pos[c] == i) pos[c] = lp;             // displaced by the swap
-      act[c] = ph0 + c < n && ph0 + c != pp && pos[c] > i;
-      d[c] = 0.0;
-#pragma unroll
-      for (int r = 0; r < R; ++r) d[c] = fma(vr[r], x[c][r], d[c]);
-    }
-    for (int o = tpc >> 1; o; o >>= 1)
-#pragma unroll
-      for (int c = 0; c < C; ++c) d[c] += __shfl_xor_sync(0xffffffffu, d[c], o);
-    double ns[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const double w = act[c] ? tau * d[c] : 0.0;
-      ns[c] = 0.0;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        x[c][r] = fma(-w, vr[r], x[c][r]);
-        ns[c] = fma(mk[r] * x[c][r], x[c][r], ns[c]);
-      }
-    }
-    for (int o = tpc >> 1; o; o >>= 1)
-#pragma unroll
-      for (int c = 0; c < C; ++c) ns[c] += __shfl_xor_sync(0xffffffffu, ns[c], o);
-    double bv = -1.0;
-    unsigned long long bkk = rg_pack(0x7fffffff, 0);
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-      if (act[c]) {
-        const double nv = sqrt(ns[c]);
-        const unsigned long long k = rg_pack(pos[c], ph0 + c);
-        if (rg_better(nv, k, bv, bkk)) { bv = nv; bkk = k; }
-      }
-    // no push after the last step: nobody would wait for it, and a bulk
-    // copy still in flight when its destination CTA exits lands in shared
-    // memory that may already belong to another CTA
-    if (i + 1 < kmax) publish(bv, bkk, slot ^ 1);
-  }
-  if (q == 0 && tid == 0) *J.rank = r_out;
-  if (sub == 0)
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-      if (ph0 + c < n) J.perm[pos[c]] = ph0 + c;
-  // every push addressed to this CTA was waited for; keep the CTAs resident
-  // until all of them issued theirs
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
-}
-
-// ---- v3 of the register-resident kernel.  clock64 stamps of v1/v2
-// (tools/cpqr_trace.py, profiles/r02c) showed a pivot step of ~7800 cycles that
+// clock64 stamps of the first versions of this kernel (512-thread CTAs,
+// every warp repeating the scalar work; tools/cpqr_trace.py, profiles/r02c)
+// showed a pivot step of ~7800 cycles that
 // is bound by one SM's ISSUE throughput, not by the exchange (the mbarrier
 // wait was ~200 cycles): 16 warps each repeated the winner scan, sigma, the
 // sqrt/div scalars and the CTA-winner scan (fp64 division and 64-bit
@@ -1343,7 +1085,7 @@ __device__ long long g_cpqr_trace[64 * 12];
 #endif
 
 template <int R, int C>
-__global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __restrict__ jobs_g,
+__global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __restrict__ jobs_g,
                                                              int tpc,
                                                              const __grid_constant__ PList<CpqrJob, PL_SMALL> pl) {
   const CpqrJob* jobs = jobs_g ? jobs_g : pl.v;
@@ -1613,14 +1355,11 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg2_kernel(const CpqrJob* __re
 int cpqr_reg_plan(int m, int n, int v, int* tpc_out, int* nt_out) {
   static const int RR[3] = {16, 8, 4}, CC[3] = {2, 4, 8};
   static int clmax = -1, ntmin = 128;
-  static bool v1 = false;
   if (clmax < 0) {
     const char* e = getenv("SPQ_CPQR_CLMAX");
     clmax = e ? atoi(e) : 16;
     const char* f = getenv("SPQ_CPQR_NTMIN");
     if (f) ntmin = std::max(32, std::min(RG_NT, atoi(f)));
-    v1 = getenv("SPQ_CPQR_V1") && atoi(getenv("SPQ_CPQR_V1")) != 0;
-    if (v1) ntmin = RG_NT;   // the v1 kernel is compiled for 512 threads
   }
   if (m <= 0 || n <= 0) return 0;
   const int R = RR[v], C = CC[v];
@@ -1645,7 +1384,7 @@ int cpqr_reg_plan(int m, int n, int v, int* tpc_out, int* nt_out) {
 }
 
 size_t cpqr_reg_smem(int mp, int cl, int nt) {   // mp = tpc * R
-  return std::max(RgLayout(mp, cl).bytes(), Rg3Layout(mp, cl, nt / 32).bytes());
+  return Rg3Layout(mp, cl, nt / 32).bytes();
 }
 
 template <int R, int C>
@@ -1657,16 +1396,11 @@ static void launch_rg(const CpqrJob* d_jobs, const PList<CpqrJob, PL_SMALL>& pl,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CUDA_TRY(cudaFuncSetAttribute(cpqr_reg_kernel<R, C>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CUDA_TRY(cudaFuncSetAttribute(cpqr_reg2_kernel<R, C>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CUDA_TRY(cudaFuncSetAttribute(cpqr_reg2_kernel<R, C>,
-                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     init = true;
   }
-  static const bool v1 = getenv("SPQ_CPQR_V1") && atoi(getenv("SPQ_CPQR_V1")) != 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(njobs * cl));
-  cfg.blockDim = dim3(v1 ? RG_NT : nt);
+  cfg.blockDim = dim3(nt);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1676,8 +1410,7 @@ static void launch_rg(const CpqrJob* d_jobs, const PList<CpqrJob, PL_SMALL>& pl,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (v1) CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg_kernel<R, C>, d_jobs, tpc, pl));
-  else CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg2_kernel<R, C>, d_jobs, tpc, pl));
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_reg_kernel<R, C>, d_jobs, tpc, pl));
 }
 
 void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int v, int cl, int tpc,

@@ -1098,6 +1098,9 @@ void ensure_err_slots(spq_ctx* c, int n) {
 struct CopyBatch {
   std::vector<CopyTask> t;
   int64_t maxe = 0;
+  // callers that know their task count reserve it: growing a 10^4-task vector
+  // by doubling was ~4 ms of memmove per C3 factorization (host profile r02)
+  void reserve(size_t n) { t.reserve(t.size() + n); }
   void add(const CopyTask& x) {
     if (x.nr <= 0 || x.nc <= 0) return;
     t.push_back(x);
@@ -1387,9 +1390,20 @@ size_t chunk_bytes() {   // SPQ_CHUNK_BYTES overrides (tests force the chunked p
 // consecutive groups that reuse one scratch buffer (stream order).  A level
 // of interface scalings otherwise needs 2 k n doubles for ALL its targets
 // at once (~100 GB at 64^3).
-void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs_in, bool transpose, int fam = F_WY) {
+// join_side: the T factors of this batch are still being built on the side
+// stream (build_full_T under a SideScope).  Only T^T W needs them, so the
+// first product W = V^T C -- the long one -- runs beside G = V^T V and the
+// larft recurrence; the main stream joins the side stream just before the
+// first kernel that reads T.
+void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs_in, bool transpose, int fam = F_WY,
+              bool join_side = false) {
   Stage stage_(c, "wy_batch");
   (void)fam;
+  struct Joiner {   // whatever path returns, the side stream is joined
+    spq_ctx* c;
+    bool* pending;
+    ~Joiner() { if (*pending) side_join(c); }
+  } joiner_{c, &join_side};
   const size_t budget = std::max<size_t>(chunk_bytes() / sizeof(double), 2);
   std::vector<WyProb> probs;
   size_t tot = 0;
@@ -1435,6 +1449,7 @@ void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs_in, bool transpose, i
         c->tm.flops[F_WY] += 4.0 * p.m * (double)p.n * p.k - (double)p.n * p.k * p.k;
         wj.push_back(w);
       }
+      if (join_side) { side_join(c); join_side = false; }
       Scope s(c, F_WY, wyf_tag(c, wj, tiles, cl));
       launch_wyf(up_or_param(c, wj, PL_WYF), wj.data(), (int)wj.size(), tiles, kmax, cl, c->st);
       c->tm.launches[F_WY]++;
@@ -1466,6 +1481,7 @@ void wy_batch(spq_ctx* c, const std::vector<WyProb>& probs_in, bool transpose, i
       g3.add(p.V, p.m, W2, p.k, p.C, p.ldc, p.m, p.n, p.k, -1.0, 1.0);
     }
     g1.run(c, true, flops);
+    if (join_side) { side_join(c); join_side = false; }
     g2.run(c, transpose, 0);
     g3.run(c, false, 0);
   }
@@ -1627,8 +1643,15 @@ void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
     for (auto& t : q.targets) wp.push_back(WyProb{q.P, q.T, q.m, q.k, t.C, t.ldc, t.n});
   }
   if (!tp.empty()) {
-    build_full_T(c, tp);
-    wy_batch(c, wp, true);
+    static const bool overlap_T = !env_flag("SPQ_NO_T_OVERLAP");
+    const bool ov = overlap_T && !wp.empty() && !c->on_side && !c->side_pending;
+    if (ov) {
+      SideScope side_(c);
+      build_full_T(c, tp);
+    } else {
+      build_full_T(c, tp);
+    }
+    wy_batch(c, wp, true, F_WY, ov);
   }
 }
 
@@ -1974,6 +1997,9 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
   Stage stage_(c, "apply_front_structure");
   HostTimer ht(&c->host_ms[6]);
   const int s = f.s;
+  f.psrc.reserve(f.parts.size());
+  f.gsrc.reserve(f.parts.size() * f.cols_t.size());
+  f.dsts.reserve(f.parts.size() * (f.cols_t.size() + 1));
   // gather sources (current blocks, before any replacement)
   for (int pi = 0; pi < (int)f.parts.size(); ++pi) {
     auto& p = f.parts[pi];
@@ -2011,9 +2037,15 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
       const int nr = (int)c->rows_of[p.r].size();
       if (p.full) {
         Block* old = find_block(c, p.r, cc);
-        if (old) release_mem(c, *old);
-        Block& b = put_block(c, p.r, cc, full_slab[pi] + (int64_t)f.woff[ci] * nr, nr, ncol,
-                             full_slab[pi]);
+        double* mem = full_slab[pi] + (int64_t)f.woff[ci] * nr;
+        if (old) {   // replaced in place: the map and adjacency entries stay
+          release_mem(c, *old);
+          old->p = mem;
+          old->base = full_slab[pi];
+          old->nr = nr;
+          old->nc = ncol;
+        }
+        Block& b = old ? *old : put_block(c, p.r, cc, mem, nr, ncol, full_slab[pi]);
         // speculative: every row is a panel row and receives a row of
         // H^T C_all with cc present -- nonzero (verified at the next query)
         b.flags.assign(nr, c->spec ? 1 : 2);
@@ -2045,11 +2077,25 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
       }
     }
   }
-  // delete row/col s (factor.py:481-484)
-  std::vector<int> rr(c->cix[s].begin(), c->cix[s].end());
-  for (int r : rr) drop_block(c, r, s);
-  std::vector<int> cc2(c->rix[s].begin(), c->rix[s].end());
-  for (int cc : cc2) drop_block(c, s, cc);
+  // delete row/col s (factor.py:481-484): the blocks leave the map and the
+  // NEIGHBOURS' adjacency lists; the lists of s itself are cleared by retire()
+  {
+    const FlatSet& col = c->cix[s];
+    for (size_t t = 0; t < col.v.size(); ++t) {
+      const int r = col.v[t];
+      if (Block* b = col.b[t] ? col.b[t] : c->blk.find(bkey(r, s))) release_mem(c, *b);
+      c->blk.erase(bkey(r, s));
+      if (r != s) c->rix[r].erase(s);
+    }
+    const FlatSet& row = c->rix[s];
+    for (size_t t = 0; t < row.v.size(); ++t) {
+      const int cc = row.v[t];
+      if (cc == s) continue;   // (s, s) went with the column
+      if (Block* b = row.b[t] ? row.b[t] : c->blk.find(bkey(s, cc))) release_mem(c, *b);
+      c->blk.erase(bkey(s, cc));
+      c->cix[cc].erase(s);
+    }
+  }
   // record + bookkeeping (factor.py:486-492)
   Record rec;
   rec.kind = REC_ELIM;
@@ -2057,7 +2103,7 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
   rec.m = f.m;
   rec.k = f.k;
   rec.n = f.n;
-  rec.rows = f.stack_rows;
+  rec.rows = std::move(f.stack_rows);   // (the planner stamped its rows before this call)
   rec.cols_s = c->cols_of[s];
   for (int cc : f.cols_t) rec.cols_n.insert(rec.cols_n.end(), c->cols_of[cc].begin(), c->cols_of[cc].end());
   const size_t mk = (size_t)f.m * f.k, kk = (size_t)f.k * f.k, kn = (size_t)f.k * f.n;
@@ -2174,6 +2220,11 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
   const int* d_ixpack = ixpack.empty() ? nullptr : upload(c, ixpack);
   // gather
   CopyBatch g;
+  {
+    size_t ng = 0;
+    for (auto& f : wave) ng += f.psrc.size() + f.gsrc.size();
+    g.reserve(ng);
+  }
   for (size_t fi = 0; fi < wave.size(); ++fi) {
     Front& f = wave[fi];
     Record& rec = c->recs[f.rec];
@@ -2217,6 +2268,11 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
   }
   // scatter: R_sn = C[:k], neighbour rows back into blocks
   CopyBatch sc;
+  {
+    size_t ns = 0;
+    for (auto& f : wave) ns += f.dsts.size() + 1;
+    sc.reserve(ns);
+  }
   for (size_t fi = 0; fi < wave.size(); ++fi) {
     Front& f = wave[fi];
     if (front_chunked(f)) continue;
@@ -2275,7 +2331,9 @@ void do_factor(spq_ctx* c, const std::vector<int>& ids) {
     if (!c->spec) pivot_raise(c, ps);
     ++wave_id;
     std::vector<Front> wave;
+    wave.reserve(ids.size() - pos);
     CopyBatch zeros;
+    zeros.reserve(2 * (ids.size() - pos) + 64);
     size_t wave_bytes = 0;
     while (pos < ids.size()) {
       const int s = ids[pos];
@@ -2696,6 +2754,8 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
     tp.push_back(TProb{j.V, j.np, j.rank, j.tau, j.T});
     wp.push_back(WyProb{j.V, j.T, j.np, j.rank, j.M, j.np, j.ncols});
   }
+  // (no T / W overlap here: the side stream still carries the previous
+  // wave's dropped-norm statistics, which must stay off the critical path)
   build_full_T(c, tp);
   wy_batch(c, wp, true);
   // dropped = max(||E1||_2, ||E2||_2), E1^T = QtM[r:, :nu], E2 = QtM[r:, nu:]
@@ -3534,6 +3594,11 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
         nb.origin = 7;
         off += (size_t)R * C;
       }
+    }
+    {
+      size_t ncp = 0;
+      for (int q = g0; q < Pi; ++q) ncp += by_prow[q].size();
+      cp.reserve(ncp);
     }
     for (int q = g0; q < Pi; ++q)
       for (auto& kb : by_prow[q]) {
