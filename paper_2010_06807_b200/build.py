@@ -29,6 +29,8 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std
 # diagnostic build: clock64 stamps inside the latency-bound kernels (tools/*_trace.py)
 if os.environ.get("SPQ_TRACE") == "1":
     FLAGS.append("-DSPQ_TRACE")
+    if os.environ.get("SPQ_TRACE_MMAX"):
+        FLAGS.append("-DSPQ_TRACE_MMAX=" + os.environ["SPQ_TRACE_MMAX"])
 
 
 def needs_build():

@@ -1079,7 +1079,10 @@ struct Rg3Layout {   // shared memory in doubles; rows padded to mp = tpc * R
 // diagnostic build only (SPQ_TRACE=1 python -m paper_2010_06807_b200.build):
 // per-step clock64 stamps of thread 0 / CTA 0, read by spq_debug_cpqr_trace
 __device__ long long g_cpqr_trace[64 * 12];
-#define RG_STAMP(slot) do { if (q == 0 && tid == 0 && i < 64) g_cpqr_trace[i * 12 + (slot)] = clock64(); } while (0)
+#ifndef SPQ_TRACE_MMAX
+#define SPQ_TRACE_MMAX 1000000   // -DSPQ_TRACE_MMAX=64: stamps of the small (typical 2D) interfaces only
+#endif
+#define RG_STAMP(slot) do { if (q == 0 && tid == 0 && i < 64 && m <= SPQ_TRACE_MMAX) g_cpqr_trace[i * 12 + (slot)] = clock64(); } while (0)
 #else
 #define RG_STAMP(slot) do { } while (0)
 #endif

@@ -734,6 +734,111 @@ __global__ void __launch_bounds__(4 * LARFT_FULL_MAX) larft_full_kernel(const La
   }
 }
 
+// Blocked variant of the same launch (default): the long row recurrence above
+// is a dependent chain of k steps (row 0: ~450 cycles per step, ~60 us at
+// k = 130) on ONE SM.  Here
+//   1. the 32 x 32 diagonal blocks T_JJ -- each depends only on G_JJ and
+//      tau_J -- are built at the same time, four lanes per row (32 steps);
+//   2. block column J (rows above it, j0 = 32, 64, ...) by two small
+//      products, all in shared memory:
+//        Y = G[0:j0, J] T_JJ                (in place over G[0:j0, J])
+//        T[0:j0, J] = -T[0:j0, 0:j0] Y      (rows independent)
+// T[a,b] (b > a) lives in the strictly lower triangle (S[b + a ld]), tau on
+// the diagonal; ld is odd so a row read across 32 columns is conflict-free.
+constexpr int LARFT_BLK_NT = 512;
+
+__global__ void __launch_bounds__(LARFT_BLK_NT) larft_blk_kernel(const LarftJob* __restrict__ jobs_g,
+                                                               const __grid_constant__ PList<LarftJob, PL_SMALL> pl) {
+  const LarftJob J = jobs_g ? jobs_g[blockIdx.x] : pl.v[blockIdx.x];
+  const int k = J.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = LARFT_BLK_NT, NW = NT / 32;
+  const int ld = k | 1;
+  extern __shared__ double S[];
+  // G (strict upper triangle) and tau (diagonal), eight independent loads per thread
+  for (int e0 = 0; e0 < k * k; e0 += 8 * NT) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + tid + u * NT;
+      const int a = e % k, b = e / k;
+      t[u] = (e < k * k && a <= b) ? (a < b ? __ldg(J.G + a + (int64_t)b * J.ldg) : __ldg(J.tau + a)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + tid + u * NT;
+      const int a = e % k, b = e / k;
+      if (e < k * k && a <= b) S[a + b * ld] = t[u];
+    }
+  }
+  __syncthreads();
+  // ---- 1. diagonal blocks: row f of block jb by four lanes
+  const int nblk = (k + 31) / 32;
+  for (int jb0 = 0; jb0 < nblk; jb0 += NT / 128) {
+    const int jb = jb0 + tid / 128;
+    const int f = (tid & 127) >> 2, sub = tid & 3;
+    const int j0 = jb * 32, w = min(32, k - j0);
+    const unsigned gm = 0xFu << (lane & 28);
+    if (jb < nblk && f < w) {
+      const int a = j0 + f;
+      const double ta = S[a + a * ld];
+      double* Ta = S + a * ld;   // Ta[b] = T[a,b], b > a
+      for (int i = a + 1; i < j0 + w; ++i) {
+        const double* Gi = S + i * ld;   // Gi[b] = G[b,i], b < i
+        double s0 = sub == 0 ? ta * Gi[a] : 0.0, s1 = 0.0;
+        int b = a + 1 + sub;
+        for (; b + 4 < i; b += 8) {
+          s0 = fma(Ta[b], Gi[b], s0);
+          s1 = fma(Ta[b + 4], Gi[b + 4], s1);
+        }
+        if (b < i) s0 = fma(Ta[b], Gi[b], s0);
+        double sv = s0 + s1;
+        sv += __shfl_xor_sync(gm, sv, 1);
+        sv += __shfl_xor_sync(gm, sv, 2);
+        const double ti = Gi[i];
+        if (sub == 0) Ta[i] = (ti != 0.0) ? -ti * sv : 0.0;
+        __syncwarp(gm);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- 2. block columns above the diagonal blocks
+  for (int j0 = 32; j0 < k; j0 += 32) {
+    const int w = min(32, k - j0);
+    // Y[b][e] = sum_{f<=e} G[b][j0+f] T_JJ[f][e]: warp per row b, lane e; in
+    // place (every lane has read its G entries before any lane writes)
+    for (int b = warp; b < j0; b += NW) {
+      double y = 0.0;
+      if (lane < w) {
+        const int ce = j0 + lane;
+        for (int f = 0; f < lane; ++f) y = fma(S[b + (j0 + f) * ld], S[ce + (j0 + f) * ld], y);
+        y = fma(S[b + ce * ld], S[ce + ce * ld], y);   // f = e: T[e][e] = tau_e
+      }
+      __syncwarp();
+      if (lane < w) S[b + (j0 + lane) * ld] = y;
+    }
+    __syncthreads();
+    // T[a][j0+e] = -sum_{b=a}^{j0-1} T[a][b] Y[b][e]   (T[a][a] = tau_a)
+    for (int a = warp; a < j0; a += NW) {
+      if (lane < w) {
+        const int ce = j0 + lane;
+        double t0 = S[a + a * ld] * S[a + ce * ld], t1 = 0.0;
+        int b = a + 1;
+        for (; b + 1 < j0; b += 2) {
+          t0 = fma(S[b + a * ld], S[b + ce * ld], t0);
+          t1 = fma(S[b + 1 + a * ld], S[b + 1 + ce * ld], t1);
+        }
+        if (b < j0) t0 = fma(S[b + a * ld], S[b + ce * ld], t0);
+        S[ce + a * ld] = -(t0 + t1);
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < k * k; e += NT) {
+    const int a2 = e % k, i = e / k;
+    J.T[a2 + (int64_t)i * J.ldt] = a2 < i ? S[i + a2 * ld] : (a2 == i ? S[a2 + a2 * ld] : 0.0);
+  }
+}
+
 int larft_full_max() { return LARFT_FULL_MAX; }
 
 void launch_larft_full(const LarftJob* d_jobs, const LarftJob* h_jobs, int njobs, int kmax,
@@ -743,6 +848,17 @@ void launch_larft_full(const LarftJob* d_jobs, const LarftJob* h_jobs, int njobs
   if (!d_jobs) {
     if (njobs > PL_SMALL) throw std::runtime_error("launch_larft_full: parameter list too long");
     for (int i = 0; i < njobs; ++i) pl.v[i] = h_jobs[i];
+  }
+  static const bool rowwise = getenv("SPQ_LARFT_ROWWISE") && getenv("SPQ_LARFT_ROWWISE")[0] == '1';
+  if (!rowwise) {
+    const size_t smem = (size_t)kmax * (kmax | 1) * sizeof(double);
+    static size_t conf = 0;
+    if (smem > conf) {
+      CUDA_TRY(cudaFuncSetAttribute(larft_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      conf = smem;
+    }
+    larft_blk_kernel<<<njobs, LARFT_BLK_NT, smem, st>>>(d_jobs, pl); SPQ_LAUNCH_CHECK();
+    return;
   }
   const size_t smem = (size_t)kmax * ((kmax + 1) & ~1) * sizeof(double);
   static size_t conf = 0;
