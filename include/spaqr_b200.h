@@ -125,6 +125,12 @@ int spq_trailing_stats(spq_ctx* ctx, int64_t* nblocks, int64_t* nnz);
  * for slots [0, n) by spq_trailing_nnz (one synchronization). */
 int spq_trailing_stats_async(spq_ctx* ctx, int slot, int64_t* nblocks);
 int spq_trailing_nnz(spq_ctx* ctx, int n, int64_t* out);
+/* keys (row cluster, column cluster) of the live trailing blocks -- the keys of
+ * the reference's `TrailingState.trailing` dict (factor.py:349), which its
+ * symbolic audit compares with `symbolic_fill_levels` (factor.py:1004-1050,
+ * tests/test_factor.py:168-183).  At most `cap` pairs are written; *n
+ * receives the full count. */
+int spq_trailing_keys(spq_ctx* ctx, int64_t cap, int32_t* rows, int32_t* cols, int64_t* n);
 int spq_row_of_col(spq_ctx* ctx, int64_t* out);
 int spq_payload_scalars(spq_ctx* ctx, int64_t* out);
 /* per kernel family [ms, algorithmic flops, launches, bytes] x 7 families

@@ -50,6 +50,7 @@ SIGNATURES = {
     "spq_trailing_stats_async": (C.c_int, [_ctx, C.c_int, C.POINTER(C.c_int64)]),
     "spq_trailing_nnz": (C.c_int, [_ctx, C.c_int, _i64p]),
     "spq_row_of_col": (C.c_int, [_ctx, _i64p]),
+    "spq_trailing_keys": (C.c_int, [_ctx, C.c_int64, _i32p, _i32p, C.POINTER(C.c_int64)]),
     "spq_payload_scalars": (C.c_int, [_ctx, C.POINTER(C.c_int64)]),
     "spq_timings": (C.c_int, [_ctx, _f64p, C.c_int]),
     "spq_reset_timings": (C.c_int, [_ctx]),

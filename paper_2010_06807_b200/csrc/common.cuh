@@ -252,6 +252,9 @@ int cpqr_cluster_size(int m, int ncap);
 size_t cpqr_cluster_smem(int m, int ncap, int cl);
 void launch_cpqr_cluster(const CpqrJob* d_jobs, int njobs, int cl, size_t smem, cudaStream_t st);
 int cpqr_reg_plan(int m, int n, int variant, int* tpc, int* nt);
+int cpqr_reg_nvar();
+int cpqr_reg_rows(int variant);
+int cpqr_reg_elems(int variant);
 size_t cpqr_reg_smem(int padded_rows, int cl, int nt);
 void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int variant, int cl, int tpc, int nt, size_t smem,
                      cudaStream_t st);

@@ -1355,8 +1355,15 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
 // holds all n columns wins: a pivot step is bound by one SM's issue rate, so
 // the columns are spread as widely as the cluster limit allows
 // (SPQ_CPQR_NTMIN / SPQ_CPQR_CLMAX narrow the choice for A/B runs).
+constexpr int RG_NVAR = 5;
+static const int RG_R[RG_NVAR] = {16, 8, 4, 16, 8}, RG_C[RG_NVAR] = {2, 4, 8, 1, 2};
+int cpqr_reg_nvar() { return RG_NVAR; }
+int cpqr_reg_rows(int v) { return RG_R[v]; }
+int cpqr_reg_elems(int v) { return RG_R[v] * RG_C[v]; }
+
 int cpqr_reg_plan(int m, int n, int v, int* tpc_out, int* nt_out) {
-  static const int RR[3] = {16, 8, 4}, CC[3] = {2, 4, 8};
+  const int* RR = RG_R;
+  const int* CC = RG_C;
   static int clmax = -1, ntmin = 128;
   if (clmax < 0) {
     const char* e = getenv("SPQ_CPQR_CLMAX");
@@ -1428,6 +1435,8 @@ void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, in
     case 0: launch_rg<16, 2>(d_jobs, pl, njobs, cl, tpc, nt, smem, st); break;
     case 1: launch_rg<8, 4>(d_jobs, pl, njobs, cl, tpc, nt, smem, st); break;
     case 2: launch_rg<4, 8>(d_jobs, pl, njobs, cl, tpc, nt, smem, st); break;
+    case 3: launch_rg<16, 1>(d_jobs, pl, njobs, cl, tpc, nt, smem, st); break;
+    case 4: launch_rg<8, 2>(d_jobs, pl, njobs, cl, tpc, nt, smem, st); break;
     default: throw std::runtime_error("cpqr_reg: bad variant");
   }
 }

@@ -2548,21 +2548,23 @@ void run_cpqr_jobs(spq_ctx* c, const std::vector<CpqrJob>& jobs) {
     // register plan: smallest CTA (widest spread), then fewest lanes per
     // column (fewest shuffles per reduction), then least row padding
     int bv = -1, bcl = 0, btpc = 0, bnt = 0;
-    static const int RR[3] = {16, 8, 4};
+    static const int only_var = getenv("SPQ_CPQR_VAR") ? atoi(getenv("SPQ_CPQR_VAR")) : -1;   // A/B runs
+    static const int nvar = getenv("SPQ_CPQR_NVAR") ? atoi(getenv("SPQ_CPQR_NVAR")) : 3;
     if (!coop_only && !no_ws)
-      for (int v = 0; v < 3; ++v) {
+      for (int v = 0; v < std::min(nvar, cpqr_reg_nvar()); ++v) {
+        if (only_var >= 0 && v != only_var) continue;
         int tpc = 0, nt = 0;
         const int cl = cpqr_reg_plan(np, ncap, v, &tpc, &nt);
         if (cl == 0) continue;
-        const auto key = std::make_tuple(nt, tpc * RR[v], tpc, cl);
-        if (bv < 0 || key < std::make_tuple(bnt, btpc * RR[bv], btpc, bcl)) { bv = v; bcl = cl; btpc = tpc; bnt = nt; }
+        const auto key = std::make_tuple(nt, tpc * cpqr_reg_rows(v), tpc, cl);
+        if (bv < 0 || key < std::make_tuple(bnt, btpc * cpqr_reg_rows(bv), btpc, bcl)) { bv = v; bcl = cl; btpc = tpc; bnt = nt; }
       }
     static const bool cpqr_log = env_flag("SPQ_CPQR_LOG");   // diagnostics: problem sizes and plans
     if (cpqr_log) fprintf(stderr, "[cpqr] m=%d ncap=%d n=%d variant=%d cl=%d tpc=%d nt=%d\n", np, ncap, q.n, bv, bcl, btpc, bnt);
     if (bv >= 0) {
       auto& g = rg_groups[std::make_tuple(bv, bcl, btpc, bnt)];
       g.first.push_back(q);
-      g.second = std::max(g.second, cpqr_reg_smem(btpc * RR[bv], bcl, bnt));
+      g.second = std::max(g.second, cpqr_reg_smem(btpc * cpqr_reg_rows(bv), bcl, bnt));
       continue;
     }
     if (!coop_only && !env_flag("SPQ_CPQR_CLUSTER") && cpqr_cta_smem(np, ncap) <= CPQR_CTA_MAX_SMEM) {
@@ -4498,6 +4500,22 @@ int spq_trailing_nnz(spq_ctx* c, int n, int64_t* out) {
                              cudaMemcpyDeviceToHost, c->st));
     sync(c);
     for (int i = 0; i < n; ++i) out[i] = (int64_t)h[i];
+  });
+}
+
+int spq_trailing_keys(spq_ctx* c, int64_t cap, int32_t* rows, int32_t* cols, int64_t* n) {
+  return guarded(c, [&] {
+    int64_t t = 0;
+    for (int i = 0; i < c->ncl; ++i) {   // ascending (row, column): the sorted adjacency lists
+      const FlatSet& row = c->rix[i];
+      for (size_t q = 0; q < row.v.size(); ++q) {
+        const Block* b = row.b[q] ? row.b[q] : c->blk.find(bkey(i, row.v[q]));
+        if (!b || (int64_t)b->nr * b->nc == 0) continue;
+        if (t < cap) { rows[t] = i; cols[t] = row.v[q]; }
+        ++t;
+      }
+    }
+    *n = t;
   });
 }
 

@@ -319,8 +319,20 @@ class _StateView:
             return range(int(r.value if self.axis == 0 else c.value))
 
     def __init__(self, ctx):
+        self.ctx = ctx
         self.rows_of = self._Sized(ctx, 0)
         self.cols_of = self._Sized(ctx, 1)
+
+    def trailing_keys(self):
+        """(row cluster, column cluster) of every live trailing block: the
+        keys of the reference's `state.trailing` dict (factor.py:349)."""
+        import ctypes as C
+        n = C.c_int64()
+        z = np.zeros(0, np.int32)
+        self.ctx.call("spq_trailing_keys", 0, z, z, C.byref(n))
+        r, c = np.zeros(n.value, np.int32), np.zeros(n.value, np.int32)
+        self.ctx.call("spq_trailing_keys", int(n.value), r, c, C.byref(n))
+        return set(zip(r.tolist(), c.tolist()))
 
 
 def _cluster_lists(clusters, attr):

@@ -285,3 +285,29 @@ def test_variant_targets_match_reference(name, cfg, n, opts):
     g = load(name)
     A, b, F, x, rep = _run(name, cfg, n, **opts)
     _check_against_reference(F, rep, g)
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", 24), ("C3", 48), ("C4", 12)])
+def test_fill_within_symbolic_prediction(cfg, n, golden_dir):
+    """The device path creates blocks only where the reference's symbolic
+    elimination predicts fill (reference test tests/test_factor.py:168-183):
+    at every level of the drop-free factorization, the live block keys are a
+    subset of the golden `symbolic_fill_levels` pattern of the live reference."""
+    import os
+    from paper_2010_06807_b200.factor import factorize
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    g = np.load(os.path.join(golden_dir, "symbolic.npz"))
+    A, dims, L, eps, b, tol = make_config(cfg, n=n)
+    tree = partition_geometric(dims, L)
+    seen = {}
+
+    class Obs:
+        def on_level(self, state, lev, st):
+            seen[lev] = state.trailing_keys()
+
+    factorize(A, tree, eps=eps, sparsify=False, observer=Obs())
+    assert sorted(seen) == list(range(1, L + 1))
+    for lev, keys in seen.items():
+        ref = {tuple(p) for p in g[f"{cfg}_n{n}_L{lev}"].tolist()}
+        assert keys <= ref, (lev, sorted(keys - ref)[:5])

@@ -165,3 +165,21 @@ def test_bench_gpus_flag_spawns_ranks():
     assert len(lines) == 1
     assert lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
     assert lines[0]["config"]["config"] == "C1" and lines[0]["config"]["N"] == 4096
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", 24), ("C3", 48), ("C4", 12)])
+def test_symbolic_fill_levels_match_reference(cfg, n):
+    """The symbolic (drop-free) fill prediction equals the live reference's
+    `symbolic_fill_levels` (factor.py:1004-1050) level by level (golden
+    written by tests/golden/make_symbolic.py)."""
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    from paper_2010_06807_b200.symbolic import symbolic_fill_levels
+    g = np.load(os.path.join(GOLDEN, "symbolic.npz"))
+    A, dims, L, eps, b, tol = make_config(cfg, n=n)
+    tree = partition_geometric(dims, L)
+    pat = symbolic_fill_levels(A, tree)
+    assert sorted(pat) == list(range(1, L + 1))
+    for lev, pairs in pat.items():
+        ref = {tuple(p) for p in g[f"{cfg}_n{n}_L{lev}"].tolist()}
+        assert pairs == ref, (lev, len(pairs), len(ref))
