@@ -987,7 +987,9 @@ void flush_deferred(spq_ctx* c) {
 struct Fork {
   spq_ctx* c;
   int used = 0;
-  explicit Fork(spq_ctx* cc) : c(cc) {
+  bool single = false;   // one launch only: it goes straight to the context stream
+  explicit Fork(spq_ctx* cc, int nlaunch = 2) : c(cc), single(nlaunch <= 1) {
+    if (single) return;
     if (!c->ev_fork) {
       CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
       for (int k = 0; k < spq_ctx::NAUX; ++k) {
@@ -998,12 +1000,14 @@ struct Fork {
     CUDA_TRY(cudaEventRecord(c->ev_fork, c->st));
   }
   cudaStream_t next() {
+    if (single) return c->st;
     const int k = used % spq_ctx::NAUX;
     if (used < spq_ctx::NAUX) CUDA_TRY(cudaStreamWaitEvent(c->aux[k], c->ev_fork, 0));
     ++used;
     return c->aux[k];
   }
   void join() {
+    if (single) return;
     for (int k = 0; k < std::min(used, spq_ctx::NAUX); ++k) {
       CUDA_TRY(cudaEventRecord(c->ev_join[k], c->aux[k]));
       CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_join[k], 0));
@@ -2593,7 +2597,7 @@ void run_cpqr_jobs(spq_ctx* c, const std::vector<CpqrJob>& jobs) {
                       kv.second.second);
   const CpqrJob* d_cj = cj.empty() ? nullptr : upload(c, cj);
   {
-    Fork fk(c);
+    Fork fk(c, (int)(wl.size() + cl_l.size() + (d_cj ? 1 : 0)));
     for (auto& w : wl) {
       const auto& key = std::get<2>(w);
       launch_cpqr_reg(std::get<0>(w), std::get<4>(w), std::get<1>(w), std::get<0>(key), std::get<1>(key),
