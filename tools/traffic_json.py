@@ -12,7 +12,8 @@ import sys
 
 # bench.py kernel families (runtime.cu Fam scopes) -> kernel-name prefixes
 FAMILIES = {
-    "cpqr": ("cpqr_", "sparsify_select_kernel", "colsq_kernel", "gather_cols_kernel"),
+    "cpqr": ("cpqr_", "sparsify_select_kernel", "colsq_kernel", "gather_cols_kernel",
+             "select_batch_kernel", "colsq_batch_kernel", "gather_cols_batch_kernel"),
     "qr": ("panel_qr", "larft", "pivot_check_kernel"),
     "wy": ("gemm_dmma", "wyf_kernel", "splitk_reduce_kernel"),
     "trsm": ("trsm_",),
