@@ -1064,6 +1064,9 @@ __device__ __forceinline__ int rg_argbest(double v, int pos) {
   return __ffs(__ballot_sync(0xffffffffu, cand && (unsigned)pos == mp)) - 1;
 }
 
+// records at least this long travel as cp.async.bulk copies (SPQ_CPQR_BULK_BYTES)
+__constant__ uint32_t RG_BULK_BYTES = 512;
+
 struct Rg3Layout {   // shared memory in doubles; rows padded to mp = tpc * R
   int m1, cl, rec, nw;  // rec = one candidate record: [value, key, column (m1)]
   __host__ __device__ Rg3Layout(int mp, int cl_, int nw_)
@@ -1116,6 +1119,7 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
   double* sc = rs + L.sco();   // [0] tau, [1] (lp << 32 | pp), [2] stop
   uint64_t* mbar = reinterpret_cast<uint64_t*>(sc + 4);
   const uint32_t rec_bytes = (uint32_t)(L.rec * sizeof(double));
+  const bool bulk = multi && rec_bytes >= RG_BULK_BYTES;   // exchange by bulk copies
 
   if (multi && tid == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -1154,6 +1158,7 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
           for (int r = 0; r < R; ++r) st[2 + sub + tpc * r] = x[c][r];
     }
     if (lane == bl) { st[0] = bv; st[1] = __longlong_as_double((long long)bk); }
+    if (bulk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk copy
     __syncthreads();
   };
   // cluster problems: warp w pushes the CTA winner's record to the CTAs
@@ -1168,7 +1173,17 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
     for (int d = warp; d < CL; d += NW) {
       const uint32_t dst = rg_mapa(rg_smem(RX + ((size_t)slot * CL + q) * L.rec), d);
       const uint32_t mb = rg_mapa(rg_smem(&mbar[slot]), d);
-      for (int idx = lane; idx < L.rec; idx += 32) rg_st_async(dst + 8u * (uint32_t)idx, src[idx], mb);
+      if (bulk) {   // long records: one bulk copy per destination (~21 B/cycle; st.async ~7 B/cycle)
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes "
+                       "[%0], [%1], %2, [%3];" :: "r"(dst), "r"(rg_smem(src)), "r"(rec_bytes), "r"(mb)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
+        }
+      } else {
+        for (int idx = lane; idx < L.rec; idx += 32) rg_st_async(dst + 8u * (uint32_t)idx, src[idx], mb);
+      }
     }
   };
 
@@ -1406,6 +1421,10 @@ static void launch_rg(const CpqrJob* d_jobs, const PList<CpqrJob, PL_SMALL>& pl,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CUDA_TRY(cudaFuncSetAttribute(cpqr_reg_kernel<R, C>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (const char* e = getenv("SPQ_CPQR_BULK_BYTES")) {   // A/B runs
+      const uint32_t v = (uint32_t)strtoul(e, nullptr, 10);
+      CUDA_TRY(cudaMemcpyToSymbol(RG_BULK_BYTES, &v, sizeof v));
+    }
     init = true;
   }
   cudaLaunchConfig_t cfg = {};
