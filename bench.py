@@ -113,17 +113,65 @@ def csc_bytes(A, tree):
 
 
 class Clocks:
-    """nvidia-smi sampler over the timed region (rank 0)."""
+    """SM clock / throttle-reason sampler over the timed region (rank 0).
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    In-process NVML (pynvml) on a sampling thread: `nvidia-smi -lms` -- the
+    first implementation -- holds a driver lock for tens of ms per query,
+    which showed up as +70..95 ms outlier steps in this host-bound benchmark
+    (more samples, more outliers; profiles/r02g).  nvidia-smi remains the
+    fallback when pynvml is missing.  Only samples taken inside `with
+    clocks:` are summarised; the sampler itself is started before the
+    warm-up so its start-up cost is not timed."""
+
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, period=0.1):
         self.index = index
+        self.period = period
         self.p = None
+        self.thread = None
+        self.stop = False
+        self.samples = []      # (time, sm_mhz, sm_max_mhz, reasons bitmask)
+        self.t0 = self.t1 = None
+        self.rows = []
 
-    def __enter__(self):
+    def _visible_index(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            if self.index < len(ids) and ids[self.index].isdigit():
+                return int(ids[self.index])
+        return self.index
+
+    def _loop(self, nv, h):
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h) \
+                    if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons") \
+                    else nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((time.time(), float(sm), float(mx), int(rs)))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.thread is not None or self.p is not None:
+            return self
+        try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self._visible_index())
+            self.nv = nv
+            self.thread = threading.Thread(target=self._loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -133,10 +181,32 @@ class Clocks:
             self.p = None
         return self
 
+    def __enter__(self):
+        self.start()
+        self.t0 = time.time()
+        return self
+
     def __exit__(self, *a):
+        import datetime
+        self.t1 = time.time()
         self.rows = []
+        if self.thread is not None:
+            time.sleep(self.period)
+            self.stop = True
+            self.thread.join(timeout=2)
+            nv = self.nv
+            bits = [("hw_slowdown", nv.nvmlClocksThrottleReasonHwSlowdown),
+                    ("hw_thermal_slowdown", nv.nvmlClocksThrottleReasonHwThermalSlowdown),
+                    ("sw_thermal_slowdown", nv.nvmlClocksThrottleReasonSwThermalSlowdown),
+                    ("sw_power_cap", nv.nvmlClocksThrottleReasonSwPowerCap)]
+            for ts, sm, mx, rs in self.samples:
+                if self.t0 - 0.05 <= ts <= self.t1 + 0.05:
+                    self.rows.append([str(sm), str(mx)] + ["Active" if rs & b else "Not Active"
+                                                           for _, b in bits])
+            return
         if self.p is None:
             return
+        time.sleep(0.3)   # let the sampler print the last in-region sample
         self.p.terminate()
         try:
             out, _ = self.p.communicate(timeout=5)
@@ -145,8 +215,14 @@ class Clocks:
             out = ""
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) >= 6:
-                self.rows.append(f)
+            if len(f) < 7:
+                continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            if self.t0 - 0.05 <= ts <= self.t1 + 0.05:
+                self.rows.append(f[1:])
 
     def summary(self):
         if not getattr(self, "rows", None):
@@ -157,7 +233,8 @@ class Clocks:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows),
+                "sampler": "nvml" if self.thread is not None else "nvidia-smi"}
 
 
 def fp64_peak_tflops():
@@ -389,6 +466,7 @@ def main():
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     l2buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
 
+    clocks = Clocks(local).start()
     for _ in range(max(args.warmup, 0)):
         FZ.factorize(A, tree, eps=eps, device=local)
 
@@ -402,9 +480,6 @@ def main():
     agg = {}
     launches = 0
     barrier()
-    clocks = Clocks(local)
-    if os.environ.get("SPQ_BENCH_NOCLOCKS") == "1":   # diagnostics: is the sampler perturbing the steps?
-        clocks.__enter__ = lambda: clocks
     if os.environ.get("SPQ_BENCH_NOGC") == "1":       # diagnostics: are the outliers collector pauses?
         import gc
         gc.collect()
