@@ -539,8 +539,18 @@ struct Arena {
   }
 };
 
+// streams and synchronisation events of a closed context: creating (and
+// destroying) six streams per factorization showed up as an occasional
+// 30-75 ms host stall at the first fork of a factorization (the first
+// multi-group CPQR wave), and the side stream used to leak
+struct StreamSet {
+  cudaStream_t st = nullptr, side = nullptr, aux[spq_ctx::NAUX] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[spq_ctx::NAUX] = {}, ev_side_a = nullptr, ev_side_b = nullptr;
+};
+
 struct GlobalCache {
   std::mutex mu;
+  std::vector<StreamSet> stream_sets;            // idle (synchronized) sets of closed contexts
   std::vector<std::pair<void*, size_t>> slabs;   // (ptr, bytes)
   Arena arena;
   std::vector<std::pair<char*, char*>> rings;    // (pinned, device) of RING_BYTES
@@ -2608,7 +2618,16 @@ void run_cpqr_jobs(spq_ctx* c, const std::vector<CpqrJob>& jobs) {
     }
     coop.push_back(q);
   }
-  Scope s(c, F_CPQR);
+  std::string cq_tag;
+  if (Scope::scope_log()) {
+    char b[200];
+    int m0 = 0, n0 = 0;
+    for (auto& q : jobs) { m0 = std::max(m0, q.m); n0 = std::max(n0, q.ncap); }
+    snprintf(b, sizeof b, "cpqr jobs=%zu reg_groups=%zu cta=%zu cluster=%zu coop=%zu max_m=%d max_n=%d",
+             jobs.size(), rg_groups.size(), cj.size(), by_cl.size(), coop.size(), m0, n0);
+    cq_tag = b;
+  }
+  Scope s(c, F_CPQR, cq_tag);
   // upload every job list first (the ring), then fork
   std::vector<std::tuple<const CpqrJob*, int, std::tuple<int, int, int, int>, size_t, const CpqrJob*>> wl;
   for (auto& kv : rg_groups)
@@ -2720,7 +2739,7 @@ void do_sparsify_wave(spq_ctx* c, const std::vector<int>& wave, double eps,
   g.run(c);
   SpScal* dsc = (SpScal*)dalloc(c, std::max(nw, 1) * sizeof(SpScal));
   {
-    Scope s(c, F_CPQR);
+    Scope s(c, F_CPQR, Scope::scope_log() ? std::string("prep") : std::string());
     std::vector<PrepJob> pj;
     for (int t = 0; t < nw; ++t) {
       SpJob& j = J[t];
@@ -4228,7 +4247,21 @@ int spq_create(spq_ctx** out, int device) {
     CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
     if (major < 10) throw SpqError(SPQ_ERR_CUDA, "sm_100a device required");
     c->nsm = nsm;
-    CUDA_TRY(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    {
+      auto& g = gcache(c->dev);
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (!g.stream_sets.empty()) {
+        const StreamSet ss = g.stream_sets.back();
+        g.stream_sets.pop_back();
+        c->st = ss.st;
+        c->side = ss.side;
+        c->ev_side_a = ss.ev_side_a;
+        c->ev_side_b = ss.ev_side_b;
+        c->ev_fork = ss.ev_fork;
+        for (int k = 0; k < spq_ctx::NAUX; ++k) { c->aux[k] = ss.aux[k]; c->ev_join[k] = ss.ev_join[k]; }
+      }
+    }
+    if (!c->st) CUDA_TRY(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     cudaMemPool_t pool;
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
@@ -4316,12 +4349,36 @@ void spq_destroy(spq_ctx* c) {
       if (c->pin && c->dring) g.rings.push_back({c->pin, c->dring});
       if (c->counted) --g.n_ctx;
     }
-    for (int k = 0; k < spq_ctx::NAUX; ++k) {
-      if (c->aux[k]) { cudaStreamSynchronize(c->aux[k]); cudaStreamDestroy(c->aux[k]); }
-      if (c->ev_join[k]) cudaEventDestroy(c->ev_join[k]);
+    {   // every stream drained: the whole set goes back to the device's cache
+      StreamSet ss;
+      for (int k = 0; k < spq_ctx::NAUX; ++k) {
+        if (c->aux[k]) cudaStreamSynchronize(c->aux[k]);
+        ss.aux[k] = c->aux[k];
+        ss.ev_join[k] = c->ev_join[k];
+      }
+      if (c->side) cudaStreamSynchronize(c->side);
+      if (c->st) cudaStreamSynchronize(c->st);
+      ss.st = c->st;
+      ss.side = c->side;
+      ss.ev_side_a = c->ev_side_a;
+      ss.ev_side_b = c->ev_side_b;
+      ss.ev_fork = c->ev_fork;
+      auto& g = gcache(c->dev);
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (ss.st && g.stream_sets.size() < 16) {
+        g.stream_sets.push_back(ss);
+      } else {
+        for (int k = 0; k < spq_ctx::NAUX; ++k) {
+          if (ss.aux[k]) cudaStreamDestroy(ss.aux[k]);
+          if (ss.ev_join[k]) cudaEventDestroy(ss.ev_join[k]);
+        }
+        if (ss.ev_fork) cudaEventDestroy(ss.ev_fork);
+        if (ss.side) cudaStreamDestroy(ss.side);
+        if (ss.ev_side_a) cudaEventDestroy(ss.ev_side_a);
+        if (ss.ev_side_b) cudaEventDestroy(ss.ev_side_b);
+        if (ss.st) cudaStreamDestroy(ss.st);
+      }
     }
-    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-    if (c->st) cudaStreamDestroy(c->st);
     if (c->h_spec_bad) {   // every stream of the context is drained: back to the pool
       auto& g = gcache(c->dev);
       std::lock_guard<std::mutex> lk(g.mu);
