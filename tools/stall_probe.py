@@ -56,3 +56,10 @@ for k, (d, lg) in enumerate(steps):
                 print(f"   call #{i} {n}: {1e3 * t:.1f} ms (typical {1e3 * ref:.1f})")
         tot = sum(t for _, t, _ in lg)
         print(f"   in-library {1e3 * tot:.1f} ms of {1e3 * d:.1f}")
+print("typical per-call wall (ms), calls in order:")
+order = sorted(base, key=lambda k: k[0])
+for i, n in order:
+    t = 1e3 * float(np.median(base[(i, n)]))
+    if t >= 0.3:
+        print(f"   #{i:3d} {n:28s} {t:7.2f}")
+print(f"sum of medians {1e3 * sum(float(np.median(v)) for v in base.values()):.1f} ms")
