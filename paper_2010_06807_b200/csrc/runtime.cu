@@ -1188,6 +1188,14 @@ struct CopyBatch {
   }
 };
 
+// (Host threads were tried for the per-front task construction of the large
+// leaf-level waves -- every front fills its own slice -- and measured SLOWER
+// on the GPU boxes: 133.9 ms per C3 factorization with 1 thread, 141.5 with 4,
+// 154.7 with 8, every host phase slowing down, profiles/r02g/host_threads.txt.
+// The loops below therefore run on the calling thread.)
+template <class F>
+void parallel_fronts(size_t n, size_t, F&& fn) { fn((size_t)0, n); }
+
 // --------------------------------------------------------- gemm batches
 // A batch whose output tiles cannot fill the machine splits long-K problems
 // (K >= 1024) into partial products reduced in a fixed order.
@@ -2255,35 +2263,47 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
     }
   }
   const int* d_ixpack = ixpack.empty() ? nullptr : upload(c, ixpack);
-  // gather
+  // gather: every front's tasks at a precomputed offset (empty tasks stay in
+  // the list as no-ops), filled by a few host threads on the large waves
   CopyBatch g;
   {
-    size_t ng = 0;
-    for (auto& f : wave) ng += f.psrc.size() + f.gsrc.size();
-    g.reserve(ng);
-  }
-  for (size_t fi = 0; fi < wave.size(); ++fi) {
-    Front& f = wave[fi];
-    Record& rec = c->recs[f.rec];
-    double* C = scr + coff[fi];
-    f.d_ix.assign(f.parts.size(), nullptr);
-    for (size_t pi = 0; pi < f.parts.size(); ++pi)
-      if (ixoff[fi][pi] != (size_t)-1) f.d_ix[pi] = d_ixpack + ixoff[fi][pi];
-    for (auto& sp : f.psrc) {
-      auto& p = f.parts[sp.part];
-      CopyTask t{};
-      t.src = sp.p; t.dst = rec.V + p.o0; t.src_rows = f.d_ix[sp.part];
-      t.nr = p.o1 - p.o0; t.nc = sp.ncols; t.lds = sp.nr; t.ldd = f.m;
-      g.add(t);
-    }
-    for (auto& sg : f.gsrc) {
-      if (front_chunked(f)) break;
-      auto& p = f.parts[sg.part];
-      CopyTask t{};
-      t.src = sg.p; t.dst = C + p.o0 + (int64_t)sg.col_off * f.m; t.src_rows = f.d_ix[sg.part];
-      t.nr = p.o1 - p.o0; t.nc = sg.ncols; t.lds = sg.nr; t.ldd = f.m;
-      g.add(t);
-    }
+    std::vector<size_t> goff(wave.size() + 1, 0);
+    for (size_t fi = 0; fi < wave.size(); ++fi)
+      goff[fi + 1] = goff[fi] + wave[fi].psrc.size() + (front_chunked(wave[fi]) ? 0 : wave[fi].gsrc.size());
+    g.reserve(goff.back());
+    g.t.resize(goff.back());
+    std::vector<int64_t> tmax(wave.size(), 0);
+    parallel_fronts(wave.size(), goff.back(), [&](size_t f0, size_t f1) {
+      for (size_t fi = f0; fi < f1; ++fi) {
+        Front& f = wave[fi];
+        Record& rec = c->recs[f.rec];
+        double* C = scr + coff[fi];
+        f.d_ix.assign(f.parts.size(), nullptr);
+        for (size_t pi = 0; pi < f.parts.size(); ++pi)
+          if (ixoff[fi][pi] != (size_t)-1) f.d_ix[pi] = d_ixpack + ixoff[fi][pi];
+        CopyTask* out = g.t.data() + goff[fi];
+        int64_t mx = 0;
+        for (auto& sp : f.psrc) {
+          auto& p = f.parts[sp.part];
+          CopyTask t{};
+          t.src = sp.p; t.dst = rec.V + p.o0; t.src_rows = f.d_ix[sp.part];
+          t.nr = p.o1 - p.o0; t.nc = sp.ncols; t.lds = sp.nr; t.ldd = f.m;
+          mx = std::max<int64_t>(mx, (int64_t)std::max(t.nr, 0) * std::max(t.nc, 0));
+          *out++ = t;
+        }
+        if (!front_chunked(f))
+          for (auto& sg : f.gsrc) {
+            auto& p = f.parts[sg.part];
+            CopyTask t{};
+            t.src = sg.p; t.dst = C + p.o0 + (int64_t)sg.col_off * f.m; t.src_rows = f.d_ix[sg.part];
+            t.nr = p.o1 - p.o0; t.nc = sg.ncols; t.lds = sg.nr; t.ldd = f.m;
+            mx = std::max<int64_t>(mx, (int64_t)std::max(t.nr, 0) * std::max(t.nc, 0));
+            *out++ = t;
+          }
+        tmax[fi] = mx;
+      }
+    });
+    for (int64_t v : tmax) g.maxe = std::max(g.maxe, v);
   }
   g.run(c);
   // QR of every panel, its reflectors applied block by block to C_all
@@ -2306,30 +2326,41 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
   // scatter: R_sn = C[:k], neighbour rows back into blocks
   CopyBatch sc;
   {
-    size_t ns = 0;
-    for (auto& f : wave) ns += f.dsts.size() + 1;
-    sc.reserve(ns);
-  }
-  for (size_t fi = 0; fi < wave.size(); ++fi) {
-    Front& f = wave[fi];
-    if (front_chunked(f)) continue;
-    Record& rec = c->recs[f.rec];
-    double* C = scr + coff[fi];
-    CopyTask t{};
-    t.src = C; t.dst = rec.Rsn; t.nr = f.k; t.nc = f.n; t.lds = f.m; t.ldd = f.k;
-    sc.add(t);
-    for (auto& d : f.dsts) {
-      auto& p = f.parts[d.part];
-      CopyTask u{};
-      u.src = C + p.o0 + (int64_t)d.col_off * f.m;
-      u.dst = d.p;
-      u.nr = p.o1 - p.o0;
-      u.nc = d.ncols;
-      u.lds = f.m;
-      u.ldd = d.nr;
-      u.dst_rows = d.full ? nullptr : f.d_ix[d.part];
-      sc.add(u);
-    }
+    std::vector<size_t> soff(wave.size() + 1, 0);
+    for (size_t fi = 0; fi < wave.size(); ++fi)
+      soff[fi + 1] = soff[fi] + (front_chunked(wave[fi]) ? 0 : wave[fi].dsts.size() + 1);
+    sc.reserve(soff.back());
+    sc.t.resize(soff.back());
+    std::vector<int64_t> tmax(wave.size(), 0);
+    parallel_fronts(wave.size(), soff.back(), [&](size_t f0, size_t f1) {
+      for (size_t fi = f0; fi < f1; ++fi) {
+        Front& f = wave[fi];
+        if (front_chunked(f)) continue;
+        Record& rec = c->recs[f.rec];
+        double* C = scr + coff[fi];
+        CopyTask* out = sc.t.data() + soff[fi];
+        int64_t mx = 0;
+        CopyTask t{};
+        t.src = C; t.dst = rec.Rsn; t.nr = f.k; t.nc = f.n; t.lds = f.m; t.ldd = f.k;
+        mx = std::max<int64_t>(mx, (int64_t)std::max(t.nr, 0) * std::max(t.nc, 0));
+        *out++ = t;
+        for (auto& d : f.dsts) {
+          auto& p = f.parts[d.part];
+          CopyTask u{};
+          u.src = C + p.o0 + (int64_t)d.col_off * f.m;
+          u.dst = d.p;
+          u.nr = p.o1 - p.o0;
+          u.nc = d.ncols;
+          u.lds = f.m;
+          u.ldd = d.nr;
+          u.dst_rows = d.full ? nullptr : f.d_ix[d.part];
+          mx = std::max<int64_t>(mx, (int64_t)std::max(u.nr, 0) * std::max(u.nc, 0));
+          *out++ = u;
+        }
+        tmax[fi] = mx;
+      }
+    });
+    for (int64_t v : tmax) sc.maxe = std::max(sc.maxe, v);
   }
   sc.run(c);
   if (scr) dfree(c, scr);
@@ -3662,8 +3693,11 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
         cp.add(x);
         if (tgt->clean) {
           if (B.clean && B.flags.size() == (size_t)B.nr) {
-            for (int t = 0; t < B.nr; ++t)
-              if (B.flags[t] == 1) tgt->flags[roff[i] + t] = 1;
+            {   // clean flags are 0/1: a byte-wise OR (vectorised) instead of a branch per row
+              const uint8_t* src = B.flags.begin();
+              uint8_t* dst = &tgt->flags[roff[i]];
+              for (int t = 0; t < B.nr; ++t) dst[t] |= (uint8_t)(src[t] & 1);
+            }
             if (B.unverified && !tgt->unverified) tgt->origin = (uint8_t)(10 + B.origin % 10);
             tgt->unverified = tgt->unverified || B.unverified;
           } else {
@@ -3695,11 +3729,18 @@ void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
   c->row_of_col.assign(N, -1);
   const int64_t nnz = indptr[N];
   for (int64_t j = 0; j < N; ++j) {
+    bool nz = false;   // the column's squared norm is positive (same products as the device sum)
     for (int64_t e = indptr[j]; e < indptr[j + 1]; ++e) {
       if (indices[e] < 0 || indices[e] >= N) throw SpqError(SPQ_ERR_BAD_INPUT, "row index out of range");
       if (e > indptr[j] && indices[e] <= indices[e - 1])
         throw SpqError(SPQ_ERR_BAD_INPUT, "CSC row indices must be strictly increasing per column");
+      nz = nz || data[e] * data[e] > 0.0;
     }
+    // sparse.py:158-166: a zero column cannot be equilibrated.  Decided on the
+    // host (no read-back of the device's column norms: the load used to end
+    // with a stream synchronization for this one integer)
+    if (equilibrate && !nz)
+      throw SpqError(SPQ_ERR_BAD_INPUT, "cannot equilibrate: column " + std::to_string(j) + " has zero norm");
   }
   std::vector<int> rown(N, -1), coln(N, -1), rpos(N), cpos(N);
   for (int t = 0; t < nleaf; ++t) {
@@ -3797,14 +3838,9 @@ void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
     double** d_bases = (double**)dalloc(c, std::max<size_t>(bases.size(), 1) * sizeof(double*));
     CUDA_TRY(cudaMemcpyAsync(d_bases, bases.data(), bases.size() * sizeof(double*), cudaMemcpyHostToDevice, c->st));
     launch_csc_scatter(d_indptr, nullptr, d_data, nnz, d_off, d_bases, d_eb, c->st);
-    int hz = big;
-    CUDA_TRY(cudaMemcpyAsync(&hz, d_zero, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    dfree(c, d_off);
+    dfree(c, d_off);     // stream-ordered reuse: the scatter is queued before any later user
     dfree(c, d_eb);
     dfree(c, d_bases);
-    if (equilibrate && hz != big)
-      throw SpqError(SPQ_ERR_BAD_INPUT, "cannot equilibrate: column " + std::to_string(hz) + " has zero norm");
   }
   dfree(c, d_indptr);
   dfree(c, d_data);
