@@ -207,7 +207,7 @@ struct CpqrJob {
 namespace spq {
 // d_* == nullptr: the list is passed in the launch parameters from h_* (n <= PL_*)
 void launch_copy(const CopyTask* d_tasks, const CopyTask* h_tasks, int ntasks, int64_t max_elems,
-                 int64_t total_ctas, cudaStream_t st);
+                 int64_t total_ctas, cudaStream_t st, int64_t gran = 2048);
 void launch_rowflags(const double* const* d_ptrs, const int* d_nr, const int* d_nc,
                      const int64_t* d_off, unsigned char* d_out, int nblk, cudaStream_t st);
 void launch_rowflags_verify(const double* const* d_ptrs, const int* d_nr, const int* d_nc,

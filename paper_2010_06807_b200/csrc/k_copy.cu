@@ -126,9 +126,10 @@ __global__ void __launch_bounds__(256) copy_tasks_flat_kernel(const CopyTask* __
 // h_tasks carry cta0/ncta (set by the caller for the flattened grid);
 // total_ctas = their sum; max_elems = the largest task.
 void launch_copy(const CopyTask* d_tasks, const CopyTask* h_tasks, int ntasks, int64_t max_elems,
-                 int64_t total_ctas, cudaStream_t st) {
+                 int64_t total_ctas, cudaStream_t st, int64_t gran) {
   if (ntasks <= 0) return;
-  int64_t y = (max_elems + 256 * 8 - 1) / (256 * 8);
+  if (gran < 256) gran = 256 * 8;
+  int64_t y = (max_elems + gran - 1) / gran;
   if (y < 1) y = 1;
   if (y > 512) y = 512;
   if (d_tasks != nullptr && total_ctas > 0 && (int64_t)ntasks * y > 4 * total_ctas + 4096) {

@@ -1170,14 +1170,23 @@ struct CopyBatch {
       tag = b;
     }
     Scope s(c, F_COPY, tag);
+    // elements per CTA: 2048 (eight per thread) while that still fills the
+    // machine, up to 8192 for the big batches -- a CTA's task lookup and launch
+    // cost amortised over more elements (SPQ_COPY_GRAN overrides)
+    int64_t tot_e = 0;
+    for (auto& x : t) tot_e += (int64_t)std::max(x.nr, 0) * std::max(x.nc, 0);
+    static const int64_t gran_env = getenv("SPQ_COPY_GRAN") ? atoll(getenv("SPQ_COPY_GRAN")) : 0;
+    int64_t gran = 2048;
+    while (gran < 8192 && tot_e / (2 * gran) >= (int64_t)c->nsm * 8) gran *= 2;
+    if (gran_env > 0) gran = gran_env;
     int64_t ctas = 0;   // flattened-grid assignment (used for mixed task sizes)
     for (auto& x : t) {
-      const int64_t nb = std::min<int64_t>(512, std::max<int64_t>(1, ((int64_t)x.nr * x.nc + 2047) / 2048));
+      const int64_t nb = std::min<int64_t>(512, std::max<int64_t>(1, ((int64_t)x.nr * x.nc + gran - 1) / gran));
       x.cta0 = (int)ctas;
       x.ncta = (int)nb;
       ctas += nb;
     }
-    launch_copy(up_or_param(c, t, PL_COPY), t.data(), (int)t.size(), maxe, ctas, c->st);
+    launch_copy(up_or_param(c, t, PL_COPY), t.data(), (int)t.size(), maxe, ctas, c->st, gran);
     c->tm.launches[F_COPY]++;
     c->n_kernels++;
     double by = 0;
