@@ -128,6 +128,7 @@ class RowFlags {
 struct Block {
   double* p = nullptr;
   void* base = nullptr;        // shared (refcounted) allocation this block lives in
+  size_t abytes = 0;           // own allocation (base == nullptr): bytes requested from the pool
   int nr = 0, nc = 0;
   RowFlags flags;              // per row: 0 zero, 1 nonzero, 2 unknown (written)
   bool clean = false;
@@ -397,6 +398,8 @@ struct spq_ctx {
   BlockMap blk;
   std::vector<int64_t> row_of_col;
   std::vector<double*> deferred;
+  std::vector<std::pair<void*, size_t>> deferred_blk;   // block memory: (pointer, bytes), see dfree_block
+  std::vector<std::pair<void*, size_t>> side_free_blk;
   // transform chain
   std::vector<Record> recs;
   double* d_scale = nullptr;
@@ -601,11 +604,9 @@ struct Stage {   // tags allocations with the runtime stage making them
 // cudaFreeAsync gives) without the per-call driver cost.
 size_t size_class(size_t b) {
   if (b <= 256) return 256;
-  size_t p = 1;
-  while ((p << 1) <= b) p <<= 1;
+  const size_t p = (size_t)1 << (63 - __builtin_clzll((unsigned long long)b));   // largest power of two <= b
   const size_t q = p >> 2;  // quarter steps: <= 25% waste
-  size_t c = p;
-  while (c < b) c += q;
+  const size_t c = p + ((b - p + q - 1) / q) * q;
   return (c + 255) & ~(size_t)255;
 }
 
@@ -713,7 +714,11 @@ void ensure_arena(GlobalCache& g) {
   if (cap) g.arena.add_free(0, cap);
 }
 
-double* dalloc(spq_ctx* c, size_t bytes) {
+// tracked = false (block memory, new_block_mem): the pointer is not entered in
+// the pointer -> class table; its owner frees it with its size (dfree_block).
+// The table's insert / find / erase per block was ~3 ms of host time per C3
+// factorization (two cache misses per operation, 10^5 operations).
+double* dalloc(spq_ctx* c, size_t bytes, bool tracked = true) {
   if (bytes >= BIG_ALLOC) {
     auto t0 = std::chrono::steady_clock::now();
     // large buffers: process-wide best-fit arena
@@ -788,7 +793,7 @@ double* dalloc(spq_ctx* c, size_t bytes) {
     sid = c->cur_slab;
     c->slab_off += cls;
   }
-  c->pool_size[pkey(p)] = spq_ctx::PoolEnt{cls, sid};
+  if (tracked) c->pool_size[pkey(p)] = spq_ctx::PoolEnt{cls, sid};
   c->slab_live[sid]++;
   c->live_bytes += cls;
   c->peak_bytes = std::max(c->peak_bytes, c->live_bytes);
@@ -863,6 +868,33 @@ void dfree(spq_ctx* c, void* p) {
   c->live_bytes -= e.cls;
 }
 
+int env_flag(const char* name);
+inline bool blocks_untracked() {   // SPQ_ALLOC_TRACK_ALL=1: block memory through the pointer table (A/B runs)
+  static const bool v = !env_flag("SPQ_ALLOC_TRACK_ALL");
+  return v;
+}
+
+// free of untracked block memory (dalloc(..., tracked = false)) by size
+void dfree_block(spq_ctx* c, void* p, size_t bytes) {
+  if (!p) return;
+  if (bytes >= BIG_ALLOC) { dfree(c, p); return; }   // large buffers are tracked in c->big
+  if (c->on_side) {   // still used by queued side work: released at side_join
+    c->side_free_blk.push_back({p, bytes});
+    return;
+  }
+  const size_t cls = size_class(bytes == 0 ? 8 : bytes);
+  int slab = -1;
+  for (size_t i = 0; i < c->slabs.size(); ++i)
+    if (c->slabs[i] && (char*)p >= (char*)c->slabs[i] && (char*)p < (char*)c->slabs[i] + c->slab_caps[i]) {
+      slab = (int)i;
+      break;
+    }
+  if (slab < 0) throw std::runtime_error("dfree_block of unknown pointer");
+  c->pool_free[cls].push_back({p, slab});
+  c->slab_live[slab]--;
+  c->live_bytes -= cls;
+}
+
 // stream-ordered release of a block's memory (shared allocations refcounted)
 void release_mem(spq_ctx* c, Block& b) {
   if (b.base) {
@@ -872,10 +904,12 @@ void release_mem(spq_ctx* c, Block& b) {
       c->refcnt.erase(pkey(b.base));
     }
   } else if (b.p) {
-    c->deferred.push_back(b.p);
+    if (blocks_untracked()) c->deferred_blk.push_back({b.p, b.abytes});
+    else c->deferred.push_back(b.p);
   }
   b.p = nullptr;
   b.base = nullptr;
+  b.abytes = 0;
 }
 
 double* shared_alloc(spq_ctx* c, size_t elems, int nref) {
@@ -937,6 +971,9 @@ void side_join(spq_ctx* c) {
   std::vector<void*> f;
   f.swap(c->side_free);
   for (void* p : f) dfree(c, p);
+  std::vector<std::pair<void*, size_t>> fb;
+  fb.swap(c->side_free_blk);
+  for (auto& e : fb) dfree_block(c, e.first, e.second);
 }
 
 template <class T>
@@ -989,6 +1026,8 @@ const T* up_or_param(spq_ctx* c, const std::vector<T>& v, int pmax) {
 void flush_deferred(spq_ctx* c) {
   for (double* p : c->deferred) dfree(c, p);
   c->deferred.clear();
+  for (auto& e : c->deferred_blk) dfree_block(c, e.first, e.second);
+  c->deferred_blk.clear();
 }
 
 // fork-join: independent launches on auxiliary streams that start after
@@ -1760,6 +1799,7 @@ Block& put_block(spq_ctx* c, int i, int j, double* p, int nr, int nc, void* base
   Block& b = c->blk.get_or_create(bkey(i, j));
   b.p = p;
   b.base = base;
+  b.abytes = base ? 0 : (size_t)std::max(1, nr) * std::max(1, nc) * sizeof(double);   // = new_block_mem(nr, nc)
   b.nr = nr;
   b.nc = nc;
   c->rix[i].insert(j, &b);
@@ -1785,7 +1825,7 @@ void retire(spq_ctx* c, int s) {
 }
 
 double* new_block_mem(spq_ctx* c, int nr, int nc) {
-  return dalloc(c, (size_t)std::max(1, nr) * std::max(1, nc) * sizeof(double));
+  return dalloc(c, (size_t)std::max(1, nr) * std::max(1, nc) * sizeof(double), /*tracked=*/!blocks_untracked());
 }
 
 // refresh row flags of every non-clean block in the given row clusters.
