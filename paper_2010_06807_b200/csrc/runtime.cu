@@ -205,95 +205,39 @@ class FlatMap {
 };
 inline uint64_t pkey(const void* p) { return (uint64_t)(uintptr_t)p; }
 
-// (row cluster, col cluster) -> Block.  Open addressing with linear probing
-// over 64-bit keys; Blocks live in a deque (stable references across
-// inserts) recycled through a free list.  The planner does ~10^5 lookups per
-// factorization: a node-based unordered_map costs two cache misses each.
+// Block objects live in a deque (stable references across inserts) recycled
+// through a free list.  There is no (row, col) -> Block hash table any more:
+// every lookup goes through the sorted row adjacency list of the row cluster
+// (FlatSet below carries the Block pointers), which the planner had at hand
+// anyway; the hash insert / erase per block was ~3 ms of host time per C3
+// factorization.
 class BlockMap {
-  static constexpr uint64_t EMPTY = ~0ull, TOMB = ~1ull;
-  std::vector<uint64_t> keys_;
-  std::vector<uint32_t> idx_;
   std::deque<Block> pool_;
-  std::vector<uint32_t> free_;
-  size_t live_ = 0, used_ = 0;   // used_ = live + tombstones
-  static size_t mix(uint64_t k) {
-    k ^= k >> 31; k *= 0x7fb5d329728ea185ull; k ^= k >> 27; k *= 0x81dadef4bc2dd44dull; k ^= k >> 33;
-    return (size_t)k;
-  }
-  void rehash(size_t cap) {
-    std::vector<uint64_t> ok;
-    std::vector<uint32_t> oi;
-    ok.swap(keys_);
-    oi.swap(idx_);
-    keys_.assign(cap, EMPTY);
-    idx_.assign(cap, 0);
-    used_ = live_;
-    for (size_t t = 0; t < ok.size(); ++t)
-      if (ok[t] < TOMB) {
-        size_t h = mix(ok[t]) & (cap - 1);
-        while (keys_[h] != EMPTY) h = (h + 1) & (cap - 1);
-        keys_[h] = ok[t];
-        idx_[h] = oi[t];
-      }
-  }
-  size_t slot_of(uint64_t k) const {   // slot holding k, or SIZE_MAX
-    if (keys_.empty()) return SIZE_MAX;
-    const size_t m = keys_.size() - 1;
-    for (size_t h = mix(k) & m;; h = (h + 1) & m) {
-      if (keys_[h] == k) return h;
-      if (keys_[h] == EMPTY) return SIZE_MAX;
-    }
-  }
+  std::vector<Block*> free_;
+  size_t live_ = 0;
 
  public:
-  BlockMap() { rehash(1024); }
   size_t size() const { return live_; }
   bool empty() const { return live_ == 0; }
-  void reserve(size_t n) {
-    size_t cap = keys_.size();
-    while (cap < 2 * n) cap <<= 1;
-    if (cap != keys_.size()) rehash(cap);
-  }
-  Block* find(uint64_t k) {
-    const size_t h = slot_of(k);
-    return h == SIZE_MAX ? nullptr : &pool_[idx_[h]];
-  }
-  Block& at(uint64_t k) {
-    Block* b = find(k);
-    if (!b) throw std::out_of_range("block map: missing key");
-    return *b;
-  }
-  Block& get_or_create(uint64_t k) {
-    if (Block* b = find(k)) return *b;
-    if (2 * (used_ + 1) > keys_.size()) rehash(keys_.size() * (2 * (live_ + 1) > keys_.size() / 2 ? 2 : 1));
-    const size_t m = keys_.size() - 1;
-    size_t h = mix(k) & m;
-    while (keys_[h] < TOMB) h = (h + 1) & m;
-    if (keys_[h] == EMPTY) ++used_;
-    uint32_t id;
-    if (!free_.empty()) { id = free_.back(); free_.pop_back(); }
-    else { id = (uint32_t)pool_.size(); pool_.emplace_back(); }
-    keys_[h] = k;
-    idx_[h] = id;
+  void reserve(size_t) {}
+  Block& create() {
     ++live_;
-    return pool_[id];
+    if (!free_.empty()) {
+      Block* b = free_.back();
+      free_.pop_back();
+      return *b;
+    }
+    pool_.emplace_back();
+    return pool_.back();
   }
-  bool erase(uint64_t k) {
-    const size_t h = slot_of(k);
-    if (h == SIZE_MAX) return false;
-    pool_[idx_[h]] = Block();
-    free_.push_back(idx_[h]);
-    keys_[h] = TOMB;
+  void destroy(Block* b) {
+    *b = Block();
+    free_.push_back(b);
     --live_;
-    return true;
   }
   void swap(BlockMap& o) {
-    keys_.swap(o.keys_); idx_.swap(o.idx_); pool_.swap(o.pool_); free_.swap(o.free_);
-    std::swap(live_, o.live_); std::swap(used_, o.used_);
-  }
-  template <class F> void for_each(F&& f) {   // f(key, Block&), unspecified order
-    for (size_t t = 0; t < keys_.size(); ++t)
-      if (keys_[t] < TOMB) f(keys_[t], pool_[idx_[t]]);
+    pool_.swap(o.pool_); free_.swap(o.free_);
+    std::swap(live_, o.live_);
   }
 };
 
@@ -1796,7 +1740,8 @@ void pivot_raise(spq_ctx* c, PivotSet& ps) {
 inline Block* find_block(spq_ctx* c, int i, int j) { return c->rix[i].find(j); }
 
 Block& put_block(spq_ctx* c, int i, int j, double* p, int nr, int nc, void* base = nullptr) {
-  Block& b = c->blk.get_or_create(bkey(i, j));
+  Block* have = c->rix[i].find(j);
+  Block& b = have ? *have : c->blk.create();
   b.p = p;
   b.base = base;
   b.abytes = base ? 0 : (size_t)std::max(1, nr) * std::max(1, nc) * sizeof(double);   // = new_block_mem(nr, nc)
@@ -1808,12 +1753,22 @@ Block& put_block(spq_ctx* c, int i, int j, double* p, int nr, int nc, void* base
 }
 
 void drop_block(spq_ctx* c, int i, int j) {
-  if (Block* b = c->blk.find(bkey(i, j))) {
+  if (Block* b = c->rix[i].find(j)) {
     release_mem(c, *b);
-    c->blk.erase(bkey(i, j));
+    c->blk.destroy(b);
   }
   c->rix[i].erase(j);
   c->cix[j].erase(i);
+}
+
+// every live block with its key, rows ascending, columns ascending within a row
+template <class F>
+void for_each_block(spq_ctx* c, F&& f) {
+  for (int i = 0; i < c->ncl; ++i) {
+    const FlatSet& row = c->rix[i];
+    for (size_t t = 0; t < row.v.size(); ++t)
+      if (row.b[t]) f(bkey(i, row.v[t]), *row.b[t]);
+  }
 }
 
 void retire(spq_ctx* c, int s) {
@@ -1888,7 +1843,7 @@ void refresh_flags(spq_ctx* c, const std::vector<int>& row_clusters) {
       if (bad) {
         Block* hit = nullptr;
         int hr = -1, hc = -1;
-        c->blk.for_each([&](uint64_t key, Block& bb) {
+        for_each_block(c, [&](uint64_t key, Block& bb) {
           if (bb.p == vptrs[t]) { hit = &bb; hr = (int)(key >> 32); hc = (int)(key & 0xffffffffu); }
         });
         fprintf(stderr, "[spec] block (%d,%d) %dx%d origin %d: %d rows differ, first %d pred %d actual %d\n",
@@ -2177,16 +2132,20 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
     const FlatSet& col = c->cix[s];
     for (size_t t = 0; t < col.v.size(); ++t) {
       const int r = col.v[t];
-      if (Block* b = col.b[t] ? col.b[t] : c->blk.find(bkey(r, s))) release_mem(c, *b);
-      c->blk.erase(bkey(r, s));
+      if (Block* b = col.b[t]) {
+        release_mem(c, *b);
+        c->blk.destroy(b);
+      }
       if (r != s) c->rix[r].erase(s);
     }
     const FlatSet& row = c->rix[s];
     for (size_t t = 0; t < row.v.size(); ++t) {
       const int cc = row.v[t];
       if (cc == s) continue;   // (s, s) went with the column
-      if (Block* b = row.b[t] ? row.b[t] : c->blk.find(bkey(s, cc))) release_mem(c, *b);
-      c->blk.erase(bkey(s, cc));
+      if (Block* b = row.b[t]) {
+        release_mem(c, *b);
+        c->blk.destroy(b);
+      }
       c->cix[cc].erase(s);
     }
   }
@@ -3638,18 +3597,11 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
     const FlatSet& row = c->rix[i];
     for (size_t t = 0; t < row.v.size(); ++t) keys.push_back({bkey(i, row.v[t]), row.b[t]});
   }
-  bool walk_ok = keys.size() == c->blk.size();
-  for (size_t t = 0; walk_ok && t < keys.size(); ++t) walk_ok = keys[t].second != nullptr;
-  BlockMap old;
+  if (keys.size() != c->blk.size()) throw SpqError(SPQ_ERR_INTERNAL, "merge: adjacency lists and block count disagree");
+  for (auto& kb : keys)
+    if (!kb.second) throw SpqError(SPQ_ERR_INTERNAL, "merge: adjacency entry without a block");
+  BlockMap old;   // the children's Block objects stay alive (their pool) until the copies are planned
   old.swap(c->blk);
-  if (!walk_ok) {
-    keys.clear();
-    old.for_each([&](uint64_t key, Block& B) { keys.push_back({key, &B}); });
-    std::sort(keys.begin(), keys.end(),
-              [](const std::pair<uint64_t, Block*>& x, const std::pair<uint64_t, Block*>& y) {
-                return x.first < y.first;
-              });
-  }
   for (int s = 0; s < c->ncl; ++s) {
     if (c->active[s]) { c->rows_of[s].clear(); c->cols_of[s].clear(); }
     c->active[s] = 0;
@@ -4619,7 +4571,7 @@ int spq_trailing_stats(spq_ctx* c, int64_t* nblocks, int64_t* nnz) {
     *nblocks = (int64_t)c->blk.size();
     std::vector<const double*> ptrs;
     std::vector<int64_t> sizes;
-    c->blk.for_each([&](uint64_t, Block& b) {
+    for_each_block(c, [&](uint64_t, Block& b) {
       const int64_t n = (int64_t)b.nr * b.nc;
       if (n > 0) { ptrs.push_back(b.p); sizes.push_back(n); }
     });
@@ -4648,7 +4600,7 @@ int spq_trailing_stats_async(spq_ctx* c, int slot, int64_t* nblocks) {
     *nblocks = (int64_t)c->blk.size();
     std::vector<const double*> ptrs;
     std::vector<int64_t> sizes;
-    c->blk.for_each([&](uint64_t, Block& b) {
+    for_each_block(c, [&](uint64_t, Block& b) {
       const int64_t n = (int64_t)b.nr * b.nc;
       if (n > 0) { ptrs.push_back(b.p); sizes.push_back(n); }
     });
@@ -4678,7 +4630,7 @@ int spq_trailing_keys(spq_ctx* c, int64_t cap, int32_t* rows, int32_t* cols, int
     for (int i = 0; i < c->ncl; ++i) {   // ascending (row, column): the sorted adjacency lists
       const FlatSet& row = c->rix[i];
       for (size_t q = 0; q < row.v.size(); ++q) {
-        const Block* b = row.b[q] ? row.b[q] : c->blk.find(bkey(i, row.v[q]));
+        const Block* b = row.b[q];
         if (!b || (int64_t)b->nr * b->nc == 0) continue;
         if (t < cap) { rows[t] = i; cols[t] = row.v[q]; }
         ++t;
