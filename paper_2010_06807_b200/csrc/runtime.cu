@@ -381,7 +381,24 @@ struct spq_ctx {
   double* d_part = nullptr;
   size_t vec_cap = 0, w_cap = 0, part_cap = 0;
   // device memory pool
-  std::unordered_map<size_t, std::vector<std::pair<void*, int>>> pool_free;   // (ptr, slab)
+  // free lists by size class (flat: class sizes grow in quarter-octave steps, ~100 classes
+  // below 8 MB): kv.first = class bytes, kv.second = (ptr, slab) entries
+  struct ClassFree {
+    std::vector<std::pair<size_t, std::vector<std::pair<void*, int>>>> v;
+    std::vector<std::pair<void*, int>>& operator[](size_t cls) {
+      const size_t i = index_of(cls);
+      if (i >= v.size()) v.resize(i + 1);
+      v[i].first = cls;
+      return v[i].second;
+    }
+    static size_t index_of(size_t cls) {   // cls is a size_class() value: 256-byte multiples
+      const size_t u = cls >> 8;
+      const int l = 63 - __builtin_clzll((unsigned long long)u);
+      return l < 2 ? u : (size_t)4 * l + ((u >> (l - 2)) & 3);
+    }
+    std::vector<std::pair<size_t, std::vector<std::pair<void*, int>>>>::iterator begin() { return v.begin(); }
+    std::vector<std::pair<size_t, std::vector<std::pair<void*, int>>>>::iterator end() { return v.end(); }
+  } pool_free;
   bool counted = false;   // included in gcache().n_ctx
   // side stream: work off the critical path whose result is only read at a
   // later join (the sparsifiers' dropped-norm statistic).  While `on_side`,
@@ -1752,6 +1769,19 @@ Block& put_block(spq_ctx* c, int i, int j, double* p, int nr, int nc, void* base
   return b;
 }
 
+// same for a key the caller knows to be absent (no lookup)
+Block& put_block_new(spq_ctx* c, int i, int j, double* p, int nr, int nc, void* base = nullptr) {
+  Block& b = c->blk.create();
+  b.p = p;
+  b.base = base;
+  b.abytes = base ? 0 : (size_t)std::max(1, nr) * std::max(1, nc) * sizeof(double);
+  b.nr = nr;
+  b.nc = nc;
+  c->rix[i].insert(j, &b);
+  c->cix[j].insert(i, &b);
+  return b;
+}
+
 void drop_block(spq_ctx* c, int i, int j) {
   if (Block* b = c->rix[i].find(j)) {
     release_mem(c, *b);
@@ -2049,7 +2079,12 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
   f.psrc.reserve(f.parts.size());
   f.gsrc.reserve(f.parts.size() * f.cols_t.size());
   f.dsts.reserve(f.parts.size() * (f.cols_t.size() + 1));
-  // gather sources (current blocks, before any replacement)
+  // gather sources (current blocks, before any replacement); the same walk
+  // records which (part, target column) blocks exist, so the structure loop
+  // below needs no lookups
+  const int nct = (int)f.cols_t.size();
+  static thread_local std::vector<Block*> exist;
+  exist.assign(f.parts.size() * (size_t)std::max(nct, 1), nullptr);
   for (int pi = 0; pi < (int)f.parts.size(); ++pi) {
     auto& p = f.parts[pi];
     Block* b = find_block(c, p.r, s);
@@ -2057,12 +2092,13 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
     // blocks (p.r, cols_t[ci]): merge-walk of the sorted row list and cols_t
     const FlatSet& row = c->rix[p.r];
     size_t t = 0;
-    for (int ci = 0; ci < (int)f.cols_t.size(); ++ci) {
+    for (int ci = 0; ci < nct; ++ci) {
       const int cc = f.cols_t[ci];
       while (t < row.v.size() && row.v[t] < cc) ++t;
       if (t == row.v.size()) break;
       if (row.v[t] != cc) continue;
       Block* bc = row.b[t];
+      exist[(size_t)pi * nct + ci] = bc;
       if (bc && bc->nr > 0 && bc->nc > 0)
         f.gsrc.push_back({bc->p, bc->nr, pi, f.woff[ci], bc->nc, p.full});
     }
@@ -2085,7 +2121,7 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
       auto& p = f.parts[pi];
       const int nr = (int)c->rows_of[p.r].size();
       if (p.full) {
-        Block* old = find_block(c, p.r, cc);
+        Block* old = exist[(size_t)pi * nct + ci];
         double* mem = full_slab[pi] + (int64_t)f.woff[ci] * nr;
         if (old) {   // replaced in place: the map and adjacency entries stay
           release_mem(c, *old);
@@ -2094,7 +2130,7 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
           old->nr = nr;
           old->nc = ncol;
         }
-        Block& b = old ? *old : put_block(c, p.r, cc, mem, nr, ncol, full_slab[pi]);
+        Block& b = old ? *old : put_block_new(c, p.r, cc, mem, nr, ncol, full_slab[pi]);
         // speculative: every row is a panel row and receives a row of
         // H^T C_all with cc present -- nonzero (verified at the next query)
         b.flags.assign(nr, c->spec ? 1 : 2);
@@ -2102,11 +2138,11 @@ void apply_front_structure(spq_ctx* c, Front& f, CopyBatch& zeros) {
         b.unverified = c->spec;
         b.origin = 1;
       } else {
-        Block* b = find_block(c, p.r, cc);
+        Block* b = exist[(size_t)pi * nct + ci];
         if (!b) {
           double* mem = new_block_mem(c, nr, ncol);
           zeros.zero(mem, (int64_t)nr * ncol);
-          Block& nb = put_block(c, p.r, cc, mem, nr, ncol);
+          Block& nb = put_block_new(c, p.r, cc, mem, nr, ncol);
           nb.flags.assign(nr, 0);
           nb.clean = true;
           b = &nb;
@@ -3664,7 +3700,7 @@ void do_merge(spq_ctx* c, int np_, const int32_t* pid, const int32_t* cptr, cons
       size_t off = 0;
       for (int Pj : v) {
         const int C = (int)c->cols_of[Pj].size();
-        Block& nb = put_block(c, Pi, Pj, slab + off, R, C, slab);
+        Block& nb = put_block_new(c, Pi, Pj, slab + off, R, C, slab);   // the lists were cleared: every parent key is new
         // merged values are copies: the parent's row flags are the OR of its
         // children's (exact given theirs; unverified if any child is)
         if (c->spec) nb.flags.assign(R, 0);
@@ -3800,7 +3836,7 @@ void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
     const int nr = (int)c->rows_of[i].size(), nc = (int)c->cols_of[j].size();
     double* mem = new_block_mem(c, nr, nc);
     zeros.zero(mem, (int64_t)nr * nc);
-    Block& B = put_block(c, i, j, mem, nr, nc);
+    Block& B = put_block_new(c, i, j, mem, nr, nc);   // bkeys are unique
     B.clean = false;
     bases[b] = mem;
   }
