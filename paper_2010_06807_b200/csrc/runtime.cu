@@ -249,6 +249,11 @@ struct FlatSet {
   std::vector<int> v;
   std::vector<Block*> b;
   void insert(int x, Block* blk = nullptr) {
+    if (v.empty() || x > v.back()) {   // ascending arrival (merge, load): append, no search
+      v.push_back(x);
+      b.push_back(blk);
+      return;
+    }
     auto it = std::lower_bound(v.begin(), v.end(), x);
     const size_t i = (size_t)(it - v.begin());
     if (it == v.end() || *it != x) {
