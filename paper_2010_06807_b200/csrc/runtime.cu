@@ -1990,18 +1990,23 @@ bool plan_front(spq_ctx* c, int s, Front& f) {
   p0.o0 = 0;
   p0.o1 = (int)rows_s.size();
   f.parts.push_back(p0);
-  std::vector<int> rs(c->cix[s].begin(), c->cix[s].end());
+  const FlatSet& col_s = c->cix[s];   // (plan_front does not change the structure)
   int off = p0.o1;
-  for (int r : rs) {
+  for (size_t q = 0; q < col_s.v.size(); ++q) {
+    const int r = col_s.v[q];
     if (r == s) continue;
-    Block* b = find_block(c, r, s);
+    Block* b = col_s.b[q];
     if (!b) continue;
     Part p;
     p.r = r;
-    for (int i = 0; i < b->nr; ++i) {
-      const uint8_t fl = b->clean ? b->flags[i] : (b->flags.empty() ? 2 : b->flags[i]);
-      if (fl == 2) return false;
-      if (fl == 1) p.ix.push_back(i);
+    if (b->nr > 0) {
+      if (!b->clean && b->flags.empty()) return false;   // unknown flags
+      const uint8_t* fl = b->flags.begin();
+      p.ix.reserve(b->nr);
+      for (int i = 0; i < b->nr; ++i) {
+        if (fl[i] == 2) return false;
+        if (fl[i] == 1) p.ix.push_back(i);
+      }
     }
     if (p.ix.empty()) continue;
     p.full = (int)p.ix.size() == b->nr;
@@ -2012,7 +2017,8 @@ bool plan_front(spq_ctx* c, int s, Front& f) {
   }
   f.m = off;
   // candidate trailing columns (sorted, unique)
-  std::vector<int> cand;
+  static thread_local std::vector<int> cand;
+  cand.clear();
   {
     static thread_local std::vector<int> mark;   // epoch stamps per cluster
     static thread_local int epoch = 0;
@@ -2028,7 +2034,8 @@ bool plan_front(spq_ctx* c, int s, Front& f) {
   // (block pointers at hand, no lookups); for every candidate the parts and
   // rows examined -- hence the unknown-flag bail-out -- are exactly those of
   // the candidate-major loop.
-  std::vector<char> present(cand.size(), 0);
+  static thread_local std::vector<char> present;
+  present.assign(cand.size(), 0);
   for (auto& p : f.parts) {
     const FlatSet& row = c->rix[p.r];
     size_t q = 0;
@@ -3861,10 +3868,11 @@ void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
         if (data[e] != 0.0) bp[eb[e]]->flags[rpos[indices[e]]] = 1;
   }
   zeros.run(c);
-  int64_t* d_indptr = (int64_t*)dalloc(c, (N + 1) * sizeof(int64_t));
-  double* d_data = dalloc(c, std::max<int64_t>(nnz, 1) * sizeof(double));
-  CUDA_TRY(cudaMemcpyAsync(d_indptr, indptr, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
-  CUDA_TRY(cudaMemcpyAsync(d_data, data, nnz * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  // CSC arrays and the per-entry block map through the pinned upload ring: a
+  // host memcpy into pinned memory plus an asynchronous DMA each, instead of
+  // pageable cudaMemcpyAsync calls (staged synchronously, ~8 MB at C3)
+  int64_t* d_indptr = upload(c, indptr, (size_t)N + 1);
+  double* d_data = nnz ? upload(c, data, (size_t)nnz) : dalloc(c, sizeof(double));
   c->equil = equilibrate != 0;
   c->d_scale = dalloc(c, N * sizeof(double));
   int* d_zero = (int*)dalloc(c, sizeof(int));
@@ -3873,19 +3881,14 @@ void do_load(spq_ctx* c, int64_t N, const int64_t* indptr, const int64_t* indice
   {
     Scope s(c, F_COPY);
     launch_colnorms_scale(d_indptr, nullptr, d_data, N, c->d_scale, d_zero, equilibrate, c->st);
-    int64_t* d_off = (int64_t*)dalloc(c, std::max<int64_t>(nnz, 1) * sizeof(int64_t));
-    int* d_eb = (int*)dalloc(c, std::max<int64_t>(nnz, 1) * sizeof(int));
-    CUDA_TRY(cudaMemcpyAsync(d_off, eoff.data(), nnz * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
-    CUDA_TRY(cudaMemcpyAsync(d_eb, eb.data(), nnz * sizeof(int), cudaMemcpyHostToDevice, c->st));
-    double** d_bases = (double**)dalloc(c, std::max<size_t>(bases.size(), 1) * sizeof(double*));
-    CUDA_TRY(cudaMemcpyAsync(d_bases, bases.data(), bases.size() * sizeof(double*), cudaMemcpyHostToDevice, c->st));
-    launch_csc_scatter(d_indptr, nullptr, d_data, nnz, d_off, d_bases, d_eb, c->st);
-    dfree(c, d_off);     // stream-ordered reuse: the scatter is queued before any later user
-    dfree(c, d_eb);
-    dfree(c, d_bases);
+    if (nnz) {
+      int64_t* d_off = upload(c, eoff);
+      int* d_eb = upload(c, eb);
+      double** d_bases = upload(c, bases);
+      launch_csc_scatter(d_indptr, nullptr, d_data, nnz, d_off, d_bases, d_eb, c->st);
+    }
   }
-  dfree(c, d_indptr);
-  dfree(c, d_data);
+  if (!nnz) dfree(c, d_data);
   dfree(c, d_zero);
 }
 
