@@ -202,7 +202,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 }  // namespace
 
 template <bool TA, int NP>
-__global__ void __launch_bounds__(NT2) gemm_dmma2_kernel(const GemmProb* __restrict__ probs_g,
+__global__ void __launch_bounds__(NT2, 2) gemm_dmma2_kernel(const GemmProb* __restrict__ probs_g,
                                                          int nprob,
                                                          const __grid_constant__ PList<GemmProb, NP> pl) {
   const GemmProb* probs = NP > 1 ? pl.v : probs_g;
