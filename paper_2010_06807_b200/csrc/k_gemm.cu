@@ -189,7 +189,8 @@ void launch_splitk_reduce(const SplitRed* d_tasks, const SplitRed* h_tasks, int 
 // cp.async pipeline (8-byte copies with zero-fill for the ragged edges, any
 // leading dimension), same conflict-free k-major shared layout.
 namespace {
-constexpr int BM2 = 128, BN2 = 64, BK2 = 16, PA2 = 132, PB2 = 68, NT2 = 256, ST2 = 3;
+constexpr int BK2 = 16, NT2 = 256, ST2 = 3;
+constexpr int TILE2_M = 128, TILE2_N = 64;   // variant 2; variant 3 swaps them
 
 __device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -201,10 +202,13 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 }  // namespace
 
-template <bool TA, int NP>
+// BMx x BNx = 128 x 64 (variant 2) or 64 x 128 (variant 3: few rows, e.g. the
+// k x n products W = V^T C, where a 128-row tile pads k = 300 to 384)
+template <bool TA, int NP, int BMx, int BNx>
 __global__ void __launch_bounds__(NT2, 2) gemm_dmma2_kernel(const GemmProb* __restrict__ probs_g,
                                                          int nprob,
                                                          const __grid_constant__ PList<GemmProb, NP> pl) {
+  constexpr int BM2 = BMx, BN2 = BNx, PA2 = BMx + 4, PB2 = BNx + 4, WM = BMx / 32;
   const GemmProb* probs = NP > 1 ? pl.v : probs_g;
   int lo = 0, hi = nprob - 1;
   const int bid = blockIdx.x;
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(NT2, 2) gemm_dmma2_kernel(const GemmProb* __re
   double* Bs = smem2 + ST2 * BK2 * PA2;     // [ST2][BK2][PB2]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  const int wm = (warp % WM) * 32, wn = (warp / WM) * 32;
   const int g = lane >> 2, q = lane & 3;
 
   double acc[4][4][2];
@@ -235,17 +239,17 @@ __global__ void __launch_bounds__(NT2, 2) gemm_dmma2_kernel(const GemmProb* __re
     double* a = As + stage * BK2 * PA2;
     double* b = Bs + stage * BK2 * PB2;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {      // A: 128 x 16 = 2048 elements
+    for (int e = 0; e < BM2 * BK2 / NT2; ++e) {      // A: BM2 x 16 elements
       const int l = tid + e * NT2;
       int mi, ki;
-      if (TA) { ki = l & 15; mi = l >> 4; } else { mi = l & 127; ki = l >> 7; }
+      if (TA) { ki = l & 15; mi = l >> 4; } else { mi = l % BM2; ki = l / BM2; }
       const int gm = m0 + mi, gk = k0 + ki;
       const bool ok = gm < p.m && gk < p.k;
       const double* src = TA ? p.A + gk + (int64_t)gm * p.lda : p.A + gm + (int64_t)gk * p.lda;
       cp8(a + ki * PA2 + mi, src, ok);
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {      // B: 16 x 64 = 1024 elements
+    for (int e = 0; e < BN2 * BK2 / NT2; ++e) {      // B: 16 x BN2 elements
       const int l = tid + e * NT2;
       const int kb = l & 15, nb = l >> 4;
       const int gk = k0 + kb, gn = n0 + nb;
@@ -302,25 +306,35 @@ void gemm_set_variant(int v) { g_variant = v; }
 
 int gemm_tiles(int m, int n) {
   if (m <= 0 || n <= 0) return 0;
-  if (gemm_variant() == 2) return ((m + BM2 - 1) / BM2) * ((n + BN2 - 1) / BN2);
+  if (gemm_variant() == 2) return ((m + TILE2_M - 1) / TILE2_M) * ((n + TILE2_N - 1) / TILE2_N);
+  if (gemm_variant() == 3) return ((m + TILE2_N - 1) / TILE2_N) * ((n + TILE2_M - 1) / TILE2_M);
   return ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
 }
 
 template <int NP>
 static void launch_gemm_t(const GemmProb* d_probs, const PList<GemmProb, NP>& pl, int nprob,
                           int total_tiles, bool transA, cudaStream_t st) {
-  if (gemm_variant() == 2) {
-    const size_t smem = (size_t)ST2 * BK2 * (PA2 + PB2) * sizeof(double);
+  if (gemm_variant() == 2 || gemm_variant() == 3) {
+    const size_t smem = (size_t)ST2 * BK2 * (TILE2_M + 4 + TILE2_N + 4) * sizeof(double);
     static bool init = false;
     if (!init) {
-      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<true, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<false, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<true, NP, TILE2_M, TILE2_N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<false, NP, TILE2_M, TILE2_N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<true, NP, TILE2_N, TILE2_M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CUDA_TRY(cudaFuncSetAttribute(gemm_dmma2_kernel<false, NP, TILE2_N, TILE2_M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       init = true;
     }
-    if (transA)
-      gemm_dmma2_kernel<true, NP><<<total_tiles, NT2, smem, st>>>(d_probs, nprob, pl);
-    else
-      gemm_dmma2_kernel<false, NP><<<total_tiles, NT2, smem, st>>>(d_probs, nprob, pl);
+    if (gemm_variant() == 2) {
+      if (transA)
+        gemm_dmma2_kernel<true, NP, TILE2_M, TILE2_N><<<total_tiles, NT2, smem, st>>>(d_probs, nprob, pl);
+      else
+        gemm_dmma2_kernel<false, NP, TILE2_M, TILE2_N><<<total_tiles, NT2, smem, st>>>(d_probs, nprob, pl);
+    } else {
+      if (transA)
+        gemm_dmma2_kernel<true, NP, TILE2_N, TILE2_M><<<total_tiles, NT2, smem, st>>>(d_probs, nprob, pl);
+      else
+        gemm_dmma2_kernel<false, NP, TILE2_N, TILE2_M><<<total_tiles, NT2, smem, st>>>(d_probs, nprob, pl);
+    }
     SPQ_LAUNCH_CHECK();
     return;
   }

@@ -1230,7 +1230,19 @@ struct GemmBatch {
     int small = 0;
     gemm_set_variant(2);
     for (auto& g : p) small += gemm_tiles(g.m, g.n);
-    gemm_set_variant(small < c->nsm ? 1 : 2);
+    int variant = small < c->nsm ? 1 : 2;
+    if (variant == 2) {
+      // 64 x 128 tiles when they pad noticeably less than 128 x 64 (few rows:
+      // the k x n products W = V^T C of the 3D fronts, k = 100..600)
+      static const bool no_v3 = env_flag("SPQ_GEMM_NO_V3");
+      double a2 = 0, a3 = 0;
+      for (auto& g : p) {
+        a2 += (double)((g.m + 127) / 128) * 128 * ((g.n + 63) / 64) * 64 * g.k;
+        a3 += (double)((g.m + 63) / 64) * 64 * ((g.n + 127) / 128) * 128 * g.k;
+      }
+      if (!no_v3 && a3 < 0.93 * a2) variant = 3;
+    }
+    gemm_set_variant(variant);
     tiles = 0;
     for (auto& g : p) tiles += gemm_tiles(g.m, g.n);
     const int target = 2 * c->nsm;
