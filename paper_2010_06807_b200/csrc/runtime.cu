@@ -1230,6 +1230,9 @@ struct GemmBatch {
     int small = 0;
     gemm_set_variant(2);
     for (auto& g : p) small += gemm_tiles(g.m, g.n);
+    // few output tiles: the 64 x 64 kernel covers the SMs with 4x the CTAs per
+    // area (large tiles + split-K for long-K problems measured no better on C3
+    // and worse on the small shapes, profiles/r02i/gemm_longk_rule.txt)
     int variant = small < c->nsm ? 1 : 2;
     if (variant == 2) {
       // 64 x 128 tiles when they pad noticeably less than 128 x 64 (few rows:
