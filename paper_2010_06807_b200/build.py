@@ -26,6 +26,8 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std
          "-Xcompiler", "-g", "-Xcompiler", "-fno-omit-frame-pointer",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
          "-Xptxas", "-v" if os.environ.get("SPQ_PTXAS_V") else "-O3"]
+if os.environ.get("SPQ_PLAIN_SCALARS") == "1":   # A/B: sqrt + divisions in the reflector scalars
+    FLAGS.append("-DSPQ_PLAIN_SCALARS")
 # diagnostic build: clock64 stamps inside the latency-bound kernels (tools/*_trace.py)
 if os.environ.get("SPQ_TRACE") == "1":
     FLAGS.append("-DSPQ_TRACE")

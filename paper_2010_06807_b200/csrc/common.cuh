@@ -44,6 +44,53 @@ struct PrepJob {
   int allow_filter, pad_;
 };
 
+// Householder scalars of a column step (kernels/_numba.py:15-35) from the pivot
+// entry alpha and sigma = sum of squares below it (sigma > 0): beta, tau and
+// 1 / v0.  The latency-bound kernels run this on ONE warp per step and a warp
+// issues one fp64 instruction every ~14 cycles, so the instruction count is
+// the cost: rsqrt + one Newton step gives beta and 1 / beta (tau = -v0 / beta
+// becomes a product), and the alpha > 0 branch needs one reciprocal instead
+// of two quotients.  Results are within ~2 ulp of sqrt / division (the parity
+// tolerance is 1e-10); extreme magnitudes take the plain formulas.
+#ifdef __CUDACC__
+__device__ __forceinline__ void house_scalars(double alpha, double sigma, double& tau, double& beta,
+                                              double& inv0) {
+  const double s = fma(alpha, alpha, sigma);
+#ifdef SPQ_PLAIN_SCALARS   // A/B builds
+  const bool plain = true;
+#else
+  const bool plain = !(s > 1e-280 && s < 1e280 && sigma > 1e-280);
+#endif
+  if (plain) {
+    beta = sqrt(s);
+    if (alpha <= 0.0) {
+      const double v0 = alpha - beta;
+      inv0 = 1.0 / v0;
+      tau = -v0 / beta;
+    } else {
+      const double ab = alpha + beta;
+      inv0 = -ab / sigma;
+      tau = sigma / (ab * beta);
+    }
+    return;
+  }
+  const double rb = rsqrt(s);
+  double b = s * rb;
+  b = fma(0.5 * rb, fma(-b, b, s), b);   // one Newton step: b = sqrt(s) to ~1 ulp
+  beta = b;
+  if (alpha <= 0.0) {
+    const double v0 = alpha - b;
+    inv0 = 1.0 / v0;
+    tau = -v0 * rb;
+  } else {
+    const double ab = alpha + b;
+    const double u = 1.0 / (ab * sigma);
+    inv0 = -(ab * ab) * u;            // -ab / sigma
+    tau = (sigma * rb) * (sigma * u); // sigma / (ab * beta)
+  }
+}
+#endif
+
 // ---------------------------------------------------- job lists in params
 // Short job lists travel IN the kernel launch parameters (__grid_constant__,
 // read through a generic pointer into parameter space) instead of through

@@ -1263,16 +1263,7 @@ __global__ void __launch_bounds__(RG_NT, 1) cpqr_reg_kernel(const CpqrJob* __res
         if (sg == 0.0) {
           if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
         } else {
-          beta = sqrt(alpha * alpha + sg);
-          if (alpha <= 0.0) {
-            const double v0 = alpha - beta;
-            inv0 = 1.0 / v0;
-            tau = -v0 / beta;
-          } else {
-            const double ab = alpha + beta;
-            inv0 = -ab / sg;
-            tau = sg / (ab * beta);
-          }
+          house_scalars(alpha, sg, tau, beta, inv0);
         }
         // v (zero outside rows i..m-1: row i-1 is cleared, rows < i-1 were)
         for (int a = i + lane; a < m; a += 32) {

@@ -46,6 +46,34 @@ __device__ __forceinline__ void gemm_epilogue(const GemmProb& p, const double (&
           cv[i][j][h] = (row < p.m && col < p.n) ? __ldg(p.C + row + (int64_t)col * p.ldc) : 0.0;
         }
   }
+  // the two shapes of the compact-WY products get their own (uniform) branch:
+  // one fp64 add, or none, per element instead of a multiply and an FMA (a
+  // warp issues one fp64 instruction every ~14 cycles; on the short-K updates
+  // C -= V W the epilogue was 40% of the kernel's stall samples)
+  if (p.alpha == -1.0 && p.beta == 1.0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = r0 + i * 8, col = c0 + j * 8 + h;
+          if (row < p.m && col < p.n) p.C[row + (int64_t)col * p.ldc] = cv[i][j][h] - acc[i][j][h];
+        }
+    return;
+  }
+  if (p.alpha == 1.0 && p.beta == 0.0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = r0 + i * 8, col = c0 + j * 8 + h;
+          if (row < p.m && col < p.n) p.C[row + (int64_t)col * p.ldc] = acc[i][j][h];
+        }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll

@@ -411,16 +411,7 @@ __device__ __forceinline__ void qrr_step(const QrrCtx& x, double (&a)[R][QR_NB],
     if (sigma == 0.0) {
       if (alpha >= 0.0) { tau = 0.0; beta = alpha; } else { tau = 2.0; beta = -alpha; }
     } else {
-      beta = sqrt(alpha * alpha + sigma);
-      if (alpha <= 0.0) {
-        const double v0 = alpha - beta;
-        inv0 = 1.0 / v0;
-        tau = -v0 / beta;
-      } else {
-        const double ab = alpha + beta;
-        inv0 = -ab / sigma;
-        tau = sigma / (ab * beta);
-      }
+      house_scalars(alpha, sigma, tau, beta, inv0);
     }
     const double g = fma(dt, inv0, ap);           // v_jj^T (column lane): G entry / update dot
     const double ts = tau != 0.0 ? tau : 0.0;
