@@ -1125,6 +1125,14 @@ inline std::vector<std::vector<CopyTask>>& copy_task_pool() {
 struct CopyBatch {
   std::vector<CopyTask> t;
   int64_t maxe = 0;
+  int64_t tot_e = 0;   // elements of all tasks
+  double by = 0;       // bytes moved (read + write)
+  void account(const CopyTask& x) {
+    const int64_t e = (int64_t)std::max(x.nr, 0) * std::max(x.nc, 0);
+    maxe = std::max(maxe, e);
+    tot_e += e;
+    by += (double)e * ((x.src && !x.ident) ? 16.0 : 8.0);
+  }
   CopyBatch() {
     auto& pool = copy_task_pool();
     if (!pool.empty()) { t.swap(pool.back()); pool.pop_back(); }
@@ -1146,7 +1154,7 @@ struct CopyBatch {
   void add(const CopyTask& x) {
     if (x.nr <= 0 || x.nc <= 0) return;
     t.push_back(x);
-    maxe = std::max<int64_t>(maxe, (int64_t)x.nr * x.nc);
+    account(x);
   }
   void zero(double* dst, int64_t n) {
     if (n <= 0) return;
@@ -1168,8 +1176,6 @@ struct CopyBatch {
     if (t.empty()) return;
     std::string tag;
     if (Scope::scope_log()) {
-      double by = 0;
-      for (auto& x : t) by += (double)x.nr * x.nc * ((x.src && !x.ident) ? 16.0 : 8.0);
       char b[160];
       snprintf(b, sizeof b, "copy %s nt=%zu maxe=%lld gb=%.4f", c->stage, t.size(), (long long)maxe, by / 1e9);
       tag = b;
@@ -1178,27 +1184,44 @@ struct CopyBatch {
     // elements per CTA: 2048 (eight per thread) while that still fills the
     // machine, up to 8192 for the big batches -- a CTA's task lookup and launch
     // cost amortised over more elements (SPQ_COPY_GRAN overrides)
-    int64_t tot_e = 0;
-    for (auto& x : t) tot_e += (int64_t)std::max(x.nr, 0) * std::max(x.nc, 0);
     static const int64_t gran_env = getenv("SPQ_COPY_GRAN") ? atoll(getenv("SPQ_COPY_GRAN")) : 0;
     int64_t gran = 2048;
     while (gran < 8192 && tot_e / (2 * gran) >= (int64_t)c->nsm * 8) gran *= 2;
     if (gran_env > 0) gran = gran_env;
-    int64_t ctas = 0;   // flattened-grid assignment (used for mixed task sizes)
-    for (auto& x : t) {
+    // flattened-grid assignment (used for mixed task sizes), written in the
+    // same pass that stages a long list in the pinned upload ring
+    static const bool no_param = env_flag("SPQ_NO_PARAM_LISTS");
+    const size_t bytes = t.size() * sizeof(CopyTask), aligned = (bytes + 255) & ~(size_t)255;
+    const bool in_param = !no_param && (int)t.size() <= PL_COPY;
+    const bool in_ring = !in_param && !c->on_side && aligned <= c->ring_cap &&
+                         c->ring_off + aligned <= c->ring_cap;
+    CopyTask* stage = in_ring ? reinterpret_cast<CopyTask*>(c->pin + c->ring_off) : nullptr;
+    int64_t ctas = 0;
+    for (size_t i = 0; i < t.size(); ++i) {
+      CopyTask& x = t[i];
       const int64_t nb = std::min<int64_t>(512, std::max<int64_t>(1, ((int64_t)x.nr * x.nc + gran - 1) / gran));
       x.cta0 = (int)ctas;
       x.ncta = (int)nb;
       ctas += nb;
+      if (stage) stage[i] = x;
     }
-    launch_copy(up_or_param(c, t, PL_COPY), t.data(), (int)t.size(), maxe, ctas, c->st, gran);
+    const CopyTask* d_tasks = nullptr;
+    if (in_ring) {
+      CopyTask* d = reinterpret_cast<CopyTask*>(c->dring + c->ring_off);
+      CUDA_TRY(cudaMemcpyAsync(d, stage, bytes, cudaMemcpyHostToDevice, c->st));
+      c->ring_off += aligned;
+      d_tasks = d;
+    } else if (!in_param) {
+      d_tasks = upload(c, t);
+    }
+    launch_copy(d_tasks, t.data(), (int)t.size(), maxe, ctas, c->st, gran);
     c->tm.launches[F_COPY]++;
     c->n_kernels++;
-    double by = 0;
-    for (auto& x : t) by += (double)x.nr * x.nc * ((x.src && !x.ident) ? 16.0 : 8.0);
     c->tm.bytes[F_COPY] += by;
     t.clear();
     maxe = 0;
+    tot_e = 0;
+    by = 0;
   }
 };
 
@@ -2343,7 +2366,6 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
       goff[fi + 1] = goff[fi] + wave[fi].psrc.size() + (front_chunked(wave[fi]) ? 0 : wave[fi].gsrc.size());
     g.reserve(goff.back());
     g.t.resize(goff.back());
-    std::vector<int64_t> tmax(wave.size(), 0);
     parallel_fronts(wave.size(), goff.back(), [&](size_t f0, size_t f1) {
       for (size_t fi = f0; fi < f1; ++fi) {
         Front& f = wave[fi];
@@ -2353,13 +2375,12 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
         for (size_t pi = 0; pi < f.parts.size(); ++pi)
           if (ixoff[fi][pi] != (size_t)-1) f.d_ix[pi] = d_ixpack + ixoff[fi][pi];
         CopyTask* out = g.t.data() + goff[fi];
-        int64_t mx = 0;
         for (auto& sp : f.psrc) {
           auto& p = f.parts[sp.part];
           CopyTask t{};
           t.src = sp.p; t.dst = rec.V + p.o0; t.src_rows = f.d_ix[sp.part];
           t.nr = p.o1 - p.o0; t.nc = sp.ncols; t.lds = sp.nr; t.ldd = f.m;
-          mx = std::max<int64_t>(mx, (int64_t)std::max(t.nr, 0) * std::max(t.nc, 0));
+          g.account(t);
           *out++ = t;
         }
         if (!front_chunked(f))
@@ -2368,13 +2389,11 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
             CopyTask t{};
             t.src = sg.p; t.dst = C + p.o0 + (int64_t)sg.col_off * f.m; t.src_rows = f.d_ix[sg.part];
             t.nr = p.o1 - p.o0; t.nc = sg.ncols; t.lds = sg.nr; t.ldd = f.m;
-            mx = std::max<int64_t>(mx, (int64_t)std::max(t.nr, 0) * std::max(t.nc, 0));
+            g.account(t);
             *out++ = t;
           }
-        tmax[fi] = mx;
       }
     });
-    for (int64_t v : tmax) g.maxe = std::max(g.maxe, v);
   }
   g.run(c);
   // QR of every panel, its reflectors applied block by block to C_all
@@ -2402,7 +2421,6 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
       soff[fi + 1] = soff[fi] + (front_chunked(wave[fi]) ? 0 : wave[fi].dsts.size() + 1);
     sc.reserve(soff.back());
     sc.t.resize(soff.back());
-    std::vector<int64_t> tmax(wave.size(), 0);
     parallel_fronts(wave.size(), soff.back(), [&](size_t f0, size_t f1) {
       for (size_t fi = f0; fi < f1; ++fi) {
         Front& f = wave[fi];
@@ -2410,10 +2428,9 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
         Record& rec = c->recs[f.rec];
         double* C = scr + coff[fi];
         CopyTask* out = sc.t.data() + soff[fi];
-        int64_t mx = 0;
         CopyTask t{};
         t.src = C; t.dst = rec.Rsn; t.nr = f.k; t.nc = f.n; t.lds = f.m; t.ldd = f.k;
-        mx = std::max<int64_t>(mx, (int64_t)std::max(t.nr, 0) * std::max(t.nc, 0));
+        sc.account(t);
         *out++ = t;
         for (auto& d : f.dsts) {
           auto& p = f.parts[d.part];
@@ -2425,13 +2442,11 @@ void execute_wave(spq_ctx* c, std::vector<Front>& wave, CopyBatch& zeros, PivotS
           u.lds = f.m;
           u.ldd = d.nr;
           u.dst_rows = d.full ? nullptr : f.d_ix[d.part];
-          mx = std::max<int64_t>(mx, (int64_t)std::max(u.nr, 0) * std::max(u.nc, 0));
+          sc.account(u);
           *out++ = u;
         }
-        tmax[fi] = mx;
       }
     });
-    for (int64_t v : tmax) sc.maxe = std::max(sc.maxe, v);
   }
   sc.run(c);
   if (scr) dfree(c, scr);
