@@ -220,6 +220,8 @@ struct ChainOp {
   int nchunk;           // CTAs working on this op
   int per;              // rows (WY) or R_sn columns (TRI) per chunk
   int64_t part_off;     // offset of this op's partials in the wave scratch (x nrhs)
+  const double* Dinv;   // TRI_SOLVE: inverses of the 32 x 32 diagonal blocks of R (block t covers
+                        // columns k-32(t+1)..k-32t; 32 x 32, ld 32 each), or nullptr
 };
 constexpr size_t CHAIN_SMEM_MAX = 200 * 1024;
 
@@ -305,8 +307,11 @@ int cpqr_reg_elems(int variant);
 size_t cpqr_reg_smem(int padded_rows, int cl, int nt);
 void launch_cpqr_reg(const CpqrJob* d_jobs, const CpqrJob* h_jobs, int njobs, int variant, int cl, int tpc, int nt, size_t smem,
                      cudaStream_t st);
+extern cudaEvent_t g_chain_mid_event;
+void launch_chain_dinv(const ChainOp* d_ops, int nops, cudaStream_t st);
 void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax, int slab_k,
-                       double* part, double* z, int64_t N, int nrhs, cudaStream_t st);
+                       bool has_wy, double* part, double* z, int64_t N, int nrhs,
+                       cudaStream_t st);
 }  // namespace spq
 
 #define CUDA_TRY(x)                                                        \

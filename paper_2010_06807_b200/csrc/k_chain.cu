@@ -11,6 +11,7 @@
 //   apply_w: y_s = R_ss x_s + R_sn x_n ; DiagonalScaling ; Permutation.
 // All HBM-bound (~0.4 flop/byte).
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -191,102 +192,300 @@ namespace spq {
 constexpr int CW_NT = 512;
 constexpr int CW_NW = CW_NT / 32;
 
-// out[c] = sum_q part[q*k + c], q < nq: g lanes per column (g = power of two
-// ~ nq/4, so each lane has a few independent loads), fixed shuffle tree
+// out[c] = sum_q part[q*k + c], q < nq: columns over adjacent threads (the
+// loads of a warp are contiguous), the nq partials over S thread groups with
+// independent loads, groups combined in a fixed order through red (CW_NT)
 __device__ __forceinline__ void chain_reduce_partials(const double* part, int nq, int k,
-                                                      double* out) {
-  int g = 1;
-  while (g < 32 && g * 4 < nq) g <<= 1;
-  const int tid = threadIdx.x, sub = tid & (g - 1);
-  const int per_pass = CW_NT / g;
-  for (int c0 = 0; c0 < k; c0 += per_pass) {
-    const int c = c0 + tid / g;
-    double s0 = 0.0, s1 = 0.0;
+                                                      double* out, double* red) {
+  int cwid = 32;
+  while (cwid < k && cwid < CW_NT) cwid <<= 1;
+  const int S = CW_NT / cwid, tid = threadIdx.x, cl = tid % cwid, g = tid / cwid;
+  for (int c0 = 0; c0 < k; c0 += cwid) {
+    const int c = c0 + cl;
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (c < k) {
-      int q = sub;
-      for (; q + g < nq; q += 2 * g) {
-        s0 += __ldcg(part + (int64_t)q * k + c);
-        s1 += __ldcg(part + (int64_t)(q + g) * k + c);
+      const double* p = part + c;
+      int q = g;
+      for (; q + 7 * S < nq; q += 8 * S) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (int64_t)(q + u * S) * k);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += v[u];
       }
-      if (q < nq) s0 += __ldcg(part + (int64_t)q * k + c);
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = q + u * S < nq ? __ldcg(p + (int64_t)(q + u * S) * k) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += v[u];
     }
-    double s = s0 + s1;
-    for (int sh = g >> 1; sh; sh >>= 1) s += __shfl_xor_sync(0xffffffffu, s, sh);
-    if (sub == 0 && c < k) out[c] = s;
+    red[tid] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    __syncthreads();
+    if (g == 0 && c < k) {
+      double t = red[cl];
+      for (int j = 1; j < S; ++j) t += red[cl + j * cwid];
+      out[c] = t;
+    }
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(CW_NT) chain_phaseA_kernel(const ChainOp* __restrict__ ops,
+// Back substitution of one (wd <= 32) upper-triangular diagonal block by a
+// single warp: lane l holds row l of the block in registers and its
+// reciprocal pivot, so each of the wd sequential steps is one shuffle and one
+// FMA (the pivot division -- a long multi-instruction sequence -- is off the
+// dependency chain; x * (1/d) differs from x / d by at most one rounding).
+__device__ __forceinline__ void tri32_backsolve(const double* D, int ldd, int wd, double* wv,
+                                                int lane) {
+  // the block's entries are read from shared memory a few steps ahead of the
+  // dependency chain (addresses do not depend on it), not held in registers:
+  // the caller's kernel keeps two CTAs per SM
+  const double dinv = lane < wd ? 1.0 / D[lane + (int64_t)lane * ldd] : 0.0;
+  double wl = lane < wd ? wv[lane] : 0.0;
+#pragma unroll 8
+  for (int i = wd - 1; i >= 0; --i) {
+    const double rv = lane < i ? D[lane + (int64_t)i * ldd] : 0.0;
+    if (lane == i) wl *= dinv;
+    const double xi = __shfl_sync(0xffffffffu, wl, i);
+    wl = fma(-rv, xi, wl);
+  }
+  if (lane < wd) wv[lane] = wl;
+}
+
+// The rest of a TRI op once all its partial products are in global memory
+// (run by the op's last phase-A chunk): fixed-order reduction of the partials,
+// then R_ss back substitution (32-column blocks, R slabs streamed through
+// shared memory) or the finished R y product, scattered back into z.
+__device__ void chain_tri_finish(const ChainOp& o, const double* __restrict__ part,
+                                 double* __restrict__ z, int64_t N, int nrhs, int slab_k,
+                                 double* cw, double* Rd, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = o.k;
+  double* w = o.scratch ? o.scratch : cw;   // k
+  double* w2 = w + k;                       // k
+  for (int r = 0; r < nrhs; ++r) {
+    double* zr = z + (int64_t)r * N;
+    const double* pr = part + o.part_off * nrhs + (int64_t)r * o.nchunk * k;
+    // the first R slab and the gathered right-hand side are requested before
+    // the partials are reduced: three independent memory latencies overlap
+    const bool slabbed = o.kind == CH_TRI_SOLVE && k > 32 && k <= slab_k;
+    double* slab = cw + 2 * (int64_t)slab_k;     // two buffers of slab_k x 32
+    const int nb = (k + 31) / 32;
+    const bool inv = slabbed && o.Dinv != nullptr;
+    auto issue = [&](int t) {
+      const int i1 = k - 32 * t, i0 = max(0, i1 - 32), wd = i1 - i0;
+      double* dst = slab + (int64_t)(t & 1) * slab_k * 32;
+      if (inv) {
+        // inverse diagonal block (1024 doubles, 16-byte copies), then the
+        // panel above it: rows 0..i0 of the block's columns (ld i0)
+        for (int e = tid * 2; e < 1024; e += CW_NT * 2) {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + e);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa),
+                       "l"(o.Dinv + (int64_t)t * 1024 + e) : "memory");
+        }
+        for (int e = tid; e < i0 * wd; e += CW_NT) {
+          const int a = e % i0, b = e / i0;
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + 1024 + a + (int64_t)b * i0);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa),
+                       "l"(o.R + (i0 + b) * (int64_t)k + a) : "memory");
+        }
+      } else {
+        for (int e = tid; e < i1 * wd; e += CW_NT) {
+          const int a = e % i1, b = e / i1;
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + a + (int64_t)b * i1);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa),
+                       "l"(o.R + (i0 + b) * (int64_t)k + a) : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (slabbed) issue(0);
+    if (o.kind == CH_TRI_SOLVE)
+      for (int a = tid; a < k; a += CW_NT) w2[a] = zr[o.idx[a]];
+    if (o.n > 0 || o.kind == CH_TRI_MUL) {
+      // R_sn y_n partials (TRI_SOLVE) / R y_s + R_sn y_n partials (TRI_MUL)
+      chain_reduce_partials(pr, o.nchunk, k, w, red);
+    } else {
+      for (int a = tid; a < k; a += CW_NT) w[a] = 0.0;
+    }
+    __syncthreads();
+    if (o.kind == CH_TRI_SOLVE)
+      for (int a = tid; a < k; a += CW_NT) w[a] = w2[a] - w[a];
+    __syncthreads();
+    if (slabbed) {
+      // blocked back substitution, 32 columns per block from the bottom;
+      // the R slab of the next block (rows 0..i1, its 32 columns) streams
+      // into shared memory (cp.async, double buffered) while the current
+      // block is solved, so the solve never waits on a global load
+      for (int t = 0; t < nb; ++t) {
+        if (t + 1 < nb) {
+          issue(t + 1);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const int i1 = k - 32 * t, i0 = max(0, i1 - 32), wd = i1 - i0;
+        const double* S = slab + (int64_t)(t & 1) * slab_k * 32;
+        if (inv) {
+          // x_block = Dinv w_block: four warps take eight columns each
+          if (warp < 4) {
+            double acc = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int cc = warp * 8 + u;
+              if (cc < wd) acc = fma(S[lane + cc * 32], w[i0 + cc], acc);
+            }
+            red[tid] = acc;
+          }
+          __syncthreads();
+          if (tid < wd) w[i0 + tid] = (red[tid] + red[32 + tid]) + (red[64 + tid] + red[96 + tid]);
+          __syncthreads();
+          const double* Pn = S + 1024;   // i0 x wd, ld i0
+          for (int a = tid; a < i0; a += CW_NT) {
+            double s0 = 0.0, s1 = 0.0;
+            int b = 0;
+            for (; b + 1 < wd; b += 2) {
+              s0 = fma(Pn[a + (int64_t)b * i0], w[i0 + b], s0);
+              s1 = fma(Pn[a + (int64_t)(b + 1) * i0], w[i0 + b + 1], s1);
+            }
+            if (b < wd) s0 = fma(Pn[a + (int64_t)b * i0], w[i0 + b], s0);
+            w[a] -= s0 + s1;
+          }
+          __syncthreads();
+          continue;
+        }
+        // S: i1 x wd, ld i1
+        if (warp == 0) tri32_backsolve(S + i0, i1, wd, w + i0, lane);
+        __syncthreads();
+        for (int a = tid; a < i0; a += CW_NT) {
+          double s = 0.0;
+          for (int b = 0; b < wd; ++b) s = fma(S[a + (int64_t)b * i1], w[i0 + b], s);
+          w[a] -= s;
+        }
+        __syncthreads();
+      }
+    } else if (o.kind == CH_TRI_SOLVE) {
+      for (int i1 = k; i1 > 0; i1 -= 32) {
+        const int i0 = max(0, i1 - 32), wd = i1 - i0;
+        for (int e = tid; e < wd * wd; e += CW_NT) {     // stage the diagonal block
+          const int a = e % wd, b = e / wd;
+          Rd[a + b * 33] = o.R[(i0 + a) + (int64_t)(i0 + b) * k];
+        }
+        __syncthreads();
+        if (warp == 0) tri32_backsolve(Rd, 33, wd, w + i0, lane);
+        __syncthreads();
+        for (int a = tid; a < i0; a += CW_NT) {
+          double s = 0.0;
+          for (int b = i0; b < i1; ++b) s += o.R[a + (int64_t)b * k] * w[b];
+          w[a] -= s;
+        }
+        __syncthreads();
+      }
+    }
+    for (int a = tid; a < k; a += CW_NT) zr[o.idx[a]] = w[a];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(CW_NT, 2) chain_phaseA_kernel(const ChainOp* __restrict__ ops,
                                                              const int2* __restrict__ tasks,
                                                              double* __restrict__ part,
-                                                             const double* __restrict__ z,
-                                                             int64_t N, int nrhs) {
+                                                             double* z, int64_t N, int nrhs,
+                                                             int slab_k) {
   const int2 tk = tasks[blockIdx.x];
   const ChainOp o = ops[tk.x];
   const int chunk = tk.y;
+  // programmatic dependent launch: the next wave's CTAs may start and fetch
+  // their (static) task and op descriptors while this grid runs; everything
+  // that touches z or the partials comes after the wait
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = o.k;
+  extern __shared__ __align__(16) double cw[];
+  __shared__ int last;
+  __shared__ double sbuf[CW_NT * 2];   // gathered z / y entries, then the reduced w
+  __shared__ double redA[CW_NT];
   if (o.kind == CH_WY_T || o.kind == CH_WY_N) {
     const int i0 = chunk * o.per, i1 = min(o.m, i0 + o.per);
     for (int r = 0; r < nrhs; ++r) {
       const double* zr = z + (int64_t)r * N;
       // z rows of the chunk staged once in shared memory (gathered)
-      __shared__ double zs[CW_NT * 2];
+      double* zs = sbuf;
       const int nrow = i1 - i0;
       const bool staged = nrow <= CW_NT * 2;
       if (staged)
         for (int i = tid; i < nrow; i += CW_NT) zs[i] = zr[o.idx[i0 + i]];
       __syncthreads();
-      // two columns per warp pass, four independent accumulators (the loads
-      // are latency-bound: keep several in flight per lane)
-      for (int c = warp; c < k; c += 2 * CW_NW) {
-        const int c2 = c + CW_NW;
-        const double* vc = o.V + (int64_t)c * o.m;
-        const double* vd = o.V + (int64_t)(c2 < k ? c2 : c) * o.m;
-        double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
+      // four columns per warp pass; all loads of a pass are issued before the
+      // shuffle reductions (the loads are latency-bound: a chunk is a few
+      // dozen rows, so every lane keeps up to eight loads in flight)
+      for (int c = warp; c < k; c += 4 * CW_NW) {
+        const double* vc[4];
+        bool on[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cu = c + u * CW_NW;
+          on[u] = cu < k;
+          vc[u] = o.V + (int64_t)(on[u] ? cu : c) * o.m;
+        }
+        double s[4] = {0.0, 0.0, 0.0, 0.0}, t[4] = {0.0, 0.0, 0.0, 0.0};
         int i = i0 + lane;
         for (; i + 32 < i1; i += 64) {
           const double z0 = staged ? zs[i - i0] : zr[o.idx[i]];
           const double z1 = staged ? zs[i + 32 - i0] : zr[o.idx[i + 32]];
-          s0 = fma(vc[i], z0, s0);
-          s1 = fma(vc[i + 32], z1, s1);
-          t0 = fma(vd[i], z0, t0);
-          t1 = fma(vd[i + 32], z1, t1);
+          double a0[4], a1[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            a0[u] = vc[u][i];
+            a1[u] = vc[u][i + 32];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            s[u] = fma(a0[u], z0, s[u]);
+            t[u] = fma(a1[u], z1, t[u]);
+          }
         }
         if (i < i1) {
           const double z0 = staged ? zs[i - i0] : zr[o.idx[i]];
-          s0 = fma(vc[i], z0, s0);
-          t0 = fma(vd[i], z0, t0);
+          double a0[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a0[u] = vc[u][i];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s[u] = fma(a0[u], z0, s[u]);
         }
-        double s = s0 + s1, t = t0 + t1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] += t[u];
 #pragma unroll
         for (int q = 16; q; q >>= 1) {
-          s += __shfl_xor_sync(0xffffffffu, s, q);
-          t += __shfl_xor_sync(0xffffffffu, t, q);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], q);
         }
         if (lane == 0) {
-          part[o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k + c] = s;
-          if (c2 < k) part[o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k + c2] = t;
+          double* pw = part + o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (on[u]) pw[c + u * CW_NW] = s[u];
         }
       }
       __syncthreads();
     }
     // the last chunk to arrive reduces the partials (fixed chunk order) and
     // forms u = w (W precomputed) or T^T w / T w, once per operation
-    __shared__ int last;
     __threadfence();
     __syncthreads();
     if (tid == 0) last = atomicAdd(o.cnt, 1) == o.nchunk - 1;
     __syncthreads();
     if (!last) return;
     __threadfence();
-    __shared__ double wred[CW_NT * 2];
+    double* wred = sbuf;
     for (int r = 0; r < nrhs; ++r) {
       const double* pr = part + o.part_off * nrhs + (int64_t)r * o.nchunk * k;
       double* u = part + o.u_off * nrhs + (int64_t)r * 2 * k;   // u (k) | global w (k)
       const bool sm = k <= CW_NT * 2;
       double* wv = o.W ? u : (sm ? wred : u + k);
-      chain_reduce_partials(pr, o.nchunk, k, wv);
+      chain_reduce_partials(pr, o.nchunk, k, wv, redA);
       __syncthreads();
       if (!o.W && o.kind == CH_WY_T) {   // (T^T w)_a = sum_{b<=a} T[b,a] w_b: warp per a (coalesced)
         for (int a = warp; a < k; a += CW_NW) {
@@ -309,88 +508,96 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseA_kernel(const ChainOp* __re
     }
     if (tid == 0) *o.cnt = 0;   // ready for the next application
     return;
-  } else if (o.n > 0 || o.kind == CH_TRI_MUL) {
-    // [R | R_sn][:, chunk] [y_s; y_n][chunk] (TRI_MUL: the whole product, R
-    // upper triangular; TRI_SOLVE: the R_sn part only): rows a split over
-    // threads, columns over P partitions
-    __shared__ double redA[CW_NT];
-    const bool mul = o.kind == CH_TRI_MUL;
-    const int ncol = mul ? k + o.n : o.n;
-    const int j0 = chunk * o.per, j1 = min(ncol, j0 + o.per);
-    int P = CW_NT / max(k, 1);
-    P = P >= 16 ? 16 : (P >= 8 ? 8 : (P >= 4 ? 4 : (P >= 2 ? 2 : 1)));
-    const int rows_per_pass = CW_NT / P;
-    for (int r = 0; r < nrhs; ++r) {
-      const double* zr = z + (int64_t)r * N;
-      for (int a0 = 0; a0 < k; a0 += rows_per_pass) {
-        const int a = a0 + tid % rows_per_pass, jp = tid / rows_per_pass;
-        double s = 0.0;
-        if (a < k) {
-          if (mul) {
-            for (int j = j0 + jp; j < j1; j += P) {
-              if (j < k) {
-                if (a <= j) s += o.R[a + (int64_t)j * k] * zr[o.idx[j]];
-              } else {
-                s += o.Rsn[a + (int64_t)(j - k) * k] * zr[o.idx_n[j - k]];
+  } else {
+    __shared__ double Rd[32 * 33];
+    if (o.n > 0 || o.kind == CH_TRI_MUL) {
+      // [R | R_sn][:, chunk] [y_s; y_n][chunk] (TRI_MUL: the whole product, R
+      // upper triangular; TRI_SOLVE: the R_sn part only): rows a split over
+      // threads, columns over P partitions; the chunk's y entries are gathered
+      // into shared memory first so the matrix loads are all independent
+      double* ys = sbuf;
+      const bool mul = o.kind == CH_TRI_MUL;
+      const int ncol = mul ? k + o.n : o.n;
+      const int j0 = chunk * o.per, j1 = min(ncol, j0 + o.per), nj = j1 - j0;
+      const bool staged = nj <= CW_NT * 2;
+      int P = CW_NT / max(k, 1);
+      P = P >= 16 ? 16 : (P >= 8 ? 8 : (P >= 4 ? 4 : (P >= 2 ? 2 : 1)));
+      const int rows_per_pass = CW_NT / P;
+      for (int r = 0; r < nrhs; ++r) {
+        const double* zr = z + (int64_t)r * N;
+        auto yv = [&](int j) {
+          return mul ? (j < k ? zr[o.idx[j]] : zr[o.idx_n[j - k]]) : zr[o.idx_n[j]];
+        };
+        if (staged) {
+          for (int i = tid; i < nj; i += CW_NT) ys[i] = yv(j0 + i);
+          __syncthreads();
+        }
+        for (int a0 = 0; a0 < k; a0 += rows_per_pass) {
+          const int a = a0 + tid % rows_per_pass, jp = tid / rows_per_pass;
+          double s0 = 0.0, s1 = 0.0;
+          if (a < k) {
+            if (mul) {
+              for (int j = j0 + jp; j < j1; j += P) {
+                const double yj = staged ? ys[j - j0] : yv(j);
+                if (j < k) {
+                  if (a <= j) s0 = fma(o.R[a + (int64_t)j * k], yj, s0);
+                } else {
+                  s1 = fma(o.Rsn[a + (int64_t)(j - k) * k], yj, s1);
+                }
               }
+            } else {
+              const double* Ra = o.Rsn + a;
+              int j = j0 + jp;
+#pragma unroll 4
+              for (; j + P < j1; j += 2 * P) {
+                s0 = fma(Ra[(int64_t)j * k], staged ? ys[j - j0] : yv(j), s0);
+                s1 = fma(Ra[(int64_t)(j + P) * k], staged ? ys[j + P - j0] : yv(j + P), s1);
+              }
+              if (j < j1) s0 = fma(Ra[(int64_t)j * k], staged ? ys[j - j0] : yv(j), s0);
             }
-          } else {
-            for (int j = j0 + jp; j < j1; j += P) s += o.Rsn[a + (int64_t)j * k] * zr[o.idx_n[j]];
           }
+          redA[tid] = s0 + s1;
+          __syncthreads();
+          if (tid < rows_per_pass && a0 + tid < k) {
+            double t = 0.0;
+            for (int q = 0; q < P; ++q) t += redA[tid + q * rows_per_pass];
+            part[o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k + a0 + tid] = t;
+          }
+          __syncthreads();
         }
-        redA[tid] = s;
-        __syncthreads();
-        if (tid < rows_per_pass && a0 + tid < k) {
-          double t = 0.0;
-          for (int q = 0; q < P; ++q) t += redA[tid + q * rows_per_pass];
-          part[o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k + a0 + tid] = t;
-        }
-        __syncthreads();
       }
+      // the last chunk to arrive finishes the operation
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) last = atomicAdd(o.cnt, 1) == o.nchunk - 1;
+      __syncthreads();
+      if (!last) return;
+      __threadfence();
+      if (tid == 0) *o.cnt = 0;
     }
+    chain_tri_finish(o, part, z, N, nrhs, slab_k, cw, Rd, redA);
   }
-}
-
-// Back substitution of one (wd <= 32) upper-triangular diagonal block by a
-// single warp: lane l holds row l of the block in registers and its
-// reciprocal pivot, so each of the wd sequential steps is one shuffle and one
-// FMA (the pivot division -- a long multi-instruction sequence -- is off the
-// dependency chain; x * (1/d) differs from x / d by at most one rounding).
-__device__ __forceinline__ void tri32_backsolve(const double* D, int ldd, int wd, double* wv,
-                                                int lane) {
-  double rrow[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) rrow[j] = (j < wd && lane < j) ? D[lane + (int64_t)j * ldd] : 0.0;
-  const double dinv = lane < wd ? 1.0 / D[lane + (int64_t)lane * ldd] : 0.0;
-  double wl = lane < wd ? wv[lane] : 0.0;
-#pragma unroll
-  for (int i = 31; i >= 0; --i) {
-    if (i < wd) {
-      if (lane == i) wl *= dinv;
-      const double xi = __shfl_sync(0xffffffffu, wl, i);
-      if (lane < i) wl = fma(-rrow[i], xi, wl);
-    }
-  }
-  if (lane < wd) wv[lane] = wl;
 }
 
 __global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __restrict__ ops,
                                                              const int2* __restrict__ tasks,
                                                              const double* __restrict__ part,
                                                              double* __restrict__ z, int64_t N,
-                                                             int nrhs, int slab_k) {
+                                                             int nrhs) {
   const int2 tk = tasks[blockIdx.x];
   const ChainOp o = ops[tk.x];
   const int chunk = tk.y;
+  // programmatic dependent launch: the next wave's CTAs may start and fetch
+  // their (static) task and op descriptors while this grid runs; everything
+  // that touches z or the partials comes after the wait
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ __align__(16) double cw[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int k = o.k;
   double* w = o.scratch ? o.scratch + (int64_t)chunk * 3 * k : cw;   // k
-  double* w2 = w + k;                                                   // k
-  __shared__ double Rd[32 * 33];
   for (int r = 0; r < nrhs; ++r) {
     double* zr = z + (int64_t)r * N;
-    const double* pr = part + o.part_off * nrhs + (int64_t)r * o.nchunk * k;
     if (o.kind == CH_WY_T || o.kind == CH_WY_N) {
       // u (reduced by the last chunk of phase A) into shared memory, then
       // z[rows] -= M u with M = W (= V T^T / V T, precomputed) or V
@@ -407,17 +614,18 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __re
         int rp = 1;
         while (rp < nrow) rp <<= 1;
         const int tpr = CW_NT / rp, row = tid % rp, cs = tid / rp;
-        double s0 = 0.0, s1 = 0.0;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
         if (row < nrow) {
           const double* Mi = M + i0 + row;
-          int c = cs;
-          for (; c + tpr < k; c += 2 * tpr) {
-            s0 = fma(Mi[(int64_t)c * o.m], w[c], s0);
-            s1 = fma(Mi[(int64_t)(c + tpr) * o.m], w[c + tpr], s1);
+          for (int c = cs; c < k; c += 4 * tpr) {   // four independent loads per round
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = c + u * tpr < k ? Mi[(int64_t)(c + u * tpr) * o.m] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(v[u], c + u * tpr < k ? w[c + u * tpr] : 0.0, acc[u]);
           }
-          if (c < k) s0 = fma(Mi[(int64_t)c * o.m], w[c], s0);
         }
-        redB[tid] = s0 + s1;
+        redB[tid] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
         __syncthreads();
         if (cs == 0 && row < nrow) {
           double t = 0.0;
@@ -441,75 +649,7 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __re
         __syncthreads();
       }
     } else {
-      if (chunk != 0) return;
-      if (o.n > 0 || o.kind == CH_TRI_MUL) {
-        // R_sn y_n partials (TRI_SOLVE) / R y_s + R_sn y_n partials (TRI_MUL)
-        chain_reduce_partials(pr, o.nchunk, k, w);
-      } else {
-        for (int a = tid; a < k; a += CW_NT) w[a] = 0.0;
-      }
-      __syncthreads();
-      if (o.kind == CH_TRI_SOLVE)
-        for (int a = tid; a < k; a += CW_NT) w[a] = zr[o.idx[a]] - w[a];
-      __syncthreads();
-      if (o.kind == CH_TRI_SOLVE && k > 32 && k <= slab_k) {
-        // blocked back substitution, 32 columns per block from the bottom;
-        // the R slab of the next block (rows 0..i1, its 32 columns) streams
-        // into shared memory (cp.async, double buffered) while the current
-        // block is solved, so the solve never waits on a global load
-        double* slab = cw + 2 * (int64_t)slab_k;     // two buffers of slab_k x 32
-        const int nb = (k + 31) / 32;
-        auto issue = [&](int t) {
-          const int i1 = k - 32 * t, i0 = max(0, i1 - 32), wd = i1 - i0;
-          double* dst = slab + (int64_t)(t & 1) * slab_k * 32;
-          for (int e = tid; e < i1 * wd; e += CW_NT) {
-            const int a = e % i1, b = e / i1;
-            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + a + (int64_t)b * i1);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa),
-                         "l"(o.R + (i0 + b) * (int64_t)k + a) : "memory");
-          }
-          asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        issue(0);
-        for (int t = 0; t < nb; ++t) {
-          if (t + 1 < nb) {
-            issue(t + 1);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-          } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-          }
-          __syncthreads();
-          const int i1 = k - 32 * t, i0 = max(0, i1 - 32), wd = i1 - i0;
-          const double* S = slab + (int64_t)(t & 1) * slab_k * 32;   // i1 x wd, ld i1
-          if (warp == 0) tri32_backsolve(S + i0, i1, wd, w + i0, lane);
-          __syncthreads();
-          for (int a = tid; a < i0; a += CW_NT) {
-            double s = 0.0;
-            for (int b = 0; b < wd; ++b) s = fma(S[a + (int64_t)b * i1], w[i0 + b], s);
-            w[a] -= s;
-          }
-          __syncthreads();
-        }
-      } else if (o.kind == CH_TRI_SOLVE) {
-        for (int i1 = k; i1 > 0; i1 -= 32) {
-          const int i0 = max(0, i1 - 32), wd = i1 - i0;
-          for (int e = tid; e < wd * wd; e += CW_NT) {     // stage the diagonal block
-            const int a = e % wd, b = e / wd;
-            Rd[a + b * 33] = o.R[(i0 + a) + (int64_t)(i0 + b) * k];
-          }
-          __syncthreads();
-          if (warp == 0) tri32_backsolve(Rd, 33, wd, w + i0, lane);
-          __syncthreads();
-          for (int a = tid; a < i0; a += CW_NT) {
-            double s = 0.0;
-            for (int b = i0; b < i1; ++b) s += o.R[a + (int64_t)b * k] * w[b];
-            w[a] -= s;
-          }
-          __syncthreads();
-        }
-      }
-      for (int a = tid; a < k; a += CW_NT) zr[o.idx[a]] = w[a];
-      __syncthreads();
+      return;   // TRI ops are finished by their last chunk in phase A
     }
   }
 }
@@ -520,12 +660,59 @@ size_t chain_wave_smem(int kmax, int slab_k) {
   return b <= CHAIN_SMEM_MAX ? b : 0;
 }
 
+// Inverses of the 32 x 32 diagonal blocks of R_ss (chain compile time, like
+// the W = V T^T products): the blocked back substitution then multiplies by
+// the inverse block instead of running 32 dependent substitution steps.
+// One warp per block, lane j solves R_block x = e_j by back substitution.
+__global__ void __launch_bounds__(64) chain_dinv_kernel(const ChainOp* __restrict__ ops) {
+  const ChainOp o = ops[blockIdx.x];
+  if (o.kind != CH_TRI_SOLVE || !o.Dinv) return;
+  __shared__ double D[2][32 * 33], X[2][32 * 33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, k = o.k, nb = (k + 31) / 32;
+  double* out = const_cast<double*>(o.Dinv);
+  for (int t = warp; t < nb; t += 2) {
+    const int i1 = k - 32 * t, i0 = max(0, i1 - 32), wd = i1 - i0;
+    double* Dw = D[warp];
+    double* Xw = X[warp];
+    for (int b = 0; b < 32; ++b)   // identity padding beyond wd
+      Dw[lane + b * 33] = (lane < wd && b < wd) ? (lane <= b ? o.R[(i0 + lane) + (int64_t)(i0 + b) * k] : 0.0)
+                                                : (lane == b ? 1.0 : 0.0);
+    __syncwarp();
+    for (int i = 31; i >= 0; --i) {   // X[i, lane]
+      double x = 0.0;
+      if (i == lane) {
+        x = 1.0 / Dw[i + i * 33];
+      } else if (i < lane) {
+        double s = 0.0;
+        for (int l = i + 1; l <= lane; ++l) s = fma(Dw[i + l * 33], Xw[l + lane * 33], s);
+        x = -s / Dw[i + i * 33];
+      }
+      Xw[i + lane * 33] = x;
+    }
+    __syncwarp();
+    for (int b = 0; b < 32; ++b) out[(int64_t)t * 1024 + lane + b * 32] = Xw[lane + b * 33];
+    __syncwarp();
+  }
+}
+
+void launch_chain_dinv(const ChainOp* d_ops, int nops, cudaStream_t st) {
+  if (nops <= 0) return;
+  chain_dinv_kernel<<<nops, 64, 0, st>>>(d_ops);
+  SPQ_LAUNCH_CHECK();
+}
+
+cudaEvent_t g_chain_mid_event = nullptr;   // diagnostics: recorded between the two phases
+
 void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, int kmax, int slab_k,
-                       double* part, double* z, int64_t N, int nrhs, cudaStream_t st) {
+                       bool has_wy, double* part, double* z, int64_t N, int nrhs,
+                       cudaStream_t st) {
   if (ntasks <= 0) return;
   const size_t smem = chain_wave_smem(std::max(kmax, slab_k), slab_k);
+  const size_t smemB = (size_t)std::max(kmax, 1) * sizeof(double);
   static size_t conf = 0;
   if (smem > conf) {   // the default 48 KB cap counts static + dynamic
+    CUDA_TRY(cudaFuncSetAttribute(chain_phaseA_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     CUDA_TRY(cudaFuncSetAttribute(chain_phaseB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     conf = smem;
@@ -539,9 +726,24 @@ void launch_chain_wave(const ChainOp* d_ops, const int2* d_tasks, int ntasks, in
                                " conf=" + std::to_string(conf) + ")");
   };
   fail("pending before chain wave");
-  chain_phaseA_kernel<<<ntasks, CW_NT, 0, st>>>(d_ops, d_tasks, part, z, N, nrhs);
+  static const bool pdl = getenv("SPQ_CHAIN_NO_PDL") == nullptr;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ntasks);
+  cfg.blockDim = dim3(CW_NT);
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.dynamicSmemBytes = smem;
+  const double* cpart = part;
+  cudaLaunchKernelEx(&cfg, chain_phaseA_kernel, d_ops, d_tasks, part, z, N, nrhs, slab_k);
   fail("at chain phase A launch");
-  chain_phaseB_kernel<<<ntasks, CW_NT, smem, st>>>(d_ops, d_tasks, part, z, N, nrhs, slab_k);
+  if (g_chain_mid_event) cudaEventRecord(g_chain_mid_event, st);
+  if (!has_wy) return;   // TRI ops finish inside phase A (their last chunk)
+  cfg.dynamicSmemBytes = smemB;
+  cudaLaunchKernelEx(&cfg, chain_phaseB_kernel, d_ops, d_tasks, cpart, z, N, nrhs);
   fail("at chain phase B launch");
 }
 

@@ -443,6 +443,7 @@ struct spq_ctx {
     std::vector<int64_t> part_sz;         // per wave: partial-sum doubles (x nrhs)
     std::map<int, double*> part_buf;      // nrhs -> wave scratch (max over waves)
     std::vector<int> off, cnt, kmax, slabk;   // slabk: back-substitution slab width (0: none)
+    std::vector<char> has_wy;                 // per wave: any WY op (phase B launched)
     std::map<int, cudaGraphExec_t> graphs;   // nrhs -> executable graph (z = d_vec)
     std::vector<ChainOp> hops;               // host copy of the ordered ops (diagnostics)
   } prog[3];
@@ -3999,7 +4000,7 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
   // ~4 CTAs per SM (the chain is latency-bound wave by wave), at least 32
   // rows (WY) / columns (R_sn) per chunk
   std::vector<int2> tasks;
-  P.toff.clear(); P.tcnt.clear(); P.part_sz.clear(); P.slabk.clear();
+  P.toff.clear(); P.tcnt.clear(); P.part_sz.clear(); P.slabk.clear(); P.has_wy.clear();
   size_t scr = 0;
   for (size_t w = 0; w < P.off.size(); ++w) {
     double wave_work = 0;
@@ -4009,7 +4010,8 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
       const int64_t len = wy ? o.m : (o.kind == CH_TRI_MUL ? (int64_t)o.k + o.n : o.n);
       wave_work += (double)std::max<int64_t>(len, 1) * std::max(o.k, 1);
     }
-    const double per_cta = std::max(2048.0, wave_work / (4.0 * c->nsm));
+    static const int min_chunk = std::max(8, getenv("SPQ_CHAIN_MINCHUNK") ? atoi(getenv("SPQ_CHAIN_MINCHUNK")) : 32);
+    const double per_cta = std::max(64.0 * min_chunk, wave_work / (4.0 * c->nsm));
     for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
       ChainOp& o = ordered[t];
       const bool wy = o.kind == CH_WY_T || o.kind == CH_WY_N;
@@ -4018,7 +4020,7 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
       const int64_t len = wy ? o.m : (o.kind == CH_TRI_MUL ? (int64_t)o.k + o.n : o.n);
       const double work = (double)std::max(len, (int64_t)1) * std::max(o.k, 1);
       int64_t nch = (int64_t)std::ceil(work / per_cta);
-      nch = std::max<int64_t>(1, std::min<int64_t>(nch, (len + 31) / 32));
+      nch = std::max<int64_t>(1, std::min<int64_t>(nch, (len + min_chunk - 1) / min_chunk));
       nch = std::min<int64_t>(nch, 512);
       if (!wy && len == 0) nch = 1;
       o.per = (int)std::max<int64_t>(1, (len + nch - 1) / nch);
@@ -4058,6 +4060,10 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
     P.tcnt.push_back((int)tasks.size() - P.toff.back());
     P.kmax[w] = km;
     int sk = 0;   // TRI_SOLVE ops whose R slabs stream through shared memory
+    char wy_any = 0;
+    for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t)
+      if (ordered[t].kind == CH_WY_T || ordered[t].kind == CH_WY_N) wy_any = 1;
+    P.has_wy.push_back(wy_any);
     for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
       const ChainOp& o = ordered[t];
       if (o.kind == CH_TRI_SOLVE && !o.scratch && o.k > 32 && o.k <= CHAIN_SLAB_KMAX) sk = std::max(sk, o.k);
@@ -4065,6 +4071,29 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
     if ((size_t)(2 * std::max(km, sk) + 64 * sk) * sizeof(double) > CHAIN_SMEM_MAX) sk = 0;
     P.slabk.push_back(sk);
     P.part_sz.push_back(psz);
+  }
+  // inverse diagonal blocks for the slab-streamed back substitutions
+  bool any_dinv = false;
+  if (!env_flag("SPQ_CHAIN_NO_DINV")) {
+    size_t nd = 0;
+    for (size_t w = 0; w < P.off.size(); ++w)
+      for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
+        const ChainOp& o = ordered[t];
+        if (o.kind == CH_TRI_SOLVE && !o.scratch && o.k > 32 && o.k <= P.slabk[w]) nd += (size_t)((o.k + 31) / 32) * 1024;
+      }
+    if (nd) {
+      double* base = dalloc(c, nd * sizeof(double));
+      size_t off = 0;
+      for (size_t w = 0; w < P.off.size(); ++w)
+        for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
+          ChainOp& o = ordered[t];
+          if (o.kind == CH_TRI_SOLVE && !o.scratch && o.k > 32 && o.k <= P.slabk[w]) {
+            o.Dinv = base + off;
+            off += (size_t)((o.k + 31) / 32) * 1024;
+          }
+        }
+      any_dinv = true;
+    }
   }
   if (env_flag("SPQ_CHAIN_PROFILE")) P.hops = ordered;
   if (!ordered.empty()) {
@@ -4074,6 +4103,7 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
     P.d_tasks = (int2*)dalloc(c, std::max<size_t>(tasks.size(), 1) * sizeof(int2));
     CUDA_TRY(cudaMemcpyAsync(P.d_tasks, tasks.data(), tasks.size() * sizeof(int2),
                              cudaMemcpyHostToDevice, c->st));
+    if (any_dinv) launch_chain_dinv(P.d_ops, (int)ordered.size(), c->st);
     sync(c);
   }
 }
@@ -4218,7 +4248,7 @@ void run_prog(spq_ctx* c, int which, double* z, int nrhs) {
   if (it == P.part_buf.end()) throw SpqError(SPQ_ERR_INTERNAL, "chain scratch missing");
   for (size_t w = 0; w < P.off.size(); ++w)
     launch_chain_wave(P.d_ops + P.off[w], P.d_tasks + P.toff[w], P.tcnt[w], P.kmax[w], P.slabk[w],
-                      it->second, z, c->N, nrhs, c->st);
+                      P.has_wy[w] != 0, it->second, z, c->N, nrhs, c->st);
 }
 
 // full application on c->d_vec (result in d_vec), captured once per nrhs
@@ -4228,33 +4258,43 @@ void run_chain(spq_ctx* c, int which, int nrhs) {
     c->compiled = true;
   }
   auto& P = c->prog[which];
-  if (env_flag("SPQ_CHAIN_PROFILE") && which != 0) {
+  if (env_flag("SPQ_CHAIN_PROFILE")) {
     // diagnostics: every wave timed on its own (no graph), one line per wave
     double* part = ensure_part(c, which, nrhs);
     if (which == 2 && c->equil) chain_diag(c->d_vec, c->d_scale, c->N, nrhs, false, c->st);
-    cudaEvent_t e0, e1;
+    cudaEvent_t e0, e1, em;
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventCreate(&em));
+    g_chain_mid_event = em;
     for (size_t w = 0; w < P.off.size(); ++w) {
       CUDA_TRY(cudaEventRecord(e0, c->st));
-      launch_chain_wave(P.d_ops + P.off[w], P.d_tasks + P.toff[w], P.tcnt[w], P.kmax[w], P.slabk[w], part,
-                        c->d_vec, c->N, nrhs, c->st);
+      launch_chain_wave(P.d_ops + P.off[w], P.d_tasks + P.toff[w], P.tcnt[w], P.kmax[w], P.slabk[w],
+                        P.has_wy[w] != 0, part, c->d_vec, c->N, nrhs, c->st);
       CUDA_TRY(cudaEventRecord(e1, c->st));
       CUDA_TRY(cudaEventSynchronize(e1));
-      float ms = 0;
+      float ms = 0, msa = 0;
       CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      CUDA_TRY(cudaEventElapsedTime(&msa, e0, em));
       int nwy = 0, ntri = 0, kmx = 0, mmx = 0, nmx = 0;
       for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
         const ChainOp& o = P.hops[t];
         (o.kind == CH_WY_T || o.kind == CH_WY_N ? nwy : ntri)++;
         kmx = std::max(kmx, o.k); mmx = std::max(mmx, o.m); nmx = std::max(nmx, o.n);
       }
-      fprintf(stderr, "chain %d wave %zu: %.1f us ops %d (wy %d tri %d) tasks %d kmax %d mmax %d nmax %d\n",
-              which, w, 1e3 * ms, P.cnt[w], nwy, ntri, P.tcnt[w], kmx, mmx, nmx);
+      fprintf(stderr, "chain %d wave %zu: %.1f us (A %.1f) ops %d (wy %d tri %d) tasks %d kmax %d mmax %d nmax %d\n",
+              which, w, 1e3 * ms, 1e3 * msa, P.cnt[w], nwy, ntri, P.tcnt[w], kmx, mmx, nmx);
     }
     if (which == 1 && c->equil) chain_diag(c->d_vec, c->d_scale, c->N, nrhs, true, c->st);
+    if (which == 0) {
+      chain_perm(c->d_vec, c->d_roc, c->N, nrhs, c->d_vec2, c->st);
+      CUDA_TRY(cudaMemcpyAsync(c->d_vec, c->d_vec2, (size_t)c->N * nrhs * sizeof(double),
+                               cudaMemcpyDeviceToDevice, c->st));
+    }
+    g_chain_mid_event = nullptr;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    cudaEventDestroy(em);
     return;
   }
   auto it = P.graphs.find(nrhs);

@@ -14,5 +14,6 @@ A, dims, L, eps, b, tol = make_config(sys.argv[1] if len(sys.argv) > 1 else "C3"
 F = factorize(A, partition_geometric(dims, L), eps=eps)
 y = np.random.default_rng(0).standard_normal(A.ncols)
 for _ in range(2):
+    F.apply_qt(y)
     F.solve_w(y)
     F.apply_w(y)
