@@ -4112,7 +4112,7 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
 // becomes z -= W (V^T z) with no triangular product per chunk.  Built with
 // the batched DMMA GEMM at chain compile time; skipped (kernels fall back
 // to the T path) when the extra payload would not fit comfortably.
-constexpr int CHAIN_W_KMIN = 192;   // below: T w in the reducing chunk is cheaper
+constexpr int CHAIN_W_KMIN = 32;   // below: T w in the reducing chunk is cheap (one short pass)
 void build_chain_W(spq_ctx* c) {
   const int kmin = env_flag("SPQ_CHAIN_W") ? 1 : CHAIN_W_KMIN;
   size_t need = 0;
