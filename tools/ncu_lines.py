@@ -24,7 +24,7 @@ for r in rows[hdr + 1:]:
             s = int(r[si])
         except ValueError:
             continue
-        st = sorted(((int(r[i]) if r[i].isdigit() else 0, n[6:]) for i, n in stall_cols), reverse=True)[:3]
+        st = sorted(((int(r[i]) if i < len(r) and r[i].isdigit() else 0, n[6:]) for i, n in stall_cols), reverse=True)[:3]
         lines.append((s, r[0], r[1].strip()[:80], st))
 tot = sum(l[0] for l in lines)
 print(f"total samples {tot}")
