@@ -222,6 +222,13 @@ struct ChainOp {
   int64_t part_off;     // offset of this op's partials in the wave scratch (x nrhs)
   const double* Dinv;   // TRI_SOLVE: inverses of the 32 x 32 diagonal blocks of R (block t covers
                         // columns k-32(t+1)..k-32t; 32 x 32, ld 32 each), or nullptr
+  // a row block of a large TRI_SOLVE (compile_chains splits R_ss into row blocks so the
+  // products with the already solved part run over many CTAs): R / R2 have leading
+  // dimension ldr, R_sn ldn (0: k); R2 (k x n2) multiplies y[idx2], the columns of R_ss to
+  // the right of this block
+  int ldr, ldn, n2;
+  const double* R2;
+  const int* idx2;
 };
 constexpr size_t CHAIN_SMEM_MAX = 200 * 1024;
 

@@ -261,6 +261,8 @@ __device__ void chain_tri_finish(const ChainOp& o, const double* __restrict__ pa
                                  double* cw, double* Rd, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = o.k;
+  const int64_t ldr = o.ldr ? o.ldr : k;
+  const bool has_part = o.n + o.n2 > 0 || o.kind == CH_TRI_MUL;
   double* w = o.scratch ? o.scratch : cw;   // k
   double* w2 = w + k;                       // k
   for (int r = 0; r < nrhs; ++r) {
@@ -287,14 +289,14 @@ __device__ void chain_tri_finish(const ChainOp& o, const double* __restrict__ pa
           const int a = e % i0, b = e / i0;
           const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + 1024 + a + (int64_t)b * i0);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa),
-                       "l"(o.R + (i0 + b) * (int64_t)k + a) : "memory");
+                       "l"(o.R + (i0 + b) * ldr + a) : "memory");
         }
       } else {
         for (int e = tid; e < i1 * wd; e += CW_NT) {
           const int a = e % i1, b = e / i1;
           const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + a + (int64_t)b * i1);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(sa),
-                       "l"(o.R + (i0 + b) * (int64_t)k + a) : "memory");
+                       "l"(o.R + (i0 + b) * ldr + a) : "memory");
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -302,7 +304,7 @@ __device__ void chain_tri_finish(const ChainOp& o, const double* __restrict__ pa
     if (slabbed) issue(0);
     if (o.kind == CH_TRI_SOLVE)
       for (int a = tid; a < k; a += CW_NT) w2[a] = zr[o.idx[a]];
-    if (o.n > 0 || o.kind == CH_TRI_MUL) {
+    if (has_part) {
       // R_sn y_n partials (TRI_SOLVE) / R y_s + R_sn y_n partials (TRI_MUL)
       chain_reduce_partials(pr, o.nchunk, k, w, red);
     } else {
@@ -370,14 +372,14 @@ __device__ void chain_tri_finish(const ChainOp& o, const double* __restrict__ pa
         const int i0 = max(0, i1 - 32), wd = i1 - i0;
         for (int e = tid; e < wd * wd; e += CW_NT) {     // stage the diagonal block
           const int a = e % wd, b = e / wd;
-          Rd[a + b * 33] = o.R[(i0 + a) + (int64_t)(i0 + b) * k];
+          Rd[a + b * 33] = o.R[(i0 + a) + (i0 + b) * ldr];
         }
         __syncthreads();
         if (warp == 0) tri32_backsolve(Rd, 33, wd, w + i0, lane);
         __syncthreads();
         for (int a = tid; a < i0; a += CW_NT) {
           double s = 0.0;
-          for (int b = i0; b < i1; ++b) s += o.R[a + (int64_t)b * k] * w[b];
+          for (int b = i0; b < i1; ++b) s += o.R[a + b * ldr] * w[b];
           w[a] -= s;
         }
         __syncthreads();
@@ -510,14 +512,16 @@ __global__ void __launch_bounds__(CW_NT, 2) chain_phaseA_kernel(const ChainOp* _
     return;
   } else {
     __shared__ double Rd[32 * 33];
-    if (o.n > 0 || o.kind == CH_TRI_MUL) {
+    if (o.n + o.n2 > 0 || o.kind == CH_TRI_MUL) {
       // [R | R_sn][:, chunk] [y_s; y_n][chunk] (TRI_MUL: the whole product, R
       // upper triangular; TRI_SOLVE: the R_sn part only): rows a split over
       // threads, columns over P partitions; the chunk's y entries are gathered
       // into shared memory first so the matrix loads are all independent
       double* ys = sbuf;
       const bool mul = o.kind == CH_TRI_MUL;
-      const int ncol = mul ? k + o.n : o.n;
+      const int n2 = o.n2;   // TRI_SOLVE row block: columns of R_ss right of the block first
+      const int64_t ldr = o.ldr ? o.ldr : k, ldn = o.ldn ? o.ldn : k;
+      const int ncol = mul ? k + o.n : n2 + o.n;
       const int j0 = chunk * o.per, j1 = min(ncol, j0 + o.per), nj = j1 - j0;
       const bool staged = nj <= CW_NT * 2;
       int P = CW_NT / max(k, 1);
@@ -526,7 +530,8 @@ __global__ void __launch_bounds__(CW_NT, 2) chain_phaseA_kernel(const ChainOp* _
       for (int r = 0; r < nrhs; ++r) {
         const double* zr = z + (int64_t)r * N;
         auto yv = [&](int j) {
-          return mul ? (j < k ? zr[o.idx[j]] : zr[o.idx_n[j - k]]) : zr[o.idx_n[j]];
+          return mul ? (j < k ? zr[o.idx[j]] : zr[o.idx_n[j - k]])
+                     : (j < n2 ? zr[o.idx2[j]] : zr[o.idx_n[j - n2]]);
         };
         if (staged) {
           for (int i = tid; i < nj; i += CW_NT) ys[i] = yv(j0 + i);
@@ -546,14 +551,26 @@ __global__ void __launch_bounds__(CW_NT, 2) chain_phaseA_kernel(const ChainOp* _
                 }
               }
             } else {
-              const double* Ra = o.Rsn + a;
+              // two column segments: R_ss right of a row block (split ops only), then R_sn
               int j = j0 + jp;
+              const int je = min(j1, n2);
+              const double* R2a = o.R2 + a;
+#pragma unroll 4
+              for (; j + P < je; j += 2 * P) {
+                s0 = fma(R2a[j * ldr], staged ? ys[j - j0] : yv(j), s0);
+                s1 = fma(R2a[(j + P) * ldr], staged ? ys[j + P - j0] : yv(j + P), s1);
+              }
+              if (j < je) {
+                s0 = fma(R2a[j * ldr], staged ? ys[j - j0] : yv(j), s0);
+                j += P;
+              }
+              const double* Rna = o.Rsn + a - n2 * ldn;
 #pragma unroll 4
               for (; j + P < j1; j += 2 * P) {
-                s0 = fma(Ra[(int64_t)j * k], staged ? ys[j - j0] : yv(j), s0);
-                s1 = fma(Ra[(int64_t)(j + P) * k], staged ? ys[j + P - j0] : yv(j + P), s1);
+                s0 = fma(Rna[j * ldn], staged ? ys[j - j0] : yv(j), s0);
+                s1 = fma(Rna[(j + P) * ldn], staged ? ys[j + P - j0] : yv(j + P), s1);
               }
-              if (j < j1) s0 = fma(Ra[(int64_t)j * k], staged ? ys[j - j0] : yv(j), s0);
+              if (j < j1) s0 = fma(Rna[j * ldn], staged ? ys[j - j0] : yv(j), s0);
             }
           }
           redA[tid] = s0 + s1;
@@ -669,13 +686,14 @@ __global__ void __launch_bounds__(64) chain_dinv_kernel(const ChainOp* __restric
   if (o.kind != CH_TRI_SOLVE || !o.Dinv) return;
   __shared__ double D[2][32 * 33], X[2][32 * 33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, k = o.k, nb = (k + 31) / 32;
+  const int64_t ldr = o.ldr ? o.ldr : k;
   double* out = const_cast<double*>(o.Dinv);
   for (int t = warp; t < nb; t += 2) {
     const int i1 = k - 32 * t, i0 = max(0, i1 - 32), wd = i1 - i0;
     double* Dw = D[warp];
     double* Xw = X[warp];
     for (int b = 0; b < 32; ++b)   // identity padding beyond wd
-      Dw[lane + b * 33] = (lane < wd && b < wd) ? (lane <= b ? o.R[(i0 + lane) + (int64_t)(i0 + b) * k] : 0.0)
+      Dw[lane + b * 33] = (lane < wd && b < wd) ? (lane <= b ? o.R[(i0 + lane) + (i0 + b) * ldr] : 0.0)
                                                 : (lane == b ? 1.0 : 0.0);
     __syncwarp();
     for (int i = 31; i >= 0; --i) {   // X[i, lane]

@@ -4007,7 +4007,7 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
     for (int t = P.off[w]; t < P.off[w] + P.cnt[w]; ++t) {
       const ChainOp& o = ordered[t];
       const bool wy = o.kind == CH_WY_T || o.kind == CH_WY_N;
-      const int64_t len = wy ? o.m : (o.kind == CH_TRI_MUL ? (int64_t)o.k + o.n : o.n);
+      const int64_t len = wy ? o.m : (o.kind == CH_TRI_MUL ? (int64_t)o.k + o.n : (int64_t)o.n + o.n2);
       wave_work += (double)std::max<int64_t>(len, 1) * std::max(o.k, 1);
     }
     static const int min_chunk = std::max(8, getenv("SPQ_CHAIN_MINCHUNK") ? atoi(getenv("SPQ_CHAIN_MINCHUNK")) : 32);
@@ -4017,7 +4017,7 @@ void build_prog(spq_ctx* c, int which, const std::vector<ChainOp>& ops,
       const bool wy = o.kind == CH_WY_T || o.kind == CH_WY_N;
       // the dimension that is split: WY rows; TRI_MUL the columns of [R | R_sn];
       // TRI_SOLVE the R_sn columns (the back substitution stays in one CTA)
-      const int64_t len = wy ? o.m : (o.kind == CH_TRI_MUL ? (int64_t)o.k + o.n : o.n);
+      const int64_t len = wy ? o.m : (o.kind == CH_TRI_MUL ? (int64_t)o.k + o.n : (int64_t)o.n + o.n2);
       const double work = (double)std::max(len, (int64_t)1) * std::max(o.k, 1);
       int64_t nch = (int64_t)std::ceil(work / per_cta);
       nch = std::max<int64_t>(1, std::min<int64_t>(nch, (len + min_chunk - 1) / min_chunk));
@@ -4169,14 +4169,51 @@ void compile_chains(spq_ctx* c) {
   build_prog(c, 0, ops, wr, rd);
   // solve_w: reversed W-chain
   ops.clear(); wr.clear(); rd.clear();
+  // A back substitution runs in one CTA; R_ss larger than the shared-memory
+  // slab limit is split into row blocks from the bottom, each its own op
+  // whose product with the already solved unknowns (the columns of R_ss to
+  // the right of the block, then R_sn) is spread over many CTAs
+  // (SPQ_CHAIN_SPLIT_K=s: split everything larger than s into blocks of s)
+  const int split_env = getenv("SPQ_CHAIN_SPLIT_K") ? std::max(32, atoi(getenv("SPQ_CHAIN_SPLIT_K"))) : 0;
+  const int split_thr = split_env ? split_env : CHAIN_SLAB_KMAX, split_sz = split_env ? split_env : 256;
+  auto push_tri_solve = [&](int k, int n, const int* d_idx, const int* d_idx_n, const double* R,
+                            const double* Rsn, const std::vector<int>& cols,
+                            const std::vector<int>& cols_n) {
+    if (k <= split_thr || env_flag("SPQ_CHAIN_NO_SPLIT")) {
+      ops.push_back(ChainOp{CH_TRI_SOLVE, k, k, n, d_idx, d_idx_n, nullptr, nullptr, R, Rsn, nullptr,
+                            nullptr, nullptr, 0, 1, 1, 0});
+      wr.push_back(cols);
+      rd.push_back(cols_n);
+      return;
+    }
+    const int nblk = (k + split_sz - 1) / split_sz;
+    const int bs = (((k + nblk - 1) / nblk) + 31) / 32 * 32;
+    for (int r1 = k; r1 > 0; r1 -= bs) {
+      const int r0 = std::max(0, r1 - bs), kk = r1 - r0;
+      ChainOp o{};
+      o.kind = CH_TRI_SOLVE;
+      o.m = kk; o.k = kk; o.n = n;
+      o.idx = d_idx + r0;
+      o.idx_n = d_idx_n;
+      o.R = R + r0 + (int64_t)r0 * k;
+      o.Rsn = Rsn ? Rsn + r0 : nullptr;
+      o.nchunk = 1; o.per = 1;
+      o.ldr = k; o.ldn = k;
+      o.n2 = k - r1;
+      o.R2 = R + r0 + (int64_t)r1 * k;
+      o.idx2 = d_idx + r1;
+      ops.push_back(o);
+      wr.push_back(std::vector<int>(cols.begin() + r0, cols.begin() + r1));
+      std::vector<int> rdv(cols.begin() + r1, cols.end());
+      rdv.insert(rdv.end(), cols_n.begin(), cols_n.end());
+      rd.push_back(std::move(rdv));
+    }
+  };
   for (auto it = c->recs.rbegin(); it != c->recs.rend(); ++it) {
     Record& r = *it;
     if (r.unscaled) {
       // v = y[cols]; v[r:] = R_ff^{-1}(v[r:] - R_fc v[:r]); y[cols] = Q v  (factor.py:195-203)
-      ops.push_back(ChainOp{CH_TRI_SOLVE, r.f, r.f, r.k, r.d_cols_f, r.d_cols_c, nullptr, nullptr,
-                            r.R, r.Rsn, nullptr, nullptr, nullptr, 0, 1, 1, 0});
-      wr.push_back(to_int(r.cols_f));
-      rd.push_back(to_int(r.cols_c));
+      push_tri_solve(r.f, r.k, r.d_cols_f, r.d_cols_c, r.R, r.Rsn, to_int(r.cols_f), to_int(r.cols_c));
       if (r.k > 0) {
         ops.push_back(ChainOp{CH_WY_N, r.m, r.k, 0, r.d_cols_s, nullptr, r.V, r.T, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 1, 1, 0});
         wr.push_back(to_int(r.cols_s));
@@ -4192,10 +4229,9 @@ void compile_chains(spq_ctx* c) {
     } else {
       if (r.k <= 0) continue;
       const bool bh = r.kind == REC_ELIM;
-      ops.push_back(ChainOp{CH_TRI_SOLVE, r.k, r.k, bh ? r.n : 0, r.d_cols_s,
-                            bh ? r.d_cols_n : nullptr, nullptr, nullptr, r.R, bh ? r.Rsn : nullptr, nullptr, nullptr, nullptr, 0, 1, 1, 0});
-      wr.push_back(to_int(r.cols_s));
-      rd.push_back(bh ? to_int(r.cols_n) : std::vector<int>());
+      push_tri_solve(r.k, bh ? r.n : 0, r.d_cols_s, bh ? r.d_cols_n : nullptr, r.R,
+                     bh ? r.Rsn : nullptr, to_int(r.cols_s),
+                     bh ? to_int(r.cols_n) : std::vector<int>());
     }
   }
   build_prog(c, 1, ops, wr, rd);

@@ -95,6 +95,46 @@ def test_chains_match_oracle():
             assert np.abs(a - o).max() <= 1e-8 * max(np.abs(o).max(), 1.0), fn
 
 
+@pytest.mark.parametrize("opts", [{}, {"mode": "unscaled"}])
+def test_split_back_substitution(monkeypatch, opts):
+    """Large R_ss are split into row blocks at chain compile time (one op per
+    block, the products with the solved part spread over CTAs); forced here
+    at 32 rows so every separator of a small problem takes that route, with
+    multiple right-hand sides, against the unsplit device chains and (scaled
+    mode) the CPU oracle's."""
+    from oracle import spaqr_oracle as O
+    from paper_2010_06807_b200.factor import factorize
+    from paper_2010_06807_b200.ordering import partition_geometric
+    from paper_2010_06807_b200.problems import make_config
+    A, dims, L, eps, b, tol = make_config("C3", n=48)
+    tree = partition_geometric(dims, L)
+    rng = np.random.default_rng(11)
+    vs = [rng.standard_normal(A.ncols), rng.standard_normal((A.ncols, 2))]
+    fns = ("solve_w", "apply_w", "apply_qt")
+
+    def run(split):
+        if split:
+            monkeypatch.setenv("SPQ_CHAIN_SPLIT_K", "32")
+        else:
+            monkeypatch.delenv("SPQ_CHAIN_SPLIT_K", raising=False)
+        F = factorize(A, tree, eps=eps, **opts)
+        out = [getattr(F, fn)(v) for v in vs for fn in fns]   # chains compile at first use
+        info = np.zeros(4, np.int64)
+        F._ctx.call("spq_chain_info", 1, info)
+        return out, int(info[1])
+
+    split, nsplit = run(True)
+    whole, nwhole = run(False)
+    assert nsplit > nwhole            # the separators' back substitutions became several ops
+    for a, o in zip(split, whole):
+        assert np.abs(a - o).max() <= 1e-10 * max(np.abs(o).max(), 1.0)
+    if not opts:
+        Fo = O.factorize(A, tree, eps=eps)
+        ref = [getattr(Fo, fn)(v) for v in vs for fn in fns]
+        for a, o in zip(split, ref):
+            assert np.abs(a - o).max() <= 1e-8 * max(np.abs(o).max(), 1.0)
+
+
 def test_exact_mode_identity():
     """eps = 0 / no sparsification: P^T Q^T A W^{-1} = I (reference
     test_factor.py:395-402) and W^T W = A^T A for the equilibrated A."""
