@@ -989,7 +989,6 @@ void launch_power_iter(const PowerJob* d_jobs, int njobs, int fmax, cudaStream_t
 namespace spq {
 
 constexpr int RG_NT = 512;
-constexpr int RG_NW = RG_NT / 32;
 
 __device__ __forceinline__ unsigned long long rg_pack(int pos, int phys) {
   return ((unsigned long long)(unsigned)pos << 32) | (unsigned)phys;

@@ -1619,7 +1619,7 @@ int panel_rows() {   // target rows per CTA of the register panel kernel
 void qr_batch(spq_ctx* c, const std::vector<QrProb>& probs) {
   Stage stage_(c, "qr_batch");
   if (probs.empty()) return;
-  double qr_flops = 0, wy_flops = 0;
+  double qr_flops = 0;
   int maxk = 0;
   for (auto& q : probs) {
     qr_flops += 2.0 * q.m * (double)q.k * q.k - 2.0 * q.k * (double)q.k * q.k / 3.0;
