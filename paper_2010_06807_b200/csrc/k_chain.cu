@@ -407,8 +407,12 @@ __global__ void __launch_bounds__(CW_NT, 2) chain_phaseA_kernel(const ChainOp* _
   const int k = o.k;
   extern __shared__ __align__(16) double cw[];
   __shared__ int last;
-  __shared__ double sbuf[CW_NT * 2];   // gathered z / y entries, then the reduced w
-  __shared__ double redA[CW_NT];
+  // one static buffer, carved per branch: gathered z / y entries (then the
+  // reduced w) | WY: per-warp 8 x 33 product tiles, TRI: reduction scratch and
+  // the staged diagonal block
+  __shared__ double sraw[CW_NT * 2 + CW_NW * 8 * 33];
+  double* sbuf = sraw;
+  double* redA = sraw + CW_NT * 2;
   if (o.kind == CH_WY_T || o.kind == CH_WY_N) {
     const int i0 = chunk * o.per, i1 = min(o.m, i0 + o.per);
     for (int r = 0; r < nrhs; ++r) {
@@ -420,6 +424,38 @@ __global__ void __launch_bounds__(CW_NT, 2) chain_phaseA_kernel(const ChainOp* _
       if (staged)
         for (int i = tid; i < nrow; i += CW_NT) zs[i] = zr[o.idx[i0 + i]];
       __syncthreads();
+      if (nrow <= 64 && staged) {
+        // eight columns per warp pass: every lane loads its one or two rows of
+        // the eight columns (up to 16 independent loads), multiplies by its z
+        // entries and parks the products in the warp's 8 x 33 tile; lane j then
+        // adds eight tile entries of column j % 8 and two shuffles combine the
+        // four quarters -- 10 additions per eight columns instead of 40
+        double* tile = sraw + CW_NT * 2 + warp * (8 * 33);
+        const bool r0 = lane < nrow, r1 = lane + 32 < nrow;
+        const double z0 = r0 ? zs[lane] : 0.0, z1 = r1 ? zs[lane + 32] : 0.0;
+        const double* vbase = o.V + i0 + lane;
+        double* pw = part + o.part_off * nrhs + ((int64_t)r * o.nchunk + chunk) * k;
+        for (int c = warp * 8; c < k; c += 8 * CW_NW) {
+          double a0[8], a1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const double* vc = vbase + (int64_t)min(c + u, k - 1) * o.m;
+            a0[u] = r0 ? vc[0] : 0.0;
+            a1[u] = r1 ? vc[32] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) tile[u * 33 + lane] = fma(a1[u], z1, a0[u] * z0);
+          __syncwarp();
+          const int cu = lane & 7, q = lane >> 3;
+          double sacc = 0.0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sacc += tile[cu * 33 + q * 8 + e];
+          sacc += __shfl_xor_sync(0xffffffffu, sacc, 8);
+          sacc += __shfl_xor_sync(0xffffffffu, sacc, 16);
+          if (lane < 8 && c + lane < k) pw[c + lane] = sacc;
+          __syncwarp();
+        }
+      } else
       // four columns per warp pass; all loads of a pass are issued before the
       // shuffle reductions (the loads are latency-bound: a chunk is a few
       // dozen rows, so every lane keeps up to eight loads in flight)
@@ -511,7 +547,7 @@ __global__ void __launch_bounds__(CW_NT, 2) chain_phaseA_kernel(const ChainOp* _
     if (tid == 0) *o.cnt = 0;   // ready for the next application
     return;
   } else {
-    __shared__ double Rd[32 * 33];
+    double* Rd = sraw + CW_NT * 3;
     if (o.n + o.n2 > 0 || o.kind == CH_TRI_MUL) {
       // [R | R_sn][:, chunk] [y_s; y_n][chunk] (TRI_MUL: the whole product, R
       // upper triangular; TRI_SOLVE: the R_sn part only): rows a split over
@@ -634,7 +670,7 @@ __global__ void __launch_bounds__(CW_NT) chain_phaseB_kernel(const ChainOp* __re
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         if (row < nrow) {
           const double* Mi = M + i0 + row;
-          for (int c = cs; c < k; c += 4 * tpr) {   // four independent loads per round
+          for (int c = cs; c < k; c += 4 * tpr) {   // four independent loads per round (eight measured slower)
             double v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) v[u] = c + u * tpr < k ? Mi[(int64_t)(c + u * tpr) * o.m] : 0.0;
